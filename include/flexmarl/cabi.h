@@ -1,0 +1,246 @@
+/* include/flexmarl/cabi.h — the C ABI of the B200 micro-batch policy-update path.
+ *
+ * The reference (FlexMARL artifact, /root/reference/proj/include/marlsim) has
+ * no FFI: its hot path sits behind C++ class methods in header-only code.
+ * This ABI is what those methods bind to in the drop-in replacement
+ * (INTEGRATION.md shows the reference-side C++ shim and the ctypes binding).
+ * Each entry point names the reference interface it replaces (file:line,
+ * paths relative to proj/include/marlsim/).
+ *
+ * Conventions: plain pointers and sizes, no exceptions across the boundary;
+ * every call returns an fm_status (0 = OK) and sets a thread-local message
+ * readable with fm_last_error().  Status codes 1..28 are marlsim::ErrorCode
+ * (errors.hpp:10-39) + 1, so the C++ shim can re-raise them verbatim.
+ * Calls on one fm_ctx come from one host thread (the reference is a
+ * single-threaded event loop by contract, sim.hpp:19-23).
+ * There is no CPU fallback: without a usable sm_100 device every compute
+ * entry point fails with FM_ERR_NO_DEVICE.
+ */
+#ifndef FLEXMARL_CABI_H
+#define FLEXMARL_CABI_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum fm_status {
+    FM_OK = 0,
+    /* marlsim::ErrorCode + 1 (errors.hpp:10-39) */
+    FM_ERR_SCHEDULING_IN_PAST = 1,
+    FM_ERR_DEVICE_OOM = 2,
+    FM_ERR_HOST_OOM = 3,
+    FM_ERR_EMPTY_POOL = 4,
+    FM_ERR_DUPLICATE_KEY = 5,
+    FM_ERR_KEY_NOT_FOUND = 6,
+    FM_ERR_GET_TIMEOUT = 7,
+    FM_ERR_LAYOUT_OUT_OF_BOUNDS = 8,
+    FM_ERR_EMPTY_LIST = 9,
+    FM_ERR_TABLE_EXISTS = 10,
+    FM_ERR_RESERVED_COLUMN_NAME = 11,
+    FM_ERR_DUPLICATE_SAMPLE = 12,
+    FM_ERR_UNKNOWN_COLUMN = 13,
+    FM_ERR_RECORD_NOT_FOUND = 14,
+    FM_ERR_CELL_ALREADY_SET = 15,
+    FM_ERR_UNKNOWN_TABLE = 16,
+    FM_ERR_NOT_PROCESSING = 17,
+    FM_ERR_BAD_SAMPLE_ID = 18,
+    FM_ERR_UNKNOWN_WORKFLOW = 19,
+    FM_ERR_NO_INSTANCE = 20,
+    FM_ERR_INSUFFICIENT_RESOURCES = 21,
+    FM_ERR_BUSY_GROUP = 22,
+    FM_ERR_VERSION_MISMATCH = 23,
+    FM_ERR_INACTIVE_GROUP = 24,
+    FM_ERR_INCOMPLETE_BATCH = 25,
+    FM_ERR_CONFIG_ERROR = 26,
+    FM_ERR_STALL_DETECTED = 27,
+    FM_ERR_SYNC_TIMEOUT = 28,
+    /* B200 runtime */
+    FM_ERR_CUDA = 100,
+    FM_ERR_NCCL = 101,
+    FM_ERR_NO_DEVICE = 102,
+    FM_ERR_INVALID_ARG = 103
+} fm_status;
+
+/* Arithmetic of an agent's trainer (declared per agent). */
+typedef enum fm_precision {
+    FM_PRECISION_BF16_TC = 0,  /* tcgen05 bf16 GEMMs, fp32 accumulate, fp64 master weights */
+    FM_PRECISION_PARITY_F64 = 1 /* exact-featurizer fp64 SIMT path (correctness anchor, small V*D) */
+} fm_precision;
+
+/* Where a suspended agent's training state is parked (object_store.hpp:80-86 tiers). */
+typedef enum fm_tier {
+    FM_TIER_HOST = 0,   /* pinned host memory of this process (D2H / H2D copies) */
+    FM_TIER_DEVICE = 1, /* a parking arena in this GPU's HBM (D2D copy engine) */
+    FM_TIER_PEER = 2    /* a peer GPU's HBM over NVLink (cudaMemcpyPeerAsync) */
+} fm_tier;
+
+typedef struct fm_ctx fm_ctx;     /* one GPU: streams, token arena, workspace */
+typedef struct fm_agent fm_agent; /* one agent's trainer state (training.hpp:98-105) */
+typedef struct fm_store fm_store; /* host control plane of the experience store */
+typedef struct fm_comm fm_comm;   /* NCCL communicator of one agent gang */
+
+/* ---- misc ------------------------------------------------------------- */
+const char* fm_last_error(void);
+const char* fm_status_name(int status);
+int fm_abi_version(void);
+/* Number of hot-path kernel launches issued by this process so far. */
+uint64_t fm_launch_count(void);
+
+/* ---- host-side bit-exact helpers (rng.hpp, policy.hpp, training.hpp) --- */
+/* training.hpp:245-248: mix_str(mix_u64(seed, 0x1217), agent) */
+uint64_t fm_agent_seed(uint64_t seed, const char* agent);
+/* policy.hpp:29-35 PolicyModel::seeded, bit-identical (host glibc libm), multi-threaded */
+int fm_seeded_weights(uint64_t V, uint64_t D, uint64_t seed, double* out, int threads);
+/* codec.hpp:15-22 encode_tokens; returns bytes written (8 + 8n) */
+uint64_t fm_encode_tokens(const int32_t* tokens, uint64_t n, uint8_t* out);
+
+/* ---- device context ------------------------------------------------------ */
+int fm_ctx_create(int device, fm_ctx** out);
+int fm_ctx_destroy(fm_ctx* ctx);
+int fm_ctx_device(const fm_ctx* ctx);
+int fm_ctx_num_sms(const fm_ctx* ctx);
+int fm_ctx_synchronize(fm_ctx* ctx);
+/* Pre-size the token arena and the per-micro-batch workspace. */
+int fm_ctx_reserve(fm_ctx* ctx, uint64_t arena_bytes, int64_t max_rows, uint64_t max_vocab,
+                   uint64_t max_feat);
+
+/* ---- token arena: the device side of ObjectStore::set/get for the List
+ * cells "prompt"/"response" (object_store.hpp:116-197, codec.hpp:15-30).
+ * fm_arena_put uploads one encoded token list and returns its arena offset. */
+int fm_arena_put(fm_ctx* ctx, const uint8_t* payload, uint64_t nbytes, uint64_t* offset_out);
+int fm_arena_reset(fm_ctx* ctx);
+uint64_t fm_arena_used(const fm_ctx* ctx);
+
+/* ---- agent trainer (TrainingEngine, training.hpp:192-540) ----------------- */
+int fm_agent_create(fm_ctx* ctx, const char* agent, uint64_t vocab, uint64_t feat,
+                    int precision, fm_agent** out);
+int fm_agent_destroy(fm_agent* a);
+/* initial_model / peek_state (training.hpp:224-248): V*D f64 row-major */
+int fm_agent_set_weights(fm_agent* a, const double* W);
+int fm_agent_read_weights(fm_agent* a, double* W_out);
+/* Adam moments (fp32 on device) and step count (training.hpp:31-35) */
+int fm_agent_read_moments(fm_agent* a, float* m_out, float* v_out, int64_t* step_out);
+/* gradient accumulator (V*D, as f64) — the reduced -1/G * sum term of training.hpp:444-446 */
+int fm_agent_read_grad(fm_agent* a, double* g_out);
+int64_t fm_agent_version(const fm_agent* a);
+int64_t fm_agent_samples_accumulated(const fm_agent* a);
+int fm_agent_is_active(const fm_agent* a);
+
+/* One polled record as handed to the trainer (sample.hpp:94-111): arena
+ * offsets of its prompt / response payloads and its advantage cell. */
+typedef struct fm_sample {
+    uint64_t prompt_off;
+    uint64_t response_off;
+    double advantage;
+} fm_sample;
+
+/* Same, with host payload pointers (end-to-end path: the ABI stages the
+ * encoded lists through pinned memory into the arena inside the call). */
+typedef struct fm_host_sample {
+    const uint8_t* prompt;
+    const uint8_t* response;
+    double advantage;
+} fm_host_sample;
+
+/* Completion record of one micro-batch (GradReport, training.hpp:169-177). */
+typedef struct fm_report {
+    int64_t ticket;
+    int64_t tokens;
+    int64_t batch_size;
+    double grad_norm; /* ||sum_mb A_i term_i|| / G (training.hpp:417); NaN under DP */
+    double loss;      /* -(1/G) sum_i A_i sum_t log pi, this micro-batch */
+} fm_report;
+
+/* TrainingEngine::train_micro_batch (training.hpp:355-430): gather -> logits ->
+ * fused loss -> weight-gradient accumulate, enqueued on the agent's stream.
+ * Returns immediately; *ticket_out identifies the report (fm_agent_poll_report).
+ * global_batch is G of the -1/G normalisation (training.hpp:446). */
+int fm_train_micro_batch(fm_agent* a, const fm_sample* samples, int n, int64_t global_batch,
+                         int64_t* ticket_out);
+int fm_train_micro_batch_host(fm_agent* a, const fm_host_sample* samples, int n,
+                              int64_t global_batch, int64_t* ticket_out);
+/* Optional PPO clipped-ratio surrogate (off by default = the reference's
+ * ratio-free objective).  old_logp: per packed row of the next
+ * micro-batch (host array, n_rows entries) or NULL to disable. */
+int fm_agent_set_clip(fm_agent* a, float clip_eps, const float* old_logp, int64_t n_rows);
+/* Data-parallel gang: every rank receives the whole micro-batch and trains
+ * the token-balanced row range [M*rank/nranks, M*(rank+1)/nranks). */
+int fm_agent_set_shard(fm_agent* a, int rank, int nranks);
+/* Per-row log pi(a_t|s_t) of the last micro-batch (f32; f64 in parity mode). */
+int fm_agent_read_logp(fm_agent* a, double* out, int64_t n_rows);
+/* Packed rows of the last micro-batch on ctx (the device gather's output,
+ * bit-exact target of the oracle's fmo_pack_rows); any pointer may be NULL. */
+int fm_debug_read_rows(fm_ctx* ctx, int64_t n_rows, int32_t* action, int32_t* ctx4,
+                       int32_t* n_ctx, int32_t* sample, float* coef);
+/* Blocks until the agent's stream drains; completed reports become pollable. */
+int fm_agent_sync(fm_agent* a);
+/* Non-blocking: 1 and fills *out if the ticket's micro-batch has finished. */
+int fm_agent_poll_report(fm_agent* a, int64_t ticket, fm_report* out);
+
+/* apply_global_update (training.hpp:435-456): IncompleteBatch unless
+ * samples_accumulated == global_batch; fused Adam; version += 1.
+ * If grad_norm_out != NULL the call waits and writes ||grad||_F. */
+int fm_apply_update(fm_agent* a, int64_t global_batch, double lr, double beta1, double beta2,
+                    double eps, double* grad_norm_out, int64_t* version_out);
+
+/* ---- training-state swap (suspend / activate, training.hpp:259-350) -------
+ * suspend: copy {W, m, v, accumulated gradient} to the parking tier on the
+ * ctx's copy stream (ordered after the agent's compute) and release the
+ * agent's slot; activate: copy back into a slot of `ctx` (may differ from the
+ * one it was suspended from), regenerate the bf16 shadow.  Both are async;
+ * compute issued after activate waits on the copy-in event. */
+int fm_agent_suspend(fm_agent* a, int tier, int peer_device);
+int fm_agent_activate(fm_agent* a, fm_ctx* ctx);
+/* FNV-1a over the bytes of {W, m, v, grad, step, version, samples}: swap-identity check. */
+int fm_agent_state_checksum(fm_agent* a, uint64_t* out);
+
+/* ---- GRPO advantages (training.hpp:54-67), device kernel K-adv --------------
+ * rewards[seg_off[i]:seg_off[i+1]] is group i; host arrays in/out. */
+int fm_group_advantages(fm_ctx* ctx, const double* rewards, const int32_t* seg_off, int nseg,
+                        double eps, double* out);
+
+/* ---- data-parallel gang (NCCL over NVLink) ------------------------------- */
+int fm_comm_unique_id(uint8_t out[128]);
+int fm_comm_create(fm_ctx* ctx, const uint8_t id[128], int nranks, int rank, fm_comm** out);
+int fm_comm_destroy(fm_comm* c);
+/* Sum the agent's gradient accumulator across the gang (before fm_apply_update). */
+int fm_agent_allreduce_grad(fm_agent* a, fm_comm* c);
+
+/* ---- experience store host control plane (experience_store.hpp:19-276) ---- */
+int fm_store_create(fm_store** out);
+int fm_store_destroy(fm_store* s);
+/* column types: ColumnType (sample.hpp:69): 0 Int 1 Float 2 Bool 3 String 4 List 5 Tensor */
+int fm_store_create_table(fm_store* s, const char* agent, const char* const* col_names,
+                          const int* col_types, int ncols);
+int fm_store_insert(fm_store* s, const char* agent, int64_t version, const char* input_id,
+                    int turns, int traj);
+int fm_store_set_float(fm_store* s, const char* agent, const char* input_id, int turns, int traj,
+                       int64_t version, const char* column, double value);
+/* set_cell_payload (experience_store.hpp:82-88): the payload goes to ctx's
+ * token arena; the cell records its arena offset as the reference key. */
+int fm_store_set_payload(fm_store* s, fm_ctx* ctx, const char* agent, const char* input_id,
+                         int turns, int traj, int64_t version, const char* column,
+                         const uint8_t* payload, uint64_t nbytes);
+/* ready_count (experience_store.hpp:181-187) */
+int fm_store_ready_count(fm_store* s, const char* agent, int64_t version, uint64_t* out);
+int fm_store_record_count(fm_store* s, const char* agent, uint64_t* out);
+/* poll_micro_batch (experience_store.hpp:92-114): canonical-first mb ready
+ * records; writes mb samples (prompt/response arena offsets + advantage) and
+ * their handles; *got = mb, or 0 for the reference's nullopt. */
+int fm_store_poll(fm_store* s, const char* agent, int64_t version, int64_t mb,
+                  const char* prompt_col, const char* response_col, const char* adv_col,
+                  fm_sample* samples_out, int64_t* handles_out, int64_t* got);
+/* Identity of a polled record (for the reference's MicroBatch view). */
+int fm_store_record_id(fm_store* s, const char* agent, int64_t handle, char* input_id_out,
+                       size_t cap, int* turns, int* traj, int64_t* version);
+/* complete (experience_store.hpp:134-148): NotProcessing unless all polled */
+int fm_store_complete(fm_store* s, const char* agent, const int64_t* handles, int64_t n);
+/* purge_stale (experience_store.hpp:118-132) */
+int fm_store_purge_stale(fm_store* s, const char* agent, int64_t current_version, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,326 @@
+/* oracle/flexmarl_oracle.c — TEST INFRASTRUCTURE ONLY (see flexmarl_oracle.h).
+ *
+ * Plain-C restatement of the reference micro-batch policy-update path.  Each
+ * function follows the reference arithmetic operation-for-operation (same
+ * summation order, same libm calls) so that it agrees bit-for-bit with the
+ * compiled reference (oracle/_ref) on every golden vector.  Parity pinned by
+ * tests/test_oracle.py against tests/golden/*.npz and, when oracle/_ref is
+ * built, against the live reference.
+ */
+#define _GNU_SOURCE
+#include "flexmarl_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---- rng.hpp:14-64 --------------------------------------------------- */
+
+uint64_t fmo_splitmix64(uint64_t* state) { /* rng.hpp:14-19 */
+    uint64_t z = (*state += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+uint64_t fmo_mix_u64(uint64_t seed, uint64_t value) { /* rng.hpp:21-24 */
+    uint64_t s = seed ^ (value + 0x9e3779b97f4a7c15ULL + (seed << 6) + (seed >> 2));
+    return fmo_splitmix64(&s);
+}
+
+uint64_t fmo_mix_str(uint64_t seed, const char* text) { /* rng.hpp:26-34 */
+    uint64_t h = seed ^ 0xcbf29ce484222325ULL;
+    for (const unsigned char* c = (const unsigned char*)text; *c; ++c) {
+        h ^= *c;
+        h *= 0x100000001b3ULL;
+        h = fmo_mix_u64(h, *c);
+    }
+    return h;
+}
+
+static double rng_unit(uint64_t* st) { /* rng.hpp:43-48 */
+    const uint64_t bits = fmo_splitmix64(st) >> 11;
+    double u = (double)bits * 0x1.0p-53;
+    if (u <= 0.0) u = 0x1.0p-53;
+    return u;
+}
+
+static double rng_normal(uint64_t* st) { /* rng.hpp:55-59 */
+    const double u1 = rng_unit(st);
+    const double u2 = rng_unit(st);
+    return sqrt(-2.0 * log(u1)) * cos(2.0 * M_PI * u2);
+}
+
+void fmo_rng_draw(uint64_t seed, int kind, uint64_t arg, uint64_t n, void* out) {
+    uint64_t st = seed;
+    for (uint64_t i = 0; i < n; ++i) {
+        switch (kind) {
+            case 0: ((uint64_t*)out)[i] = fmo_splitmix64(&st); break;
+            case 1: ((double*)out)[i] = rng_unit(&st); break;
+            case 2: ((double*)out)[i] = rng_normal(&st); break;
+            default: ((uint64_t*)out)[i] = arg == 0 ? 0 : fmo_splitmix64(&st) % arg; break;
+        }
+    }
+}
+
+/* ---- training.hpp:245-248, policy.hpp:29-35 --------------------------- */
+
+uint64_t fmo_agent_seed(uint64_t seed, const char* agent) {
+    return fmo_mix_str(fmo_mix_u64(seed, 0x1217), agent);
+}
+
+void fmo_seeded_weights(uint64_t V, uint64_t D, uint64_t seed, double* out) {
+    uint64_t st = seed;
+    for (uint64_t i = 0; i < V * D; ++i) out[i] = 0.5 * rng_normal(&st);
+}
+
+/* ---- training.hpp:54-67 ----------------------------------------------- */
+
+void fmo_group_advantages(const double* r, int n, double eps, double* out) {
+    if (n <= 0) return;
+    double mean = 0.0;
+    for (int i = 0; i < n; ++i) mean += r[i];
+    mean /= (double)n;
+    double var = 0.0;
+    for (int i = 0; i < n; ++i) var += (r[i] - mean) * (r[i] - mean);
+    var /= (double)n;
+    const double sd = sqrt(var);
+    for (int i = 0; i < n; ++i) out[i] = (r[i] - mean) / (sd + eps);
+}
+
+/* ---- training.hpp:71-83 ----------------------------------------------- */
+
+double fmo_rule_reward(const int* resp, int n, const int* pattern, int np) {
+    if (n == 0 || np == 0) return 0.0;
+    int best = 0;
+    for (int s = 0; s < n; ++s) {
+        int len = 0;
+        while (len < np && s + len < n && resp[s + len] == pattern[len]) ++len;
+        if (len > best) best = len;
+    }
+    return (double)best / (double)np;
+}
+
+/* ---- training.hpp:37-51 ----------------------------------------------- */
+
+void fmo_adam_step(double* w, double* m, double* v, int64_t* step, const double* g, uint64_t n,
+                   double lr, double b1, double b2, double eps) {
+    *step += 1;
+    const double bc1 = 1.0 - pow(b1, (double)*step);
+    const double bc2 = 1.0 - pow(b2, (double)*step);
+    for (uint64_t i = 0; i < n; ++i) {
+        const double gi = g[i];
+        m[i] = b1 * m[i] + (1.0 - b1) * gi;
+        v[i] = b2 * v[i] + (1.0 - b2) * gi * gi;
+        const double mhat = m[i] / bc1;
+        const double vhat = v[i] / bc2;
+        w[i] -= lr * mhat / (sqrt(vhat) + eps);
+    }
+}
+
+/* ---- codec.hpp:15-30 -------------------------------------------------- */
+
+uint64_t fmo_decode_tokens(const uint8_t* payload, int* out) {
+    uint64_t n;
+    memcpy(&n, payload, 8);
+    if (out) {
+        for (uint64_t i = 0; i < n; ++i) {
+            uint64_t t;
+            memcpy(&t, payload + 8 + 8 * i, 8);
+            out[i] = (int)(uint32_t)t; /* static_cast<Token>(u64): modular (C++20) */
+        }
+    }
+    return n;
+}
+
+uint64_t fmo_encode_tokens(const int* tokens, uint64_t n, uint8_t* out) {
+    memcpy(out, &n, 8);
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t t = (uint64_t)(int64_t)tokens[i]; /* static_cast<uint64_t>(int) */
+        memcpy(out + 8 + 8 * i, &t, 8);
+    }
+    return 8 + 8 * n;
+}
+
+/* ---- policy.hpp:42-91 ------------------------------------------------- */
+
+void fmo_featurize(uint64_t V, uint64_t D, const int* ctx, int len, double* phi) {
+    (void)V;
+    for (uint64_t d = 0; d < D; ++d) phi[d] = 0.0;
+    const int n = len < 4 ? len : 4;
+    if (n == 0) return;
+    const double w = 1.0 / (double)n;
+    for (int i = len - n; i < len; ++i) phi[(uint64_t)(int64_t)ctx[i] % D] += w;
+}
+
+static void probs_from_phi(uint64_t V, uint64_t D, const double* W, const double* phi, double* z) {
+    for (uint64_t v = 0; v < V; ++v) {
+        double s = 0.0;
+        for (uint64_t d = 0; d < D; ++d) s += W[v * D + d] * phi[d];
+        z[v] = s;
+    }
+    double zmax = z[0];
+    for (uint64_t v = 1; v < V; ++v)
+        if (z[v] > zmax) zmax = z[v]; /* std::max_element: first maximum */
+    double denom = 0.0;
+    for (uint64_t v = 0; v < V; ++v) {
+        z[v] = exp(z[v] - zmax);
+        denom += z[v];
+    }
+    for (uint64_t v = 0; v < V; ++v) z[v] /= denom;
+}
+
+void fmo_probabilities(uint64_t V, uint64_t D, const double* W, const int* ctx, int n, double* p) {
+    double* phi = (double*)malloc(D * sizeof(double));
+    fmo_featurize(V, D, ctx, n, phi);
+    probs_from_phi(V, D, W, phi, p);
+    free(phi);
+}
+
+double fmo_log_prob(uint64_t V, uint64_t D, const double* W, const int* ctx, int n, int action) {
+    double* p = (double*)malloc(V * sizeof(double));
+    fmo_probabilities(V, D, W, ctx, n, p);
+    const double lp = log(p[action]);
+    free(p);
+    return lp;
+}
+
+static void accumulate(uint64_t V, uint64_t D, const double* W, const int* ctx, int n, int action,
+                       double weight, double* out, double* phi, double* p, double* logp) {
+    fmo_featurize(V, D, ctx, n, phi);
+    probs_from_phi(V, D, W, phi, p);
+    if (logp) *logp = (action >= 0 && (uint64_t)action < V) ? log(p[action]) : NAN;
+    for (uint64_t v = 0; v < V; ++v) {
+        const double coef = weight * (((int)v == action ? 1.0 : 0.0) - p[v]);
+        if (coef == 0.0) continue;
+        for (uint64_t d = 0; d < D; ++d) out[v * D + d] += coef * phi[d];
+    }
+}
+
+void fmo_accumulate_grad(uint64_t V, uint64_t D, const double* W, const int* ctx, int n, int action,
+                         double weight, double* out) {
+    double* phi = (double*)malloc(D * sizeof(double));
+    double* p = (double*)malloc(V * sizeof(double));
+    accumulate(V, D, W, ctx, n, action, weight, out, phi, p, NULL);
+    free(phi);
+    free(p);
+}
+
+/* ---- experience_store.hpp:92-114 -------------------------------------- */
+
+typedef struct {
+    const char* id;
+    int32_t turns, traj;
+    int64_t ver;
+    int32_t idx;
+} rec_key;
+
+static int key_cmp(const void* a, const void* b) { /* std::tuple<string,int,int,int64> < */
+    const rec_key* x = (const rec_key*)a;
+    const rec_key* y = (const rec_key*)b;
+    const int c = strcmp(x->id, y->id);
+    if (c) return c;
+    if (x->turns != y->turns) return x->turns < y->turns ? -1 : 1;
+    if (x->traj != y->traj) return x->traj < y->traj ? -1 : 1;
+    if (x->ver != y->ver) return x->ver < y->ver ? -1 : 1;
+    return 0;
+}
+
+int fmo_poll_select(int n, const char* const* ids, const int32_t* turns, const int32_t* trajs,
+                    const int64_t* versions, const uint8_t* ready, const uint8_t* processing,
+                    int64_t current_version, int64_t mb, int32_t* out) {
+    if (mb < 1) return -1;
+    rec_key* k = (rec_key*)malloc((size_t)(n > 0 ? n : 1) * sizeof(rec_key));
+    for (int i = 0; i < n; ++i) k[i] = (rec_key){ids[i], turns[i], trajs[i], versions[i], i};
+    qsort(k, (size_t)n, sizeof(rec_key), key_cmp);
+    int chosen = 0;
+    for (int i = 0; i < n && chosen < mb; ++i) {
+        const int j = k[i].idx;
+        if (processing[j] || versions[j] != current_version || !ready[j]) continue;
+        out[chosen++] = j;
+    }
+    free(k);
+    return chosen < mb ? 0 : (int)mb;
+}
+
+/* ---- packed rows (training.hpp:378-394 + policy.hpp:42-51) ------------ */
+
+int64_t fmo_pack_rows(int n_samples, const uint8_t* payloads, const int64_t* prompt_off,
+                      const int64_t* resp_off, const double* adv, int64_t G, int32_t* actions,
+                      int32_t* ctx4, int32_t* n_ctx, int32_t* row_sample, float* coef) {
+    int64_t r = 0;
+    for (int s = 0; s < n_samples; ++s) {
+        const uint64_t np = fmo_decode_tokens(payloads + prompt_off[s], NULL);
+        const uint64_t nr = fmo_decode_tokens(payloads + resp_off[s], NULL);
+        int* ctx = (int*)malloc((np + nr + 1) * sizeof(int));
+        fmo_decode_tokens(payloads + prompt_off[s], ctx);
+        fmo_decode_tokens(payloads + resp_off[s], ctx + np);
+        for (uint64_t t = 0; t < nr; ++t, ++r) {
+            const int64_t len = (int64_t)(np + t);
+            const int n = len < 4 ? (int)len : 4;
+            if (actions) actions[r] = ctx[np + t];
+            if (n_ctx) n_ctx[r] = n;
+            if (row_sample) row_sample[r] = s;
+            if (ctx4)
+                for (int j = 0; j < 4; ++j) ctx4[4 * r + j] = j < n ? ctx[len - n + j] : -1;
+            if (coef) coef[r] = n ? (float)(-adv[s] / ((double)G * (double)n)) : 0.0f;
+        }
+        free(ctx);
+    }
+    return r;
+}
+
+/* ---- training.hpp:355-456 --------------------------------------------- */
+
+static double frob(const double* a, uint64_t n) { /* tensor.hpp:36-40 */
+    double s = 0.0;
+    for (uint64_t i = 0; i < n; ++i) s += a[i] * a[i];
+    return sqrt(s);
+}
+
+int fmo_run_agent(uint64_t V, uint64_t D, int64_t G, int64_t mb, int n_updates,
+                  const uint8_t* payloads, const int64_t* prompt_off, const int64_t* resp_off,
+                  const double* adv, double lr, double b1, double b2, double eps, double* W,
+                  double* m, double* v, double* mb_grad_norm, double* upd_grad_norm,
+                  double* token_logp, double* last_grad) {
+    const uint64_t P = V * D;
+    double* term = (double*)malloc(P * sizeof(double));
+    double* micro = (double*)malloc(P * sizeof(double));
+    double* grad = (double*)malloc(P * sizeof(double));
+    double* phi = (double*)malloc(D * sizeof(double));
+    double* p = (double*)malloc(V * sizeof(double));
+    int64_t step = 0, tok = 0;
+    int s = 0, mbi = 0;
+    for (int u = 0; u < n_updates; ++u) {
+        memset(grad, 0, P * sizeof(double));
+        for (int64_t b = 0; b < G / mb; ++b) {
+            memset(micro, 0, P * sizeof(double));
+            for (int64_t k = 0; k < mb; ++k, ++s) {
+                const uint64_t np = fmo_decode_tokens(payloads + prompt_off[s], NULL);
+                const uint64_t nr = fmo_decode_tokens(payloads + resp_off[s], NULL);
+                int* ctx = (int*)malloc((np + nr + 1) * sizeof(int));
+                fmo_decode_tokens(payloads + prompt_off[s], ctx);
+                fmo_decode_tokens(payloads + resp_off[s], ctx + np);
+                memset(term, 0, P * sizeof(double));
+                for (uint64_t t = 0; t < nr; ++t, ++tok)
+                    accumulate(V, D, W, ctx, (int)(np + t), ctx[np + t], 1.0, term, phi, p,
+                               token_logp ? &token_logp[tok] : NULL);
+                for (uint64_t i = 0; i < P; ++i) term[i] *= adv[s];   /* term.scale(A) */
+                for (uint64_t i = 0; i < P; ++i) micro[i] += term[i]; /* micro_sum.add */
+                for (uint64_t i = 0; i < P; ++i) grad[i] += term[i];  /* canonical sum */
+                free(ctx);
+            }
+            mb_grad_norm[mbi++] = frob(micro, P) / (double)G;
+        }
+        for (uint64_t i = 0; i < P; ++i) grad[i] *= -1.0 / (double)G;
+        fmo_adam_step(W, m, v, &step, grad, P, lr, b1, b2, eps);
+        upd_grad_norm[u] = frob(grad, P);
+        if (last_grad) memcpy(last_grad, grad, P * sizeof(double));
+    }
+    free(term);
+    free(micro);
+    free(grad);
+    free(phi);
+    free(p);
+    return 0;
+}

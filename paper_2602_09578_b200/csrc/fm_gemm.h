@@ -1,0 +1,44 @@
+// fm_gemm.h — host-visible interface of the tcgen05 TN GEMM (k_gemm_tc.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace fm {
+
+constexpr int kGemmBM = 128;
+constexpr int kGemmBN = 256;
+constexpr int kGemmBK = 64;
+constexpr int kGemmStages = 4;
+
+enum class GemmKind { Logits, Grad };
+
+// C[M][N] = sum_k A[M][K] * B[N][K]; A/B bf16 K-major, described by TMA maps
+// with boxes {64, 128} (A) and {64, 256} (B), SWIZZLE_128B.
+struct GemmArgs {
+    int M, N, K;
+    int group_m;          // L2 raster: tiles visited in column-major groups of group_m row-tiles
+    float* out;           // Logits: Z [M][ld_out]; Grad: dW [M][ld_out]
+    long long ld_out;
+    const float* row_scale;  // Logits: per-row 1/n_ctx
+    float2* stats;           // Logits: [M][stats_ld] (max, sum exp) per 256-col tile
+    int stats_ld;
+    int accumulate;          // Grad: 1 = dW += acc, 0 = dW = acc
+    double* sumsq;           // Grad: += sum(acc^2) (micro-batch grad norm^2)
+};
+
+size_t gemm_smem_bytes();
+cudaError_t gemm_tn_launch(GemmKind kind, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                           const GemmArgs& args, int num_sms, cudaStream_t stream);
+
+// Builds a 2-D bf16 K-major tensor map over a row-major [rows][cols] matrix
+// (cols contiguous), box {64, box_rows}, SWIZZLE_128B.
+bool make_tmap_bf16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
+                           uint32_t box_rows);
+// Plain (no swizzle) 2-D map, any 4/2-byte dtype, box {box_cols, box_rows}.
+bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, uint32_t elem_bytes,
+                  uint64_t rows, uint64_t cols, uint32_t box_rows, uint32_t box_cols);
+
+}  // namespace fm

@@ -1,0 +1,81 @@
+// fm_kernels.h — launch wrappers for the HBM-bound hot-path kernels
+// (k_path.cu).  All take an explicit stream; none synchronise.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace fm {
+
+// One sample of a micro-batch as the device sees it: byte offsets of the
+// encoded prompt / response token lists in the token arena (codec.hpp:15-22
+// format), their token counts, the first packed row of the sample and its
+// advantage (training.hpp:371, 386).
+struct SampleDesc {
+    int64_t prompt_off;
+    int64_t resp_off;
+    int32_t prompt_n;
+    int32_t resp_n;
+    int64_t row_start;
+    double adv;
+};
+
+struct RowBuffers {
+    int32_t* action;   // [Mpad]
+    int4* ctx4;        // [Mpad] last <=4 context tokens, -1 padded
+    int32_t* n_ctx;    // [Mpad]
+    int32_t* sample;   // [Mpad]
+    float* coef;       // [Mpad] -A/(G*n)   (0 for padding rows)
+    float* rscale;     // [Mpad] 1/n        (0 for n == 0)
+    float* lse;        // [Mpad]
+    float* logp;       // [Mpad]
+    float* coef_eff;   // [Mpad] coef * surrogate factor
+};
+
+// K-gather: decode the selected records' token payloads straight out of the
+// arena into packed rows; optionally scatter integer-count features into the
+// dense bf16 operands Phic [Mpad][D] and Phic^T [D][Mpad] (pre-zeroed).
+cudaError_t launch_gather(const uint8_t* arena, const SampleDesc* sd, int n_samples, int64_t row_lo,
+                          int64_t M, int64_t Mpad, int64_t global_batch, uint64_t D, RowBuffers rows,
+                          __nv_bfloat16* phic, __nv_bfloat16* phict, cudaStream_t s);
+
+// K-lse: combine GEMM1's per-tile softmax partials into lse, taken-token
+// log-prob and the effective row coefficient (PPO-clip surrogate optional).
+cudaError_t launch_lse(const float* Z, int64_t ldz, const float2* stats, int stats_ld, int64_t M,
+                       int64_t Mpad, int64_t V, const SampleDesc* sd, int64_t global_batch,
+                       RowBuffers rows, const float* old_logp, float clip_eps, double* loss_acc,
+                       cudaStream_t s);
+
+// K-loss (fused log-softmax gradient): G^T[v][t] = coef_eff_t * (delta(v,a_t) - exp(z - lse_t)),
+// Z tiles streamed in through TMA, G^T tiles stored through TMA.
+cudaError_t launch_softmax_grad(const CUtensorMap& tmZ, const CUtensorMap& tmGt, int64_t Mpad,
+                                int64_t V, RowBuffers rows, cudaStream_t s);
+
+// K-adam (training.hpp:37-51): fp64 master weights, fp32 moments, gradient
+// of type G (float for the tensor-core path, double for parity mode);
+// optionally writes the bf16 shadow and zeroes the gradient.  Accumulates
+// sum(g^2) into *gsq for the update grad_norm.
+template <typename G>
+cudaError_t launch_adam(double* w, float* m, float* v, G* g, __nv_bfloat16* w16, uint64_t n,
+                        double lr, double b1, double b2, double eps, double bc1, double bc2,
+                        int zero_grad, double* gsq, int num_sms, cudaStream_t s);
+
+cudaError_t launch_to_bf16(const double* w, __nv_bfloat16* w16, uint64_t n, int num_sms,
+                           cudaStream_t s);
+
+// K-adv (training.hpp:54-67): one warp per reward group, fp64 shuffle reductions.
+cudaError_t launch_group_advantages(const double* rewards, const int32_t* seg_off, int nseg,
+                                    double eps, double* out, cudaStream_t s);
+
+// Parity mode (exact featurizer, fp64 SIMT): per row logits/softmax/grad into dWmb.
+cudaError_t launch_parity_rows(const double* W, uint64_t V, uint64_t D, int64_t M,
+                               RowBuffers rows, const SampleDesc* sd, int64_t global_batch,
+                               double* zscratch, double* dWmb, double* logp64, double* loss_acc,
+                               cudaStream_t s);
+// sumsq += |dWmb|^2; dW += dWmb; dWmb = 0
+cudaError_t launch_parity_fold(double* dW, double* dWmb, uint64_t n, double* sumsq, int num_sms,
+                               cudaStream_t s);
+
+}  // namespace fm

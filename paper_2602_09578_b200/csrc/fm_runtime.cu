@@ -1,0 +1,1169 @@
+// fm_runtime.cu — C ABI implementation: device contexts, the token arena,
+// per-agent trainer state, the micro-batch pipeline
+//   K-gather -> K-GEMM1 (tcgen05) -> K-lse -> K-softmax-grad -> K-GEMM2 (tcgen05)
+// (or the fp64 parity pipeline), the fused Adam update, training-state swap
+// and the NCCL gradient all-reduce.
+//
+// Memory layout in HBM: every agent matrix is row-major
+// [V][D] (row = vocab id, col = feature; tensor.hpp:13-22):
+//   W    f64   master weights            (8 B/param)
+//   m, v f32   Adam moments              (4+4 B/param)
+//   dW   f32   gradient accumulator      (4 B/param; f64 in parity mode)
+//   W16  bf16  GEMM shadow of W          (2 B/param; tensor-core mode only)
+// Per-GPU workspace, sized for the largest micro-batch (Mpad = rows rounded
+// up to 128): packed rows, Phic [Mpad][D] / Phic^T [D][Mpad] bf16, Z [Mpad][V]
+// fp32 logits, softmax partials [Mpad][V/256], G^T [V][Mpad] bf16.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "fm_gemm.h"
+#include "fm_internal.h"
+#include "fm_kernels.h"
+
+using namespace fm;
+
+namespace {
+
+constexpr int kReportRing = 256;
+constexpr int kStagingSlots = 4;
+
+// ---- driver entry point for cuTensorMapEncodeTiled (no -lcuda link) -------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t n) {
+    *p = nullptr;
+    if (n == 0) return cudaSuccess;
+    return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+}
+
+}  // namespace
+
+namespace fm {
+
+bool make_tmap_bf16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    EncodeTiledFn f = encode_fn();
+    if (!f) return false;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint32_t box[2] = {64, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return f(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, uint32_t elem_bytes, uint64_t rows,
+                  uint64_t cols, uint32_t box_rows, uint32_t box_cols) {
+    EncodeTiledFn f = encode_fn();
+    if (!f) return false;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * elem_bytes};
+    const cuuint32_t box[2] = {box_cols, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return f(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace fm
+
+// ===========================================================================
+// context
+// ===========================================================================
+struct Workspace {
+    int64_t rows_cap = 0;  // Mpad capacity
+    uint64_t vocab_cap = 0, feat_cap = 0;
+    int32_t* action = nullptr;
+    int4* ctx4 = nullptr;
+    int32_t* n_ctx = nullptr;
+    int32_t* sample = nullptr;
+    float *coef = nullptr, *rscale = nullptr, *lse = nullptr, *logp = nullptr, *coef_eff = nullptr;
+    float* old_logp = nullptr;
+    __nv_bfloat16 *phic = nullptr, *phict = nullptr, *gt = nullptr;
+    float* Z = nullptr;
+    float2* stats = nullptr;
+    // parity mode scratch
+    int64_t prow_cap = 0;
+    uint64_t pvocab_cap = 0, pparam_cap = 0;
+    double *zscratch = nullptr, *dWmb = nullptr, *logp64 = nullptr;
+    SampleDesc* sd = nullptr;
+    int sd_cap = 0;
+};
+
+struct fm_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;    // compute
+    cudaStream_t copy_in = nullptr;   // swap-in (H2D / D2D / P2P)
+    cudaStream_t copy_out = nullptr;  // swap-out
+    uint8_t* arena = nullptr;
+    uint64_t arena_cap = 0, arena_used = 0;
+    std::unordered_map<uint64_t, uint64_t> arena_ntok;  // offset -> token count
+    Workspace ws;
+    // pinned staging (sample descriptors, host payloads) with reuse events
+    uint8_t* staging[kStagingSlots] = {};
+    size_t staging_cap[kStagingSlots] = {};
+    cudaEvent_t staging_ev[kStagingSlots] = {};
+    int staging_next = 0;
+    // arena region reserved for the end-to-end host path
+    uint64_t e2e_off = 0, e2e_cap = 0;
+};
+
+namespace fm {
+uint64_t arena_token_count(const fm_ctx* ctx, uint64_t offset, bool* found) {
+    auto it = ctx->arena_ntok.find(offset);
+    *found = it != ctx->arena_ntok.end();
+    return *found ? it->second : 0;
+}
+}  // namespace fm
+
+namespace {
+
+int set_dev(const fm_ctx* c) {
+    FM_CUDA(cudaSetDevice(c->device));
+    return FM_OK;
+}
+
+// Returns a pinned staging slot of >= bytes whose previous use has completed.
+int staging_acquire(fm_ctx* c, size_t bytes, uint8_t** out, cudaEvent_t* ev) {
+    const int k = c->staging_next;
+    c->staging_next = (k + 1) % kStagingSlots;
+    FM_CUDA(cudaEventSynchronize(c->staging_ev[k]));
+    if (c->staging_cap[k] < bytes) {
+        if (c->staging[k]) FM_CUDA(cudaFreeHost(c->staging[k]));
+        size_t cap = std::max<size_t>(bytes, 1 << 20);
+        FM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->staging[k]), cap, cudaHostAllocDefault));
+        c->staging_cap[k] = cap;
+    }
+    *out = c->staging[k];
+    *ev = c->staging_ev[k];
+    return FM_OK;
+}
+
+void ws_free(Workspace& w) {
+    cudaFree(w.action);
+    cudaFree(w.ctx4);
+    cudaFree(w.n_ctx);
+    cudaFree(w.sample);
+    cudaFree(w.coef);
+    cudaFree(w.rscale);
+    cudaFree(w.lse);
+    cudaFree(w.logp);
+    cudaFree(w.coef_eff);
+    cudaFree(w.old_logp);
+    cudaFree(w.phic);
+    cudaFree(w.phict);
+    cudaFree(w.gt);
+    cudaFree(w.Z);
+    cudaFree(w.stats);
+    cudaFree(w.zscratch);
+    cudaFree(w.dWmb);
+    cudaFree(w.logp64);
+    cudaFree(w.sd);
+    w = Workspace{};
+}
+
+uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
+
+// Ensure tensor-core workspace for Mpad rows, vocab V, features D.
+int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
+    Workspace& w = c->ws;
+    if (Mpad <= w.rows_cap && V <= w.vocab_cap && D <= w.feat_cap && w.Z) return FM_OK;
+    const int64_t R = std::max<int64_t>(Mpad, w.rows_cap);
+    const uint64_t VV = std::max<uint64_t>(V, w.vocab_cap), DD = std::max<uint64_t>(D, w.feat_cap);
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    Workspace keep_parity;
+    std::swap(keep_parity.zscratch, w.zscratch);
+    std::swap(keep_parity.dWmb, w.dWmb);
+    std::swap(keep_parity.logp64, w.logp64);
+    keep_parity.prow_cap = w.prow_cap;
+    keep_parity.pvocab_cap = w.pvocab_cap;
+    keep_parity.pparam_cap = w.pparam_cap;
+    ws_free(w);
+    w.zscratch = keep_parity.zscratch;
+    w.dWmb = keep_parity.dWmb;
+    w.logp64 = keep_parity.logp64;
+    w.prow_cap = keep_parity.prow_cap;
+    w.pvocab_cap = keep_parity.pvocab_cap;
+    w.pparam_cap = keep_parity.pparam_cap;
+    const uint64_t ldz = round_up(VV, 4);
+    const uint64_t tiles_n = (VV + kGemmBN - 1) / kGemmBN;
+    cudaError_t e = cudaSuccess;
+    e = e ? e : dalloc(&w.action, R);
+    e = e ? e : dalloc(&w.ctx4, R);
+    e = e ? e : dalloc(&w.n_ctx, R);
+    e = e ? e : dalloc(&w.sample, R);
+    e = e ? e : dalloc(&w.coef, R);
+    e = e ? e : dalloc(&w.rscale, R);
+    e = e ? e : dalloc(&w.lse, R);
+    e = e ? e : dalloc(&w.logp, R);
+    e = e ? e : dalloc(&w.coef_eff, R);
+    e = e ? e : dalloc(&w.old_logp, R);
+    e = e ? e : dalloc(&w.phic, static_cast<size_t>(R) * DD);
+    e = e ? e : dalloc(&w.phict, static_cast<size_t>(R) * DD);
+    e = e ? e : dalloc(&w.gt, static_cast<size_t>(R) * VV);
+    e = e ? e : dalloc(&w.Z, static_cast<size_t>(R) * ldz);
+    e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n);
+    if (e != cudaSuccess) {
+        ws_free(w);
+        return fail(FM_ERR_DEVICE_OOM, std::string("workspace allocation: ") + cudaGetErrorString(e));
+    }
+    w.rows_cap = R;
+    w.vocab_cap = VV;
+    w.feat_cap = DD;
+    return FM_OK;
+}
+
+int ws_reserve_rows(fm_ctx* c, int64_t R) {  // row arrays only (parity mode)
+    Workspace& w = c->ws;
+    if (R <= w.rows_cap && w.action) return FM_OK;
+    if (w.Z) return ws_reserve_tc(c, R, w.vocab_cap, w.feat_cap);
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(w.action);
+    cudaFree(w.ctx4);
+    cudaFree(w.n_ctx);
+    cudaFree(w.sample);
+    cudaFree(w.coef);
+    cudaFree(w.rscale);
+    cudaFree(w.lse);
+    cudaFree(w.logp);
+    cudaFree(w.coef_eff);
+    cudaFree(w.old_logp);
+    cudaError_t e = cudaSuccess;
+    e = e ? e : dalloc(&w.action, R);
+    e = e ? e : dalloc(&w.ctx4, R);
+    e = e ? e : dalloc(&w.n_ctx, R);
+    e = e ? e : dalloc(&w.sample, R);
+    e = e ? e : dalloc(&w.coef, R);
+    e = e ? e : dalloc(&w.rscale, R);
+    e = e ? e : dalloc(&w.lse, R);
+    e = e ? e : dalloc(&w.logp, R);
+    e = e ? e : dalloc(&w.coef_eff, R);
+    e = e ? e : dalloc(&w.old_logp, R);
+    if (e != cudaSuccess) return fail(FM_ERR_DEVICE_OOM, cudaGetErrorString(e));
+    w.rows_cap = R;
+    return FM_OK;
+}
+
+int ws_reserve_parity(fm_ctx* c, int64_t M, uint64_t V, uint64_t P) {
+    Workspace& w = c->ws;
+    int st = ws_reserve_rows(c, std::max<int64_t>(M, 1));
+    if (st) return st;
+    if (M * static_cast<int64_t>(V) > w.prow_cap * static_cast<int64_t>(w.pvocab_cap) || !w.zscratch) {
+        FM_CUDA(cudaStreamSynchronize(c->stream));
+        cudaFree(w.zscratch);
+        cudaFree(w.logp64);
+        const int64_t R = std::max<int64_t>(M, w.prow_cap);
+        const uint64_t VV = std::max<uint64_t>(V, w.pvocab_cap);
+        if (dalloc(&w.zscratch, static_cast<size_t>(R) * VV) || dalloc(&w.logp64, R))
+            return fail(FM_ERR_DEVICE_OOM, "parity scratch");
+        w.prow_cap = R;
+        w.pvocab_cap = VV;
+    }
+    if (M > w.prow_cap) {
+        FM_CUDA(cudaStreamSynchronize(c->stream));
+        cudaFree(w.logp64);
+        if (dalloc(&w.logp64, M)) return fail(FM_ERR_DEVICE_OOM, "parity logp");
+        w.prow_cap = M;
+    }
+    if (P > w.pparam_cap || !w.dWmb) {
+        FM_CUDA(cudaStreamSynchronize(c->stream));
+        cudaFree(w.dWmb);
+        if (dalloc(&w.dWmb, P)) return fail(FM_ERR_DEVICE_OOM, "parity dWmb");
+        FM_CUDA(cudaMemset(w.dWmb, 0, P * sizeof(double)));
+        w.pparam_cap = P;
+    }
+    return FM_OK;
+}
+
+int ws_reserve_sd(fm_ctx* c, int n) {
+    Workspace& w = c->ws;
+    if (n <= w.sd_cap) return FM_OK;
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(w.sd);
+    const int cap = std::max(n, 256);
+    if (dalloc(&w.sd, cap)) return fail(FM_ERR_DEVICE_OOM, "sample descriptors");
+    w.sd_cap = cap;
+    return FM_OK;
+}
+
+RowBuffers row_buffers(Workspace& w) {
+    RowBuffers r;
+    r.action = w.action;
+    r.ctx4 = w.ctx4;
+    r.n_ctx = w.n_ctx;
+    r.sample = w.sample;
+    r.coef = w.coef;
+    r.rscale = w.rscale;
+    r.lse = w.lse;
+    r.logp = w.logp;
+    r.coef_eff = w.coef_eff;
+    return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fm_ctx_create(int device, fm_ctx** out) {
+    FM_GUARD_BEGIN
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(FM_ERR_NO_DEVICE, "no CUDA device visible (the B200 path has no CPU fallback)");
+    }
+    if (device < 0 || device >= n) return fail(FM_ERR_NO_DEVICE, "device index out of range");
+    cudaDeviceProp prop;
+    FM_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(FM_ERR_NO_DEVICE, std::string("sm_100 device required, found ") + prop.name);
+    FM_CUDA(cudaSetDevice(device));
+    auto* c = new fm_ctx();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    FM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    FM_CUDA(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
+    FM_CUDA(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
+    for (int i = 0; i < kStagingSlots; ++i)
+        FM_CUDA(cudaEventCreateWithFlags(&c->staging_ev[i], cudaEventDisableTiming));
+    {   // keep freed agent state in the stream-ordered pool: swaps re-use it without remapping
+        cudaMemPool_t pool;
+        FM_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = ~0ull;
+        FM_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
+    if (!encode_fn()) {
+        delete c;
+        return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    }
+    *out = c;
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int fm_ctx_destroy(fm_ctx* c) {
+    if (!c) return FM_OK;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    ws_free(c->ws);
+    cudaFree(c->arena);
+    for (int i = 0; i < kStagingSlots; ++i) {
+        if (c->staging[i]) cudaFreeHost(c->staging[i]);
+        cudaEventDestroy(c->staging_ev[i]);
+    }
+    cudaStreamDestroy(c->stream);
+    cudaStreamDestroy(c->copy_in);
+    cudaStreamDestroy(c->copy_out);
+    delete c;
+    return FM_OK;
+}
+
+int fm_ctx_device(const fm_ctx* c) { return c->device; }
+int fm_ctx_num_sms(const fm_ctx* c) { return c->num_sms; }
+
+int fm_ctx_synchronize(fm_ctx* c) {
+    if (int st = set_dev(c)) return st;
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    FM_CUDA(cudaStreamSynchronize(c->copy_in));
+    FM_CUDA(cudaStreamSynchronize(c->copy_out));
+    return FM_OK;
+}
+
+int fm_ctx_reserve(fm_ctx* c, uint64_t arena_bytes, int64_t max_rows, uint64_t V, uint64_t D) {
+    FM_GUARD_BEGIN
+    if (int st = set_dev(c)) return st;
+    if (arena_bytes > c->arena_cap) {
+        FM_CUDA(cudaStreamSynchronize(c->stream));
+        uint8_t* na = nullptr;
+        if (cudaMalloc(&na, arena_bytes) != cudaSuccess) return fail(FM_ERR_DEVICE_OOM, "token arena");
+        if (c->arena_used) FM_CUDA(cudaMemcpy(na, c->arena, c->arena_used, cudaMemcpyDeviceToDevice));
+        cudaFree(c->arena);
+        c->arena = na;
+        c->arena_cap = arena_bytes;
+    }
+    if (max_rows > 0 && V > 0 && D > 0) return ws_reserve_tc(c, static_cast<int64_t>(round_up(max_rows, 128)), V, D);
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int fm_arena_put(fm_ctx* c, const uint8_t* payload, uint64_t nbytes, uint64_t* off_out) {
+    FM_GUARD_BEGIN
+    if (nbytes < 8) return fail(FM_ERR_INVALID_ARG, "payload shorter than its u64 count header");
+    uint64_t ntok;
+    std::memcpy(&ntok, payload, 8);
+    if (nbytes != 8 + 8 * ntok) return fail(FM_ERR_LAYOUT_OUT_OF_BOUNDS, "payload length != 8 + 8*count");
+    if (int st = set_dev(c)) return st;
+    const uint64_t off = round_up(c->arena_used, 16);
+    if (off + nbytes > c->arena_cap) {
+        const uint64_t cap = std::max<uint64_t>(2 * c->arena_cap, off + nbytes + (64u << 20));
+        int st = fm_ctx_reserve(c, cap, 0, 0, 0);
+        if (st) return st;
+    }
+    uint8_t* stg;
+    cudaEvent_t ev;
+    if (int st = staging_acquire(c, nbytes, &stg, &ev)) return st;
+    std::memcpy(stg, payload, nbytes);
+    FM_CUDA(cudaMemcpyAsync(c->arena + off, stg, nbytes, cudaMemcpyHostToDevice, c->stream));
+    FM_CUDA(cudaEventRecord(ev, c->stream));
+    c->arena_used = off + nbytes;
+    c->arena_ntok[off] = ntok;
+    *off_out = off;
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int fm_arena_reset(fm_ctx* c) {
+    if (int st = set_dev(c)) return st;
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    c->arena_used = 0;
+    c->arena_ntok.clear();
+    c->e2e_off = c->e2e_cap = 0;
+    return FM_OK;
+}
+
+uint64_t fm_arena_used(const fm_ctx* c) { return c->arena_used; }
+
+}  // extern "C"
+
+// ===========================================================================
+// agents
+// ===========================================================================
+struct fm_agent {
+    fm_ctx* ctx = nullptr;  // GPU the agent is bound to (null while suspended)
+    std::string name;
+    uint64_t V = 0, D = 0, P = 0;
+    int precision = FM_PRECISION_BF16_TC;
+    // device state
+    double* W = nullptr;
+    float* m = nullptr;
+    float* v = nullptr;
+    void* dW = nullptr;  // float (TC) or double (parity)
+    __nv_bfloat16* W16 = nullptr;
+    bool dw_valid = false;  // dW holds this step's partial sum
+    int64_t step = 0, version = 0, samples = 0;
+    // reports
+    double* d_scalars = nullptr;  // [kReportRing][2]: sumsq, loss
+    double* h_scalars = nullptr;  // pinned mirror
+    cudaEvent_t ev[kReportRing] = {};
+    int64_t rep_tokens[kReportRing] = {};
+    int64_t rep_bs[kReportRing] = {};
+    int64_t next_ticket = 0;
+    bool dp = false;
+    int shard_rank = 0, shard_count = 1;  // token-balanced DP shard of every micro-batch
+    double* d_upd = nullptr;  // update sum g^2
+    double* h_upd = nullptr;
+    int64_t last_rows = 0;
+    // PPO clip
+    float clip_eps = 0.f;
+    bool have_old_logp = false;
+    // swap
+    bool active = false;
+    int park_tier = -1;
+    int park_device = -1;
+    void* park = nullptr;  // W | m | v | dW   (host pinned or device)
+    size_t park_bytes = 0;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_compute = nullptr;
+};
+
+namespace {
+
+size_t dw_elem(const fm_agent* a) { return a->precision == FM_PRECISION_PARITY_F64 ? 8 : 4; }
+
+int agent_alloc_device(fm_agent* a, cudaStream_t s) {
+    const size_t P = a->P;
+    cudaError_t e = cudaSuccess;
+    e = e ? e : cudaMallocAsync(reinterpret_cast<void**>(&a->W), P * 8, s);
+    e = e ? e : cudaMallocAsync(reinterpret_cast<void**>(&a->m), P * 4, s);
+    e = e ? e : cudaMallocAsync(reinterpret_cast<void**>(&a->v), P * 4, s);
+    e = e ? e : cudaMallocAsync(&a->dW, P * dw_elem(a), s);
+    if (a->precision == FM_PRECISION_BF16_TC)
+        e = e ? e : cudaMallocAsync(reinterpret_cast<void**>(&a->W16), P * 2, s);
+    if (e != cudaSuccess) return fail(FM_ERR_DEVICE_OOM, std::string("agent state: ") + cudaGetErrorString(e));
+    return FM_OK;
+}
+
+void agent_free_device(fm_agent* a, cudaStream_t s) {
+    if (a->W) cudaFreeAsync(a->W, s);
+    if (a->m) cudaFreeAsync(a->m, s);
+    if (a->v) cudaFreeAsync(a->v, s);
+    if (a->dW) cudaFreeAsync(a->dW, s);
+    if (a->W16) cudaFreeAsync(a->W16, s);
+    a->W = nullptr;
+    a->m = a->v = nullptr;
+    a->dW = nullptr;
+    a->W16 = nullptr;
+}
+
+int check_active(const fm_agent* a) {
+    if (!a->active || !a->ctx) return fail(FM_ERR_INACTIVE_GROUP, a->name);
+    return FM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fm_agent_create(fm_ctx* c, const char* name, uint64_t V, uint64_t D, int precision, fm_agent** out) {
+    FM_GUARD_BEGIN
+    *out = nullptr;
+    if (!c) return fail(FM_ERR_NO_DEVICE, "null context");
+    if (V == 0 || D == 0) return fail(FM_ERR_CONFIG_ERROR, "vocab and feature dims must be positive");
+    if (precision != FM_PRECISION_BF16_TC && precision != FM_PRECISION_PARITY_F64)
+        return fail(FM_ERR_INVALID_ARG, "unknown precision");
+    if (precision == FM_PRECISION_BF16_TC && (D % 8 != 0 || V % 4 != 0))
+        return fail(FM_ERR_CONFIG_ERROR, "tensor-core mode needs D % 8 == 0 and V % 4 == 0 (TMA row pitch)");
+    if (int st = set_dev(c)) return st;
+    auto* a = new fm_agent();
+    a->ctx = c;
+    a->name = name ? name : "";
+    a->V = V;
+    a->D = D;
+    a->P = V * D;
+    a->precision = precision;
+    if (int st = agent_alloc_device(a, c->stream)) {
+        delete a;
+        return st;
+    }
+    FM_CUDA(cudaMemsetAsync(a->W, 0, a->P * 8, c->stream));
+    FM_CUDA(cudaMemsetAsync(a->m, 0, a->P * 4, c->stream));
+    FM_CUDA(cudaMemsetAsync(a->v, 0, a->P * 4, c->stream));
+    FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * dw_elem(a), c->stream));
+    if (a->W16) FM_CUDA(cudaMemsetAsync(a->W16, 0, a->P * 2, c->stream));
+    FM_CUDA(cudaMalloc(&a->d_scalars, kReportRing * 2 * sizeof(double)));
+    FM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&a->h_scalars), kReportRing * 2 * sizeof(double), 0));
+    FM_CUDA(cudaMalloc(&a->d_upd, sizeof(double)));
+    FM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&a->h_upd), sizeof(double), 0));
+    for (int i = 0; i < kReportRing; ++i) FM_CUDA(cudaEventCreateWithFlags(&a->ev[i], cudaEventDisableTiming));
+    FM_CUDA(cudaEventCreateWithFlags(&a->ev_in, cudaEventDisableTiming));
+    FM_CUDA(cudaEventCreateWithFlags(&a->ev_out, cudaEventDisableTiming));
+    FM_CUDA(cudaEventCreateWithFlags(&a->ev_compute, cudaEventDisableTiming));
+    a->active = true;
+    *out = a;
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int fm_agent_destroy(fm_agent* a) {
+    if (!a) return FM_OK;
+    if (a->ctx) {
+        cudaSetDevice(a->ctx->device);
+        cudaStreamSynchronize(a->ctx->stream);
+        cudaStreamSynchronize(a->ctx->copy_out);
+        agent_free_device(a, a->ctx->stream);
+        cudaStreamSynchronize(a->ctx->stream);
+    }
+    if (a->park) {
+        if (a->park_tier == FM_TIER_HOST) cudaFreeHost(a->park);
+        else {
+            cudaSetDevice(a->park_device);
+            cudaFree(a->park);
+        }
+    }
+    cudaFree(a->d_scalars);
+    cudaFreeHost(a->h_scalars);
+    cudaFree(a->d_upd);
+    cudaFreeHost(a->h_upd);
+    for (int i = 0; i < kReportRing; ++i) cudaEventDestroy(a->ev[i]);
+    cudaEventDestroy(a->ev_in);
+    cudaEventDestroy(a->ev_out);
+    cudaEventDestroy(a->ev_compute);
+    delete a;
+    return FM_OK;
+}
+
+int fm_agent_set_weights(fm_agent* a, const double* W) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
+    fm_ctx* c = a->ctx;
+    if (int st = set_dev(c)) return st;
+    FM_CUDA(cudaMemcpyAsync(a->W, W, a->P * 8, cudaMemcpyHostToDevice, c->stream));
+    if (a->W16) {
+        FM_CUDA(launch_to_bf16(a->W, a->W16, a->P, c->num_sms, c->stream));
+        count_launch();
+    }
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int fm_agent_read_weights(fm_agent* a, double* W) {
+    if (int st = check_active(a)) return st;
+    if (int st = set_dev(a->ctx)) return st;
+    FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
+    FM_CUDA(cudaMemcpy(W, a->W, a->P * 8, cudaMemcpyDeviceToHost));
+    return FM_OK;
+}
+
+int fm_agent_read_moments(fm_agent* a, float* m, float* v, int64_t* step) {
+    if (int st = check_active(a)) return st;
+    if (int st = set_dev(a->ctx)) return st;
+    FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
+    if (m) FM_CUDA(cudaMemcpy(m, a->m, a->P * 4, cudaMemcpyDeviceToHost));
+    if (v) FM_CUDA(cudaMemcpy(v, a->v, a->P * 4, cudaMemcpyDeviceToHost));
+    if (step) *step = a->step;
+    return FM_OK;
+}
+
+int fm_agent_read_grad(fm_agent* a, double* g) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
+    if (int st = set_dev(a->ctx)) return st;
+    FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
+    if (!a->dw_valid) {
+        std::fill(g, g + a->P, 0.0);
+        return FM_OK;
+    }
+    if (a->precision == FM_PRECISION_PARITY_F64) {
+        FM_CUDA(cudaMemcpy(g, a->dW, a->P * 8, cudaMemcpyDeviceToHost));
+    } else {
+        std::vector<float> tmp(a->P);
+        FM_CUDA(cudaMemcpy(tmp.data(), a->dW, a->P * 4, cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < a->P; ++i) g[i] = tmp[i];
+    }
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int64_t fm_agent_version(const fm_agent* a) { return a->version; }
+int64_t fm_agent_samples_accumulated(const fm_agent* a) { return a->samples; }
+int fm_agent_is_active(const fm_agent* a) { return a->active ? 1 : 0; }
+
+int fm_agent_set_clip(fm_agent* a, float clip_eps, const float* old_logp, int64_t n_rows) {
+    if (int st = check_active(a)) return st;
+    fm_ctx* c = a->ctx;
+    if (int st = set_dev(c)) return st;
+    a->clip_eps = clip_eps;
+    a->have_old_logp = false;
+    if (old_logp && clip_eps > 0.f) {
+        if (int st = ws_reserve_rows(c, static_cast<int64_t>(round_up(n_rows, 128)))) return st;
+        FM_CUDA(cudaMemcpyAsync(c->ws.old_logp, old_logp, n_rows * 4, cudaMemcpyHostToDevice, c->stream));
+        FM_CUDA(cudaStreamSynchronize(c->stream));
+        a->have_old_logp = true;
+    }
+    return FM_OK;
+}
+
+int fm_agent_set_shard(fm_agent* a, int rank, int nranks) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(FM_ERR_INVALID_ARG, "bad shard");
+    a->shard_rank = rank;
+    a->shard_count = nranks;
+    a->dp = nranks > 1;
+    return FM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// the micro-batch pipeline
+// ---------------------------------------------------------------------------
+static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total, int64_t G, int64_t* ticket_out) {
+    // data-parallel gang: this rank trains rows [row_lo, row_hi) of the micro-batch
+    const int64_t row_lo = M_total * a->shard_rank / a->shard_count;
+    const int64_t row_hi = M_total * (a->shard_rank + 1) / a->shard_count;
+    const int64_t M = row_hi - row_lo;
+    fm_ctx* c = a->ctx;
+    Workspace& w = c->ws;
+    cudaStream_t s = c->stream;
+    const bool tc = a->precision == FM_PRECISION_BF16_TC;
+    const int64_t Mpad = tc ? static_cast<int64_t>(round_up(static_cast<uint64_t>(M), 128)) : M;
+    if (tc) {
+        if (int st = ws_reserve_tc(c, std::max<int64_t>(Mpad, 128), a->V, a->D)) return st;
+    } else {
+        if (int st = ws_reserve_parity(c, M, a->V, a->P)) return st;
+    }
+    if (int st = ws_reserve_sd(c, n)) return st;
+    // descriptors -> device through pinned staging
+    uint8_t* stg;
+    cudaEvent_t sev;
+    if (int st = staging_acquire(c, sizeof(SampleDesc) * n, &stg, &sev)) return st;
+    std::memcpy(stg, hsd, sizeof(SampleDesc) * n);
+    FM_CUDA(cudaMemcpyAsync(w.sd, stg, sizeof(SampleDesc) * n, cudaMemcpyHostToDevice, s));
+    FM_CUDA(cudaEventRecord(sev, s));
+
+    const int64_t ticket = a->next_ticket++;
+    const int slot = static_cast<int>(ticket % kReportRing);
+    if (ticket >= kReportRing) FM_CUDA(cudaEventSynchronize(a->ev[slot]));  // slot reuse
+    double* scal = a->d_scalars + 2 * slot;
+    FM_CUDA(cudaMemsetAsync(scal, 0, 2 * sizeof(double), s));
+    RowBuffers rows = row_buffers(w);
+
+    if (M > 0) {
+        if (tc) {
+            const uint64_t ldz = round_up(a->V, 4);
+            FM_CUDA(cudaMemsetAsync(w.phic, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
+            FM_CUDA(cudaMemsetAsync(w.phict, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
+            FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, Mpad, G, a->D, rows, w.phic, w.phict, s));
+            // K-GEMM1: Z = Phic * W16^T, epilogue z *= 1/n, softmax partials
+            CUtensorMap tA, tB, tZ, tGt, tPt;
+            if (!make_tmap_bf16_kmajor(&tA, w.phic, Mpad, a->D, kGemmBM) ||
+                !make_tmap_bf16_kmajor(&tB, a->W16, a->V, a->D, kGemmBN) ||
+                !make_tmap_2d(&tZ, w.Z, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Mpad, ldz, 64, 128) ||
+                !make_tmap_bf16_kmajor(&tGt, w.gt, a->V, Mpad, kGemmBM) ||
+                !make_tmap_bf16_kmajor(&tPt, w.phict, a->D, Mpad, kGemmBN))
+                return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+            const int tiles_n = static_cast<int>((a->V + kGemmBN - 1) / kGemmBN);
+            GemmArgs g1{};
+            g1.M = static_cast<int>(M);
+            g1.N = static_cast<int>(a->V);
+            g1.K = static_cast<int>(a->D);
+            g1.group_m = 16;
+            g1.out = w.Z;
+            g1.ld_out = static_cast<long long>(ldz);
+            g1.row_scale = w.rscale;
+            g1.stats = w.stats;
+            g1.stats_ld = tiles_n;
+            FM_CUDA(gemm_tn_launch(GemmKind::Logits, tA, tB, g1, c->num_sms, s));
+            // K-lse
+            FM_CUDA(launch_lse(w.Z, static_cast<int64_t>(ldz), w.stats, tiles_n, M, Mpad,
+                               static_cast<int64_t>(a->V), w.sd, G, rows,
+                               a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1, s));
+            // K-softmax-grad: G^T tiles (zero for padding rows)
+            FM_CUDA(launch_softmax_grad(tZ, tGt, Mpad, static_cast<int64_t>(a->V), rows, s));
+            // K-GEMM2: dW (+)= G^T * Phic ; first contribution of the step overwrites
+            GemmArgs g2{};
+            g2.M = static_cast<int>(a->V);
+            g2.N = static_cast<int>(a->D);
+            g2.K = static_cast<int>(Mpad);
+            g2.group_m = 8;
+            g2.out = static_cast<float*>(a->dW);
+            g2.ld_out = static_cast<long long>(a->D);
+            g2.accumulate = a->dw_valid ? 1 : 0;
+            g2.sumsq = scal;
+            FM_CUDA(gemm_tn_launch(GemmKind::Grad, tGt, tPt, g2, c->num_sms, s));
+            count_launch(5);
+        } else {
+            FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, M, G, a->D, rows, nullptr, nullptr, s));
+            if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * 8, s));
+            FM_CUDA(launch_parity_rows(a->W, a->V, a->D, M, rows, w.sd, G, w.zscratch, w.dWmb, w.logp64,
+                                       scal + 1, s));
+            FM_CUDA(launch_parity_fold(static_cast<double*>(a->dW), w.dWmb, a->P, scal, c->num_sms, s));
+            count_launch(3);
+        }
+        a->dw_valid = true;
+    }
+    a->have_old_logp = false;  // old log-probs apply to one micro-batch
+    a->last_rows = M;
+    FM_CUDA(cudaMemcpyAsync(a->h_scalars + 2 * slot, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    FM_CUDA(cudaEventRecord(a->ev[slot], s));
+    a->rep_tokens[slot] = M;
+    a->rep_bs[slot] = n;
+    a->samples += n;
+    if (ticket_out) *ticket_out = ticket;
+    return FM_OK;
+}
+
+int fm_train_micro_batch(fm_agent* a, const fm_sample* samples, int n, int64_t G, int64_t* ticket_out) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
+    if (n < 0 || (n > 0 && !samples)) return fail(FM_ERR_INVALID_ARG, "bad sample list");
+    if (G <= 0) return fail(FM_ERR_CONFIG_ERROR, "global batch must be positive");
+    if (int st = set_dev(a->ctx)) return st;
+    std::vector<SampleDesc> sd(static_cast<size_t>(n));
+    int64_t rows = 0;
+    for (int i = 0; i < n; ++i) {
+        bool f1, f2;
+        const uint64_t np = arena_token_count(a->ctx, samples[i].prompt_off, &f1);
+        const uint64_t nr = arena_token_count(a->ctx, samples[i].response_off, &f2);
+        if (!f1 || !f2) return fail(FM_ERR_KEY_NOT_FOUND, "sample payload not in this GPU's token arena");
+        sd[i].prompt_off = static_cast<int64_t>(samples[i].prompt_off);
+        sd[i].resp_off = static_cast<int64_t>(samples[i].response_off);
+        sd[i].prompt_n = static_cast<int32_t>(np);
+        sd[i].resp_n = static_cast<int32_t>(nr);
+        sd[i].row_start = rows;
+        sd[i].adv = samples[i].advantage;
+        rows += static_cast<int64_t>(nr);
+    }
+    return train_impl(a, sd.data(), n, rows, G, ticket_out);
+    FM_GUARD_END
+}
+
+// End-to-end variant: host payloads are staged through pinned memory into a
+// reusable arena region inside the call (H2D on the compute stream).
+int fm_train_micro_batch_host(fm_agent* a, const fm_host_sample* samples, int n, int64_t G, int64_t* ticket_out) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
+    if (n < 0 || (n > 0 && !samples)) return fail(FM_ERR_INVALID_ARG, "bad sample list");
+    if (G <= 0) return fail(FM_ERR_CONFIG_ERROR, "global batch must be positive");
+    fm_ctx* c = a->ctx;
+    if (int st = set_dev(c)) return st;
+    std::vector<SampleDesc> sd(static_cast<size_t>(n));
+    uint64_t bytes = 0;
+    int64_t rows = 0;
+    for (int i = 0; i < n; ++i) {
+        uint64_t np, nr;
+        std::memcpy(&np, samples[i].prompt, 8);
+        std::memcpy(&nr, samples[i].response, 8);
+        sd[i].prompt_off = static_cast<int64_t>(bytes);
+        bytes += round_up(8 + 8 * np, 16);
+        sd[i].resp_off = static_cast<int64_t>(bytes);
+        bytes += round_up(8 + 8 * nr, 16);
+        sd[i].prompt_n = static_cast<int32_t>(np);
+        sd[i].resp_n = static_cast<int32_t>(nr);
+        sd[i].row_start = rows;
+        sd[i].adv = samples[i].advantage;
+        rows += static_cast<int64_t>(nr);
+    }
+    // a dedicated region at the arena tail, reused call after call (stream-ordered)
+    if (c->e2e_cap < bytes || c->e2e_off + c->e2e_cap != c->arena_used) {
+        const uint64_t off = round_up(c->arena_used, 256);
+        const uint64_t cap = std::max<uint64_t>(bytes, 1 << 20);
+        if (off + cap > c->arena_cap)
+            if (int st = fm_ctx_reserve(c, off + cap, 0, 0, 0)) return st;
+        c->e2e_off = off;
+        c->e2e_cap = cap;
+        c->arena_used = off + cap;
+    }
+    uint8_t* stg;
+    cudaEvent_t ev;
+    if (int st = staging_acquire(c, bytes, &stg, &ev)) return st;
+    for (int i = 0; i < n; ++i) {
+        std::memcpy(stg + sd[i].prompt_off, samples[i].prompt, 8 + 8 * static_cast<uint64_t>(sd[i].prompt_n));
+        std::memcpy(stg + sd[i].resp_off, samples[i].response, 8 + 8 * static_cast<uint64_t>(sd[i].resp_n));
+        sd[i].prompt_off += static_cast<int64_t>(c->e2e_off);
+        sd[i].resp_off += static_cast<int64_t>(c->e2e_off);
+    }
+    FM_CUDA(cudaMemcpyAsync(c->arena + c->e2e_off, stg, bytes, cudaMemcpyHostToDevice, c->stream));
+    FM_CUDA(cudaEventRecord(ev, c->stream));
+    return train_impl(a, sd.data(), n, rows, G, ticket_out);
+    FM_GUARD_END
+}
+
+int fm_agent_read_logp(fm_agent* a, double* out, int64_t n_rows) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
+    fm_ctx* c = a->ctx;
+    if (int st = set_dev(c)) return st;
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    const int64_t n = std::min<int64_t>(n_rows, a->last_rows);
+    if (a->precision == FM_PRECISION_PARITY_F64) {
+        FM_CUDA(cudaMemcpy(out, c->ws.logp64, n * 8, cudaMemcpyDeviceToHost));
+    } else {
+        std::vector<float> t(static_cast<size_t>(n));
+        FM_CUDA(cudaMemcpy(t.data(), c->ws.logp, n * 4, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i) out[i] = t[static_cast<size_t>(i)];
+    }
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int fm_debug_read_rows(fm_ctx* c, int64_t n, int32_t* action, int32_t* ctx4, int32_t* n_ctx, int32_t* sample,
+                       float* coef) {
+    if (int st = set_dev(c)) return st;
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    if (n > c->ws.rows_cap) return fail(FM_ERR_INVALID_ARG, "more rows than the workspace holds");
+    if (action) FM_CUDA(cudaMemcpy(action, c->ws.action, n * 4, cudaMemcpyDeviceToHost));
+    if (ctx4) FM_CUDA(cudaMemcpy(ctx4, c->ws.ctx4, n * 16, cudaMemcpyDeviceToHost));
+    if (n_ctx) FM_CUDA(cudaMemcpy(n_ctx, c->ws.n_ctx, n * 4, cudaMemcpyDeviceToHost));
+    if (sample) FM_CUDA(cudaMemcpy(sample, c->ws.sample, n * 4, cudaMemcpyDeviceToHost));
+    if (coef) FM_CUDA(cudaMemcpy(coef, c->ws.coef, n * 4, cudaMemcpyDeviceToHost));
+    return FM_OK;
+}
+
+int fm_agent_sync(fm_agent* a) {
+    if (!a->ctx) return FM_OK;
+    if (int st = set_dev(a->ctx)) return st;
+    FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
+    return FM_OK;
+}
+
+int fm_agent_poll_report(fm_agent* a, int64_t ticket, fm_report* out) {
+    if (ticket < 0 || ticket >= a->next_ticket || ticket < a->next_ticket - kReportRing)
+        return fail(FM_ERR_INVALID_ARG, "unknown or expired ticket");
+    const int slot = static_cast<int>(ticket % kReportRing);
+    const cudaError_t q = cudaEventQuery(a->ev[slot]);
+    if (q == cudaErrorNotReady) return 0;
+    if (q != cudaSuccess) return fail(FM_ERR_CUDA, cudaGetErrorString(q));
+    out->ticket = ticket;
+    out->tokens = a->rep_tokens[slot];
+    out->batch_size = a->rep_bs[slot];
+    out->grad_norm = a->dp ? NAN : std::sqrt(a->h_scalars[2 * slot]);
+    out->loss = a->h_scalars[2 * slot + 1];
+    return 1;
+}
+
+int fm_apply_update(fm_agent* a, int64_t G, double lr, double b1, double b2, double eps, double* grad_norm_out,
+                    int64_t* version_out) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
+    if (a->samples != G)
+        return fail(FM_ERR_INCOMPLETE_BATCH,
+                    a->name + " accumulated " + std::to_string(a->samples) + " of " + std::to_string(G));
+    fm_ctx* c = a->ctx;
+    if (int st = set_dev(c)) return st;
+    cudaStream_t s = c->stream;
+    if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * dw_elem(a), s));
+    a->step += 1;
+    const double bc1 = 1.0 - std::pow(b1, static_cast<double>(a->step));  // training.hpp:42-43
+    const double bc2 = 1.0 - std::pow(b2, static_cast<double>(a->step));
+    FM_CUDA(cudaMemsetAsync(a->d_upd, 0, sizeof(double), s));
+    if (a->precision == FM_PRECISION_PARITY_F64) {
+        FM_CUDA(launch_adam<double>(a->W, a->m, a->v, static_cast<double*>(a->dW), nullptr, a->P, lr, b1, b2, eps,
+                                    bc1, bc2, 1, a->d_upd, c->num_sms, s));
+    } else {
+        // the next step's first GEMM2 overwrites dW, so no zeroing pass here
+        FM_CUDA(launch_adam<float>(a->W, a->m, a->v, static_cast<float*>(a->dW), a->W16, a->P, lr, b1, b2, eps,
+                                   bc1, bc2, 0, a->d_upd, c->num_sms, s));
+    }
+    count_launch();
+    a->dw_valid = false;
+    a->samples = 0;
+    a->version += 1;
+    FM_CUDA(cudaMemcpyAsync(a->h_upd, a->d_upd, sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (grad_norm_out) {
+        FM_CUDA(cudaStreamSynchronize(s));
+        *grad_norm_out = std::sqrt(*a->h_upd);
+    }
+    if (version_out) *version_out = a->version;
+    return FM_OK;
+    FM_GUARD_END
+}
+
+// ---------------------------------------------------------------------------
+// training-state swap
+// ---------------------------------------------------------------------------
+int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
+    fm_ctx* c = a->ctx;
+    if (int st = set_dev(c)) return st;
+    const size_t P = a->P;
+    const size_t dwb = a->dw_valid ? P * dw_elem(a) : 0;
+    const size_t bytes = P * 16 + P * dw_elem(a);
+    const int pdev = tier == FM_TIER_PEER ? peer_device : c->device;
+    if (a->park && (a->park_tier != tier || a->park_device != pdev || a->park_bytes < bytes)) {
+        FM_CUDA(cudaStreamSynchronize(c->copy_out));
+        if (a->park_tier == FM_TIER_HOST) cudaFreeHost(a->park);
+        else {
+            cudaSetDevice(a->park_device);
+            cudaFree(a->park);
+            cudaSetDevice(c->device);
+        }
+        a->park = nullptr;
+    }
+    if (!a->park) {
+        if (tier == FM_TIER_HOST) {
+            if (cudaHostAlloc(&a->park, bytes, cudaHostAllocDefault) != cudaSuccess)
+                return fail(FM_ERR_HOST_OOM, "pinned parking buffer");
+        } else if (tier == FM_TIER_DEVICE || tier == FM_TIER_PEER) {
+            if (tier == FM_TIER_PEER) {
+                int can = 0;
+                FM_CUDA(cudaDeviceCanAccessPeer(&can, c->device, pdev));
+                if (!can) return fail(FM_ERR_CONFIG_ERROR, "no peer access to device " + std::to_string(pdev));
+                cudaError_t pe = cudaDeviceEnablePeerAccess(pdev, 0);
+                if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) FM_CUDA(pe);
+                cudaGetLastError();
+                FM_CUDA(cudaSetDevice(pdev));
+            }
+            const cudaError_t e = cudaMalloc(&a->park, bytes);
+            FM_CUDA(cudaSetDevice(c->device));
+            if (e != cudaSuccess) return fail(FM_ERR_DEVICE_OOM, "parking buffer");
+        } else {
+            return fail(FM_ERR_INVALID_ARG, "unknown tier");
+        }
+        a->park_tier = tier;
+        a->park_device = pdev;
+        a->park_bytes = bytes;
+    }
+    // order the copy-out after everything the agent has queued on the compute stream
+    FM_CUDA(cudaEventRecord(a->ev_compute, c->stream));
+    FM_CUDA(cudaStreamWaitEvent(c->copy_out, a->ev_compute, 0));
+    uint8_t* p = static_cast<uint8_t*>(a->park);
+    auto cp = [&](void* dst, const void* src, size_t n) -> cudaError_t {
+        if (tier == FM_TIER_PEER) return cudaMemcpyPeerAsync(dst, pdev, src, c->device, n, c->copy_out);
+        return cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, c->copy_out);
+    };
+    FM_CUDA(cp(p, a->W, P * 8));
+    FM_CUDA(cp(p + P * 8, a->m, P * 4));
+    FM_CUDA(cp(p + P * 12, a->v, P * 4));
+    if (dwb) FM_CUDA(cp(p + P * 16, a->dW, dwb));  // only mid-step gradients travel
+    FM_CUDA(cudaEventRecord(a->ev_out, c->copy_out));
+    agent_free_device(a, c->copy_out);
+    a->active = false;
+    a->ctx = nullptr;
+    a->park_device = pdev;
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int fm_agent_activate(fm_agent* a, fm_ctx* c) {
+    FM_GUARD_BEGIN
+    if (a->active) return fail(FM_ERR_CONFIG_ERROR, a->name + " already active");
+    if (!c) return fail(FM_ERR_NO_DEVICE, "null context");
+    if (int st = set_dev(c)) return st;
+    const size_t P = a->P;
+    // the parked copy must have landed before we read it back
+    FM_CUDA(cudaStreamWaitEvent(c->copy_in, a->ev_out, 0));
+    if (int st = agent_alloc_device(a, c->copy_in)) return st;
+    uint8_t* p = static_cast<uint8_t*>(a->park);
+    const bool peer = a->park_tier != FM_TIER_HOST && a->park_device != c->device;
+    if (peer) {
+        int can = 0;
+        FM_CUDA(cudaDeviceCanAccessPeer(&can, c->device, a->park_device));
+        if (!can) return fail(FM_ERR_CONFIG_ERROR, "no peer access to parking device");
+        cudaError_t pe = cudaDeviceEnablePeerAccess(a->park_device, 0);
+        if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) FM_CUDA(pe);
+        cudaGetLastError();
+    }
+    auto cp = [&](void* dst, const void* src, size_t n) -> cudaError_t {
+        if (peer) return cudaMemcpyPeerAsync(dst, c->device, src, a->park_device, n, c->copy_in);
+        return cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, c->copy_in);
+    };
+    FM_CUDA(cp(a->W, p, P * 8));
+    FM_CUDA(cp(a->m, p + P * 8, P * 4));
+    FM_CUDA(cp(a->v, p + P * 12, P * 4));
+    if (a->dw_valid) FM_CUDA(cp(a->dW, p + P * 16, P * dw_elem(a)));
+    if (a->W16) {
+        FM_CUDA(launch_to_bf16(a->W, a->W16, P, c->num_sms, c->copy_in));  // shadow regenerated, not copied
+        count_launch();
+    }
+    FM_CUDA(cudaEventRecord(a->ev_in, c->copy_in));
+    FM_CUDA(cudaStreamWaitEvent(c->stream, a->ev_in, 0));
+    a->ctx = c;
+    a->active = true;
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int fm_agent_state_checksum(fm_agent* a, uint64_t* out) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
+    if (int st = set_dev(a->ctx)) return st;
+    FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
+    const size_t P = a->P;
+    std::vector<uint8_t> buf(P * (16 + dw_elem(a)));
+    FM_CUDA(cudaMemcpy(buf.data(), a->W, P * 8, cudaMemcpyDeviceToHost));
+    FM_CUDA(cudaMemcpy(buf.data() + P * 8, a->m, P * 4, cudaMemcpyDeviceToHost));
+    FM_CUDA(cudaMemcpy(buf.data() + P * 12, a->v, P * 4, cudaMemcpyDeviceToHost));
+    if (a->dw_valid) FM_CUDA(cudaMemcpy(buf.data() + P * 16, a->dW, P * dw_elem(a), cudaMemcpyDeviceToHost));
+    else std::fill(buf.begin() + P * 16, buf.end(), 0);
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (uint8_t b : buf) {
+        h ^= b;
+        h *= 0x100000001b3ULL;
+    }
+    for (int64_t x : {a->step, a->version, a->samples}) {
+        h ^= static_cast<uint64_t>(x);
+        h *= 0x100000001b3ULL;
+    }
+    *out = h;
+    return FM_OK;
+    FM_GUARD_END
+}
+
+// ---------------------------------------------------------------------------
+// GRPO advantages on device
+// ---------------------------------------------------------------------------
+int fm_group_advantages(fm_ctx* c, const double* rewards, const int32_t* seg_off, int nseg, double eps, double* out) {
+    FM_GUARD_BEGIN
+    if (nseg <= 0) return FM_OK;
+    if (int st = set_dev(c)) return st;
+    const int n = seg_off[nseg];
+    if (n <= 0) return FM_OK;
+    double *dr = nullptr, *dout = nullptr;
+    int32_t* doff = nullptr;
+    cudaStream_t s = c->stream;
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dr), n * 8, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dout), n * 8, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&doff), (nseg + 1) * 4, s));
+    FM_CUDA(cudaMemcpyAsync(dr, rewards, n * 8, cudaMemcpyHostToDevice, s));
+    FM_CUDA(cudaMemcpyAsync(doff, seg_off, (nseg + 1) * 4, cudaMemcpyHostToDevice, s));
+    FM_CUDA(cudaMemsetAsync(dout, 0, n * 8, s));
+    FM_CUDA(launch_group_advantages(dr, doff, nseg, eps, dout, s));
+    count_launch();
+    FM_CUDA(cudaMemcpyAsync(out, dout, n * 8, cudaMemcpyDeviceToHost, s));
+    FM_CUDA(cudaFreeAsync(dr, s));
+    FM_CUDA(cudaFreeAsync(dout, s));
+    FM_CUDA(cudaFreeAsync(doff, s));
+    FM_CUDA(cudaStreamSynchronize(s));
+    return FM_OK;
+    FM_GUARD_END
+}
+
+// ---------------------------------------------------------------------------
+// NCCL gang
+// ---------------------------------------------------------------------------
+struct fm_comm {
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    fm_ctx* ctx = nullptr;
+};
+
+#define FM_NCCL(expr)                                                                          \
+    do {                                                                                       \
+        ncclResult_t _r = (expr);                                                              \
+        if (_r != ncclSuccess) return fail(FM_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+    } while (0)
+
+int fm_comm_unique_id(uint8_t out[128]) {
+    ncclUniqueId id;
+    FM_NCCL(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(out, &id, 128);
+    return FM_OK;
+}
+
+int fm_comm_create(fm_ctx* c, const uint8_t id_bytes[128], int nranks, int rank, fm_comm** out) {
+    FM_GUARD_BEGIN
+    if (int st = set_dev(c)) return st;
+    ncclUniqueId id;
+    std::memcpy(&id, id_bytes, 128);
+    auto* cm = new fm_comm();
+    cm->nranks = nranks;
+    cm->rank = rank;
+    cm->ctx = c;
+    const ncclResult_t r = ncclCommInitRank(&cm->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        delete cm;
+        return fail(FM_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    *out = cm;
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int fm_comm_destroy(fm_comm* c) {
+    if (!c) return FM_OK;
+    if (c->comm) ncclCommDestroy(c->comm);
+    delete c;
+    return FM_OK;
+}
+
+int fm_agent_allreduce_grad(fm_agent* a, fm_comm* cm) {
+    if (int st = check_active(a)) return st;
+    if (cm->ctx != a->ctx) return fail(FM_ERR_CONFIG_ERROR, "communicator bound to another GPU");
+    fm_ctx* c = a->ctx;
+    if (int st = set_dev(c)) return st;
+    if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * dw_elem(a), c->stream));
+    a->dw_valid = true;
+    a->dp = cm->nranks > 1;
+    FM_NCCL(ncclAllReduce(a->dW, a->dW, a->P, a->precision == FM_PRECISION_PARITY_F64 ? ncclFloat64 : ncclFloat32,
+                          ncclSum, cm->comm, c->stream));
+    return FM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,297 @@
+// k_gemm_tc.cu — persistent, warp-specialised tcgen05 GEMM for the policy's
+// two dense products:
+//
+//   K-GEMM1  Z[t][v]  = (1/n_t) * sum_d Phic[t][d] * W16[v][d]      (policy.hpp:57-61)
+//            epilogue: fp32 Z store + per-(row, 256-col tile) softmax partials
+//            (max, sum exp) consumed by K-lse                        (policy.hpp:62-66)
+//   K-GEMM2  dW[v][d] (+)= sum_t G^T[v][t] * Phic^T[d][t]           (policy.hpp:83-90,
+//            training.hpp:394-395, 444-446); epilogue RMW of the fp32 gradient
+//            accumulator + sum(acc^2) of this micro-batch (training.hpp:417)
+//
+// Both are "TN" GEMMs  C[m][n] = sum_k A[m][k] * B[n][k]  with A and B bf16
+// K-major in HBM.  Tiles: 128 x 256 x 64, 4-stage TMA->smem ring
+// (SWIZZLE_128B), one elected thread issues tcgen05.mma (M128 N256 K16) into
+// a double-buffered TMEM accumulator (2 x 256 fp32 columns), 4 epilogue warps
+// drain TMEM with tcgen05.ld while the next tile's MMAs run.
+//
+// Warp roles (192 threads): w0 TMA producer, w1 MMA issuer (+TMEM owner),
+// w2..w5 epilogue (w%4 selects the TMEM lane quadrant it may access).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "fm_gemm.h"
+#include "fm_ptx.cuh"
+
+namespace fm {
+
+namespace {
+constexpr int BM = kGemmBM, BN = kGemmBN, BK = kGemmBK, STAGES = kGemmStages;
+constexpr uint32_t A_STAGE = BM * BK * 2;
+constexpr uint32_t B_STAGE = BN * BK * 2;
+constexpr uint32_t STAGE_BYTES = A_STAGE + B_STAGE;
+constexpr uint32_t kIdesc = idesc_bf16_f32<BM, BN>();
+constexpr uint32_t kTmemCols = 2 * BN;  // two accumulator buffers
+constexpr int kThreads = 192;
+
+struct TileCoord {
+    int mb, nb;
+};
+
+__device__ __forceinline__ TileCoord tile_coord(int t, int tiles_m, int tiles_n, int group_m) {
+    const int per_group = group_m * tiles_n;
+    const int g = t / per_group;
+    const int first_m = g * group_m;
+    const int gsz = min(tiles_m - first_m, group_m);
+    const int local = t - g * per_group;
+    return TileCoord{first_m + local % gsz, local / gsz};
+}
+
+__device__ __forceinline__ float fast_exp(float x) { return exp2f(x * 1.4426950408889634f); }
+
+// ---- epilogues ------------------------------------------------------------
+
+// One thread owns one accumulator row of the tile; it sees 32 consecutive
+// columns per call.  State carried across the 8 column chunks of a tile.
+struct LogitsEpi {
+    float row_scale;
+    float run_max, run_sum;
+    __device__ __forceinline__ void begin(const GemmArgs& a, int row) {
+        row_scale = row < a.M ? a.row_scale[row] : 0.f;
+        run_max = -INFINITY;
+        run_sum = 0.f;
+    }
+    __device__ __forceinline__ void chunk(const GemmArgs& a, int row, int col0, uint32_t (&r)[32]) {
+        float z[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) z[j] = __uint_as_float(r[j]) * row_scale;
+        if (row >= a.M) return;
+        const int nvalid = min(32, a.N - col0);
+        if (nvalid <= 0) return;
+        float* dst = a.out + static_cast<size_t>(row) * a.ld_out + col0;
+        if (nvalid == 32) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(dst + j) = make_float4(z[j], z[j + 1], z[j + 2], z[j + 3]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (j < nvalid) dst[j] = z[j];
+        }
+        float cmax = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < nvalid) cmax = fmaxf(cmax, z[j]);
+        const float nm = fmaxf(run_max, cmax);
+        float s = run_sum * fast_exp(run_max - nm);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < nvalid) s += fast_exp(z[j] - nm);
+        run_max = nm;
+        run_sum = s;
+    }
+    __device__ __forceinline__ void end(const GemmArgs& a, int row, int nb) {
+        if (row < a.M) a.stats[static_cast<size_t>(row) * a.stats_ld + nb] = make_float2(run_max, run_sum);
+    }
+};
+
+struct GradEpi {
+    double sumsq;
+    __device__ __forceinline__ void begin(const GemmArgs&, int) {}
+    __device__ __forceinline__ void chunk(const GemmArgs& a, int row, int col0, uint32_t (&r)[32]) {
+        if (row >= a.M) return;
+        const int nvalid = min(32, a.N - col0);
+        if (nvalid <= 0) return;
+        float* dst = a.out + static_cast<size_t>(row) * a.ld_out + col0;
+        float part = 0.f;
+        if (nvalid == 32) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+                float4 acc = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                         __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                part += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
+                if (a.accumulate) {
+                    const float4 o = *reinterpret_cast<const float4*>(dst + j);
+                    acc.x += o.x;
+                    acc.y += o.y;
+                    acc.z += o.z;
+                    acc.w += o.w;
+                }
+                *reinterpret_cast<float4*>(dst + j) = acc;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                if (j < nvalid) {
+                    const float acc = __uint_as_float(r[j]);
+                    part += acc * acc;
+                    dst[j] = a.accumulate ? dst[j] + acc : acc;
+                }
+            }
+        }
+        sumsq += static_cast<double>(part);
+    }
+    __device__ __forceinline__ void end(const GemmArgs&, int, int) {}
+};
+
+template <class Epi>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   GemmArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_STAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t warp = warp_id();
+    const uint32_t lane = lane_id();
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmA);
+        tma_prefetch(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);  // one arrive per epilogue warp
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int tiles_m = (args.M + BM - 1) / BM;
+    const int tiles_n = (args.N + BN - 1) / BN;
+    const int num_tiles = tiles_m * tiles_n;
+    const int k_iters = (args.K + BK - 1) / BK;
+
+    if (warp == 0) {
+        // ===== TMA producer =====
+        if (elect_one()) {
+            const uint64_t pol_a = policy_evict_last();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                const TileCoord tc = tile_coord(t, tiles_m, tiles_n, args.group_m);
+                for (int k = 0; k < k_iters; ++k) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+                    tma_load_2d_hint(sA + stage * A_STAGE, &tmA, &full[stage], k * BK, tc.mb * BM, pol_a);
+                    tma_load_2d_hint(sB + stage * B_STAGE, &tmB, &full[stage], k * BK, tc.nb * BN, pol_a);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer (single elected thread) =====
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+                for (int k = 0; k < k_iters; ++k) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint64_t adesc = umma_desc_k_sw128(smem_u32(sA + stage * A_STAGE));
+                    const uint64_t bdesc = umma_desc_k_sw128(smem_u32(sB + stage * B_STAGE));
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        // advance 16 bf16 = 32 B along K inside the 128 B swizzle atom
+                        umma_bf16(d_tmem, adesc + static_cast<uint64_t>(kk * 2),
+                                  bdesc + static_cast<uint64_t>(kk * 2), kIdesc, (k | kk) != 0);
+                    }
+                    umma_commit(&empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+        __syncwarp();
+    } else {
+        // ===== epilogue warps =====
+        const uint32_t quad = warp & 3;
+        const int row_in_tile = static_cast<int>(quad * 32 + lane);
+        Epi epi;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        double sumsq_total = 0.0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            const TileCoord tc = tile_coord(t, tiles_m, tiles_n, args.group_m);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int row = tc.mb * BM + row_in_tile;
+            epi.begin(args, row);
+            if constexpr (std::is_same_v<Epi, GradEpi>) epi.sumsq = 0.0;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem_base + ((quad * 32u) << 16) + static_cast<uint32_t>(acc * BN + c * 32), r);
+                tmem_ld_wait();
+                epi.chunk(args, row, tc.nb * BN + c * 32, r);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            epi.end(args, row, tc.nb);
+            if constexpr (std::is_same_v<Epi, GradEpi>) sumsq_total += epi.sumsq;
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+        if constexpr (std::is_same_v<Epi, GradEpi>) {
+            for (int o = 16; o > 0; o >>= 1) sumsq_total += __shfl_xor_sync(0xffffffffu, sumsq_total, o);
+            if (lane == 0 && args.sumsq) atomicAdd(args.sumsq, sumsq_total);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+}  // namespace
+
+size_t gemm_smem_bytes() { return STAGES * STAGE_BYTES + 1024 + 256; }
+
+cudaError_t gemm_tn_launch(GemmKind kind, const CUtensorMap& tmA, const CUtensorMap& tmB,
+                           const GemmArgs& args, int num_sms, cudaStream_t stream) {
+    const int tiles = ((args.M + BM - 1) / BM) * ((args.N + BN - 1) / BN);
+    if (tiles == 0) return cudaSuccess;
+    const int grid = tiles < num_sms ? tiles : num_sms;
+    const size_t smem = gemm_smem_bytes();
+    if (kind == GemmKind::Logits) {
+        auto k = gemm_tn_kernel<LogitsEpi>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        k<<<grid, kThreads, smem, stream>>>(tmA, tmB, args);
+    } else {
+        auto k = gemm_tn_kernel<GradEpi>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        k<<<grid, kThreads, smem, stream>>>(tmA, tmB, args);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace fm

@@ -1,0 +1,545 @@
+// k_path.cu — HBM-bound kernels of the micro-batch policy-update path.
+//
+//   K-gather        experience-store gather + featurizer      experience_store.hpp:92-114,
+//                                                               training.hpp:378-393, codec.hpp:24-30,
+//                                                               policy.hpp:42-51
+//   K-lse           cross-tile softmax normaliser, taken-token  policy.hpp:62-75
+//                   log-prob, surrogate coefficient
+//   K-softmax-grad  fused log-softmax gradient over the vocab   policy.hpp:83-90, training.hpp:394
+//                   (TMA-staged Z tiles in, TMA-stored G^T out)
+//   K-adam          fused Adam + bf16 shadow + grad reset        training.hpp:37-51
+//   K-adv           segmented GRPO normalisation                 training.hpp:54-67
+//   parity mode     exact-featurizer fp64 SIMT path              policy.hpp:42-91
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fm_kernels.h"
+#include "fm_ptx.cuh"
+
+namespace fm {
+
+namespace {
+
+__device__ __forceinline__ int token_of(uint64_t x) {  // static_cast<Token>(u64), codec.hpp:28
+    return static_cast<int>(static_cast<uint32_t>(x));
+}
+__device__ __forceinline__ uint64_t feature_of(int tok, uint64_t D) {  // policy.hpp:48
+    return static_cast<uint64_t>(static_cast<int64_t>(tok)) % D;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// Block-wide sum for 256-thread blocks; result valid in every thread.
+template <typename T>
+__device__ T block_sum(T x, T* red) {
+    x = warp_sum(x);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    T t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : T(0);
+    if (threadIdx.x < 32) t = warp_sum(t);
+    if (threadIdx.x == 0) red[0] = t;
+    __syncthreads();
+    return red[0];
+}
+
+__device__ double block_max(double x, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    double t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : -INFINITY;
+    if (threadIdx.x < 32) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
+    }
+    if (threadIdx.x == 0) red[0] = t;
+    __syncthreads();
+    return red[0];
+}
+
+// ---------------------------------------------------------------------------
+// K-gather
+// ---------------------------------------------------------------------------
+constexpr int kMaxSamplesSmem = 1024;
+
+__global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__ arena,
+                                                     const SampleDesc* __restrict__ sd, int n_samples,
+                                                     int64_t row_lo, int64_t M, int64_t Mpad, int64_t G,
+                                                     uint64_t D,
+                                                     RowBuffers rows, __nv_bfloat16* phic,
+                                                     __nv_bfloat16* phict) {
+    __shared__ int64_t s_start[kMaxSamplesSmem];
+    const int ns = n_samples < kMaxSamplesSmem ? n_samples : kMaxSamplesSmem;
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) s_start[i] = sd[i].row_start;
+    __syncthreads();
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= Mpad) return;
+    if (r >= M) {
+        rows.action[r] = -1;
+        rows.ctx4[r] = make_int4(-1, -1, -1, -1);
+        rows.n_ctx[r] = 0;
+        rows.sample[r] = -1;
+        rows.coef[r] = 0.f;
+        rows.rscale[r] = 0.f;
+        return;
+    }
+    // sample owning global row gr: last s with row_start[s] <= gr (rows are in poll order)
+    const int64_t gr = row_lo + r;
+    int lo = 0, hi = ns - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_start[mid] <= gr) lo = mid;
+        else hi = mid - 1;
+    }
+    const SampleDesc d = sd[lo];
+    const int64_t t = gr - d.row_start;
+    const uint64_t* P = reinterpret_cast<const uint64_t*>(arena + d.prompt_off + 8);
+    const uint64_t* R = reinterpret_cast<const uint64_t*>(arena + d.resp_off + 8);
+    const int action = token_of(__ldg(R + t));
+    const int64_t len = d.prompt_n + t;  // context = prompt ++ response[0:t]
+    const int n = len < 4 ? static_cast<int>(len) : 4;
+    int ctx[4] = {-1, -1, -1, -1};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (j < n) {
+            const int64_t pos = len - n + j;
+            ctx[j] = token_of(pos < d.prompt_n ? __ldg(P + pos) : __ldg(R + (pos - d.prompt_n)));
+        }
+    }
+    rows.action[r] = action;
+    rows.ctx4[r] = make_int4(ctx[0], ctx[1], ctx[2], ctx[3]);
+    rows.n_ctx[r] = n;
+    rows.sample[r] = lo;
+    rows.coef[r] = n ? static_cast<float>(-d.adv / (static_cast<double>(G) * static_cast<double>(n))) : 0.f;
+    rows.rscale[r] = n ? static_cast<float>(1.0 / static_cast<double>(n)) : 0.f;
+    if (phic) {
+        uint64_t f[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) f[j] = j < n ? feature_of(ctx[j], D) : ~0ull;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (j >= n) continue;
+            int cnt = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cnt += (f[k] == f[j]);
+            const __nv_bfloat16 c = __float2bfloat16_rn(static_cast<float>(cnt));  // exact: 1..4
+            phic[static_cast<size_t>(r) * D + f[j]] = c;
+            phict[static_cast<size_t>(f[j]) * Mpad + r] = c;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K-lse
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ Z, int64_t ldz,
+                                                  const float2* __restrict__ stats, int stats_ld,
+                                                  int64_t M, int64_t Mpad, int64_t V,
+                                                  const SampleDesc* __restrict__ sd, int64_t G,
+                                                  RowBuffers rows, const float* old_logp,
+                                                  float clip_eps, double* loss_acc) {
+    __shared__ double red[8];
+    const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    double loss = 0.0;
+    if (r < Mpad) {
+        if (r >= M) {
+            if (lane == 0) {
+                rows.lse[r] = 0.f;
+                rows.logp[r] = 0.f;
+                rows.coef_eff[r] = 0.f;
+            }
+        } else {
+            float m = -INFINITY, s = 0.f;
+            const float2* st = stats + static_cast<size_t>(r) * stats_ld;
+            for (int j = lane; j < stats_ld; j += 32) {
+                const float2 p = st[j];
+                const float nm = fmaxf(m, p.x);
+                s = s * __expf(m - nm) + p.y * __expf(p.x - nm);
+                m = nm;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float om = __shfl_xor_sync(0xffffffffu, m, o);
+                const float os = __shfl_xor_sync(0xffffffffu, s, o);
+                const float nm = fmaxf(m, om);
+                s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+                m = nm;
+            }
+            if (lane == 0) {
+                const float lse = m + logf(s);
+                const int a = rows.action[r];
+                const bool valid = a >= 0 && a < V;
+                const float lp = valid ? Z[static_cast<size_t>(r) * ldz + a] - lse : 0.f;
+                float ce = rows.coef[r];
+                const double adv = sd[rows.sample[r]].adv;
+                if (old_logp && clip_eps > 0.f) {
+                    // PPO clipped-ratio surrogate min(rho*A, clip(rho,1-e,1+e)*A): the
+                    // gradient flows (scaled by rho) only through the unclipped branch.
+                    const float rho = __expf(lp - old_logp[r]);
+                    const bool active = adv >= 0.0 ? rho <= 1.f + clip_eps : rho >= 1.f - clip_eps;
+                    ce = active ? ce * rho : 0.f;
+                }
+                rows.lse[r] = lse;
+                rows.logp[r] = lp;
+                rows.coef_eff[r] = ce;
+                loss = valid ? -(adv / static_cast<double>(G)) * static_cast<double>(lp) : 0.0;
+            }
+        }
+    }
+    if (loss_acc) {
+        const double tot = block_sum(loss, red);
+        if (threadIdx.x == 0 && tot != 0.0) atomicAdd(loss_acc, tot);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K-softmax-grad: 64 rows x 128 vocab per CTA.
+// ---------------------------------------------------------------------------
+constexpr int kSgRows = 64, kSgCols = 128;
+constexpr uint32_t kSgZBytes = kSgRows * kSgCols * 4;  // 32 KB fp32 tile
+constexpr uint32_t kSgGBytes = kSgRows * kSgCols * 2;  // 16 KB bf16 tile (swizzled 128 B rows)
+
+__global__ void __launch_bounds__(256) softmax_grad_kernel(const __grid_constant__ CUtensorMap tmZ,
+                                                           const __grid_constant__ CUtensorMap tmGt,
+                                                           RowBuffers rows) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    float* Zs = reinterpret_cast<float*>(smem);
+    uint8_t* Gs = smem + kSgZBytes;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kSgZBytes + kSgGBytes);
+    float* s_lse = reinterpret_cast<float*>(bar + 2);
+    float* s_coef = s_lse + kSgRows;
+    int* s_act = reinterpret_cast<int*>(s_coef + kSgRows);
+
+    const int v0 = blockIdx.x * kSgCols;
+    const int r0 = blockIdx.y * kSgRows;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        tma_prefetch(&tmZ);
+        mbar_init(bar, 1);
+        fence_barrier_init();
+        mbar_arrive_expect_tx(bar, kSgZBytes);
+        tma_load_2d_hint(Zs, &tmZ, bar, v0, r0, policy_evict_first());
+    }
+    if (tid < kSgRows) {
+        s_lse[tid] = rows.lse[r0 + tid];
+        s_coef[tid] = rows.coef_eff[r0 + tid];
+        s_act[tid] = rows.action[r0 + tid];
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+
+    const int vl = tid & (kSgCols - 1);
+    const int rg = tid >> 7;  // 0/1: rows [32*rg, 32*rg+32)
+    const int v = v0 + vl;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int chunk = rg * 4 + c;  // 8 consecutive rows = one 16 B chunk of the G^T row
+        uint32_t packed[4];
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+            const int ra = chunk * 8 + i, rb = ra + 1;
+            const float ca = s_coef[ra], cb = s_coef[rb];
+            const float ga = ca == 0.f ? 0.f
+                                       : ca * ((v == s_act[ra] ? 1.f : 0.f) -
+                                               __expf(Zs[ra * kSgCols + vl] - s_lse[ra]));
+            const float gb = cb == 0.f ? 0.f
+                                       : cb * ((v == s_act[rb] ? 1.f : 0.f) -
+                                               __expf(Zs[rb * kSgCols + vl] - s_lse[rb]));
+            const __nv_bfloat162 h = __floats2bfloat162_rn(ga, gb);  // .x = low = row ra
+            packed[i >> 1] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        // SWIZZLE_128B: 16 B chunk j of 128 B row i lives at chunk j ^ (i % 8)
+        *reinterpret_cast<uint4*>(Gs + vl * 128 + ((chunk ^ (vl & 7)) << 4)) =
+            make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+        tma_store_2d(&tmGt, Gs, r0, v0);
+        tma_store_commit();
+        tma_store_wait<0>();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K-adam
+// ---------------------------------------------------------------------------
+template <typename G>
+__device__ __forceinline__ double adam_one(double& w, float& m, float& v, G g, double lr, double b1,
+                                           double b2, double eps, double bc1, double bc2) {
+    const double gi = static_cast<double>(g);
+    const double mm = b1 * static_cast<double>(m) + (1.0 - b1) * gi;
+    const double vv = b2 * static_cast<double>(v) + (1.0 - b2) * gi * gi;
+    const double mhat = mm / bc1;
+    const double vhat = vv / bc2;
+    w -= lr * mhat / (sqrt(vhat) + eps);
+    m = static_cast<float>(mm);
+    v = static_cast<float>(vv);
+    return gi * gi;
+}
+
+template <typename G>
+__global__ void __launch_bounds__(256) adam_kernel(double* __restrict__ w, float* __restrict__ m,
+                                                   float* __restrict__ v, G* __restrict__ g,
+                                                   __nv_bfloat16* __restrict__ w16, uint64_t n,
+                                                   double lr, double b1, double b2, double eps,
+                                                   double bc1, double bc2, int zero_grad, double* gsq) {
+    __shared__ double red[8];
+    double acc = 0.0;
+    const uint64_t n4 = n / 4;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        double4 wv = reinterpret_cast<double4*>(w)[i];
+        float4 mv = reinterpret_cast<float4*>(m)[i];
+        float4 vv = reinterpret_cast<float4*>(v)[i];
+        G gv[4];
+        if constexpr (sizeof(G) == 4) {
+            const float4 t = reinterpret_cast<float4*>(g)[i];
+            gv[0] = t.x; gv[1] = t.y; gv[2] = t.z; gv[3] = t.w;
+        } else {
+            const double4 t = reinterpret_cast<double4*>(g)[i];
+            gv[0] = t.x; gv[1] = t.y; gv[2] = t.z; gv[3] = t.w;
+        }
+        acc += adam_one(wv.x, mv.x, vv.x, gv[0], lr, b1, b2, eps, bc1, bc2);
+        acc += adam_one(wv.y, mv.y, vv.y, gv[1], lr, b1, b2, eps, bc1, bc2);
+        acc += adam_one(wv.z, mv.z, vv.z, gv[2], lr, b1, b2, eps, bc1, bc2);
+        acc += adam_one(wv.w, mv.w, vv.w, gv[3], lr, b1, b2, eps, bc1, bc2);
+        reinterpret_cast<double4*>(w)[i] = wv;
+        reinterpret_cast<float4*>(m)[i] = mv;
+        reinterpret_cast<float4*>(v)[i] = vv;
+        if (w16) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(static_cast<float>(wv.x), static_cast<float>(wv.y));
+            __nv_bfloat162 hi = __floats2bfloat162_rn(static_cast<float>(wv.z), static_cast<float>(wv.w));
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&lo);
+            pk.y = *reinterpret_cast<uint32_t*>(&hi);
+            reinterpret_cast<uint2*>(w16)[i] = pk;
+        }
+        if (zero_grad) {
+            if constexpr (sizeof(G) == 4) reinterpret_cast<float4*>(g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            else reinterpret_cast<double4*>(g)[i] = make_double4(0.0, 0.0, 0.0, 0.0);
+        }
+    }
+    // scalar tail
+    const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gid < n - n4 * 4) {
+        const uint64_t i = n4 * 4 + gid;
+        acc += adam_one(w[i], m[i], v[i], g[i], lr, b1, b2, eps, bc1, bc2);
+        if (w16) w16[i] = __float2bfloat16_rn(static_cast<float>(w[i]));
+        if (zero_grad) g[i] = G(0);
+    }
+    if (gsq) {
+        const double tot = block_sum(acc, red);
+        if (threadIdx.x == 0) atomicAdd(gsq, tot);
+    }
+}
+
+__global__ void to_bf16_kernel(const double* __restrict__ w, __nv_bfloat16* __restrict__ w16, uint64_t n) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        w16[i] = __float2bfloat16_rn(static_cast<float>(w[i]));
+}
+
+// ---------------------------------------------------------------------------
+// K-adv: one warp per reward group.
+// ---------------------------------------------------------------------------
+__global__ void group_adv_kernel(const double* __restrict__ r, const int32_t* __restrict__ off, int nseg,
+                                 double eps, double* __restrict__ out) {
+    const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (seg >= nseg) return;
+    const int b = off[seg], e = off[seg + 1];
+    const int n = e - b;
+    if (n <= 0) return;
+    double s = 0.0;
+    for (int i = b + lane; i < e; i += 32) s += r[i];
+    const double mean = warp_sum(s) / static_cast<double>(n);
+    double q = 0.0;
+    for (int i = b + lane; i < e; i += 32) q += (r[i] - mean) * (r[i] - mean);
+    const double sd = sqrt(warp_sum(q) / static_cast<double>(n));
+    for (int i = b + lane; i < e; i += 32) out[i] = (r[i] - mean) / (sd + eps);
+}
+
+// ---------------------------------------------------------------------------
+// Parity mode: one 256-thread block per packed row, fp64 throughout.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) parity_rows_kernel(const double* __restrict__ W, uint64_t V, uint64_t D,
+                                                          RowBuffers rows, const SampleDesc* __restrict__ sd,
+                                                          int64_t G, double* __restrict__ zs,
+                                                          double* __restrict__ dWmb, double* logp64,
+                                                          double* loss_acc) {
+    __shared__ double red[8];
+    __shared__ uint64_t s_f[4];
+    __shared__ double s_phi[4];
+    __shared__ int s_nf;
+    const int64_t r = blockIdx.x;
+    const int n = rows.n_ctx[r];
+    const int a = rows.action[r];
+    if (threadIdx.x == 0) {
+        const int4 c4 = rows.ctx4[r];
+        const int ctx[4] = {c4.x, c4.y, c4.z, c4.w};
+        const double w = n ? 1.0 / static_cast<double>(n) : 0.0;
+        int nf = 0;
+        for (int j = 0; j < n; ++j) {  // phi[tok % D] += 1/n   (policy.hpp:46-49)
+            const uint64_t f = feature_of(ctx[j], D);
+            int k = 0;
+            while (k < nf && s_f[k] != f) ++k;
+            if (k == nf) {
+                s_f[nf] = f;
+                s_phi[nf] = 0.0;
+                ++nf;
+            }
+            s_phi[k] = __dadd_rn(s_phi[k], w);
+        }
+        for (int i = 1; i < nf; ++i)  // ascending feature order = the reference's d loop order
+            for (int k = i; k > 0 && s_f[k - 1] > s_f[k]; --k) {
+                const uint64_t tf = s_f[k]; s_f[k] = s_f[k - 1]; s_f[k - 1] = tf;
+                const double tp = s_phi[k]; s_phi[k] = s_phi[k - 1]; s_phi[k - 1] = tp;
+            }
+        s_nf = nf;
+    }
+    __syncthreads();
+    const int nf = s_nf;
+    double* z = zs + static_cast<size_t>(r) * V;
+    double lmax = -INFINITY;
+    for (uint64_t v = threadIdx.x; v < V; v += blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < nf; ++k) s = __dadd_rn(s, __dmul_rn(W[v * D + s_f[k]], s_phi[k]));
+        z[v] = s;
+        lmax = fmax(lmax, s);
+    }
+    const double zmax = block_max(lmax, red);
+    double lsum = 0.0;
+    for (uint64_t v = threadIdx.x; v < V; v += blockDim.x) {
+        const double e = exp(z[v] - zmax);
+        z[v] = e;
+        lsum += e;
+    }
+    const double denom = block_sum(lsum, red);
+    const double adv = sd[rows.sample[r]].adv;
+    const double scale = -adv / static_cast<double>(G);  // term.scale(A) then grad.scale(-1/G)
+    for (uint64_t v = threadIdx.x; v < V; v += blockDim.x) {
+        const double p = z[v] / denom;
+        const double coef = ((static_cast<int64_t>(v) == a) ? 1.0 : 0.0) - p;
+        if (coef == 0.0) continue;  // policy.hpp:86
+        for (int k = 0; k < nf; ++k) atomicAdd(&dWmb[v * D + s_f[k]], scale * (coef * s_phi[k]));
+    }
+    if (threadIdx.x == 0) {  // z[] holds exp(z - zmax); block_sum's barrier made it visible
+        const bool valid = a >= 0 && static_cast<uint64_t>(a) < V;
+        const double lp = valid ? log(z[a] / denom) : 0.0;  // policy.hpp:72-75
+        if (logp64) logp64[r] = lp;
+        if (loss_acc && valid) atomicAdd(loss_acc, -(adv / static_cast<double>(G)) * lp);
+    }
+}
+
+__global__ void parity_fold_kernel(double* __restrict__ dW, double* __restrict__ dWmb, uint64_t n, double* sumsq) {
+    __shared__ double red[8];
+    double acc = 0.0;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double x = dWmb[i];
+        acc += x * x;
+        dW[i] += x;
+        dWmb[i] = 0.0;
+    }
+    const double tot = block_sum(acc, red);
+    if (threadIdx.x == 0 && sumsq) atomicAdd(sumsq, tot);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launch wrappers
+// ---------------------------------------------------------------------------
+cudaError_t launch_gather(const uint8_t* arena, const SampleDesc* sd, int n_samples, int64_t row_lo, int64_t M,
+                          int64_t Mpad, int64_t global_batch, uint64_t D, RowBuffers rows, __nv_bfloat16* phic,
+                          __nv_bfloat16* phict, cudaStream_t s) {
+    if (Mpad == 0) return cudaSuccess;
+    if (n_samples > kMaxSamplesSmem) return cudaErrorInvalidValue;
+    const int blocks = static_cast<int>((Mpad + 255) / 256);
+    gather_kernel<<<blocks, 256, 0, s>>>(arena, sd, n_samples, row_lo, M, Mpad, global_batch, D, rows, phic, phict);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lse(const float* Z, int64_t ldz, const float2* stats, int stats_ld, int64_t M, int64_t Mpad,
+                       int64_t V, const SampleDesc* sd, int64_t global_batch, RowBuffers rows,
+                       const float* old_logp, float clip_eps, double* loss_acc, cudaStream_t s) {
+    if (Mpad == 0) return cudaSuccess;
+    const int blocks = static_cast<int>((Mpad * 32 + 255) / 256);
+    lse_kernel<<<blocks, 256, 0, s>>>(Z, ldz, stats, stats_ld, M, Mpad, V, sd, global_batch, rows, old_logp,
+                                      clip_eps, loss_acc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_softmax_grad(const CUtensorMap& tmZ, const CUtensorMap& tmGt, int64_t Mpad, int64_t V,
+                                RowBuffers rows, cudaStream_t s) {
+    if (Mpad == 0) return cudaSuccess;
+    const size_t smem = 1024 + kSgZBytes + kSgGBytes + 16 + kSgRows * 12;
+    cudaFuncSetAttribute(softmax_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    dim3 grid(static_cast<unsigned>((V + kSgCols - 1) / kSgCols), static_cast<unsigned>(Mpad / kSgRows));
+    softmax_grad_kernel<<<grid, 256, smem, s>>>(tmZ, tmGt, rows);
+    return cudaGetLastError();
+}
+
+template <typename G>
+cudaError_t launch_adam(double* w, float* m, float* v, G* g, __nv_bfloat16* w16, uint64_t n, double lr, double b1,
+                        double b2, double eps, double bc1, double bc2, int zero_grad, double* gsq, int num_sms,
+                        cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g)) & 31) return cudaErrorMisalignedAddress;
+    const uint64_t want = (n / 4 + 255) / 256;
+    const uint64_t cap = static_cast<uint64_t>(num_sms) * 8;
+    const int blocks = static_cast<int>(want < 1 ? 1 : (want > cap ? cap : want));
+    adam_kernel<G><<<blocks, 256, 0, s>>>(w, m, v, g, w16, n, lr, b1, b2, eps, bc1, bc2, zero_grad, gsq);
+    return cudaGetLastError();
+}
+template cudaError_t launch_adam<float>(double*, float*, float*, float*, __nv_bfloat16*, uint64_t, double, double,
+                                        double, double, double, double, int, double*, int, cudaStream_t);
+template cudaError_t launch_adam<double>(double*, float*, float*, double*, __nv_bfloat16*, uint64_t, double,
+                                         double, double, double, double, double, int, double*, int, cudaStream_t);
+
+cudaError_t launch_to_bf16(const double* w, __nv_bfloat16* w16, uint64_t n, int num_sms, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    to_bf16_kernel<<<num_sms * 8, 256, 0, s>>>(w, w16, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_group_advantages(const double* rewards, const int32_t* seg_off, int nseg, double eps,
+                                    double* out, cudaStream_t s) {
+    if (nseg == 0) return cudaSuccess;
+    const int blocks = (nseg * 32 + 255) / 256;
+    group_adv_kernel<<<blocks, 256, 0, s>>>(rewards, seg_off, nseg, eps, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_parity_rows(const double* W, uint64_t V, uint64_t D, int64_t M, RowBuffers rows,
+                               const SampleDesc* sd, int64_t global_batch, double* zscratch, double* dWmb,
+                               double* logp64, double* loss_acc, cudaStream_t s) {
+    if (M == 0) return cudaSuccess;
+    parity_rows_kernel<<<static_cast<unsigned>(M), 256, 0, s>>>(W, V, D, rows, sd, global_batch, zscratch, dWmb,
+                                                                logp64, loss_acc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_parity_fold(double* dW, double* dWmb, uint64_t n, double* sumsq, int num_sms, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t want = (n + 255) / 256;
+    const uint64_t cap = static_cast<uint64_t>(num_sms) * 8;
+    parity_fold_kernel<<<static_cast<unsigned>(want > cap ? cap : want), 256, 0, s>>>(dW, dWmb, n, sumsq);
+    return cudaGetLastError();
+}
+
+}  // namespace fm
