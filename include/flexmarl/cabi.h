@@ -102,6 +102,13 @@ int fm_ctx_destroy(fm_ctx* ctx);
 int fm_ctx_device(const fm_ctx* ctx);
 int fm_ctx_num_sms(const fm_ctx* ctx);
 int fm_ctx_synchronize(fm_ctx* ctx);
+/* Device step timer on the compute stream (copy streams joined at stop). */
+int fm_ctx_timer_start(fm_ctx* ctx);
+int fm_ctx_timer_stop(fm_ctx* ctx, double* ms);
+/* Per-kernel CUDA-event timing of the hot path (off by default).  Kinds:
+ * 0 gather, 1 gemm1, 2 lse, 3 softmax_grad, 4 gemm2, 5 adam, 6 parity, 7 memset. */
+int fm_ctx_set_kernel_timing(fm_ctx* ctx, int on);
+int fm_ctx_kernel_times(fm_ctx* ctx, double* ms_out, int64_t* count_out, int reset);
 /* Pre-size the token arena and the per-micro-batch workspace. */
 int fm_ctx_reserve(fm_ctx* ctx, uint64_t arena_bytes, int64_t max_rows, uint64_t max_vocab,
                    uint64_t max_feat);

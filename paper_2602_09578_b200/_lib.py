@@ -60,6 +60,10 @@ _PROTOS = {
     "fm_ctx_num_sms": (I, [P]),
     "fm_ctx_synchronize": (I, [P]),
     "fm_ctx_reserve": (I, [P, U64, I64, U64, U64]),
+    "fm_ctx_timer_start": (I, [P]),
+    "fm_ctx_timer_stop": (I, [P, PD]),
+    "fm_ctx_set_kernel_timing": (I, [P, I]),
+    "fm_ctx_kernel_times": (I, [P, P, P, I]),
     "fm_arena_put": (I, [P, P, U64, PU64]),
     "fm_arena_reset": (I, [P]),
     "fm_arena_used": (U64, [P]),

@@ -116,8 +116,43 @@ struct Workspace {
     int sd_cap = 0;
 };
 
+// Per-kernel device timing (bench.py's roofline): event pairs recorded on the
+// launching stream around each hot-path kernel when enabled.
+enum KKind { K_GATHER = 0, K_GEMM1, K_LSE, K_SOFTMAX_GRAD, K_GEMM2, K_ADAM, K_PARITY, K_MEMSET, K_NKINDS };
+struct KTimer {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> open;
+    double ms[K_NKINDS] = {};
+    int64_t count[K_NKINDS] = {};
+    cudaEvent_t get() {
+        if (pool.empty()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            return e;
+        }
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+};
+
+// One training slot: the device home of an active agent's {W, m, v, dW, W16}.
+// Slots are allocated once and recycled across activate/suspend (the
+// reference's training_slots, config.hpp:89); reuse is ordered on the GPU by
+// the event recorded after the previous tenant's copy-out.
+struct Slot {
+    void* base = nullptr;
+    size_t cap = 0;
+    bool busy = false;
+    cudaEvent_t ev_free = nullptr;
+};
+
 struct fm_ctx {
     int device = 0;
+    KTimer kt;
+    std::vector<Slot*> slots;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
     int num_sms = 148;
     cudaStream_t stream = nullptr;    // compute
     cudaStream_t copy_in = nullptr;   // swap-in (H2D / D2D / P2P)
@@ -327,9 +362,90 @@ RowBuffers row_buffers(Workspace& w) {
     return r;
 }
 
+// RAII event pair around one launch (no-op unless kernel timing is on).
+struct KScope {
+    fm_ctx* c;
+    int kind;
+    cudaStream_t s;
+    cudaEvent_t e0 = nullptr;
+    KScope(fm_ctx* c_, int k, cudaStream_t s_) : c(c_), kind(k), s(s_) {
+        if (c->kt.on) {
+            e0 = c->kt.get();
+            cudaEventRecord(e0, s);
+        }
+    }
+    ~KScope() {
+        if (e0) {
+            cudaEvent_t e1 = c->kt.get();
+            cudaEventRecord(e1, s);
+            c->kt.open.push_back({kind, {e0, e1}});
+        }
+    }
+};
+
 }  // namespace
 
 extern "C" {
+
+int fm_ctx_set_kernel_timing(fm_ctx* c, int on) {
+    c->kt.on = on != 0;
+    return FM_OK;
+}
+
+// Drains the recorded event pairs; out_ms / out_count have K_NKINDS (8) slots:
+// gather, gemm1, lse, softmax_grad, gemm2, adam, parity, memset.
+int fm_ctx_kernel_times(fm_ctx* c, double* out_ms, int64_t* out_count, int reset) {
+    if (int st = set_dev(c)) return st;
+    KTimer& k = c->kt;
+    for (auto& o : k.open) {
+        FM_CUDA(cudaEventSynchronize(o.second.second));
+        float ms = 0.f;
+        FM_CUDA(cudaEventElapsedTime(&ms, o.second.first, o.second.second));
+        k.ms[o.first] += ms;
+        k.count[o.first] += 1;
+        k.pool.push_back(o.second.first);
+        k.pool.push_back(o.second.second);
+    }
+    k.open.clear();
+    for (int i = 0; i < K_NKINDS; ++i) {
+        if (out_ms) out_ms[i] = k.ms[i];
+        if (out_count) out_count[i] = k.count[i];
+        if (reset) {
+            k.ms[i] = 0.0;
+            k.count[i] = 0;
+        }
+    }
+    return FM_OK;
+}
+
+// Device-side step timer on the compute stream (the copy streams are joined
+// first, so swaps in flight are inside the measured interval).
+int fm_ctx_timer_start(fm_ctx* c) {
+    if (int st = set_dev(c)) return st;
+    if (!c->t0) {
+        FM_CUDA(cudaEventCreate(&c->t0));
+        FM_CUDA(cudaEventCreate(&c->t1));
+    }
+    FM_CUDA(cudaEventRecord(c->t0, c->stream));
+    return FM_OK;
+}
+
+int fm_ctx_timer_stop(fm_ctx* c, double* ms) {
+    if (int st = set_dev(c)) return st;
+    cudaEvent_t j;
+    FM_CUDA(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
+    for (cudaStream_t cs : {c->copy_in, c->copy_out}) {
+        FM_CUDA(cudaEventRecord(j, cs));
+        FM_CUDA(cudaStreamWaitEvent(c->stream, j, 0));
+    }
+    FM_CUDA(cudaEventRecord(c->t1, c->stream));
+    FM_CUDA(cudaEventSynchronize(c->t1));
+    cudaEventDestroy(j);
+    float f = 0.f;
+    FM_CUDA(cudaEventElapsedTime(&f, c->t0, c->t1));
+    *ms = f;
+    return FM_OK;
+}
 
 int fm_ctx_create(int device, fm_ctx** out) {
     FM_GUARD_BEGIN
@@ -374,6 +490,11 @@ int fm_ctx_destroy(fm_ctx* c) {
     cudaDeviceSynchronize();
     ws_free(c->ws);
     cudaFree(c->arena);
+    for (Slot* sl : c->slots) {
+        cudaFree(sl->base);
+        cudaEventDestroy(sl->ev_free);
+        delete sl;
+    }
     for (int i = 0; i < kStagingSlots; ++i) {
         if (c->staging[i]) cudaFreeHost(c->staging[i]);
         cudaEventDestroy(c->staging_ev[i]);
@@ -490,31 +611,64 @@ struct fm_agent {
     void* park = nullptr;  // W | m | v | dW   (host pinned or device)
     size_t park_bytes = 0;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_compute = nullptr;
+    Slot* slot = nullptr;
 };
 
 namespace {
 
 size_t dw_elem(const fm_agent* a) { return a->precision == FM_PRECISION_PARITY_F64 ? 8 : 4; }
 
-int agent_alloc_device(fm_agent* a, cudaStream_t s) {
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+size_t slot_bytes(const fm_agent* a) {
     const size_t P = a->P;
-    cudaError_t e = cudaSuccess;
-    e = e ? e : cudaMallocAsync(reinterpret_cast<void**>(&a->W), P * 8, s);
-    e = e ? e : cudaMallocAsync(reinterpret_cast<void**>(&a->m), P * 4, s);
-    e = e ? e : cudaMallocAsync(reinterpret_cast<void**>(&a->v), P * 4, s);
-    e = e ? e : cudaMallocAsync(&a->dW, P * dw_elem(a), s);
-    if (a->precision == FM_PRECISION_BF16_TC)
-        e = e ? e : cudaMallocAsync(reinterpret_cast<void**>(&a->W16), P * 2, s);
-    if (e != cudaSuccess) return fail(FM_ERR_DEVICE_OOM, std::string("agent state: ") + cudaGetErrorString(e));
+    return align256(P * 8) + 2 * align256(P * 4) + align256(P * dw_elem(a)) +
+           (a->precision == FM_PRECISION_BF16_TC ? align256(P * 2) : 0);
+}
+
+// Binds a free slot of ctx c (allocating one the first time), ordered on
+// stream s after the slot's previous tenant has been copied out.
+int agent_alloc_device(fm_agent* a, fm_ctx* c, cudaStream_t s) {
+    const size_t need = slot_bytes(a);
+    Slot* pick = nullptr;
+    for (Slot* sl : c->slots)
+        if (!sl->busy && sl->cap >= need && (!pick || sl->cap < pick->cap)) pick = sl;
+    if (!pick) {
+        pick = new Slot();
+        if (cudaMalloc(&pick->base, need) != cudaSuccess) {
+            cudaGetLastError();
+            delete pick;
+            return fail(FM_ERR_DEVICE_OOM, "no HBM for another training slot (" + std::to_string(need) + " B)");
+        }
+        pick->cap = need;
+        FM_CUDA(cudaEventCreateWithFlags(&pick->ev_free, cudaEventDisableTiming));
+        FM_CUDA(cudaEventRecord(pick->ev_free, s));
+        c->slots.push_back(pick);
+    }
+    FM_CUDA(cudaStreamWaitEvent(s, pick->ev_free, 0));
+    pick->busy = true;
+    a->slot = pick;
+    uint8_t* p = static_cast<uint8_t*>(pick->base);
+    const size_t P = a->P;
+    a->W = reinterpret_cast<double*>(p);
+    p += align256(P * 8);
+    a->m = reinterpret_cast<float*>(p);
+    p += align256(P * 4);
+    a->v = reinterpret_cast<float*>(p);
+    p += align256(P * 4);
+    a->dW = p;
+    p += align256(P * dw_elem(a));
+    a->W16 = a->precision == FM_PRECISION_BF16_TC ? reinterpret_cast<__nv_bfloat16*>(p) : nullptr;
     return FM_OK;
 }
 
+// Releases the agent's slot once everything queued on stream s has run.
 void agent_free_device(fm_agent* a, cudaStream_t s) {
-    if (a->W) cudaFreeAsync(a->W, s);
-    if (a->m) cudaFreeAsync(a->m, s);
-    if (a->v) cudaFreeAsync(a->v, s);
-    if (a->dW) cudaFreeAsync(a->dW, s);
-    if (a->W16) cudaFreeAsync(a->W16, s);
+    if (a->slot) {
+        cudaEventRecord(a->slot->ev_free, s);
+        a->slot->busy = false;
+        a->slot = nullptr;
+    }
     a->W = nullptr;
     a->m = a->v = nullptr;
     a->dW = nullptr;
@@ -547,7 +701,7 @@ int fm_agent_create(fm_ctx* c, const char* name, uint64_t V, uint64_t D, int pre
     a->D = D;
     a->P = V * D;
     a->precision = precision;
-    if (int st = agent_alloc_device(a, c->stream)) {
+    if (int st = agent_alloc_device(a, c, c->stream)) {
         delete a;
         return st;
     }
@@ -715,9 +869,15 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
     if (M > 0) {
         if (tc) {
             const uint64_t ldz = round_up(a->V, 4);
-            FM_CUDA(cudaMemsetAsync(w.phic, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
-            FM_CUDA(cudaMemsetAsync(w.phict, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
-            FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, Mpad, G, a->D, rows, w.phic, w.phict, s));
+            {
+                KScope k(c, K_MEMSET, s);
+                FM_CUDA(cudaMemsetAsync(w.phic, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
+                FM_CUDA(cudaMemsetAsync(w.phict, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
+            }
+            {
+                KScope k(c, K_GATHER, s);
+                FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, Mpad, G, a->D, rows, w.phic, w.phict, s));
+            }
             // K-GEMM1: Z = Phic * W16^T, epilogue z *= 1/n, softmax partials
             CUtensorMap tA, tB, tZ, tGt, tPt;
             if (!make_tmap_bf16_kmajor(&tA, w.phic, Mpad, a->D, kGemmBM) ||
@@ -737,13 +897,22 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g1.row_scale = w.rscale;
             g1.stats = w.stats;
             g1.stats_ld = tiles_n;
-            FM_CUDA(gemm_tn_launch(GemmKind::Logits, tA, tB, g1, c->num_sms, s));
+            {
+                KScope k(c, K_GEMM1, s);
+                FM_CUDA(gemm_tn_launch(GemmKind::Logits, tA, tB, g1, c->num_sms, s));
+            }
             // K-lse
-            FM_CUDA(launch_lse(w.Z, static_cast<int64_t>(ldz), w.stats, tiles_n, M, Mpad,
-                               static_cast<int64_t>(a->V), w.sd, G, rows,
-                               a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1, s));
+            {
+                KScope k(c, K_LSE, s);
+                FM_CUDA(launch_lse(w.Z, static_cast<int64_t>(ldz), w.stats, tiles_n, M, Mpad,
+                                   static_cast<int64_t>(a->V), w.sd, G, rows,
+                                   a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1, s));
+            }
             // K-softmax-grad: G^T tiles (zero for padding rows)
-            FM_CUDA(launch_softmax_grad(tZ, tGt, Mpad, static_cast<int64_t>(a->V), rows, s));
+            {
+                KScope k(c, K_SOFTMAX_GRAD, s);
+                FM_CUDA(launch_softmax_grad(tZ, tGt, Mpad, static_cast<int64_t>(a->V), rows, s));
+            }
             // K-GEMM2: dW (+)= G^T * Phic ; first contribution of the step overwrites
             GemmArgs g2{};
             g2.M = static_cast<int>(a->V);
@@ -754,11 +923,15 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g2.ld_out = static_cast<long long>(a->D);
             g2.accumulate = a->dw_valid ? 1 : 0;
             g2.sumsq = scal;
-            FM_CUDA(gemm_tn_launch(GemmKind::Grad, tGt, tPt, g2, c->num_sms, s));
+            {
+                KScope k(c, K_GEMM2, s);
+                FM_CUDA(gemm_tn_launch(GemmKind::Grad, tGt, tPt, g2, c->num_sms, s));
+            }
             count_launch(5);
         } else {
             FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, M, G, a->D, rows, nullptr, nullptr, s));
             if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * 8, s));
+            KScope k(c, K_PARITY, s);
             FM_CUDA(launch_parity_rows(a->W, a->V, a->D, M, rows, w.sd, G, w.zscratch, w.dWmb, w.logp64,
                                        scal + 1, s));
             FM_CUDA(launch_parity_fold(static_cast<double*>(a->dW), w.dWmb, a->P, scal, c->num_sms, s));
@@ -921,6 +1094,7 @@ int fm_apply_update(fm_agent* a, int64_t G, double lr, double b1, double b2, dou
     const double bc1 = 1.0 - std::pow(b1, static_cast<double>(a->step));  // training.hpp:42-43
     const double bc2 = 1.0 - std::pow(b2, static_cast<double>(a->step));
     FM_CUDA(cudaMemsetAsync(a->d_upd, 0, sizeof(double), s));
+    KScope ks(c, K_ADAM, s);
     if (a->precision == FM_PRECISION_PARITY_F64) {
         FM_CUDA(launch_adam<double>(a->W, a->m, a->v, static_cast<double*>(a->dW), nullptr, a->P, lr, b1, b2, eps,
                                     bc1, bc2, 1, a->d_upd, c->num_sms, s));
@@ -1018,7 +1192,7 @@ int fm_agent_activate(fm_agent* a, fm_ctx* c) {
     const size_t P = a->P;
     // the parked copy must have landed before we read it back
     FM_CUDA(cudaStreamWaitEvent(c->copy_in, a->ev_out, 0));
-    if (int st = agent_alloc_device(a, c->copy_in)) return st;
+    if (int st = agent_alloc_device(a, c, c->copy_in)) return st;
     uint8_t* p = static_cast<uint8_t*>(a->park);
     const bool peer = a->park_tier != FM_TIER_HOST && a->park_device != c->device;
     if (peer) {
