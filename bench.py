@@ -164,7 +164,7 @@ def run_ours(args, dist: Dist) -> dict | None:
     if args.resp_len:
         cfg = wl.Config(cfg.name, cfg.agents, cfg.vocab, cfg.feat, cfg.group_k, cfg.micro_batch,
                         cfg.global_batch, args.resp_len, cfg.seed, cfg.lr)
-    agents = list(cfg.agents)
+    agents = list(cfg.agents)[: args.agents or None]
     place = placement(agents, dist.world)
     mine = [a for a in agents if dist.rank in place[a]]
     tier = {"device": _lib.TIER_DEVICE, "host": _lib.TIER_HOST}[args.tier]
@@ -431,7 +431,7 @@ def run_e2e(args, cfg, ctx, mine, handles, place, comms, dist, tier) -> dict:
     dist.barrier()
     max_ms = dist.max(ms.value)
     n = len(steps) - 1
-    tokens = len(cfg.agents) * G * cfg.resp_len * n
+    tokens = len(place) * G * cfg.resp_len * n
     return {"value": tokens / (max_ms / 1e3), "unit": "trained tokens/s",
             "h2d_bytes_per_step": int(dist.sum(h2d) / n), "d2h_bytes_per_step": int(dist.sum(d2h) / n),
             "steps": n, "ms_per_step": round(max_ms / n, 3)}
@@ -515,15 +515,16 @@ METRIC = "trained tokens/sec (policy-update micro-batches) at 1/2/4/8 B200 vs CP
 
 
 def config_obj(cfg, args) -> dict:
-    return {"workload": f"{cfg.name}: {len(cfg.agents)} agents, V={cfg.vocab}, D={cfg.feat} "
+    na = args.agents or len(cfg.agents)
+    return {"workload": f"{cfg.name}: {na} agents, V={cfg.vocab}, D={cfg.feat} "
                         f"({cfg.params / 1e6:.1f}M params/agent), GRPO k={cfg.group_k}, micro-batch "
                         f"{cfg.micro_batch}/global {cfg.global_batch}, response {cfg.resp_len} tokens, "
                         f"state swap tier={args.tier}",
-            "agents": len(cfg.agents), "vocab": cfg.vocab, "feat": cfg.feat, "micro_batch": cfg.micro_batch,
+            "agents": na, "vocab": cfg.vocab, "feat": cfg.feat, "micro_batch": cfg.micro_batch,
             "global_batch": cfg.global_batch, "resp_len": cfg.resp_len,
             "formulation": "dense 4*V*D flop/token (reference's own dense loops, policy.hpp:57-61, 87-89)",
             "l2": "inputs larger than L2 (W16 262 MB, Z 2.1 GB per micro-batch); no flush needed",
-            "parallelism": f"agent-centric placement, dp gangs of max(1, N/{len(cfg.agents)}) GPUs"}
+            "parallelism": f"agent-centric placement, dp gangs of max(1, N/{na}) GPUs"}
 
 
 def main():
@@ -539,6 +540,7 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=4, help="reference tokens per thread per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--host-breakdown", action="store_true")
+    ap.add_argument("--agents", type=int, default=0, help="use only the first K agents of the config")
     args = ap.parse_args()
     dist = Dist()
     try:
