@@ -440,20 +440,22 @@ def run_e2e(args, cfg, ctx, mine, handles, place, comms, dist, tier) -> dict:
 # ---------------------------------------------------------------------------
 # reference CPU path (oracle/_ref: the unmodified reference headers)
 # ---------------------------------------------------------------------------
-def reference_sample(cfg, tokens_per_thread: int, threads: int) -> dict:
+def reference_sample(cfg, tokens_per_thread: int, threads: int, update_s: float | None = None) -> dict:
     """Each thread drives the reference ExperienceStore + TrainingEngine at
     the workload's full V x D on one sample with a `tokens_per_thread`-token
-    response (global batch 1, so apply_global_update runs once and is timed).
-    Per-token cost is position-independent (phi sees 4 tokens), so tokens/s
-    extrapolate; the update cost is amortised over the real global step."""
+    response.  Per-token cost is position-independent (phi sees 4 tokens), so
+    tokens/s extrapolate.  The reference's apply_global_update is timed once
+    (update_s None -> measured here with global batch 1) and amortised over a
+    real global step (G x L tokens)."""
     from oracle import oracle as orc
     from paper_2602_09578_b200 import workload as wl
     s = wl.step_samples(cfg, cfg.agents[0], 0, n=1, resp_len=tokens_per_thread)[0]
     results = [None] * threads
 
     def work(i):
-        results[i] = orc.ref_run_agent(f"cpu{i}", cfg.vocab, cfg.feat, cfg.seed, 1, 1, 1, [s.input_id], [0], [0], [0],
-                                       [(s.prompt, s.response)], [0.5], want_state=False)
+        results[i] = orc.ref_run_agent(f"cpu{i}", cfg.vocab, cfg.feat, cfg.seed, 1, 1, 1, [s.input_id], [0], [0],
+                                       [0], [(s.prompt, s.response)], [0.5], want_state=False,
+                                       skip_update=update_s is not None)
 
     th = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
     t0 = time.time()
@@ -463,7 +465,7 @@ def reference_sample(cfg, tokens_per_thread: int, threads: int) -> dict:
         t.join()
     wall = time.time() - t0
     t_train = max(r["t_train"] for r in results)
-    t_upd = max(r["t_update"] for r in results)
+    t_upd = max(r["t_update"] for r in results) if update_s is None else update_s
     tok = threads * tokens_per_thread
     per_tok_upd = t_upd / (cfg.global_batch * cfg.resp_len)  # amortised over a real global step
     value = tok / (t_train + per_tok_upd * tokens_per_thread)
@@ -492,8 +494,10 @@ def run_reference(args, dist: Dist):
     threads = ref_threads(cfg)
     tpt = args.ref_tokens
     vals = []
+    upd = None
     for i in range(args.warmup + args.steps):
-        r = reference_sample(cfg, tpt, threads)
+        r = reference_sample(cfg, tpt, threads, update_s=upd)
+        upd = r["t_update_s"]  # measured in the first (warm-up) step, reused after
         if i >= args.warmup:
             vals.append(r)
     v = float(np.mean([r["value"] for r in vals]))

@@ -112,7 +112,7 @@ def rlib() -> C.CDLL:
         L.ref_generate.argtypes = [U64, U64, P, P, I, I, U64, P, P]
         L.ref_run_agent.restype = I
         L.ref_run_agent.argtypes = [C.c_char_p, U64, U64, U64, I64, I64, I, I, P, P, P, P, P, P, P, P, P, D,
-                                    P, P, P, P, P, P, P, P, P]
+                                    P, P, P, P, P, P, P, P, P, I]
         L.ref_poll_order.restype = I
         L.ref_poll_order.argtypes = [I, P, P, P, P, P, I64, I64, P]
         _r = L
@@ -230,7 +230,7 @@ def run_agent(V, D_, G, mb, n_updates, samples, advantages, W0, lr=1e-6, b1=0.9,
 # reference (compiled, unmodified headers) wrappers
 # ---------------------------------------------------------------------------
 def ref_run_agent(agent, V, D_, seed, G, mb, n_updates, ids, turns, trajs, versions, samples, advantages,
-                  insert_order=None, lr=1e-6, want_state=True) -> dict:
+                  insert_order=None, lr=1e-6, want_state=True, skip_update=False) -> dict:
     L = rlib()
     n = len(ids)
     arr = (C.c_char_p * n)(*[s.encode() for s in ids])
@@ -254,7 +254,7 @@ def ref_run_agent(agent, V, D_, seed, G, mb, n_updates, ids, turns, trajs, versi
                          _p(poff), _p(roff), _p(adv), _p(order), lr,
                          _p(W0) if want_state else None, _p(W) if want_state else None,
                          _p(m) if want_state else None, _p(v) if want_state else None,
-                         _p(polled), _p(mbn), _p(upd), _p(tt), _p(tu))
+                         _p(polled), _p(mbn), _p(upd), _p(tt), _p(tu), int(skip_update))
     if rc != 0:
         raise RuntimeError(f"ref_run_agent failed ({rc}): {L.ref_last_error().decode()}")
     return dict(W0=W0.reshape(V, D_), W=W.reshape(V, D_), m=m.reshape(V, D_), v=v.reshape(V, D_),

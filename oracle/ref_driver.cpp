@@ -170,7 +170,7 @@ int ref_run_agent(const char* agent, std::uint64_t V, std::uint64_t D, std::uint
                   const std::int32_t* insert_order, double lr, double* W0_out, double* W_out,
                   double* m_out, double* v_out, std::int32_t* poll_order_out,
                   double* mb_grad_norm_out, double* upd_grad_norm_out, double* t_train_s,
-                  double* t_update_s) {
+                  double* t_update_s, int skip_update) {
     try {
         EventLoop loop;
         Cluster cluster(1, 8, 1ULL << 50, 1ULL << 50);
@@ -236,10 +236,16 @@ int ref_run_agent(const char* agent, std::uint64_t V, std::uint64_t D, std::uint
                 exp.complete(a, batch->samples);
                 mb_grad_norm_out[mb_i++] = gn;
             }
+            if (skip_update) continue;  // timing-only runs (bench.py reference arm)
             const double t1 = now_s();
             trainer.apply_global_update(a);
             tu += now_s() - t1;
             upd_grad_norm_out[u] = log.filter("update").back()->payload["grad_norm"].get<double>();
+        }
+        if (!W_out && !m_out && !v_out) {
+            if (t_train_s) *t_train_s = tt;
+            if (t_update_s) *t_update_s = tu;
+            return 0;
         }
         PolicyState st = trainer.peek_state(a);
         if (W_out) std::memcpy(W_out, st.model.weights().a.data(), V * D * 8);
