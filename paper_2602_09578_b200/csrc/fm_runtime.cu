@@ -881,10 +881,10 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             // K-GEMM1: Z = Phic * W16^T, epilogue z *= 1/n, softmax partials
             CUtensorMap tA, tB, tZ, tGt, tPt;
             if (!make_tmap_bf16_kmajor(&tA, w.phic, Mpad, a->D, kGemmBM) ||
-                !make_tmap_bf16_kmajor(&tB, a->W16, a->V, a->D, kGemmBN) ||
+                !make_tmap_bf16_kmajor(&tB, a->W16, a->V, a->D, gemm_b_box_rows()) ||
                 !make_tmap_2d(&tZ, w.Z, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Mpad, ldz, 64, 128) ||
                 !make_tmap_bf16_kmajor(&tGt, w.gt, a->V, Mpad, kGemmBM) ||
-                !make_tmap_bf16_kmajor(&tPt, w.phict, a->D, Mpad, kGemmBN))
+                !make_tmap_bf16_kmajor(&tPt, w.phict, a->D, Mpad, gemm_b_box_rows()))
                 return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
             const int tiles_n = static_cast<int>((a->V + kGemmBN - 1) / kGemmBN);
             GemmArgs g1{};

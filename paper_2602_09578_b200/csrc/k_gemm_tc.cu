@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "fm_gemm.h"
@@ -272,16 +273,203 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant: a 2-CTA cluster computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M256 N256 K16).  Each CTA TMA-loads its own 128
+// rows of A and its half (128 rows) of B per stage (32 KB), so the pair moves
+// 3/4 of the operand bytes two single-CTA 128x256 tiles would; the leader CTA
+// issues every MMA and commits to both CTAs' barriers; each CTA drains its
+// own 128-lane half of the accumulator from its TMEM.
+// ---------------------------------------------------------------------------
+constexpr int P_STAGES = 6;
+constexpr uint32_t P_A_STAGE = 128 * BK * 2;    // 16 KB: this CTA's 128 rows of A
+constexpr uint32_t P_B_STAGE = 128 * BK * 2;    // 16 KB: this CTA's half of B's 256 rows
+constexpr uint32_t P_STAGE_BYTES = P_A_STAGE + P_B_STAGE;
+constexpr uint32_t kIdesc2 = idesc_bf16_f32<256, BN>();
+
+template <class Epi>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_tn_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       GemmArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + P_STAGES * P_A_STAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
+    uint64_t* empty = full + P_STAGES;
+    uint64_t* tfull = empty + P_STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const uint32_t warp = warp_id();
+    const uint32_t lane = lane_id();
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmA);
+        tma_prefetch(&tmB);
+        for (int s = 0; s < P_STAGES; ++s) {
+            mbar_init(&full[s], 1);   // leader's producer arrives (expect_tx of both CTAs' bytes)
+            mbar_init(&empty[s], 1);  // one multicast commit per consumed stage
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_2sm<kTmemCols>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int tiles_m = (args.M + 255) / 256;
+    const int tiles_n = (args.N + BN - 1) / BN;
+    const int num_tiles = tiles_m * tiles_n;
+    const int k_iters = (args.K + BK - 1) / BK;
+    const int cid = blockIdx.x >> 1;
+    const int nclusters = gridDim.x >> 1;
+
+    if (warp == 0) {
+        // ===== TMA producer (both CTAs) =====
+        if (elect_one()) {
+            const uint64_t pol = policy_evict_last();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = cid; t < num_tiles; t += nclusters) {
+                const TileCoord tc = tile_coord(t, tiles_m, tiles_n, args.group_m);
+                const int arow = tc.mb * 256 + static_cast<int>(rank) * 128;
+                const int brow = tc.nb * BN + static_cast<int>(rank) * 128;
+                for (int k = 0; k < k_iters; ++k) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    const uint32_t fb = mapa_shared(&full[stage], 0);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+                    tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, k * BK, arow, pol);
+                    tma_load_2d_2sm(sB + stage * P_B_STAGE, &tmB, fb, k * BK, brow, pol);
+                    if (++stage == P_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer: leader CTA only =====
+        if (leader && elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = cid; t < num_tiles; t += nclusters) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+                for (int k = 0; k < k_iters; ++k) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint64_t adesc = umma_desc_k_sw128(smem_u32(sA + stage * P_A_STAGE));
+                    const uint64_t bdesc = umma_desc_k_sw128(smem_u32(sB + stage * P_B_STAGE));
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        umma_bf16_2sm(d_tmem, adesc + static_cast<uint64_t>(kk * 2),
+                                      bdesc + static_cast<uint64_t>(kk * 2), kIdesc2, (k | kk) != 0);
+                    umma_commit_2sm(&empty[stage], 0x3);
+                    if (++stage == P_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit_2sm(&tfull[acc], 0x3);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+        __syncwarp();
+    } else {
+        // ===== epilogue warps (both CTAs; each drains its own 128 rows) =====
+        const uint32_t quad = warp & 3;
+        const int row_in_tile = static_cast<int>(rank * 128 + quad * 32 + lane);
+        const uint32_t tempty_leader[2] = {mapa_shared(&tempty[0], 0), mapa_shared(&tempty[1], 0)};
+        Epi epi;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        double sumsq_total = 0.0;
+        for (int t = cid; t < num_tiles; t += nclusters) {
+            const TileCoord tc = tile_coord(t, tiles_m, tiles_n, args.group_m);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int row = tc.mb * 256 + row_in_tile;
+            epi.begin(args, row);
+            if constexpr (std::is_same_v<Epi, GradEpi>) epi.sumsq = 0.0;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem_base + ((quad * 32u) << 16) + static_cast<uint32_t>(acc * BN + c * 32), r);
+                tmem_ld_wait();
+                epi.chunk(args, row, tc.nb * BN + c * 32, r);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
+            epi.end(args, row, tc.nb);
+            if constexpr (std::is_same_v<Epi, GradEpi>) sumsq_total += epi.sumsq;
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+        if constexpr (std::is_same_v<Epi, GradEpi>) {
+            for (int o = 16; o > 0; o >>= 1) sumsq_total += __shfl_xor_sync(0xffffffffu, sumsq_total, o);
+            if (lane == 0 && args.sumsq) atomicAdd(args.sumsq, sumsq_total);
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_2sm<kTmemCols>(tmem_base);
+    }
+}
+
+bool use_pair_mma() {
+    static const bool on = [] {
+        const char* e = getenv("FM_GEMM_2SM");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 }  // namespace
 
-size_t gemm_smem_bytes() { return STAGES * STAGE_BYTES + 1024 + 256; }
+size_t gemm_smem_bytes() {
+    return use_pair_mma() ? P_STAGES * P_STAGE_BYTES + 1024 + 256 : STAGES * STAGE_BYTES + 1024 + 256;
+}
+
+uint32_t gemm_b_box_rows() { return use_pair_mma() ? 128u : static_cast<uint32_t>(BN); }
 
 cudaError_t gemm_tn_launch(GemmKind kind, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const GemmArgs& args, int num_sms, cudaStream_t stream) {
+    const size_t smem = gemm_smem_bytes();
+    if (use_pair_mma()) {
+        const int tiles = ((args.M + 255) / 256) * ((args.N + BN - 1) / BN);
+        if (tiles == 0) return cudaSuccess;
+        const int pairs = num_sms / 2;
+        const int grid = 2 * (tiles < pairs ? tiles : pairs);
+        if (kind == GemmKind::Logits) {
+            auto k = gemm_tn_2sm_kernel<LogitsEpi>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k<<<grid, kThreads, smem, stream>>>(tmA, tmB, args);
+        } else {
+            auto k = gemm_tn_2sm_kernel<GradEpi>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            k<<<grid, kThreads, smem, stream>>>(tmA, tmB, args);
+        }
+        return cudaGetLastError();
+    }
     const int tiles = ((args.M + BM - 1) / BM) * ((args.N + BN - 1) / BN);
     if (tiles == 0) return cudaSuccess;
     const int grid = tiles < num_sms ? tiles : num_sms;
-    const size_t smem = gemm_smem_bytes();
     if (kind == GemmKind::Logits) {
         auto k = gemm_tn_kernel<LogitsEpi>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
