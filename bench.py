@@ -137,7 +137,10 @@ class Dist:
 
     def close(self):
         if self.world > 1:
-            self.dist.destroy_process_group()
+            try:
+                self.dist.barrier()
+            finally:
+                self.dist.destroy_process_group()
 
 
 def placement(agents, world):
@@ -489,7 +492,7 @@ def run_reference(args, dist: Dist):
         return
     cfg = wl.CONFIGS[args.config]
     if not orc.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmarlsim_ref.so not built"}))
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmarlsim_ref.so not built"}), flush=True)
         return
     threads = ref_threads(cfg)
     tpt = args.ref_tokens
@@ -512,7 +515,7 @@ def run_reference(args, dist: Dist):
            "cpu_baseline": {"value": v, "unit": "trained tokens/s", "cores": threads, "kind": "reference",
                             "sample": sample},
            "e2e": {"value": v, "unit": "trained tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out))
+    print(json.dumps(out), flush=True)
 
 
 METRIC = "trained tokens/sec (policy-update micro-batches) at 1/2/4/8 B200 vs CPU ref"
@@ -571,7 +574,7 @@ def main():
                    "config": config_obj(cfg, args), "roofline": res["roofline"], "kernels": res["kernels"],
                    "cpu_baseline": cpu, "e2e": res["e2e"], "gpu_launches": int(res["launches"]),
                    "clocks": res["clocks"]}
-            print(json.dumps(out))
+            print(json.dumps(out), flush=True)
     finally:
         dist.close()
 
