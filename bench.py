@@ -311,7 +311,7 @@ def run_ours(args, dist: Dist) -> dict | None:
     V, Dm, P = cfg.vocab, cfg.feat, cfg.params
     flops_gemm = 2.0 * M_local * V * Dm  # per launch (2VD per trained token)
     Mpad = int(np.ceil(M_local / 128) * 128)
-    bytes_sg = 6.0 * V * Mpad            # read Z fp32 + write G^T bf16
+    bytes_sg = 4.0 * V * Mpad            # read p~ bf16 + write G^T bf16
     bytes_adam = 38.0 * P                # r: w8 m4 v4 g4; w: w8 m4 v4 shadow2
     bytes_lse = M_local * (np.ceil(V / 256) * 8 + 24)
     kernels = {}

@@ -1,6 +1,7 @@
 // fm_gemm.h — host-visible interface of the tcgen05 TN GEMM (k_gemm_tc.cu).
 #pragma once
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstddef>
@@ -20,7 +21,10 @@ enum class GemmKind { Logits, Grad };
 struct GemmArgs {
     int M, N, K;
     int group_m;          // L2 raster: tiles visited in column-major groups of group_m row-tiles
-    float* out;           // Logits: Z [M][ld_out]; Grad: dW [M][ld_out]
+    float* out;           // Grad: dW [M][ld_out]
+    __nv_bfloat16* pexp;  // Logits: p~ = exp(z - m_tile) [M][ld_out] bf16
+    float* zact;          // Logits: fp32 logit of each row's taken token
+    const int32_t* action;   // Logits: taken token per row
     long long ld_out;
     const float* row_scale;  // Logits: per-row 1/n_ctx
     float2* stats;           // Logits: [M][stats_ld] (max, sum exp) per 256-col tile

@@ -41,17 +41,18 @@ cudaError_t launch_gather(const uint8_t* arena, const SampleDesc* sd, int n_samp
                           int64_t M, int64_t Mpad, int64_t global_batch, uint64_t D, RowBuffers rows,
                           __nv_bfloat16* phic, __nv_bfloat16* phict, cudaStream_t s);
 
-// K-lse: combine GEMM1's per-tile softmax partials into lse, taken-token
-// log-prob and the effective row coefficient (PPO-clip surrogate optional).
-cudaError_t launch_lse(const float* Z, int64_t ldz, const float2* stats, int stats_ld, int64_t M,
-                       int64_t Mpad, int64_t V, const SampleDesc* sd, int64_t global_batch,
-                       RowBuffers rows, const float* old_logp, float clip_eps, double* loss_acc,
-                       cudaStream_t s);
+// K-lse: combine GEMM1's per-tile softmax partials into lse, the taken-token
+// log-prob (from the fp32 logit GEMM1 captured) and the effective row
+// coefficient (PPO-clip surrogate optional).
+cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int64_t M, int64_t Mpad,
+                       int64_t V, const SampleDesc* sd, int64_t global_batch, RowBuffers rows,
+                       const float* old_logp, float clip_eps, double* loss_acc, cudaStream_t s);
 
-// K-loss (fused log-softmax gradient): G^T[v][t] = coef_eff_t * (delta(v,a_t) - exp(z - lse_t)),
-// Z tiles streamed in through TMA, G^T tiles stored through TMA.
-cudaError_t launch_softmax_grad(const CUtensorMap& tmZ, const CUtensorMap& tmGt, int64_t Mpad,
-                                int64_t V, RowBuffers rows, cudaStream_t s);
+// K-loss (fused log-softmax gradient):
+//   G^T[v][t] = coef_eff_t * (delta(v, a_t) - p~[t][v] * exp(m_tile(t, v) - lse_t))
+// p~ tiles (bf16, from GEMM1) streamed in through TMA, G^T tiles stored through TMA.
+cudaError_t launch_softmax_grad(const CUtensorMap& tmP, const CUtensorMap& tmGt, const float2* stats,
+                                int stats_ld, int64_t Mpad, int64_t V, RowBuffers rows, cudaStream_t s);
 
 // K-adam (training.hpp:37-51): fp64 master weights, fp32 moments, gradient
 // of type G (float for the tensor-core path, double for parity mode);

@@ -106,7 +106,8 @@ struct Workspace {
     float *coef = nullptr, *rscale = nullptr, *lse = nullptr, *logp = nullptr, *coef_eff = nullptr;
     float* old_logp = nullptr;
     __nv_bfloat16 *phic = nullptr, *phict = nullptr, *gt = nullptr;
-    float* Z = nullptr;
+    __nv_bfloat16* Pexp = nullptr;  // p~ = exp(z - m_tile) [Mpad][ldz] bf16
+    float* zact = nullptr;          // logit of the taken token [Mpad]
     float2* stats = nullptr;
     // parity mode scratch
     int64_t prow_cap = 0;
@@ -215,7 +216,8 @@ void ws_free(Workspace& w) {
     cudaFree(w.phic);
     cudaFree(w.phict);
     cudaFree(w.gt);
-    cudaFree(w.Z);
+    cudaFree(w.Pexp);
+    cudaFree(w.zact);
     cudaFree(w.stats);
     cudaFree(w.zscratch);
     cudaFree(w.dWmb);
@@ -229,7 +231,7 @@ uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
 // Ensure tensor-core workspace for Mpad rows, vocab V, features D.
 int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
     Workspace& w = c->ws;
-    if (Mpad <= w.rows_cap && V <= w.vocab_cap && D <= w.feat_cap && w.Z) return FM_OK;
+    if (Mpad <= w.rows_cap && V <= w.vocab_cap && D <= w.feat_cap && w.Pexp) return FM_OK;
     const int64_t R = std::max<int64_t>(Mpad, w.rows_cap);
     const uint64_t VV = std::max<uint64_t>(V, w.vocab_cap), DD = std::max<uint64_t>(D, w.feat_cap);
     FM_CUDA(cudaStreamSynchronize(c->stream));
@@ -247,7 +249,7 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
     w.prow_cap = keep_parity.prow_cap;
     w.pvocab_cap = keep_parity.pvocab_cap;
     w.pparam_cap = keep_parity.pparam_cap;
-    const uint64_t ldz = round_up(VV, 4);
+    const uint64_t ldz = round_up(VV, 8);
     const uint64_t tiles_n = (VV + kGemmBN - 1) / kGemmBN;
     cudaError_t e = cudaSuccess;
     e = e ? e : dalloc(&w.action, R);
@@ -263,7 +265,8 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
     e = e ? e : dalloc(&w.phic, static_cast<size_t>(R) * DD);
     e = e ? e : dalloc(&w.phict, static_cast<size_t>(R) * DD);
     e = e ? e : dalloc(&w.gt, static_cast<size_t>(R) * VV);
-    e = e ? e : dalloc(&w.Z, static_cast<size_t>(R) * ldz);
+    e = e ? e : dalloc(&w.Pexp, static_cast<size_t>(R) * ldz);
+    e = e ? e : dalloc(&w.zact, R);
     e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n);
     if (e != cudaSuccess) {
         ws_free(w);
@@ -278,7 +281,7 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
 int ws_reserve_rows(fm_ctx* c, int64_t R) {  // row arrays only (parity mode)
     Workspace& w = c->ws;
     if (R <= w.rows_cap && w.action) return FM_OK;
-    if (w.Z) return ws_reserve_tc(c, R, w.vocab_cap, w.feat_cap);
+    if (w.Pexp) return ws_reserve_tc(c, R, w.vocab_cap, w.feat_cap);
     FM_CUDA(cudaStreamSynchronize(c->stream));
     cudaFree(w.action);
     cudaFree(w.ctx4);
@@ -868,7 +871,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
 
     if (M > 0) {
         if (tc) {
-            const uint64_t ldz = round_up(a->V, 4);
+            const uint64_t ldz = round_up(a->V, 8);
             {
                 KScope k(c, K_MEMSET, s);
                 FM_CUDA(cudaMemsetAsync(w.phic, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
@@ -878,11 +881,12 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 KScope k(c, K_GATHER, s);
                 FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, Mpad, G, a->D, rows, w.phic, w.phict, s));
             }
-            // K-GEMM1: Z = Phic * W16^T, epilogue z *= 1/n, softmax partials
-            CUtensorMap tA, tB, tZ, tGt, tPt;
+            // K-GEMM1: z = Phic * W16^T / n; epilogue stores p~ = exp(z - m_tile) (bf16),
+            // the (m_tile, sum p~) softmax partials and the taken token's logit
+            CUtensorMap tA, tB, tP, tGt, tPt;
             if (!make_tmap_bf16_kmajor(&tA, w.phic, Mpad, a->D, kGemmBM) ||
                 !make_tmap_bf16_kmajor(&tB, a->W16, a->V, a->D, gemm_b_box_rows()) ||
-                !make_tmap_2d(&tZ, w.Z, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, Mpad, ldz, 64, 128) ||
+                !make_tmap_2d(&tP, w.Pexp, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Mpad, ldz, 64, 128) ||
                 !make_tmap_bf16_kmajor(&tGt, w.gt, a->V, Mpad, kGemmBM) ||
                 !make_tmap_bf16_kmajor(&tPt, w.phict, a->D, Mpad, gemm_b_box_rows()))
                 return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -892,7 +896,9 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g1.N = static_cast<int>(a->V);
             g1.K = static_cast<int>(a->D);
             g1.group_m = 16;
-            g1.out = w.Z;
+            g1.pexp = w.Pexp;
+            g1.zact = w.zact;
+            g1.action = w.action;
             g1.ld_out = static_cast<long long>(ldz);
             g1.row_scale = w.rscale;
             g1.stats = w.stats;
@@ -904,14 +910,13 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             // K-lse
             {
                 KScope k(c, K_LSE, s);
-                FM_CUDA(launch_lse(w.Z, static_cast<int64_t>(ldz), w.stats, tiles_n, M, Mpad,
-                                   static_cast<int64_t>(a->V), w.sd, G, rows,
+                FM_CUDA(launch_lse(w.zact, w.stats, tiles_n, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
                                    a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1, s));
             }
             // K-softmax-grad: G^T tiles (zero for padding rows)
             {
                 KScope k(c, K_SOFTMAX_GRAD, s);
-                FM_CUDA(launch_softmax_grad(tZ, tGt, Mpad, static_cast<int64_t>(a->V), rows, s));
+                FM_CUDA(launch_softmax_grad(tP, tGt, w.stats, tiles_n, Mpad, static_cast<int64_t>(a->V), rows, s));
             }
             // K-GEMM2: dW (+)= G^T * Phic ; first contribution of the step overwrites
             GemmArgs g2{};

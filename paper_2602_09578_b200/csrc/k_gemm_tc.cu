@@ -57,42 +57,62 @@ __device__ __forceinline__ float fast_exp(float x) { return exp2f(x * 1.44269504
 
 // One thread owns one accumulator row of the tile; it sees 32 consecutive
 // columns per call.  State carried across the 8 column chunks of a tile.
+// Two passes over the tile's TMEM columns: pass 1 finds the row's tile max
+// (and captures the taken token's logit z_a in fp32); pass 2 stores
+// p~ = exp(z - m_tile) as bf16 and accumulates sum p~.  K-lse turns the
+// (m_tile, sum) partials into lse; K-loss rescales p~ by exp(m_tile - lse).
+// Storing p~ (in (0,1], bf16 rel. error 2^-9) instead of fp32 z halves the
+// logits round trip and keeps exp() out of K-loss.
 struct LogitsEpi {
+    static constexpr bool kTwoPass = true;
     float row_scale;
     float run_max, run_sum;
+    int action;
     __device__ __forceinline__ void begin(const GemmArgs& a, int row) {
-        row_scale = row < a.M ? a.row_scale[row] : 0.f;
+        const bool ok = row < a.M;
+        row_scale = ok ? a.row_scale[row] : 0.f;
+        action = ok ? a.action[row] : -1;
         run_max = -INFINITY;
         run_sum = 0.f;
     }
-    __device__ __forceinline__ void chunk(const GemmArgs& a, int row, int col0, uint32_t (&r)[32]) {
-        float z[32];
+    __device__ __forceinline__ void pass1(const GemmArgs& a, int row, int col0, uint32_t (&r)[32]) {
+        if (row >= a.M) return;
+        const int nvalid = min(32, a.N - col0);
+        float cmax = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) z[j] = __uint_as_float(r[j]) * row_scale;
+        for (int j = 0; j < 32; ++j) {
+            const float z = __uint_as_float(r[j]) * row_scale;
+            if (j < nvalid) cmax = fmaxf(cmax, z);
+            if (col0 + j == action && j < nvalid) a.zact[row] = z;
+        }
+        run_max = fmaxf(run_max, cmax);
+    }
+    __device__ __forceinline__ void chunk(const GemmArgs& a, int row, int col0, uint32_t (&r)[32]) {
         if (row >= a.M) return;
         const int nvalid = min(32, a.N - col0);
         if (nvalid <= 0) return;
-        float* dst = a.out + static_cast<size_t>(row) * a.ld_out + col0;
+        const float m = run_max;
+        uint32_t pk[16];
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+            const float p0 = j < nvalid ? fast_exp(__uint_as_float(r[j]) * row_scale - m) : 0.f;
+            const float p1 = j + 1 < nvalid ? fast_exp(__uint_as_float(r[j + 1]) * row_scale - m) : 0.f;
+            s += p0 + p1;
+            const __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+            pk[j >> 1] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        run_sum += s;
+        __nv_bfloat16* dst = a.pexp + static_cast<size_t>(row) * a.ld_out + col0;
         if (nvalid == 32) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4*>(dst + j) = make_float4(z[j], z[j + 1], z[j + 2], z[j + 3]);
+            for (int q = 0; q < 4; ++q)
+                reinterpret_cast<uint4*>(dst)[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-                if (j < nvalid) dst[j] = z[j];
+                if (j < nvalid) dst[j] = reinterpret_cast<const __nv_bfloat16*>(pk)[j];
         }
-        float cmax = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            if (j < nvalid) cmax = fmaxf(cmax, z[j]);
-        const float nm = fmaxf(run_max, cmax);
-        float s = run_sum * fast_exp(run_max - nm);
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            if (j < nvalid) s += fast_exp(z[j] - nm);
-        run_max = nm;
-        run_sum = s;
     }
     __device__ __forceinline__ void end(const GemmArgs& a, int row, int nb) {
         if (row < a.M) a.stats[static_cast<size_t>(row) * a.stats_ld + nb] = make_float2(run_max, run_sum);
@@ -100,7 +120,9 @@ struct LogitsEpi {
 };
 
 struct GradEpi {
+    static constexpr bool kTwoPass = false;
     double sumsq;
+    __device__ __forceinline__ void pass1(const GemmArgs&, int, int, uint32_t (&)[32]) {}
     __device__ __forceinline__ void begin(const GemmArgs&, int) {}
     __device__ __forceinline__ void chunk(const GemmArgs& a, int row, int col0, uint32_t (&r)[32]) {
         if (row >= a.M) return;
@@ -249,6 +271,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int row = tc.mb * BM + row_in_tile;
             epi.begin(args, row);
             if constexpr (std::is_same_v<Epi, GradEpi>) epi.sumsq = 0.0;
+            if constexpr (Epi::kTwoPass) {
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tmem_base + ((quad * 32u) << 16) + static_cast<uint32_t>(acc * BN + c * 32), r);
+                    tmem_ld_wait();
+                    epi.pass1(args, row, tc.nb * BN + c * 32, r);
+                }
+            }
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t r[32];
@@ -404,6 +435,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int row = tc.mb * 256 + row_in_tile;
             epi.begin(args, row);
             if constexpr (std::is_same_v<Epi, GradEpi>) epi.sumsq = 0.0;
+            if constexpr (Epi::kTwoPass) {
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tmem_base + ((quad * 32u) << 16) + static_cast<uint32_t>(acc * BN + c * 32), r);
+                    tmem_ld_wait();
+                    epi.pass1(args, row, tc.nb * BN + c * 32, r);
+                }
+            }
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t r[32];

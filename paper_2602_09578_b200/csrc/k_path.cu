@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
 // ---------------------------------------------------------------------------
 // K-lse
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ Z, int64_t ldz,
+__global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ zact,
                                                   const float2* __restrict__ stats, int stats_ld,
                                                   int64_t M, int64_t Mpad, int64_t V,
                                                   const SampleDesc* __restrict__ sd, int64_t G,
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ Z, i
                 const float lse = m + logf(s);
                 const int a = rows.action[r];
                 const bool valid = a >= 0 && a < V;
-                const float lp = valid ? Z[static_cast<size_t>(r) * ldz + a] - lse : 0.f;
+                const float lp = valid ? zact[r] - lse : 0.f;  // policy.hpp:72-75, fp32 logit
                 float ce = rows.coef[r];
                 const double adv = sd[rows.sample[r]].adv;
                 if (old_logp && clip_eps > 0.f) {
@@ -207,36 +207,41 @@ __global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ Z, i
 // K-softmax-grad: 64 rows x 128 vocab per CTA.
 // ---------------------------------------------------------------------------
 constexpr int kSgRows = 64, kSgCols = 128;
-constexpr uint32_t kSgZBytes = kSgRows * kSgCols * 4;  // 32 KB fp32 tile
-constexpr uint32_t kSgGBytes = kSgRows * kSgCols * 2;  // 16 KB bf16 tile (swizzled 128 B rows)
+constexpr uint32_t kSgPBytes = kSgRows * kSgCols * 2;  // 16 KB bf16 p~ tile
+constexpr uint32_t kSgGBytes = kSgRows * kSgCols * 2;  // 16 KB bf16 G^T tile (swizzled 128 B rows)
 
-__global__ void __launch_bounds__(256) softmax_grad_kernel(const __grid_constant__ CUtensorMap tmZ,
+__global__ void __launch_bounds__(256) softmax_grad_kernel(const __grid_constant__ CUtensorMap tmP,
                                                            const __grid_constant__ CUtensorMap tmGt,
+                                                           const float2* __restrict__ stats, int stats_ld,
                                                            RowBuffers rows) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
-    float* Zs = reinterpret_cast<float*>(smem);
-    uint8_t* Gs = smem + kSgZBytes;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kSgZBytes + kSgGBytes);
-    float* s_lse = reinterpret_cast<float*>(bar + 2);
-    float* s_coef = s_lse + kSgRows;
+    const __nv_bfloat16* Ps = reinterpret_cast<const __nv_bfloat16*>(smem);
+    uint8_t* Gs = smem + kSgPBytes;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kSgPBytes + kSgGBytes);
+    float* s_scale = reinterpret_cast<float*>(bar + 2);
+    float* s_coef = s_scale + kSgRows;
     int* s_act = reinterpret_cast<int*>(s_coef + kSgRows);
 
     const int v0 = blockIdx.x * kSgCols;
     const int r0 = blockIdx.y * kSgRows;
+    const int tile = v0 / 256;  // GEMM1's 256-wide softmax-partial tile holding these columns
     const int tid = threadIdx.x;
     if (tid == 0) {
-        tma_prefetch(&tmZ);
+        tma_prefetch(&tmP);
         mbar_init(bar, 1);
         fence_barrier_init();
-        mbar_arrive_expect_tx(bar, kSgZBytes);
-        tma_load_2d_hint(Zs, &tmZ, bar, v0, r0, policy_evict_first());
+        mbar_arrive_expect_tx(bar, kSgPBytes);
+        tma_load_2d_hint(reinterpret_cast<void*>(smem), &tmP, bar, v0, r0, policy_evict_first());
     }
     if (tid < kSgRows) {
-        s_lse[tid] = rows.lse[r0 + tid];
-        s_coef[tid] = rows.coef_eff[r0 + tid];
-        s_act[tid] = rows.action[r0 + tid];
+        const int r = r0 + tid;
+        const float c = rows.coef_eff[r];
+        s_coef[tid] = c;
+        s_act[tid] = rows.action[r];
+        // p = p~ * exp(m_tile - lse)   (p~ = exp(z - m_tile) from GEMM1's epilogue)
+        s_scale[tid] = c == 0.f ? 0.f : __expf(stats[static_cast<size_t>(r) * stats_ld + tile].x - rows.lse[r]);
     }
     __syncthreads();
     mbar_wait(bar, 0);
@@ -254,10 +259,10 @@ __global__ void __launch_bounds__(256) softmax_grad_kernel(const __grid_constant
             const float ca = s_coef[ra], cb = s_coef[rb];
             const float ga = ca == 0.f ? 0.f
                                        : ca * ((v == s_act[ra] ? 1.f : 0.f) -
-                                               __expf(Zs[ra * kSgCols + vl] - s_lse[ra]));
+                                               __bfloat162float(Ps[ra * kSgCols + vl]) * s_scale[ra]);
             const float gb = cb == 0.f ? 0.f
                                        : cb * ((v == s_act[rb] ? 1.f : 0.f) -
-                                               __expf(Zs[rb * kSgCols + vl] - s_lse[rb]));
+                                               __bfloat162float(Ps[rb * kSgCols + vl]) * s_scale[rb]);
             const __nv_bfloat162 h = __floats2bfloat162_rn(ga, gb);  // .x = low = row ra
             packed[i >> 1] = *reinterpret_cast<const uint32_t*>(&h);
         }
@@ -474,23 +479,23 @@ cudaError_t launch_gather(const uint8_t* arena, const SampleDesc* sd, int n_samp
     return cudaGetLastError();
 }
 
-cudaError_t launch_lse(const float* Z, int64_t ldz, const float2* stats, int stats_ld, int64_t M, int64_t Mpad,
-                       int64_t V, const SampleDesc* sd, int64_t global_batch, RowBuffers rows,
-                       const float* old_logp, float clip_eps, double* loss_acc, cudaStream_t s) {
+cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int64_t M, int64_t Mpad, int64_t V,
+                       const SampleDesc* sd, int64_t global_batch, RowBuffers rows, const float* old_logp,
+                       float clip_eps, double* loss_acc, cudaStream_t s) {
     if (Mpad == 0) return cudaSuccess;
     const int blocks = static_cast<int>((Mpad * 32 + 255) / 256);
-    lse_kernel<<<blocks, 256, 0, s>>>(Z, ldz, stats, stats_ld, M, Mpad, V, sd, global_batch, rows, old_logp,
-                                      clip_eps, loss_acc);
+    lse_kernel<<<blocks, 256, 0, s>>>(zact, stats, stats_ld, M, Mpad, V, sd, global_batch, rows, old_logp, clip_eps,
+                                      loss_acc);
     return cudaGetLastError();
 }
 
-cudaError_t launch_softmax_grad(const CUtensorMap& tmZ, const CUtensorMap& tmGt, int64_t Mpad, int64_t V,
-                                RowBuffers rows, cudaStream_t s) {
+cudaError_t launch_softmax_grad(const CUtensorMap& tmP, const CUtensorMap& tmGt, const float2* stats, int stats_ld,
+                                int64_t Mpad, int64_t V, RowBuffers rows, cudaStream_t s) {
     if (Mpad == 0) return cudaSuccess;
-    const size_t smem = 1024 + kSgZBytes + kSgGBytes + 16 + kSgRows * 12;
+    const size_t smem = 1024 + kSgPBytes + kSgGBytes + 16 + kSgRows * 12;
     cudaFuncSetAttribute(softmax_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     dim3 grid(static_cast<unsigned>((V + kSgCols - 1) / kSgCols), static_cast<unsigned>(Mpad / kSgRows));
-    softmax_grad_kernel<<<grid, 256, smem, s>>>(tmZ, tmGt, rows);
+    softmax_grad_kernel<<<grid, 256, smem, s>>>(tmP, tmGt, stats, stats_ld, rows);
     return cudaGetLastError();
 }
 
