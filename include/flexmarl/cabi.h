@@ -203,6 +203,30 @@ int fm_agent_activate(fm_agent* a, fm_ctx* ctx);
 /* FNV-1a over the bytes of {W, m, v, grad, step, version, samples}: swap-identity check. */
 int fm_agent_state_checksum(fm_agent* a, uint64_t* out);
 
+/* ---- weight publish / rollout sync ----------------------------
+ * publish_weights (training.hpp:459-467): one contiguous device buffer in
+ * pack_weights' single-tensor layout (object_store.hpp:258-273), stamped with
+ * the agent version.  dtype 0 = f64 (reference payload bytes), 1 = f32, 2 = bf16. */
+typedef struct fm_weights fm_weights;
+int fm_publish_weights(fm_agent* a, int dtype, fm_weights** out);
+int fm_weights_alloc(fm_ctx* ctx, uint64_t rows, uint64_t cols, int dtype, fm_weights** out);
+int fm_weights_info(const fm_weights* w, int64_t* version, uint64_t* rows, uint64_t* cols, int* dtype,
+                    uint64_t* nbytes, int* device);
+/* One Get per rollout consumer (rollout.hpp:510-541): host (dst_device -1) or any GPU (NVLink P2P). */
+int fm_weights_get(const fm_weights* w, void* dst, int dst_device);
+/* Sync every rank of a communicator from `root` in one NCCL broadcast (NVLink/NVSwitch). */
+int fm_weights_broadcast(fm_weights* w, fm_comm* c, int root);
+int fm_weights_destroy(fm_weights* w);
+
+/* ---- PolicyState wire format (training.hpp:107-164) -----------
+ * Byte-identical to PolicyState::serialize when no gradient is pending; a
+ * pending step is one cache entry ("__sum__",0,0,version) holding sum(term).
+ * out == NULL returns the required length.  deserialize reads matrix dims in
+ * the defined rows-then-cols order (training.hpp:146 evaluates them in
+ * unspecified order and transposes W when V != D). */
+int fm_agent_serialize(fm_agent* a, int64_t global_batch, uint8_t* out, uint64_t cap, uint64_t* len);
+int fm_agent_deserialize(fm_agent* a, int64_t global_batch, const uint8_t* in, uint64_t len);
+
 /* ---- GRPO advantages (training.hpp:54-67), device kernel K-adv --------------
  * rewards[seg_off[i]:seg_off[i+1]] is group i; host arrays in/out. */
 int fm_group_advantages(fm_ctx* ctx, const double* rewards, const int32_t* seg_off, int nseg,

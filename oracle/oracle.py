@@ -113,6 +113,10 @@ def rlib() -> C.CDLL:
         L.ref_run_agent.restype = I
         L.ref_run_agent.argtypes = [C.c_char_p, U64, U64, U64, I64, I64, I, I, P, P, P, P, P, P, P, P, P, D,
                                     P, P, P, P, P, P, P, P, P, I]
+        L.ref_serialize_state.restype = U64
+        L.ref_serialize_state.argtypes = [I64, I64, I64, U64, U64, P, P, P, P, U64]
+        L.ref_deserialize_state.restype = I
+        L.ref_deserialize_state.argtypes = [P, U64, P, P, P, P, P]
         L.ref_poll_order.restype = I
         L.ref_poll_order.argtypes = [I, P, P, P, P, P, I64, I64, P]
         _r = L
@@ -269,3 +273,27 @@ def ref_generate(W, prompt, max_tokens, tok_seed):
     lps = np.zeros(max_tokens, dtype=np.float64)
     n = rlib().ref_generate(W.shape[0], W.shape[1], _p(W), _p(p), len(p), max_tokens, tok_seed, _p(toks), _p(lps))
     return toks[:n].copy(), lps[:n].copy()
+
+
+def ref_serialize_state(version, step, samples, W, m, v) -> bytes:
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    V, D_ = W.shape
+    m = None if m is None else np.ascontiguousarray(m, dtype=np.float64)
+    v = None if v is None else np.ascontiguousarray(v, dtype=np.float64)
+    L = rlib()
+    n = L.ref_serialize_state(version, step, samples, V, D_, _p(W), _p(m) if m is not None else None,
+                              _p(v) if v is not None else None, None, 0)
+    out = np.zeros(n, dtype=np.uint8)
+    L.ref_serialize_state(version, step, samples, V, D_, _p(W), _p(m) if m is not None else None,
+                          _p(v) if v is not None else None, _p(out), n)
+    return out.tobytes()
+
+
+def ref_deserialize_state(blob: bytes, P_: int) -> dict:
+    buf = np.frombuffer(blob, dtype=np.uint8).copy()
+    r, c, ver, cn = (np.zeros(1, np.uint64), np.zeros(1, np.uint64), np.zeros(1, np.int64), np.zeros(1, np.uint64))
+    W = np.zeros(P_)
+    rc = rlib().ref_deserialize_state(_p(buf), len(buf), _p(r), _p(c), _p(W), _p(ver), _p(cn))
+    if rc != 0:
+        raise RuntimeError(rlib().ref_last_error().decode())
+    return dict(rows=int(r[0]), cols=int(c[0]), W=W, version=int(ver[0]), cache_n=int(cn[0]))

@@ -299,3 +299,50 @@ int ref_poll_order(int n, const char* const* input_ids, const std::int32_t* turn
 }
 
 }  // extern "C"
+
+extern "C" {
+
+// PolicyState::serialize (training.hpp:107-133) of a state with the given
+// fields and an empty gradient cache.  Returns the byte length; writes when
+// out != NULL and cap suffices.
+std::uint64_t ref_serialize_state(std::int64_t version, std::int64_t step, std::int64_t samples,
+                                  std::uint64_t V, std::uint64_t D, const double* W, const double* m,
+                                  const double* v, std::uint8_t* out, std::uint64_t cap) {
+    PolicyState st;
+    st.version = version;
+    st.samples_accumulated = samples;
+    st.opt.step_count = step;
+    st.model = PolicyModel(V, D);
+    std::memcpy(st.model.weights().a.data(), W, V * D * 8);
+    if (m && v) {
+        st.opt.m = Matrix(V, D);
+        st.opt.v = Matrix(V, D);
+        std::memcpy(st.opt.m.a.data(), m, V * D * 8);
+        std::memcpy(st.opt.v.a.data(), v, V * D * 8);
+    }
+    const std::vector<std::uint8_t> b = st.serialize();
+    if (out && cap >= b.size()) std::memcpy(out, b.data(), b.size());
+    return b.size();
+}
+
+// PolicyState::deserialize (training.hpp:135-164) as the reference does it;
+// reports the dims it read for W (exposes the argument-order defect at :146).
+int ref_deserialize_state(const std::uint8_t* in, std::uint64_t len, std::uint64_t* w_rows,
+                          std::uint64_t* w_cols, double* W_out, std::int64_t* version,
+                          std::uint64_t* cache_n) {
+    try {
+        std::vector<std::uint8_t> b(in, in + len);
+        PolicyState st = PolicyState::deserialize("x", b);
+        *w_rows = st.model.weights().rows;
+        *w_cols = st.model.weights().cols;
+        if (W_out) std::memcpy(W_out, st.model.weights().a.data(), st.model.weights().a.size() * 8);
+        *version = st.version;
+        *cache_n = st.grad_cache.size();
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+}  // extern "C"

@@ -93,6 +93,14 @@ _PROTOS = {
     "fm_comm_create": (I, [P, P, I, I, C.POINTER(P)]),
     "fm_comm_destroy": (I, [P]),
     "fm_agent_allreduce_grad": (I, [P, P]),
+    "fm_publish_weights": (I, [P, I, C.POINTER(P)]),
+    "fm_weights_alloc": (I, [P, U64, U64, I, C.POINTER(P)]),
+    "fm_weights_info": (I, [P, PI64, PU64, PU64, C.POINTER(C.c_int), PU64, C.POINTER(C.c_int)]),
+    "fm_weights_get": (I, [P, P, I]),
+    "fm_weights_broadcast": (I, [P, P, I]),
+    "fm_weights_destroy": (I, [P]),
+    "fm_agent_serialize": (I, [P, I64, P, U64, PU64]),
+    "fm_agent_deserialize": (I, [P, I64, P, U64]),
     "fm_store_create": (I, [C.POINTER(P)]),
     "fm_store_destroy": (I, [P]),
     "fm_store_create_table": (I, [P, S, P, P, I]),

@@ -158,3 +158,15 @@ def test_live_reference_cross_check():
         L.ref_accumulate_grad(V, D, W.ctypes.data, ctx.ctypes.data, len(ctx), a, 0.7, o1.ctypes.data)
         orc.olib().fmo_accumulate_grad(V, D, W.ctypes.data, ctx.ctypes.data, len(ctx), a, 0.7, o2.ctypes.data)
         assert np.array_equal(o1, o2)
+
+
+@pytest.mark.skipif(not orc.ref_available(), reason="oracle/_ref not built")
+def test_reference_state_swap_transposes_nonsquare():
+    """Documents reference defect #1: PolicyState::deserialize
+    reads Matrix(r.read_u64(), r.read_u64()) with unspecified argument order,
+    so a V x D state comes back D x V under GCC.  The B200 swap must not (and
+    does not) replicate this; fm_agent_deserialize reads rows then cols."""
+    W = np.arange(6.0).reshape(3, 2)
+    blob = orc.ref_serialize_state(1, 1, 0, W, W, W)
+    r = orc.ref_deserialize_state(blob, 6)
+    assert (r["rows"], r["cols"]) == (2, 3)
