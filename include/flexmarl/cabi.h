@@ -218,6 +218,16 @@ int fm_weights_get(const fm_weights* w, void* dst, int dst_device);
 int fm_weights_broadcast(fm_weights* w, fm_comm* c, int root);
 int fm_weights_destroy(fm_weights* w);
 
+/* ---- rollout generation on the GPU ----------------------------
+ * PolicyModel::generate (policy.hpp:119-130) for n requests from a published
+ * f64 weight buffer on ctx's GPU: request i has prompt
+ * prompts[prompt_off[i]:prompt_off[i+1]] and token seed seeds[i] (the
+ * reference derives it as rollout.hpp:640-644); outputs are n x max_tokens
+ * row-major (tokens, log pi) and per-request lengths (EOS included). */
+int fm_generate(fm_ctx* ctx, const fm_weights* w, const int32_t* prompts, const int32_t* prompt_off, int n,
+                int max_tokens, const uint64_t* seeds, int32_t* out_tokens, double* out_logp,
+                int32_t* out_len);
+
 /* ---- PolicyState wire format (training.hpp:107-164) -----------
  * Byte-identical to PolicyState::serialize when no gradient is pending; a
  * pending step is one cache entry ("__sum__",0,0,version) holding sum(term).

@@ -99,6 +99,7 @@ _PROTOS = {
     "fm_weights_get": (I, [P, P, I]),
     "fm_weights_broadcast": (I, [P, P, I]),
     "fm_weights_destroy": (I, [P]),
+    "fm_generate": (I, [P, P, P, P, I, I, P, P, P, P]),
     "fm_agent_serialize": (I, [P, I64, P, U64, PU64]),
     "fm_agent_deserialize": (I, [P, I64, P, U64]),
     "fm_store_create": (I, [C.POINTER(P)]),

@@ -75,6 +75,12 @@ cudaError_t launch_parity_rows(const double* W, uint64_t V, uint64_t D, int64_t 
                                RowBuffers rows, const SampleDesc* sd, int64_t global_batch,
                                double* zscratch, double* dWmb, double* logp64, double* loss_acc,
                                cudaStream_t s);
+// Rollout-side generation (policy.hpp:119-130), one CTA per request (k_rollout.cu).
+cudaError_t launch_generate(const double* W, uint64_t V, uint64_t D, const int32_t* prompts,
+                            const int32_t* prompt_off, int n_req, int max_tokens, const uint64_t* seeds,
+                            double* zbuf, int32_t* out_tok, double* out_logp, int32_t* out_len,
+                            cudaStream_t s);
+
 // sumsq += |dWmb|^2; dW += dWmb; dWmb = 0
 cudaError_t launch_parity_fold(double* dW, double* dWmb, uint64_t n, double* sumsq, int num_sms,
                                cudaStream_t s);

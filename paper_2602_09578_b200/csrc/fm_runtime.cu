@@ -1643,4 +1643,45 @@ int fm_agent_deserialize(fm_agent* a, int64_t global_batch, const uint8_t* in, u
     FM_GUARD_END
 }
 
+// §8f-3: PolicyModel::generate (policy.hpp:119-130) for n requests on the GPU
+// from a published f64 weight buffer; seeds are the per-request token seeds
+// (rollout.hpp:638-645).  Host arrays in and out.
+int fm_generate(fm_ctx* c, const fm_weights* w, const int32_t* prompts, const int32_t* prompt_off, int n,
+                int max_tokens, const uint64_t* seeds, int32_t* out_tokens, double* out_logp, int32_t* out_len) {
+    FM_GUARD_BEGIN
+    if (w->dtype != 0) return fail(FM_ERR_CONFIG_ERROR, "generation reads f64 weights (publish with dtype 0)");
+    if (w->device != c->device) return fail(FM_ERR_CONFIG_ERROR, "weights live on another GPU (fm_weights_get)");
+    if (n <= 0 || max_tokens <= 0) return FM_OK;
+    if (int st = set_dev(c)) return st;
+    cudaStream_t s = c->stream;
+    const int np = prompt_off[n];
+    int32_t *dp = nullptr, *doff = nullptr, *dtok = nullptr, *dlen = nullptr;
+    uint64_t* dseed = nullptr;
+    double *dz = nullptr, *dlp = nullptr;
+    const size_t nt = static_cast<size_t>(n) * max_tokens;
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dp), std::max(np, 1) * 4, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&doff), (n + 1) * 4, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dseed), n * 8, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dz), static_cast<size_t>(n) * w->rows * 8, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dtok), nt * 4, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dlp), nt * 8, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dlen), n * 4, s));
+    if (np) FM_CUDA(cudaMemcpyAsync(dp, prompts, np * 4, cudaMemcpyHostToDevice, s));
+    FM_CUDA(cudaMemcpyAsync(doff, prompt_off, (n + 1) * 4, cudaMemcpyHostToDevice, s));
+    FM_CUDA(cudaMemcpyAsync(dseed, seeds, n * 8, cudaMemcpyHostToDevice, s));
+    FM_CUDA(launch_generate(static_cast<const double*>(w->buf), w->rows, w->cols, dp, doff, n, max_tokens, dseed, dz,
+                            dtok, dlp, dlen, s));
+    count_launch();
+    FM_CUDA(cudaMemcpyAsync(out_tokens, dtok, nt * 4, cudaMemcpyDeviceToHost, s));
+    FM_CUDA(cudaMemcpyAsync(out_logp, dlp, nt * 8, cudaMemcpyDeviceToHost, s));
+    FM_CUDA(cudaMemcpyAsync(out_len, dlen, n * 4, cudaMemcpyDeviceToHost, s));
+    for (void* p : {static_cast<void*>(dp), static_cast<void*>(doff), static_cast<void*>(dseed),
+                    static_cast<void*>(dz), static_cast<void*>(dtok), static_cast<void*>(dlp),
+                    static_cast<void*>(dlen)})
+        FM_CUDA(cudaFreeAsync(p, s));
+    FM_CUDA(cudaStreamSynchronize(s));
+    return FM_OK;
+    FM_GUARD_END
+}
+
 }  // extern "C"
