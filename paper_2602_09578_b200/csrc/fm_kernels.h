@@ -36,10 +36,12 @@ struct RowBuffers {
 
 // K-gather: decode the selected records' token payloads straight out of the
 // arena into packed rows; optionally scatter integer-count features into the
-// dense bf16 operands Phic [Mpad][D] and Phic^T [D][Mpad] (pre-zeroed).
+// dense bf16 operands Phic [Mpad][D] and Phic^T [D][Mpad] (pre-zeroed, or
+// holding the previous micro-batch's pattern for the same Mpad/D when
+// clear_old != 0, in which case each row first erases its old entries).
 cudaError_t launch_gather(const uint8_t* arena, const SampleDesc* sd, int n_samples, int64_t row_lo,
                           int64_t M, int64_t Mpad, int64_t global_batch, uint64_t D, RowBuffers rows,
-                          __nv_bfloat16* phic, __nv_bfloat16* phict, cudaStream_t s);
+                          __nv_bfloat16* phic, __nv_bfloat16* phict, int clear_old, cudaStream_t s);
 
 // K-lse: combine GEMM1's per-tile softmax partials into lse, the taken-token
 // log-prob (from the fp32 logit GEMM1 captured) and the effective row

@@ -115,6 +115,11 @@ struct Workspace {
     double *zscratch = nullptr, *dWmb = nullptr, *logp64 = nullptr;
     SampleDesc* sd = nullptr;
     int sd_cap = 0;
+    // Phic / Phic^T hold exactly the entries of the rows in the row buffers
+    // (for phi_Mpad, phi_D): the next gather erases them row by row
+    bool phi_valid = false;
+    int64_t phi_Mpad = 0;
+    uint64_t phi_D = 0;
 };
 
 // Per-kernel device timing (bench.py's roofline): event pairs recorded on the
@@ -283,6 +288,7 @@ int ws_reserve_rows(fm_ctx* c, int64_t R) {  // row arrays only (parity mode)
     if (R <= w.rows_cap && w.action) return FM_OK;
     if (w.Pexp) return ws_reserve_tc(c, R, w.vocab_cap, w.feat_cap);
     FM_CUDA(cudaStreamSynchronize(c->stream));
+    w.phi_valid = false;
     cudaFree(w.action);
     cudaFree(w.ctx4);
     cudaFree(w.n_ctx);
@@ -591,6 +597,8 @@ struct fm_agent {
     void* dW = nullptr;  // float (TC) or double (parity)
     __nv_bfloat16* W16 = nullptr;
     bool dw_valid = false;  // dW holds this step's partial sum
+    bool pending_in = false;  // a swap-in copy the next use must wait for
+    bool park_w16 = false;    // the parked copy includes the bf16 shadow
     int64_t step = 0, version = 0, samples = 0;
     // reports
     double* d_scalars = nullptr;  // [kReportRing][2]: sumsq, loss
@@ -678,8 +686,17 @@ void agent_free_device(fm_agent* a, cudaStream_t s) {
     a->W16 = nullptr;
 }
 
-int check_active(const fm_agent* a) {
+// Every operation on an agent goes through here: besides the InactiveGroup
+// check it inserts the lazy dependency on a pending swap-in, so that an
+// activate() prefetch never stalls other agents' work on the shared compute
+// stream — only this agent's first use waits for its copy-in.
+int check_active(fm_agent* a) {
     if (!a->active || !a->ctx) return fail(FM_ERR_INACTIVE_GROUP, a->name);
+    if (a->pending_in) {
+        FM_CUDA(cudaSetDevice(a->ctx->device));
+        FM_CUDA(cudaStreamWaitEvent(a->ctx->stream, a->ev_in, 0));
+        a->pending_in = false;
+    }
     return FM_OK;
 }
 
@@ -872,15 +889,20 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
     if (M > 0) {
         if (tc) {
             const uint64_t ldz = round_up(a->V, 8);
-            {
+            const bool reuse = w.phi_valid && w.phi_Mpad == Mpad && w.phi_D == a->D;
+            if (!reuse) {
                 KScope k(c, K_MEMSET, s);
                 FM_CUDA(cudaMemsetAsync(w.phic, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
                 FM_CUDA(cudaMemsetAsync(w.phict, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
             }
             {
                 KScope k(c, K_GATHER, s);
-                FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, Mpad, G, a->D, rows, w.phic, w.phict, s));
+                FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, Mpad, G, a->D, rows, w.phic, w.phict,
+                                      reuse ? 1 : 0, s));
             }
+            w.phi_valid = true;
+            w.phi_Mpad = Mpad;
+            w.phi_D = a->D;
             // K-GEMM1: z = Phic * W16^T / n; epilogue stores p~ = exp(z - m_tile) (bf16),
             // the (m_tile, sum p~) softmax partials and the taken token's logit
             CUtensorMap tA, tB, tP, tGt, tPt;
@@ -934,7 +956,8 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             }
             count_launch(5);
         } else {
-            FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, M, G, a->D, rows, nullptr, nullptr, s));
+            w.phi_valid = false;  // the row buffers no longer describe Phic's contents
+            FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, M, G, a->D, rows, nullptr, nullptr, 0, s));
             if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * 8, s));
             KScope k(c, K_PARITY, s);
             FM_CUDA(launch_parity_rows(a->W, a->V, a->D, M, rows, w.sd, G, w.zscratch, w.dWmb, w.logp64,
@@ -1132,7 +1155,11 @@ int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
     if (int st = set_dev(c)) return st;
     const size_t P = a->P;
     const size_t dwb = a->dw_valid ? P * dw_elem(a) : 0;
-    const size_t bytes = P * 16 + P * dw_elem(a);
+    // park layout: W | m | v | dW | W16.  The bf16 shadow travels on the HBM /
+    // NVLink tiers (a copy-engine copy is cheaper than regenerating it on the
+    // SMs); over PCIe it is regenerated from W on activation instead.
+    const bool park_w16 = a->W16 && tier != FM_TIER_HOST;
+    const size_t bytes = P * 16 + P * dw_elem(a) + (a->W16 ? P * 2 : 0);
     const int pdev = tier == FM_TIER_PEER ? peer_device : c->device;
     if (a->park && (a->park_tier != tier || a->park_device != pdev || a->park_bytes < bytes)) {
         FM_CUDA(cudaStreamSynchronize(c->copy_out));
@@ -1180,6 +1207,8 @@ int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
     FM_CUDA(cp(p + P * 8, a->m, P * 4));
     FM_CUDA(cp(p + P * 12, a->v, P * 4));
     if (dwb) FM_CUDA(cp(p + P * 16, a->dW, dwb));  // only mid-step gradients travel
+    if (park_w16) FM_CUDA(cp(p + P * (16 + dw_elem(a)), a->W16, P * 2));
+    a->park_w16 = park_w16;
     FM_CUDA(cudaEventRecord(a->ev_out, c->copy_out));
     agent_free_device(a, c->copy_out);
     a->active = false;
@@ -1216,12 +1245,14 @@ int fm_agent_activate(fm_agent* a, fm_ctx* c) {
     FM_CUDA(cp(a->m, p + P * 8, P * 4));
     FM_CUDA(cp(a->v, p + P * 12, P * 4));
     if (a->dw_valid) FM_CUDA(cp(a->dW, p + P * 16, P * dw_elem(a)));
-    if (a->W16) {
-        FM_CUDA(launch_to_bf16(a->W, a->W16, P, c->num_sms, c->copy_in));  // shadow regenerated, not copied
+    if (a->W16 && a->park_w16) {
+        FM_CUDA(cp(a->W16, p + P * (16 + dw_elem(a)), P * 2));
+    } else if (a->W16) {
+        FM_CUDA(launch_to_bf16(a->W, a->W16, P, c->num_sms, c->copy_in));  // shadow regenerated
         count_launch();
     }
     FM_CUDA(cudaEventRecord(a->ev_in, c->copy_in));
-    FM_CUDA(cudaStreamWaitEvent(c->stream, a->ev_in, 0));
+    a->pending_in = true;  // consumers wait lazily (check_active)
     a->ctx = c;
     a->active = true;
     return FM_OK;

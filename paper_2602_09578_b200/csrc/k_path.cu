@@ -77,13 +77,30 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
                                                      int64_t row_lo, int64_t M, int64_t Mpad, int64_t G,
                                                      uint64_t D,
                                                      RowBuffers rows, __nv_bfloat16* phic,
-                                                     __nv_bfloat16* phict) {
+                                                     __nv_bfloat16* phict, int clear_old) {
     __shared__ int64_t s_start[kMaxSamplesSmem];
     const int ns = n_samples < kMaxSamplesSmem ? n_samples : kMaxSamplesSmem;
     for (int i = threadIdx.x; i < ns; i += blockDim.x) s_start[i] = sd[i].row_start;
     __syncthreads();
     const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (r >= Mpad) return;
+    if (phic && clear_old) {
+        // Phic / Phic^T still hold the previous micro-batch's pattern (same Mpad, D):
+        // row r's thread owns row r of Phic and column r of Phic^T, so it erases its
+        // <= 4 old entries instead of a 2 x Mpad x D memset.
+        const int on = rows.n_ctx[r];
+        const int4 oc = rows.ctx4[r];
+        const int old[4] = {oc.x, oc.y, oc.z, oc.w};
+        const __nv_bfloat16 z = __float2bfloat16_rn(0.f);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (j < on) {
+                const uint64_t f = feature_of(old[j], D);
+                phic[static_cast<size_t>(r) * D + f] = z;
+                phict[static_cast<size_t>(f) * Mpad + r] = z;
+            }
+        }
+    }
     if (r >= M) {
         rows.action[r] = -1;
         rows.ctx4[r] = make_int4(-1, -1, -1, -1);
@@ -471,11 +488,12 @@ __global__ void parity_fold_kernel(double* __restrict__ dW, double* __restrict__
 // ---------------------------------------------------------------------------
 cudaError_t launch_gather(const uint8_t* arena, const SampleDesc* sd, int n_samples, int64_t row_lo, int64_t M,
                           int64_t Mpad, int64_t global_batch, uint64_t D, RowBuffers rows, __nv_bfloat16* phic,
-                          __nv_bfloat16* phict, cudaStream_t s) {
+                          __nv_bfloat16* phict, int clear_old, cudaStream_t s) {
     if (Mpad == 0) return cudaSuccess;
     if (n_samples > kMaxSamplesSmem) return cudaErrorInvalidValue;
     const int blocks = static_cast<int>((Mpad + 255) / 256);
-    gather_kernel<<<blocks, 256, 0, s>>>(arena, sd, n_samples, row_lo, M, Mpad, global_batch, D, rows, phic, phict);
+    gather_kernel<<<blocks, 256, 0, s>>>(arena, sd, n_samples, row_lo, M, Mpad, global_batch, D, rows, phic, phict,
+                                         clear_old);
     return cudaGetLastError();
 }
 
