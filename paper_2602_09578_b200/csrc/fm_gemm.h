@@ -31,7 +31,21 @@ struct GemmArgs {
     int stats_ld;
     int accumulate;          // Grad: 1 = dW += acc, 0 = dW = acc
     double* sumsq;           // Grad: += sum(acc^2) (micro-batch grad norm^2)
+    // Fused-loss path (pair MMA only):
+    //  Logits: store p~ TRANSPOSED into pexp_t [N][ldt] (rows < store_rows; zeros for M <= row)
+    __nv_bfloat16* pexp_t;
+    long long ldt;
+    int store_rows;
+    //  Grad: B tile (Phic^T counts) patched in smem to sig[t][m_tile] * count, so that
+    //  A (= p~'^T) x B' is exactly G^T x Phic; per-row features come from n_ctx / ctx4.
+    const int4* feat4;       // per token: unique features (-1 padded), from K-gather
+    const uint32_t* cnt4;    // per token: their multiplicities (8 bits each)
+    const float* sig;
+    int sig_ld;
 };
+
+// 1 when the fused-loss path (no separate K-loss kernel) is active.
+bool fused_loss_enabled();
 
 size_t gemm_smem_bytes();
 // Rows of B per TMA box: 256 (single-CTA tiles) or 128 (CTA-pair tiles, FM_GEMM_2SM != 0).

@@ -32,6 +32,8 @@ struct RowBuffers {
     float* lse;        // [Mpad]
     float* logp;       // [Mpad]
     float* coef_eff;   // [Mpad] coef * surrogate factor
+    int4* feat4;       // [Mpad] unique features of the row (-1 padded)   (tensor-core path)
+    uint32_t* cnt4;    // [Mpad] their multiplicities, 8 bits each
 };
 
 // K-gather: decode the selected records' token payloads straight out of the
@@ -46,9 +48,12 @@ cudaError_t launch_gather(const uint8_t* arena, const SampleDesc* sd, int n_samp
 // K-lse: combine GEMM1's per-tile softmax partials into lse, the taken-token
 // log-prob (from the fp32 logit GEMM1 captured) and the effective row
 // coefficient (PPO-clip surrogate optional).
+// Fused-loss path (sig != NULL): also writes sig[t][tile] = -c_t * exp(m_tile - lse_t)
+// and folds the taken token's delta into p~^T (pexp_t, leading dim ldt).
 cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int64_t M, int64_t Mpad,
                        int64_t V, const SampleDesc* sd, int64_t global_batch, RowBuffers rows,
-                       const float* old_logp, float clip_eps, double* loss_acc, cudaStream_t s);
+                       const float* old_logp, float clip_eps, double* loss_acc, float* sig,
+                       __nv_bfloat16* pexp_t, int64_t ldt, cudaStream_t s);
 
 // K-loss (fused log-softmax gradient):
 //   G^T[v][t] = coef_eff_t * (delta(v, a_t) - p~[t][v] * exp(m_tile(t, v) - lse_t))

@@ -101,6 +101,8 @@ struct Workspace {
     uint64_t vocab_cap = 0, feat_cap = 0;
     int32_t* action = nullptr;
     int4* ctx4 = nullptr;
+    int4* feat4 = nullptr;
+    uint32_t* cnt4 = nullptr;
     int32_t* n_ctx = nullptr;
     int32_t* sample = nullptr;
     float *coef = nullptr, *rscale = nullptr, *lse = nullptr, *logp = nullptr, *coef_eff = nullptr;
@@ -109,6 +111,7 @@ struct Workspace {
     __nv_bfloat16* Pexp = nullptr;  // p~ = exp(z - m_tile) [Mpad][ldz] bf16
     float* zact = nullptr;          // logit of the taken token [Mpad]
     float2* stats = nullptr;
+    float* sig = nullptr;  // fused loss: -c_t * exp(m_tile - lse_t) per (row, 256-vocab tile)
     // parity mode scratch
     int64_t prow_cap = 0;
     uint64_t pvocab_cap = 0, pparam_cap = 0;
@@ -210,6 +213,8 @@ int staging_acquire(fm_ctx* c, size_t bytes, uint8_t** out, cudaEvent_t* ev) {
 void ws_free(Workspace& w) {
     cudaFree(w.action);
     cudaFree(w.ctx4);
+    cudaFree(w.feat4);
+    cudaFree(w.cnt4);
     cudaFree(w.n_ctx);
     cudaFree(w.sample);
     cudaFree(w.coef);
@@ -224,6 +229,7 @@ void ws_free(Workspace& w) {
     cudaFree(w.Pexp);
     cudaFree(w.zact);
     cudaFree(w.stats);
+    cudaFree(w.sig);
     cudaFree(w.zscratch);
     cudaFree(w.dWmb);
     cudaFree(w.logp64);
@@ -259,6 +265,8 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
     cudaError_t e = cudaSuccess;
     e = e ? e : dalloc(&w.action, R);
     e = e ? e : dalloc(&w.ctx4, R);
+    e = e ? e : dalloc(&w.feat4, R);
+    e = e ? e : dalloc(&w.cnt4, R);
     e = e ? e : dalloc(&w.n_ctx, R);
     e = e ? e : dalloc(&w.sample, R);
     e = e ? e : dalloc(&w.coef, R);
@@ -273,6 +281,7 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
     e = e ? e : dalloc(&w.Pexp, static_cast<size_t>(R) * ldz);
     e = e ? e : dalloc(&w.zact, R);
     e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n);
+    e = e ? e : dalloc(&w.sig, static_cast<size_t>(R) * tiles_n);
     if (e != cudaSuccess) {
         ws_free(w);
         return fail(FM_ERR_DEVICE_OOM, std::string("workspace allocation: ") + cudaGetErrorString(e));
@@ -361,6 +370,8 @@ RowBuffers row_buffers(Workspace& w) {
     RowBuffers r;
     r.action = w.action;
     r.ctx4 = w.ctx4;
+    r.feat4 = w.feat4;
+    r.cnt4 = w.cnt4;
     r.n_ctx = w.n_ctx;
     r.sample = w.sample;
     r.coef = w.coef;
@@ -918,7 +929,14 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g1.N = static_cast<int>(a->V);
             g1.K = static_cast<int>(a->D);
             g1.group_m = 16;
-            g1.pexp = w.Pexp;
+            const bool fused = fused_loss_enabled();
+            if (fused) {  // p~^T straight into GEMM2's A operand buffer
+                g1.pexp_t = w.gt;
+                g1.ldt = static_cast<long long>(Mpad);
+                g1.store_rows = static_cast<int>(Mpad);
+            } else {
+                g1.pexp = w.Pexp;
+            }
             g1.zact = w.zact;
             g1.action = w.action;
             g1.ld_out = static_cast<long long>(ldz);
@@ -933,10 +951,11 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             {
                 KScope k(c, K_LSE, s);
                 FM_CUDA(launch_lse(w.zact, w.stats, tiles_n, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
-                                   a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1, s));
+                                   a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1,
+                                   fused ? w.sig : nullptr, fused ? w.gt : nullptr, Mpad, s));
             }
-            // K-softmax-grad: G^T tiles (zero for padding rows)
-            {
+            // K-softmax-grad: G^T tiles (zero for padding rows) — folded into GEMM2 when fused
+            if (!fused) {
                 KScope k(c, K_SOFTMAX_GRAD, s);
                 FM_CUDA(launch_softmax_grad(tP, tGt, w.stats, tiles_n, Mpad, static_cast<int64_t>(a->V), rows, s));
             }
@@ -950,11 +969,17 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g2.ld_out = static_cast<long long>(a->D);
             g2.accumulate = a->dw_valid ? 1 : 0;
             g2.sumsq = scal;
+            if (fused) {  // B' = sig[t][m_tile] * Phic^T, built in smem by the transform warp
+                g2.sig = w.sig;  // sig^T [tiles_n][Mpad]
+                g2.sig_ld = static_cast<int>(Mpad);
+                g2.feat4 = w.feat4;
+                g2.cnt4 = w.cnt4;
+            }
             {
                 KScope k(c, K_GEMM2, s);
                 FM_CUDA(gemm_tn_launch(GemmKind::Grad, tGt, tPt, g2, c->num_sms, s));
             }
-            count_launch(5);
+            count_launch(fused ? 4 : 5);
         } else {
             w.phi_valid = false;  // the row buffers no longer describe Phic's contents
             FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, M, G, a->D, rows, nullptr, nullptr, 0, s));

@@ -104,6 +104,10 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
     if (r >= M) {
         rows.action[r] = -1;
         rows.ctx4[r] = make_int4(-1, -1, -1, -1);
+        if (rows.feat4) {
+            rows.feat4[r] = make_int4(-1, -1, -1, -1);
+            rows.cnt4[r] = 0u;
+        }
         rows.n_ctx[r] = 0;
         rows.sample[r] = -1;
         rows.coef[r] = 0.f;
@@ -143,15 +147,29 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
         uint64_t f[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) f[j] = j < n ? feature_of(ctx[j], D) : ~0ull;
+        int uf[4] = {-1, -1, -1, -1};
+        uint32_t packed = 0u;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if (j >= n) continue;
             int cnt = 0;
+            bool first = true;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) cnt += (f[k] == f[j]);
+            for (int k = 0; k < 4; ++k) {
+                cnt += (f[k] == f[j]);
+                if (k < j && f[k] == f[j]) first = false;
+            }
             const __nv_bfloat16 c = __float2bfloat16_rn(static_cast<float>(cnt));  // exact: 1..4
             phic[static_cast<size_t>(r) * D + f[j]] = c;
             phict[static_cast<size_t>(f[j]) * Mpad + r] = c;
+            if (first) {  // unique features + counts for the fused-loss B transform
+                uf[j] = static_cast<int>(f[j]);
+                packed |= static_cast<uint32_t>(cnt) << (8 * j);
+            }
+        }
+        if (rows.feat4) {
+            rows.feat4[r] = make_int4(uf[0], uf[1], uf[2], uf[3]);
+            rows.cnt4[r] = packed;
         }
     }
 }
@@ -164,7 +182,8 @@ __global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ zact
                                                   int64_t M, int64_t Mpad, int64_t V,
                                                   const SampleDesc* __restrict__ sd, int64_t G,
                                                   RowBuffers rows, const float* old_logp,
-                                                  float clip_eps, double* loss_acc) {
+                                                  float clip_eps, double* loss_acc, float* sig,
+                                                  __nv_bfloat16* pexp_t, int64_t ldt) {
     __shared__ double red[8];
     const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -176,6 +195,8 @@ __global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ zact
                 rows.logp[r] = 0.f;
                 rows.coef_eff[r] = 0.f;
             }
+            if (sig)
+                for (int j = lane; j < stats_ld; j += 32) sig[static_cast<size_t>(j) * Mpad + r] = 0.f;
         } else {
             float m = -INFINITY, s = 0.f;
             const float2* st = stats + static_cast<size_t>(r) * stats_ld;
@@ -211,6 +232,21 @@ __global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ zact
                 rows.logp[r] = lp;
                 rows.coef_eff[r] = ce;
                 loss = valid ? -(adv / static_cast<double>(G)) * static_cast<double>(lp) : 0.0;
+                if (sig && valid && ce != 0.f) {  // sig is stored transposed: sig^T[tile][t], ld = Mpad
+                    // fold the taken token's delta into A: p~' = p~ - exp(lse - m_tile), so that
+                    // sig * p~' = -c * (p - delta) = G  (GEMM2 applies sig through its B operand)
+                    const int pt = a / 256;
+                    const float e = __expf(fminf(lse - st[pt].x, 80.f));
+                    __nv_bfloat16* q = pexp_t + static_cast<size_t>(a) * ldt + r;
+                    *q = __float2bfloat16_rn(__bfloat162float(*q) - e);
+                }
+            }
+            if (sig) {
+                // sig[t][tile] = -c_t * exp(m_tile - lse_t): the per-(row, 256-vocab tile) scale
+                const float lse = __shfl_sync(0xffffffffu, m + logf(s), 0);
+                const float ce = __shfl_sync(0xffffffffu, lane == 0 ? rows.coef_eff[r] : 0.f, 0);
+                for (int j = lane; j < stats_ld; j += 32)
+                    sig[static_cast<size_t>(j) * Mpad + r] = ce == 0.f ? 0.f : -ce * __expf(st[j].x - lse);
             }
         }
     }
@@ -499,11 +535,12 @@ cudaError_t launch_gather(const uint8_t* arena, const SampleDesc* sd, int n_samp
 
 cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int64_t M, int64_t Mpad, int64_t V,
                        const SampleDesc* sd, int64_t global_batch, RowBuffers rows, const float* old_logp,
-                       float clip_eps, double* loss_acc, cudaStream_t s) {
+                       float clip_eps, double* loss_acc, float* sig, __nv_bfloat16* pexp_t, int64_t ldt,
+                       cudaStream_t s) {
     if (Mpad == 0) return cudaSuccess;
     const int blocks = static_cast<int>((Mpad * 32 + 255) / 256);
     lse_kernel<<<blocks, 256, 0, s>>>(zact, stats, stats_ld, M, Mpad, V, sd, global_batch, rows, old_logp, clip_eps,
-                                      loss_acc);
+                                      loss_acc, sig, pexp_t, ldt);
     return cudaGetLastError();
 }
 
