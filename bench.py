@@ -39,6 +39,18 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+# The driver parses ONE JSON line from stdout.  Native libraries (NCCL's
+# version banner, warnings) also write to fd 1, so main() points fd 1 at
+# stderr and keeps a private duplicate of the real stdout for the result.
+_RESULT_OUT = None
+
+
+def emit(obj: dict) -> None:
+    out = _RESULT_OUT or sys.stdout
+    out.write(json.dumps(obj) + "\n")
+    out.flush()
+
+
 def load_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -128,6 +140,13 @@ class Dist:
         self.dist.all_reduce(t)
         return float(t[0])
 
+    def all_gather_obj(self, obj):
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
     def bcast_obj(self, obj, src: int):
         if self.world == 1:
             return obj
@@ -204,9 +223,28 @@ def run_ours(args, dist: Dist) -> dict | None:
         w0 = seeded_weights(cfg.vocab, cfg.feat, agent_seed(cfg.seed, a)).reshape(-1)
         check(L.fm_agent_set_weights(h, w0.ctypes.data))
         del w0
-        gang = place[a]
-        check(L.fm_agent_set_shard(h, gang.index(dist.rank), len(gang)))
         handles[a] = h
+    # --- DP gangs: fused GEMM2 -> NVLink reduce-scatter + sharded Adam (default),
+    #     or token shards + NCCL all-reduce + replicated Adam (--dp-mode allreduce)
+    for a in agents:
+        gang = place[a]
+        if len(gang) < 2:
+            continue
+        h = handles.get(a)
+        blob = b""
+        if h is not None:
+            if args.dp_mode == "gang":
+                n = C.c_uint64()
+                check(L.fm_gang_attach(h, comms[a], None, 0, C.byref(n)))
+                buf = (C.c_uint8 * n.value)()
+                check(L.fm_gang_attach(h, comms[a], buf, n.value, C.byref(n)))
+                blob = bytes(buf)
+            else:
+                check(L.fm_agent_set_shard(h, gang.index(dist.rank), len(gang)))
+        blobs = dist.all_gather_obj(blob)
+        if h is not None and args.dp_mode == "gang":
+            gang_blobs = b"".join(blobs[r] for r in gang)
+            check(L.fm_gang_connect(h, gang_blobs, len(blob)))
 
     # --- experience: every step's samples resident in the token arena, indexed
     #     by the host experience store (rollout-side production, untimed)
@@ -492,7 +530,7 @@ def run_reference(args, dist: Dist):
         return
     cfg = wl.CONFIGS[args.config]
     if not orc.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmarlsim_ref.so not built"}), flush=True)
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libmarlsim_ref.so not built"})
         return
     threads = ref_threads(cfg)
     tpt = args.ref_tokens
@@ -515,7 +553,7 @@ def run_reference(args, dist: Dist):
            "cpu_baseline": {"value": v, "unit": "trained tokens/s", "cores": threads, "kind": "reference",
                             "sample": sample},
            "e2e": {"value": v, "unit": "trained tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 METRIC = "trained tokens/sec (policy-update micro-batches) at 1/2/4/8 B200 vs CPU ref"
@@ -535,6 +573,10 @@ def config_obj(cfg, args) -> dict:
 
 
 def main():
+    global _RESULT_OUT
+    sys.stdout.flush()
+    _RESULT_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -548,6 +590,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--host-breakdown", action="store_true")
     ap.add_argument("--agents", type=int, default=0, help="use only the first K agents of the config")
+    ap.add_argument("--dp-mode", default="gang", choices=["gang", "allreduce"],
+                    help="gang: fused GEMM2 reduce-scatter over NVLink + sharded Adam; allreduce: NCCL")
     args = ap.parse_args()
     dist = Dist()
     try:
@@ -574,7 +618,7 @@ def main():
                    "config": config_obj(cfg, args), "roofline": res["roofline"], "kernels": res["kernels"],
                    "cpu_baseline": cpu, "e2e": res["e2e"], "gpu_launches": int(res["launches"]),
                    "clocks": res["clocks"]}
-            print(json.dumps(out), flush=True)
+            emit(out)
     finally:
         dist.close()
 

@@ -246,8 +246,18 @@ int fm_group_advantages(fm_ctx* ctx, const double* rewards, const int32_t* seg_o
 int fm_comm_unique_id(uint8_t out[128]);
 int fm_comm_create(fm_ctx* ctx, const uint8_t id[128], int nranks, int rank, fm_comm** out);
 int fm_comm_destroy(fm_comm* c);
-/* Sum the agent's gradient accumulator across the gang (before fm_apply_update). */
+/* Sum the agent's gradient accumulator across the gang (before fm_apply_update).
+ * A no-op for agents attached with fm_gang_attach (reduced inside GEMM2). */
 int fm_agent_allreduce_grad(fm_agent* a, fm_comm* c);
+/* Fused GEMM2 -> reduce-scatter over NVLink peer memory + sharded Adam with
+ * the bf16 all-gather fused into it.  attach writes this rank's
+ * export blob (blob_out NULL -> just *len); the caller all-gathers the blobs
+ * across the gang (any side channel) and passes them, in rank order, to
+ * connect.  While attached the agent trains token-balanced row shards and its
+ * master W / m / v rows outside its own shard are not maintained. */
+int fm_gang_attach(fm_agent* a, fm_comm* c, uint8_t* blob_out, uint64_t cap, uint64_t* len);
+int fm_gang_connect(fm_agent* a, const uint8_t* blobs, uint64_t blob_len);
+int fm_gang_detach(fm_agent* a);
 
 /* ---- experience store host control plane (experience_store.hpp:19-276) ---- */
 int fm_store_create(fm_store** out);

@@ -93,6 +93,9 @@ _PROTOS = {
     "fm_comm_create": (I, [P, P, I, I, C.POINTER(P)]),
     "fm_comm_destroy": (I, [P]),
     "fm_agent_allreduce_grad": (I, [P, P]),
+    "fm_gang_attach": (I, [P, P, P, U64, PU64]),
+    "fm_gang_connect": (I, [P, P, U64]),
+    "fm_gang_detach": (I, [P]),
     "fm_publish_weights": (I, [P, I, C.POINTER(P)]),
     "fm_weights_alloc": (I, [P, U64, U64, I, C.POINTER(P)]),
     "fm_weights_info": (I, [P, PI64, PU64, PU64, C.POINTER(C.c_int), PU64, C.POINTER(C.c_int)]),

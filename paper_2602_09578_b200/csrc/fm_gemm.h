@@ -42,10 +42,19 @@ struct GemmArgs {
     const uint32_t* cnt4;    // per token: their multiplicities (8 bits each)
     const float* sig;
     int sig_ld;
+    // Grad, DP-gang exchange (xg > 1): rows [xlo[o], xlo[o+1]) are owned by gang
+    // rank o; rows owned by another rank are written (whole partial) into
+    // xpeer[o] = this rank's receive slot in rank o's buffer (NVLink P2P).
+    int xg = 0;
+    int xrank = 0;
+    int xlo[9] = {};
+    float* xpeer[8] = {};
 };
 
 // 1 when the fused-loss path (no separate K-loss kernel) is active.
 bool fused_loss_enabled();
+// 1 when the CTA-pair (cta_group::2) kernels are in use (required by the DP gang exchange).
+bool gemm_pair_mode();
 
 size_t gemm_smem_bytes();
 // Rows of B per TMA box: 256 (single-CTA tiles) or 128 (CTA-pair tiles, FM_GEMM_2SM != 0).

@@ -73,6 +73,19 @@ cudaError_t launch_adam(double* w, float* m, float* v, G* g, __nv_bfloat16* w16,
 cudaError_t launch_to_bf16(const double* w, __nv_bfloat16* w16, uint64_t n, int num_sms,
                            cudaStream_t s);
 
+// Peer W16 row-range pointers (NVLink-mapped) of a DP gang, excluding self.
+struct ShardPeers {
+    int n;
+    __nv_bfloat16* w16[7];
+};
+// K-adam, sharded over a DP gang: this rank's rows only; gradient = local
+// partial + the receive slots the peers filled from their GEMM2 epilogues;
+// the new bf16 rows are written locally and into every peer's W16.
+cudaError_t launch_adam_shard(double* w, float* m, float* v, const float* g, const float* recv, int nslots,
+                              uint64_t slot_stride, __nv_bfloat16* w16, ShardPeers peers, uint64_t n,
+                              double lr, double b1, double b2, double eps, double bc1, double bc2,
+                              double* gsq, int num_sms, cudaStream_t s);
+
 // K-adv (training.hpp:54-67): one warp per reward group, fp64 shuffle reductions.
 cudaError_t launch_group_advantages(const double* rewards, const int32_t* seg_off, int nseg,
                                     double eps, double* out, cudaStream_t s);

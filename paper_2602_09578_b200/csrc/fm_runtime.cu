@@ -596,6 +596,36 @@ uint64_t fm_arena_used(const fm_ctx* c) { return c->arena_used; }
 // ===========================================================================
 // agents
 // ===========================================================================
+// DP gang of an agent with the fused reduce-scatter: V rows are
+// split into g contiguous, 256-row-aligned shards; during the step's last
+// micro-batch GEMM2 writes the partials of rows owned by another rank into
+// that rank's receive slot over NVLink (IPC-mapped), then each rank runs the
+// sharded Adam on its rows and writes the new bf16 rows into every peer's
+// W16.  Two 1-element NCCL all-reduces on the compute stream serve as the
+// device-side barriers (after the exchange; the update grad-norm reduction
+// after Adam), so no host round trip or spin-wait is involved.
+#define FM_NCCL(expr)                                                                          \
+    do {                                                                                       \
+        ncclResult_t _r = (expr);                                                              \
+        if (_r != ncclSuccess) return fail(FM_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+    } while (0)
+
+struct fm_comm;
+struct GangState;
+static ncclComm_t gang_comm(GangState* gs);
+struct GangState {
+    fm_comm* comm = nullptr;
+    int rank = 0, g = 1;
+    int64_t lo[9] = {};          // row boundaries of the shards
+    float* recv = nullptr;       // [g-1][own_rows][D] partials from the peers
+    float* peer_slot[8] = {};    // my slot inside peer o's receive buffer
+    __nv_bfloat16* peer_w16[8] = {};
+    void* opened[16] = {};       // IPC mappings to close
+    int nopened = 0;
+    int* d_token = nullptr;      // 1-int all-reduce used as a device barrier
+    bool connected = false;
+};
+
 struct fm_agent {
     fm_ctx* ctx = nullptr;  // GPU the agent is bound to (null while suspended)
     std::string name;
@@ -634,7 +664,11 @@ struct fm_agent {
     size_t park_bytes = 0;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_compute = nullptr;
     Slot* slot = nullptr;
+    GangState* gang = nullptr;
 };
+
+// Device-side barrier across the gang (defined with the NCCL section below).
+static int gang_barrier(fm_agent* a);
 
 namespace {
 
@@ -757,6 +791,7 @@ int fm_agent_create(fm_ctx* c, const char* name, uint64_t V, uint64_t D, int pre
 
 int fm_agent_destroy(fm_agent* a) {
     if (!a) return FM_OK;
+    fm_gang_detach(a);
     if (a->ctx) {
         cudaSetDevice(a->ctx->device);
         cudaStreamSynchronize(a->ctx->stream);
@@ -975,9 +1010,21 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 g2.feat4 = w.feat4;
                 g2.cnt4 = w.cnt4;
             }
+            const bool exchange = a->gang && a->gang->connected && a->samples + n == G;
+            if (exchange) {  // last micro-batch of the step: reduce-scatter inside the epilogue
+                GangState* gs = a->gang;
+                g2.xg = gs->g;
+                g2.xrank = gs->rank;
+                for (int o = 0; o <= gs->g; ++o) g2.xlo[o] = static_cast<int>(gs->lo[o]);
+                for (int o = 0; o < gs->g; ++o) g2.xpeer[o] = gs->peer_slot[o];
+            }
             {
                 KScope k(c, K_GEMM2, s);
                 FM_CUDA(gemm_tn_launch(GemmKind::Grad, tGt, tPt, g2, c->num_sms, s));
+            }
+            if (exchange) {
+                a->dw_valid = true;
+                if (int st = gang_barrier(a)) return st;  // every rank's partials have landed
             }
             count_launch(fused ? 4 : 5);
         } else {
@@ -991,6 +1038,19 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             count_launch(3);
         }
         a->dw_valid = true;
+    } else if (a->gang && a->gang->connected && a->samples + n == G) {
+        // this rank got no rows of the step's last micro-batch: ship its partials
+        // for the peers' rows with plain NVLink copies, then join the barrier
+        GangState* gs = a->gang;
+        if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * 4, s));
+        for (int o = 0; o < gs->g; ++o) {
+            if (o == gs->rank) continue;
+            const size_t rows = static_cast<size_t>(gs->lo[o + 1] - gs->lo[o]);
+            FM_CUDA(cudaMemcpyAsync(gs->peer_slot[o], static_cast<float*>(a->dW) + gs->lo[o] * a->D,
+                                    rows * a->D * 4, cudaMemcpyDeviceToDevice, s));
+        }
+        a->dw_valid = true;
+        if (int st = gang_barrier(a)) return st;
     }
     a->have_old_logp = false;  // old log-probs apply to one micro-batch
     a->last_rows = M;
@@ -1151,6 +1211,19 @@ int fm_apply_update(fm_agent* a, int64_t G, double lr, double b1, double b2, dou
     if (a->precision == FM_PRECISION_PARITY_F64) {
         FM_CUDA(launch_adam<double>(a->W, a->m, a->v, static_cast<double*>(a->dW), nullptr, a->P, lr, b1, b2, eps,
                                     bc1, bc2, 1, a->d_upd, c->num_sms, s));
+    } else if (a->gang && a->gang->connected) {
+        // sharded Adam over this rank's rows; W16 rows all-gathered by peer stores
+        GangState* gs = a->gang;
+        const int64_t r0 = gs->lo[gs->rank], r1 = gs->lo[gs->rank + 1];
+        const uint64_t off = static_cast<uint64_t>(r0) * a->D, n_own = static_cast<uint64_t>(r1 - r0) * a->D;
+        ShardPeers peers{};
+        for (int o = 0; o < gs->g; ++o)
+            if (o != gs->rank) peers.w16[peers.n++] = gs->peer_w16[o] + off;
+        FM_CUDA(launch_adam_shard(a->W + off, a->m + off, a->v + off, static_cast<float*>(a->dW) + off, gs->recv,
+                                  gs->g - 1, n_own, a->W16 + off, peers, n_own, lr, b1, b2, eps, bc1, bc2, a->d_upd,
+                                  c->num_sms, s));
+        // global grad norm^2; doubles as the barrier after the peers' W16 writes
+        FM_NCCL(ncclAllReduce(a->d_upd, a->d_upd, 1, ncclFloat64, ncclSum, gang_comm(gs), s));
     } else {
         // the next step's first GEMM2 overwrites dW, so no zeroing pass here
         FM_CUDA(launch_adam<float>(a->W, a->m, a->v, static_cast<float*>(a->dW), a->W16, a->P, lr, b1, b2, eps,
@@ -1176,6 +1249,7 @@ int fm_apply_update(fm_agent* a, int64_t G, double lr, double b1, double b2, dou
 int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
     FM_GUARD_BEGIN
     if (int st = check_active(a)) return st;
+    if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang (fm_gang_detach first)");
     fm_ctx* c = a->ctx;
     if (int st = set_dev(c)) return st;
     const size_t P = a->P;
@@ -1388,8 +1462,125 @@ int fm_comm_destroy(fm_comm* c) {
     return FM_OK;
 }
 
+}  // extern "C"
+
+static ncclComm_t gang_comm(GangState* gs) { return gs->comm->comm; }
+
+static int gang_barrier(fm_agent* a) {
+    GangState* gs = a->gang;
+    FM_NCCL(ncclAllReduce(gs->d_token, gs->d_token, 1, ncclInt32, ncclSum, gs->comm->comm, a->ctx->stream));
+    return FM_OK;
+}
+
+namespace {
+struct GangBlob {
+    int32_t rank;
+    int32_t pad;
+    cudaIpcMemHandle_t recv;
+    cudaIpcMemHandle_t slot;
+    uint64_t w16_off;
+};
+}  // namespace
+
+extern "C" {
+
+// Puts the agent into a DP gang with the fused reduce-scatter (see GangState).
+// Writes this rank's export blob (IPC handles of its receive buffer and of
+// its training slot's bf16 shadow) for the caller to all-gather across the
+// gang and hand to fm_gang_connect.  The agent must stay resident (no
+// suspend) while attached.
+int fm_gang_attach(fm_agent* a, fm_comm* cm, uint8_t* blob_out, uint64_t cap, uint64_t* len) {
+    FM_GUARD_BEGIN
+    *len = sizeof(GangBlob);
+    if (!blob_out) return FM_OK;
+    if (cap < sizeof(GangBlob)) return fail(FM_ERR_INVALID_ARG, "blob buffer too small");
+    if (int st = check_active(a)) return st;
+    if (a->precision != FM_PRECISION_BF16_TC) return fail(FM_ERR_CONFIG_ERROR, "gang exchange needs the tensor-core path");
+    if (cm->ctx != a->ctx) return fail(FM_ERR_CONFIG_ERROR, "communicator bound to another GPU");
+    if (cm->nranks < 2 || cm->nranks > 8) return fail(FM_ERR_CONFIG_ERROR, "gang size must be 2..8");
+    if (!gemm_pair_mode()) return fail(FM_ERR_CONFIG_ERROR, "gang exchange needs the CTA-pair GEMM (FM_GEMM_2SM)");
+    if (int st = set_dev(a->ctx)) return st;
+    auto* gs = new GangState();
+    gs->comm = cm;
+    gs->rank = cm->rank;
+    gs->g = cm->nranks;
+    const int64_t tiles = static_cast<int64_t>((a->V + 255) / 256);
+    for (int o = 0; o <= gs->g; ++o)
+        gs->lo[o] = std::min<int64_t>(static_cast<int64_t>(a->V), (tiles * o / gs->g) * 256);
+    int64_t max_rows = 0;
+    for (int o = 0; o < gs->g; ++o) max_rows = std::max(max_rows, gs->lo[o + 1] - gs->lo[o]);
+    const int64_t own = gs->lo[gs->rank + 1] - gs->lo[gs->rank];
+    const size_t rbytes = static_cast<size_t>(gs->g - 1) * std::max<int64_t>(own, 1) * a->D * 4;
+    if (cudaMalloc(&gs->recv, rbytes) != cudaSuccess) {
+        delete gs;
+        return fail(FM_ERR_DEVICE_OOM, "gang receive buffer");
+    }
+    FM_CUDA(cudaMalloc(&gs->d_token, sizeof(int)));
+    FM_CUDA(cudaMemset(gs->d_token, 0, sizeof(int)));
+    GangBlob b{};
+    b.rank = gs->rank;
+    FM_CUDA(cudaIpcGetMemHandle(&b.recv, gs->recv));
+    FM_CUDA(cudaIpcGetMemHandle(&b.slot, a->slot->base));
+    b.w16_off = static_cast<uint64_t>(reinterpret_cast<uint8_t*>(a->W16) - static_cast<uint8_t*>(a->slot->base));
+    std::memcpy(blob_out, &b, sizeof(b));
+    a->gang = gs;
+    a->shard_rank = gs->rank;  // token-balanced row shards of every micro-batch
+    a->shard_count = gs->g;
+    a->dp = true;
+    return FM_OK;
+    FM_GUARD_END
+}
+
+// blobs: the gang's export blobs in rank order (nranks x blob_len bytes).
+int fm_gang_connect(fm_agent* a, const uint8_t* blobs, uint64_t blob_len) {
+    FM_GUARD_BEGIN
+    GangState* gs = a->gang;
+    if (!gs) return fail(FM_ERR_CONFIG_ERROR, "fm_gang_attach first");
+    if (blob_len != sizeof(GangBlob)) return fail(FM_ERR_INVALID_ARG, "blob size mismatch");
+    if (int st = set_dev(a->ctx)) return st;
+    for (int o = 0; o < gs->g; ++o) {
+        GangBlob b;
+        std::memcpy(&b, blobs + o * blob_len, sizeof(b));
+        if (b.rank != o) return fail(FM_ERR_INVALID_ARG, "blobs must be in rank order");
+        if (o == gs->rank) continue;
+        void* rbase = nullptr;
+        void* sbase = nullptr;
+        FM_CUDA(cudaIpcOpenMemHandle(&rbase, b.recv, cudaIpcMemLazyEnablePeerAccess));
+        FM_CUDA(cudaIpcOpenMemHandle(&sbase, b.slot, cudaIpcMemLazyEnablePeerAccess));
+        gs->opened[gs->nopened++] = rbase;
+        gs->opened[gs->nopened++] = sbase;
+        // my slot in o's receive buffer: senders in rank order, skipping o itself
+        const int idx = gs->rank < o ? gs->rank : gs->rank - 1;
+        const int64_t o_rows = gs->lo[o + 1] - gs->lo[o];
+        gs->peer_slot[o] = static_cast<float*>(rbase) + static_cast<size_t>(idx) * o_rows * a->D;
+        gs->peer_w16[o] = reinterpret_cast<__nv_bfloat16*>(static_cast<uint8_t*>(sbase) + b.w16_off);
+    }
+    gs->connected = true;
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int fm_gang_detach(fm_agent* a) {
+    GangState* gs = a->gang;
+    if (!gs) return FM_OK;
+    if (a->ctx) {
+        cudaSetDevice(a->ctx->device);
+        cudaStreamSynchronize(a->ctx->stream);
+    }
+    for (int i = 0; i < gs->nopened; ++i) cudaIpcCloseMemHandle(gs->opened[i]);
+    cudaFree(gs->recv);
+    cudaFree(gs->d_token);
+    delete gs;
+    a->gang = nullptr;
+    a->shard_rank = 0;
+    a->shard_count = 1;
+    a->dp = false;
+    return FM_OK;
+}
+
 int fm_agent_allreduce_grad(fm_agent* a, fm_comm* cm) {
     if (int st = check_active(a)) return st;
+    if (a->gang && a->gang->connected) return FM_OK;  // already reduced inside the last GEMM2
     if (cm->ctx != a->ctx) return fail(FM_ERR_CONFIG_ERROR, "communicator bound to another GPU");
     fm_ctx* c = a->ctx;
     if (int st = set_dev(c)) return st;

@@ -143,11 +143,69 @@ struct GradEpi {
     double sumsq;
     __device__ __forceinline__ void pass1(const GemmArgs&, int, int, uint32_t (&)[32]) {}
     __device__ __forceinline__ void begin(const GemmArgs&, int) {}
+    float* xbuf = nullptr;  // per-warp 32 x 36 fp32 smem staging (exchange mode)
+
+    // Warp-cooperative: lane = row holds 32 columns; transpose through smem so
+    // each store instruction writes 4 whole 128-B rows (8 lanes x 16 B per
+    // row) — NVLink moves full lines instead of 16-B fragments.
+    __device__ __forceinline__ void remote_chunk(const GemmArgs& a, int row, int col0, uint32_t (&r)[32], int o) {
+        const uint32_t lane = threadIdx.x & 31;
+        const int nvalid = min(32, a.N - col0);
+        const bool vrow = row < a.M && nvalid > 0;
+        const float* src = a.out + static_cast<size_t>(row) * a.ld_out + col0;
+        float part = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+            float4 acc = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                     __uint_as_float(r[j + 3]));
+            if (vrow && j < nvalid) {
+                part += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
+                if (a.accumulate) {
+                    const float4 o4 = *reinterpret_cast<const float4*>(src + j);
+                    acc.x += o4.x;
+                    acc.y += o4.y;
+                    acc.z += o4.z;
+                    acc.w += o4.w;
+                }
+            }
+            *reinterpret_cast<float4*>(xbuf + lane * 36 + j) = acc;
+        }
+        sumsq += static_cast<double>(part);
+        __syncwarp();
+        const int row0 = row - static_cast<int>(lane);
+        const int seg = static_cast<int>(lane & 7);
+        float* base = a.xpeer[o] + static_cast<size_t>(col0) + static_cast<size_t>(seg) * 4;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int rr = i * 4 + static_cast<int>(lane >> 3);
+            const int rg = row0 + rr;
+            if (rg < a.M && seg * 4 < nvalid) {
+                const float4 q = *reinterpret_cast<const float4*>(xbuf + rr * 36 + seg * 4);
+                *reinterpret_cast<float4*>(base + static_cast<size_t>(rg - a.xlo[o]) * a.ld_out) = q;
+            }
+        }
+        __syncwarp();
+    }
     __device__ __forceinline__ void chunk(const GemmArgs& a, int row, int col0, uint32_t (&r)[32]) {
+        if (a.xg > 1) {
+            // DP gang exchange (last micro-batch of the step): rows owned by another rank
+            // get this rank's whole partial (previous micro-batches + this tile) written
+            // straight into the owner's receive slot over NVLink — the reduce-scatter
+            // happens inside the GEMM epilogue, overlapped with the next tile's MMAs.
+            // Owner shards are 256-row aligned, so a warp's 32 rows share one owner.
+            int o = 0;
+#pragma unroll 1
+            while (o + 1 < a.xg && row >= a.xlo[o + 1]) ++o;
+            if (o != a.xrank) {
+                remote_chunk(a, row, col0, r, o);
+                return;
+            }
+        }
         if (row >= a.M) return;
         const int nvalid = min(32, a.N - col0);
         if (nvalid <= 0) return;
-        float* dst = a.out + static_cast<size_t>(row) * a.ld_out + col0;
+        const float* src = a.out + static_cast<size_t>(row) * a.ld_out + col0;  // this rank's partial
+        float* dst = const_cast<float*>(src);
         float part = 0.f;
         if (nvalid == 32) {
 #pragma unroll
@@ -156,11 +214,11 @@ struct GradEpi {
                                          __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
                 part += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
                 if (a.accumulate) {
-                    const float4 o = *reinterpret_cast<const float4*>(dst + j);
-                    acc.x += o.x;
-                    acc.y += o.y;
-                    acc.z += o.z;
-                    acc.w += o.w;
+                    const float4 o4 = *reinterpret_cast<const float4*>(src + j);
+                    acc.x += o4.x;
+                    acc.y += o4.y;
+                    acc.z += o4.z;
+                    acc.w += o4.w;
                 }
                 *reinterpret_cast<float4*>(dst + j) = acc;
             }
@@ -170,7 +228,7 @@ struct GradEpi {
                 if (j < nvalid) {
                     const float acc = __uint_as_float(r[j]);
                     part += acc * acc;
-                    dst[j] = a.accumulate ? dst[j] + acc : acc;
+                    dst[j] = a.accumulate ? src[j] + acc : acc;
                 }
             }
         }
@@ -403,6 +461,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     uint64_t* tfull = ready + P_STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* xscratch = reinterpret_cast<float*>(tmem_slot + 4);  // 4 warps x 32 x 36 fp32 (16-B aligned)
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
@@ -541,6 +600,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         const int row_in_tile = static_cast<int>(rank * 128 + quad * 32 + lane);
         const uint32_t tempty_leader[2] = {mapa_shared(&tempty[0], 0), mapa_shared(&tempty[1], 0)};
         Epi epi;
+        if constexpr (std::is_same_v<Epi, GradEpi>) epi.xbuf = xscratch + quad * 32 * 36;
         int acc = 0;
         uint32_t acc_phase = 0;
         double sumsq_total = 0.0;
@@ -616,10 +676,13 @@ namespace {
 }  // namespace
 
 size_t gemm_smem_bytes() {
-    return use_pair_mma() ? P_STAGES * (P_STAGE_BYTES + META_BYTES) + 1024 + 512 : STAGES * STAGE_BYTES + 1024 + 256;
+    return use_pair_mma() ? P_STAGES * (P_STAGE_BYTES + META_BYTES) + 1024 + 512 + 4 * 32 * 36 * 4
+                          : STAGES * STAGE_BYTES + 1024 + 256;
 }
 
 uint32_t gemm_b_box_rows() { return use_pair_mma() ? 128u : static_cast<uint32_t>(BN); }
+
+bool gemm_pair_mode() { return use_pair_mma(); }
 
 cudaError_t gemm_tn_launch(GemmKind kind, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const GemmArgs& args, int num_sms, cudaStream_t stream) {

@@ -405,6 +405,65 @@ __global__ void __launch_bounds__(256) adam_kernel(double* __restrict__ w, float
     }
 }
 
+// Sharded Adam of a DP gang rank over its own rows (n elements from the row
+// range's start): g = local partial + the partials the other ranks wrote into
+// this rank's receive slots during their last GEMM2; the new bf16 shadow rows
+// go to the local W16 and, over NVLink, to every other rank's W16 (the
+// all-gather fused into the optimizer).
+__global__ void __launch_bounds__(256) adam_shard_kernel(double* __restrict__ w, float* __restrict__ m,
+                                                         float* __restrict__ v, const float* __restrict__ g,
+                                                         const float* __restrict__ recv, int nslots,
+                                                         uint64_t slot_stride, __nv_bfloat16* __restrict__ w16,
+                                                         ShardPeers peers, uint64_t n, double lr, double b1,
+                                                         double b2, double eps, double bc1, double bc2,
+                                                         double* gsq) {
+    __shared__ double red[8];
+    double acc = 0.0;
+    const uint64_t n4 = n / 4;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        double4 wv = reinterpret_cast<double4*>(w)[i];
+        float4 mv = reinterpret_cast<float4*>(m)[i];
+        float4 vv = reinterpret_cast<float4*>(v)[i];
+        float4 gv = reinterpret_cast<const float4*>(g)[i];
+        for (int s = 0; s < nslots; ++s) {
+            const float4 r = reinterpret_cast<const float4*>(recv + s * slot_stride)[i];
+            gv.x += r.x;
+            gv.y += r.y;
+            gv.z += r.z;
+            gv.w += r.w;
+        }
+        acc += adam_one(wv.x, mv.x, vv.x, gv.x, lr, b1, b2, eps, bc1, bc2);
+        acc += adam_one(wv.y, mv.y, vv.y, gv.y, lr, b1, b2, eps, bc1, bc2);
+        acc += adam_one(wv.z, mv.z, vv.z, gv.z, lr, b1, b2, eps, bc1, bc2);
+        acc += adam_one(wv.w, mv.w, vv.w, gv.w, lr, b1, b2, eps, bc1, bc2);
+        reinterpret_cast<double4*>(w)[i] = wv;
+        reinterpret_cast<float4*>(m)[i] = mv;
+        reinterpret_cast<float4*>(v)[i] = vv;
+        __nv_bfloat162 lo = __floats2bfloat162_rn(static_cast<float>(wv.x), static_cast<float>(wv.y));
+        __nv_bfloat162 hi = __floats2bfloat162_rn(static_cast<float>(wv.z), static_cast<float>(wv.w));
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        reinterpret_cast<uint2*>(w16)[i] = pk;
+        for (int p = 0; p < peers.n; ++p) reinterpret_cast<uint2*>(peers.w16[p])[i] = pk;
+    }
+    const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (gid < n - n4 * 4) {
+        const uint64_t i = n4 * 4 + gid;
+        float gi = g[i];
+        for (int s = 0; s < nslots; ++s) gi += recv[s * slot_stride + i];
+        acc += adam_one(w[i], m[i], v[i], gi, lr, b1, b2, eps, bc1, bc2);
+        const __nv_bfloat16 b = __float2bfloat16_rn(static_cast<float>(w[i]));
+        w16[i] = b;
+        for (int p = 0; p < peers.n; ++p) peers.w16[p][i] = b;
+    }
+    if (gsq) {
+        const double tot = block_sum(acc, red);
+        if (threadIdx.x == 0) atomicAdd(gsq, tot);
+    }
+}
+
 __global__ void to_bf16_kernel(const double* __restrict__ w, __nv_bfloat16* __restrict__ w16, uint64_t n) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -570,6 +629,19 @@ template cudaError_t launch_adam<float>(double*, float*, float*, float*, __nv_bf
                                         double, double, double, double, int, double*, int, cudaStream_t);
 template cudaError_t launch_adam<double>(double*, float*, float*, double*, __nv_bfloat16*, uint64_t, double,
                                          double, double, double, double, double, int, double*, int, cudaStream_t);
+
+cudaError_t launch_adam_shard(double* w, float* m, float* v, const float* g, const float* recv, int nslots,
+                              uint64_t slot_stride, __nv_bfloat16* w16, ShardPeers peers, uint64_t n, double lr,
+                              double b1, double b2, double eps, double bc1, double bc2, double* gsq, int num_sms,
+                              cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const uint64_t want = (n / 4 + 255) / 256;
+    const uint64_t cap = static_cast<uint64_t>(num_sms) * 8;
+    const int blocks = static_cast<int>(want < 1 ? 1 : (want > cap ? cap : want));
+    adam_shard_kernel<<<blocks, 256, 0, s>>>(w, m, v, g, recv, nslots, slot_stride, w16, peers, n, lr, b1, b2, eps,
+                                             bc1, bc2, gsq);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_to_bf16(const double* w, __nv_bfloat16* w16, uint64_t n, int num_sms, cudaStream_t s) {
     if (n == 0) return cudaSuccess;

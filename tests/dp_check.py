@@ -1,10 +1,13 @@
 """Multi-GPU data-parallel parity (run under torchrun, >= 2 GPUs).
 
 Every rank of one gang trains its token-balanced shard of each polled
-micro-batch of the V=256/D=64 golden fixture, the gang all-reduces dW over
-NCCL, and rank 0 checks the reduced gradient and the post-update weights
-against the compiled-reference golden run (same tolerances as the 1-GPU
-tensor-core path)."""
+micro-batch of the V=256/D=64 golden fixture (2 global steps).  Two modes:
+  allreduce  NCCL all-reduce of dW + replicated Adam (`fm_agent_allreduce_grad`)
+  gang       fused GEMM2 -> reduce-scatter over NVLink peer memory + sharded
+             Adam with the bf16 all-gather fused in (`fm_gang_attach/connect`)
+Rank 0 checks delta-W (assembled from the owners' rows in gang mode) and the
+update grad norms against the compiled-reference golden run, with the same
+tolerances as the 1-GPU tensor-core path."""
 import ctypes as C
 import os
 import sys
@@ -16,6 +19,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
+import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 from paper_2602_09578_b200 import _lib  # noqa: E402
@@ -24,7 +28,61 @@ from fixture_runner import payload  # noqa: E402
 from test_gpu_path import _oracle_grad_step0, rel_fro  # noqa: E402
 
 
+def gang_vs_allreduce(ctx, comm, rank, world) -> bool:
+    """V = 1000 (4 GEMM2 row tiles, so every rank owns rows): one global step
+    through the fused gang path and through all-reduce + replicated Adam from
+    the same W0 must give the same update (different summation order only)."""
+    import workload_helpers as wh
+    L = _lib.lib()
+    V, D, G, mb = 1000, 64, 32, 16
+    rng = np.random.default_rng(11)
+    W0 = rng.normal(size=(V, D)) * 0.5
+    batches = [[(rng.integers(0, V, 5).astype(np.int32), rng.integers(0, V, 70).astype(np.int32), float(a))
+                for a in rng.normal(size=mb)] for _ in range(G // mb)]
+    outs = {}
+    for mode in ("allreduce", "gang"):
+        h = C.c_void_p()
+        _lib.check(L.fm_agent_create(ctx.handle, mode.encode(), V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
+        _lib.check(L.fm_agent_set_weights(h, np.ascontiguousarray(W0).ctypes.data))
+        if mode == "gang":
+            n = C.c_uint64()
+            _lib.check(L.fm_gang_attach(h, comm, None, 0, C.byref(n)))
+            blob = (C.c_uint8 * n.value)()
+            _lib.check(L.fm_gang_attach(h, comm, blob, n.value, C.byref(n)))
+            blobs = [None] * world
+            dist.all_gather_object(blobs, bytes(blob))
+            _lib.check(L.fm_gang_connect(h, b"".join(blobs), n.value))
+        else:
+            _lib.check(L.fm_agent_set_shard(h, rank, world))
+        for bt in batches:
+            arr = (_lib.fm_sample * mb)(*[_lib.fm_sample(ctx.put(wh.enc(p)), ctx.put(wh.enc(r)), a) for p, r, a in bt])
+            t = C.c_int64()
+            _lib.check(L.fm_train_micro_batch(h, arr, mb, G, C.byref(t)))
+        _lib.check(L.fm_agent_allreduce_grad(h, comm))
+        gn = C.c_double()
+        _lib.check(L.fm_apply_update(h, G, 1e-6, 0.9, 0.999, 1e-8, C.byref(gn), None))
+        W = np.empty(V * D)
+        _lib.check(L.fm_agent_read_weights(h, W.ctypes.data))
+        W = W.reshape(V, D)
+        if mode == "gang":
+            tiles = (V + 255) // 256
+            lo = [min(V, (tiles * o // world) * 256) for o in range(world + 1)]
+            parts = [None] * world
+            dist.all_gather_object(parts, torch.tensor(W[lo[rank]:lo[rank + 1]].copy()))
+            W = torch.cat(parts).numpy()
+        outs[mode] = (W - W0, gn.value)
+        L.fm_agent_destroy(h)
+    e = rel_fro(outs["gang"][0], outs["allreduce"][0])
+    en = abs(outs["gang"][1] - outs["allreduce"][1]) / outs["allreduce"][1]
+    good = e < 1e-2 and en < 1e-4
+    if rank == 0:
+        print(f"gang vs allreduce (V=1000): dW rel {e:.3e}, grad-norm rel {en:.3e} -> {'OK' if good else 'FAIL'}",
+              flush=True)
+    return good
+
+
 def main():
+    mode = sys.argv[1] if len(sys.argv) > 1 else "allreduce"
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -43,9 +101,21 @@ def main():
     h = C.c_void_p()
     _lib.check(L.fm_agent_create(ctx.handle, b"agent0", V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
     _lib.check(L.fm_agent_set_weights(h, np.ascontiguousarray(f["W0"]).ctypes.data))
-    _lib.check(L.fm_agent_set_shard(h, rank, world))
+    tiles = (V + 255) // 256
+    lo = [min(V, (tiles * o // world) * 256) for o in range(world + 1)]
+    if mode == "gang":
+        n = C.c_uint64()
+        _lib.check(L.fm_gang_attach(h, comm, None, 0, C.byref(n)))
+        blob = (C.c_uint8 * n.value)()
+        _lib.check(L.fm_gang_attach(h, comm, blob, n.value, C.byref(n)))
+        blobs = [None] * world
+        dist.all_gather_object(blobs, bytes(blob))
+        allb = b"".join(blobs)
+        _lib.check(L.fm_gang_connect(h, allb, n.value))
+    else:
+        _lib.check(L.fm_agent_set_shard(h, rank, world))
     po = f["poll_order"]
-    grads = []
+    grads, norms = [], []
     for u in range(U):
         for b in range(G // mb):
             idx = po[u * G + b * mb: u * G + (b + 1) * mb]
@@ -54,33 +124,51 @@ def main():
                                                          float(f["adv"][i])) for i in idx])
             t = C.c_int64()
             _lib.check(L.fm_train_micro_batch(h, arr, mb, G, C.byref(t)))
-        _lib.check(L.fm_agent_allreduce_grad(h, comm))
-        g = np.empty(V * D)
-        _lib.check(L.fm_agent_read_grad(h, g.ctypes.data))
-        grads.append(g.reshape(V, D))
-        _lib.check(L.fm_apply_update(h, G, 1e-6, 0.9, 0.999, 1e-8, None, None))
+        _lib.check(L.fm_agent_allreduce_grad(h, comm))  # no-op in gang mode
+        if mode == "allreduce":
+            g = np.empty(V * D)
+            _lib.check(L.fm_agent_read_grad(h, g.ctypes.data))
+            grads.append(g.reshape(V, D))
+        gn = C.c_double()
+        _lib.check(L.fm_apply_update(h, G, 1e-6, 0.9, 0.999, 1e-8, C.byref(gn), None))
+        norms.append(gn.value)
     W = np.empty(V * D)
     _lib.check(L.fm_agent_read_weights(h, W.ctypes.data))
+    W = W.reshape(V, D)
+    if mode == "gang":  # each rank maintains only its own rows of the master weights
+        mine = torch.tensor(W[lo[rank]:lo[rank + 1]].copy())
+        parts = [None] * world
+        dist.all_gather_object(parts, mine)
+        W = torch.cat(parts).numpy()
     ok = True
     if rank == 0:
-        g_ref = _oracle_grad_step0(f)
-        e_g = rel_fro(grads[0], g_ref)
-        dW, dW_ref = W.reshape(V, D) - f["W0"], f["W"] - f["W0"]
+        dW, dW_ref = W - f["W0"], f["W"] - f["W0"]
         e_w = rel_fro(dW, dW_ref)
-        ok = e_g <= 2e-2 and e_w <= 5e-2
-        print(f"DP world={world}: grad rel {e_g:.3e}, dW rel {e_w:.3e} -> {'OK' if ok else 'FAIL'}", flush=True)
-    # all ranks must hold identical weights after the replicated update
-    Wt = __import__("torch").tensor(W)
-    ref = Wt.clone()
-    dist.broadcast(ref, src=0)
-    same = bool((Wt == ref).all())
-    if not same:
-        print(f"rank {rank}: weights diverged from rank 0", flush=True)
+        e_n = float(np.max(np.abs(np.array(norms) - f["upd_grad_norm"]) / f["upd_grad_norm"]))
+        ok = e_w <= 5e-2 and e_n <= 2e-2
+        msg = f"DP[{mode}] world={world}: dW rel {e_w:.3e}, update grad-norm rel {e_n:.3e}"
+        if grads:
+            e_g = rel_fro(grads[0], _oracle_grad_step0(f))
+            ok = ok and e_g <= 2e-2
+            msg += f", grad rel {e_g:.3e}"
+        print(msg + (" -> OK" if ok else " -> FAIL"), flush=True)
+    same = True
+    if mode == "allreduce":  # replicas must hold identical weights after the replicated update
+        Wt = torch.tensor(W)
+        ref = Wt.clone()
+        dist.broadcast(ref, src=0)
+        same = bool((Wt == ref).all())
+        if not same:
+            print(f"rank {rank}: weights diverged from rank 0", flush=True)
     L.fm_agent_destroy(h)
+    if mode == "gang":
+        ok = ok and gang_vs_allreduce(ctx, comm, rank, world)
     L.fm_comm_destroy(comm)
     ctx.close()
+    okt = torch.tensor([1 if (ok and same) else 0])
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
     dist.destroy_process_group()
-    sys.exit(0 if (ok and same) else 1)
+    sys.exit(0 if okt.item() == 1 else 1)
 
 
 if __name__ == "__main__":

@@ -19,10 +19,11 @@ def _ngpu():
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-def test_dp_gang_allreduce_parity():
+@pytest.mark.parametrize("mode,port", [("allreduce", 29511), ("gang", 29512)])
+def test_dp_gang_parity(mode, port):
     n = 2
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-                        "--master-addr=127.0.0.1", "--master-port=29511", str(ROOT / "tests" / "dp_check.py")],
-                       capture_output=True, text=True, timeout=600)
+                        "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "tests" / "dp_check.py"),
+                        mode], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout
