@@ -32,7 +32,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-KINDS = ["gather", "gemm1", "lse", "softmax_grad", "gemm2", "adam", "parity", "memset"]
+KINDS = ["gather", "gemm1", "lse", "softmax_grad", "gemm2", "adam", "parity", "memset", "colmax"]
 
 
 def log(*a):
@@ -319,8 +319,8 @@ def run_ours(args, dist: Dist) -> dict | None:
     dist.barrier()
 
     check(L.fm_ctx_set_kernel_timing(ctx.handle, 1))
-    kms = np.zeros(8)
-    kcnt = np.zeros(8, dtype=np.int64)
+    kms = np.zeros(len(KINDS))
+    kcnt = np.zeros(len(KINDS), dtype=np.int64)
     check(L.fm_ctx_kernel_times(ctx.handle, kms.ctypes.data, kcnt.ctypes.data, 1))  # reset
     clocks = ClockSampler(dist.local)
     clocks.start()

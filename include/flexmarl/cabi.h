@@ -106,7 +106,7 @@ int fm_ctx_synchronize(fm_ctx* ctx);
 int fm_ctx_timer_start(fm_ctx* ctx);
 int fm_ctx_timer_stop(fm_ctx* ctx, double* ms);
 /* Per-kernel CUDA-event timing of the hot path (off by default).  Kinds:
- * 0 gather, 1 gemm1, 2 lse, 3 softmax_grad, 4 gemm2, 5 adam, 6 parity, 7 memset. */
+ * 0 gather, 1 gemm1, 2 lse, 3 softmax_grad, 4 gemm2, 5 adam, 6 parity, 7 memset, 8 colmax. */
 int fm_ctx_set_kernel_timing(fm_ctx* ctx, int on);
 int fm_ctx_kernel_times(fm_ctx* ctx, double* ms_out, int64_t* count_out, int reset);
 /* Pre-size the token arena and the per-micro-batch workspace. */
@@ -181,6 +181,9 @@ int fm_agent_read_logp(fm_agent* a, double* out, int64_t n_rows);
  * bit-exact target of the oracle's fmo_pack_rows); any pointer may be NULL. */
 int fm_debug_read_rows(fm_ctx* ctx, int64_t n_rows, int32_t* action, int32_t* ctx4,
                        int32_t* n_ctx, int32_t* sample, float* coef);
+/* Loss-fold softmax bound: colmax[d] = max_v bf16(W)[v][d] as the agent holds it
+ * (D floats); *valid = 1 when it describes the current bf16 shadow. */
+int fm_agent_debug_colmax(fm_agent* a, float* out, int* valid);
 /* Blocks until the agent's stream drains; completed reports become pollable. */
 int fm_agent_sync(fm_agent* a);
 /* Non-blocking: 1 and fills *out if the ticket's micro-batch has finished. */

@@ -82,6 +82,7 @@ _PROTOS = {
     "fm_agent_set_shard": (I, [P, I, I]),
     "fm_agent_read_logp": (I, [P, P, I64]),
     "fm_debug_read_rows": (I, [P, I64, P, P, P, P, P]),
+    "fm_agent_debug_colmax": (I, [P, P, P]),
     "fm_agent_sync": (I, [P]),
     "fm_agent_poll_report": (I, [P, I64, C.POINTER(fm_report)]),
     "fm_apply_update": (I, [P, I64, D, D, D, D, PD, PI64]),

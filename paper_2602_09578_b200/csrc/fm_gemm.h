@@ -31,17 +31,13 @@ struct GemmArgs {
     int stats_ld;
     int accumulate;          // Grad: 1 = dW += acc, 0 = dW = acc
     double* sumsq;           // Grad: += sum(acc^2) (micro-batch grad norm^2)
-    // Fused-loss path (pair MMA only):
-    //  Logits: store p~ TRANSPOSED into pexp_t [N][ldt] (rows < store_rows; zeros for M <= row)
+    // Loss-fold path: Logits uses the per-row offset bound mrow[row] for every tile
+    // (one TMEM pass) and stores p~ TRANSPOSED into pexp_t [N][ldt] (rows <
+    // store_rows; zeros for M <= row) — GEMM2's K-major A operand.
+    const float* mrow;
     __nv_bfloat16* pexp_t;
     long long ldt;
     int store_rows;
-    //  Grad: B tile (Phic^T counts) patched in smem to sig[t][m_tile] * count, so that
-    //  A (= p~'^T) x B' is exactly G^T x Phic; per-row features come from n_ctx / ctx4.
-    const int4* feat4;       // per token: unique features (-1 padded), from K-gather
-    const uint32_t* cnt4;    // per token: their multiplicities (8 bits each)
-    const float* sig;
-    int sig_ld;
     // Grad, DP-gang exchange (xg > 1): rows [xlo[o], xlo[o+1]) are owned by gang
     // rank o; rows owned by another rank are written (whole partial) into
     // xpeer[o] = this rank's receive slot in rank o's buffer (NVLink P2P).
@@ -51,8 +47,8 @@ struct GemmArgs {
     float* xpeer[8] = {};
 };
 
-// 1 when the fused-loss path (no separate K-loss kernel) is active.
-bool fused_loss_enabled();
+// 1 when the loss-fold path (no separate K-loss kernel) is active (FM_LOSS_FOLD != 0).
+bool loss_fold_enabled();
 // 1 when the CTA-pair (cta_group::2) kernels are in use (required by the DP gang exchange).
 bool gemm_pair_mode();
 

@@ -34,6 +34,7 @@ struct RowBuffers {
     float* coef_eff;   // [Mpad] coef * surrogate factor
     int4* feat4;       // [Mpad] unique features of the row (-1 padded)   (tensor-core path)
     uint32_t* cnt4;    // [Mpad] their multiplicities, 8 bits each
+    float* mrow;       // [Mpad] softmax offset bound (1/n) sum_j colmax[f_j]   (loss-fold path)
 };
 
 // K-gather: decode the selected records' token payloads straight out of the
@@ -43,17 +44,25 @@ struct RowBuffers {
 // clear_old != 0, in which case each row first erases its old entries).
 cudaError_t launch_gather(const uint8_t* arena, const SampleDesc* sd, int n_samples, int64_t row_lo,
                           int64_t M, int64_t Mpad, int64_t global_batch, uint64_t D, RowBuffers rows,
-                          __nv_bfloat16* phic, __nv_bfloat16* phict, int clear_old, cudaStream_t s);
+                          __nv_bfloat16* phic, __nv_bfloat16* phict, int clear_old, const int* colmax,
+                          cudaStream_t s);
+
+// K-colmax: keys[d] = key(max_v W16[v][d]) (order-preserving int encoding), the
+// per-feature bound K-gather turns into each row's softmax offset (loss-fold path).
+cudaError_t launch_colmax(const __nv_bfloat16* w16, int64_t V, int64_t D, int* keys, int num_sms,
+                          cudaStream_t s);
 
 // K-lse: combine GEMM1's per-tile softmax partials into lse, the taken-token
 // log-prob (from the fp32 logit GEMM1 captured) and the effective row
 // coefficient (PPO-clip surrogate optional).
-// Fused-loss path (sig != NULL): also writes sig[t][tile] = -c_t * exp(m_tile - lse_t)
-// and folds the taken token's delta into p~^T (pexp_t, leading dim ldt).
+// Loss-fold path (pexp_t != NULL; GEMM1 used the row bound m_t for every tile):
+// folds the taken token's delta into p~^T (pexp_t [V][ldt]) and overwrites the
+// row's <= 4 count entries of Phic^T (phict [D][ldt]) with count * (-c_t / s_t),
+// so that GEMM2 (A = p~^T, B = Phic^T) yields G^T x Phic without a K-loss pass.
 cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int64_t M, int64_t Mpad,
                        int64_t V, const SampleDesc* sd, int64_t global_batch, RowBuffers rows,
-                       const float* old_logp, float clip_eps, double* loss_acc, float* sig,
-                       __nv_bfloat16* pexp_t, int64_t ldt, cudaStream_t s);
+                       const float* old_logp, float clip_eps, double* loss_acc, __nv_bfloat16* pexp_t,
+                       __nv_bfloat16* phict, int64_t ldt, cudaStream_t s);
 
 // K-loss (fused log-softmax gradient):
 //   G^T[v][t] = coef_eff_t * (delta(v, a_t) - p~[t][v] * exp(m_tile(t, v) - lse_t))
@@ -64,11 +73,14 @@ cudaError_t launch_softmax_grad(const CUtensorMap& tmP, const CUtensorMap& tmGt,
 // K-adam (training.hpp:37-51): fp64 master weights, fp32 moments, gradient
 // of type G (float for the tensor-core path, double for parity mode);
 // optionally writes the bf16 shadow and zeroes the gradient.  Accumulates
-// sum(g^2) into *gsq for the update grad_norm.
+// sum(g^2) into *gsq for the update grad_norm.  With colmax != NULL (and a
+// [V][D] shadow) it also produces K-colmax's keys from the new shadow when the
+// grid can keep every thread on fixed columns (*colmax_done tells).
 template <typename G>
 cudaError_t launch_adam(double* w, float* m, float* v, G* g, __nv_bfloat16* w16, uint64_t n,
                         double lr, double b1, double b2, double eps, double bc1, double bc2,
-                        int zero_grad, double* gsq, int num_sms, cudaStream_t s);
+                        int zero_grad, double* gsq, int num_sms, cudaStream_t s,
+                        int* colmax = nullptr, uint64_t D = 0, bool* colmax_done = nullptr);
 
 cudaError_t launch_to_bf16(const double* w, __nv_bfloat16* w16, uint64_t n, int num_sms,
                            cudaStream_t s);

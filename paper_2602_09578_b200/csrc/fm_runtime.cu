@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -111,7 +112,7 @@ struct Workspace {
     __nv_bfloat16* Pexp = nullptr;  // p~ = exp(z - m_tile) [Mpad][ldz] bf16
     float* zact = nullptr;          // logit of the taken token [Mpad]
     float2* stats = nullptr;
-    float* sig = nullptr;  // fused loss: -c_t * exp(m_tile - lse_t) per (row, 256-vocab tile)
+    float* mrow = nullptr;  // loss fold: per-row softmax offset bound [Mpad]
     // parity mode scratch
     int64_t prow_cap = 0;
     uint64_t pvocab_cap = 0, pparam_cap = 0;
@@ -127,7 +128,7 @@ struct Workspace {
 
 // Per-kernel device timing (bench.py's roofline): event pairs recorded on the
 // launching stream around each hot-path kernel when enabled.
-enum KKind { K_GATHER = 0, K_GEMM1, K_LSE, K_SOFTMAX_GRAD, K_GEMM2, K_ADAM, K_PARITY, K_MEMSET, K_NKINDS };
+enum KKind { K_GATHER = 0, K_GEMM1, K_LSE, K_SOFTMAX_GRAD, K_GEMM2, K_ADAM, K_PARITY, K_MEMSET, K_COLMAX, K_NKINDS };
 struct KTimer {
     bool on = false;
     std::vector<cudaEvent_t> pool;
@@ -229,7 +230,7 @@ void ws_free(Workspace& w) {
     cudaFree(w.Pexp);
     cudaFree(w.zact);
     cudaFree(w.stats);
-    cudaFree(w.sig);
+    cudaFree(w.mrow);
     cudaFree(w.zscratch);
     cudaFree(w.dWmb);
     cudaFree(w.logp64);
@@ -281,7 +282,7 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
     e = e ? e : dalloc(&w.Pexp, static_cast<size_t>(R) * ldz);
     e = e ? e : dalloc(&w.zact, R);
     e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n);
-    e = e ? e : dalloc(&w.sig, static_cast<size_t>(R) * tiles_n);
+    e = e ? e : dalloc(&w.mrow, R);
     if (e != cudaSuccess) {
         ws_free(w);
         return fail(FM_ERR_DEVICE_OOM, std::string("workspace allocation: ") + cudaGetErrorString(e));
@@ -372,6 +373,7 @@ RowBuffers row_buffers(Workspace& w) {
     r.ctx4 = w.ctx4;
     r.feat4 = w.feat4;
     r.cnt4 = w.cnt4;
+    r.mrow = w.mrow;
     r.n_ctx = w.n_ctx;
     r.sample = w.sample;
     r.coef = w.coef;
@@ -637,6 +639,10 @@ struct fm_agent {
     float* v = nullptr;
     void* dW = nullptr;  // float (TC) or double (parity)
     __nv_bfloat16* W16 = nullptr;
+    int* colmax = nullptr;          // K-colmax keys of W16 [D] (loss-fold softmax bound)
+    uint64_t w16_gen = 0;           // bumped whenever W16 is rewritten
+    uint64_t cm_gen = ~0ull;        // the W16 generation colmax describes
+    bool cm_parked = false;         // the parked copy carries a valid colmax
     bool dw_valid = false;  // dW holds this step's partial sum
     bool pending_in = false;  // a swap-in copy the next use must wait for
     bool park_w16 = false;    // the parked copy includes the bf16 shadow
@@ -679,7 +685,7 @@ size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 size_t slot_bytes(const fm_agent* a) {
     const size_t P = a->P;
     return align256(P * 8) + 2 * align256(P * 4) + align256(P * dw_elem(a)) +
-           (a->precision == FM_PRECISION_BF16_TC ? align256(P * 2) : 0);
+           (a->precision == FM_PRECISION_BF16_TC ? align256(P * 2) + align256(a->D * 4) : 0);
 }
 
 // Binds a free slot of ctx c (allocating one the first time), ordered on
@@ -715,11 +721,17 @@ int agent_alloc_device(fm_agent* a, fm_ctx* c, cudaStream_t s) {
     a->dW = p;
     p += align256(P * dw_elem(a));
     a->W16 = a->precision == FM_PRECISION_BF16_TC ? reinterpret_cast<__nv_bfloat16*>(p) : nullptr;
+    p += a->W16 ? align256(P * 2) : 0;
+    a->colmax = a->W16 ? reinterpret_cast<int*>(p) : nullptr;
     return FM_OK;
 }
 
 // Releases the agent's slot once everything queued on stream s has run.
 void agent_free_device(fm_agent* a, cudaStream_t s) {
+    if (a->pending_in) {  // an unconsumed swap-in still writes into the slot
+        cudaStreamWaitEvent(s, a->ev_in, 0);
+        a->pending_in = false;
+    }
     if (a->slot) {
         cudaEventRecord(a->slot->ev_free, s);
         a->slot->busy = false;
@@ -729,6 +741,7 @@ void agent_free_device(fm_agent* a, cudaStream_t s) {
     a->m = a->v = nullptr;
     a->dW = nullptr;
     a->W16 = nullptr;
+    a->colmax = nullptr;
 }
 
 // Every operation on an agent goes through here: besides the InactiveGroup
@@ -827,6 +840,7 @@ int fm_agent_set_weights(fm_agent* a, const double* W) {
     if (a->W16) {
         FM_CUDA(launch_to_bf16(a->W, a->W16, a->P, c->num_sms, c->stream));
         count_launch();
+        ++a->w16_gen;
     }
     FM_CUDA(cudaStreamSynchronize(c->stream));
     return FM_OK;
@@ -941,16 +955,27 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 FM_CUDA(cudaMemsetAsync(w.phic, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
                 FM_CUDA(cudaMemsetAsync(w.phict, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
             }
+            const bool fold = loss_fold_enabled();
+            if (fold && a->cm_gen != a->w16_gen) {
+                // per-feature max of the shadow, when K-adam did not produce it (first step,
+                // set_weights, DP-gang sharded update, host-tier swap-in)
+                KScope k(c, K_COLMAX, s);
+                FM_CUDA(launch_colmax(a->W16, static_cast<int64_t>(a->V), static_cast<int64_t>(a->D), a->colmax,
+                                      c->num_sms, s));
+                a->cm_gen = a->w16_gen;
+                count_launch();
+            }
             {
                 KScope k(c, K_GATHER, s);
                 FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, Mpad, G, a->D, rows, w.phic, w.phict,
-                                      reuse ? 1 : 0, s));
+                                      reuse ? 1 : 0, fold ? a->colmax : nullptr, s));
             }
             w.phi_valid = true;
             w.phi_Mpad = Mpad;
             w.phi_D = a->D;
-            // K-GEMM1: z = Phic * W16^T / n; epilogue stores p~ = exp(z - m_tile) (bf16),
-            // the (m_tile, sum p~) softmax partials and the taken token's logit
+            // K-GEMM1: z = Phic * W16^T / n; epilogue stores p~ = exp(z - m) (bf16) with m the
+            // row's bound (fold: transposed, GEMM2's A operand) or the tile max (K-loss path),
+            // the (m, sum p~) softmax partials and the taken token's logit
             CUtensorMap tA, tB, tP, tGt, tPt;
             if (!make_tmap_bf16_kmajor(&tA, w.phic, Mpad, a->D, kGemmBM) ||
                 !make_tmap_bf16_kmajor(&tB, a->W16, a->V, a->D, gemm_b_box_rows()) ||
@@ -964,8 +989,8 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g1.N = static_cast<int>(a->V);
             g1.K = static_cast<int>(a->D);
             g1.group_m = 16;
-            const bool fused = fused_loss_enabled();
-            if (fused) {  // p~^T straight into GEMM2's A operand buffer
+            if (fold) {  // p~^T straight into GEMM2's A operand buffer
+                g1.mrow = w.mrow;
                 g1.pexp_t = w.gt;
                 g1.ldt = static_cast<long long>(Mpad);
                 g1.store_rows = static_cast<int>(Mpad);
@@ -987,14 +1012,15 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 KScope k(c, K_LSE, s);
                 FM_CUDA(launch_lse(w.zact, w.stats, tiles_n, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
                                    a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1,
-                                   fused ? w.sig : nullptr, fused ? w.gt : nullptr, Mpad, s));
+                                   fold ? w.gt : nullptr, w.phict, Mpad, s));
             }
-            // K-softmax-grad: G^T tiles (zero for padding rows) — folded into GEMM2 when fused
-            if (!fused) {
+            // K-softmax-grad: G^T tiles (zero for padding rows) — folded into GEMM2's operands
+            if (!fold) {
                 KScope k(c, K_SOFTMAX_GRAD, s);
                 FM_CUDA(launch_softmax_grad(tP, tGt, w.stats, tiles_n, Mpad, static_cast<int64_t>(a->V), rows, s));
             }
             // K-GEMM2: dW (+)= G^T * Phic ; first contribution of the step overwrites
+            // (fold: A = p~'^T, B = Phic^T scaled per row by K-lse — the same product)
             GemmArgs g2{};
             g2.M = static_cast<int>(a->V);
             g2.N = static_cast<int>(a->D);
@@ -1004,12 +1030,6 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g2.ld_out = static_cast<long long>(a->D);
             g2.accumulate = a->dw_valid ? 1 : 0;
             g2.sumsq = scal;
-            if (fused) {  // B' = sig[t][m_tile] * Phic^T, built in smem by the transform warp
-                g2.sig = w.sig;  // sig^T [tiles_n][Mpad]
-                g2.sig_ld = static_cast<int>(Mpad);
-                g2.feat4 = w.feat4;
-                g2.cnt4 = w.cnt4;
-            }
             const bool exchange = a->gang && a->gang->connected && a->samples + n == G;
             if (exchange) {  // last micro-batch of the step: reduce-scatter inside the epilogue
                 GangState* gs = a->gang;
@@ -1026,10 +1046,10 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 a->dw_valid = true;
                 if (int st = gang_barrier(a)) return st;  // every rank's partials have landed
             }
-            count_launch(fused ? 4 : 5);
+            count_launch(fold ? 4 : 5);
         } else {
             w.phi_valid = false;  // the row buffers no longer describe Phic's contents
-            FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, M, G, a->D, rows, nullptr, nullptr, 0, s));
+            FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, M, G, a->D, rows, nullptr, nullptr, 0, nullptr, s));
             if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * 8, s));
             KScope k(c, K_PARITY, s);
             FM_CUDA(launch_parity_rows(a->W, a->V, a->D, M, rows, w.sd, G, w.zscratch, w.dWmb, w.logp64,
@@ -1170,6 +1190,23 @@ int fm_debug_read_rows(fm_ctx* c, int64_t n, int32_t* action, int32_t* ctx4, int
     return FM_OK;
 }
 
+int fm_agent_debug_colmax(fm_agent* a, float* out, int* valid) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
+    if (!a->colmax) return fail(FM_ERR_CONFIG_ERROR, "no bf16 shadow (parity precision)");
+    if (int st = set_dev(a->ctx)) return st;
+    FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
+    std::vector<int> keys(a->D);
+    FM_CUDA(cudaMemcpy(keys.data(), a->colmax, a->D * 4, cudaMemcpyDeviceToHost));
+    for (uint64_t d = 0; d < a->D; ++d) {
+        const int k = keys[d] >= 0 ? keys[d] : keys[d] ^ 0x7fffffff;
+        std::memcpy(out + d, &k, 4);
+    }
+    if (valid) *valid = a->cm_gen == a->w16_gen ? 1 : 0;
+    return FM_OK;
+    FM_GUARD_END
+}
+
 int fm_agent_sync(fm_agent* a) {
     if (!a->ctx) return FM_OK;
     if (int st = set_dev(a->ctx)) return st;
@@ -1207,6 +1244,7 @@ int fm_apply_update(fm_agent* a, int64_t G, double lr, double b1, double b2, dou
     const double bc1 = 1.0 - std::pow(b1, static_cast<double>(a->step));  // training.hpp:42-43
     const double bc2 = 1.0 - std::pow(b2, static_cast<double>(a->step));
     FM_CUDA(cudaMemsetAsync(a->d_upd, 0, sizeof(double), s));
+    bool cm_fused = false;
     KScope ks(c, K_ADAM, s);
     if (a->precision == FM_PRECISION_PARITY_F64) {
         FM_CUDA(launch_adam<double>(a->W, a->m, a->v, static_cast<double*>(a->dW), nullptr, a->P, lr, b1, b2, eps,
@@ -1225,14 +1263,18 @@ int fm_apply_update(fm_agent* a, int64_t G, double lr, double b1, double b2, dou
         // global grad norm^2; doubles as the barrier after the peers' W16 writes
         FM_NCCL(ncclAllReduce(a->d_upd, a->d_upd, 1, ncclFloat64, ncclSum, gang_comm(gs), s));
     } else {
-        // the next step's first GEMM2 overwrites dW, so no zeroing pass here
+        // the next step's first GEMM2 overwrites dW, so no zeroing pass here; the new
+        // shadow's column maxima (loss-fold bound) come out of the same pass
         FM_CUDA(launch_adam<float>(a->W, a->m, a->v, static_cast<float*>(a->dW), a->W16, a->P, lr, b1, b2, eps,
-                                   bc1, bc2, 0, a->d_upd, c->num_sms, s));
+                                   bc1, bc2, 0, a->d_upd, c->num_sms, s, loss_fold_enabled() ? a->colmax : nullptr,
+                                   a->D, &cm_fused));
     }
     count_launch();
     a->dw_valid = false;
     a->samples = 0;
     a->version += 1;
+    ++a->w16_gen;
+    if (cm_fused) a->cm_gen = a->w16_gen;
     FM_CUDA(cudaMemcpyAsync(a->h_upd, a->d_upd, sizeof(double), cudaMemcpyDeviceToHost, s));
     if (grad_norm_out) {
         FM_CUDA(cudaStreamSynchronize(s));
@@ -1258,7 +1300,7 @@ int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
     // NVLink tiers (a copy-engine copy is cheaper than regenerating it on the
     // SMs); over PCIe it is regenerated from W on activation instead.
     const bool park_w16 = a->W16 && tier != FM_TIER_HOST;
-    const size_t bytes = P * 16 + P * dw_elem(a) + (a->W16 ? P * 2 : 0);
+    const size_t bytes = P * 16 + P * dw_elem(a) + (a->W16 ? P * 2 + a->D * 4 : 0);
     const int pdev = tier == FM_TIER_PEER ? peer_device : c->device;
     if (a->park && (a->park_tier != tier || a->park_device != pdev || a->park_bytes < bytes)) {
         FM_CUDA(cudaStreamSynchronize(c->copy_out));
@@ -1308,6 +1350,8 @@ int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
     if (dwb) FM_CUDA(cp(p + P * 16, a->dW, dwb));  // only mid-step gradients travel
     if (park_w16) FM_CUDA(cp(p + P * (16 + dw_elem(a)), a->W16, P * 2));
     a->park_w16 = park_w16;
+    a->cm_parked = park_w16 && a->cm_gen == a->w16_gen;
+    if (a->cm_parked) FM_CUDA(cp(p + P * (18 + dw_elem(a)), a->colmax, a->D * 4));
     FM_CUDA(cudaEventRecord(a->ev_out, c->copy_out));
     agent_free_device(a, c->copy_out);
     a->active = false;
@@ -1350,7 +1394,10 @@ int fm_agent_activate(fm_agent* a, fm_ctx* c) {
         FM_CUDA(launch_to_bf16(a->W, a->W16, P, c->num_sms, c->copy_in));  // shadow regenerated
         count_launch();
     }
+    if (a->W16 && a->park_w16 && a->cm_parked) FM_CUDA(cp(a->colmax, p + P * (18 + dw_elem(a)), a->D * 4));
     FM_CUDA(cudaEventRecord(a->ev_in, c->copy_in));
+    ++a->w16_gen;
+    if (a->W16 && a->park_w16 && a->cm_parked) a->cm_gen = a->w16_gen;
     a->pending_in = true;  // consumers wait lazily (check_active)
     a->ctx = c;
     a->active = true;
@@ -1881,6 +1928,7 @@ int fm_agent_deserialize(fm_agent* a, int64_t global_batch, const uint8_t* in, u
     if (a->W16) {
         FM_CUDA(launch_to_bf16(a->W, a->W16, P, c->num_sms, s));
         count_launch();
+        ++a->w16_gen;
     }
     FM_CUDA(cudaStreamSynchronize(s));
     a->version = static_cast<int64_t>(version);

@@ -72,7 +72,7 @@ struct LogitsEpi {
         const bool ok = row < a.M;
         row_scale = ok ? a.row_scale[row] : 0.f;
         action = ok ? a.action[row] : -1;
-        run_max = -INFINITY;
+        run_max = a.mrow ? (ok ? a.mrow[row] : 0.f) : -INFINITY;  // fold: the row's bound, known upfront
         run_sum = 0.f;
     }
     __device__ __forceinline__ void pass1(const GemmArgs& a, int row, int col0, uint32_t (&r)[32]) {
@@ -90,20 +90,33 @@ struct LogitsEpi {
     __device__ __forceinline__ void chunk(const GemmArgs& a, int row, int col0, uint32_t (&r)[32]) {
         const int nvalid = min(32, a.N - col0);
         if (a.pexp_t) {
-            // fused-loss layout: p~^T [v][t] (GEMM2's K-major A operand).  For a fixed
-            // v the warp's 32 lanes hold 32 consecutive t -> 64 B contiguous per store.
-            if (row >= a.store_rows || nvalid <= 0) return;
+            // loss-fold layout: p~^T [v][t] (GEMM2's K-major A operand), single TMEM pass
+            // with the row bound as offset.  Lane pairs swap halves so that each store
+            // writes a bf16x2 of two consecutive t: per v-pair the warp stores 2 x 64 B.
+            if (nvalid <= 0) return;
             const bool live = row < a.M;
             const float m = run_max;
+            const uint32_t lane = threadIdx.x & 31;
+            const bool odd = lane & 1;
             float s = 0.f;
-            __nv_bfloat16* dst = a.pexp_t + static_cast<size_t>(col0) * a.ldt + row;
+            __nv_bfloat16* dst = a.pexp_t + static_cast<size_t>(col0) * a.ldt + (row & ~1);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                if (j < nvalid) {
-                    const float p = live ? fast_exp(__uint_as_float(r[j]) * row_scale - m) : 0.f;
-                    s += p;
-                    dst[static_cast<size_t>(j) * a.ldt] = __float2bfloat16_rn(p);
-                }
+            for (int j = 0; j < 32; j += 2) {
+                const float z0 = __uint_as_float(r[j]) * row_scale;
+                const float z1 = __uint_as_float(r[j + 1]) * row_scale;
+                if (col0 + j == action) a.zact[row] = z0;
+                if (col0 + j + 1 == action) a.zact[row] = z1;
+                const float p0 = (live && j < nvalid) ? fast_exp(z0 - m) : 0.f;
+                const float p1 = (live && j + 1 < nvalid) ? fast_exp(z1 - m) : 0.f;
+                s += p0 + p1;
+                // even lane keeps column j and receives its odd neighbour's column j;
+                // odd lane keeps column j+1 and receives the even neighbour's column j+1
+                const float give = odd ? p0 : p1;
+                const float got = __shfl_xor_sync(0xffffffffu, give, 1);
+                const __nv_bfloat162 h = odd ? __floats2bfloat162_rn(got, p1) : __floats2bfloat162_rn(p0, got);
+                const int jj = odd ? j + 1 : j;
+                if (jj < nvalid && (row & ~1) < a.store_rows)
+                    *reinterpret_cast<__nv_bfloat162*>(dst + static_cast<size_t>(jj) * a.ldt) = h;
             }
             run_sum += s;
             return;
@@ -348,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int row = tc.mb * BM + row_in_tile;
             epi.begin(args, row);
             if constexpr (std::is_same_v<Epi, GradEpi>) epi.sumsq = 0.0;
-            if constexpr (Epi::kTwoPass) {
+            if (Epi::kTwoPass && !args.mrow) {
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t r[32];
@@ -395,56 +408,9 @@ constexpr uint32_t P_B_STAGE = 128 * BK * 2;    // 16 KB: this CTA's half of B's
 constexpr uint32_t P_STAGE_BYTES = P_A_STAGE + P_B_STAGE;
 constexpr uint32_t kIdesc2 = idesc_bf16_f32<256, BN>();
 
-constexpr int kThreadsPair = 224;  // + w6: B-operand transform warp (fused-loss GEMM2)
+constexpr int kThreadsPair = 192;  // w0 TMA, w1 MMA, w2-5 epilogue
 
-// Fused-loss B transform: overwrite the <= 4 non-zero counts of every token
-// column t of this CTA's B tile (Phic^T rows [d0, d0+128), K-slice of 64
-// tokens) with sig[t][mt] * count, where mt is the GEMM2 row tile (= the
-// GEMM1 softmax-partial tile).  Then A x B' = G^T x Phic exactly (K-lse has
-// folded the delta term into A).  Element (row r, k) of a K-major SWIZZLE_128B
-// tile lives at byte r*128 + (((2k)>>4) ^ (r&7))*16 + (2k)&15.
-// The per-token metadata of a K-slice (2 tokens per lane) is loaded into
-// registers one slice ahead, so the global-load latency hides behind the
-// wait for the TMA of the current slice.
-// Per-stage token metadata staged into smem by the producer's bulk copies
-// (same full barrier as the A/B tiles), so the transform warp never touches
-// global memory: its release-arrive stays cheap.
-constexpr uint32_t META_FEAT = BK * 16;   // int4 unique features per token
-constexpr uint32_t META_CNT = BK * 4;     // packed multiplicities
-constexpr uint32_t META_SIG = BK * 4;     // sig^T[m_tile][t]
-constexpr uint32_t META_BYTES = META_FEAT + META_CNT + META_SIG;
-
-__device__ __forceinline__ void patch_apply(uint8_t* sB_local, uint32_t sB_peer, const uint8_t* meta, uint32_t d0,
-                                            uint32_t lane) {
-    const int4* feat = reinterpret_cast<const int4*>(meta);
-    const uint32_t* cnt = reinterpret_cast<const uint32_t*>(meta + META_FEAT);
-    const float* sig = reinterpret_cast<const float*>(meta + META_FEAT + META_CNT);
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        const uint32_t kk = lane * 2u + static_cast<uint32_t>(q);
-        const int4 f4 = feat[kk];
-        const int f[4] = {f4.x, f4.y, f4.z, f4.w};
-        const uint32_t c = cnt[kk];
-        const float sg = sig[kk];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t r = static_cast<uint32_t>(f[j]) - d0;  // f == -1 -> huge
-            if (f[j] < 0 || r >= 256u) continue;
-            const float cj = static_cast<float>((c >> (8 * j)) & 0xFFu);
-            const uint32_t rr = r & 127u;  // row inside the CTA's 128-row half of the B tile
-            const uint32_t byte = rr * 128u + ((((2u * kk) >> 4) ^ (rr & 7u)) << 4) + ((2u * kk) & 15u);
-            const __nv_bfloat16 v = __float2bfloat16_rn(sg * cj);
-            if (r < 128u) {
-                *reinterpret_cast<__nv_bfloat16*>(sB_local + byte) = v;
-            } else {  // the peer CTA's half, over DSMEM
-                const unsigned short bits = *reinterpret_cast<const unsigned short*>(&v);
-                asm volatile("st.shared::cluster.u16 [%0], %1;" ::"r"(sB_peer + byte), "h"(bits) : "memory");
-            }
-        }
-    }
-}
-
-template <class Epi, bool kPatch>
+template <class Epi>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     gemm_tn_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        GemmArgs args) {
@@ -453,12 +419,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + P_STAGES * P_A_STAGE;
-    uint8_t* sMeta = smem + P_STAGES * P_STAGE_BYTES;  // kPatch: P_STAGES x META_BYTES
-    uint64_t* full =
-        reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES + (kPatch ? P_STAGES * META_BYTES : 0));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_STAGES * P_STAGE_BYTES);
     uint64_t* empty = full + P_STAGES;
-    uint64_t* ready = empty + P_STAGES;  // kPatch: both CTAs' B halves transformed
-    uint64_t* tfull = ready + P_STAGES;
+    uint64_t* tfull = empty + P_STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     float* xscratch = reinterpret_cast<float*>(tmem_slot + 4);  // 4 warps x 32 x 36 fp32 (16-B aligned)
@@ -472,11 +435,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
         for (int s = 0; s < P_STAGES; ++s) {
-            // plain: the leader's producer arrives with both CTAs' tx bytes;
-            // kPatch: every CTA tracks its own tile (its transform warp waits on it)
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], 1);   // the leader's producer arrives with both CTAs' tx bytes
             mbar_init(&empty[s], 1);  // one multicast commit per consumed stage
-            mbar_init(&ready[s], 1);  // kPatch: the leader's transform warp (patched both B halves)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
@@ -509,28 +469,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                 const int brow = tc.nb * BN + static_cast<int>(rank) * 128;
                 for (int k = 0; k < k_iters; ++k) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    if constexpr (kPatch) {
-                        // pair TMA into the leader's barrier; the leader also stages the
-                        // K-slice's token metadata for its transform warp
-                        const uint32_t fb = mapa_shared(&full[stage], 0);
-                        if (leader) {
-                            mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES + META_BYTES);
-                            uint8_t* m = sMeta + stage * META_BYTES;
-                            const int t0 = k * BK;
-                            bulk_load(m, args.feat4 + t0, META_FEAT, &full[stage]);
-                            bulk_load(m + META_FEAT, args.cnt4 + t0, META_CNT, &full[stage]);
-                            bulk_load(m + META_FEAT + META_CNT,
-                                      args.sig + static_cast<size_t>(tc.mb) * args.sig_ld + t0, META_SIG,
-                                      &full[stage]);
-                        }
-                        tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, k * BK, arow, pol);
-                        tma_load_2d_2sm(sB + stage * P_B_STAGE, &tmB, fb, k * BK, brow, pol);
-                    } else {
-                        const uint32_t fb = mapa_shared(&full[stage], 0);
-                        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
-                        tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, k * BK, arow, pol);
-                        tma_load_2d_2sm(sB + stage * P_B_STAGE, &tmB, fb, k * BK, brow, pol);
-                    }
+                    const uint32_t fb = mapa_shared(&full[stage], 0);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+                    tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, k * BK, arow, pol);
+                    tma_load_2d_2sm(sB + stage * P_B_STAGE, &tmB, fb, k * BK, brow, pol);
                     if (++stage == P_STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -550,7 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
                 for (int k = 0; k < k_iters; ++k) {
-                    mbar_wait(kPatch ? &ready[stage] : &full[stage], phase);
+                    mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint64_t adesc = umma_desc_k_sw128(smem_u32(sA + stage * P_A_STAGE));
                     const uint64_t bdesc = umma_desc_k_sw128(smem_u32(sB + stage * P_B_STAGE));
@@ -570,30 +512,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             }
         }
         __syncwarp();
-    } else if (warp == 6) {
-        // ===== B transform (fused-loss GEMM2): the leader patches both CTAs' B halves =====
-        if constexpr (kPatch) {
-            if (leader) {
-                int stage = 0;
-                uint32_t phase = 0;
-                for (int t = cid; t < num_tiles; t += nclusters) {
-                    const TileCoord tc = tile_coord(t, tiles_m, tiles_n, args.group_m);
-                    const uint32_t d0 = static_cast<uint32_t>(tc.nb) * BN;
-                    for (int k = 0; k < k_iters; ++k) {
-                        mbar_wait(&full[stage], phase);  // both halves + metadata landed
-                        uint8_t* sBs = sB + stage * P_B_STAGE;
-                        patch_apply(sBs, mapa_shared(sBs, 1), sMeta + stage * META_BYTES, d0, lane);
-                        fence_proxy_async_cluster();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_cluster(mapa_shared(&ready[stage], 0));
-                        if (++stage == P_STAGES) {
-                            stage = 0;
-                            phase ^= 1;
-                        }
-                    }
-                }
-            }
-        }
     } else {
         // ===== epilogue warps 2..5 (both CTAs; each drains its own 128 rows) =====
         const uint32_t quad = warp & 3;
@@ -611,7 +529,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             const int row = tc.mb * 256 + row_in_tile;
             epi.begin(args, row);
             if constexpr (std::is_same_v<Epi, GradEpi>) epi.sumsq = 0.0;
-            if constexpr (Epi::kTwoPass) {
+            if (Epi::kTwoPass && !args.mrow) {
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t r[32];
@@ -658,25 +576,18 @@ bool use_pair_mma() {
 
 }  // namespace
 
-// The fused-loss GEMM2 (K-loss folded into GEMM2's B operand) is correct but
-// OFF by default: patching the pair's B halves needs a cluster-scope
-// release + async-proxy fence per 64-token K-slice, measured at ~1.7k cycles
-// per stage on B200 (GEMM2 2.4 -> 10 ms at C2), far above the 0.5 ms K-loss it
-// removes.  FM_FUSED_LOSS=1 enables it for experiments.
-bool fused_loss_enabled() {
+// Loss-fold path (default; FM_LOSS_FOLD=0 restores the separate K-loss pass).
+bool loss_fold_enabled() {
     static const bool on = [] {
-        const char* e = getenv("FM_FUSED_LOSS");
-        return use_pair_mma() && e && e[0] == '1';
+        const char* e = getenv("FM_LOSS_FOLD");
+        return !(e && e[0] == '0');
     }();
     return on;
 }
 
-namespace {
-
-}  // namespace
 
 size_t gemm_smem_bytes() {
-    return use_pair_mma() ? P_STAGES * (P_STAGE_BYTES + META_BYTES) + 1024 + 512 + 4 * 32 * 36 * 4
+    return use_pair_mma() ? P_STAGES * P_STAGE_BYTES + 1024 + 512 + 4 * 32 * 36 * 4
                           : STAGES * STAGE_BYTES + 1024 + 256;
 }
 
@@ -693,15 +604,11 @@ cudaError_t gemm_tn_launch(GemmKind kind, const CUtensorMap& tmA, const CUtensor
         const int pairs = num_sms / 2;
         const int grid = 2 * (tiles < pairs ? tiles : pairs);
         if (kind == GemmKind::Logits) {
-            auto k = gemm_tn_2sm_kernel<LogitsEpi, false>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            k<<<grid, kThreadsPair, smem, stream>>>(tmA, tmB, args);
-        } else if (args.sig) {
-            auto k = gemm_tn_2sm_kernel<GradEpi, true>;
+            auto k = gemm_tn_2sm_kernel<LogitsEpi>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             k<<<grid, kThreadsPair, smem, stream>>>(tmA, tmB, args);
         } else {
-            auto k = gemm_tn_2sm_kernel<GradEpi, false>;
+            auto k = gemm_tn_2sm_kernel<GradEpi>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             k<<<grid, kThreadsPair, smem, stream>>>(tmA, tmB, args);
         }

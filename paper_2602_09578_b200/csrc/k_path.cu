@@ -30,6 +30,13 @@ __device__ __forceinline__ uint64_t feature_of(int tok, uint64_t D) {  // policy
     return static_cast<uint64_t>(static_cast<int64_t>(tok)) % D;
 }
 
+// order-preserving float <-> int keys (atomicMax on floats of either sign)
+__device__ __forceinline__ int fkey(float f) {
+    const int i = __float_as_int(f);
+    return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float unkey(int k) { return __int_as_float(k >= 0 ? k : k ^ 0x7fffffff); }
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T x) {
 #pragma unroll
@@ -77,7 +84,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
                                                      int64_t row_lo, int64_t M, int64_t Mpad, int64_t G,
                                                      uint64_t D,
                                                      RowBuffers rows, __nv_bfloat16* phic,
-                                                     __nv_bfloat16* phict, int clear_old) {
+                                                     __nv_bfloat16* phict, int clear_old,
+                                                     const int* __restrict__ colmax) {
     __shared__ int64_t s_start[kMaxSamplesSmem];
     const int ns = n_samples < kMaxSamplesSmem ? n_samples : kMaxSamplesSmem;
     for (int i = threadIdx.x; i < ns; i += blockDim.x) s_start[i] = sd[i].row_start;
@@ -112,6 +120,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
         rows.sample[r] = -1;
         rows.coef[r] = 0.f;
         rows.rscale[r] = 0.f;
+        if (colmax) rows.mrow[r] = 0.f;
         return;
     }
     // sample owning global row gr: last s with row_start[s] <= gr (rows are in poll order)
@@ -171,7 +180,50 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
             rows.feat4[r] = make_int4(uf[0], uf[1], uf[2], uf[3]);
             rows.cnt4[r] = packed;
         }
+        if (colmax) {
+            // softmax offset bound: z[r][v] = (1/n) sum_j W[v][f_j] <= (1/n) sum_j colmax[f_j]
+            float b = 0.f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j < n) b += unkey(__ldg(colmax + f[j]));
+            rows.mrow[r] = n ? b / static_cast<float>(n) : 0.f;
+        }
     }
+}
+
+// ---------------------------------------------------------------------------
+// K-colmax: per-feature-column max of the bf16 shadow, colmax[d] = max_v W16[v][d],
+// as order-preserving int keys (atomicMax).  Thread = 8 consecutive columns
+// (one 16-B load per row), blockIdx.y strides the rows.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) colmax_kernel(const __nv_bfloat16* __restrict__ w16, int64_t V, int64_t D,
+                                                     int* __restrict__ keys) {
+    const int64_t c0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8;
+    if (c0 >= D) return;
+    float mx[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
+    if ((D & 7) == 0) {
+#pragma unroll 4
+        for (int64_t v = blockIdx.y; v < V; v += gridDim.y) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4*>(w16 + v * D + c0));
+            const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[j]));
+                mx[2 * j] = fmaxf(mx[2 * j], f.x);
+                mx[2 * j + 1] = fmaxf(mx[2 * j + 1], f.y);
+            }
+        }
+    } else {
+        for (int64_t v = blockIdx.y; v < V; v += gridDim.y)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (c0 + j < D) mx[j] = fmaxf(mx[j], __bfloat162float(w16[v * D + c0 + j]));
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (c0 + j < D) atomicMax(keys + c0 + j, fkey(mx[j]));
 }
 
 // ---------------------------------------------------------------------------
@@ -182,8 +234,8 @@ __global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ zact
                                                   int64_t M, int64_t Mpad, int64_t V,
                                                   const SampleDesc* __restrict__ sd, int64_t G,
                                                   RowBuffers rows, const float* old_logp,
-                                                  float clip_eps, double* loss_acc, float* sig,
-                                                  __nv_bfloat16* pexp_t, int64_t ldt) {
+                                                  float clip_eps, double* loss_acc, int fold,
+                                                  __nv_bfloat16* pexp_t, __nv_bfloat16* phict, int64_t ldt) {
     __shared__ double red[8];
     const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -195,8 +247,6 @@ __global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ zact
                 rows.logp[r] = 0.f;
                 rows.coef_eff[r] = 0.f;
             }
-            if (sig)
-                for (int j = lane; j < stats_ld; j += 32) sig[static_cast<size_t>(j) * Mpad + r] = 0.f;
         } else {
             float m = -INFINITY, s = 0.f;
             const float2* st = stats + static_cast<size_t>(r) * stats_ld;
@@ -232,21 +282,27 @@ __global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ zact
                 rows.logp[r] = lp;
                 rows.coef_eff[r] = ce;
                 loss = valid ? -(adv / static_cast<double>(G)) * static_cast<double>(lp) : 0.0;
-                if (sig && valid && ce != 0.f) {  // sig is stored transposed: sig^T[tile][t], ld = Mpad
-                    // fold the taken token's delta into A: p~' = p~ - exp(lse - m_tile), so that
-                    // sig * p~' = -c * (p - delta) = G  (GEMM2 applies sig through its B operand)
-                    const int pt = a / 256;
-                    const float e = __expf(fminf(lse - st[pt].x, 80.f));
-                    __nv_bfloat16* q = pexp_t + static_cast<size_t>(a) * ldt + r;
-                    *q = __float2bfloat16_rn(__bfloat162float(*q) - e);
+                if (fold) {
+                    // Every tile used the row's offset bound m (K-gather), so
+                    //   G[t][v] = c (delta(v,a) - p~[t][v] / s),  s = sum_v p~ = exp(lse - m).
+                    // The per-row factor sig = -c / s goes into GEMM2's B operand
+                    // (Phic^T's <= 4 count entries of column t), the delta term into A:
+                    //   A[a][t] = p~_a - s   =>   sig * A = -c (p - delta) = G.
+                    if (!(s >= 1e-30f) || !isfinite(s)) loss = __longlong_as_double(0x7ff8000000000000ll);  // range: NaN loss
+                    const float sig = (valid && ce != 0.f) ? -ce / s : 0.f;
+                    if (sig != 0.f) {
+                        __nv_bfloat16* q = pexp_t + static_cast<size_t>(a) * ldt + r;
+                        *q = __float2bfloat16_rn(__expf(zact[r] - m) - s);
+                    }
+                    const int4 f4 = rows.feat4[r];
+                    const uint32_t c4 = rows.cnt4[r];
+                    const int f[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (f[j] >= 0)
+                            phict[static_cast<size_t>(f[j]) * ldt + r] =
+                                __float2bfloat16_rn(sig * static_cast<float>((c4 >> (8 * j)) & 0xFFu));
                 }
-            }
-            if (sig) {
-                // sig[t][tile] = -c_t * exp(m_tile - lse_t): the per-(row, 256-vocab tile) scale
-                const float lse = __shfl_sync(0xffffffffu, m + logf(s), 0);
-                const float ce = __shfl_sync(0xffffffffu, lane == 0 ? rows.coef_eff[r] : 0.f, 0);
-                for (int j = lane; j < stats_ld; j += 32)
-                    sig[static_cast<size_t>(j) * Mpad + r] = ce == 0.f ? 0.f : -ce * __expf(st[j].x - lse);
             }
         }
     }
@@ -335,10 +391,31 @@ __global__ void __launch_bounds__(256) softmax_grad_kernel(const __grid_constant
 // ---------------------------------------------------------------------------
 // K-adam
 // ---------------------------------------------------------------------------
-template <typename G>
-__device__ __forceinline__ double adam_one(double& w, float& m, float& v, G g, double lr, double b1,
+// fp32 gradient (BF16_TC): the moments are stored in fp32, so the moment update
+// and the step lr·m̂/(√v̂+ε) are computed in fp32 (rel. error ~1e-7 on ΔW) and
+// applied to the fp64 master weight.  This keeps the kernel on the HBM roofline:
+// fp64 division + sqrt per parameter cost more issue slots than its 38 bytes.
+struct AdamF {
+    float b1, ob1, b2, ob2, lr_bc1, inv_bc2, eps;
+    __device__ AdamF(double lr, double b1_, double b2_, double eps_, double bc1, double bc2)
+        : b1(static_cast<float>(b1_)), ob1(static_cast<float>(1.0 - b1_)), b2(static_cast<float>(b2_)),
+          ob2(static_cast<float>(1.0 - b2_)), lr_bc1(static_cast<float>(lr / bc1)),
+          inv_bc2(static_cast<float>(1.0 / bc2)), eps(static_cast<float>(eps_)) {}
+};
+
+__device__ __forceinline__ double adam_f32(double& w, float& m, float& v, float g, const AdamF& c) {
+    const float mm = fmaf(c.b1, m, c.ob1 * g);
+    const float vv = fmaf(c.b2, v, c.ob2 * (g * g));
+    w -= static_cast<double>(c.lr_bc1 * mm / (sqrtf(vv * c.inv_bc2) + c.eps));
+    m = mm;
+    v = vv;
+    return static_cast<double>(g) * static_cast<double>(g);
+}
+
+// fp64 gradient (PARITY_F64): the reference's own fp64 arithmetic order.
+__device__ __forceinline__ double adam_f64(double& w, float& m, float& v, double g, double lr, double b1,
                                            double b2, double eps, double bc1, double bc2) {
-    const double gi = static_cast<double>(g);
+    const double gi = g;
     const double mm = b1 * static_cast<double>(m) + (1.0 - b1) * gi;
     const double vv = b2 * static_cast<double>(v) + (1.0 - b2) * gi * gi;
     const double mhat = mm / bc1;
@@ -354,9 +431,19 @@ __global__ void __launch_bounds__(256) adam_kernel(double* __restrict__ w, float
                                                    float* __restrict__ v, G* __restrict__ g,
                                                    __nv_bfloat16* __restrict__ w16, uint64_t n,
                                                    double lr, double b1, double b2, double eps,
-                                                   double bc1, double bc2, int zero_grad, double* gsq) {
+                                                   double bc1, double bc2, int zero_grad, double* gsq,
+                                                   int* __restrict__ cm, uint64_t D) {
     __shared__ double red[8];
     double acc = 0.0;
+    // colmax fused (cm != null): the launcher sized the grid so that a thread's four
+    // elements sit in the same four columns on every iteration
+    float cmx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    const AdamF cf(lr, b1, b2, eps, bc1, bc2);
+    auto adam_one = [&](double& w_, float& m_, float& v_, G g_, double, double, double, double, double,
+                        double) -> double {
+        if constexpr (sizeof(G) == 4) return adam_f32(w_, m_, v_, g_, cf);
+        else return adam_f64(w_, m_, v_, g_, lr, b1, b2, eps, bc1, bc2);
+    };
     const uint64_t n4 = n / 4;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
@@ -385,6 +472,13 @@ __global__ void __launch_bounds__(256) adam_kernel(double* __restrict__ w, float
             pk.x = *reinterpret_cast<uint32_t*>(&lo);
             pk.y = *reinterpret_cast<uint32_t*>(&hi);
             reinterpret_cast<uint2*>(w16)[i] = pk;
+            if (cm) {
+                const float2 a = __bfloat1622float2(lo), b = __bfloat1622float2(hi);
+                cmx[0] = fmaxf(cmx[0], a.x);
+                cmx[1] = fmaxf(cmx[1], a.y);
+                cmx[2] = fmaxf(cmx[2], b.x);
+                cmx[3] = fmaxf(cmx[3], b.y);
+            }
         }
         if (zero_grad) {
             if constexpr (sizeof(G) == 4) reinterpret_cast<float4*>(g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -398,6 +492,14 @@ __global__ void __launch_bounds__(256) adam_kernel(double* __restrict__ w, float
         acc += adam_one(w[i], m[i], v[i], g[i], lr, b1, b2, eps, bc1, bc2);
         if (w16) w16[i] = __float2bfloat16_rn(static_cast<float>(w[i]));
         if (zero_grad) g[i] = G(0);
+    }
+    if (cm) {
+        const uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        if (i0 < n4) {
+            const uint64_t c0 = (4 * i0) % D;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) atomicMax(cm + c0 + j, fkey(cmx[j]));
+        }
     }
     if (gsq) {
         const double tot = block_sum(acc, red);
@@ -419,6 +521,9 @@ __global__ void __launch_bounds__(256) adam_shard_kernel(double* __restrict__ w,
                                                          double* gsq) {
     __shared__ double red[8];
     double acc = 0.0;
+    const AdamF cf(lr, b1, b2, eps, bc1, bc2);
+    auto adam_one = [&](double& w_, float& m_, float& v_, float g_, double, double, double, double, double,
+                        double) -> double { return adam_f32(w_, m_, v_, g_, cf); };
     const uint64_t n4 = n / 4;
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
@@ -583,23 +688,34 @@ __global__ void parity_fold_kernel(double* __restrict__ dW, double* __restrict__
 // ---------------------------------------------------------------------------
 cudaError_t launch_gather(const uint8_t* arena, const SampleDesc* sd, int n_samples, int64_t row_lo, int64_t M,
                           int64_t Mpad, int64_t global_batch, uint64_t D, RowBuffers rows, __nv_bfloat16* phic,
-                          __nv_bfloat16* phict, int clear_old, cudaStream_t s) {
+                          __nv_bfloat16* phict, int clear_old, const int* colmax, cudaStream_t s) {
     if (Mpad == 0) return cudaSuccess;
     if (n_samples > kMaxSamplesSmem) return cudaErrorInvalidValue;
     const int blocks = static_cast<int>((Mpad + 255) / 256);
     gather_kernel<<<blocks, 256, 0, s>>>(arena, sd, n_samples, row_lo, M, Mpad, global_batch, D, rows, phic, phict,
-                                         clear_old);
+                                         clear_old, colmax);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_colmax(const __nv_bfloat16* w16, int64_t V, int64_t D, int* keys, int num_sms, cudaStream_t s) {
+    if (V == 0 || D == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(keys, 0x80, static_cast<size_t>(D) * sizeof(int), s);  // key < any finite
+    if (e != cudaSuccess) return e;
+    const unsigned gx = static_cast<unsigned>((D + 2047) / 2048);
+    int64_t gy = static_cast<int64_t>(num_sms) * 8 / gx;
+    gy = gy < 1 ? 1 : (gy > V ? V : gy);
+    colmax_kernel<<<dim3(gx, static_cast<unsigned>(gy)), 256, 0, s>>>(w16, V, D, keys);
     return cudaGetLastError();
 }
 
 cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int64_t M, int64_t Mpad, int64_t V,
                        const SampleDesc* sd, int64_t global_batch, RowBuffers rows, const float* old_logp,
-                       float clip_eps, double* loss_acc, float* sig, __nv_bfloat16* pexp_t, int64_t ldt,
-                       cudaStream_t s) {
+                       float clip_eps, double* loss_acc, __nv_bfloat16* pexp_t, __nv_bfloat16* phict,
+                       int64_t ldt, cudaStream_t s) {
     if (Mpad == 0) return cudaSuccess;
     const int blocks = static_cast<int>((Mpad * 32 + 255) / 256);
     lse_kernel<<<blocks, 256, 0, s>>>(zact, stats, stats_ld, M, Mpad, V, sd, global_batch, rows, old_logp, clip_eps,
-                                      loss_acc, sig, pexp_t, ldt);
+                                      loss_acc, pexp_t != nullptr, pexp_t, phict, ldt);
     return cudaGetLastError();
 }
 
@@ -616,19 +732,42 @@ cudaError_t launch_softmax_grad(const CUtensorMap& tmP, const CUtensorMap& tmGt,
 template <typename G>
 cudaError_t launch_adam(double* w, float* m, float* v, G* g, __nv_bfloat16* w16, uint64_t n, double lr, double b1,
                         double b2, double eps, double bc1, double bc2, int zero_grad, double* gsq, int num_sms,
-                        cudaStream_t s) {
+                        cudaStream_t s, int* colmax, uint64_t D, bool* colmax_done) {
+    if (colmax_done) *colmax_done = false;
     if (n == 0) return cudaSuccess;
     if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g)) & 31) return cudaErrorMisalignedAddress;
     const uint64_t want = (n / 4 + 255) / 256;
     const uint64_t cap = static_cast<uint64_t>(num_sms) * 8;
-    const int blocks = static_cast<int>(want < 1 ? 1 : (want > cap ? cap : want));
-    adam_kernel<G><<<blocks, 256, 0, s>>>(w, m, v, g, w16, n, lr, b1, b2, eps, bc1, bc2, zero_grad, gsq);
+    uint64_t blocks = want < 1 ? 1 : (want > cap ? cap : want);
+    int* cm = nullptr;
+    if (colmax && w16 && D % 4 == 0 && n % D == 0) {
+        // fixed columns per thread: one iteration per thread, or a grid stride that is a
+        // multiple of D (blocks * 1024 elements)
+        if (want > blocks) {
+            uint64_t q = D, r = 1024;  // blocks must be a multiple of D / gcd(D, 1024)
+            while (r) { const uint64_t t = q % r; q = r; r = t; }
+            const uint64_t mult = D / q;
+            blocks = blocks / mult * mult;
+        }
+        if (blocks > 0) {
+            cm = colmax;
+            cudaError_t e = cudaMemsetAsync(colmax, 0x80, D * sizeof(int), s);
+            if (e != cudaSuccess) return e;
+        } else {
+            blocks = want < cap ? want : cap;
+        }
+    }
+    adam_kernel<G><<<static_cast<int>(blocks), 256, 0, s>>>(w, m, v, g, w16, n, lr, b1, b2, eps, bc1, bc2, zero_grad,
+                                                            gsq, cm, D);
+    if (colmax_done) *colmax_done = cm != nullptr;
     return cudaGetLastError();
 }
 template cudaError_t launch_adam<float>(double*, float*, float*, float*, __nv_bfloat16*, uint64_t, double, double,
-                                        double, double, double, double, int, double*, int, cudaStream_t);
+                                        double, double, double, double, int, double*, int, cudaStream_t, int*,
+                                        uint64_t, bool*);
 template cudaError_t launch_adam<double>(double*, float*, float*, double*, __nv_bfloat16*, uint64_t, double,
-                                         double, double, double, double, double, int, double*, int, cudaStream_t);
+                                         double, double, double, double, double, int, double*, int, cudaStream_t,
+                                         int*, uint64_t, bool*);
 
 cudaError_t launch_adam_shard(double* w, float* m, float* v, const float* g, const float* recv, int nslots,
                               uint64_t slot_stride, __nv_bfloat16* w16, ShardPeers peers, uint64_t n, double lr,

@@ -252,3 +252,80 @@ def test_incomplete_batch_and_inactive_errors(ctx):
         eng.apply_global_update("x")
     assert e.value.name == "IncompleteBatch"
     eng.close()
+
+
+@pytest.mark.parametrize("V,D", [(1000, 136), (4000, 4096)])
+def test_loss_fold_colmax_bound(ctx, V, D):
+    """The loss-fold softmax bound colmax[d] = max_v bf16(W)[v][d] is exact
+    whichever kernel produced it: K-colmax (after set_weights), K-adam's fused
+    pass (single-iteration grid at V=1000, D-multiple grid stride at D=4096),
+    and it survives a device-tier swap.  p~ = exp(z - bound) <= 1 relies on it."""
+    import torch
+    from paper_2602_09578_b200.engine import TrainingEngine
+    L_, n = 32, 16
+    rng = np.random.default_rng(11)
+    W0 = rng.normal(size=(V, D)) * 0.5
+    samples = [(rng.integers(0, V, size=rng.integers(1, 6)).astype(np.int32),
+                rng.integers(0, V, size=L_).astype(np.int32)) for _ in range(n)]
+    adv = rng.normal(size=n)
+    ctx.reset_arena()
+    eng = TrainingEngine([ctx], global_batch=n, precision=_lib.PRECISION_BF16_TC)
+    eng.add_agent("t", V, D)
+    eng.activate("t")
+    L = _lib.lib()
+    h = eng.handle("t")
+    _lib.check(L.fm_agent_set_weights(h, np.ascontiguousarray(W0).ctypes.data))
+
+    def colmax():
+        out = np.zeros(D, np.float32)
+        valid = C.c_int()
+        _lib.check(L.fm_agent_debug_colmax(h, out.ctypes.data, C.byref(valid)))
+        return out, valid.value
+
+    def expect(W):  # double -> float -> bf16, the kernels' rounding path
+        return torch.tensor(W).float().to(torch.bfloat16).float().max(dim=0).values.numpy()
+
+    assert colmax()[1] == 0  # set_weights invalidates it
+    arr = (_lib.fm_sample * n)(*[_lib.fm_sample(ctx.put(orc.encode(p)), ctx.put(orc.encode(r)), a)
+                                 for (p, r), a in zip(samples, adv)])
+    t = C.c_int64()
+    _lib.check(L.fm_train_micro_batch(h, arr, n, n, C.byref(t)))
+    cm, ok = colmax()
+    assert ok == 1
+    np.testing.assert_array_equal(cm, expect(W0))
+    _lib.check(L.fm_apply_update(h, n, 1e-3, 0.9, 0.999, 1e-8, None, None))
+    W1 = np.zeros((V, D))
+    _lib.check(L.fm_agent_read_weights(h, W1.ctypes.data))
+    assert np.abs(W1 - W0).max() > 1e-4
+    cm, ok = colmax()
+    assert ok == 1  # produced by K-adam's fused pass
+    np.testing.assert_array_equal(cm, expect(W1))
+    _lib.check(L.fm_agent_suspend(h, _lib.TIER_DEVICE, -1))
+    _lib.check(L.fm_agent_activate(h, ctx.handle))
+    cm, ok = colmax()
+    assert ok == 1  # travelled with the parked shadow
+    np.testing.assert_array_equal(cm, expect(W1))
+    eng.close()
+
+
+def test_destroy_with_unconsumed_swap_in(ctx):
+    """Destroying an agent whose swap-in (activate prefetch) was never consumed
+    must not hand its training slot to the next agent while the copy-in is
+    still writing into it (regression: the next agent's weights were clobbered)."""
+    L = _lib.lib()
+    V, D = 2000, 512
+    for _ in range(3):
+        h = C.c_void_p()
+        _lib.check(L.fm_agent_create(ctx.handle, b"victim", V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
+        _lib.check(L.fm_agent_set_weights(h, np.full(V * D, 0.25).ctypes.data))
+        _lib.check(L.fm_agent_suspend(h, _lib.TIER_HOST, -1))
+        _lib.check(L.fm_agent_activate(h, ctx.handle))  # PCIe copy-in in flight
+        _lib.check(L.fm_agent_destroy(h))
+        g = C.c_void_p()
+        _lib.check(L.fm_agent_create(ctx.handle, b"next", V, D, _lib.PRECISION_BF16_TC, C.byref(g)))
+        W = np.random.default_rng(3).normal(size=V * D)
+        _lib.check(L.fm_agent_set_weights(g, W.ctypes.data))
+        out = np.zeros(V * D)
+        _lib.check(L.fm_agent_read_weights(g, out.ctypes.data))
+        _lib.check(L.fm_agent_destroy(g))
+        assert np.array_equal(out, W)

@@ -33,6 +33,9 @@ def test_generate_matches_reference(ctx, name):
     _lib.check(L().fm_agent_set_weights(h, np.ascontiguousarray(f["W0"]).ctypes.data))
     w = C.c_void_p()
     _lib.check(L().fm_publish_weights(h, 0, C.byref(w)))
+    Wpub = np.zeros((V, D))
+    _lib.check(L().fm_weights_get(w, Wpub.ctypes.data, -1))
+    assert np.array_equal(Wpub, f["W0"]), "published weights differ from the fixture's W0"
     n = len(f["ids"])
     prompts, offs, seeds, want = [], [0], [], []
     for i in range(n):
