@@ -210,6 +210,12 @@ __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Relaxed arrive: no ordering of this thread's prior memory operations (no
+// MEMBAR / store-ack wait).  For TMEM-drained signals: tcgen05.wait::ld has
+// already completed the reads the barrier protects.
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 // Pair TMA: data lands in this CTA's smem, complete_tx goes to the barrier at
 // `bar_cluster_addr` (the leader CTA's full barrier).
 __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* map, uint32_t bar_cluster_addr,

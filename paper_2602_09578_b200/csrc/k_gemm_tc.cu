@@ -543,11 +543,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + ((quad * 32u) << 16) + static_cast<uint32_t>(acc * BN + c * 32), r);
                 tmem_ld_wait();
+                if (c == BN / 32 - 1) {
+                    // the accumulator is fully in registers: hand TMEM back to the MMA
+                    // warp before the last chunk's math and stores (relaxed: no wait
+                    // for this warp's outstanding global stores)
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader[acc]);
+                }
                 epi.chunk(args, row, tc.nb * BN + c * 32, r);
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
             epi.end(args, row, tc.nb);
             if constexpr (std::is_same_v<Epi, GradEpi>) sumsq_total += epi.sumsq;
             acc ^= 1;

@@ -33,8 +33,8 @@ def c1_samples(agent: str, n_updates: int = 2, max_tokens: int = 256, seed: int 
             trajs.append(i % k)
             versions.append(u)
             samples.append((prompt.astype(np.int32), resp.astype(np.int32)))
-            rewards.append(orc.olib().fmo_rule_reward(
-                resp.ctypes.data, len(resp), np.array([3, 1, 4], np.int32).ctypes.data, 3))
+            target = np.array([3, 1, 4], np.int32)  # kept alive across the C call
+            rewards.append(orc.olib().fmo_rule_reward(resp.ctypes.data, len(resp), target.ctypes.data, 3))
     rewards = np.asarray(rewards)
     adv = np.concatenate([orc.group_advantages(rewards[g:g + k]) for g in range(0, len(rewards), k)])
     return ids, turns, trajs, versions, samples, rewards, adv

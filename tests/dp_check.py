@@ -100,7 +100,8 @@ def main():
     _lib.check(L.fm_comm_create(ctx.handle, (C.c_uint8 * 128).from_buffer_copy(uid[0]), world, rank, C.byref(comm)))
     h = C.c_void_p()
     _lib.check(L.fm_agent_create(ctx.handle, b"agent0", V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
-    _lib.check(L.fm_agent_set_weights(h, np.ascontiguousarray(f["W0"]).ctypes.data))
+    W0 = np.ascontiguousarray(f["W0"])  # named: a temporary could be freed before the C call reads it
+    _lib.check(L.fm_agent_set_weights(h, W0.ctypes.data))
     tiles = (V + 255) // 256
     lo = [min(V, (tiles * o // world) * 256) for o in range(world + 1)]
     if mode == "gang":

@@ -317,7 +317,8 @@ def test_destroy_with_unconsumed_swap_in(ctx):
     for _ in range(3):
         h = C.c_void_p()
         _lib.check(L.fm_agent_create(ctx.handle, b"victim", V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
-        _lib.check(L.fm_agent_set_weights(h, np.full(V * D, 0.25).ctypes.data))
+        Wc = np.full(V * D, 0.25)
+        _lib.check(L.fm_agent_set_weights(h, Wc.ctypes.data))
         _lib.check(L.fm_agent_suspend(h, _lib.TIER_HOST, -1))
         _lib.check(L.fm_agent_activate(h, ctx.handle))  # PCIe copy-in in flight
         _lib.check(L.fm_agent_destroy(h))

@@ -30,12 +30,19 @@ def test_generate_matches_reference(ctx, name):
     V, D = int(f["V"]), int(f["D"])
     h = C.c_void_p()
     _lib.check(L().fm_agent_create(ctx.handle, agent.encode(), V, D, _lib.PRECISION_PARITY_F64, C.byref(h)))
-    _lib.check(L().fm_agent_set_weights(h, np.ascontiguousarray(f["W0"]).ctypes.data))
+    W0 = np.ascontiguousarray(f["W0"])  # named: a temporary could be freed before the C call reads it
+    _lib.check(L().fm_agent_set_weights(h, W0.ctypes.data))
     w = C.c_void_p()
     _lib.check(L().fm_publish_weights(h, 0, C.byref(w)))
     Wpub = np.zeros((V, D))
     _lib.check(L().fm_weights_get(w, Wpub.ctypes.data, -1))
-    assert np.array_equal(Wpub, f["W0"]), "published weights differ from the fixture's W0"
+    if not np.array_equal(Wpub, f["W0"]):
+        Wa = np.zeros((V, D))
+        _lib.check(L().fm_agent_read_weights(h, Wa.ctypes.data))
+        bad = np.argwhere(Wpub != f["W0"])
+        raise AssertionError(f"published weights differ: {len(bad)} of {V * D} (first {bad[:3].tolist()}), "
+                             f"values {Wpub.reshape(-1)[:4]} vs {np.asarray(f['W0']).reshape(-1)[:4]}; agent W "
+                             f"now equal: {np.array_equal(Wa, f['W0'])}; V={V} D={D}")
     n = len(f["ids"])
     prompts, offs, seeds, want = [], [0], [], []
     for i in range(n):
