@@ -189,7 +189,8 @@ def run_ours(args, dist: Dist) -> dict | None:
     agents = list(cfg.agents)[: args.agents or None]
     place = placement(agents, dist.world)
     mine = [a for a in agents if dist.rank in place[a]]
-    tier = {"device": _lib.TIER_DEVICE, "host": _lib.TIER_HOST}[args.tier]
+    tier = {"device": _lib.TIER_DEVICE, "host": _lib.TIER_HOST, "resident": None}[args.tier]
+    swap = tier is not None  # "resident": analysis mode, every agent stays in HBM (no swaps)
     G, mb = cfg.global_batch, cfg.micro_batch
     n_steps = args.warmup + args.steps
 
@@ -270,7 +271,7 @@ def run_ours(args, dist: Dist) -> dict | None:
     #     agent's state is prefetched (copy_in stream) while the current one trains
     order = mine
     active = {a: True for a in order}
-    if len(order) > 1:
+    if len(order) > 1 and swap:
         for a in order[1:]:
             check(L.fm_agent_suspend(handles[a], tier, -1))
             active[a] = False
@@ -293,7 +294,7 @@ def run_ours(args, dist: Dist) -> dict | None:
         for i, a in enumerate(order):
             h = handles[a]
             nxt = order[(i + 1) % len(order)]
-            if len(order) > 1 and not active[nxt]:
+            if len(order) > 1 and swap and not active[nxt]:
                 check(timed("activate", L.fm_agent_activate, handles[nxt], ctx.handle))  # prefetch
                 active[nxt] = True
             for _ in range(G // mb):
@@ -308,7 +309,7 @@ def run_ours(args, dist: Dist) -> dict | None:
             if a in comms:
                 check(timed("allreduce", L.fm_agent_allreduce_grad, h, comms[a]))
             check(timed("update", L.fm_apply_update, h, G, cfg.lr, 0.9, 0.999, 1e-8, None, None))
-            if len(order) > 1:
+            if len(order) > 1 and swap:
                 check(timed("suspend", L.fm_agent_suspend, h, tier, -1))
                 active[a] = False
         return ntok
@@ -587,10 +588,10 @@ def run_e2e(args, cfg, ctx, mine, handles, place, comms, dist, tier) -> dict:
         for i, a in enumerate(order):
             h = handles[a]
             nxt = order[(i + 1) % len(order)]
-            if len(order) > 1 and not active[nxt]:
+            if len(order) > 1 and tier is not None and not active[nxt]:
                 check(L.fm_agent_activate(handles[nxt], ctx.handle))
                 active[nxt] = True
-            if len(order) > 1 and not active[a]:
+            if len(order) > 1 and tier is not None and not active[a]:
                 check(L.fm_agent_activate(h, ctx.handle))
                 active[a] = True
             bufs, adv, nbytes = data[(a, step)]
@@ -615,7 +616,7 @@ def run_e2e(args, cfg, ctx, mine, handles, place, comms, dist, tier) -> dict:
                 if r != 1:
                     raise RuntimeError("micro-batch report not ready after the update")
                 d2h += 16
-            if len(order) > 1:
+            if len(order) > 1 and tier is not None:
                 check(L.fm_agent_suspend(h, tier, -1))
                 active[a] = False
 
@@ -742,7 +743,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--tier", default="device", choices=["device", "host"])
+    ap.add_argument("--tier", default="device", choices=["device", "host", "resident"],
+                    help="parking tier of the state swap; 'resident' = no swaps (analysis only)")
     ap.add_argument("--resp-len", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-tokens", type=int, default=4, help="reference tokens per thread per step")
