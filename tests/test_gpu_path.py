@@ -330,3 +330,61 @@ def test_destroy_with_unconsumed_swap_in(ctx):
         _lib.check(L.fm_agent_read_weights(g, out.ctypes.data))
         _lib.check(L.fm_agent_destroy(g))
         assert np.array_equal(out, W)
+
+
+def test_ppo_clip_surrogate_vs_torch_fp32(ctx):
+    """Optional PPO clipped-ratio surrogate (a8): the gradient flows, scaled by
+    rho = exp(logp - old_logp), only through rows whose unclipped branch is the
+    min (A >= 0: rho <= 1+eps; A < 0: rho >= 1-eps).  Checked against a torch
+    fp32 restatement; target ratios stay 0.1 away from the clip edges so bf16
+    logits cannot flip a row's branch."""
+    import torch
+    from paper_2602_09578_b200.engine import TrainingEngine
+    V, D, L_, n, eps = 1000, 136, 120, 16, 0.2
+    rng = np.random.default_rng(21)
+    W0 = rng.normal(size=(V, D)) * 0.5
+    samples = [(rng.integers(0, V, size=rng.integers(1, 6)).astype(np.int32),
+                rng.integers(0, V, size=L_).astype(np.int32)) for _ in range(n)]
+    adv = rng.normal(size=n)
+    rows = orc.pack_rows(samples, adv, 64)
+    M = n * L_
+    # torch fp32 restatement of the dense op on the bf16 shadow
+    phi = torch.zeros(M, D, dtype=torch.float32, device="cuda")
+    for j in range(4):
+        valid = rows["n_ctx"] > j
+        r_idx = torch.tensor(np.nonzero(valid)[0], device="cuda")
+        f_idx = torch.tensor((rows["ctx4"][valid, j].astype(np.int64) % D), device="cuda")
+        phi.index_put_((r_idx, f_idx), torch.ones(len(r_idx), device="cuda"), accumulate=True)
+    w16 = torch.tensor(W0, device="cuda").float().to(torch.bfloat16).float()
+    nctx = torch.tensor(rows["n_ctx"], device="cuda").float()
+    rs = torch.where(nctx > 0, 1.0 / nctx.clamp(min=1), torch.zeros_like(nctx))
+    z = (phi @ w16.T) * rs[:, None]
+    lse = torch.logsumexp(z, dim=1)
+    act = torch.tensor(rows["action"].astype(np.int64), device="cuda")
+    lp = z.gather(1, act[:, None])[:, 0] - lse
+    rho_t = torch.tensor(rng.choice([0.5, 0.7, 1.0, 1.3, 1.6], size=M), device="cuda").float()
+    old = (lp - torch.log(rho_t)).cpu().numpy().astype(np.float32)
+    a_row = torch.tensor(adv[rows["sample"]], device="cuda").float()
+    active = torch.where(a_row >= 0, rho_t <= 1 + eps, rho_t >= 1 - eps)
+    coef = torch.tensor(rows["coef"], device="cuda") * torch.where(active, rho_t, torch.zeros_like(rho_t))
+    p = torch.softmax(z, dim=1)
+    Gm = -p
+    Gm[torch.arange(M, device="cuda"), act] += 1.0
+    g_t = ((Gm * coef[:, None]).T @ phi).double().cpu().numpy()
+    assert 0.2 < float(active.float().mean()) < 0.95  # both branches exercised
+    # the same micro-batch through the tensor-core path with the clip enabled
+    ctx.reset_arena()
+    eng = TrainingEngine([ctx], global_batch=64, precision=_lib.PRECISION_BF16_TC)
+    eng.add_agent("c", V, D)
+    eng.activate("c")
+    h = eng.handle("c")
+    L = _lib.lib()
+    _lib.check(L.fm_agent_set_weights(h, W0.ctypes.data))
+    _lib.check(L.fm_agent_set_clip(h, eps, old.ctypes.data, M))
+    arr = (_lib.fm_sample * n)(*[_lib.fm_sample(ctx.put(orc.encode(pr)), ctx.put(orc.encode(r)), a)
+                                 for (pr, r), a in zip(samples, adv)])
+    t = C.c_int64()
+    _lib.check(L.fm_train_micro_batch(h, arr, n, 64, C.byref(t)))
+    g = eng.read_grad("c")
+    eng.close()
+    assert rel_fro(g, g_t) < 1e-2
