@@ -556,6 +556,131 @@ def run_c4(args, dist: Dist) -> dict:
                 core_updates_per_epoch=Cn, aux_updates_per_epoch=A)
 
 
+def _best_time(fn, reps=3):
+    fn()
+    best = 1e30
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        best = min(best, time.perf_counter() - t0)
+    return best
+
+
+def run_next(args) -> None:
+    """--next: the SURVEY §8f "next" rows (f1 publish/Get, f2 serialize, f3
+    generate) at C2 dims on one B200, each beside the compiled reference on the
+    host cores (the cpu_baseline leg).  One JSON line per row."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2602_09578_b200 import _lib
+    from paper_2602_09578_b200.engine import Context, seeded_weights
+    V, D = args.next_vocab, args.next_feat
+    P = V * D
+    L = _lib.lib()
+    ctx = Context(0)
+    h = C.c_void_p()
+    _lib.check(L.fm_agent_create(ctx.handle, b"agent0", V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
+    W0 = seeded_weights(V, D, 7).reshape(-1)
+    _lib.check(L.fm_agent_set_weights(h, W0.ctypes.data))
+    out = []
+
+    # ---- f1: publish (device copy; the bf16 copy is the shadow) and Get (host, peer)
+    import torch
+    for dtype, name, esz in ((0, "f64", 8), (2, "bf16", 2)):
+        w = C.c_void_p()
+        t_alloc = _best_time(lambda: (_lib.check(L.fm_publish_weights(h, dtype, C.byref(w))),
+                                      L.fm_weights_destroy(w)), reps=2)
+        _lib.check(L.fm_publish_weights(h, dtype, C.byref(w)))
+        t = _best_time(lambda: _lib.check(L.fm_publish_into(h, w)))
+        nbytes = P * esz
+        rec = {"row": "f1 publish", "dtype": name, "payload_bytes": nbytes, "publish_into_ms": round(t * 1e3, 3),
+               "publish_into_GB_per_s": round(2 * nbytes / t / 1e9, 1),  # read + write, HBM roofline 6,544
+               "publish_new_buffer_ms": round(t_alloc * 1e3, 3)}
+        host = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        tg = _best_time(lambda: _lib.check(L.fm_weights_get(w, C.c_void_p(host.data_ptr()), -1)))
+        rec["get_host_pinned_GB_per_s"] = round(nbytes / tg / 1e9, 1)
+        if torch.cuda.device_count() > 1:  # rollout instance on a peer GPU: one NVLink copy
+            dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda:1")
+            tp = _best_time(lambda: _lib.check(L.fm_weights_get(w, C.c_void_p(dst.data_ptr()), 1)))
+            rec["get_peer_GB_per_s"] = round(nbytes / tp / 1e9, 1)
+            del dst
+        if dtype == 0:
+            # reference: pack_weights copies the V x D f64 matrix into the payload (one memcpy)
+            src = W0.copy()
+            pk = np.empty_like(src)
+            tr = _best_time(lambda: np.copyto(pk, src))
+            rec["reference_pack_GB_per_s_1core"] = round(src.nbytes / tr / 1e9, 2)
+        _lib.check(L.fm_weights_destroy(w))
+        _lib.check(L.fm_ctx_synchronize(ctx.handle))
+        out.append(rec)
+
+    # ---- f2: serialize / deserialize (bytes identical to the reference format)
+    n = C.c_uint64()
+    _lib.check(L.fm_agent_serialize(h, 64, None, 0, C.byref(n)))
+    blob = np.empty(n.value, np.uint8)
+    ts = _best_time(lambda: _lib.check(L.fm_agent_serialize(h, 64, blob.ctypes.data, n.value, C.byref(n))), reps=2)
+    td = _best_time(lambda: _lib.check(L.fm_agent_deserialize(h, 64, blob.ctypes.data, n.value)), reps=2)
+    rec = {"row": "f2 serialize", "bytes": int(n.value), "serialize_GB_per_s": round(n.value / ts / 1e9, 2),
+           "deserialize_GB_per_s": round(n.value / td / 1e9, 2)}
+    try:
+        from oracle import oracle as orc
+        if orc.ref_available():
+            Wm = W0.reshape(V, D)
+            z = np.zeros_like(Wm)
+            tr = _best_time(lambda: orc.ref_serialize_state(0, 0, 0, Wm, z, z), reps=1)
+            rec["reference_serialize_GB_per_s_1core"] = round(n.value / tr / 1e9, 3)
+    except Exception as e:  # noqa: BLE001
+        rec["reference_error"] = str(e)[:200]
+    out.append(rec)
+
+    # ---- f3: generation (token-for-token the reference's sampler, fp64)
+    w = C.c_void_p()
+    _lib.check(L.fm_publish_weights(h, 0, C.byref(w)))
+    rng = np.random.default_rng(5)
+    nreq, maxt = args.next_requests, args.next_tokens
+    prompts = [rng.integers(1, V, size=8).astype(np.int32) for _ in range(nreq)]
+    Pc = np.concatenate(prompts).astype(np.int32)
+    O = np.arange(0, 8 * (nreq + 1), 8, dtype=np.int32)
+    S = rng.integers(1, 2**63, size=nreq, dtype=np.uint64)
+    tok = np.zeros((nreq, maxt), np.int32)
+    lp = np.zeros((nreq, maxt))
+    ln = np.zeros(nreq, np.int32)
+
+    def gen():
+        _lib.check(L.fm_generate(ctx.handle, w, Pc.ctypes.data, O.ctypes.data, nreq, maxt, S.ctypes.data,
+                                 tok.ctypes.data, lp.ctypes.data, ln.ctypes.data))
+    tg = _best_time(gen, reps=2)
+    ntok = int(ln.sum())
+    rec = {"row": "f3 generate", "requests": nreq, "max_tokens": maxt, "tokens": ntok,
+           "gpu_tokens_per_s": round(ntok / tg, 1), "gpu_ms": round(tg * 1e3, 2),
+           "bytes_per_token_W_columns": 4 * V * 32}
+    try:
+        from oracle import oracle as orc
+        if orc.ref_available():
+            th = os.cpu_count() or 1
+            nr = th
+            Wm = W0.reshape(V, D)
+            t0 = time.perf_counter()
+            with ThreadPoolExecutor(th) as ex:
+                res = list(ex.map(lambda i: orc.ref_generate(Wm, prompts[i % nreq], 8, int(S[i % nreq])),
+                                  range(nr)))
+            tr = time.perf_counter() - t0
+            rt = sum(len(r[0]) for r in res)
+            rec.update(reference_tokens_per_s=round(rt / tr, 2), reference_threads=th,
+                       reference_sample=f"{nr} requests x <= 8 tokens")
+            # token-for-token agreement on the first requests' 8-token prefixes
+            agree = all(np.array_equal(tok[i % nreq, :min(8, ln[i % nreq])][:len(res[i][0])], res[i][0])
+                        for i in range(min(nr, nreq)))
+            rec["prefix_identical_to_reference"] = bool(agree)
+    except Exception as e:  # noqa: BLE001
+        rec["reference_error"] = str(e)[:200]
+    out.append(rec)
+    L.fm_weights_destroy(w)
+    L.fm_agent_destroy(h)
+    ctx.close()
+    for r in out:
+        emit(r)
+
+
 def run_e2e(args, cfg, ctx, mine, handles, place, comms, dist, tier) -> dict:
     """Same metric through the public API with HOST payload buffers: each step
     stages that step's encoded token lists host->device inside the timed
@@ -753,6 +878,11 @@ def main():
     ap.add_argument("--agents", type=int, default=0, help="use only the first K agents of the config")
     ap.add_argument("--dp-mode", default="gang", choices=["gang", "allreduce"],
                     help="gang: fused GEMM2 reduce-scatter over NVLink + sharded Adam; allreduce: NCCL")
+    ap.add_argument("--next", action="store_true", help="measure the SURVEY §8f next rows (one GPU)")
+    ap.add_argument("--next-vocab", type=int, default=32000)
+    ap.add_argument("--next-feat", type=int, default=4096)
+    ap.add_argument("--next-requests", type=int, default=256)
+    ap.add_argument("--next-tokens", type=int, default=64)
     ap.add_argument("--c4-policy", default="agent-centric", choices=["agent-centric", "static"],
                     help="C4 only: agent-to-GPU binding policy")
     args = ap.parse_args()
@@ -760,6 +890,10 @@ def main():
     try:
         if args.impl == "reference":
             run_reference(args, dist)
+            return
+        if args.next:
+            if dist.rank == 0:
+                run_next(args)
             return
         from paper_2602_09578_b200 import workload as wl
         cfg = wl.CONFIGS[args.config]

@@ -212,10 +212,14 @@ int fm_agent_state_checksum(fm_agent* a, uint64_t* out);
  * the agent version.  dtype 0 = f64 (reference payload bytes), 1 = f32, 2 = bf16. */
 typedef struct fm_weights fm_weights;
 int fm_publish_weights(fm_agent* a, int dtype, fm_weights** out);
+/* Republish the agent's current weights into an existing buffer (same V x D,
+ * dtype from the buffer): the allocation-free steady-state path. */
+int fm_publish_into(fm_agent* a, fm_weights* w);
 int fm_weights_alloc(fm_ctx* ctx, uint64_t rows, uint64_t cols, int dtype, fm_weights** out);
 int fm_weights_info(const fm_weights* w, int64_t* version, uint64_t* rows, uint64_t* cols, int* dtype,
                     uint64_t* nbytes, int* device);
-/* One Get per rollout consumer (rollout.hpp:510-541): host (dst_device -1) or any GPU (NVLink P2P). */
+/* One Get per rollout consumer (rollout.hpp:510-541): host (dst_device -1) or any GPU (NVLink P2P);
+ * synchronous (returns when the copy has landed), keeps the caller's current device. */
 int fm_weights_get(const fm_weights* w, void* dst, int dst_device);
 /* Sync every rank of a communicator from `root` in one NCCL broadcast (NVLink/NVSwitch). */
 int fm_weights_broadcast(fm_weights* w, fm_comm* c, int root);

@@ -98,6 +98,7 @@ _PROTOS = {
     "fm_gang_connect": (I, [P, P, U64]),
     "fm_gang_detach": (I, [P]),
     "fm_publish_weights": (I, [P, I, C.POINTER(P)]),
+    "fm_publish_into": (I, [P, P]),
     "fm_weights_alloc": (I, [P, U64, U64, I, C.POINTER(P)]),
     "fm_weights_info": (I, [P, PI64, PU64, PU64, C.POINTER(C.c_int), PU64, C.POINTER(C.c_int)]),
     "fm_weights_get": (I, [P, P, I]),

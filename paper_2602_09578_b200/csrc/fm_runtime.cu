@@ -622,6 +622,7 @@ struct GangState {
     float* recv = nullptr;       // [g-1][own_rows][D] partials from the peers
     float* peer_slot[8] = {};    // my slot inside peer o's receive buffer
     __nv_bfloat16* peer_w16[8] = {};
+    uint8_t* peer_base[8] = {};  // peer o's training slot (same layout as ours)
     void* opened[16] = {};       // IPC mappings to close
     int nopened = 0;
     int* d_token = nullptr;      // 1-int all-reduce used as a device barrier
@@ -675,12 +676,18 @@ struct fm_agent {
 
 // Device-side barrier across the gang (defined with the NCCL section below).
 static int gang_barrier(fm_agent* a);
+// Copies a full [V][D] state buffer (slot offset off, elem bytes/param) to dst
+// (host or device), gathering a DP gang's row shards (defined below).
+static int copy_state(fm_agent* a, size_t off, size_t elem, void* dst, cudaStream_t s);
 
 namespace {
 
 size_t dw_elem(const fm_agent* a) { return a->precision == FM_PRECISION_PARITY_F64 ? 8 : 4; }
 
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+size_t slot_off_m(const fm_agent* a) { return align256(a->P * 8); }
+size_t slot_off_v(const fm_agent* a) { return align256(a->P * 8) + align256(a->P * 4); }
 
 size_t slot_bytes(const fm_agent* a) {
     const size_t P = a->P;
@@ -850,17 +857,19 @@ int fm_agent_set_weights(fm_agent* a, const double* W) {
 int fm_agent_read_weights(fm_agent* a, double* W) {
     if (int st = check_active(a)) return st;
     if (int st = set_dev(a->ctx)) return st;
+    if (int st = copy_state(a, 0, 8, W, a->ctx->stream)) return st;
     FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
-    FM_CUDA(cudaMemcpy(W, a->W, a->P * 8, cudaMemcpyDeviceToHost));
     return FM_OK;
 }
 
 int fm_agent_read_moments(fm_agent* a, float* m, float* v, int64_t* step) {
     if (int st = check_active(a)) return st;
     if (int st = set_dev(a->ctx)) return st;
+    if (m)
+        if (int st = copy_state(a, slot_off_m(a), 4, m, a->ctx->stream)) return st;
+    if (v)
+        if (int st = copy_state(a, slot_off_v(a), 4, v, a->ctx->stream)) return st;
     FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
-    if (m) FM_CUDA(cudaMemcpy(m, a->m, a->P * 4, cudaMemcpyDeviceToHost));
-    if (v) FM_CUDA(cudaMemcpy(v, a->v, a->P * 4, cudaMemcpyDeviceToHost));
     if (step) *step = a->step;
     return FM_OK;
 }
@@ -1601,11 +1610,37 @@ int fm_gang_connect(fm_agent* a, const uint8_t* blobs, uint64_t blob_len) {
         const int64_t o_rows = gs->lo[o + 1] - gs->lo[o];
         gs->peer_slot[o] = static_cast<float*>(rbase) + static_cast<size_t>(idx) * o_rows * a->D;
         gs->peer_w16[o] = reinterpret_cast<__nv_bfloat16*>(static_cast<uint8_t*>(sbase) + b.w16_off);
+        gs->peer_base[o] = static_cast<uint8_t*>(sbase);
     }
     gs->connected = true;
     return FM_OK;
     FM_GUARD_END
 }
+
+}  // extern "C"
+
+// A DP-gang agent maintains W / m / v only on its own row shard (the sharded
+// K-adam); the other rows live in the owners' slots, mapped over NVLink at
+// connect.  Outside a gang this is one contiguous copy.
+static int copy_state(fm_agent* a, size_t off, size_t elem, void* dst, cudaStream_t s) {
+    const uint8_t* mine = static_cast<const uint8_t*>(a->slot->base) + off;
+    GangState* gs = a->gang;
+    if (!gs || !gs->connected) {
+        FM_CUDA(cudaMemcpyAsync(dst, mine, a->P * elem, cudaMemcpyDefault, s));
+        return FM_OK;
+    }
+    const size_t row = a->D * elem;
+    for (int o = 0; o < gs->g; ++o) {
+        const int64_t r0 = gs->lo[o], r1 = gs->lo[o + 1];
+        if (r1 <= r0) continue;
+        const uint8_t* src = (o == gs->rank ? mine : gs->peer_base[o] + off) + static_cast<size_t>(r0) * row;
+        FM_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + static_cast<size_t>(r0) * row, src,
+                                static_cast<size_t>(r1 - r0) * row, cudaMemcpyDefault, s));
+    }
+    return FM_OK;
+}
+
+extern "C" {
 
 int fm_gang_detach(fm_agent* a) {
     GangState* gs = a->gang;
@@ -1699,17 +1734,44 @@ int fm_weights_alloc(fm_ctx* c, uint64_t rows, uint64_t cols, int dtype, fm_weig
 int fm_publish_weights(fm_agent* a, int dtype, fm_weights** out) {
     FM_GUARD_BEGIN
     if (int st = check_active(a)) return st;
+    if (int st = fm_weights_alloc(a->ctx, a->V, a->D, dtype, out)) return st;
+    if (int st = fm_publish_into(a, *out)) {
+        fm_weights_destroy(*out);
+        *out = nullptr;
+        return st;
+    }
+    return FM_OK;
+    FM_GUARD_END
+}
+
+// Republish into an existing buffer (same agent dims; dtype taken from w): the
+// steady-state path, no allocation.
+int fm_publish_into(fm_agent* a, fm_weights* w) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
     fm_ctx* c = a->ctx;
-    if (int st = fm_weights_alloc(c, a->V, a->D, dtype, out)) return st;
-    fm_weights* w = *out;
+    if (int st = set_dev(c)) return st;
+    if (w->rows != a->V || w->cols != a->D) return fail(FM_ERR_CONFIG_ERROR, "weights buffer shape mismatch");
+    if (w->device != c->device) return fail(FM_ERR_CONFIG_ERROR, "weights buffer on another GPU");
+    const int dtype = w->dtype;
     w->version = a->version;
     cudaStream_t s = c->stream;
+    const bool sharded = a->gang && a->gang->connected;  // f64 master rows live on their owners
     if (dtype == 0) {
-        FM_CUDA(cudaMemcpyAsync(w->buf, a->W, a->P * 8, cudaMemcpyDeviceToDevice, s));
+        if (int st = copy_state(a, 0, 8, w->buf, s)) return st;
     } else if (dtype == 1) {
-        f64_to_f32_kernel<<<c->num_sms * 8, 256, 0, s>>>(a->W, static_cast<float*>(w->buf), a->P);
+        double* src = a->W;
+        if (sharded) {
+            FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&src), a->P * 8, s));
+            if (int st = copy_state(a, 0, 8, src, s)) return st;
+        }
+        f64_to_f32_kernel<<<c->num_sms * 8, 256, 0, s>>>(src, static_cast<float*>(w->buf), a->P);
         FM_CUDA(cudaGetLastError());
         count_launch();
+        if (sharded) FM_CUDA(cudaFreeAsync(src, s));
+    } else if (a->W16) {
+        // the bf16 shadow IS bf16(W) (same double -> float -> bf16 rounding; full replica in a gang)
+        FM_CUDA(cudaMemcpyAsync(w->buf, a->W16, a->P * 2, cudaMemcpyDeviceToDevice, s));
     } else {
         FM_CUDA(launch_to_bf16(a->W, static_cast<__nv_bfloat16*>(w->buf), a->P, c->num_sms, s));
         count_launch();
@@ -1735,21 +1797,36 @@ int fm_weights_info(const fm_weights* w, int64_t* version, uint64_t* rows, uint6
 // (peer GPUs over NVLink via cudaMemcpyPeer).
 int fm_weights_get(const fm_weights* w, void* dst, int dst_device) {
     FM_GUARD_BEGIN
+    // synchronous: returns when the copy has landed (the caller may free or
+    // republish the source right after); the caller's current device is kept
+    int prev = 0;
+    FM_CUDA(cudaGetDevice(&prev));
+    struct Restore {
+        int d;
+        ~Restore() { cudaSetDevice(d); }
+    } restore{prev};
     FM_CUDA(cudaSetDevice(w->device));
     if (dst_device < 0) {
         FM_CUDA(cudaMemcpy(dst, w->buf, w->nbytes, cudaMemcpyDeviceToHost));
     } else if (dst_device == w->device) {
         FM_CUDA(cudaMemcpy(dst, w->buf, w->nbytes, cudaMemcpyDeviceToDevice));
+        FM_CUDA(cudaDeviceSynchronize());
     } else {
         int can = 0;
         FM_CUDA(cudaDeviceCanAccessPeer(&can, dst_device, w->device));
+        FM_CUDA(cudaSetDevice(dst_device));
         if (can) {
-            FM_CUDA(cudaSetDevice(dst_device));
             cudaError_t pe = cudaDeviceEnablePeerAccess(w->device, 0);
             if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) FM_CUDA(pe);
             cudaGetLastError();
         }
-        FM_CUDA(cudaMemcpyPeer(dst, dst_device, w->buf, w->device, w->nbytes));
+        // one NVLink copy on a private stream of the consumer GPU
+        cudaStream_t st;
+        FM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        const cudaError_t e = cudaMemcpyPeerAsync(dst, dst_device, w->buf, w->device, w->nbytes, st);
+        const cudaError_t e2 = e == cudaSuccess ? cudaStreamSynchronize(st) : e;
+        cudaStreamDestroy(st);
+        FM_CUDA(e2);
     }
     return FM_OK;
     FM_GUARD_END
@@ -1819,12 +1896,14 @@ int fm_agent_serialize(fm_agent* a, int64_t global_batch, uint8_t* out, uint64_t
         p += 16;
     };
     put_hdr(a->V, a->D);
-    FM_CUDA(cudaMemcpy(p, a->W, P * 8, cudaMemcpyDeviceToHost));
+    if (int st = copy_state(a, 0, 8, p, c->stream)) return st;  // gathers a gang's row shards
+    FM_CUDA(cudaStreamSynchronize(c->stream));
     p += P * 8;
     std::vector<float> tmp(P);
-    for (float* src : {a->m, a->v}) {  // fp32 moments widen exactly to f64
+    for (size_t off : {slot_off_m(a), slot_off_v(a)}) {  // fp32 moments widen exactly to f64
         put_hdr(a->V, a->D);
-        FM_CUDA(cudaMemcpy(tmp.data(), src, P * 4, cudaMemcpyDeviceToHost));
+        if (int st = copy_state(a, off, 4, tmp.data(), c->stream)) return st;
+        FM_CUDA(cudaStreamSynchronize(c->stream));
         if (a->step == 0) std::fill(tmp.begin(), tmp.end(), 0.f);
         double* d = reinterpret_cast<double*>(p);
         for (uint64_t i = 0; i < P; ++i) {

@@ -9,6 +9,7 @@ Rank 0 checks delta-W (assembled from the owners' rows in gang mode) and the
 update grad norms against the compiled-reference golden run, with the same
 tolerances as the 1-GPU tensor-core path."""
 import ctypes as C
+import hashlib
 import os
 import sys
 from pathlib import Path
@@ -136,11 +137,31 @@ def main():
     W = np.empty(V * D)
     _lib.check(L.fm_agent_read_weights(h, W.ctypes.data))
     W = W.reshape(V, D)
+    full_ok = True
     if mode == "gang":  # each rank maintains only its own rows of the master weights
         mine = torch.tensor(W[lo[rank]:lo[rank + 1]].copy())
         parts = [None] * world
         dist.all_gather_object(parts, mine)
-        W = torch.cat(parts).numpy()
+        W_owner = torch.cat(parts).numpy()
+        # read_weights / publish(f64) / serialize gather the owners' rows over NVLink:
+        # every rank must see the owner-assembled weights, and identical bytes
+        full_ok = bool(np.array_equal(W, W_owner))
+        w = C.c_void_p()
+        _lib.check(L.fm_publish_weights(h, 0, C.byref(w)))
+        Wp = np.empty(V * D)
+        _lib.check(L.fm_weights_get(w, Wp.ctypes.data, -1))
+        L.fm_weights_destroy(w)
+        full_ok = full_ok and bool(np.array_equal(Wp.reshape(V, D), W_owner))
+        n = C.c_uint64()
+        _lib.check(L.fm_agent_serialize(h, G, None, 0, C.byref(n)))
+        blob = np.empty(n.value, np.uint8)
+        _lib.check(L.fm_agent_serialize(h, G, blob.ctypes.data, n.value, C.byref(n)))
+        digest = [None] * world
+        dist.all_gather_object(digest, hashlib.sha1(blob.tobytes()).hexdigest())
+        full_ok = full_ok and len(set(digest)) == 1
+        if not full_ok:
+            print(f"rank {rank}: gang-sharded state not assembled consistently", flush=True)
+        W = W_owner
     ok = True
     if rank == 0:
         dW, dW_ref = W - f["W0"], f["W"] - f["W0"]
@@ -166,7 +187,7 @@ def main():
         ok = ok and gang_vs_allreduce(ctx, comm, rank, world)
     L.fm_comm_destroy(comm)
     ctx.close()
-    okt = torch.tensor([1 if (ok and same) else 0])
+    okt = torch.tensor([1 if (ok and same and full_ok) else 0])
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
     dist.destroy_process_group()
     sys.exit(0 if okt.item() == 1 else 1)

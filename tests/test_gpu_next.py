@@ -128,6 +128,18 @@ def test_publish_weights_contiguous_buffer(ctx, dtype):
         else:
             want = torch.tensor(W.astype(np.float32)).to(torch.bfloat16).view(torch.int16).numpy()
             assert np.array_equal(host.view(np.int16), want)
+        # republish into the same buffer after another step: new version, new bytes
+        _train_step(ctx, h, f)
+        _lib.check(L().fm_publish_into(h, w))
+        _lib.check(L().fm_weights_info(w, C.byref(ver), None, None, None, None, None))
+        assert ver.value == 2
+        w2 = C.c_void_p()
+        _lib.check(L().fm_publish_weights(h, dtype, C.byref(w2)))
+        fresh = np.zeros(nb.value, np.uint8)
+        _lib.check(L().fm_weights_get(w2, fresh.ctypes.data, -1))
+        L().fm_weights_destroy(w2)
+        _lib.check(L().fm_weights_get(w, host.ctypes.data, -1))
+        assert host.tobytes() == fresh.tobytes()
     finally:
         if w:
             L().fm_weights_destroy(w)
