@@ -209,7 +209,8 @@ int fm_agent_state_checksum(fm_agent* a, uint64_t* out);
 /* ---- weight publish / rollout sync ----------------------------
  * publish_weights (training.hpp:459-467): one contiguous device buffer in
  * pack_weights' single-tensor layout (object_store.hpp:258-273), stamped with
- * the agent version.  dtype 0 = f64 (reference payload bytes), 1 = f32, 2 = bf16. */
+ * the agent version.  dtype 0 = f64 (reference payload bytes), 1 = f32, 2 = bf16,
+ * 3 = f64 transposed [D][V] (rollout layout for fm_generate: coalesced feature reads). */
 typedef struct fm_weights fm_weights;
 int fm_publish_weights(fm_agent* a, int dtype, fm_weights** out);
 /* Republish the agent's current weights into an existing buffer (same V x D,
@@ -227,7 +228,7 @@ int fm_weights_destroy(fm_weights* w);
 
 /* ---- rollout generation on the GPU ----------------------------
  * PolicyModel::generate (policy.hpp:119-130) for n requests from a published
- * f64 weight buffer on ctx's GPU: request i has prompt
+ * f64 weight buffer (dtype 0 or 3) on ctx's GPU: request i has prompt
  * prompts[prompt_off[i]:prompt_off[i+1]] and token seed seeds[i] (the
  * reference derives it as rollout.hpp:640-644); outputs are n x max_tokens
  * row-major (tokens, log pi) and per-request lengths (EOS included). */

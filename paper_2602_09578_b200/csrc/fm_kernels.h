@@ -108,7 +108,8 @@ cudaError_t launch_parity_rows(const double* W, uint64_t V, uint64_t D, int64_t 
                                double* zscratch, double* dWmb, double* logp64, double* loss_acc,
                                cudaStream_t s);
 // Rollout-side generation (policy.hpp:119-130), one CTA per request (k_rollout.cu).
-cudaError_t launch_generate(const double* W, uint64_t V, uint64_t D, const int32_t* prompts,
+// W is [V][D] (transposed = false) or the rollout layout [D][V].
+cudaError_t launch_generate(const double* W, bool transposed, uint64_t V, uint64_t D, const int32_t* prompts,
                             const int32_t* prompt_off, int n_req, int max_tokens, const uint64_t* seeds,
                             double* zbuf, int32_t* out_tok, double* out_logp, int32_t* out_len,
                             cudaStream_t s);

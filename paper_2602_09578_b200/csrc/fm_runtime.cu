@@ -1684,7 +1684,7 @@ struct fm_weights {
     int device = -1;
     void* buf = nullptr;
     uint64_t rows = 0, cols = 0;
-    int dtype = 0;  // 0 f64, 1 f32, 2 bf16
+    int dtype = 0;  // 0 f64, 1 f32, 2 bf16, 3 f64 transposed [D][V] (rollout layout)
     int64_t version = 0;
     uint64_t nbytes = 0;
 };
@@ -1695,7 +1695,22 @@ __global__ void f64_to_f32_kernel(const double* __restrict__ w, float* __restric
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
         o[i] = static_cast<float>(w[i]);
 }
-size_t dtype_bytes(int dt) { return dt == 0 ? 8 : dt == 1 ? 4 : 2; }
+size_t dtype_bytes(int dt) { return dt == 0 || dt == 3 ? 8 : dt == 1 ? 4 : 2; }
+
+// W [V][D] -> Wt [D][V] through 32 x 32 shared-memory tiles (both sides coalesced)
+__global__ void transpose_f64_kernel(const double* __restrict__ w, double* __restrict__ wt, uint64_t V, uint64_t D) {
+    __shared__ double tile[32][33];
+    const uint64_t d0 = static_cast<uint64_t>(blockIdx.x) * 32, v0 = static_cast<uint64_t>(blockIdx.y) * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const uint64_t v = v0 + r, d = d0 + threadIdx.x;
+        if (v < V && d < D) tile[r][threadIdx.x] = w[v * D + d];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const uint64_t d = d0 + r, v = v0 + threadIdx.x;
+        if (v < V && d < D) wt[d * V + v] = tile[threadIdx.x][r];
+    }
+}
 
 void put_u64(std::vector<uint8_t>& v, uint64_t x) {
     const size_t o = v.size();
@@ -1708,7 +1723,8 @@ extern "C" {
 
 int fm_weights_alloc(fm_ctx* c, uint64_t rows, uint64_t cols, int dtype, fm_weights** out) {
     FM_GUARD_BEGIN
-    if (dtype < 0 || dtype > 2) return fail(FM_ERR_INVALID_ARG, "dtype must be 0 (f64), 1 (f32) or 2 (bf16)");
+    if (dtype < 0 || dtype > 3)
+        return fail(FM_ERR_INVALID_ARG, "dtype must be 0 (f64), 1 (f32), 2 (bf16) or 3 (f64 transposed)");
     if (int st = set_dev(c)) return st;
     auto* w = new fm_weights();
     w->device = c->device;
@@ -1766,6 +1782,19 @@ int fm_publish_into(fm_agent* a, fm_weights* w) {
             if (int st = copy_state(a, 0, 8, src, s)) return st;
         }
         f64_to_f32_kernel<<<c->num_sms * 8, 256, 0, s>>>(src, static_cast<float*>(w->buf), a->P);
+        FM_CUDA(cudaGetLastError());
+        count_launch();
+        if (sharded) FM_CUDA(cudaFreeAsync(src, s));
+    } else if (dtype == 3) {
+        // rollout layout: one feature's weights over the vocabulary are contiguous, so the
+        // generator's per-token column reads coalesce
+        double* src = a->W;
+        if (sharded) {
+            FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&src), a->P * 8, s));
+            if (int st = copy_state(a, 0, 8, src, s)) return st;
+        }
+        const dim3 grid(static_cast<unsigned>((a->D + 31) / 32), static_cast<unsigned>((a->V + 31) / 32));
+        transpose_f64_kernel<<<grid, dim3(32, 8), 0, s>>>(src, static_cast<double*>(w->buf), a->V, a->D);
         FM_CUDA(cudaGetLastError());
         count_launch();
         if (sharded) FM_CUDA(cudaFreeAsync(src, s));
@@ -2023,7 +2052,8 @@ int fm_agent_deserialize(fm_agent* a, int64_t global_batch, const uint8_t* in, u
 int fm_generate(fm_ctx* c, const fm_weights* w, const int32_t* prompts, const int32_t* prompt_off, int n,
                 int max_tokens, const uint64_t* seeds, int32_t* out_tokens, double* out_logp, int32_t* out_len) {
     FM_GUARD_BEGIN
-    if (w->dtype != 0) return fail(FM_ERR_CONFIG_ERROR, "generation reads f64 weights (publish with dtype 0)");
+    if (w->dtype != 0 && w->dtype != 3)
+        return fail(FM_ERR_CONFIG_ERROR, "generation reads f64 weights (publish with dtype 0 or 3)");
     if (w->device != c->device) return fail(FM_ERR_CONFIG_ERROR, "weights live on another GPU (fm_weights_get)");
     if (n <= 0 || max_tokens <= 0) return FM_OK;
     if (int st = set_dev(c)) return st;
@@ -2043,8 +2073,8 @@ int fm_generate(fm_ctx* c, const fm_weights* w, const int32_t* prompts, const in
     if (np) FM_CUDA(cudaMemcpyAsync(dp, prompts, np * 4, cudaMemcpyHostToDevice, s));
     FM_CUDA(cudaMemcpyAsync(doff, prompt_off, (n + 1) * 4, cudaMemcpyHostToDevice, s));
     FM_CUDA(cudaMemcpyAsync(dseed, seeds, n * 8, cudaMemcpyHostToDevice, s));
-    FM_CUDA(launch_generate(static_cast<const double*>(w->buf), w->rows, w->cols, dp, doff, n, max_tokens, dseed, dz,
-                            dtok, dlp, dlen, s));
+    FM_CUDA(launch_generate(static_cast<const double*>(w->buf), w->dtype == 3, w->rows, w->cols, dp, doff, n,
+                            max_tokens, dseed, dz, dtok, dlp, dlen, s));
     count_launch();
     FM_CUDA(cudaMemcpyAsync(out_tokens, dtok, nt * 4, cudaMemcpyDeviceToHost, s));
     FM_CUDA(cudaMemcpyAsync(out_logp, dlp, nt * 8, cudaMemcpyDeviceToHost, s));

@@ -29,6 +29,9 @@ __device__ __forceinline__ uint64_t splitmix(uint64_t& s) {
 
 constexpr int kThreads = 256;
 
+// kTransposed: W is the rollout layout Wt [D][V] (fm_publish dtype 3): the
+// per-token reads of a context feature's weights are contiguous over v.
+template <bool kTransposed>
 __global__ void __launch_bounds__(kThreads) generate_kernel(const double* __restrict__ W, uint64_t V, uint64_t D,
                                                             const int32_t* __restrict__ prompts,
                                                             const int32_t* __restrict__ prompt_off,
@@ -87,7 +90,10 @@ __global__ void __launch_bounds__(kThreads) generate_kernel(const double* __rest
         double lmax = -INFINITY;
         for (uint64_t v = tid; v < V; v += kThreads) {
             double s = 0.0;
-            for (int k = 0; k < nf; ++k) s = __dadd_rn(s, __dmul_rn(W[v * D + s_f[k]], s_phi[k]));
+            for (int k = 0; k < nf; ++k) {
+                const double wv = kTransposed ? __ldg(W + s_f[k] * V + v) : W[v * D + s_f[k]];
+                s = __dadd_rn(s, __dmul_rn(wv, s_phi[k]));
+            }
             z[v] = s;
             lmax = fmax(lmax, s);
         }
@@ -156,12 +162,16 @@ __global__ void __launch_bounds__(kThreads) generate_kernel(const double* __rest
 
 }  // namespace
 
-cudaError_t launch_generate(const double* W, uint64_t V, uint64_t D, const int32_t* prompts, const int32_t* prompt_off,
-                            int n_req, int max_tokens, const uint64_t* seeds, double* zbuf, int32_t* out_tok,
-                            double* out_logp, int32_t* out_len, cudaStream_t s) {
+cudaError_t launch_generate(const double* W, bool transposed, uint64_t V, uint64_t D, const int32_t* prompts,
+                            const int32_t* prompt_off, int n_req, int max_tokens, const uint64_t* seeds, double* zbuf,
+                            int32_t* out_tok, double* out_logp, int32_t* out_len, cudaStream_t s) {
     if (n_req == 0) return cudaSuccess;
-    generate_kernel<<<n_req, kThreads, 0, s>>>(W, V, D, prompts, prompt_off, max_tokens, seeds, zbuf, out_tok,
-                                               out_logp, out_len);
+    if (transposed)
+        generate_kernel<true><<<n_req, kThreads, 0, s>>>(W, V, D, prompts, prompt_off, max_tokens, seeds, zbuf,
+                                                         out_tok, out_logp, out_len);
+    else
+        generate_kernel<false><<<n_req, kThreads, 0, s>>>(W, V, D, prompts, prompt_off, max_tokens, seeds, zbuf,
+                                                          out_tok, out_logp, out_len);
     return cudaGetLastError();
 }
 

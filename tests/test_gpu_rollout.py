@@ -23,8 +23,9 @@ def _dec(b):
     return wl.decode_tokens(b)
 
 
+@pytest.mark.parametrize("layout", [0, 3])  # published f64 [V][D] or the transposed rollout layout
 @pytest.mark.parametrize("name", ["c1_planner", "c1_executor"])
-def test_generate_matches_reference(ctx, name):
+def test_generate_matches_reference(ctx, name, layout):
     f = np.load(GOLD / f"{name}.npz")
     agent = str(f["agent"])
     V, D = int(f["V"]), int(f["D"])
@@ -33,9 +34,14 @@ def test_generate_matches_reference(ctx, name):
     W0 = np.ascontiguousarray(f["W0"])  # named: a temporary could be freed before the C call reads it
     _lib.check(L().fm_agent_set_weights(h, W0.ctypes.data))
     w = C.c_void_p()
-    _lib.check(L().fm_publish_weights(h, 0, C.byref(w)))
+    _lib.check(L().fm_publish_weights(h, layout, C.byref(w)))
     Wpub = np.zeros((V, D))
-    _lib.check(L().fm_weights_get(w, Wpub.ctypes.data, -1))
+    if layout == 3:
+        Wt = np.zeros((D, V))
+        _lib.check(L().fm_weights_get(w, Wt.ctypes.data, -1))
+        Wpub = np.ascontiguousarray(Wt.T)
+    else:
+        _lib.check(L().fm_weights_get(w, Wpub.ctypes.data, -1))
     if not np.array_equal(Wpub, f["W0"]):
         Wa = np.zeros((V, D))
         _lib.check(L().fm_agent_read_weights(h, Wa.ctypes.data))
