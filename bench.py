@@ -352,6 +352,11 @@ def run_ours(args, dist: Dist) -> dict | None:
     Mpad = int(np.ceil(M_local / 128) * 128)
     bytes_sg = 4.0 * V * Mpad            # read p~ bf16 + write G^T bf16
     bytes_adam = 38.0 * P                # r: w8 m4 v4 g4; w: w8 m4 v4 shadow2
+    g_adam = len(place[mine[0]]) if mine and args.dp_mode == "gang" else 1
+    if g_adam > 1:
+        # sharded K-adam on P/g params: + the g-1 received fp32 partials read; the
+        # bf16 rows it writes into the g-1 peers' shadows go over NVLink, not local HBM
+        bytes_adam = (38.0 + 4.0 * (g_adam - 1)) * P / g_adam
     bytes_lse = M_local * (np.ceil(V / 256) * 8 + 24)
     kernels = {}
     for i, name in enumerate(KINDS):

@@ -299,6 +299,75 @@ int fm_store_complete(fm_store* s, const char* agent, const int64_t* handles, in
 /* purge_stale (experience_store.hpp:118-132) */
 int fm_store_purge_stale(fm_store* s, const char* agent, int64_t current_version, uint64_t* out);
 
+/* ---- on-device experience table (experience_store.hpp:19-276) --
+ * One agent's table kept in the HBM of ctx's GPU: cells (f64 by value, ref
+ * columns as token-arena offsets), status flags, processing marks and the
+ * canonical key of every record.  The host keeps only the record keys (to
+ * raise the reference's synchronous errors: DuplicateSample, RecordNotFound,
+ * CellAlreadySet, NotProcessing ...).  The poll's selection, the trainer's
+ * micro-batch descriptors, group release (rule_reward + group_advantages) and
+ * GPU-generated responses never leave HBM; a poll returns only the chosen slots
+ * and the row count the GEMM shapes need.  Records are addressed by the slot
+ * insert returns.  Table ops run in call order on the table's own stream, so a
+ * poll overlaps the agent's in-flight micro-batch. */
+typedef struct fm_dtable fm_dtable;
+/* create_table (experience_store.hpp:24-36); capacity = max live records, <= 1<<20 */
+int fm_dtable_create(fm_ctx* ctx, const char* agent, const char* const* col_names, const int* col_types,
+                     int ncols, int64_t capacity, fm_dtable** out);
+int fm_dtable_destroy(fm_dtable* t);
+/* insert (experience_store.hpp:44-59), n records of one policy version; all-or-nothing */
+int fm_dtable_insert(fm_dtable* t, int64_t version, int n, const char* const* input_ids, const int* turns,
+                     const int* trajs, int64_t* slots_out);
+/* find (experience_store.hpp:196-201): *slot_out = -1 when absent */
+int fm_dtable_find(fm_dtable* t, const char* input_id, int turns, int traj, int64_t version, int64_t* slot_out);
+/* set_cell by value (experience_store.hpp:61-80), n cells of one column; all-or-nothing */
+int fm_dtable_set_float(fm_dtable* t, const char* column, int n, const int64_t* slots, const double* values);
+/* set_cell_payload (experience_store.hpp:82-88): codec bytes ([u64 n][u64 x] * n) into the arena */
+int fm_dtable_set_payload(fm_dtable* t, const char* column, int64_t slot, const uint8_t* payload, uint64_t nbytes);
+/* Rollout completion on the GPU (rollout.hpp:715-731 with PolicyModel::generate, policy.hpp:119-130)
+ * for n records: responses from published f64 weights (dtype 0 or 3) are encoded into the arena
+ * and set as `response_col` (+ `logprob_col` as [u64 n][f64] * n, or NULL); prompts/seeds as fm_generate. */
+int fm_dtable_generate(fm_dtable* t, const fm_weights* w, const char* response_col, const char* logprob_col,
+                       int n, const int64_t* slots, const int32_t* prompts, const int32_t* prompt_off,
+                       int max_tokens, const uint64_t* seeds);
+/* release_group (rollout.hpp:812-834) for ngroups groups of survivors seg_off[g]..seg_off[g+1]:
+ * survivor i's reward = rule_reward(response cell of slot score_slot[i] in tables[score_tab[i]],
+ * pattern) (training.hpp:71-83) computed from the arena; advantages = group_advantages(eps)
+ * (training.hpp:54-67, bit-identical order); both written to the reward/adv columns of records
+ * rec_slot[rec_off[i]..rec_off[i+1]) (tables[rec_tab[.]]).  All tables share one GPU.
+ * rewards_out/adv_out (host, one per survivor) may be NULL. */
+int fm_dtable_release_groups(fm_dtable* const* tables, int ntables, const char* response_col,
+                             const char* reward_col, const char* adv_col, int ngroups, const int32_t* seg_off,
+                             const int32_t* score_tab, const int64_t* score_slot, const int32_t* rec_off,
+                             const int32_t* rec_tab, const int64_t* rec_slot, const int32_t* pattern,
+                             int npattern, double eps, double* rewards_out, double* adv_out);
+/* poll_micro_batch (experience_store.hpp:92-114) on the GPU: canonical-first mb (<= 1024) ready
+ * records of `version`, marked processing; *got = mb with slots_out in canonical order and
+ * *rows_out = their response tokens, or *got = 0 (nullopt).  Column names may be NULL for a
+ * selection without trainer descriptors.  *poll_id names the descriptors for fm_train_polled. */
+int fm_dtable_poll(fm_dtable* t, int64_t version, int64_t mb, const char* prompt_col,
+                   const char* response_col, const char* adv_col, int64_t* slots_out, int64_t* rows_out,
+                   int64_t* got, int64_t* poll_id);
+/* train_micro_batch (training.hpp:355-430) on a device poll's micro batch: the descriptors
+ * are copied D2D from the table's ring (the last 8 polls); same ticket/report as fm_train_micro_batch. */
+int fm_train_polled(fm_agent* a, fm_dtable* t, int64_t poll_id, int64_t global_batch, int64_t* ticket_out);
+/* complete (experience_store.hpp:134-148): NotProcessing unless every slot is processing */
+int fm_dtable_complete(fm_dtable* t, const int64_t* slots, int n);
+/* purge_stale (experience_store.hpp:118-132) / purge_inputs (:153-164): device scans */
+int fm_dtable_purge_stale(fm_dtable* t, int64_t current_version, uint64_t* out);
+int fm_dtable_purge_inputs(fm_dtable* t, const char* const* input_ids, int n, uint64_t* out);
+/* drop_record (experience_store.hpp:166-175): *dropped = 0 if absent or processing */
+int fm_dtable_drop_record(fm_dtable* t, const char* input_id, int turns, int traj, int64_t version,
+                          int* dropped);
+/* ready_count (experience_store.hpp:181-187, counted on the GPU) / record_count (:189-191) */
+int fm_dtable_ready_count(fm_dtable* t, int64_t version, uint64_t* out);
+int fm_dtable_record_count(fm_dtable* t, uint64_t* out);
+/* Identity and flags of a slot's record (dump_table view, experience_store.hpp:210-238). */
+int fm_dtable_record(fm_dtable* t, int64_t slot, char* input_id_out, size_t cap, int* turns, int* traj,
+                     int64_t* version, int* processing, uint32_t* status);
+/* Cells of n slots read back from HBM: by-value columns as f64, ref columns as arena offsets. */
+int fm_dtable_read_cells(fm_dtable* t, const char* column, int n, const int64_t* slots, uint64_t* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,7 +4,7 @@
  * function follows the reference arithmetic operation-for-operation (same
  * summation order, same libm calls) so that it agrees bit-for-bit with the
  * compiled reference (oracle/_ref) on every golden vector.  Parity pinned by
- * tests/test_oracle.py against tests/golden/*.npz and, when oracle/_ref is
+ * tests/test_oracle.py against the tests/golden npz fixtures and, when oracle/_ref is
  * built, against the live reference.
  */
 #define _GNU_SOURCE

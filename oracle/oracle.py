@@ -119,6 +119,8 @@ def rlib() -> C.CDLL:
         L.ref_deserialize_state.argtypes = [P, U64, P, P, P, P, P]
         L.ref_poll_order.restype = I
         L.ref_poll_order.argtypes = [I, P, P, P, P, P, I64, I64, P]
+        L.ref_store_script.restype = U64
+        L.ref_store_script.argtypes = [C.c_char_p, C.c_char_p, U64]
         _r = L
     return _r
 
@@ -297,3 +299,14 @@ def ref_deserialize_state(blob: bytes, P_: int) -> dict:
     if rc != 0:
         raise RuntimeError(rlib().ref_last_error().decode())
     return dict(rows=int(r[0]), cols=int(c[0]), W=W, version=int(ver[0]), cache_n=int(cn[0]))
+
+
+def ref_store_script(script: str) -> str:
+    """Replays a store lifecycle script on the reference ExperienceStore (oracle/_ref)."""
+    L = rlib()
+    n = L.ref_store_script(script.encode(), None, 0)
+    if n == 0:
+        raise RuntimeError(L.ref_last_error().decode())
+    buf = C.create_string_buffer(int(n))
+    L.ref_store_script(script.encode(), buf, n)
+    return buf.value.decode()

@@ -17,7 +17,9 @@
 // bench.py's reference arm / cpu_baseline leg.  Never linked into the product.
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -343,6 +345,208 @@ int ref_deserialize_state(const std::uint8_t* in, std::uint64_t len, std::uint64
         g_err = e.what();
         return 1;
     }
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Experience-store lifecycle script (SURVEY §8f-4 golden vectors).
+//
+// Replays a text script against the reference's own ExperienceStore on one
+// table with the orchestrator's schema (orchestrator.hpp:191-195: prompt List,
+// response List, logprobs Tensor, reward Float, advantage Float) and writes
+// one result line per op.  Group release follows RolloutEngine::release_group
+// (rollout.hpp:812-834): rule_reward on each survivor's scored response,
+// group_advantages over the survivors, both cells set on every listed record.
+//   insert V id t j              -> "ok" | "err <fm_status>"
+//   setf V id t j col <hexfloat> -> "ok" | "err .."
+//   setp V id t j col n x1..xn   -> "ok" | "err .."   (token list payload)
+//   poll V mb                    -> "none" | "id_t_j@V:<adv hexfloat> ..." | "err .."
+//   complete k (V id t j)*k      -> "ok" | "err .."
+//   purge_stale V                -> "<count>"
+//   purge_inputs k id*k          -> "<count>"
+//   drop V id t j                -> "0" | "1"
+//   ready V                      -> "<count>"
+//   count                        -> "<count>"
+//   release eps np p*np ns (V id t j nrec (V id t j)*nrec)*ns
+//                                -> "<reward hex>/<adv hex> ..." | "err .."
+// ---------------------------------------------------------------------------
+namespace {
+// whitespace tokenizer (no iostreams: the driver's static libstdc++ is not
+// initialised for them when loaded into Python)
+struct Toks {
+    std::vector<std::string> v;
+    std::size_t i = 0;
+    explicit Toks(const std::string& line) {
+        std::size_t p = 0;
+        while (p < line.size()) {
+            while (p < line.size() && (line[p] == ' ' || line[p] == '\t' || line[p] == '\r')) ++p;
+            std::size_t q = p;
+            while (q < line.size() && line[q] != ' ' && line[q] != '\t' && line[q] != '\r') ++q;
+            if (q > p) v.push_back(line.substr(p, q - p));
+            p = q;
+        }
+    }
+    std::string str() { return i < v.size() ? v[i++] : std::string(); }
+    long long num() { return std::strtoll(str().c_str(), nullptr, 10); }
+    Toks& operator>>(std::string& x) { x = str(); return *this; }
+    Toks& operator>>(int& x) { x = static_cast<int>(num()); return *this; }
+    Toks& operator>>(std::int64_t& x) { x = num(); return *this; }
+    Toks& operator>>(std::size_t& x) { x = static_cast<std::size_t>(num()); return *this; }
+};
+}  // namespace
+
+extern "C" {
+
+std::uint64_t ref_store_script(const char* script, char* out, std::uint64_t cap) {
+    std::string res;
+    try {
+        EventLoop loop;
+        Cluster cluster(1, 1, 1ULL << 40, 1ULL << 40);
+        EventLog log;
+        ObjectStore objects(loop, cluster, log);
+        ExperienceStore exp(objects);
+        const std::string A = "agent";
+        exp.create_table(TableSchema{A,
+                                     {{"prompt", ColumnType::List},
+                                      {"response", ColumnType::List},
+                                      {"logprobs", ColumnType::Tensor},
+                                      {"reward", ColumnType::Float},
+                                      {"advantage", ColumnType::Float}}});
+        std::map<std::tuple<std::string, int, int, std::int64_t>, std::vector<Token>> responses;
+        const std::string text(script);
+        std::size_t pos = 0;
+        char buf[64];
+        auto hexf = [&](double x) {
+            std::snprintf(buf, sizeof buf, "%a", x);
+            return std::string(buf);
+        };
+        while (pos < text.size()) {
+            std::size_t nl = text.find('\n', pos);
+            if (nl == std::string::npos) nl = text.size();
+            const std::string line = text.substr(pos, nl - pos);
+            pos = nl + 1;
+            if (line.empty()) continue;
+            Toks ls(line);
+            std::string op;
+            ls >> op;
+            std::string r;
+            try {
+                if (op == "insert") {
+                    std::int64_t v; std::string id; int t, j;
+                    ls >> v >> id >> t >> j;
+                    exp.insert(A, v, SampleId{id, t, j});
+                    r = "ok";
+                } else if (op == "setf") {
+                    std::int64_t v; std::string id, col, x; int t, j;
+                    ls >> v >> id >> t >> j >> col >> x;
+                    exp.set_cell(A, SampleId{id, t, j}, v, col, CellValue::of_float(std::strtod(x.c_str(), nullptr)));
+                    r = "ok";
+                } else if (op == "setp") {
+                    std::int64_t v; std::string id, col; int t, j; std::size_t n;
+                    ls >> v >> id >> t >> j >> col >> n;
+                    std::vector<Token> toks(n);
+                    for (auto& x : toks) ls >> x;
+                    exp.set_cell_payload(A, SampleId{id, t, j}, v, col, encode_tokens(toks), 0);
+                    if (col == "response") responses[{id, t, j, v}] = toks;
+                    r = "ok";
+                } else if (op == "poll") {
+                    std::int64_t v; std::size_t mb;
+                    ls >> v >> mb;
+                    auto b = exp.poll_micro_batch(A, v, mb);
+                    if (!b) {
+                        r = "none";
+                    } else {
+                        const int ac = exp.schema(A).column_index("advantage");
+                        for (const SampleRecord& rec : b->samples) {
+                            if (!r.empty()) r += ' ';
+                            r += rec.sample_id.render() + "@" + std::to_string(rec.policy_version) + ":" +
+                                 hexf(rec.data[static_cast<std::size_t>(ac)].as_float());
+                        }
+                    }
+                } else if (op == "complete") {
+                    int k;
+                    ls >> k;
+                    std::vector<SampleRecord> recs;
+                    for (int i = 0; i < k; ++i) {
+                        std::int64_t v; std::string id; int t, j;
+                        ls >> v >> id >> t >> j;
+                        SampleRecord sr;
+                        sr.policy_version = v;
+                        sr.sample_id = SampleId{id, t, j};
+                        recs.push_back(sr);
+                    }
+                    exp.complete(A, recs);
+                    r = "ok";
+                } else if (op == "purge_stale") {
+                    std::int64_t v;
+                    ls >> v;
+                    r = std::to_string(exp.purge_stale(A, v));
+                } else if (op == "purge_inputs") {
+                    int k;
+                    ls >> k;
+                    std::set<std::string> ids;
+                    for (int i = 0; i < k; ++i) {
+                        std::string id;
+                        ls >> id;
+                        ids.insert(id);
+                    }
+                    r = std::to_string(exp.purge_inputs(A, ids));
+                } else if (op == "drop") {
+                    std::int64_t v; std::string id; int t, j;
+                    ls >> v >> id >> t >> j;
+                    r = exp.drop_record(A, SampleId{id, t, j}, v) ? "1" : "0";
+                } else if (op == "ready") {
+                    std::int64_t v;
+                    ls >> v;
+                    r = std::to_string(exp.ready_count(A, v));
+                } else if (op == "count") {
+                    r = std::to_string(exp.record_count(A));
+                } else if (op == "release") {
+                    double eps; int np, ns;
+                    std::string epss;
+                    ls >> epss >> np;
+                    eps = std::strtod(epss.c_str(), nullptr);
+                    std::vector<Token> pat(static_cast<std::size_t>(np));
+                    for (auto& x : pat) ls >> x;
+                    ls >> ns;
+                    std::vector<double> rewards;
+                    std::vector<std::vector<std::pair<SampleId, std::int64_t>>> recs(static_cast<std::size_t>(ns));
+                    for (int i = 0; i < ns; ++i) {
+                        std::int64_t v; std::string id; int t, j, nrec;
+                        ls >> v >> id >> t >> j >> nrec;
+                        rewards.push_back(rule_reward(responses.at({id, t, j, v}), pat));
+                        for (int q = 0; q < nrec; ++q) {
+                            std::int64_t v2; std::string id2; int t2, j2;
+                            ls >> v2 >> id2 >> t2 >> j2;
+                            recs[static_cast<std::size_t>(i)].push_back({SampleId{id2, t2, j2}, v2});
+                        }
+                    }
+                    const std::vector<double> adv = group_advantages(rewards, eps);
+                    for (int i = 0; i < ns; ++i) {
+                        for (const auto& [sid, v] : recs[static_cast<std::size_t>(i)]) {
+                            exp.set_cell(A, sid, v, "reward", CellValue::of_float(rewards[static_cast<std::size_t>(i)]));
+                            exp.set_cell(A, sid, v, "advantage", CellValue::of_float(adv[static_cast<std::size_t>(i)]));
+                        }
+                        if (!r.empty()) r += ' ';
+                        r += hexf(rewards[static_cast<std::size_t>(i)]) + "/" + hexf(adv[static_cast<std::size_t>(i)]);
+                    }
+                    if (r.empty()) r = "ok";
+                } else {
+                    r = "bad-op";
+                }
+            } catch (const Error& e) {
+                r = "err " + std::to_string(static_cast<int>(e.code()) + 1);
+            }
+            res += r;
+            res += '\n';
+        }
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 0;
+    }
+    if (out && cap > res.size()) std::memcpy(out, res.c_str(), res.size() + 1);
+    return res.size() + 1;
 }
 
 }  // extern "C"

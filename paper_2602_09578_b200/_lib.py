@@ -119,6 +119,26 @@ _PROTOS = {
     "fm_store_record_id": (I, [P, S, I64, S, C.c_size_t, C.POINTER(C.c_int), C.POINTER(C.c_int), PI64]),
     "fm_store_complete": (I, [P, S, P, I64]),
     "fm_store_purge_stale": (I, [P, S, I64, PU64]),
+    # on-device experience table
+    "fm_dtable_create": (I, [P, S, P, P, I, I64, C.POINTER(P)]),
+    "fm_dtable_destroy": (I, [P]),
+    "fm_dtable_insert": (I, [P, I64, I, P, P, P, P]),
+    "fm_dtable_find": (I, [P, S, I, I, I64, PI64]),
+    "fm_dtable_set_float": (I, [P, S, I, P, P]),
+    "fm_dtable_set_payload": (I, [P, S, I64, P, U64]),
+    "fm_dtable_generate": (I, [P, P, S, S, I, P, P, P, I, P]),
+    "fm_dtable_release_groups": (I, [P, I, S, S, S, I, P, P, P, P, P, P, P, I, D, P, P]),
+    "fm_dtable_poll": (I, [P, I64, I64, S, S, S, P, PI64, PI64, PI64]),
+    "fm_train_polled": (I, [P, P, I64, I64, PI64]),
+    "fm_dtable_complete": (I, [P, P, I]),
+    "fm_dtable_purge_stale": (I, [P, I64, PU64]),
+    "fm_dtable_purge_inputs": (I, [P, P, I, PU64]),
+    "fm_dtable_drop_record": (I, [P, S, I, I, I64, C.POINTER(C.c_int)]),
+    "fm_dtable_ready_count": (I, [P, I64, PU64]),
+    "fm_dtable_record_count": (I, [P, PU64]),
+    "fm_dtable_record": (I, [P, I64, S, C.c_size_t, C.POINTER(C.c_int), C.POINTER(C.c_int), PI64,
+                             C.POINTER(C.c_int), C.POINTER(C.c_uint32)]),
+    "fm_dtable_read_cells": (I, [P, S, I, P, P]),
 }
 
 # every symbol the header declares (checked by tests/test_abi.py)

@@ -543,7 +543,7 @@ int fm_ctx_reserve(fm_ctx* c, uint64_t arena_bytes, int64_t max_rows, uint64_t V
     FM_GUARD_BEGIN
     if (int st = set_dev(c)) return st;
     if (arena_bytes > c->arena_cap) {
-        FM_CUDA(cudaStreamSynchronize(c->stream));
+        FM_CUDA(cudaDeviceSynchronize());  // every stream reading the arena (compute, on-device tables)
         uint8_t* na = nullptr;
         if (cudaMalloc(&na, arena_bytes) != cudaSuccess) return fail(FM_ERR_DEVICE_OOM, "token arena");
         if (c->arena_used) FM_CUDA(cudaMemcpy(na, c->arena, c->arena_used, cudaMemcpyDeviceToDevice));
@@ -924,7 +924,10 @@ int fm_agent_set_shard(fm_agent* a, int rank, int nranks) {
 // ---------------------------------------------------------------------------
 // the micro-batch pipeline
 // ---------------------------------------------------------------------------
-static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total, int64_t G, int64_t* ticket_out) {
+// hsd: host descriptors (staged H2D), or dsd: descriptors already in HBM (the
+// on-device experience table's poll), ready when `dsd_ready` completes.
+static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total, int64_t G, int64_t* ticket_out,
+                      const SampleDesc* dsd = nullptr, cudaEvent_t dsd_ready = nullptr) {
     // data-parallel gang: this rank trains rows [row_lo, row_hi) of the micro-batch
     const int64_t row_lo = M_total * a->shard_rank / a->shard_count;
     const int64_t row_hi = M_total * (a->shard_rank + 1) / a->shard_count;
@@ -940,13 +943,19 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
         if (int st = ws_reserve_parity(c, M, a->V, a->P)) return st;
     }
     if (int st = ws_reserve_sd(c, n)) return st;
-    // descriptors -> device through pinned staging
-    uint8_t* stg;
-    cudaEvent_t sev;
-    if (int st = staging_acquire(c, sizeof(SampleDesc) * n, &stg, &sev)) return st;
-    std::memcpy(stg, hsd, sizeof(SampleDesc) * n);
-    FM_CUDA(cudaMemcpyAsync(w.sd, stg, sizeof(SampleDesc) * n, cudaMemcpyHostToDevice, s));
-    FM_CUDA(cudaEventRecord(sev, s));
+    if (dsd) {
+        // descriptors built in HBM by the device poll: order after it, copy D2D
+        if (dsd_ready) FM_CUDA(cudaStreamWaitEvent(s, dsd_ready, 0));
+        if (n) FM_CUDA(cudaMemcpyAsync(w.sd, dsd, sizeof(SampleDesc) * n, cudaMemcpyDeviceToDevice, s));
+    } else {
+        // descriptors -> device through pinned staging
+        uint8_t* stg;
+        cudaEvent_t sev;
+        if (int st = staging_acquire(c, sizeof(SampleDesc) * n, &stg, &sev)) return st;
+        std::memcpy(stg, hsd, sizeof(SampleDesc) * n);
+        FM_CUDA(cudaMemcpyAsync(w.sd, stg, sizeof(SampleDesc) * n, cudaMemcpyHostToDevice, s));
+        FM_CUDA(cudaEventRecord(sev, s));
+    }
 
     const int64_t ticket = a->next_ticket++;
     const int slot = static_cast<int>(ticket % kReportRing);
@@ -2089,3 +2098,81 @@ int fm_generate(fm_ctx* c, const fm_weights* w, const int32_t* prompts, const in
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// internal hooks for the on-device experience table (fm_dtable.cu)
+// ---------------------------------------------------------------------------
+namespace fm {
+int ctx_device(const fm_ctx* c) { return c->device; }
+cudaStream_t ctx_stream(const fm_ctx* c) { return c->stream; }
+uint8_t* ctx_arena(const fm_ctx* c) { return c->arena; }
+int ctx_staging(fm_ctx* c, size_t bytes, uint8_t** out, cudaEvent_t* ev) { return staging_acquire(c, bytes, out, ev); }
+fm_ctx* agent_ctx(const fm_agent* a) { return a->ctx; }
+int agent_check_active(fm_agent* a) { return check_active(a); }
+
+int ctx_arena_alloc(fm_ctx* c, uint64_t bytes, uint64_t* off_out) {
+    if (int st = set_dev(c)) return st;
+    const uint64_t off = round_up(c->arena_used, 16);
+    if (off + bytes > c->arena_cap) {
+        const uint64_t cap = std::max<uint64_t>(2 * c->arena_cap, off + bytes + (64u << 20));
+        if (int st = fm_ctx_reserve(c, cap, 0, 0, 0)) return st;
+    }
+    c->arena_used = off + bytes;
+    *off_out = off;
+    return FM_OK;
+}
+
+int train_device_desc(fm_agent* a, const SampleDesc* dsd, int n, int64_t M_total, int64_t G, cudaEvent_t ready,
+                      int64_t* ticket_out) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
+    if (G <= 0) return fail(FM_ERR_CONFIG_ERROR, "global batch must be positive");
+    if (int st = set_dev(a->ctx)) return st;
+    return train_impl(a, nullptr, n, M_total, G, ticket_out, dsd, ready);
+    FM_GUARD_END
+}
+
+// K-generate into device buffers (caller frees them on ctx's stream)
+int generate_device(fm_ctx* c, const fm_weights* w, const int32_t* prompts, const int32_t* prompt_off, int n,
+                    int max_tokens, const uint64_t* seeds, GenBuffers* out) {
+    if (w->dtype != 0 && w->dtype != 3)
+        return fail(FM_ERR_CONFIG_ERROR, "generation reads f64 weights (publish with dtype 0 or 3)");
+    if (w->device != c->device) return fail(FM_ERR_CONFIG_ERROR, "weights live on another GPU (fm_weights_get)");
+    if (int st = set_dev(c)) return st;
+    cudaStream_t s = c->stream;
+    const int np = prompt_off[n];
+    const size_t nt = static_cast<size_t>(n) * max_tokens;
+    *out = GenBuffers{};
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out->prompts), std::max(np, 1) * 4, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out->prompt_off), (n + 1) * 4, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out->seeds), n * 8, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out->z), static_cast<size_t>(n) * w->rows * 8, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out->tok), nt * 4, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out->logp), nt * 8, s));
+    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&out->len), n * 4, s));
+    uint8_t* stg;
+    cudaEvent_t ev;
+    const size_t bytes = static_cast<size_t>(np) * 4 + (n + 1) * 4 + n * 8;
+    if (int st = staging_acquire(c, bytes, &stg, &ev)) return st;
+    std::memcpy(stg, seeds, n * 8);
+    std::memcpy(stg + n * 8, prompt_off, (n + 1) * 4);
+    if (np) std::memcpy(stg + n * 8 + (n + 1) * 4, prompts, np * 4);
+    FM_CUDA(cudaMemcpyAsync(out->seeds, stg, n * 8, cudaMemcpyHostToDevice, s));
+    FM_CUDA(cudaMemcpyAsync(out->prompt_off, stg + n * 8, (n + 1) * 4, cudaMemcpyHostToDevice, s));
+    if (np) FM_CUDA(cudaMemcpyAsync(out->prompts, stg + n * 8 + (n + 1) * 4, np * 4, cudaMemcpyHostToDevice, s));
+    FM_CUDA(cudaEventRecord(ev, s));
+    FM_CUDA(launch_generate(static_cast<const double*>(w->buf), w->dtype == 3, w->rows, w->cols, out->prompts,
+                            out->prompt_off, n, max_tokens, out->seeds, out->z, out->tok, out->logp, out->len, s));
+    count_launch();
+    return FM_OK;
+}
+
+int free_gen_buffers(fm_ctx* c, GenBuffers* g) {
+    for (void* p : {static_cast<void*>(g->prompts), static_cast<void*>(g->prompt_off), static_cast<void*>(g->seeds),
+                    static_cast<void*>(g->z), static_cast<void*>(g->tok), static_cast<void*>(g->logp),
+                    static_cast<void*>(g->len)})
+        if (p) FM_CUDA(cudaFreeAsync(p, c->stream));
+    *g = GenBuffers{};
+    return FM_OK;
+}
+}  // namespace fm

@@ -236,73 +236,95 @@ __global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ zact
                                                   RowBuffers rows, const float* old_logp,
                                                   float clip_eps, double* loss_acc, int fold,
                                                   __nv_bfloat16* pexp_t, __nv_bfloat16* phict, int64_t ldt) {
+    // One warp per row, persistent over rows.  Latency, not bandwidth, bounds this
+    // kernel (1 KB of partials per row at C2), so every load a row needs is issued
+    // before any arithmetic: the per-row scalars and the first 4 x 32 partials.
     __shared__ double red[8];
-    const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
     double loss = 0.0;
-    if (r < Mpad) {
+    for (int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; r < Mpad; r += nwarps) {
         if (r >= M) {
             if (lane == 0) {
                 rows.lse[r] = 0.f;
                 rows.logp[r] = 0.f;
                 rows.coef_eff[r] = 0.f;
             }
-        } else {
-            float m = -INFINITY, s = 0.f;
-            const float2* st = stats + static_cast<size_t>(r) * stats_ld;
-            for (int j = lane; j < stats_ld; j += 32) {
-                const float2 p = st[j];
-                const float nm = fmaxf(m, p.x);
-                s = s * __expf(m - nm) + p.y * __expf(p.x - nm);
+            continue;
+        }
+        const int a = rows.action[r];
+        const float za = zact[r];
+        const float c0 = rows.coef[r];
+        const double adv = sd[rows.sample[r]].adv;
+        const float olp = old_logp ? old_logp[r] : 0.f;
+        int4 f4 = make_int4(-1, -1, -1, -1);
+        uint32_t c4 = 0;
+        if (fold) {
+            f4 = rows.feat4[r];
+            c4 = rows.cnt4[r];
+        }
+        const float2* st = stats + static_cast<size_t>(r) * stats_ld;
+        float m = -INFINITY, s = 0.f;
+        for (int base = 0; base < stats_ld; base += 128) {
+            float2 p[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int j = base + lane + 32 * k;
+                p[k] = j < stats_ld ? st[j] : make_float2(-INFINITY, 0.f);
+            }
+            float lm = fmaxf(fmaxf(p[0].x, p[1].x), fmaxf(p[2].x, p[3].x));
+            const float nm = fmaxf(m, lm);
+            if (nm != -INFINITY) {
+                float ls = 0.f;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) ls += p[k].x == -INFINITY ? 0.f : p[k].y * __expf(p[k].x - nm);
+                s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + ls;
                 m = nm;
             }
+        }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const float om = __shfl_xor_sync(0xffffffffu, m, o);
-                const float os = __shfl_xor_sync(0xffffffffu, s, o);
-                const float nm = fmaxf(m, om);
-                s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
-                m = nm;
-            }
-            if (lane == 0) {
-                const float lse = m + logf(s);
-                const int a = rows.action[r];
-                const bool valid = a >= 0 && a < V;
-                const float lp = valid ? zact[r] - lse : 0.f;  // policy.hpp:72-75, fp32 logit
-                float ce = rows.coef[r];
-                const double adv = sd[rows.sample[r]].adv;
-                if (old_logp && clip_eps > 0.f) {
-                    // PPO clipped-ratio surrogate min(rho*A, clip(rho,1-e,1+e)*A): the
-                    // gradient flows (scaled by rho) only through the unclipped branch.
-                    const float rho = __expf(lp - old_logp[r]);
-                    const bool active = adv >= 0.0 ? rho <= 1.f + clip_eps : rho >= 1.f - clip_eps;
-                    ce = active ? ce * rho : 0.f;
-                }
-                rows.lse[r] = lse;
-                rows.logp[r] = lp;
-                rows.coef_eff[r] = ce;
-                loss = valid ? -(adv / static_cast<double>(G)) * static_cast<double>(lp) : 0.0;
-                if (fold) {
-                    // Every tile used the row's offset bound m (K-gather), so
-                    //   G[t][v] = c (delta(v,a) - p~[t][v] / s),  s = sum_v p~ = exp(lse - m).
-                    // The per-row factor sig = -c / s goes into GEMM2's B operand
-                    // (Phic^T's <= 4 count entries of column t), the delta term into A:
-                    //   A[a][t] = p~_a - s   =>   sig * A = -c (p - delta) = G.
-                    if (!(s >= 1e-30f) || !isfinite(s)) loss = __longlong_as_double(0x7ff8000000000000ll);  // range: NaN loss
-                    const float sig = (valid && ce != 0.f) ? -ce / s : 0.f;
-                    if (sig != 0.f) {
-                        __nv_bfloat16* q = pexp_t + static_cast<size_t>(a) * ldt + r;
-                        *q = __float2bfloat16_rn(__expf(zact[r] - m) - s);
-                    }
-                    const int4 f4 = rows.feat4[r];
-                    const uint32_t c4 = rows.cnt4[r];
-                    const int f[4] = {f4.x, f4.y, f4.z, f4.w};
-#pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (f[j] >= 0)
-                            phict[static_cast<size_t>(f[j]) * ldt + r] =
-                                __float2bfloat16_rn(sig * static_cast<float>((c4 >> (8 * j)) & 0xFFu));
-                }
+        for (int o = 16; o > 0; o >>= 1) {
+            const float om = __shfl_xor_sync(0xffffffffu, m, o);
+            const float os = __shfl_xor_sync(0xffffffffu, s, o);
+            const float nm = fmaxf(m, om);
+            s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
+            m = nm;
+        }
+        // every lane now holds the row's (m, s): the epilogue is computed redundantly
+        // and its scattered stores are spread over lanes 0-5
+        const float lse = m + logf(s);
+        const bool valid = a >= 0 && a < V;
+        const float lp = valid ? za - lse : 0.f;  // policy.hpp:72-75, fp32 logit
+        float ce = c0;
+        if (old_logp && clip_eps > 0.f) {
+            // PPO clipped-ratio surrogate min(rho*A, clip(rho,1-e,1+e)*A): the
+            // gradient flows (scaled by rho) only through the unclipped branch.
+            const float rho = __expf(lp - olp);
+            const bool active = adv >= 0.0 ? rho <= 1.f + clip_eps : rho >= 1.f - clip_eps;
+            ce = active ? ce * rho : 0.f;
+        }
+        if (lane == 0) {
+            rows.lse[r] = lse;
+            rows.logp[r] = lp;
+            rows.coef_eff[r] = ce;
+            loss += valid ? -(adv / static_cast<double>(G)) * static_cast<double>(lp) : 0.0;
+            if (fold && (!(s >= 1e-30f) || !isfinite(s)))
+                loss = __longlong_as_double(0x7ff8000000000000ll);  // range guard: NaN loss, never silent
+        }
+        if (fold) {
+            // Every tile used the row's offset bound m (K-gather), so
+            //   G[t][v] = c (delta(v,a) - p~[t][v] / s),  s = sum_v p~ = exp(lse - m).
+            // The per-row factor sig = -c / s goes into GEMM2's B operand
+            // (Phic^T's <= 4 count entries of column t), the delta term into A:
+            //   A[a][t] = p~_a - s   =>   sig * A = -c (p - delta) = G.
+            const float sig = (valid && ce != 0.f) ? -ce / s : 0.f;
+            if (lane == 4 && sig != 0.f)
+                pexp_t[static_cast<size_t>(a) * ldt + r] = __float2bfloat16_rn(__expf(za - m) - s);
+            if (lane < 4) {
+                const int f = lane == 0 ? f4.x : lane == 1 ? f4.y : lane == 2 ? f4.z : f4.w;
+                if (f >= 0)
+                    phict[static_cast<size_t>(f) * ldt + r] =
+                        __float2bfloat16_rn(sig * static_cast<float>((c4 >> (8 * lane)) & 0xFFu));
             }
         }
     }
@@ -713,8 +735,9 @@ cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int
                        float clip_eps, double* loss_acc, __nv_bfloat16* pexp_t, __nv_bfloat16* phict,
                        int64_t ldt, cudaStream_t s) {
     if (Mpad == 0) return cudaSuccess;
-    const int blocks = static_cast<int>((Mpad * 32 + 255) / 256);
-    lse_kernel<<<blocks, 256, 0, s>>>(zact, stats, stats_ld, M, Mpad, V, sd, global_batch, rows, old_logp, clip_eps,
+    int64_t blocks = (Mpad * 32 + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;  // persistent warps: 8 resident 256-thread blocks per SM
+    lse_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(zact, stats, stats_ld, M, Mpad, V, sd, global_batch, rows, old_logp, clip_eps,
                                       loss_acc, pexp_t != nullptr, pexp_t, phict, ldt);
     return cudaGetLastError();
 }

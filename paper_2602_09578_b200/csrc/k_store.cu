@@ -1,0 +1,402 @@
+// k_store.cu — on-device experience table.
+//
+//   K-poll      poll_micro_batch: eligibility, canonical rank,   experience_store.hpp:92-114,
+//               selection + processing mark + micro-batch         sample.hpp:98-102, :45-46
+//               descriptors straight from HBM cells
+//   K-cells     set_cell / set_cell_payload (batched)            experience_store.hpp:61-88
+//   K-erase     complete / drop_record                           experience_store.hpp:134-148, :166-175
+//   K-purge     purge_stale / purge_inputs (device scan)         experience_store.hpp:118-132, :153-164
+//   K-release   release_group: rule_reward on the arena          rollout.hpp:812-834,
+//               response + group_advantages, both cells written   training.hpp:54-83
+//   K-encode    generated responses -> codec payloads + cells    rollout.hpp:715-731, codec.hpp:15-22
+//
+// The table is SoA in HBM (one slot per record).  The canonical order of the
+// reference's std::map<(input_id, turns, traj, version)> is kept with an
+// order-preserving 64-bit label per input_id (assigned by the host index), so
+// the key compare is four integer compares.  Selection is rank counting over
+// the eligible records (tables hold hundreds to a few thousand records):
+// rank(e) = #{eligible e' : key(e') < key(e)}; keys are unique, so the ranks
+// are a permutation and records with rank < mb are exactly the canonical-first
+// mb ready records — bit-exact with the reference's map walk.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fm_kernels.h"
+#include "fm_store.h"
+
+namespace fm {
+namespace {
+
+__device__ __forceinline__ bool key_less(const DTableView& t, int a, int b) {
+    const uint64_t la = t.label[a], lb = t.label[b];
+    if (la != lb) return la < lb;
+    if (t.turns[a] != t.turns[b]) return t.turns[a] < t.turns[b];
+    if (t.traj[a] != t.traj[b]) return t.traj[a] < t.traj[b];
+    return t.version[a] < t.version[b];
+}
+
+__device__ __forceinline__ bool eligible(const DTableView& t, int s, int64_t version) {
+    // experience_store.hpp:100: !processing && policy_version == current && ready()
+    return (t.flags[s] & (kSlotLive | kSlotProcessing)) == kSlotLive && t.version[s] == version &&
+           t.status[s] == t.full_mask;
+}
+
+__global__ void eligible_kernel(DTableView t, int64_t version, int* __restrict__ count, int* __restrict__ elist) {
+    const int stride = gridDim.x * blockDim.x;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < t.cap; s += stride) {
+        if (eligible(t, s, version)) elist[atomicAdd(count, 1)] = s;
+    }
+}
+
+// 2D grid: x = a 256-record block of the eligible list, y strides over 256-record
+// comparison tiles staged in shared memory.
+__global__ void __launch_bounds__(256) rank_kernel(DTableView t, const int* __restrict__ count,
+                                                   const int* __restrict__ elist, int* __restrict__ rank) {
+    __shared__ uint64_t s_label[256];
+    __shared__ int s_turns[256], s_traj[256];
+    __shared__ int64_t s_ver[256];
+    const int n = *count;
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (static_cast<int>(blockIdx.x) * 256 >= n) return;
+    uint64_t li = 0;
+    int ti = 0, ji = 0;
+    int64_t vi = 0;
+    if (i < n) {
+        const int s = elist[i];
+        li = t.label[s];
+        ti = t.turns[s];
+        ji = t.traj[s];
+        vi = t.version[s];
+    }
+    int less = 0;
+    for (int base = blockIdx.y * 256; base < n; base += gridDim.y * 256) {
+        __syncthreads();
+        const int j = base + threadIdx.x;
+        if (j < n) {
+            const int s = elist[j];
+            s_label[threadIdx.x] = t.label[s];
+            s_turns[threadIdx.x] = t.turns[s];
+            s_traj[threadIdx.x] = t.traj[s];
+            s_ver[threadIdx.x] = t.version[s];
+        }
+        __syncthreads();
+        const int m = min(256, n - base);
+        if (i < n) {
+            for (int k = 0; k < m; ++k) {
+                const uint64_t lk = s_label[k];
+                const bool lt = lk != li ? lk < li
+                                         : (s_turns[k] != ti ? s_turns[k] < ti
+                                                             : (s_traj[k] != ji ? s_traj[k] < ji : s_ver[k] < vi));
+                less += lt ? 1 : 0;
+            }
+        }
+    }
+    if (i < n && less) atomicAdd(&rank[i], less);
+}
+
+// One block: picks rank < mb, marks processing, builds the trainer's sample
+// descriptors from the HBM cells and the arena's codec headers, and writes the
+// host-visible result (slots in canonical order, total rows).
+__global__ void __launch_bounds__(1024) finish_kernel(DTableView t, const int* __restrict__ count,
+                                                      const int* __restrict__ elist, const int* __restrict__ rank,
+                                                      int mb, int pc, int rc, int ac, const uint8_t* __restrict__ arena,
+                                                      SampleDesc* __restrict__ desc, PollResult* __restrict__ res) {
+    __shared__ int sel[kMaxPollMb];
+    __shared__ int64_t scan[kMaxPollMb];
+    const int n = *count;
+    if (n < mb) {  // experience_store.hpp:104: fewer than mb ready -> nullopt, nothing marked
+        if (threadIdx.x == 0) {
+            res->got = 0;
+            res->rows = 0;
+        }
+        return;
+    }
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        const int r = rank[e];
+        if (r < mb) sel[r] = elist[e];
+    }
+    __syncthreads();
+    int64_t nr = 0;
+    if (static_cast<int>(threadIdx.x) < mb) {
+        const int s = sel[threadIdx.x];
+        t.flags[s] |= kSlotProcessing;  // experience_store.hpp:109
+        res->slots[threadIdx.x] = s;
+        if (pc >= 0) {
+            SampleDesc d;
+            d.prompt_off = static_cast<int64_t>(t.cells[static_cast<size_t>(pc) * t.cap + s]);
+            d.resp_off = static_cast<int64_t>(t.cells[static_cast<size_t>(rc) * t.cap + s]);
+            d.prompt_n = static_cast<int32_t>(*reinterpret_cast<const uint64_t*>(arena + d.prompt_off));
+            d.resp_n = static_cast<int32_t>(*reinterpret_cast<const uint64_t*>(arena + d.resp_off));
+            d.adv = __longlong_as_double(static_cast<long long>(t.cells[static_cast<size_t>(ac) * t.cap + s]));
+            d.row_start = 0;
+            desc[threadIdx.x] = d;
+            nr = d.resp_n;
+        }
+    }
+    // inclusive scan of the response lengths (mb <= 1024, Hillis-Steele in smem)
+    if (static_cast<int>(threadIdx.x) < mb) scan[threadIdx.x] = nr;
+    __syncthreads();
+    for (int o = 1; o < mb; o <<= 1) {
+        int64_t add = 0;
+        if (static_cast<int>(threadIdx.x) < mb && static_cast<int>(threadIdx.x) >= o) add = scan[threadIdx.x - o];
+        __syncthreads();
+        if (static_cast<int>(threadIdx.x) < mb) scan[threadIdx.x] += add;
+        __syncthreads();
+    }
+    if (static_cast<int>(threadIdx.x) < mb && pc >= 0) desc[threadIdx.x].row_start = scan[threadIdx.x] - nr;
+    if (threadIdx.x == 0) {
+        res->got = mb;
+        res->rows = scan[mb - 1];
+    }
+}
+
+__global__ void count_ready_kernel(DTableView t, int64_t version, unsigned long long* __restrict__ out) {
+    unsigned long long c = 0;
+    const int stride = gridDim.x * blockDim.x;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < t.cap; s += stride) c += eligible(t, s, version) ? 1 : 0;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+__global__ void set_cells_kernel(DTableView t, int col, int n, const int64_t* __restrict__ slots,
+                                 const uint64_t* __restrict__ vals) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t s = slots[i];
+    t.cells[static_cast<size_t>(col) * t.cap + s] = vals[i];
+    t.status[s] |= 1u << col;  // experience_store.hpp:78-79 (host index raised CellAlreadySet)
+}
+
+// insert (experience_store.hpp:55-58): a fresh record, every cell unset
+__global__ void insert_kernel(DTableView t, int n, const DInsert* __restrict__ recs) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const DInsert r = recs[i];
+    t.label[r.slot] = r.label;
+    t.turns[r.slot] = r.turns;
+    t.traj[r.slot] = r.traj;
+    t.version[r.slot] = r.version;
+    t.status[r.slot] = 0u;
+    t.flags[r.slot] = kSlotLive;
+}
+
+__global__ void erase_kernel(DTableView t, int n, const int64_t* __restrict__ slots) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    t.flags[slots[i]] = 0u;
+    t.status[slots[i]] = 0u;
+}
+
+__global__ void relabel_kernel(DTableView t, const uint64_t* __restrict__ labels) {
+    const int stride = gridDim.x * blockDim.x;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < t.cap; s += stride)
+        if (t.flags[s] & kSlotLive) t.label[s] = labels[s];
+}
+
+// purge_stale (mode 0): !processing && version < current;  purge_inputs (mode 1):
+// !processing && label in the sorted set.  Matching slots are erased here and
+// listed (in slot order after the host sorts) so the host index drops their keys.
+__global__ void purge_kernel(DTableView t, int mode, int64_t current_version, const uint64_t* __restrict__ set,
+                             int nset, int* __restrict__ count, int* __restrict__ out) {
+    const int stride = gridDim.x * blockDim.x;
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < t.cap; s += stride) {
+        if ((t.flags[s] & (kSlotLive | kSlotProcessing)) != kSlotLive) continue;
+        bool hit;
+        if (mode == 0) {
+            hit = t.version[s] < current_version;
+        } else {
+            const uint64_t l = t.label[s];
+            int lo = 0, hi = nset;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (set[mid] < l) lo = mid + 1; else hi = mid;
+            }
+            hit = lo < nset && set[lo] == l;
+        }
+        if (hit) {
+            t.flags[s] = 0u;
+            t.status[s] = 0u;
+            out[atomicAdd(count, 1)] = s;
+        }
+    }
+}
+
+__device__ __forceinline__ int token_at(const uint8_t* arena, uint64_t off, uint64_t i) {
+    // decode_tokens (codec.hpp:28): static_cast<Token>(u64)
+    return static_cast<int>(static_cast<uint32_t>(reinterpret_cast<const uint64_t*>(arena + off + 8)[i]));
+}
+
+// rule_reward (training.hpp:71-83): longest prefix of `pattern` occurring
+// contiguously in the response, / |pattern|.
+__device__ double rule_reward_dev(const uint8_t* arena, uint64_t off, const int* pat, int np) {
+    const uint64_t n = *reinterpret_cast<const uint64_t*>(arena + off);
+    if (n == 0 || np == 0) return 0.0;
+    int best = 0;
+    for (uint64_t start = 0; start < n && best < np; ++start) {
+        int len = 0;
+        while (len < np && start + len < n && token_at(arena, off, start + len) == pat[len]) ++len;
+        best = max(best, len);
+    }
+    return static_cast<double>(best) / static_cast<double>(np);
+}
+
+// release_group (rollout.hpp:812-834): one warp per group; lane i scores
+// survivor i (strided for k > 32); lane 0 normalises in the reference's
+// sequential order with explicit round-to-nearest ops (no FMA contraction), so
+// the advantages are bit-identical to group_advantages (training.hpp:54-67);
+// then every record of every survivor gets both cells.
+__global__ void release_kernel(const DTableView* __restrict__ tabs, const DReleaseCols* __restrict__ cols,
+                               int ngroups, const int32_t* __restrict__ seg_off,
+                               const int32_t* __restrict__ score_tab, const int64_t* __restrict__ score_slot,
+                               const int32_t* __restrict__ rec_off, const int32_t* __restrict__ rec_tab,
+                               const int64_t* __restrict__ rec_slot, const int* __restrict__ pat, int np,
+                               double eps, const uint8_t* __restrict__ arena, double* __restrict__ rewards,
+                               double* __restrict__ advs) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= ngroups) return;
+    const int b = seg_off[warp], e = seg_off[warp + 1];
+    for (int i = b + lane; i < e; i += 32) {
+        const DTableView& t = tabs[score_tab[i]];
+        const uint64_t off = t.cells[static_cast<size_t>(cols[score_tab[i]].response) * t.cap + score_slot[i]];
+        rewards[i] = rule_reward_dev(arena, off, pat, np);
+    }
+    __syncwarp();
+    if (lane == 0 && e > b) {
+        const double k = static_cast<double>(e - b);
+        double mean = 0.0;
+        for (int i = b; i < e; ++i) mean = __dadd_rn(mean, rewards[i]);
+        mean = __ddiv_rn(mean, k);
+        double var = 0.0;
+        for (int i = b; i < e; ++i) {
+            const double d = __dadd_rn(rewards[i], -mean);
+            var = __dadd_rn(var, __dmul_rn(d, d));
+        }
+        var = __ddiv_rn(var, k);
+        const double sd = __dsqrt_rn(var);
+        const double den = __dadd_rn(sd, eps);
+        for (int i = b; i < e; ++i) advs[i] = __ddiv_rn(__dadd_rn(rewards[i], -mean), den);
+    }
+    __syncwarp();
+    for (int i = b; i < e; ++i) {
+        for (int r = rec_off[i] + lane; r < rec_off[i + 1]; r += 32) {
+            const DTableView& t = tabs[rec_tab[r]];
+            const DReleaseCols& c = cols[rec_tab[r]];
+            const int64_t s = rec_slot[r];
+            t.cells[static_cast<size_t>(c.reward) * t.cap + s] = static_cast<uint64_t>(__double_as_longlong(rewards[i]));
+            t.cells[static_cast<size_t>(c.advantage) * t.cap + s] = static_cast<uint64_t>(__double_as_longlong(advs[i]));
+            atomicOr(&t.status[s], (1u << c.reward) | (1u << c.advantage));
+        }
+    }
+}
+
+// Generated responses -> the reference codec in the arena ([u64 n][u64 tok] x n,
+// codec.hpp:15-22; log-probs as [u64 n][f64] x n) + the two ref cells.
+__global__ void encode_kernel(DTableView t, int rc, int lc, const int64_t* __restrict__ slots,
+                              const int32_t* __restrict__ tok, const double* __restrict__ lp,
+                              const int32_t* __restrict__ len, int max_tokens, uint8_t* __restrict__ arena,
+                              uint64_t base_off, uint64_t stride) {
+    const int i = blockIdx.x;
+    const int n = len[i];
+    const uint64_t ro = base_off + static_cast<uint64_t>(i) * stride;
+    const uint64_t lo = ro + 8 + 8 * static_cast<uint64_t>(max_tokens);
+    uint64_t* r = reinterpret_cast<uint64_t*>(arena + ro);
+    uint64_t* l = reinterpret_cast<uint64_t*>(arena + lo);
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        r[1 + j] = static_cast<uint64_t>(static_cast<int64_t>(tok[static_cast<size_t>(i) * max_tokens + j]));
+        l[1 + j] = static_cast<uint64_t>(__double_as_longlong(lp[static_cast<size_t>(i) * max_tokens + j]));
+    }
+    if (threadIdx.x == 0) {
+        r[0] = static_cast<uint64_t>(n);
+        l[0] = static_cast<uint64_t>(n);
+        const int64_t s = slots[i];
+        uint32_t bits = 1u << rc;
+        t.cells[static_cast<size_t>(rc) * t.cap + s] = ro;
+        if (lc >= 0) {
+            t.cells[static_cast<size_t>(lc) * t.cap + s] = lo;
+            bits |= 1u << lc;
+        }
+        t.status[s] |= bits;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_dt_poll(const DTableView& t, int64_t version, int mb, int pc, int rc, int ac,
+                           const uint8_t* arena, DPollScratch sc, SampleDesc* desc, PollResult* res,
+                           cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(sc.count, 0, sizeof(int), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(sc.rank, 0, sizeof(int) * static_cast<size_t>(t.cap), s);
+    if (e != cudaSuccess) return e;
+    const int blocks = (t.cap + 255) / 256;
+    eligible_kernel<<<blocks < 148 * 4 ? blocks : 148 * 4, 256, 0, s>>>(t, version, sc.count, sc.elist);
+    dim3 g(static_cast<unsigned>(blocks), static_cast<unsigned>(blocks < 16 ? blocks : 16));
+    rank_kernel<<<g, 256, 0, s>>>(t, sc.count, sc.elist, sc.rank);
+    finish_kernel<<<1, 1024, 0, s>>>(t, sc.count, sc.elist, sc.rank, mb, pc, rc, ac, arena, desc, res);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dt_ready_count(const DTableView& t, int64_t version, unsigned long long* out, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    const int blocks = (t.cap + 255) / 256;
+    count_ready_kernel<<<blocks < 148 * 4 ? blocks : 148 * 4, 256, 0, s>>>(t, version, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dt_insert(const DTableView& t, int n, const DInsert* recs, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    insert_kernel<<<(n + 255) / 256, 256, 0, s>>>(t, n, recs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dt_set_cells(const DTableView& t, int col, int n, const int64_t* slots, const uint64_t* vals,
+                                cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    set_cells_kernel<<<(n + 255) / 256, 256, 0, s>>>(t, col, n, slots, vals);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dt_erase(const DTableView& t, int n, const int64_t* slots, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    erase_kernel<<<(n + 255) / 256, 256, 0, s>>>(t, n, slots);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dt_relabel(const DTableView& t, const uint64_t* labels, cudaStream_t s) {
+    const int blocks = (t.cap + 255) / 256;
+    relabel_kernel<<<blocks < 148 * 4 ? blocks : 148 * 4, 256, 0, s>>>(t, labels);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dt_purge(const DTableView& t, int mode, int64_t current_version, const uint64_t* set, int nset,
+                            int* count, int* out, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    const int blocks = (t.cap + 255) / 256;
+    purge_kernel<<<blocks < 148 * 4 ? blocks : 148 * 4, 256, 0, s>>>(t, mode, current_version, set, nset, count, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dt_release(const DTableView* tabs, const DReleaseCols* cols, int ngroups, const int32_t* seg_off,
+                              const int32_t* score_tab, const int64_t* score_slot, const int32_t* rec_off,
+                              const int32_t* rec_tab, const int64_t* rec_slot, const int* pat, int np, double eps,
+                              const uint8_t* arena, double* rewards, double* advs, cudaStream_t s) {
+    if (ngroups <= 0) return cudaSuccess;
+    const int threads = 128;
+    release_kernel<<<(ngroups * 32 + threads - 1) / threads, threads, 0, s>>>(
+        tabs, cols, ngroups, seg_off, score_tab, score_slot, rec_off, rec_tab, rec_slot, pat, np, eps, arena, rewards,
+        advs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dt_encode(const DTableView& t, int rc, int lc, int n, const int64_t* slots, const int32_t* tok,
+                             const double* lp, const int32_t* len, int max_tokens, uint8_t* arena, uint64_t base_off,
+                             uint64_t stride, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    encode_kernel<<<n, 128, 0, s>>>(t, rc, lc, slots, tok, lp, len, max_tokens, arena, base_off, stride);
+    return cudaGetLastError();
+}
+
+}  // namespace fm

@@ -66,6 +66,10 @@ class MicroBatch:
     agent_id: str
     policy_version: int
     samples: list = field(default_factory=list)
+    # set when polled from a DeviceExperienceStore: the descriptors stay in HBM
+    dtable: object = None
+    poll_id: int = -1
+    rows: int = 0
 
     def size(self) -> int:
         return len(self.samples)
@@ -256,6 +260,212 @@ class ExperienceStore:
 
 
 # ---------------------------------------------------------------------------
+# on-device experience store (experience_store.hpp, rollout.hpp:812-834)
+# ---------------------------------------------------------------------------
+def _ids(strings):
+    enc = [x.encode() for x in strings]
+    return (C.c_char_p * max(len(enc), 1))(*enc)
+
+
+class DeviceExperienceStore:
+    """ExperienceStore whose tables live in one GPU's HBM (fm_dtable).
+
+    Same methods and error behaviour as :class:`ExperienceStore`; records are
+    also addressable by their slot (``find``).  Two rollout-side entry points
+    keep the producer on the device too: :meth:`generate` (rollout completion,
+    rollout.hpp:715-731) and :meth:`release_groups` (rollout.hpp:812-834).
+    """
+
+    def __init__(self, ctx: Context, capacity: int = 4096):
+        self.ctx = ctx
+        self.capacity = capacity
+        self._t: dict[str, C.c_void_p] = {}
+        self._schemas: dict[str, TableSchema] = {}
+
+    def _h(self, agent_id: str):
+        if agent_id not in self._t:
+            raise MarlsimError(16, agent_id)  # UnknownTable
+        return self._t[agent_id]
+
+    def create_table(self, schema: TableSchema, capacity: int | None = None) -> None:
+        if schema.agent_id in self._t:
+            raise MarlsimError(10, schema.agent_id)  # TableExists
+        names = [n.encode() for n, _ in schema.columns]
+        arr = (C.c_char_p * max(len(names), 1))(*names)
+        types = (C.c_int * max(len(names), 1))(*[COLUMN_TYPES[t] for _, t in schema.columns])
+        h = C.c_void_p()
+        check(lib().fm_dtable_create(self.ctx.handle, schema.agent_id.encode(), arr, types, len(names),
+                                     capacity or self.capacity, C.byref(h)))
+        self._t[schema.agent_id] = h
+        self._schemas[schema.agent_id] = schema
+
+    def has_table(self, agent_id: str) -> bool:
+        return agent_id in self._t
+
+    def schema(self, agent_id: str) -> TableSchema:
+        self._h(agent_id)
+        return self._schemas[agent_id]
+
+    def table(self, agent_id: str):
+        return self._h(agent_id)
+
+    def insert(self, agent_id: str, policy_version: int, sid: SampleId) -> int:
+        return int(self.insert_many(agent_id, policy_version, [sid])[0])
+
+    def insert_many(self, agent_id: str, policy_version: int, sids) -> np.ndarray:
+        sids = list(sids)
+        out = np.zeros(max(len(sids), 1), np.int64)
+        turns = np.array([s.number_of_turns for s in sids] or [0], np.int32)
+        trajs = np.array([s.trajectory_id for s in sids] or [0], np.int32)
+        check(lib().fm_dtable_insert(self._h(agent_id), policy_version, len(sids), _ids([s.input_id for s in sids]),
+                                     ptr(turns), ptr(trajs), ptr(out)))
+        return out[:len(sids)]
+
+    def find(self, agent_id: str, sid: SampleId, version: int) -> int:
+        out = C.c_int64()
+        check(lib().fm_dtable_find(self._h(agent_id), sid.input_id.encode(), sid.number_of_turns,
+                                   sid.trajectory_id, version, C.byref(out)))
+        return out.value
+
+    def _slot(self, agent_id: str, sid: SampleId, version: int) -> int:
+        s = self.find(agent_id, sid, version)
+        if s < 0:
+            raise MarlsimError(14, sid.render())  # RecordNotFound
+        return s
+
+    def set_cell(self, agent_id: str, sid: SampleId, version: int, column: str, value: float) -> None:
+        self.set_cells(agent_id, column, [self._slot(agent_id, sid, version)], [value])
+
+    def set_cells(self, agent_id: str, column: str, slots, values) -> None:
+        sl = np.ascontiguousarray(slots, np.int64)
+        vals = np.ascontiguousarray(values, np.float64)
+        check(lib().fm_dtable_set_float(self._h(agent_id), column.encode(), len(sl), ptr(sl), ptr(vals)))
+
+    def set_cell_payload(self, agent_id: str, sid: SampleId, version: int, column: str, payload: bytes) -> None:
+        self.set_payload_slot(agent_id, column, self._slot(agent_id, sid, version), payload)
+
+    def set_payload_slot(self, agent_id: str, column: str, slot: int, payload: bytes) -> None:
+        buf = (C.c_uint8 * len(payload)).from_buffer_copy(payload)
+        check(lib().fm_dtable_set_payload(self._h(agent_id), column.encode(), slot, buf, len(payload)))
+
+    def generate(self, agent_id: str, weights, slots, prompts, max_tokens: int, seeds,
+                 response_col: str = "response", logprob_col: str | None = "logprobs") -> None:
+        """Rollout completion on the GPU: PolicyModel::generate per record, the
+        responses (and log-probs) written straight into the arena and the cells."""
+        sl = np.ascontiguousarray(slots, np.int64)
+        off = np.zeros(len(prompts) + 1, np.int32)
+        off[1:] = np.cumsum([len(p) for p in prompts])
+        flat = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in prompts])
+                                    if off[-1] else np.zeros(1, np.int32), np.int32)
+        sd = np.ascontiguousarray(seeds, np.uint64)
+        check(lib().fm_dtable_generate(self._h(agent_id), weights, response_col.encode(),
+                                       logprob_col.encode() if logprob_col else None, len(sl), ptr(sl),
+                                       ptr(flat), ptr(off), max_tokens, ptr(sd)))
+
+    def release_groups(self, groups, pattern=(3, 1, 4), eps_adv: float = 1e-8, response_col: str = "response",
+                       reward_col: str = "reward", adv_col: str = "advantage", read_back: bool = False):
+        """release_group (rollout.hpp:812-834) for several groups at once.  A group
+        is a list of survivors; a survivor is ``(score, records)`` with ``score`` =
+        (agent, slot) of the record whose response is scored and ``records`` the
+        (agent, slot) list that receives reward and advantage."""
+        agents = []
+        for grp in groups:
+            for (sa, _), recs in grp:
+                for a in [sa] + [r[0] for r in recs]:
+                    if a not in agents:
+                        agents.append(a)
+        tix = {a: i for i, a in enumerate(agents)}
+        seg = [0]
+        st, ss, ro, rt, rs = [], [], [0], [], []
+        for grp in groups:
+            for (sa, sslot), recs in grp:
+                st.append(tix[sa])
+                ss.append(sslot)
+                for a, slot in recs:
+                    rt.append(tix[a])
+                    rs.append(slot)
+                ro.append(len(rs))
+            seg.append(len(st))
+        tabs = (C.c_void_p * len(agents))(*[self._h(a).value for a in agents])
+        arrs = [np.ascontiguousarray(x, dt) if len(x) else np.zeros(1, dt) for x, dt in
+                ((seg, np.int32), (st, np.int32), (ss, np.int64), (ro, np.int32), (rt, np.int32), (rs, np.int64))]
+        pat = np.ascontiguousarray(pattern if len(pattern) else [0], np.int32)
+        n = len(st)
+        rew = np.zeros(max(n, 1))
+        adv = np.zeros(max(n, 1))
+        check(lib().fm_dtable_release_groups(tabs, len(agents), response_col.encode(), reward_col.encode(),
+                                             adv_col.encode(), len(groups), *[ptr(a) for a in arrs], ptr(pat),
+                                             len(pattern), eps_adv, ptr(rew) if read_back else None,
+                                             ptr(adv) if read_back else None))
+        return (rew[:n], adv[:n]) if read_back else None
+
+    def ready_count(self, agent_id: str, version: int) -> int:
+        out = C.c_uint64()
+        check(lib().fm_dtable_ready_count(self._h(agent_id), version, C.byref(out)))
+        return out.value
+
+    def record_count(self, agent_id: str) -> int:
+        out = C.c_uint64()
+        check(lib().fm_dtable_record_count(self._h(agent_id), C.byref(out)))
+        return out.value
+
+    def record(self, agent_id: str, slot: int) -> SampleRecord:
+        idbuf = C.create_string_buffer(256)
+        turns, traj, ver, proc, st = C.c_int(), C.c_int(), C.c_int64(), C.c_int(), C.c_uint32()
+        check(lib().fm_dtable_record(self._h(agent_id), slot, idbuf, 256, C.byref(turns), C.byref(traj),
+                                     C.byref(ver), C.byref(proc), C.byref(st)))
+        return SampleRecord(ver.value, SampleId(idbuf.value.decode(), turns.value, traj.value), slot, None)
+
+    def poll_micro_batch(self, agent_id: str, current_version: int, micro_batch_size: int,
+                         columns=("prompt", "response", "advantage")) -> Optional[MicroBatch]:
+        n = int(micro_batch_size)
+        slots = np.zeros(max(n, 1), np.int64)
+        rows, got, pid = C.c_int64(), C.c_int64(), C.c_int64()
+        pc, rc, ac = (c.encode() if c else None for c in (columns or (None, None, None)))
+        check(lib().fm_dtable_poll(self._h(agent_id), current_version, n, pc, rc, ac, ptr(slots),
+                                   C.byref(rows), C.byref(got), C.byref(pid)))
+        if got.value == 0:
+            return None
+        batch = MicroBatch(agent_id, current_version, dtable=self._h(agent_id), poll_id=pid.value,
+                           rows=rows.value)
+        batch.samples = [self.record(agent_id, int(s)) for s in slots[:n]]
+        return batch
+
+    def read_cells(self, agent_id: str, column: str, slots, as_float: bool = True) -> np.ndarray:
+        sl = np.ascontiguousarray(slots, np.int64)
+        out = np.zeros(max(len(sl), 1), np.uint64)
+        check(lib().fm_dtable_read_cells(self._h(agent_id), column.encode(), len(sl), ptr(sl), ptr(out)))
+        out = out[:len(sl)]
+        return out.view(np.float64) if as_float else out
+
+    def complete(self, agent_id: str, samples: list) -> None:
+        hs = np.ascontiguousarray([s.handle for s in samples] or [0], np.int64)
+        check(lib().fm_dtable_complete(self._h(agent_id), ptr(hs), len(samples)))
+
+    def purge_stale(self, agent_id: str, current_version: int) -> int:
+        out = C.c_uint64()
+        check(lib().fm_dtable_purge_stale(self._h(agent_id), current_version, C.byref(out)))
+        return out.value
+
+    def purge_inputs(self, agent_id: str, inputs) -> int:
+        inputs = list(inputs)
+        out = C.c_uint64()
+        check(lib().fm_dtable_purge_inputs(self._h(agent_id), _ids(inputs), len(inputs), C.byref(out)))
+        return out.value
+
+    def drop_record(self, agent_id: str, sid: SampleId, version: int) -> bool:
+        out = C.c_int()
+        check(lib().fm_dtable_drop_record(self._h(agent_id), sid.input_id.encode(), sid.number_of_turns,
+                                          sid.trajectory_id, version, C.byref(out)))
+        return bool(out.value)
+
+    def close(self) -> None:
+        for h in self._t.values():
+            lib().fm_dtable_destroy(h)
+        self._t.clear()
+
+
+# ---------------------------------------------------------------------------
 # training engine (training.hpp)
 # ---------------------------------------------------------------------------
 @dataclass
@@ -379,9 +589,12 @@ class TrainingEngine:
         if min(schema.column_index(c) for c in ("prompt", "response", "advantage")) < 0:
             raise MarlsimError(13, "trainer needs prompt/response/advantage columns")
         n = len(batch.samples)
-        arr = (_lib.fm_sample * max(n, 1))(*[s.cell for s in batch.samples])
         ticket = C.c_int64()
-        check(lib().fm_train_micro_batch(g.handle, arr, n, self.global_batch, C.byref(ticket)))
+        if batch.dtable is not None:  # polled on the device: descriptors stay in HBM
+            check(lib().fm_train_polled(g.handle, batch.dtable, batch.poll_id, self.global_batch, C.byref(ticket)))
+        else:
+            arr = (_lib.fm_sample * max(n, 1))(*[s.cell for s in batch.samples])
+            check(lib().fm_train_micro_batch(g.handle, arr, n, self.global_batch, C.byref(ticket)))
         g.in_flight = True
         base = GradReport(agent, batch.policy_version, ver, n, float("nan"))
         self._pending.append((agent, ticket.value, base, on_done))
