@@ -86,7 +86,7 @@ class OracleStore:
         if col in rec["cells"]:
             # set_cell_payload registers the object first (experience_store.hpp:86): its
             # sample-field key already exists -> DuplicateKey (object_store.hpp:144-148)
-            raise StoreError(CELL_ALREADY_SET if by_value else DUPLICATE_KEY)
+            raise StoreError(DUPLICATE_KEY if not by_value and types[col] not in BY_VALUE else CELL_ALREADY_SET)
         if (types[col] in BY_VALUE) != by_value:
             raise StoreError(CONFIG_ERROR)
         rec["cells"][col] = value

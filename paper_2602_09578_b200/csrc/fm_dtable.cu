@@ -361,19 +361,22 @@ int fm_dtable_find(fm_dtable* t, const char* id, int turns, int traj, int64_t ve
 }
 
 static int check_cells(fm_dtable* t, const char* column, int n, const int64_t* slots, bool want_value, int* col_out) {
+    // the reference's order (experience_store.hpp:65-79): column, record, status, storage class
     const int c = t->col(column);
     if (c < 0) return fail(FM_ERR_UNKNOWN_COLUMN, column ? column : "(null)");
-    if (by_value(t->types[static_cast<size_t>(c)]) != want_value)
-        return fail(FM_ERR_CONFIG_ERROR, std::string("cell storage class mismatch for column ") + column);
-    for (int i = 0; i < n; ++i) {  // experience_store.hpp:65-76
+    const bool col_by_value = by_value(t->types[static_cast<size_t>(c)]);
+    // set_cell_payload registers the payload object first (experience_store.hpp:86); a ref cell
+    // set before already owns that sample-field key -> DuplicateKey (object_store.hpp:144-148)
+    const int already = (!want_value && !col_by_value) ? FM_ERR_DUPLICATE_KEY : FM_ERR_CELL_ALREADY_SET;
+    for (int i = 0; i < n; ++i) {
         if (!t->live_slot(slots[i])) return fail(FM_ERR_RECORD_NOT_FOUND, "slot " + std::to_string(slots[i]));
         const HostRec& r = t->recs[static_cast<size_t>(slots[i])];
-        // a payload cell's object is registered before set_cell runs (experience_store.hpp:86):
-        // its sample-field key exists already -> DuplicateKey (object_store.hpp:144-148)
-        if (r.status & (1u << c)) return fail(want_value ? FM_ERR_CELL_ALREADY_SET : FM_ERR_DUPLICATE_KEY, column);
+        if (r.status & (1u << c)) return fail(already, column);
         for (int j = 0; j < i; ++j)
-            if (slots[j] == slots[i]) return fail(FM_ERR_CELL_ALREADY_SET, column);
+            if (slots[j] == slots[i]) return fail(already, column);
     }
+    if (col_by_value != want_value)
+        return fail(FM_ERR_CONFIG_ERROR, std::string("cell storage class mismatch for column ") + column);
     *col_out = c;
     return FM_OK;
 }

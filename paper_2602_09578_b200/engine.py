@@ -410,9 +410,9 @@ class DeviceExperienceStore:
         return out.value
 
     def record(self, agent_id: str, slot: int) -> SampleRecord:
-        idbuf = C.create_string_buffer(256)
+        idbuf = C.create_string_buffer(4096)
         turns, traj, ver, proc, st = C.c_int(), C.c_int(), C.c_int64(), C.c_int(), C.c_uint32()
-        check(lib().fm_dtable_record(self._h(agent_id), slot, idbuf, 256, C.byref(turns), C.byref(traj),
+        check(lib().fm_dtable_record(self._h(agent_id), slot, idbuf, 4096, C.byref(turns), C.byref(traj),
                                      C.byref(ver), C.byref(proc), C.byref(st)))
         return SampleRecord(ver.value, SampleId(idbuf.value.decode(), turns.value, traj.value), slot, None)
 

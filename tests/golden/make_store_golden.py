@@ -58,6 +58,7 @@ def make_script(seed: int, versions: int = 4, groups_per_version: int = 6, k: in
         lines.append(f"setf {v} zz9 0 0 reward 0x1p+0")                # RecordNotFound
         lines.append(f"setp {v} {g0} {r0[1]} {r0[2]} prompt 1 5")      # CellAlreadySet
         lines.append(f"poll {v} 0")                                    # ConfigError
+        lines.append(f"setp {v} {g0} {r0[1]} {r0[2]} advantage 1 5")   # payload into a by-value column
         # responses (some contain the reward pattern), logprobs
         order = [(g, r) for g, recs in groups for r in recs]
         rng.shuffle(order)
@@ -85,6 +86,8 @@ def make_script(seed: int, versions: int = 4, groups_per_version: int = 6, k: in
             lines.append(" ".join(parts))
         lines.append(f"ready {v}")
         lines.append("count")
+        lines.append(f"setp {v} {g0} {r0[1]} {r0[2]} reward 1 5")      # by-value cell already set
+        lines.append(f"setf {v} {g0} {r0[1]} {r0[2]} response 0x1p+0")  # ref cell already set
         # polls and completes
         for _ in range(rng.randint(2, 5)):
             lines.append(f"poll {v} {mb}")
