@@ -249,8 +249,9 @@ def run_ours(args, dist: Dist) -> dict | None:
 
     # --- experience: every step's samples resident in the token arena, indexed
     #     by the host experience store (rollout-side production, untimed)
-    from paper_2602_09578_b200.engine import ExperienceStore, SampleId, TableSchema
-    store = ExperienceStore(ctx)
+    from paper_2602_09578_b200.engine import DeviceExperienceStore, ExperienceStore, SampleId, TableSchema
+    device_store = args.store == "device"
+    store = DeviceExperienceStore(ctx, capacity=G * n_steps) if device_store else ExperienceStore(ctx)
     schema_cols = [("prompt", "List"), ("response", "List"), ("advantage", "Float")]
     host_payloads = {}
     for a in mine:
@@ -259,6 +260,13 @@ def run_ours(args, dist: Dist) -> dict | None:
             samples = wl.step_samples(cfg, a, s)
             adv = group_advantages(ctx, [x.reward for x in samples], wl.group_offsets(samples))  # K-adv
             host_payloads[(a, s)] = (samples, adv)
+            if device_store:  # the table (cells, payloads, flags) lives in HBM
+                slots = store.insert_many(a, s, [SampleId(x.input_id, x.turns, x.traj) for x in samples])
+                for x, sl in zip(samples, slots):
+                    store.set_payload_slot(a, "prompt", int(sl), x.prompt_payload)
+                    store.set_payload_slot(a, "response", int(sl), x.response_payload)
+                store.set_cells(a, "advantage", slots, adv)
+                continue
             for x, av in zip(samples, adv):
                 sid = SampleId(x.input_id, x.turns, x.traj)
                 store.insert(a, s, sid)
@@ -301,9 +309,12 @@ def run_ours(args, dist: Dist) -> dict | None:
                 batch = timed("poll", store.poll_micro_batch, a, step, mb)
                 if batch is None:
                     raise RuntimeError(f"experience store ran dry for {a} at step {step}")
-                arr = (FS * mb)(*[r.cell for r in batch.samples])
                 t = C.c_int64()
-                check(timed("train", L.fm_train_micro_batch, h, arr, mb, G, C.byref(t)))
+                if device_store:  # descriptors built by the device poll, consumed from HBM
+                    check(timed("train", L.fm_train_polled, h, batch.dtable, batch.poll_id, G, C.byref(t)))
+                else:
+                    arr = (FS * mb)(*[r.cell for r in batch.samples])
+                    check(timed("train", L.fm_train_micro_batch, h, arr, mb, G, C.byref(t)))
                 timed("complete", store.complete, a, batch.samples)
                 ntok += cfg.resp_len * mb
             if a in comms:
@@ -695,6 +706,56 @@ def run_next(args) -> None:
     except Exception as e:  # noqa: BLE001
         rec["reference_error"] = str(e)[:200]
     out.append(rec)
+
+    # ---- f4: on-device experience table — poll latency (host call -> canonical slots back,
+    #      processing marked) against the host control plane, and group release on the GPU
+    from paper_2602_09578_b200.engine import DeviceExperienceStore, ExperienceStore, SampleId, TableSchema
+    ctx.reset_arena()
+    for nrec in (256, 4096):
+        ids = [SampleId(f"q{i // 16:05d}", 0, i % 16) for i in range(nrec)]
+        order = rng.permutation(nrec)
+        ds, hs = DeviceExperienceStore(ctx, capacity=nrec), ExperienceStore(ctx)
+        for st in (ds, hs):
+            st.create_table(TableSchema("a", [("advantage", "Float")]))
+        slots = ds.insert_many("a", 0, [ids[i] for i in order])
+        ds.set_cells("a", "advantage", slots, np.zeros(nrec))
+        for i in order:
+            hs.insert("a", 0, ids[i])
+            hs.set_cell("a", ids[i], 0, "advantage", 0.0)
+        res = {}
+        for name, st in (("device", ds), ("host", hs)):
+            t0 = time.perf_counter()
+            n = 0
+            while st.poll_micro_batch("a", 0, 16, columns=None) is not None:
+                n += 1
+            res[name] = (time.perf_counter() - t0) / max(n, 1) * 1e6
+        out.append({"row": "f4 device table", "records": nrec, "micro_batch": 16,
+                    "poll_us": {k: round(v, 1) for k, v in res.items()}})
+        ds.close()
+        hs.close()
+    # release: 64 groups x 16 survivors, 1,024-token responses scored on the GPU (rule_reward + group_advantages)
+    ngrp, k, Lr = 64, 16, 1024
+    ds = DeviceExperienceStore(ctx, capacity=ngrp * k)
+    ds.create_table(TableSchema("a", [("response", "List"), ("reward", "Float"), ("advantage", "Float")]))
+    sl = ds.insert_many("a", 0, [SampleId(f"q{i // k:05d}", 0, i % k) for i in range(ngrp * k)])
+    resp = rng.integers(0, 8, size=(ngrp * k, Lr))
+    for i, s_ in enumerate(sl):
+        t = resp[i].astype(np.int64).astype(np.uint64)
+        ds.set_payload_slot("a", "response", int(s_), np.uint64(Lr).tobytes() + t.tobytes())
+    groups = [[(("a", int(sl[g * k + j])), [("a", int(sl[g * k + j]))]) for j in range(k)] for g in range(ngrp)]
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    rew, adv = ds.release_groups(groups, read_back=True)
+    tr = time.perf_counter() - t0
+    from oracle import store_oracle as so
+    t0 = time.perf_counter()
+    ref_rew = [so.rule_reward(list(resp[i]), [3, 1, 4]) for i in range(ngrp * k)]
+    ref_adv = sum((so.group_advantages(ref_rew[g * k:(g + 1) * k]) for g in range(ngrp)), [])
+    tp = time.perf_counter() - t0
+    out.append({"row": "f4 group release", "groups": ngrp, "survivors": k, "response_tokens": Lr,
+                "gpu_ms": round(tr * 1e3, 3), "python_oracle_ms_1core": round(tp * 1e3, 1),
+                "bit_identical": bool(np.array_equal(rew, ref_rew) and np.array_equal(adv, ref_adv))})
+    ds.close()
     L.fm_agent_destroy(h)
     ctx.close()
     for r in out:
@@ -874,7 +935,8 @@ def config_obj(cfg, args) -> dict:
             "global_batch": cfg.global_batch, "resp_len": cfg.resp_len,
             "formulation": "dense 4*V*D flop/token (reference's own dense loops, policy.hpp:57-61, 87-89)",
             "l2": "inputs larger than L2 (W16 262 MB, Z 2.1 GB per micro-batch); no flush needed",
-            "parallelism": f"agent-centric placement, dp gangs of max(1, N/{na}) GPUs"}
+            "parallelism": f"agent-centric placement, dp gangs of max(1, N/{na}) GPUs",
+            "experience_store": getattr(args, "store", "host")}
 
 
 def main():
@@ -898,6 +960,8 @@ def main():
     ap.add_argument("--agents", type=int, default=0, help="use only the first K agents of the config")
     ap.add_argument("--dp-mode", default="gang", choices=["gang", "allreduce"],
                     help="gang: fused GEMM2 reduce-scatter over NVLink + sharded Adam; allreduce: NCCL")
+    ap.add_argument("--store", default="host", choices=["host", "device"],
+                    help="experience store: host control plane (default) or the on-device table (§8f-4)")
     ap.add_argument("--next", action="store_true", help="measure the SURVEY §8f next rows (one GPU)")
     ap.add_argument("--next-vocab", type=int, default=32000)
     ap.add_argument("--next-feat", type=int, default=4096)

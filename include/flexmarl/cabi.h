@@ -365,6 +365,10 @@ int fm_dtable_record_count(fm_dtable* t, uint64_t* out);
 /* Identity and flags of a slot's record (dump_table view, experience_store.hpp:210-238). */
 int fm_dtable_record(fm_dtable* t, int64_t slot, char* input_id_out, size_t cap, int* turns, int* traj,
                      int64_t* version, int* processing, uint32_t* status);
+/* Identities of n records at once (the MicroBatch's record copies, experience_store.hpp:111);
+ * ids_out holds n strings of id_cap bytes each. */
+int fm_dtable_records(fm_dtable* t, int n, const int64_t* slots, char* ids_out, size_t id_cap, int* turns,
+                      int* trajs, int64_t* versions);
 /* Cells of n slots read back from HBM: by-value columns as f64, ref columns as arena offsets. */
 int fm_dtable_read_cells(fm_dtable* t, const char* column, int n, const int64_t* slots, uint64_t* out);
 

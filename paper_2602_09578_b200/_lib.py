@@ -138,6 +138,7 @@ _PROTOS = {
     "fm_dtable_record_count": (I, [P, PU64]),
     "fm_dtable_record": (I, [P, I64, S, C.c_size_t, C.POINTER(C.c_int), C.POINTER(C.c_int), PI64,
                              C.POINTER(C.c_int), C.POINTER(C.c_uint32)]),
+    "fm_dtable_records": (I, [P, I, P, P, C.c_size_t, P, P, P]),
     "fm_dtable_read_cells": (I, [P, S, I, P, P]),
 }
 

@@ -77,7 +77,8 @@ struct fm_dtable {
     fm::DTableView view{};
     fm::DPollScratch sc{};
     fm::PollResult* d_res = nullptr;
-    fm::PollResult* h_res = nullptr;  // pinned
+    fm::PollResult* h_res = nullptr;  // pinned, mapped: the poll's finish kernel writes it directly
+    fm::PollResult* m_res = nullptr;  // its device alias
     fm::SampleDesc* d_desc = nullptr; // [kRing][kMaxPollMb]
     unsigned long long* d_cnt = nullptr;
     unsigned long long* h_cnt = nullptr;  // pinned
@@ -268,7 +269,8 @@ int fm_dtable_create(fm_ctx* ctx, const char* agent, const char* const* names, c
     t->d_desc = reinterpret_cast<fm::SampleDesc*>(take(11));
     t->d_cnt = reinterpret_cast<unsigned long long*>(take(12));
     t->d_list = reinterpret_cast<int*>(take(13));
-    FM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&t->h_res), sizeof(fm::PollResult), cudaHostAllocDefault));
+    FM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&t->h_res), sizeof(fm::PollResult), cudaHostAllocMapped));
+    FM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&t->m_res), t->h_res, 0));
     FM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&t->h_cnt), 16, cudaHostAllocDefault));
     FM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&t->h_list), C * 4, cudaHostAllocDefault));
     for (int k = 0; k < kRing; ++k) {
@@ -582,9 +584,8 @@ int fm_dtable_poll(fm_dtable* t, int64_t version, int64_t mb, const char* prompt
     const int k = static_cast<int>(t->poll_seq % kRing);
     if (t->ring_used[k]) FM_CUDA(cudaStreamWaitEvent(t->stream, t->ring_consumed[k], 0));  // descriptors reused
     FM_CUDA(fm::launch_dt_poll(t->view, version, static_cast<int>(mb), pc, rc, ac, fm::ctx_arena(t->ctx), t->sc,
-                               t->d_desc + static_cast<size_t>(k) * fm::kMaxPollMb, t->d_res, t->stream));
+                               t->d_desc + static_cast<size_t>(k) * fm::kMaxPollMb, t->m_res, t->stream));
     fm::count_launch(3);
-    FM_CUDA(cudaMemcpyAsync(t->h_res, t->d_res, 16 + 8 * static_cast<size_t>(mb), cudaMemcpyDeviceToHost, t->stream));
     FM_CUDA(cudaEventRecord(t->ring_ready[k], t->stream));
     FM_CUDA(cudaEventSynchronize(t->ring_ready[k]));
     *got = t->h_res->got;
@@ -745,6 +746,23 @@ int fm_dtable_record(fm_dtable* t, int64_t slot, char* id_out, size_t cap, int* 
     if (version) *version = r.version;
     if (processing) *processing = r.processing ? 1 : 0;
     if (status) *status = r.status;
+    return FM_OK;
+}
+
+int fm_dtable_records(fm_dtable* t, int n, const int64_t* slots, char* ids_out, size_t id_cap, int* turns,
+                      int* trajs, int64_t* versions) {
+    for (int i = 0; i < n; ++i) {
+        if (!t->live_slot(slots[i])) return fail(FM_ERR_RECORD_NOT_FOUND, "slot " + std::to_string(slots[i]));
+        const HostRec& r = t->recs[static_cast<size_t>(slots[i])];
+        if (ids_out && id_cap) {
+            char* o = ids_out + static_cast<size_t>(i) * id_cap;
+            std::strncpy(o, r.id.c_str(), id_cap - 1);
+            o[id_cap - 1] = 0;
+        }
+        if (turns) turns[i] = r.turns;
+        if (trajs) trajs[i] = r.traj;
+        if (versions) versions[i] = r.version;
+    }
     return FM_OK;
 }
 

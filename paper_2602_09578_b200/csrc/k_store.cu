@@ -28,24 +28,21 @@
 namespace fm {
 namespace {
 
-__device__ __forceinline__ bool key_less(const DTableView& t, int a, int b) {
-    const uint64_t la = t.label[a], lb = t.label[b];
-    if (la != lb) return la < lb;
-    if (t.turns[a] != t.turns[b]) return t.turns[a] < t.turns[b];
-    if (t.traj[a] != t.traj[b]) return t.traj[a] < t.traj[b];
-    return t.version[a] < t.version[b];
-}
-
 __device__ __forceinline__ bool eligible(const DTableView& t, int s, int64_t version) {
     // experience_store.hpp:100: !processing && policy_version == current && ready()
     return (t.flags[s] & (kSlotLive | kSlotProcessing)) == kSlotLive && t.version[s] == version &&
            t.status[s] == t.full_mask;
 }
 
-__global__ void eligible_kernel(DTableView t, int64_t version, int* __restrict__ count, int* __restrict__ elist) {
+__global__ void eligible_kernel(DTableView t, int64_t version, int* __restrict__ count, int* __restrict__ elist,
+                                int* __restrict__ rank) {
     const int stride = gridDim.x * blockDim.x;
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < t.cap; s += stride) {
-        if (eligible(t, s, version)) elist[atomicAdd(count, 1)] = s;
+        if (eligible(t, s, version)) {
+            const int e = atomicAdd(count, 1);
+            elist[e] = s;
+            rank[e] = 0;  // rank_kernel accumulates into it
+        }
     }
 }
 
@@ -97,7 +94,8 @@ __global__ void __launch_bounds__(256) rank_kernel(DTableView t, const int* __re
 
 // One block: picks rank < mb, marks processing, builds the trainer's sample
 // descriptors from the HBM cells and the arena's codec headers, and writes the
-// host-visible result (slots in canonical order, total rows).
+// host-visible result (slots in canonical order, total rows) straight into
+// mapped pinned host memory (no separate D2H copy on the poll's critical path).
 __global__ void __launch_bounds__(1024) finish_kernel(DTableView t, const int* __restrict__ count,
                                                       const int* __restrict__ elist, const int* __restrict__ rank,
                                                       int mb, int pc, int rc, int ac, const uint8_t* __restrict__ arena,
@@ -327,10 +325,9 @@ cudaError_t launch_dt_poll(const DTableView& t, int64_t version, int mb, int pc,
                            const uint8_t* arena, DPollScratch sc, SampleDesc* desc, PollResult* res,
                            cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(sc.count, 0, sizeof(int), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(sc.rank, 0, sizeof(int) * static_cast<size_t>(t.cap), s);
     if (e != cudaSuccess) return e;
     const int blocks = (t.cap + 255) / 256;
-    eligible_kernel<<<blocks < 148 * 4 ? blocks : 148 * 4, 256, 0, s>>>(t, version, sc.count, sc.elist);
+    eligible_kernel<<<blocks < 148 * 4 ? blocks : 148 * 4, 256, 0, s>>>(t, version, sc.count, sc.elist, sc.rank);
     dim3 g(static_cast<unsigned>(blocks), static_cast<unsigned>(blocks < 16 ? blocks : 16));
     rank_kernel<<<g, 256, 0, s>>>(t, sc.count, sc.elist, sc.rank);
     finish_kernel<<<1, 1024, 0, s>>>(t, sc.count, sc.elist, sc.rank, mb, pc, rc, ac, arena, desc, res);

@@ -227,7 +227,7 @@ class ExperienceStore:
         samples = (_lib.fm_sample * max(n, 1))()
         handles = (C.c_int64 * max(n, 1))()
         got = C.c_int64()
-        pc, rc, ac = (c.encode() if c else None for c in columns)
+        pc, rc, ac = (c.encode() if c else None for c in (columns or (None, None, None)))
         check(lib().fm_store_poll(self._h, agent_id.encode(), current_version, n, pc, rc, ac,
                                   samples if pc else None, handles, C.byref(got)))
         if got.value == 0:
@@ -428,7 +428,16 @@ class DeviceExperienceStore:
             return None
         batch = MicroBatch(agent_id, current_version, dtable=self._h(agent_id), poll_id=pid.value,
                            rows=rows.value)
-        batch.samples = [self.record(agent_id, int(s)) for s in slots[:n]]
+        cap = 256
+        ids = C.create_string_buffer(n * cap)
+        turns, trajs, vers = np.zeros(n, np.int32), np.zeros(n, np.int32), np.zeros(n, np.int64)
+        check(lib().fm_dtable_records(self._h(agent_id), n, ptr(slots), ids, cap, ptr(turns), ptr(trajs), ptr(vers)))
+        raw = ids.raw
+        batch.samples = [SampleRecord(int(vers[i]), SampleId(raw[i * cap:(i + 1) * cap].split(b"\0", 1)[0].decode(),
+                                                             int(turns[i]), int(trajs[i])), int(slots[i]), None)
+                         for i in range(n)]
+        if any(len(s.sample_id.input_id) >= cap - 1 for s in batch.samples):  # long ids: one query each
+            batch.samples = [self.record(agent_id, int(s)) for s in slots[:n]]
         return batch
 
     def read_cells(self, agent_id: str, column: str, slots, as_float: bool = True) -> np.ndarray:
