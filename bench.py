@@ -711,7 +711,7 @@ def run_next(args) -> None:
     #      processing marked) against the host control plane, and group release on the GPU
     from paper_2602_09578_b200.engine import DeviceExperienceStore, ExperienceStore, SampleId, TableSchema
     ctx.reset_arena()
-    for nrec in (256, 4096):
+    for nrec in (256, 4096, 65536):
         ids = [SampleId(f"q{i // 16:05d}", 0, i % 16) for i in range(nrec)]
         order = rng.permutation(nrec)
         ds, hs = DeviceExperienceStore(ctx, capacity=nrec), ExperienceStore(ctx)
@@ -722,15 +722,26 @@ def run_next(args) -> None:
         for i in order:
             hs.insert("a", 0, ids[i])
             hs.set_cell("a", ids[i], 0, "advantage", 0.0)
+        # the C ABI calls a C++ orchestrator makes (no Python record building in the timed loop)
+        sl16 = np.zeros(16, np.int64)
+        got, rows, pid = C.c_int64(), C.c_int64(), C.c_int64()
+        hnd = (C.c_int64 * 16)()
+        polls = {
+            "device": lambda: (L.fm_dtable_poll(ds.table("a"), 0, 16, None, None, None, sl16.ctypes.data,
+                                                C.byref(rows), C.byref(got), C.byref(pid)), got.value)[1],
+            "host": lambda: (L.fm_store_poll(hs._h, b"a", 0, 16, None, None, None, None, hnd,
+                                             C.byref(got)), got.value)[1],
+        }
         res = {}
-        for name, st in (("device", ds), ("host", hs)):
+        for name, fn in polls.items():
             t0 = time.perf_counter()
             n = 0
-            while st.poll_micro_batch("a", 0, 16, columns=None) is not None:
+            while fn():
                 n += 1
             res[name] = (time.perf_counter() - t0) / max(n, 1) * 1e6
         out.append({"row": "f4 device table", "records": nrec, "micro_batch": 16,
-                    "poll_us": {k: round(v, 1) for k, v in res.items()}})
+                    "poll_us_c_abi": {k: round(v, 1) for k, v in res.items()},
+                    "device_path": "one-block bitonic" if nrec <= 1024 else "per-chunk bitonic candidates + rank + finish"})
         ds.close()
         hs.close()
     # release: 64 groups x 16 survivors, 1,024-token responses scored on the GPU (rule_reward + group_advantages)

@@ -9,6 +9,7 @@
 namespace fm {
 
 constexpr int kMaxPollMb = 1024;     // micro-batch size limit of the device poll
+constexpr int kSmallPollCap = 1024;  // tables up to this capacity poll in one block (bitonic sort)
 constexpr unsigned kSlotLive = 1u;
 constexpr unsigned kSlotProcessing = 2u;
 

@@ -13,11 +13,12 @@
 // The table is SoA in HBM (one slot per record).  The canonical order of the
 // reference's std::map<(input_id, turns, traj, version)> is kept with an
 // order-preserving 64-bit label per input_id (assigned by the host index), so
-// the key compare is four integer compares.  Selection is rank counting over
-// the eligible records (tables hold hundreds to a few thousand records):
-// rank(e) = #{eligible e' : key(e') < key(e)}; keys are unique, so the ranks
-// are a permutation and records with rank < mb are exactly the canonical-first
-// mb ready records — bit-exact with the reference's map walk.
+// the key compare is four integer compares.  A table of <= 1,024 slots polls in
+// one block (compaction + bitonic sort in shared memory); a larger one sorts
+// each 1,024-slot chunk in its own block and keeps the chunk's first mb, then
+// ranks those candidates: rank(e) = #{candidates e' : key(e') < key(e)}.  Keys
+// are unique, so records with rank < mb are exactly the canonical-first mb
+// ready records — bit-exact with the reference's map walk.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -32,18 +33,6 @@ __device__ __forceinline__ bool eligible(const DTableView& t, int s, int64_t ver
     // experience_store.hpp:100: !processing && policy_version == current && ready()
     return (t.flags[s] & (kSlotLive | kSlotProcessing)) == kSlotLive && t.version[s] == version &&
            t.status[s] == t.full_mask;
-}
-
-__global__ void eligible_kernel(DTableView t, int64_t version, int* __restrict__ count, int* __restrict__ elist,
-                                int* __restrict__ rank) {
-    const int stride = gridDim.x * blockDim.x;
-    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < t.cap; s += stride) {
-        if (eligible(t, s, version)) {
-            const int e = atomicAdd(count, 1);
-            elist[e] = s;
-            rank[e] = 0;  // rank_kernel accumulates into it
-        }
-    }
 }
 
 // 2D grid: x = a 256-record block of the eligible list, y strides over 256-record
@@ -92,29 +81,14 @@ __global__ void __launch_bounds__(256) rank_kernel(DTableView t, const int* __re
     if (i < n && less) atomicAdd(&rank[i], less);
 }
 
-// One block: picks rank < mb, marks processing, builds the trainer's sample
+// Marks the mb selected records processing, builds the trainer's sample
 // descriptors from the HBM cells and the arena's codec headers, and writes the
 // host-visible result (slots in canonical order, total rows) straight into
 // mapped pinned host memory (no separate D2H copy on the poll's critical path).
-__global__ void __launch_bounds__(1024) finish_kernel(DTableView t, const int* __restrict__ count,
-                                                      const int* __restrict__ elist, const int* __restrict__ rank,
-                                                      int mb, int pc, int rc, int ac, const uint8_t* __restrict__ arena,
-                                                      SampleDesc* __restrict__ desc, PollResult* __restrict__ res) {
-    __shared__ int sel[kMaxPollMb];
-    __shared__ int64_t scan[kMaxPollMb];
-    const int n = *count;
-    if (n < mb) {  // experience_store.hpp:104: fewer than mb ready -> nullopt, nothing marked
-        if (threadIdx.x == 0) {
-            res->got = 0;
-            res->rows = 0;
-        }
-        return;
-    }
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int r = rank[e];
-        if (r < mb) sel[r] = elist[e];
-    }
-    __syncthreads();
+// `sel` (shared) holds the selected slots in canonical order; one 1024-thread block.
+__device__ void emit_batch(DTableView& t, const int* sel, int mb, int pc, int rc, int ac,
+                           const uint8_t* __restrict__ arena, SampleDesc* __restrict__ desc,
+                           PollResult* __restrict__ res, int64_t* scan) {
     int64_t nr = 0;
     if (static_cast<int>(threadIdx.x) < mb) {
         const int s = sel[threadIdx.x];
@@ -146,6 +120,136 @@ __global__ void __launch_bounds__(1024) finish_kernel(DTableView t, const int* _
     if (threadIdx.x == 0) {
         res->got = mb;
         res->rows = scan[mb - 1];
+    }
+}
+
+// Large tables, last of three kernels: picks rank < mb.
+__global__ void __launch_bounds__(1024) finish_kernel(DTableView t, const int* __restrict__ count,
+                                                      const int* __restrict__ elist, const int* __restrict__ rank,
+                                                      int mb, int pc, int rc, int ac, const uint8_t* __restrict__ arena,
+                                                      SampleDesc* __restrict__ desc, PollResult* __restrict__ res) {
+    __shared__ int sel[kMaxPollMb];
+    __shared__ int64_t scan[kMaxPollMb];
+    const int n = *count;
+    if (n < mb) {  // experience_store.hpp:104: fewer than mb ready -> nullopt, nothing marked
+        if (threadIdx.x == 0) {
+            res->got = 0;
+            res->rows = 0;
+        }
+        return;
+    }
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        const int r = rank[e];
+        if (r < mb) sel[r] = elist[e];
+    }
+    __syncthreads();
+    emit_batch(t, sel, mb, pc, rc, ac, arena, desc, res, scan);
+}
+
+// Eligible records of slots [lo, lo + kSmallPollCap) compacted into shared memory
+// with their canonical key (label, turns, traj, version as order-preserving
+// unsigned words) and bitonic-sorted ascending; returns the eligible count.
+// One 1024-thread block.
+struct SortKeys {
+    uint64_t* k0;  // label
+    uint64_t* k1;  // (turns, traj)
+    uint64_t* k2;  // version
+    int* idx;      // slot
+};
+
+__device__ __forceinline__ SortKeys sort_keys(uint8_t* sm) {
+    SortKeys k;
+    k.k0 = reinterpret_cast<uint64_t*>(sm);
+    k.k1 = k.k0 + kSmallPollCap;
+    k.k2 = k.k1 + kSmallPollCap;
+    k.idx = reinterpret_cast<int*>(k.k2 + kSmallPollCap);
+    return k;
+}
+
+__device__ __forceinline__ bool key_gt(const SortKeys& k, int a, int b) {
+    if (k.k0[a] != k.k0[b]) return k.k0[a] > k.k0[b];
+    if (k.k1[a] != k.k1[b]) return k.k1[a] > k.k1[b];
+    return k.k2[a] > k.k2[b];
+}
+
+__device__ int gather_sorted(const DTableView& t, int64_t version, int lo, SortKeys k, int* cnt) {
+    if (threadIdx.x == 0) *cnt = 0;
+    __syncthreads();
+    const int hi = min(t.cap, lo + kSmallPollCap);
+    for (int s = lo + threadIdx.x; s < hi; s += blockDim.x) {
+        if (eligible(t, s, version)) {
+            const int e = atomicAdd(cnt, 1);
+            k.k0[e] = t.label[s];
+            k.k1[e] = (static_cast<uint64_t>(static_cast<uint32_t>(t.turns[s]) ^ 0x80000000u) << 32) |
+                      (static_cast<uint32_t>(t.traj[s]) ^ 0x80000000u);
+            k.k2[e] = static_cast<uint64_t>(t.version[s]) ^ 0x8000000000000000ull;
+            k.idx[e] = s;
+        }
+    }
+    __syncthreads();
+    const int n = *cnt;
+    int npad = 1;
+    while (npad < n) npad <<= 1;
+    for (int e = n + threadIdx.x; e < npad; e += blockDim.x) {
+        k.k0[e] = k.k1[e] = k.k2[e] = ~0ull;
+        k.idx[e] = -1;
+    }
+    __syncthreads();
+    for (int size = 2; size <= npad; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < npad / 2; i += blockDim.x) {
+                const int a = 2 * i - (i & (stride - 1));
+                const int b = a + stride;
+                const bool up = (a & size) == 0;
+                if (key_gt(k, a, b) == up) {
+                    uint64_t x;
+                    x = k.k0[a]; k.k0[a] = k.k0[b]; k.k0[b] = x;
+                    x = k.k1[a]; k.k1[a] = k.k1[b]; k.k1[b] = x;
+                    x = k.k2[a]; k.k2[a] = k.k2[b]; k.k2[b] = x;
+                    const int y = k.idx[a]; k.idx[a] = k.idx[b]; k.idx[b] = y;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    return n;
+}
+
+// Tables of <= kSmallPollCap slots: the whole poll in one block (one launch).
+__global__ void __launch_bounds__(1024) poll_small_kernel(DTableView t, int64_t version, int mb, int pc, int rc,
+                                                          int ac, const uint8_t* __restrict__ arena,
+                                                          SampleDesc* __restrict__ desc, PollResult* __restrict__ res) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    __shared__ int cnt;
+    __shared__ int64_t scan[kMaxPollMb];
+    const SortKeys k = sort_keys(sm);
+    const int n = gather_sorted(t, version, 0, k, &cnt);
+    if (n < mb) {  // experience_store.hpp:104: fewer than mb ready -> nullopt, nothing marked
+        if (threadIdx.x == 0) {
+            res->got = 0;
+            res->rows = 0;
+        }
+        return;
+    }
+    emit_batch(t, k.idx, mb, pc, rc, ac, arena, desc, res, scan);
+}
+
+// Larger tables, kernel 1 of 3: each block sorts one kSmallPollCap-slot chunk and
+// contributes its canonical-first min(mb, eligible) records as candidates; the
+// global first mb are among them (rank_kernel + finish_kernel pick them).
+__global__ void __launch_bounds__(1024) chunk_candidates_kernel(DTableView t, int64_t version, int mb,
+                                                                int* __restrict__ count, int* __restrict__ elist,
+                                                                int* __restrict__ rank) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    __shared__ int cnt, base;
+    const SortKeys k = sort_keys(sm);
+    const int n = gather_sorted(t, version, blockIdx.x * kSmallPollCap, k, &cnt);
+    const int take = min(n, mb);
+    if (threadIdx.x == 0) base = take ? atomicAdd(count, take) : 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < take; i += blockDim.x) {
+        elist[base + i] = k.idx[i];
+        rank[base + i] = 0;  // rank_kernel accumulates into it
     }
 }
 
@@ -324,11 +428,21 @@ __global__ void encode_kernel(DTableView t, int rc, int lc, const int64_t* __res
 cudaError_t launch_dt_poll(const DTableView& t, int64_t version, int mb, int pc, int rc, int ac,
                            const uint8_t* arena, DPollScratch sc, SampleDesc* desc, PollResult* res,
                            cudaStream_t s) {
+    const size_t smem = static_cast<size_t>(kSmallPollCap) * (3 * 8 + 4);
+    if (t.cap <= kSmallPollCap) {
+        cudaFuncSetAttribute(poll_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        poll_small_kernel<<<1, 1024, smem, s>>>(t, version, mb, pc, rc, ac, arena, desc, res);
+        return cudaGetLastError();
+    }
     cudaError_t e = cudaMemsetAsync(sc.count, 0, sizeof(int), s);
     if (e != cudaSuccess) return e;
-    const int blocks = (t.cap + 255) / 256;
-    eligible_kernel<<<blocks < 148 * 4 ? blocks : 148 * 4, 256, 0, s>>>(t, version, sc.count, sc.elist, sc.rank);
-    dim3 g(static_cast<unsigned>(blocks), static_cast<unsigned>(blocks < 16 ? blocks : 16));
+    const int chunks = (t.cap + kSmallPollCap - 1) / kSmallPollCap;
+    cudaFuncSetAttribute(chunk_candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    chunk_candidates_kernel<<<chunks, 1024, smem, s>>>(t, version, mb, sc.count, sc.elist, sc.rank);
+    // candidates <= chunks * mb: rank them pairwise (2D grid), then pick rank < mb
+    const int64_t cmax = static_cast<int64_t>(chunks) * mb;
+    const int bx = static_cast<int>((cmax + 255) / 256);
+    dim3 g(static_cast<unsigned>(bx), static_cast<unsigned>(bx < 16 ? bx : 16));
     rank_kernel<<<g, 256, 0, s>>>(t, sc.count, sc.elist, sc.rank);
     finish_kernel<<<1, 1024, 0, s>>>(t, sc.count, sc.elist, sc.rank, mb, pc, rc, ac, arena, desc, res);
     return cudaGetLastError();
