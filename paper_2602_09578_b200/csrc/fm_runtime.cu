@@ -190,6 +190,11 @@ uint64_t arena_token_count(const fm_ctx* ctx, uint64_t offset, bool* found) {
 
 namespace {
 
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return v && *v ? std::max(1, std::atoi(v)) : dflt;
+}
+
 int set_dev(const fm_ctx* c) {
     FM_CUDA(cudaSetDevice(c->device));
     return FM_OK;
@@ -1006,7 +1011,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g1.M = static_cast<int>(M);
             g1.N = static_cast<int>(a->V);
             g1.K = static_cast<int>(a->D);
-            g1.group_m = 16;
+            g1.group_m = env_int("FM_G1_GROUP_M", 16);  // raster: m-tiles per group (L2 reuse)
             if (fold) {  // p~^T straight into GEMM2's A operand buffer
                 g1.mrow = w.mrow;
                 g1.pexp_t = w.gt;
@@ -1043,7 +1048,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g2.M = static_cast<int>(a->V);
             g2.N = static_cast<int>(a->D);
             g2.K = static_cast<int>(Mpad);
-            g2.group_m = 8;
+            g2.group_m = env_int("FM_G2_GROUP_M", 8);
             g2.out = static_cast<float*>(a->dW);
             g2.ld_out = static_cast<long long>(a->D);
             g2.accumulate = a->dw_valid ? 1 : 0;

@@ -330,42 +330,48 @@ __device__ __forceinline__ int token_at(const uint8_t* arena, uint64_t off, uint
 }
 
 // rule_reward (training.hpp:71-83): longest prefix of `pattern` occurring
-// contiguously in the response, / |pattern|.
-__device__ double rule_reward_dev(const uint8_t* arena, uint64_t off, const int* pat, int np) {
+// contiguously in the response, / |pattern|.  Warp-cooperative: lane l tries the
+// start positions l, l+32, ... (coalesced u64 token loads), then a warp max.
+__device__ double rule_reward_warp(const uint8_t* arena, uint64_t off, const int* pat, int np) {
     const uint64_t n = *reinterpret_cast<const uint64_t*>(arena + off);
     if (n == 0 || np == 0) return 0.0;
     int best = 0;
-    for (uint64_t start = 0; start < n && best < np; ++start) {
+    for (uint64_t start = threadIdx.x & 31; start < n; start += 32) {
         int len = 0;
         while (len < np && start + len < n && token_at(arena, off, start + len) == pat[len]) ++len;
         best = max(best, len);
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
     return static_cast<double>(best) / static_cast<double>(np);
 }
 
-// release_group (rollout.hpp:812-834): one warp per group; lane i scores
-// survivor i (strided for k > 32); lane 0 normalises in the reference's
+// release_group (rollout.hpp:812-834): one block per group.  Each warp scores
+// survivors (warp-parallel rule_reward); thread 0 normalises in the reference's
 // sequential order with explicit round-to-nearest ops (no FMA contraction), so
 // the advantages are bit-identical to group_advantages (training.hpp:54-67);
 // then every record of every survivor gets both cells.
-__global__ void release_kernel(const DTableView* __restrict__ tabs, const DReleaseCols* __restrict__ cols,
-                               int ngroups, const int32_t* __restrict__ seg_off,
-                               const int32_t* __restrict__ score_tab, const int64_t* __restrict__ score_slot,
-                               const int32_t* __restrict__ rec_off, const int32_t* __restrict__ rec_tab,
-                               const int64_t* __restrict__ rec_slot, const int* __restrict__ pat, int np,
-                               double eps, const uint8_t* __restrict__ arena, double* __restrict__ rewards,
-                               double* __restrict__ advs) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= ngroups) return;
-    const int b = seg_off[warp], e = seg_off[warp + 1];
-    for (int i = b + lane; i < e; i += 32) {
+__global__ void __launch_bounds__(512) release_kernel(const DTableView* __restrict__ tabs,
+                                                      const DReleaseCols* __restrict__ cols, int ngroups,
+                                                      const int32_t* __restrict__ seg_off,
+                                                      const int32_t* __restrict__ score_tab,
+                                                      const int64_t* __restrict__ score_slot,
+                                                      const int32_t* __restrict__ rec_off,
+                                                      const int32_t* __restrict__ rec_tab,
+                                                      const int64_t* __restrict__ rec_slot, const int* __restrict__ pat,
+                                                      int np, double eps, const uint8_t* __restrict__ arena,
+                                                      double* __restrict__ rewards, double* __restrict__ advs) {
+    const int g = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int b = seg_off[g], e = seg_off[g + 1];
+    for (int i = b + warp; i < e; i += nw) {
         const DTableView& t = tabs[score_tab[i]];
         const uint64_t off = t.cells[static_cast<size_t>(cols[score_tab[i]].response) * t.cap + score_slot[i]];
-        rewards[i] = rule_reward_dev(arena, off, pat, np);
+        const double r = rule_reward_warp(arena, off, pat, np);
+        if (lane == 0) rewards[i] = r;
     }
-    __syncwarp();
-    if (lane == 0 && e > b) {
+    __syncthreads();
+    if (threadIdx.x == 0 && e > b) {
         const double k = static_cast<double>(e - b);
         double mean = 0.0;
         for (int i = b; i < e; ++i) mean = __dadd_rn(mean, rewards[i]);
@@ -380,8 +386,8 @@ __global__ void release_kernel(const DTableView* __restrict__ tabs, const DRelea
         const double den = __dadd_rn(sd, eps);
         for (int i = b; i < e; ++i) advs[i] = __ddiv_rn(__dadd_rn(rewards[i], -mean), den);
     }
-    __syncwarp();
-    for (int i = b; i < e; ++i) {
+    __syncthreads();
+    for (int i = b + warp; i < e; i += nw) {
         for (int r = rec_off[i] + lane; r < rec_off[i + 1]; r += 32) {
             const DTableView& t = tabs[rec_tab[r]];
             const DReleaseCols& c = cols[rec_tab[r]];
@@ -495,10 +501,8 @@ cudaError_t launch_dt_release(const DTableView* tabs, const DReleaseCols* cols, 
                               const int32_t* rec_tab, const int64_t* rec_slot, const int* pat, int np, double eps,
                               const uint8_t* arena, double* rewards, double* advs, cudaStream_t s) {
     if (ngroups <= 0) return cudaSuccess;
-    const int threads = 128;
-    release_kernel<<<(ngroups * 32 + threads - 1) / threads, threads, 0, s>>>(
-        tabs, cols, ngroups, seg_off, score_tab, score_slot, rec_off, rec_tab, rec_slot, pat, np, eps, arena, rewards,
-        advs);
+    release_kernel<<<ngroups, 512, 0, s>>>(tabs, cols, ngroups, seg_off, score_tab, score_slot, rec_off, rec_tab,
+                                           rec_slot, pat, np, eps, arena, rewards, advs);
     return cudaGetLastError();
 }
 
