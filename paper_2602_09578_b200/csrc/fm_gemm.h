@@ -20,6 +20,7 @@ enum class GemmKind { Logits, Grad };
 // with boxes {64, 128} (A) and {64, 256} (B), SWIZZLE_128B.
 struct GemmArgs {
     int M, N, K;
+    int k0 = 0;           // first K index (a K-chunk of a longer product; multiple of 64)
     int group_m;          // L2 raster: tiles visited in column-major groups of group_m row-tiles
     float* out;           // Grad: dW [M][ld_out]
     __nv_bfloat16* pexp;  // Logits: p~ = exp(z - m_tile) [M][ld_out] bf16

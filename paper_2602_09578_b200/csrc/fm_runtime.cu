@@ -1062,8 +1062,30 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 for (int o = 0; o < gs->g; ++o) g2.xpeer[o] = gs->peer_slot[o];
             }
             {
+                // Long K (rows of the micro-batch): optionally launch K-chunks of FM_G2_KCHUNK
+                // rows in sequence, each accumulating into dW, so concurrent tiles stay within
+                // one chunk's operands (L2 reuse).  Off by default: at C5 N=1 (K = 65,536) the
+                // A/B on one box was within noise (profiles/r01_kchunk.jsonl).  When chunked
+                // the micro-batch grad norm spans several accumulations and reads NaN.
+                const int kc_env = env_int("FM_G2_KCHUNK", 1 << 30);  // default: one launch
+                const int kc = static_cast<int>(round_up(static_cast<uint64_t>(std::min(kc_env, 1 << 30)), 64));
+                const int nch = (static_cast<int>(Mpad) + kc - 1) / kc;
                 KScope k(c, K_GEMM2, s);
-                FM_CUDA(gemm_tn_launch(GemmKind::Grad, tGt, tPt, g2, c->num_sms, s));
+                if (nch == 1) {
+                    FM_CUDA(gemm_tn_launch(GemmKind::Grad, tGt, tPt, g2, c->num_sms, s));
+                } else {
+                    FM_CUDA(cudaMemsetAsync(scal, 0xFF, sizeof(double), s));  // NaN grad norm
+                    for (int ch = 0; ch < nch; ++ch) {
+                        GemmArgs gc = g2;
+                        gc.k0 = ch * kc;
+                        gc.K = std::min(kc, static_cast<int>(Mpad) - gc.k0);
+                        gc.accumulate = (a->dw_valid || ch > 0) ? 1 : 0;
+                        gc.sumsq = nullptr;
+                        if (ch + 1 < nch) gc.xg = 0;  // the gang exchange rides on the last chunk
+                        FM_CUDA(gemm_tn_launch(GemmKind::Grad, tGt, tPt, gc, c->num_sms, s));
+                    }
+                    count_launch(nch - 1);
+                }
             }
             if (exchange) {
                 a->dw_valid = true;

@@ -303,8 +303,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int k = 0; k < k_iters; ++k) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-                    tma_load_2d_hint(sA + stage * A_STAGE, &tmA, &full[stage], k * BK, tc.mb * BM, pol_a);
-                    tma_load_2d_hint(sB + stage * B_STAGE, &tmB, &full[stage], k * BK, tc.nb * BN, pol_a);
+                    tma_load_2d_hint(sA + stage * A_STAGE, &tmA, &full[stage], args.k0 + k * BK, tc.mb * BM, pol_a);
+                    tma_load_2d_hint(sB + stage * B_STAGE, &tmB, &full[stage], args.k0 + k * BK, tc.nb * BN, pol_a);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -471,8 +471,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                     mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t fb = mapa_shared(&full[stage], 0);
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
-                    tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, k * BK, arow, pol);
-                    tma_load_2d_2sm(sB + stage * P_B_STAGE, &tmB, fb, k * BK, brow, pol);
+                    tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, args.k0 + k * BK, arow, pol);
+                    tma_load_2d_2sm(sB + stage * P_B_STAGE, &tmB, fb, args.k0 + k * BK, brow, pol);
                     if (++stage == P_STAGES) {
                         stage = 0;
                         phase ^= 1;
