@@ -301,11 +301,8 @@ def run_ours(args, dist: Dist) -> dict | None:
         ntok = 0
         for i, a in enumerate(order):
             h = handles[a]
-            nxt = order[(i + 1) % len(order)]
-            if len(order) > 1 and swap and not active[nxt]:
-                check(timed("activate", L.fm_agent_activate, handles[nxt], ctx.handle))  # prefetch
-                active[nxt] = True
-            for _ in range(G // mb):
+            prev, nxt = order[i - 1], order[(i + 1) % len(order)]
+            for j in range(G // mb):
                 batch = timed("poll", store.poll_micro_batch, a, step, mb)
                 if batch is None:
                     raise RuntimeError(f"experience store ran dry for {a} at step {step}")
@@ -317,12 +314,19 @@ def run_ours(args, dist: Dist) -> dict | None:
                     check(timed("train", L.fm_train_micro_batch, h, arr, mb, G, C.byref(t)))
                 timed("complete", store.complete, a, batch.samples)
                 ntok += cfg.resp_len * mb
+                if j == 0 and len(order) > 1 and swap:
+                    # swap after this agent's first micro-batch is queued: the previous agent
+                    # parks and the next one is prefetched while micro-batches 1..3 run (the
+                    # copy engines then overlap GEMMs, not the latency-bound K-gather)
+                    if prev != a and active[prev]:
+                        check(timed("suspend", L.fm_agent_suspend, handles[prev], tier, -1))
+                        active[prev] = False
+                    if not active[nxt]:
+                        check(timed("activate", L.fm_agent_activate, handles[nxt], ctx.handle))
+                        active[nxt] = True
             if a in comms:
                 check(timed("allreduce", L.fm_agent_allreduce_grad, h, comms[a]))
             check(timed("update", L.fm_apply_update, h, G, cfg.lr, 0.9, 0.999, 1e-8, None, None))
-            if len(order) > 1 and swap:
-                check(timed("suspend", L.fm_agent_suspend, h, tier, -1))
-                active[a] = False
         return ntok
 
     for s in range(args.warmup):
@@ -804,10 +808,7 @@ def run_e2e(args, cfg, ctx, mine, handles, place, comms, dist, tier) -> dict:
         nonlocal h2d, d2h
         for i, a in enumerate(order):
             h = handles[a]
-            nxt = order[(i + 1) % len(order)]
-            if len(order) > 1 and tier is not None and not active[nxt]:
-                check(L.fm_agent_activate(handles[nxt], ctx.handle))
-                active[nxt] = True
+            prev, nxt = order[i - 1], order[(i + 1) % len(order)]
             if len(order) > 1 and tier is not None and not active[a]:
                 check(L.fm_agent_activate(h, ctx.handle))
                 active[a] = True
@@ -822,6 +823,13 @@ def run_e2e(args, cfg, ctx, mine, handles, place, comms, dist, tier) -> dict:
                 t = C.c_int64()
                 check(L.fm_train_micro_batch_host(h, arr, mb, G, C.byref(t)))
                 tickets.append(t.value)
+                if b == 0 and len(order) > 1 and tier is not None:  # same swap schedule as the main loop
+                    if prev != a and active[prev]:
+                        check(L.fm_agent_suspend(handles[prev], tier, -1))
+                        active[prev] = False
+                    if not active[nxt]:
+                        check(L.fm_agent_activate(handles[nxt], ctx.handle))
+                        active[nxt] = True
             if a in comms:
                 check(L.fm_agent_allreduce_grad(h, comms[a]))
             gn = C.c_double()
@@ -833,9 +841,6 @@ def run_e2e(args, cfg, ctx, mine, handles, place, comms, dist, tier) -> dict:
                 if r != 1:
                     raise RuntimeError("micro-batch report not ready after the update")
                 d2h += 16
-            if len(order) > 1 and tier is not None:
-                check(L.fm_agent_suspend(h, tier, -1))
-                active[a] = False
 
     one(steps[0])
     ctx.synchronize()
