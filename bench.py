@@ -777,6 +777,73 @@ def run_next(args) -> None:
         emit(r)
 
 
+def run_migrate(args, dist) -> None:
+    """--migrate (torchrun, 2 ranks): a C2 agent with a pending gradient moves
+    between the two GPUs (fm_agent_migrate_export lends the live slot via CUDA
+    IPC -> import: copy-engine NVLink peer copy into the target's slot) back and
+    forth; the target's import call blocks until the state landed, so its host
+    time is the migration latency (the first hop per direction also maps the
+    peer slot).  One JSON line from rank 0."""
+    from paper_2602_09578_b200 import _lib
+    from paper_2602_09578_b200 import workload as wl
+    from paper_2602_09578_b200.engine import Context, seeded_weights
+    if dist.world != 2:
+        raise SystemExit("--migrate needs exactly 2 ranks")
+    L = _lib.lib()
+    cfg = wl.CONFIGS[args.config]
+    V, D = cfg.vocab, cfg.feat
+    ctx = Context(dist.local)
+    h = None
+    if dist.rank == 0:
+        h = C.c_void_p()
+        _lib.check(L.fm_agent_create(ctx.handle, b"mover", V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
+        W0 = seeded_weights(V, D, 7).reshape(-1)
+        _lib.check(L.fm_agent_set_weights(h, W0.ctypes.data))
+        samples = wl.step_samples(cfg, "agent0", 0)[:cfg.micro_batch]
+        arr = (_lib.fm_sample * len(samples))(*[_lib.fm_sample(ctx.put(x.prompt_payload), ctx.put(x.response_payload),
+                                                                0.5) for x in samples])
+        t = C.c_int64()
+        _lib.check(L.fm_train_micro_batch(h, arr, len(samples), cfg.global_batch, C.byref(t)))  # pending gradient
+        ctx.synchronize()
+    times = []
+    holder = 0
+    for rep in range(5):
+        dst = 1 - holder
+        blob = None
+        if dist.rank == holder:
+            n = C.c_uint64()
+            _lib.check(L.fm_agent_migrate_export(h, None, 0, C.byref(n)))
+            b = (C.c_uint8 * n.value)()
+            _lib.check(L.fm_agent_migrate_export(h, b, n.value, C.byref(n)))
+            blob = bytes(b)
+        else:  # a fresh agent (slot) on the target, ready before the timed import
+            h = C.c_void_p()
+            _lib.check(L.fm_agent_create(ctx.handle, b"mover", V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
+            ctx.synchronize()
+        blob = dist.bcast_obj(blob, src=holder)
+        if dist.rank == dst:
+            buf = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+            t0 = time.perf_counter()
+            _lib.check(L.fm_agent_migrate_import(h, ctx.handle, buf, len(blob)))
+            times.append(time.perf_counter() - t0)
+        dist.barrier()  # imported: the source may drop its parked copy
+        if dist.rank == holder:
+            L.fm_agent_destroy(h)
+            h = None
+        holder = dst
+    t_best = dist.bcast_obj(min(times) if times else None, src=1)
+    t_best = min(x for x in (t_best, dist.bcast_obj(min(times) if times else None, src=0)) if x is not None)
+    nbytes = V * D * (8 + 4 + 4 + 4 + 2) + D * 4  # W f64, m, v, pending dW, bf16 shadow, colmax
+    if dist.rank == 0:
+        emit({"row": "agent migration (cross-process, NVLink)", "config": args.config, "params": V * D,
+              "state_bytes": nbytes, "best_ms": round(t_best * 1e3, 3),
+              "GB_per_s": round(nbytes / t_best / 1e9, 1),
+              "hops": 5, "note": "best import latency over 5 hops; slots recycled, so IPC mappings are cached after the first hop per direction"})
+    if h is not None:
+        L.fm_agent_destroy(h)
+    ctx.close()
+
+
 def run_e2e(args, cfg, ctx, mine, handles, place, comms, dist, tier) -> dict:
     """Same metric through the public API with HOST payload buffers: each step
     stages that step's encoded token lists host->device inside the timed
@@ -979,6 +1046,8 @@ def main():
     ap.add_argument("--store", default="host", choices=["host", "device"],
                     help="experience store: host control plane (default) or the on-device table (§8f-4)")
     ap.add_argument("--next", action="store_true", help="measure the SURVEY §8f next rows (one GPU)")
+    ap.add_argument("--migrate", action="store_true",
+                    help="(torchrun, 2 GPUs) cross-process migration of a C2 agent over NVLink")
     ap.add_argument("--next-vocab", type=int, default=32000)
     ap.add_argument("--next-feat", type=int, default=4096)
     ap.add_argument("--next-requests", type=int, default=256)
@@ -994,6 +1063,9 @@ def main():
         if args.next:
             if dist.rank == 0:
                 run_next(args)
+            return
+        if args.migrate:
+            run_migrate(args, dist)
             return
         from paper_2602_09578_b200 import workload as wl
         cfg = wl.CONFIGS[args.config]

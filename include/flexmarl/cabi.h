@@ -206,6 +206,20 @@ int fm_agent_activate(fm_agent* a, fm_ctx* ctx);
 /* FNV-1a over the bytes of {W, m, v, grad, step, version, samples}: swap-identity check. */
 int fm_agent_state_checksum(fm_agent* a, uint64_t* out);
 
+/* ---- migration between GPUs of different processes (SURVEY §8e agents <-> GPUs) ----
+ * The location-agnostic swap (training.hpp:259-350) across the one-process-per-GPU
+ * layout.  export lends the agent's live training slot: it writes a blob (CUDA IPC
+ * handles of the slot and of an interprocess event recorded after the agent's
+ * queued compute, plus version / Adam step / accumulated samples) and the agent
+ * becomes inactive; the caller ships the blob to the target process (any side
+ * channel), whose import pulls the state into an agent of the same shape that is
+ * active on its GPU (e.g. fresh from fm_agent_create) with copy-engine NVLink peer
+ * copies on its copy stream, blocking the host until they land.  After the import
+ * returned, the sender calls migrate_release (or destroy) to return the slot. */
+int fm_agent_migrate_export(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64_t* len);
+int fm_agent_migrate_import(fm_agent* a, fm_ctx* ctx, const uint8_t* blob, uint64_t len);
+int fm_agent_migrate_release(fm_agent* a);
+
 /* ---- weight publish / rollout sync ----------------------------
  * publish_weights (training.hpp:459-467): one contiguous device buffer in
  * pack_weights' single-tensor layout (object_store.hpp:258-273), stamped with

@@ -89,6 +89,9 @@ _PROTOS = {
     "fm_agent_suspend": (I, [P, I, I]),
     "fm_agent_activate": (I, [P, P]),
     "fm_agent_state_checksum": (I, [P, PU64]),
+    "fm_agent_migrate_export": (I, [P, P, U64, PU64]),
+    "fm_agent_migrate_import": (I, [P, P, P, U64]),
+    "fm_agent_migrate_release": (I, [P]),
     "fm_group_advantages": (I, [P, P, P, I, D, P]),
     "fm_comm_unique_id": (I, [P]),
     "fm_comm_create": (I, [P, P, I, I, C.POINTER(P)]),

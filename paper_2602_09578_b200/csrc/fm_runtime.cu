@@ -23,6 +23,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -171,6 +172,7 @@ struct fm_ctx {
     // the latest K-GEMM1 launch on the compute stream (swap copies start there, see
     // fm_agent_suspend) and the op sequence numbers that say what it follows
     cudaEvent_t ev_gemm = nullptr;
+    std::map<std::string, void*> ipc_cache;  // peer training slots mapped for migrations
     uint64_t op_seq = 0, gemm_seq = 0;
     uint8_t* arena = nullptr;
     uint64_t arena_cap = 0, arena_used = 0;
@@ -537,6 +539,7 @@ int fm_ctx_destroy(fm_ctx* c) {
     cudaStreamDestroy(c->copy_in);
     cudaStreamDestroy(c->copy_out);
     if (c->ev_gemm) cudaEventDestroy(c->ev_gemm);
+    for (auto& kv : c->ipc_cache) cudaIpcCloseMemHandle(kv.second);
     delete c;
     return FM_OK;
 }
@@ -684,6 +687,8 @@ struct fm_agent {
     void* park = nullptr;  // W | m | v | dW   (host pinned or device)
     size_t park_bytes = 0;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_compute = nullptr;
+    cudaEvent_t ev_ipc = nullptr;  // interprocess: the source's work before a migration is done
+    bool lent = false;             // exported by migration; slot reserved until migrate_release
     Slot* slot = nullptr;
     GangState* gang = nullptr;
 };
@@ -826,6 +831,7 @@ int fm_agent_create(fm_ctx* c, const char* name, uint64_t V, uint64_t D, int pre
 
 int fm_agent_destroy(fm_agent* a) {
     if (!a) return FM_OK;
+    if (a->lent) fm_agent_migrate_release(a);
     fm_gang_detach(a);
     if (a->ctx) {
         cudaSetDevice(a->ctx->device);
@@ -849,6 +855,7 @@ int fm_agent_destroy(fm_agent* a) {
     cudaEventDestroy(a->ev_in);
     cudaEventDestroy(a->ev_out);
     cudaEventDestroy(a->ev_compute);
+    if (a->ev_ipc) cudaEventDestroy(a->ev_ipc);
     delete a;
     return FM_OK;
 }
@@ -1432,6 +1439,7 @@ int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
 int fm_agent_activate(fm_agent* a, fm_ctx* c) {
     FM_GUARD_BEGIN
     if (a->active) return fail(FM_ERR_CONFIG_ERROR, a->name + " already active");
+    if (a->lent) return fail(FM_ERR_CONFIG_ERROR, a->name + " was migrated away (fm_agent_migrate_release)");
     if (!c) return fail(FM_ERR_NO_DEVICE, "null context");
     if (int st = set_dev(c)) return st;
     const size_t P = a->P;
@@ -1470,6 +1478,135 @@ int fm_agent_activate(fm_agent* a, fm_ctx* c) {
     a->pending_in = true;  // consumers wait lazily (check_active)
     a->ctx = c;
     a->active = true;
+    return FM_OK;
+    FM_GUARD_END
+}
+
+// ---- cross-process migration over NVLink (location-agnostic swap between GPUs) ----
+// The sender lends its live training slot: it exports CUDA IPC handles of the
+// slot and of an interprocess event recorded on its compute stream after the
+// agent's queued work, and stops using the agent.  The receiver maps the slot
+// (mappings are cached per context: slots are recycled, so after the first hop
+// a migration is just the copy) and pulls the state into its own slot with
+// copy-engine NVLink peer copies on its copy stream.  No park copy on the
+// source.  The sender returns the slot to its pool with fm_agent_migrate_release
+// once the receiver's import has returned (training.hpp:259-350 with a
+// placement change; SURVEY §8e "agents <-> GPUs").
+namespace {
+struct MigrateBlob {
+    uint32_t magic;  // 'FMMG'
+    int32_t precision;
+    uint64_t V, D;
+    int32_t src_device;
+    uint8_t dw_valid, cm_valid, pad0, pad1;
+    int64_t step, version, samples;
+    uint64_t off_w, off_m, off_v, off_dw, off_w16, off_cm;  // within the slot
+    cudaIpcMemHandle_t mem;
+    cudaIpcEventHandle_t ev;
+};
+constexpr uint32_t kMigrateMagic = 0x474d4d46u;
+}  // namespace
+
+int fm_agent_migrate_export(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64_t* len) {
+    FM_GUARD_BEGIN
+    *len = sizeof(MigrateBlob);
+    if (!blob_out) return FM_OK;
+    if (cap < sizeof(MigrateBlob)) return fail(FM_ERR_INVALID_ARG, "blob buffer too small");
+    if (int st = check_active(a)) return st;
+    if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang (fm_gang_detach first)");
+    fm_ctx* c = a->ctx;
+    if (int st = set_dev(c)) return st;
+    if (!a->ev_ipc) FM_CUDA(cudaEventCreateWithFlags(&a->ev_ipc, cudaEventDisableTiming | cudaEventInterprocess));
+    FM_CUDA(cudaEventRecord(a->ev_ipc, c->stream));  // after everything queued for the agent
+    const uint8_t* base = static_cast<const uint8_t*>(a->slot->base);
+    auto off = [&](const void* q) { return static_cast<uint64_t>(static_cast<const uint8_t*>(q) - base); };
+    MigrateBlob b{};
+    b.magic = kMigrateMagic;
+    b.precision = a->precision;
+    b.V = a->V;
+    b.D = a->D;
+    b.src_device = c->device;
+    b.dw_valid = a->dw_valid;
+    b.cm_valid = a->W16 && a->cm_gen == a->w16_gen;
+    b.step = a->step;
+    b.version = a->version;
+    b.samples = a->samples;
+    b.off_w = off(a->W);
+    b.off_m = off(a->m);
+    b.off_v = off(a->v);
+    b.off_dw = off(a->dW);
+    b.off_w16 = a->W16 ? off(a->W16) : 0;
+    b.off_cm = a->colmax ? off(a->colmax) : 0;
+    FM_CUDA(cudaIpcGetMemHandle(&b.mem, a->slot->base));
+    FM_CUDA(cudaIpcGetEventHandle(&b.ev, a->ev_ipc));
+    std::memcpy(blob_out, &b, sizeof(b));
+    a->active = false;  // lent: the slot stays reserved until fm_agent_migrate_release
+    a->lent = true;
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int fm_agent_migrate_release(fm_agent* a) {
+    FM_GUARD_BEGIN
+    if (!a->lent) return fail(FM_ERR_CONFIG_ERROR, a->name + " was not exported");
+    fm_ctx* c = a->ctx;
+    if (int st = set_dev(c)) return st;
+    agent_free_device(a, c->stream);
+    a->lent = false;
+    a->ctx = nullptr;
+    a->dw_valid = false;
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int fm_agent_migrate_import(fm_agent* a, fm_ctx* c, const uint8_t* blob, uint64_t len) {
+    FM_GUARD_BEGIN
+    if (len != sizeof(MigrateBlob)) return fail(FM_ERR_INVALID_ARG, "migration blob size mismatch");
+    MigrateBlob b;
+    std::memcpy(&b, blob, sizeof(b));
+    if (b.magic != kMigrateMagic) return fail(FM_ERR_INVALID_ARG, "not a migration blob");
+    if (b.V != a->V || b.D != a->D || b.precision != a->precision)
+        return fail(FM_ERR_CONFIG_ERROR, "migration blob describes another model shape/precision");
+    if (!a->active || a->ctx != c) return fail(FM_ERR_INACTIVE_GROUP, a->name + " must be active on the target GPU");
+    if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang");
+    if (int st = set_dev(c)) return st;
+    const std::string key(reinterpret_cast<const char*>(&b.mem), sizeof(b.mem));
+    void* src = nullptr;
+    auto it = c->ipc_cache.find(key);
+    if (it != c->ipc_cache.end()) {
+        src = it->second;
+    } else {
+        FM_CUDA(cudaIpcOpenMemHandle(&src, b.mem, cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_cache.emplace(key, src);
+    }
+    cudaEvent_t ev = nullptr;
+    FM_CUDA(cudaIpcOpenEventHandle(&ev, b.ev));
+    // after everything already queued on the agent's slot, and after the source's queued work
+    FM_CUDA(cudaEventRecord(a->ev_compute, c->stream));
+    FM_CUDA(cudaStreamWaitEvent(c->copy_in, a->ev_compute, 0));
+    FM_CUDA(cudaStreamWaitEvent(c->copy_in, ev, 0));
+    const size_t P = a->P;
+    const uint8_t* p = static_cast<const uint8_t*>(src);
+    auto cp = [&](void* dst, uint64_t off, size_t n) {
+        return cudaMemcpyPeerAsync(dst, c->device, p + off, b.src_device, n, c->copy_in);
+    };
+    FM_CUDA(cp(a->W, b.off_w, P * 8));
+    FM_CUDA(cp(a->m, b.off_m, P * 4));
+    FM_CUDA(cp(a->v, b.off_v, P * 4));
+    if (b.dw_valid) FM_CUDA(cp(a->dW, b.off_dw, P * dw_elem(a)));
+    if (a->W16) FM_CUDA(cp(a->W16, b.off_w16, P * 2));
+    if (a->W16 && b.cm_valid) FM_CUDA(cp(a->colmax, b.off_cm, a->D * 4));
+    FM_CUDA(cudaEventRecord(a->ev_in, c->copy_in));
+    a->dw_valid = b.dw_valid;
+    a->step = b.step;
+    a->version = b.version;
+    a->samples = b.samples;
+    ++a->w16_gen;
+    a->cm_gen = (a->W16 && b.cm_valid) ? a->w16_gen : ~0ull;
+    a->pending_in = true;  // consumers wait lazily (check_active)
+    // the source may release its slot once this returns
+    FM_CUDA(cudaEventSynchronize(a->ev_in));
+    cudaEventDestroy(ev);
     return FM_OK;
     FM_GUARD_END
 }
