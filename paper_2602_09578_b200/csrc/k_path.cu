@@ -332,8 +332,10 @@ __global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ zact
             // The per-row factor sig = -c / s goes into GEMM2's B operand
             // (Phic^T's <= 4 count entries of column t), the delta term into A:
             //   A[a][t] = p~_a - s   =>   sig * A = -c (p - delta) = G.
-            const float sig = (valid && ce != 0.f) ? __fdividef(-ce, s) : 0.f;
-            if (sl == 4 && sig != 0.f)
+            // an action outside [0, V) never matches a vocab row (policy.hpp:84-85): the
+            // row still gets -c p, just no delta term
+            const float sig = ce != 0.f ? __fdividef(-ce, s) : 0.f;
+            if (sl == 4 && sig != 0.f && valid)
                 pexp_t[static_cast<size_t>(a) * ldt + r] = __float2bfloat16_rn(__expf(za - m) - s);
             if (sl < 4) {
                 const int f = sl == 0 ? f4.x : sl == 1 ? f4.y : sl == 2 ? f4.z : f4.w;
