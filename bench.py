@@ -586,6 +586,271 @@ def run_c4(args, dist: Dist) -> dict:
                 core_updates_per_epoch=Cn, aux_updates_per_epoch=A)
 
 
+def run_c4_dynamic(args, dist: Dist) -> dict:
+    """BASELINE config C4 with a drifting core (`--c4-policy dynamic` vs
+    `static`): the core role (~76% of the experience) alternates between agent0
+    and agent1 every `--c4-phase-epochs` epochs, as the activation skew of a
+    two-stage workflow moves.  Each epoch executes the same work as run_c4 (C
+    core updates + A rotating auxiliary updates).
+      dynamic: the agent-centric plan is recomputed at every phase boundary and
+        agents follow it: the old core's DP gang consolidates its sharded state
+        (fm_gang_gather_state) and migrates to an auxiliary GPU; the new core is
+        shared out of its auxiliary GPU to the GPUs of its new gang
+        (fm_agent_share_export / migrate_import over NVLink) and re-forms the
+        fused reduce-scatter gang.  Transitions are inside the timed region.
+      static: one slice per agent (agent i on GPU i mod N) for the whole run."""
+    from paper_2602_09578_b200 import _lib
+    from paper_2602_09578_b200 import workload as wl
+    from paper_2602_09578_b200._lib import check, lib
+    from paper_2602_09578_b200.engine import Context, agent_seed, group_advantages, seeded_weights
+    from paper_2602_09578_b200.engine import ExperienceStore, SampleId, TableSchema
+    from paper_2602_09578_b200.placement import agent_centric_plan, static_plan
+    L = lib()
+    cfg = wl.CONFIGS["C4"]
+    if args.resp_len:
+        cfg = wl.Config(cfg.name, cfg.agents, cfg.vocab, cfg.feat, cfg.group_k, cfg.micro_batch,
+                        cfg.global_batch, args.resp_len, cfg.seed, cfg.lr)
+    agents = list(cfg.agents)
+    N, me = dist.world, dist.rank
+    A = max(1, int(round(0.24 * N)))
+    Cn = int(round(A * 0.76 / 0.24))
+    Pe = args.c4_phase_epochs or 2
+    G, mb = cfg.global_batch, cfg.micro_batch
+    # warm-up covers one full phase cycle (both transitions), so communicators and
+    # NVLink mappings exist before the timed epochs: steady state
+    warm = max(args.warmup, 2 * Pe + 1)
+    n_epochs = warm + args.steps
+    dynamic = args.c4_policy == "dynamic"
+
+    def core_of(e):
+        return agents[(e // Pe) % 2]
+
+    def aux_of(e):
+        others = [a for a in agents if a != core_of(e)]
+        return [others[(e * A + j) % len(others)] for j in range(A)]
+
+    def plan_of(e):
+        if not dynamic:
+            return static_plan(agents, N)
+        core = core_of(e)
+        loads = {a: (float(Cn) if a == core else A / (len(agents) - 1)) for a in agents}
+        return agent_centric_plan(loads, N)
+
+    def hosts(plan, a):
+        return plan.gangs[a] if a in plan.gangs else [r for r, v in plan.shared.items() if a in v]
+
+    # experience: every rank holds every agent's samples (agents may be trained anywhere)
+    steps_of = {a: 0 for a in agents}
+    for e in range(n_epochs):
+        steps_of[core_of(e)] += Cn
+        for a in aux_of(e):
+            steps_of[a] += 1
+    ctx = Context(dist.local)
+    ctx.reserve(256 << 20, mb * cfg.resp_len, cfg.vocab, cfg.feat)
+    store = ExperienceStore(ctx)
+    cols = [("prompt", "List"), ("response", "List"), ("advantage", "Float")]
+    for a in agents:
+        store.create_table(TableSchema(a, cols))
+        for st in range(steps_of[a]):
+            samples = wl.step_samples(cfg, a, st)
+            adv = group_advantages(ctx, [x.reward for x in samples], wl.group_offsets(samples))
+            for x, av in zip(samples, adv):
+                sid = SampleId(x.input_id, x.turns, x.traj)
+                store.insert(a, st, sid)
+                store.set_cell_payload(a, sid, st, "prompt", x.prompt_payload)
+                store.set_cell_payload(a, sid, st, "response", x.response_payload)
+                store.set_cell(a, sid, st, "advantage", float(av))
+    handles, comms, active = {}, {}, {}
+    version = {a: 0 for a in agents}
+    moved = {"agents": 0, "bytes": 0}
+
+    def new_agent(a):
+        h = C.c_void_p()
+        check(L.fm_agent_create(ctx.handle, a.encode(), cfg.vocab, cfg.feat, _lib.PRECISION_BF16_TC, C.byref(h)))
+        return h
+
+    comm_cache = {}  # gang membership -> NCCL communicator (created once, reused by any agent)
+    formed = set()   # the same on every rank: transitions are deterministic
+
+    def form_gang(a, gang):
+        key = tuple(gang)
+        if key not in formed:
+            uid = None
+            if me == gang[0]:
+                buf = (C.c_uint8 * 128)()
+                check(L.fm_comm_unique_id(buf))
+                uid = bytes(buf)
+            uid = dist.bcast_obj(uid, src=gang[0])
+            if me in gang:
+                h = C.c_void_p()
+                check(L.fm_comm_create(ctx.handle, (C.c_uint8 * 128).from_buffer_copy(uid), len(gang),
+                                       gang.index(me), C.byref(h)))
+                comm_cache[key] = h
+            formed.add(key)
+        blob = b""
+        if me in gang:
+            h = comm_cache[key]
+            comms[a] = h
+            n = C.c_uint64()
+            check(L.fm_gang_attach(handles[a], h, None, 0, C.byref(n)))
+            buf = (C.c_uint8 * n.value)()
+            check(L.fm_gang_attach(handles[a], h, buf, n.value, C.byref(n)))
+            blob = bytes(buf)
+        blobs = dist.all_gather_obj(blob)
+        if me in gang:
+            check(L.fm_gang_connect(handles[a], b"".join(blobs[r] for r in gang), len(blob)))
+
+    ttrace = os.environ.get("FM_C4_TRACE")
+
+    def tlog(msg, t0):
+        if ttrace:
+            print(f"[rank {me}] {msg}: {1e3 * (time.perf_counter() - t0):.1f} ms", file=sys.stderr, flush=True)
+
+    def transition(old, new):
+        """Move every agent whose host set changed (collective over all ranks)."""
+        for a in agents:
+            src_hosts, dst_hosts = hosts(old, a), hosts(new, a)
+            if src_hosts == dst_hosts:
+                continue
+            tt = time.perf_counter()
+            if len(src_hosts) > 1:  # dissolve the gang onto its lead rank
+                ctx.synchronize()
+                dist.barrier()
+                if me == src_hosts[0]:
+                    check(L.fm_gang_gather_state(handles[a]))
+                dist.barrier()
+                if me in src_hosts:
+                    check(L.fm_gang_detach(handles[a]))
+                    comms.pop(a)  # the communicator stays cached for the next gang on these GPUs
+                    if me != src_hosts[0]:
+                        L.fm_agent_destroy(handles.pop(a))
+                        active.pop(a, None)
+                tlog(f"{a} gang dissolve", tt)
+            src = src_hosts[0]
+            blob = None
+            tt = time.perf_counter()
+            if me == src:
+                if not active.get(a, True):  # parked on its shared GPU: back in a slot first
+                    check(L.fm_agent_activate(handles[a], ctx.handle))
+                    active[a] = True
+                keep = src in dst_hosts
+                n = C.c_uint64()
+                fn = L.fm_agent_share_export if keep else L.fm_agent_migrate_export
+                check(fn(handles[a], None, 0, C.byref(n)))
+                buf = (C.c_uint8 * n.value)()
+                check(fn(handles[a], buf, n.value, C.byref(n)))
+                blob = bytes(buf)
+            blob = dist.bcast_obj(blob, src=src)
+            if me in dst_hosts and me != src:
+                h = new_agent(a)
+                b = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+                check(L.fm_agent_migrate_import(h, ctx.handle, b, len(blob)))
+                handles[a] = h
+                active[a] = True
+                version[a] = L.fm_agent_version(h)
+            dist.barrier()  # every importer holds the state
+            if me == src and src not in dst_hosts:
+                L.fm_agent_destroy(handles.pop(a))  # returns the lent slot
+                active.pop(a, None)
+            tlog(f"{a} migrate {src_hosts}->{dst_hosts}", tt)
+            moved["agents"] += 1
+            moved["bytes"] += cfg.vocab * cfg.feat * 18 * len([r for r in dst_hosts if r != src])
+            if len(dst_hosts) > 1:
+                tt = time.perf_counter()
+                form_gang(a, dst_hosts)
+                tlog(f"{a} form gang", tt)
+        # park all but one agent per shared GPU
+        for a in new.shared.get(me, [])[1:]:
+            if active.get(a):
+                check(L.fm_agent_suspend(handles[a], _lib.TIER_DEVICE, -1))
+                active[a] = False
+
+    plan0 = plan_of(0)
+    for a in agents:
+        hs = hosts(plan0, a)
+        if me in hs:
+            handles[a] = new_agent(a)
+            w0 = seeded_weights(cfg.vocab, cfg.feat, agent_seed(cfg.seed, a)).reshape(-1)
+            check(L.fm_agent_set_weights(handles[a], w0.ctypes.data))
+            active[a] = True
+        if len(hs) > 1:
+            form_gang(a, hs)
+    for a in plan0.shared.get(me, [])[1:]:
+        check(L.fm_agent_suspend(handles[a], _lib.TIER_DEVICE, -1))
+        active[a] = False
+    ctx.synchronize()
+    FS = _lib.fm_sample
+
+    def update(a):
+        h = handles[a]
+        for _ in range(G // mb):
+            batch = store.poll_micro_batch(a, version[a], mb)
+            arr = (FS * mb)(*[r.cell for r in batch.samples])
+            t = C.c_int64()
+            check(L.fm_train_micro_batch(h, arr, mb, G, C.byref(t)))
+            store.complete(a, batch.samples)
+        check(L.fm_apply_update(h, G, cfg.lr, 0.9, 0.999, 1e-8, None, None))
+        version[a] += 1
+
+    def epoch(e, plan):
+        """One global step of the workflow.  It ends with a box-wide barrier: the
+        next epoch's experience is rolled out with this epoch's weights, so no
+        GPU runs ahead into the next phase (without it a static binding would
+        overlap the two cores' phases on different GPUs)."""
+        core = core_of(e)
+        shared_here = plan.shared.get(me, [])
+        if core in handles and core not in shared_here:
+            for _ in range(Cn):
+                update(core)
+        todo = ([core] * Cn if core in shared_here else []) + [a for a in aux_of(e) if a in shared_here]
+        for i, a in enumerate(todo):
+            if not active[a]:
+                check(L.fm_agent_activate(handles[a], ctx.handle))
+                active[a] = True
+            nxt = todo[i + 1] if i + 1 < len(todo) else None
+            if nxt and nxt != a and not active[nxt]:
+                check(L.fm_agent_activate(handles[nxt], ctx.handle))  # prefetch
+                active[nxt] = True
+            update(a)
+            if len(shared_here) > 1 and nxt != a:
+                check(L.fm_agent_suspend(handles[a], _lib.TIER_DEVICE, -1))
+                active[a] = False
+        ctx.synchronize()
+        dist.barrier()
+
+    plan = plan0
+    for e in range(warm):
+        if plan_of(e) != plan:
+            transition(plan, plan_of(e))
+            plan = plan_of(e)
+        epoch(e, plan)
+    ctx.synchronize()
+    dist.barrier()
+    moved.update(agents=0, bytes=0)
+    ms = C.c_double()
+    t0 = time.perf_counter()
+    check(L.fm_ctx_timer_start(ctx.handle))
+    for e in range(warm, n_epochs):
+        if plan_of(e) != plan:
+            transition(plan, plan_of(e))
+            plan = plan_of(e)
+        epoch(e, plan)
+    check(L.fm_ctx_timer_stop(ctx.handle, C.byref(ms)))
+    wall = time.perf_counter() - t0
+    dist.barrier()
+    # transitions synchronise the host; the device timer and the wall clock are both reported
+    max_ms = dist.max(max(ms.value, wall * 1e3))
+    tokens = (Cn + A) * G * cfg.resp_len * args.steps
+    for h in handles.values():
+        L.fm_agent_destroy(h)
+    for h in comm_cache.values():
+        L.fm_comm_destroy(h)
+    store.close()
+    ctx.close()
+    return dict(value=tokens / (max_ms / 1e3), max_ms=max_ms, core_updates_per_epoch=Cn, aux_updates_per_epoch=A,
+                phase_epochs=Pe, migrations=moved["agents"], migrated_bytes=moved["bytes"], warmup=warm)
+
+
 def _best_time(fn, reps=3):
     fn()
     best = 1e30
@@ -1052,8 +1317,10 @@ def main():
     ap.add_argument("--next-feat", type=int, default=4096)
     ap.add_argument("--next-requests", type=int, default=256)
     ap.add_argument("--next-tokens", type=int, default=64)
-    ap.add_argument("--c4-policy", default="agent-centric", choices=["agent-centric", "static"],
-                    help="C4 only: agent-to-GPU binding policy")
+    ap.add_argument("--c4-policy", default="agent-centric", choices=["agent-centric", "static", "dynamic"],
+                    help="C4 only: agent-to-GPU binding policy (dynamic: drifting core, plans follow it)")
+    ap.add_argument("--c4-phase-epochs", type=int, default=0,
+                    help="C4 drifting core: epochs per phase (0 = fixed core; dynamic defaults to 2)")
     args = ap.parse_args()
     dist = Dist()
     try:
@@ -1069,6 +1336,20 @@ def main():
             return
         from paper_2602_09578_b200 import workload as wl
         cfg = wl.CONFIGS[args.config]
+        if args.config == "C4" and (args.c4_policy == "dynamic" or args.c4_phase_epochs):
+            res = run_c4_dynamic(args, dist)
+            if dist.rank == 0:
+                emit({"metric": METRIC, "value": res["value"], "unit": "trained tokens/s", "n_gpus": dist.world,
+                      "steps": args.steps, "warmup": res["warmup"], "ms_per_step": res["max_ms"] / args.steps,
+                      "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                      "data": "synthetic (seeded per SURVEY.md §8d; random-init seeded policies)",
+                      "config": {"workload": "C4 drifting core", "policy": args.c4_policy,
+                                 "phase_epochs": res["phase_epochs"],
+                                 "core_updates_per_epoch": res["core_updates_per_epoch"],
+                                 "aux_updates_per_epoch": res["aux_updates_per_epoch"],
+                                 "vocab": cfg.vocab, "feat": cfg.feat, "resp_len": args.resp_len or cfg.resp_len},
+                      "migrations_timed": res["migrations"], "migrated_bytes_timed": res["migrated_bytes"]})
+            return
         if args.config == "C4":
             res = run_c4(args, dist)
             if dist.rank == 0:

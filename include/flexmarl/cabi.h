@@ -219,6 +219,10 @@ int fm_agent_state_checksum(fm_agent* a, uint64_t* out);
 int fm_agent_migrate_export(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64_t* len);
 int fm_agent_migrate_import(fm_agent* a, fm_ctx* ctx, const uint8_t* blob, uint64_t len);
 int fm_agent_migrate_release(fm_agent* a);
+/* Same blob, the agent stays active here: several processes may import it (a DP
+ * gang forming around the agent); no work may be queued for it until every
+ * importer returned. */
+int fm_agent_share_export(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64_t* len);
 
 /* ---- weight publish / rollout sync ----------------------------
  * publish_weights (training.hpp:459-467): one contiguous device buffer in
@@ -280,6 +284,10 @@ int fm_agent_allreduce_grad(fm_agent* a, fm_comm* c);
 int fm_gang_attach(fm_agent* a, fm_comm* c, uint8_t* blob_out, uint64_t cap, uint64_t* len);
 int fm_gang_connect(fm_agent* a, const uint8_t* blobs, uint64_t blob_len);
 int fm_gang_detach(fm_agent* a);
+/* Before a gang dissolves: pull the peers' W / m / v rows (the sharded Adam keeps
+ * only the own rows current) into this rank's slot over NVLink, so that after
+ * detach this rank holds the whole training state.  All gang ranks idle. */
+int fm_gang_gather_state(fm_agent* a);
 
 /* ---- experience store host control plane (experience_store.hpp:19-276) ---- */
 int fm_store_create(fm_store** out);

@@ -92,6 +92,8 @@ _PROTOS = {
     "fm_agent_migrate_export": (I, [P, P, U64, PU64]),
     "fm_agent_migrate_import": (I, [P, P, P, U64]),
     "fm_agent_migrate_release": (I, [P]),
+    "fm_agent_share_export": (I, [P, P, U64, PU64]),
+    "fm_gang_gather_state": (I, [P]),
     "fm_group_advantages": (I, [P, P, P, I, D, P]),
     "fm_comm_unique_id": (I, [P]),
     "fm_comm_create": (I, [P, P, I, I, C.POINTER(P)]),

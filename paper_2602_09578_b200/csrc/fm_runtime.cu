@@ -172,7 +172,9 @@ struct fm_ctx {
     // the latest K-GEMM1 launch on the compute stream (swap copies start there, see
     // fm_agent_suspend) and the op sequence numbers that say what it follows
     cudaEvent_t ev_gemm = nullptr;
-    std::map<std::string, void*> ipc_cache;  // peer training slots mapped for migrations
+    std::map<std::string, void*> ipc_cache;  // peer buffers mapped over NVLink (slots, gang receive buffers)
+    std::vector<std::pair<size_t, void*>> recv_pool;  // gang receive buffers + barrier tokens, recycled
+    std::unordered_map<void*, size_t> pool_sizes;
     uint64_t op_seq = 0, gemm_seq = 0;
     uint8_t* arena = nullptr;
     uint64_t arena_cap = 0, arena_used = 0;
@@ -205,6 +207,47 @@ int env_int(const char* name, int dflt) {
 int set_dev(const fm_ctx* c) {
     FM_CUDA(cudaSetDevice(c->device));
     return FM_OK;
+}
+
+// Maps a peer's IPC handle once per context: slots and gang receive buffers are
+// recycled, so re-formed gangs and repeated migrations reuse the mapping.
+int ipc_open_cached(fm_ctx* c, const cudaIpcMemHandle_t& h, void** out) {
+    const std::string key(reinterpret_cast<const char*>(&h), sizeof(h));
+    auto it = c->ipc_cache.find(key);
+    if (it != c->ipc_cache.end()) {
+        *out = it->second;
+        return FM_OK;
+    }
+    FM_CUDA(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_cache.emplace(key, *out);
+    return FM_OK;
+}
+
+// A recycled device buffer of >= bytes (gang receive buffers keep their IPC
+// identity across gangs, so peers' cached mappings stay valid).
+int pool_take(fm_ctx* c, size_t bytes, void** out) {
+    size_t best = SIZE_MAX;
+    int pick = -1;
+    for (size_t i = 0; i < c->recv_pool.size(); ++i)
+        if (c->recv_pool[i].first >= bytes && c->recv_pool[i].first < best) {
+            best = c->recv_pool[i].first;
+            pick = static_cast<int>(i);
+        }
+    if (pick >= 0) {
+        *out = c->recv_pool[static_cast<size_t>(pick)].second;
+        c->recv_pool.erase(c->recv_pool.begin() + pick);
+        return FM_OK;
+    }
+    if (cudaMalloc(out, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(FM_ERR_DEVICE_OOM, "gang buffer");
+    }
+    c->pool_sizes[*out] = bytes;
+    return FM_OK;
+}
+
+void pool_give(fm_ctx* c, void* p) {
+    if (p) c->recv_pool.emplace_back(c->pool_sizes[p], p);
 }
 
 // Returns a pinned staging slot of >= bytes whose previous use has completed.
@@ -540,6 +583,7 @@ int fm_ctx_destroy(fm_ctx* c) {
     cudaStreamDestroy(c->copy_out);
     if (c->ev_gemm) cudaEventDestroy(c->ev_gemm);
     for (auto& kv : c->ipc_cache) cudaIpcCloseMemHandle(kv.second);
+    for (auto& pb : c->recv_pool) cudaFree(pb.second);
     delete c;
     return FM_OK;
 }
@@ -639,8 +683,6 @@ struct GangState {
     float* peer_slot[8] = {};    // my slot inside peer o's receive buffer
     __nv_bfloat16* peer_w16[8] = {};
     uint8_t* peer_base[8] = {};  // peer o's training slot (same layout as ours)
-    void* opened[16] = {};       // IPC mappings to close
-    int nopened = 0;
     int* d_token = nullptr;      // 1-int all-reduce used as a device barrier
     bool connected = false;
 };
@@ -1507,7 +1549,20 @@ struct MigrateBlob {
 constexpr uint32_t kMigrateMagic = 0x474d4d46u;
 }  // namespace
 
+static int migrate_export_impl(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64_t* len, bool share);
+
 int fm_agent_migrate_export(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64_t* len) {
+    return migrate_export_impl(a, blob_out, cap, len, false);
+}
+
+// Same blob, but the agent stays active here: several processes may import it
+// (a DP gang forming around the agent); the caller enqueues no work for it
+// until every importer returned.
+int fm_agent_share_export(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64_t* len) {
+    return migrate_export_impl(a, blob_out, cap, len, true);
+}
+
+static int migrate_export_impl(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64_t* len, bool share) {
     FM_GUARD_BEGIN
     *len = sizeof(MigrateBlob);
     if (!blob_out) return FM_OK;
@@ -1540,8 +1595,10 @@ int fm_agent_migrate_export(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64
     FM_CUDA(cudaIpcGetMemHandle(&b.mem, a->slot->base));
     FM_CUDA(cudaIpcGetEventHandle(&b.ev, a->ev_ipc));
     std::memcpy(blob_out, &b, sizeof(b));
-    a->active = false;  // lent: the slot stays reserved until fm_agent_migrate_release
-    a->lent = true;
+    if (!share) {
+        a->active = false;  // lent: the slot stays reserved until fm_agent_migrate_release
+        a->lent = true;
+    }
     return FM_OK;
     FM_GUARD_END
 }
@@ -1570,15 +1627,8 @@ int fm_agent_migrate_import(fm_agent* a, fm_ctx* c, const uint8_t* blob, uint64_
     if (!a->active || a->ctx != c) return fail(FM_ERR_INACTIVE_GROUP, a->name + " must be active on the target GPU");
     if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang");
     if (int st = set_dev(c)) return st;
-    const std::string key(reinterpret_cast<const char*>(&b.mem), sizeof(b.mem));
     void* src = nullptr;
-    auto it = c->ipc_cache.find(key);
-    if (it != c->ipc_cache.end()) {
-        src = it->second;
-    } else {
-        FM_CUDA(cudaIpcOpenMemHandle(&src, b.mem, cudaIpcMemLazyEnablePeerAccess));
-        c->ipc_cache.emplace(key, src);
-    }
+    if (int st = ipc_open_cached(c, b.mem, &src)) return st;
     cudaEvent_t ev = nullptr;
     FM_CUDA(cudaIpcOpenEventHandle(&ev, b.ev));
     // after everything already queued on the agent's slot, and after the source's queued work
@@ -1764,11 +1814,20 @@ int fm_gang_attach(fm_agent* a, fm_comm* cm, uint8_t* blob_out, uint64_t cap, ui
     for (int o = 0; o < gs->g; ++o) max_rows = std::max(max_rows, gs->lo[o + 1] - gs->lo[o]);
     const int64_t own = gs->lo[gs->rank + 1] - gs->lo[gs->rank];
     const size_t rbytes = static_cast<size_t>(gs->g - 1) * std::max<int64_t>(own, 1) * a->D * 4;
-    if (cudaMalloc(&gs->recv, rbytes) != cudaSuccess) {
+    fm_ctx* c = a->ctx;
+    void* rb = nullptr;
+    void* tk = nullptr;
+    if (int st = pool_take(c, rbytes, &rb)) {
         delete gs;
-        return fail(FM_ERR_DEVICE_OOM, "gang receive buffer");
+        return st;
     }
-    FM_CUDA(cudaMalloc(&gs->d_token, sizeof(int)));
+    if (int st = pool_take(c, 256, &tk)) {
+        pool_give(c, rb);
+        delete gs;
+        return st;
+    }
+    gs->recv = static_cast<float*>(rb);
+    gs->d_token = static_cast<int*>(tk);
     FM_CUDA(cudaMemset(gs->d_token, 0, sizeof(int)));
     GangBlob b{};
     b.rank = gs->rank;
@@ -1798,10 +1857,8 @@ int fm_gang_connect(fm_agent* a, const uint8_t* blobs, uint64_t blob_len) {
         if (o == gs->rank) continue;
         void* rbase = nullptr;
         void* sbase = nullptr;
-        FM_CUDA(cudaIpcOpenMemHandle(&rbase, b.recv, cudaIpcMemLazyEnablePeerAccess));
-        FM_CUDA(cudaIpcOpenMemHandle(&sbase, b.slot, cudaIpcMemLazyEnablePeerAccess));
-        gs->opened[gs->nopened++] = rbase;
-        gs->opened[gs->nopened++] = sbase;
+        if (int st = ipc_open_cached(a->ctx, b.recv, &rbase)) return st;
+        if (int st = ipc_open_cached(a->ctx, b.slot, &sbase)) return st;
         // my slot in o's receive buffer: senders in rank order, skipping o itself
         const int idx = gs->rank < o ? gs->rank : gs->rank - 1;
         const int64_t o_rows = gs->lo[o + 1] - gs->lo[o];
@@ -1839,6 +1896,35 @@ static int copy_state(fm_agent* a, size_t off, size_t elem, void* dst, cudaStrea
 
 extern "C" {
 
+// Pulls every peer's W / m / v rows into this rank's slot over NVLink (the gang's
+// sharded Adam keeps only the own rows current there), so that after
+// fm_gang_detach this rank holds the agent's whole training state.  The bf16
+// shadow is replicated already.  Caller: all gang ranks idle (host barrier).
+int fm_gang_gather_state(fm_agent* a) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
+    GangState* gs = a->gang;
+    if (!gs || !gs->connected) return fail(FM_ERR_CONFIG_ERROR, a->name + " is not in a connected DP gang");
+    fm_ctx* c = a->ctx;
+    if (int st = set_dev(c)) return st;
+    const size_t offs[3] = {0, slot_off_m(a), slot_off_v(a)};
+    const size_t elems[3] = {8, 4, 4};
+    for (int k = 0; k < 3; ++k) {
+        const size_t row = a->D * elems[k];
+        uint8_t* mine = static_cast<uint8_t*>(a->slot->base) + offs[k];
+        for (int o = 0; o < gs->g; ++o) {
+            const int64_t r0 = gs->lo[o], r1 = gs->lo[o + 1];
+            if (o == gs->rank || r1 <= r0) continue;
+            FM_CUDA(cudaMemcpyAsync(mine + static_cast<size_t>(r0) * row,
+                                    gs->peer_base[o] + offs[k] + static_cast<size_t>(r0) * row,
+                                    static_cast<size_t>(r1 - r0) * row, cudaMemcpyDefault, c->stream));
+        }
+    }
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    return FM_OK;
+    FM_GUARD_END
+}
+
 int fm_gang_detach(fm_agent* a) {
     GangState* gs = a->gang;
     if (!gs) return FM_OK;
@@ -1846,9 +1932,14 @@ int fm_gang_detach(fm_agent* a) {
         cudaSetDevice(a->ctx->device);
         cudaStreamSynchronize(a->ctx->stream);
     }
-    for (int i = 0; i < gs->nopened; ++i) cudaIpcCloseMemHandle(gs->opened[i]);
-    cudaFree(gs->recv);
-    cudaFree(gs->d_token);
+    // mappings stay in the context's cache; the buffers go back to its pool
+    if (a->ctx) {
+        pool_give(a->ctx, gs->recv);
+        pool_give(a->ctx, gs->d_token);
+    } else {
+        cudaFree(gs->recv);
+        cudaFree(gs->d_token);
+    }
     delete gs;
     a->gang = nullptr;
     a->shard_rank = 0;

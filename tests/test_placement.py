@@ -35,3 +35,23 @@ def test_static_plan():
     assert all(len(g) == 1 for g in p.gangs.values())
     p = static_plan(AG[:4], 2)
     assert p.shared == {0: ["agent0", "agent2"], 1: ["agent1", "agent3"]}
+
+
+def test_drifting_core_moves_only_the_two_cores():
+    """C4 with a drifting core (bench.py --c4-policy dynamic): between phases only
+    the old and the new core change GPUs; every auxiliary agent keeps its GPU."""
+    agents = [f"agent{i}" for i in range(8)]
+    for n in (2, 4, 8):
+        A = max(1, int(round(0.24 * n)))
+        Cn = int(round(A * 0.76 / 0.24))
+
+        def plan(core):
+            return agent_centric_plan({a: (float(Cn) if a == core else A / 7) for a in agents}, n)
+
+        def hosts(p, a):
+            return p.gangs[a] if a in p.gangs else [r for r, v in p.shared.items() if a in v]
+
+        p0, p1 = plan("agent0"), plan("agent1")
+        moved = {a for a in agents if hosts(p0, a) != hosts(p1, a)}
+        assert moved <= {"agent0", "agent1"}
+        assert hosts(p1, "agent1") == hosts(p0, "agent0")  # the new core takes over the core gang
