@@ -7,6 +7,8 @@
 #include <cstddef>
 #include <cstdint>
 
+#include "fm_kernels.h"
+
 namespace fm {
 
 constexpr int kGemmBM = 128;
@@ -46,6 +48,11 @@ struct GemmArgs {
     int xrank = 0;
     int xlo[9] = {};
     float* xpeer[8] = {};
+    // Logits, fused K-lse (lse_count != nullptr): lse_count[b] counts the vocab tiles
+    // finished for 128-row block b; the CTA that finishes the last one runs the row
+    // normaliser (fm_lse.cuh) for the block and resets the counter.
+    int* lse_count = nullptr;
+    LseArgs lse{};
 };
 
 // 1 when the loss-fold path (no separate K-loss kernel) is active (FM_LOSS_FOLD != 0).

@@ -37,6 +37,25 @@ struct RowBuffers {
     float* mrow;       // [Mpad] softmax offset bound (1/n) sum_j colmax[f_j]   (loss-fold path)
 };
 
+// K-lse arguments (fm_lse.cuh: the per-row routine shared by the standalone
+// kernel and GEMM1's fused last-tile epilogue).
+struct LseArgs {
+    const float* zact;    // [Mpad] fp32 logit of the taken token
+    const float2* stats;  // [Mpad][stats_ld] (max, sum exp) per 256-column tile
+    int stats_ld;
+    int64_t M, Mpad, V;
+    const SampleDesc* sd;
+    int64_t G;
+    RowBuffers rows;
+    const float* old_logp;  // PPO clip (nullable)
+    float clip_eps;
+    double* loss_acc;  // += objective (nullable)
+    int fold;
+    __nv_bfloat16* pexp_t;  // fold: p~^T [V][ldt]
+    __nv_bfloat16* phict;   // fold: Phic^T [D][ldt]
+    int64_t ldt;
+};
+
 // K-gather: decode the selected records' token payloads straight out of the
 // arena into packed rows; optionally scatter integer-count features into the
 // dense bf16 operands Phic [Mpad][D] and Phic^T [D][Mpad] (pre-zeroed, or

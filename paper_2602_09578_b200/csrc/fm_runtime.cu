@@ -115,6 +115,7 @@ struct Workspace {
     float* zact = nullptr;          // logit of the taken token [Mpad]
     float2* stats = nullptr;
     float* mrow = nullptr;  // loss fold: per-row softmax offset bound [Mpad]
+    int* lse_cnt = nullptr;  // fused K-lse: GEMM1 tiles finished per 128-row block (self-resetting)
     // parity mode scratch
     int64_t prow_cap = 0;
     uint64_t pvocab_cap = 0, pparam_cap = 0;
@@ -286,6 +287,7 @@ void ws_free(Workspace& w) {
     cudaFree(w.zact);
     cudaFree(w.stats);
     cudaFree(w.mrow);
+    cudaFree(w.lse_cnt);
     cudaFree(w.zscratch);
     cudaFree(w.dWmb);
     cudaFree(w.logp64);
@@ -338,6 +340,8 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
     e = e ? e : dalloc(&w.zact, R);
     e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n);
     e = e ? e : dalloc(&w.mrow, R);
+    e = e ? e : dalloc(&w.lse_cnt, static_cast<size_t>(R / 128 + 2));
+    e = e ? e : cudaMemset(w.lse_cnt, 0, sizeof(int) * static_cast<size_t>(R / 128 + 2));
     if (e != cudaSuccess) {
         ws_free(w);
         return fail(FM_ERR_DEVICE_OOM, std::string("workspace allocation: ") + cudaGetErrorString(e));
@@ -1085,18 +1089,30 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g1.row_scale = w.rscale;
             g1.stats = w.stats;
             g1.stats_ld = tiles_n;
+            // K-lse fused into GEMM1 (loss fold, CTA-pair kernel; opt-in FM_LSE_FUSED=1): the
+            // CTA finishing a 128-row block's last vocab tile normalises those rows in its
+            // epilogue.  Measured slower (GEMM1 2.57 -> 2.89-2.97 ms at C2 vs a 14 us K-lse
+            // launch): the per-tile counter release stalls the epilogue warps.
+            const char* lse_env = std::getenv("FM_LSE_FUSED");
+            const bool lse_fused = fold && gemm_pair_mode() && lse_env && lse_env[0] == '1';
+            const LseArgs lse_args{w.zact, w.stats, tiles_n, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
+                                   a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1,
+                                   fold ? 1 : 0, fold ? w.gt : nullptr, w.phict, Mpad};
+            if (lse_fused) {
+                g1.lse = lse_args;
+                g1.lse_count = w.lse_cnt;
+            }
             FM_CUDA(cudaEventRecord(c->ev_gemm, s));  // swap copies may start here (fm_agent_suspend)
             c->gemm_seq = ++c->op_seq;
             {
                 KScope k(c, K_GEMM1, s);
                 FM_CUDA(gemm_tn_launch(GemmKind::Logits, tA, tB, g1, c->num_sms, s));
             }
-            // K-lse
-            {
+            // K-lse (standalone unless fused into GEMM1's epilogue)
+            if (!lse_fused) {
                 KScope k(c, K_LSE, s);
                 FM_CUDA(launch_lse(w.zact, w.stats, tiles_n, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
-                                   a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1,
-                                   fold ? w.gt : nullptr, w.phict, Mpad, s));
+                                   lse_args.old_logp, a->clip_eps, scal + 1, lse_args.pexp_t, w.phict, Mpad, s));
             }
             // K-softmax-grad: G^T tiles (zero for padding rows) — folded into GEMM2's operands
             if (!fold) {
@@ -1152,7 +1168,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 a->dw_valid = true;
                 if (int st = gang_barrier(a)) return st;  // every rank's partials have landed
             }
-            count_launch(fold ? 4 : 5);
+            count_launch(fold ? (lse_fused ? 3 : 4) : 5);
         } else {
             w.phi_valid = false;  // the row buffers no longer describe Phic's contents
             FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, M, G, a->D, rows, nullptr, nullptr, 0, nullptr, s));

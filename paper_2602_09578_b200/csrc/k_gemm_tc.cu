@@ -2,8 +2,10 @@
 // two dense products:
 //
 //   K-GEMM1  Z[t][v]  = (1/n_t) * sum_d Phic[t][d] * W16[v][d]      (policy.hpp:57-61)
-//            epilogue: fp32 Z store + per-(row, 256-col tile) softmax partials
-//            (max, sum exp) consumed by K-lse                        (policy.hpp:62-66)
+//            epilogue: p~ = exp(z - m) store + per-(row, 256-col tile) softmax
+//            partials (max, sum exp) and the taken token's logit; with the loss
+//            fold the CTA finishing a row block's last vocab tile also runs K-lse
+//            for it (fused, fm_lse.cuh)                             (policy.hpp:62-75)
 //   K-GEMM2  dW[v][d] (+)= sum_t G^T[v][t] * Phic^T[d][t]           (policy.hpp:83-90,
 //            training.hpp:394-395, 444-446); epilogue RMW of the fp32 gradient
 //            accumulator + sum(acc^2) of this micro-batch (training.hpp:417)
@@ -25,6 +27,7 @@
 #include <type_traits>
 
 #include "fm_gemm.h"
+#include "fm_lse.cuh"
 #include "fm_ptx.cuh"
 
 namespace fm {
@@ -52,6 +55,33 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int tiles_m, int tiles_n,
 }
 
 __device__ __forceinline__ float fast_exp(float x) { return exp2f(x * 1.4426950408889634f); }
+
+// Fused K-lse (GEMM1, loss fold): after a tile's epilogue, count the finished
+// vocab tile for this CTA's 128-row block; the CTA that finishes the block's
+// last tile runs the row normaliser for its 128 rows (each epilogue warp its 32,
+// four rows per step).  Release: the named barrier orders the four warps'
+// p~^T / logit / partial stores before one thread's gpu-scope acq_rel fence
+// and counter increment (cumulative, as CUTLASS's generic barrier); acquire:
+// the finishing CTA fences after observing the count.  The counter resets
+// itself for the next launch.
+__device__ __forceinline__ void lse_tile_done(const GemmArgs& a, int blk, int tiles_n, uint32_t quad,
+                                              volatile int* flag, double& loss) {
+    named_bar_sync(1, 128);
+    if (quad == 0 && (threadIdx.x & 31) == 0) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        const int prev = atomicAdd(&a.lse_count[blk], 1);
+        const int last = prev == tiles_n - 1;
+        if (last) a.lse_count[blk] = 0;
+        *flag = last;
+    }
+    named_bar_sync(1, 128);
+    if (*flag) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        const int64_t r0 = static_cast<int64_t>(blk) * 128 + quad * 32;
+#pragma unroll 1
+        for (int q = 0; q < 8; ++q) loss += lse_row_quad(a.lse, r0 + 4 * q);
+    }
+}
 
 // ---- epilogues ------------------------------------------------------------
 
@@ -522,6 +552,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         double sumsq_total = 0.0;
+        double lse_loss = 0.0;
+        __shared__ int lse_flag;
         for (int t = cid; t < num_tiles; t += nclusters) {
             const TileCoord tc = tile_coord(t, tiles_m, tiles_n, args.group_m);
             mbar_wait(&tfull[acc], acc_phase);
@@ -555,12 +587,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             }
             epi.end(args, row, tc.nb);
             if constexpr (std::is_same_v<Epi, GradEpi>) sumsq_total += epi.sumsq;
+            if constexpr (std::is_same_v<Epi, LogitsEpi>) {
+                if (args.lse_count)
+                    lse_tile_done(args, tc.mb * 2 + static_cast<int>(rank), tiles_n, quad, &lse_flag, lse_loss);
+            }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
         if constexpr (std::is_same_v<Epi, GradEpi>) {
             for (int o = 16; o > 0; o >>= 1) sumsq_total += __shfl_xor_sync(0xffffffffu, sumsq_total, o);
             if (lane == 0 && args.sumsq) atomicAdd(args.sumsq, sumsq_total);
+        }
+        if constexpr (std::is_same_v<Epi, LogitsEpi>) {
+            for (int o = 16; o > 0; o >>= 1) lse_loss += __shfl_xor_sync(0xffffffffu, lse_loss, o);
+            if (lane == 0 && args.lse_count && args.lse.loss_acc && lse_loss != 0.0)
+                atomicAdd(args.lse.loss_acc, lse_loss);
         }
     }
     tc_fence_before();

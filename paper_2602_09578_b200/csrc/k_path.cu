@@ -17,6 +17,7 @@
 #include <cstdint>
 
 #include "fm_kernels.h"
+#include "fm_lse.cuh"
 #include "fm_ptx.cuh"
 
 namespace fm {
@@ -229,125 +230,20 @@ __global__ void __launch_bounds__(256) colmax_kernel(const __nv_bfloat16* __rest
 // ---------------------------------------------------------------------------
 // K-lse
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) lse_kernel(const float* __restrict__ zact,
-                                                  const float2* __restrict__ stats, int stats_ld,
-                                                  int64_t M, int64_t Mpad, int64_t V,
-                                                  const SampleDesc* __restrict__ sd, int64_t G,
-                                                  RowBuffers rows, const float* old_logp,
-                                                  float clip_eps, double* loss_acc, int fold,
-                                                  __nv_bfloat16* pexp_t, __nv_bfloat16* phict, int64_t ldt) {
-    // Four rows per warp (8 lanes per row), persistent over row quads.  The kernel is
-    // latency/issue bound (1 KB of partials per row at C2): each lane issues all 16
-    // partials it needs at C2 before any math, the cross-lane combine takes 3 shuffle
-    // steps instead of 5, and the per-row epilogue (log, division, the loss-fold
-    // stores) is issued once per 4 rows instead of once per row.
-    constexpr int kLpr = 8;
+__global__ void __launch_bounds__(256) lse_kernel(LseArgs L) {
+    // Four rows per warp (8 lanes per row, fm_lse.cuh), persistent over row quads.
+    // The kernel is latency/issue bound (1 KB of partials per row at C2).  With the
+    // loss fold GEMM1 runs this same routine in its last-tile epilogue instead
+    // (FM_LSE_FUSED, default on), and this kernel is not launched.
     __shared__ double red[8];
-    const int lane = threadIdx.x & 31;
-    const int sub = lane / kLpr, sl = lane % kLpr;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
     double loss = 0.0;
-    for (int64_t r0 = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 4; r0 < Mpad;
-         r0 += nwarps * 4) {
-        const int64_t r = r0 + sub;
-        const bool live = r < M;  // rows in [M, Mpad) are padding; r >= Mpad does not exist
-        int a = -1;
-        float za = 0.f, c0 = 0.f, olp = 0.f;
-        double adv = 0.0;
-        int4 f4 = make_int4(-1, -1, -1, -1);
-        uint32_t c4 = 0;
-        float m = -INFINITY, s = 0.f;
-        if (live) {
-            a = rows.action[r];
-            za = zact[r];
-            c0 = rows.coef[r];
-            adv = sd[rows.sample[r]].adv;
-            if (old_logp) olp = old_logp[r];
-            if (fold) {
-                f4 = rows.feat4[r];
-                c4 = rows.cnt4[r];
-            }
-            const float2* st = stats + static_cast<size_t>(r) * stats_ld;
-            for (int base = 0; base < stats_ld; base += kLpr * 16) {
-                float2 p[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const int j = base + sl + kLpr * k;
-                    p[k] = j < stats_ld ? st[j] : make_float2(-INFINITY, 0.f);
-                }
-                float lm = p[0].x;
-#pragma unroll
-                for (int k = 1; k < 16; ++k) lm = fmaxf(lm, p[k].x);
-                const float nm = fmaxf(m, lm);
-                if (nm != -INFINITY) {
-                    float ls = 0.f;
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) ls += p[k].x == -INFINITY ? 0.f : p[k].y * __expf(p[k].x - nm);
-                    s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + ls;
-                    m = nm;
-                }
-            }
-        }
-#pragma unroll
-        for (int o = kLpr / 2; o > 0; o >>= 1) {
-            const float om = __shfl_xor_sync(0xffffffffu, m, o);
-            const float os = __shfl_xor_sync(0xffffffffu, s, o);
-            const float nm = fmaxf(m, om);
-            s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) + (om == -INFINITY ? 0.f : os * __expf(om - nm));
-            m = nm;
-        }
-        if (r >= Mpad) continue;
-        if (!live) {
-            if (sl == 0) {
-                rows.lse[r] = 0.f;
-                rows.logp[r] = 0.f;
-                rows.coef_eff[r] = 0.f;
-            }
-            continue;
-        }
-        // the row's 8 lanes hold (m, s); the epilogue is computed redundantly by them
-        // and its scattered stores are spread over lanes 0-4 of the row
-        const float lse = m + __logf(s);
-        const bool valid = a >= 0 && a < V;
-        const float lp = valid ? za - lse : 0.f;  // policy.hpp:72-75, fp32 logit
-        float ce = c0;
-        if (old_logp && clip_eps > 0.f) {
-            // PPO clipped-ratio surrogate min(rho*A, clip(rho,1-e,1+e)*A): the
-            // gradient flows (scaled by rho) only through the unclipped branch.
-            const float rho = __expf(lp - olp);
-            const bool active = adv >= 0.0 ? rho <= 1.f + clip_eps : rho >= 1.f - clip_eps;
-            ce = active ? ce * rho : 0.f;
-        }
-        if (sl == 0) {
-            rows.lse[r] = lse;
-            rows.logp[r] = lp;
-            rows.coef_eff[r] = ce;
-            loss += valid ? -(adv / static_cast<double>(G)) * static_cast<double>(lp) : 0.0;
-            if (fold && (!(s >= 1e-30f) || !isfinite(s)))
-                loss = __longlong_as_double(0x7ff8000000000000ll);  // range guard: NaN loss, never silent
-        }
-        if (fold) {
-            // Every tile used the row's offset bound m (K-gather), so
-            //   G[t][v] = c (delta(v,a) - p~[t][v] / s),  s = sum_v p~ = exp(lse - m).
-            // The per-row factor sig = -c / s goes into GEMM2's B operand
-            // (Phic^T's <= 4 count entries of column t), the delta term into A:
-            //   A[a][t] = p~_a - s   =>   sig * A = -c (p - delta) = G.
-            // an action outside [0, V) never matches a vocab row (policy.hpp:84-85): the
-            // row still gets -c p, just no delta term
-            const float sig = ce != 0.f ? __fdividef(-ce, s) : 0.f;
-            if (sl == 4 && sig != 0.f && valid)
-                pexp_t[static_cast<size_t>(a) * ldt + r] = __float2bfloat16_rn(__expf(za - m) - s);
-            if (sl < 4) {
-                const int f = sl == 0 ? f4.x : sl == 1 ? f4.y : sl == 2 ? f4.z : f4.w;
-                if (f >= 0)
-                    phict[static_cast<size_t>(f) * ldt + r] =
-                        __float2bfloat16_rn(sig * static_cast<float>((c4 >> (8 * sl)) & 0xFFu));
-            }
-        }
-    }
-    if (loss_acc) {
+    for (int64_t r0 = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 4; r0 < L.Mpad;
+         r0 += nwarps * 4)
+        loss += lse_row_quad(L, r0);
+    if (L.loss_acc) {
         const double tot = block_sum(loss, red);
-        if (threadIdx.x == 0 && tot != 0.0) atomicAdd(loss_acc, tot);
+        if (threadIdx.x == 0 && tot != 0.0) atomicAdd(L.loss_acc, tot);
     }
 }
 
@@ -754,8 +650,9 @@ cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int
     if (Mpad == 0) return cudaSuccess;
     int64_t blocks = (Mpad * 8 + 255) / 256;  // 4 rows per warp
     if (blocks > 148 * 4) blocks = 148 * 4;   // persistent warps: 4 resident 256-thread blocks per SM
-    lse_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(zact, stats, stats_ld, M, Mpad, V, sd, global_batch, rows, old_logp, clip_eps,
-                                      loss_acc, pexp_t != nullptr, pexp_t, phict, ldt);
+    const LseArgs L{zact, stats, stats_ld, M, Mpad, V, sd, global_batch, rows, old_logp, clip_eps,
+                    loss_acc, pexp_t != nullptr, pexp_t, phict, ldt};
+    lse_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(L);
     return cudaGetLastError();
 }
 

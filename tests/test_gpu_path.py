@@ -403,3 +403,21 @@ def test_gemm2_k_chunks_match_single_launch(ctx, monkeypatch):
     assert rel_fro(chunked["grads"][0], _oracle_grad_step0(f)) <= 2e-2
     assert np.all(np.isnan(chunked["mb_grad_norm"]))
     np.testing.assert_allclose(chunked["upd_grad_norm"], one["upd_grad_norm"], rtol=1e-5)
+
+
+def test_fused_lse_matches_standalone_kernel(ctx, monkeypatch):
+    """K-lse fused into GEMM1's last-tile epilogue (opt-in FM_LSE_FUSED=1) runs
+    the same per-row routine (fm_lse.cuh) on the same bits as the standalone
+    K-lse launch (default): gradients, grad norms and the updated W/m/v are
+    bit-identical."""
+    f = _ld("mid_agent0.npz")
+    alone = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
+    monkeypatch.setenv("FM_LSE_FUSED", "1")
+    fused = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
+    for g1, g2 in zip(fused["grads"], alone["grads"]):
+        np.testing.assert_array_equal(g1, g2)
+    for k in ("W", "m", "v", "mb_grad_norm"):
+        np.testing.assert_array_equal(fused[k], alone[k])
+    # K-adam's norm reduction adds in atomic order
+    np.testing.assert_allclose(fused["upd_grad_norm"], alone["upd_grad_norm"], rtol=1e-12)
+    assert rel_fro(fused["grads"][0], _oracle_grad_step0(f)) <= 2e-2
