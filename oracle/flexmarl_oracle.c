@@ -324,3 +324,123 @@ int fmo_run_agent(uint64_t V, uint64_t D, int64_t G, int64_t mb, int n_updates,
     free(p);
     return 0;
 }
+
+/* ---- few-token gradient at full V x D (column-sparse restatement) -------
+ * The same arithmetic as fmo_run_agent's first update (policy.hpp:42-91,
+ * training.hpp:386-395, 444-446) restricted to the feature columns the
+ * samples' contexts touch: every other phi_d is 0, and adding W*0 / coef*0
+ * never changes an IEEE sum that starts at +0, so the touched columns are
+ * bit-identical to the dense oracle and every other column is exactly 0.
+ * W's columns are drawn directly from the seeded stream (policy.hpp:29-35):
+ * element i = v*D + d consumes draws 2i, 2i+1 of the splitmix sequence, whose
+ * state before draw k is seed + k * golden-gamma (rng.hpp:14-19).  Memory is
+ * V x (#columns) doubles instead of the dense oracle's 7 x V x D.
+ * Returns the number of columns (written ascending to cols_out, at most
+ * max_cols) or -1; grad_out is [V][ncols] row-major = -(1/G) sum_s A_s term_s,
+ * mb_norm_out = ||sum_s A_s term_s||_F / G (training.hpp:417). */
+static int cmp_i64(const void* a, const void* b) {
+    const int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+    return x < y ? -1 : x > y;
+}
+
+int64_t fmo_sparse_grad(uint64_t V, uint64_t D, uint64_t seed, int n_samples, const uint8_t* payloads,
+                        const int64_t* prompt_off, const int64_t* resp_off, const double* adv, int64_t G,
+                        int64_t max_cols, int64_t* cols_out, double* grad_out, double* mb_norm_out) {
+    /* columns touched by any context window */
+    int64_t ncand = 0, cap = 64;
+    int64_t* cand = (int64_t*)malloc(cap * sizeof(int64_t));
+    for (int s = 0; s < n_samples; ++s) {
+        const uint64_t np = fmo_decode_tokens(payloads + prompt_off[s], NULL);
+        const uint64_t nr = fmo_decode_tokens(payloads + resp_off[s], NULL);
+        int* ctx = (int*)malloc((np + nr + 1) * sizeof(int));
+        fmo_decode_tokens(payloads + prompt_off[s], ctx);
+        fmo_decode_tokens(payloads + resp_off[s], ctx + np);
+        for (uint64_t t = 0; t < nr; ++t) {
+            const int len = (int)(np + t), n = len < 4 ? len : 4;
+            for (int i = len - n; i < len; ++i) {
+                if (ncand == cap) cand = (int64_t*)realloc(cand, (cap *= 2) * sizeof(int64_t));
+                cand[ncand++] = (int64_t)((uint64_t)(int64_t)ctx[i] % D);
+            }
+        }
+        free(ctx);
+    }
+    qsort(cand, (size_t)ncand, sizeof(int64_t), cmp_i64);
+    int64_t nc = 0;
+    for (int64_t i = 0; i < ncand; ++i)
+        if (nc == 0 || cand[i] != cand[nc - 1]) cand[nc++] = cand[i];
+    if (nc > max_cols) {
+        free(cand);
+        return -1;
+    }
+    memcpy(cols_out, cand, (size_t)nc * sizeof(int64_t));
+    free(cand);
+    /* W[:, cols] straight from the seeded stream */
+    double* Wc = (double*)malloc(V * (size_t)nc * sizeof(double));
+    for (uint64_t v = 0; v < V; ++v)
+        for (int64_t j = 0; j < nc; ++j) {
+            uint64_t st = seed + 2ULL * (v * D + (uint64_t)cols_out[j]) * 0x9e3779b97f4a7c15ULL;
+            Wc[v * nc + j] = 0.5 * rng_normal(&st);
+        }
+    double* phi = (double*)calloc((size_t)nc, sizeof(double));
+    double* z = (double*)malloc(V * sizeof(double));
+    double* term = (double*)malloc(V * (size_t)nc * sizeof(double));
+    memset(grad_out, 0, V * (size_t)nc * sizeof(double));
+    for (int s = 0; s < n_samples; ++s) {
+        const uint64_t np = fmo_decode_tokens(payloads + prompt_off[s], NULL);
+        const uint64_t nr = fmo_decode_tokens(payloads + resp_off[s], NULL);
+        int* ctx = (int*)malloc((np + nr + 1) * sizeof(int));
+        fmo_decode_tokens(payloads + prompt_off[s], ctx);
+        fmo_decode_tokens(payloads + resp_off[s], ctx + np);
+        memset(term, 0, V * (size_t)nc * sizeof(double));
+        for (uint64_t t = 0; t < nr; ++t) {
+            const int len = (int)(np + t), n = len < 4 ? len : 4, action = ctx[np + t];
+            for (int64_t j = 0; j < nc; ++j) phi[j] = 0.0;
+            if (n > 0) { /* policy.hpp:46-49: phi[tok mod D] += 1/n in context order */
+                const double w = 1.0 / (double)n;
+                for (int i = len - n; i < len; ++i) {
+                    const int64_t f = (int64_t)((uint64_t)(int64_t)ctx[i] % D);
+                    int64_t lo = 0, hi = nc - 1;
+                    while (lo < hi) {
+                        const int64_t mid = (lo + hi) / 2;
+                        if (cols_out[mid] < f) lo = mid + 1; else hi = mid;
+                    }
+                    phi[lo] += w;
+                }
+            }
+            /* policy.hpp:57-69: d-ascending sum over the non-zero features */
+            for (uint64_t v = 0; v < V; ++v) {
+                double acc = 0.0;
+                for (int64_t j = 0; j < nc; ++j)
+                    if (phi[j] != 0.0) acc += Wc[v * nc + j] * phi[j];
+                z[v] = acc;
+            }
+            double zmax = z[0];
+            for (uint64_t v = 1; v < V; ++v)
+                if (z[v] > zmax) zmax = z[v];
+            double denom = 0.0;
+            for (uint64_t v = 0; v < V; ++v) {
+                z[v] = exp(z[v] - zmax);
+                denom += z[v];
+            }
+            for (uint64_t v = 0; v < V; ++v) z[v] /= denom;
+            /* policy.hpp:83-90 */
+            for (uint64_t v = 0; v < V; ++v) {
+                const double coef = (((int)v == action ? 1.0 : 0.0) - z[v]);
+                if (coef == 0.0) continue;
+                for (int64_t j = 0; j < nc; ++j)
+                    if (phi[j] != 0.0) term[v * nc + j] += coef * phi[j];
+            }
+        }
+        for (uint64_t i = 0; i < V * (uint64_t)nc; ++i) grad_out[i] += term[i] * adv[s]; /* scale, canonical sum */
+        free(ctx);
+    }
+    double ss = 0.0;
+    for (uint64_t i = 0; i < V * (uint64_t)nc; ++i) ss += grad_out[i] * grad_out[i];
+    *mb_norm_out = sqrt(ss) / (double)G;
+    for (uint64_t i = 0; i < V * (uint64_t)nc; ++i) grad_out[i] *= -1.0 / (double)G;
+    free(Wc);
+    free(phi);
+    free(z);
+    free(term);
+    return nc;
+}

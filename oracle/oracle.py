@@ -75,6 +75,8 @@ def olib() -> C.CDLL:
         L.fmo_pack_rows.argtypes = [I, P, P, P, P, I64, P, P, P, P, P]
         L.fmo_run_agent.restype = I
         L.fmo_run_agent.argtypes = [U64, U64, I64, I64, I, P, P, P, P, D, D, D, D, P, P, P, P, P, P, P]
+        L.fmo_sparse_grad.restype = I64
+        L.fmo_sparse_grad.argtypes = [U64, U64, U64, I, P, P, P, P, I64, I64, P, P, P]
         _o = L
     return _o
 
@@ -230,6 +232,22 @@ def run_agent(V, D_, G, mb, n_updates, samples, advantages, W0, lr=1e-6, b1=0.9,
                          _p(W), _p(m), _p(v), _p(mbn), _p(upd), _p(logp) if want_logp else None, _p(last))
     return dict(W=W.reshape(V, D_), m=m.reshape(V, D_), v=v.reshape(V, D_), mb_grad_norm=mbn,
                 upd_grad_norm=upd, logp=logp[:ntok] if want_logp else None, last_grad=last.reshape(V, D_))
+
+
+def sparse_grad(V, D_, seed, samples, advantages, G, max_cols=4096) -> dict:
+    """First-update gradient -(1/G) sum_s A_s term_s of a few samples at full
+    V x D, on the feature columns their contexts touch (fmo_sparse_grad:
+    bit-identical to run_agent's last_grad there, every other column 0) and the
+    micro-batch grad norm (training.hpp:417).  W comes from the seeded stream."""
+    buf, poff, roff = pack_payloads(samples)
+    adv = np.ascontiguousarray(advantages, dtype=np.float64)
+    cols = np.zeros(max_cols, dtype=np.int64)
+    grad = np.zeros(V * max_cols, dtype=np.float64)
+    mbn = np.zeros(1, dtype=np.float64)
+    nc = olib().fmo_sparse_grad(V, D_, seed, len(samples), _p(buf), _p(poff), _p(roff), _p(adv), G, max_cols,
+                                _p(cols), _p(grad), _p(mbn))
+    assert nc >= 0, "too many feature columns"
+    return dict(cols=cols[:nc].copy(), grad=grad[:V * nc].reshape(V, nc).copy(), mb_grad_norm=float(mbn[0]))
 
 
 # ---------------------------------------------------------------------------

@@ -73,6 +73,7 @@ _PROTOS = {
     "fm_agent_read_weights": (I, [P, P]),
     "fm_agent_read_moments": (I, [P, P, P, PI64]),
     "fm_agent_read_grad": (I, [P, P]),
+    "fm_agent_read_grad_cols": (I, [P, P, I64, P]),
     "fm_agent_version": (I64, [P]),
     "fm_agent_samples_accumulated": (I64, [P]),
     "fm_agent_is_active": (I, [P]),

@@ -89,6 +89,10 @@ cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int
 cudaError_t launch_softmax_grad(const CUtensorMap& tmP, const CUtensorMap& tmGt, const float2* stats,
                                 int stats_ld, int64_t Mpad, int64_t V, RowBuffers rows, cudaStream_t s);
 
+// Parity tooling: out[v][j] = dW[v][cols[j]] (f32 or f64 accumulator).
+cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D, const int64_t* cols,
+                               int64_t n_cols, void* out, cudaStream_t s);
+
 // K-adam (training.hpp:37-51): fp64 master weights, fp32 moments, gradient
 // of type G (float for the tensor-core path, double for parity mode);
 // optionally writes the bf16 shadow and zeroes the gradient.  Accumulates

@@ -962,6 +962,40 @@ int fm_agent_read_grad(fm_agent* a, double* g) {
     FM_GUARD_END
 }
 
+int fm_agent_read_grad_cols(fm_agent* a, const int64_t* cols, int64_t n_cols, double* g) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
+    if (n_cols < 0 || (n_cols > 0 && (!cols || !g))) return fail(FM_ERR_INVALID_ARG, "read_grad_cols: bad arguments");
+    for (int64_t j = 0; j < n_cols; ++j)
+        if (cols[j] < 0 || static_cast<uint64_t>(cols[j]) >= a->D)
+            return fail(FM_ERR_INVALID_ARG, "read_grad_cols: column out of range");
+    if (int st = set_dev(a->ctx)) return st;
+    FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
+    const size_t n = static_cast<size_t>(a->V) * static_cast<size_t>(n_cols);
+    if (!a->dw_valid || n == 0) {
+        std::fill(g, g + n, 0.0);
+        return FM_OK;
+    }
+    const bool f64 = a->precision == FM_PRECISION_PARITY_F64;
+    int64_t* dcols = nullptr;
+    void* dout = nullptr;
+    cudaError_t e = cudaMalloc(&dcols, sizeof(int64_t) * n_cols);
+    e = e ? e : cudaMalloc(&dout, n * (f64 ? 8 : 4));
+    e = e ? e : cudaMemcpy(dcols, cols, sizeof(int64_t) * n_cols, cudaMemcpyHostToDevice);
+    e = e ? e : launch_gather_cols(a->dW, f64, a->V, a->D, dcols, n_cols, dout, a->ctx->stream);
+    std::vector<float> tmp(f64 ? 0 : n);
+    if (!e) e = cudaStreamSynchronize(a->ctx->stream);
+    if (!e) e = f64 ? cudaMemcpy(g, dout, n * 8, cudaMemcpyDeviceToHost)
+                    : cudaMemcpy(tmp.data(), dout, n * 4, cudaMemcpyDeviceToHost);
+    cudaFree(dcols);
+    cudaFree(dout);
+    FM_CUDA(e);
+    if (!f64)
+        for (size_t i = 0; i < n; ++i) g[i] = tmp[i];
+    return FM_OK;
+    FM_GUARD_END
+}
+
 int64_t fm_agent_version(const fm_agent* a) { return a->version; }
 int64_t fm_agent_samples_accumulated(const fm_agent* a) { return a->samples; }
 int fm_agent_is_active(const fm_agent* a) { return a->active ? 1 : 0; }

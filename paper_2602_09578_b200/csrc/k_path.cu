@@ -643,6 +643,28 @@ cudaError_t launch_colmax(const __nv_bfloat16* w16, int64_t V, int64_t D, int* k
     return cudaGetLastError();
 }
 
+namespace {
+template <typename T>
+__global__ void gather_cols_kernel(const T* __restrict__ src, uint64_t V, uint64_t D,
+                                   const int64_t* __restrict__ cols, int64_t nc, T* __restrict__ out) {
+    const uint64_t n = V * static_cast<uint64_t>(nc);
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        out[i] = src[(i / nc) * D + cols[i % nc]];
+}
+}  // namespace
+
+cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D, const int64_t* cols,
+                               int64_t n_cols, void* out, cudaStream_t s) {
+    if (f64)
+        gather_cols_kernel<<<1184, 256, 0, s>>>(static_cast<const double*>(dW), V, D, cols, n_cols,
+                                                static_cast<double*>(out));
+    else
+        gather_cols_kernel<<<1184, 256, 0, s>>>(static_cast<const float*>(dW), V, D, cols, n_cols,
+                                                static_cast<float*>(out));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int64_t M, int64_t Mpad, int64_t V,
                        const SampleDesc* sd, int64_t global_batch, RowBuffers rows, const float* old_logp,
                        float clip_eps, double* loss_acc, __nv_bfloat16* pexp_t, __nv_bfloat16* phict,
