@@ -1,0 +1,13 @@
+#!/bin/bash
+# Round-1 v5 captures (session 3; under gpurun, one B200): plain bench, the ncu
+# launch list of the same command, one full capture of each hot kernel.
+set -u
+mkdir -p gpurun_out
+CMD="python bench.py --steps 1 --warmup 1 --e2e-steps 0 --no-cpu-baseline"
+timeout 300 $CMD > gpurun_out/v5_plain.json 2> gpurun_out/v5_plain.err; echo "plain rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_v5.csv $CMD > gpurun_out/v5_ncu_l.log 2>&1; echo "launches rc=$?"
+# GEMM1 + GEMM2 of the third micro-batch (-s skips the earlier launches)
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_tn_2sm -s 4 -c 2 -o gpurun_out/prof5_gemm -f $CMD > gpurun_out/v5_ncu_gemm.log 2>&1; echo "gemm rc=$?"
+for k in adam_kernel lse_kernel gather_kernel; do
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:$k -s 2 -c 1 -o gpurun_out/prof5_$k -f $CMD > gpurun_out/v5_ncu_$k.log 2>&1; echo "$k rc=$?"
+done
