@@ -53,7 +53,17 @@ struct GemmArgs {
     // normaliser (fm_lse.cuh) for the block and resets the counter.
     int* lse_count = nullptr;
     LseArgs lse{};
+    // Grad, stream-K tail (sk_ws != nullptr; CTA-pair kernel): when the tiles do not
+    // fill the last wave, the last (waves-1)*pairs tiles' worth plus the remainder are
+    // split into equal K ranges per pair; partial accumulators meet in sk_ws
+    // ([tile][256][256] fp32, zero between launches) and the last arriving CTA of
+    // each tile half runs the epilogue from it (sk_cnt[tile*2 + rank], self-resetting).
+    float* sk_ws = nullptr;
+    int* sk_cnt = nullptr;
 };
+
+// Stream-K workspace capacity: at most 2*pairs-1 split tiles (148 SMs -> 74 pairs).
+constexpr int kSkMaxTiles = 148;
 
 // 1 when the loss-fold path (no separate K-loss kernel) is active (FM_LOSS_FOLD != 0).
 bool loss_fold_enabled();

@@ -116,6 +116,8 @@ struct Workspace {
     float2* stats = nullptr;
     float* mrow = nullptr;  // loss fold: per-row softmax offset bound [Mpad]
     int* lse_cnt = nullptr;  // fused K-lse: GEMM1 tiles finished per 128-row block (self-resetting)
+    float* sk_ws = nullptr;  // GEMM2 stream-K tail: partial tiles [kSkMaxTiles][256][256] (zero between launches)
+    int* sk_cnt = nullptr;   // [kSkMaxTiles][2] arrivals per tile half (self-resetting)
     // parity mode scratch
     int64_t prow_cap = 0;
     uint64_t pvocab_cap = 0, pparam_cap = 0;
@@ -288,6 +290,8 @@ void ws_free(Workspace& w) {
     cudaFree(w.stats);
     cudaFree(w.mrow);
     cudaFree(w.lse_cnt);
+    cudaFree(w.sk_ws);
+    cudaFree(w.sk_cnt);
     cudaFree(w.zscratch);
     cudaFree(w.dWmb);
     cudaFree(w.logp64);
@@ -342,6 +346,10 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
     e = e ? e : dalloc(&w.mrow, R);
     e = e ? e : dalloc(&w.lse_cnt, static_cast<size_t>(R / 128 + 2));
     e = e ? e : cudaMemset(w.lse_cnt, 0, sizeof(int) * static_cast<size_t>(R / 128 + 2));
+    e = e ? e : dalloc(&w.sk_ws, static_cast<size_t>(kSkMaxTiles) * 256 * 256);
+    e = e ? e : cudaMemset(w.sk_ws, 0, sizeof(float) * static_cast<size_t>(kSkMaxTiles) * 256 * 256);
+    e = e ? e : dalloc(&w.sk_cnt, static_cast<size_t>(kSkMaxTiles) * 2);
+    e = e ? e : cudaMemset(w.sk_cnt, 0, sizeof(int) * static_cast<size_t>(kSkMaxTiles) * 2);
     if (e != cudaSuccess) {
         ws_free(w);
         return fail(FM_ERR_DEVICE_OOM, std::string("workspace allocation: ") + cudaGetErrorString(e));
@@ -1164,6 +1172,16 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g2.ld_out = static_cast<long long>(a->D);
             g2.accumulate = a->dw_valid ? 1 : 0;
             g2.sumsq = scal;
+            {
+                // stream-K tail (opt-in FM_G2_STREAMK=1): C2's 2,000 tiles on 74 pairs leave a
+                // last wave of 2 tiles; split the last 76 tiles' K ranges evenly instead.
+                // Measured within noise of the plain schedule at C2 (2.676 vs 2.670 ms).
+                const char* sk_env = std::getenv("FM_G2_STREAMK");
+                if (gemm_pair_mode() && c->num_sms / 2 <= kSkMaxTiles / 2 && sk_env && sk_env[0] == '1') {
+                    g2.sk_ws = w.sk_ws;
+                    g2.sk_cnt = w.sk_cnt;
+                }
+            }
             const bool exchange = a->gang && a->gang->connected && a->samples + n == G;
             if (exchange) {  // last micro-batch of the step: reduce-scatter inside the epilogue
                 GangState* gs = a->gang;

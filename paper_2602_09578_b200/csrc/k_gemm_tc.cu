@@ -432,6 +432,67 @@ __global__ void __launch_bounds__(kThreads, 1)
 // issues every MMA and commits to both CTAs' barriers; each CTA drains its
 // own 128-lane half of the accumulator from its TMEM.
 // ---------------------------------------------------------------------------
+// Work schedule of the pair kernel.  Data-parallel tiles round-robin over the
+// pairs; with stream-K (Grad, tiles % pairs != 0) the last
+// (tiles - (waves-1)*pairs) tiles are cut into equal contiguous K-iteration
+// ranges, one per pair, so no pair idles through a mostly empty last wave.
+struct WorkItem {
+    int tile, kb, ke;
+    int sk;  // stream-K tile slot when only part of the tile's K range is here, else -1
+};
+struct Sched {
+    int T, Kt, P, T_dp;
+    long long U;  // stream-K K-iterations in total
+    __device__ __forceinline__ Sched(int tiles, int k_iters, int pairs, bool streamk) {
+        T = tiles;
+        Kt = k_iters;
+        P = pairs;
+        const int waves = tiles / pairs;
+        if (streamk && waves >= 1 && tiles % pairs != 0) {
+            T_dp = (waves - 1) * pairs;
+            U = static_cast<long long>(tiles - T_dp) * k_iters;
+        } else {
+            T_dp = tiles;
+            U = 0;
+        }
+    }
+    __device__ __forceinline__ long long ustart(int c) const { return static_cast<long long>(c) * U / P; }
+    __device__ __forceinline__ int pair_of(long long u) const {
+        int c = static_cast<int>(u * P / U);
+        while (c + 1 < P && ustart(c + 1) <= u) ++c;
+        while (c > 0 && ustart(c) > u) --c;
+        return c;
+    }
+    // number of pairs whose K ranges cover stream-K tile slot lt
+    __device__ __forceinline__ int contributors(int lt) const {
+        const long long a = static_cast<long long>(lt) * Kt;
+        return pair_of(a + Kt - 1) - pair_of(a) + 1;
+    }
+    __device__ __forceinline__ bool get(int cid, int w, WorkItem& wi) const {
+        const int ndp = cid < T_dp ? (T_dp - cid + P - 1) / P : 0;
+        if (w < ndp) {
+            wi = WorkItem{cid + w * P, 0, Kt, -1};
+            return true;
+        }
+        if (U == 0) return false;
+        const long long u0 = ustart(cid), u1 = ustart(cid + 1);
+        const long long st = (w == ndp) ? u0 : (u0 / Kt + (w - ndp)) * static_cast<long long>(Kt);
+        if (st >= u1) return false;
+        const long long en = min(u1, (st / Kt + 1) * static_cast<long long>(Kt));
+        const int lt = static_cast<int>(st / Kt);
+        wi.tile = T_dp + lt;
+        wi.kb = static_cast<int>(st % Kt);
+        wi.ke = wi.kb + static_cast<int>(en - st);
+        wi.sk = (wi.kb == 0 && wi.ke == Kt) ? -1 : lt;
+        return true;
+    }
+};
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+
 constexpr int P_STAGES = 6;
 constexpr uint32_t P_A_STAGE = 128 * BK * 2;    // 16 KB: this CTA's 128 rows of A
 constexpr uint32_t P_B_STAGE = 128 * BK * 2;    // 16 KB: this CTA's half of B's 256 rows
@@ -486,6 +547,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     const int k_iters = (args.K + BK - 1) / BK;
     const int cid = blockIdx.x >> 1;
     const int nclusters = gridDim.x >> 1;
+    const Sched sch(num_tiles, k_iters, nclusters, std::is_same_v<Epi, GradEpi> && args.sk_ws != nullptr);
 
     if (warp == 0) {
         // ===== TMA producer (both CTAs) =====
@@ -493,11 +555,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             const uint64_t pol = policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = cid; t < num_tiles; t += nclusters) {
-                const TileCoord tc = tile_coord(t, tiles_m, tiles_n, args.group_m);
+            WorkItem wi;
+            for (int w = 0; sch.get(cid, w, wi); ++w) {
+                const TileCoord tc = tile_coord(wi.tile, tiles_m, tiles_n, args.group_m);
                 const int arow = tc.mb * 256 + static_cast<int>(rank) * 128;
                 const int brow = tc.nb * BN + static_cast<int>(rank) * 128;
-                for (int k = 0; k < k_iters; ++k) {
+                for (int k = wi.kb; k < wi.ke; ++k) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t fb = mapa_shared(&full[stage], 0);
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
@@ -517,11 +580,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = cid; t < num_tiles; t += nclusters) {
+            WorkItem wi;
+            for (int w = 0; sch.get(cid, w, wi); ++w) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-                for (int k = 0; k < k_iters; ++k) {
+                for (int k = wi.kb; k < wi.ke; ++k) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint64_t adesc = umma_desc_k_sw128(smem_u32(sA + stage * P_A_STAGE));
@@ -529,7 +593,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
 #pragma unroll
                     for (int kk = 0; kk < BK / 16; ++kk)
                         umma_bf16_2sm(d_tmem, adesc + static_cast<uint64_t>(kk * 2),
-                                      bdesc + static_cast<uint64_t>(kk * 2), kIdesc2, (k | kk) != 0);
+                                      bdesc + static_cast<uint64_t>(kk * 2), kIdesc2, (k != wi.kb || kk != 0));
                     umma_commit_2sm(&empty[stage], 0x3);
                     if (++stage == P_STAGES) {
                         stage = 0;
@@ -554,11 +618,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         double sumsq_total = 0.0;
         double lse_loss = 0.0;
         __shared__ int lse_flag;
-        for (int t = cid; t < num_tiles; t += nclusters) {
-            const TileCoord tc = tile_coord(t, tiles_m, tiles_n, args.group_m);
+        __shared__ int sk_flag;
+        WorkItem wi;
+        for (int w = 0; sch.get(cid, w, wi); ++w) {
+            const TileCoord tc = tile_coord(wi.tile, tiles_m, tiles_n, args.group_m);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int row = tc.mb * 256 + row_in_tile;
+            if constexpr (std::is_same_v<Epi, GradEpi>) {
+                if (wi.sk >= 0) {
+                    // stream-K partial: add this K range's accumulator into the tile's
+                    // workspace, then count the arrival; the last of the tile half's
+                    // contributors runs the epilogue on the summed tile
+                    float* wrow = args.sk_ws + (static_cast<size_t>(wi.sk) * 256 + row_in_tile) * BN;
+#pragma unroll 1
+                    for (int c = 0; c < BN / 32; ++c) {
+                        uint32_t r[32];
+                        tmem_ld_32x32b_x32(tmem_base + ((quad * 32u) << 16) + static_cast<uint32_t>(acc * BN + c * 32), r);
+                        tmem_ld_wait();
+                        if (c == BN / 32 - 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader[acc]);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            red_add_v4(wrow + c * 32 + j, __uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                       __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                    }
+                    named_bar_sync(1, 128);
+                    if (quad == 0 && lane == 0) {
+                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                        int* cnt = args.sk_cnt + wi.sk * 2 + static_cast<int>(rank);
+                        const int last = atomicAdd(cnt, 1) == sch.contributors(wi.sk) - 1;
+                        if (last) *cnt = 0;
+                        sk_flag = last;
+                    }
+                    named_bar_sync(1, 128);
+                    if (sk_flag) {
+                        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                        epi.begin(args, row);
+                        epi.sumsq = 0.0;
+#pragma unroll 1
+                        for (int c = 0; c < BN / 32; ++c) {
+                            uint32_t r[32];
+                            float4* src = reinterpret_cast<float4*>(wrow + c * 32);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 v = __ldcg(src + q);
+                                r[4 * q] = __float_as_uint(v.x);
+                                r[4 * q + 1] = __float_as_uint(v.y);
+                                r[4 * q + 2] = __float_as_uint(v.z);
+                                r[4 * q + 3] = __float_as_uint(v.w);
+                                __stcg(src + q, make_float4(0.f, 0.f, 0.f, 0.f));  // zero for the next launch
+                            }
+                            epi.chunk(args, row, tc.nb * BN + c * 32, r);
+                        }
+                        epi.end(args, row, tc.nb);
+                        sumsq_total += epi.sumsq;
+                    }
+                    acc ^= 1;
+                    if (acc == 0) acc_phase ^= 1;
+                    continue;
+                }
+            }
             epi.begin(args, row);
             if constexpr (std::is_same_v<Epi, GradEpi>) epi.sumsq = 0.0;
             if (Epi::kTwoPass && !args.mrow) {

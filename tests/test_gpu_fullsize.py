@@ -177,3 +177,14 @@ def test_large_policy_gradient_matches_sparse_f64_oracle(ctx, cfg_name):
         assert abs(rep.grad_norm - ref["mb_grad_norm"]) <= 2e-2 * ref["mb_grad_norm"]
     finally:
         eng.close()
+
+
+def test_c2_stream_k_matches_plain_schedule(ctx, c2_engine, monkeypatch):
+    """C2's GEMM2 (2,000 tiles on 74 pairs, 256 K iterations each) with the
+    stream-K tail (opt-in FM_G2_STREAMK=1) vs the plain round-robin schedule."""
+    mb = _samples(4, 16, 1024, adv_seed=4)
+    g_dp = _fresh_grad(ctx, c2_engine, [mb])
+    monkeypatch.setenv("FM_G2_STREAMK", "1")
+    g_sk = _fresh_grad(ctx, c2_engine, [mb])
+    assert np.linalg.norm(g_dp) > 0
+    assert rel_fro(g_sk, g_dp) < 1e-6

@@ -421,3 +421,45 @@ def test_fused_lse_matches_standalone_kernel(ctx, monkeypatch):
     # K-adam's norm reduction adds in atomic order
     np.testing.assert_allclose(fused["upd_grad_norm"], alone["upd_grad_norm"], rtol=1e-12)
     assert rel_fro(fused["grads"][0], _oracle_grad_step0(f)) <= 2e-2
+
+
+def _train_one(ctx, V, D_, samples, adv, G=64):
+    from paper_2602_09578_b200.engine import TrainingEngine
+    eng = TrainingEngine([ctx], global_batch=G, precision=_lib.PRECISION_BF16_TC)
+    try:
+        eng.add_agent("sk", V, D_)
+        eng.activate("sk")
+        eng.run()
+        h = eng.handle("sk")
+        arr = (_lib.fm_sample * len(samples))(*[_lib.fm_sample(ctx.put(orc.encode(p)), ctx.put(orc.encode(r)), a)
+                                                for (p, r), a in zip(samples, adv)])
+        t = C.c_int64()
+        _lib.check(_lib.lib().fm_train_micro_batch(h, arr, len(samples), G, C.byref(t)))
+        _lib.check(_lib.lib().fm_agent_sync(h))
+        rep = _lib.fm_report()
+        assert _lib.lib().fm_agent_poll_report(h, t.value, C.byref(rep)) == 1
+        return eng.read_grad("sk"), rep.grad_norm
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("V,D_,resp", [(256 * 75, 256, 6), (256 * 80, 512, 40), (256 * 150, 256, 3)])
+def test_gemm2_stream_k_tail(ctx, monkeypatch, V, D_, resp):
+    """K-GEMM2 stream-K tail (opt-in FM_G2_STREAMK=1): tile counts that leave a
+    partial last wave on 74 pairs (75, 160 and 150 output tiles; 2-12 K
+    iterations per tile, so tiles are split across 2-3 pairs) give the same
+    gradient and micro-batch norm as the plain schedule up to fp32 summation
+    order, and match the f64 oracle within the BF16_TC contract."""
+    rng = np.random.default_rng(V + D_)
+    samples = [([int(x) for x in rng.integers(0, V, size=8)], [int(x) for x in rng.integers(0, V, size=resp)])
+               for _ in range(16)]
+    adv = rng.normal(size=16)
+    g_dp, n_dp = _train_one(ctx, V, D_, samples, adv)
+    monkeypatch.setenv("FM_G2_STREAMK", "1")
+    g_sk, n_sk = _train_one(ctx, V, D_, samples, adv)
+    assert np.linalg.norm(g_dp) > 0
+    assert rel_fro(g_sk, g_dp) < 1e-5
+    assert abs(n_sk - n_dp) <= 1e-5 * n_dp
+    ref = orc.sparse_grad(V, D_, agent_seed(2048, "sk"), samples, adv, 64)
+    assert rel_fro(g_sk[:, ref["cols"]], ref["grad"]) <= 2e-2
+    assert abs(n_sk - ref["mb_grad_norm"]) <= 2e-2 * ref["mb_grad_norm"]
