@@ -1167,7 +1167,12 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g2.M = static_cast<int>(a->V);
             g2.N = static_cast<int>(a->D);
             g2.K = static_cast<int>(Mpad);
-            g2.group_m = env_int("FM_G2_GROUP_M", 8);
+            // raster: when B = Phic^T (D x Mpad bf16) is about L2-sized (C2: 134 MB) run all
+            // D/256 column tiles of a vocab row block together (group 1) so p~^T is read
+            // from DRAM once (ncu: 6.6 vs 7.0 GB, 2.22 vs 2.26 ms; profiles/r01_g2_sweep.jsonl);
+            // a larger B (C3/C5: 1.07 GB) would be re-read per row block, so group 8 there
+            const double b_bytes = 2.0 * static_cast<double>(a->D) * static_cast<double>(Mpad);
+            g2.group_m = env_int("FM_G2_GROUP_M", b_bytes <= 160e6 ? 1 : 8);
             g2.out = static_cast<float*>(a->dW);
             g2.ld_out = static_cast<long long>(a->D);
             g2.accumulate = a->dw_valid ? 1 : 0;
