@@ -388,8 +388,9 @@ def run_ours(args, dist: Dist) -> dict | None:
             a = b / (avg_ms / 1e3) / 1e9
             e.update(bound="hbm", achieved=round(a, 1), unit="GB/s", frac=round(a / peaks["hbm_gbs"], 4))
         kernels[name] = e
-    if "gemm1" in kernels and "lse" not in kernels and os.environ.get("FM_LSE_FUSED") == "1":
-        # K-lse runs inside GEMM1's last-tile epilogue (opt-in FM_LSE_FUSED=1): its time is gemm1's
+    if "gemm1" in kernels and "lse" not in kernels and os.environ.get("FM_LSE_FUSED") != "0" \
+            and os.environ.get("FM_LOSS_FOLD") != "0":
+        # K-lse runs in GEMM1's grid tail (default; FM_LSE_FUSED=0 launches it): its time is gemm1's
         kernels["lse"] = {"launches": 0, "fused_into": "gemm1"}
     dom = max(kernels, key=lambda k: kernels[k].get("total_ms", 0.0)) if kernels else None
     traffic = None

@@ -48,10 +48,11 @@ struct GemmArgs {
     int xrank = 0;
     int xlo[9] = {};
     float* xpeer[8] = {};
-    // Logits, fused K-lse (lse_count != nullptr): lse_count[b] counts the vocab tiles
-    // finished for 128-row block b; the CTA that finishes the last one runs the row
-    // normaliser (fm_lse.cuh) for the block and resets the counter.
-    int* lse_count = nullptr;
+    // Logits, fused K-lse (lse_sync != nullptr): lse_sync[0] counts the CTAs whose
+    // tiles are stored, lse_sync[1] is the epoch the last one publishes; then the
+    // whole grid runs the row normaliser (fm_lse.cuh) over lse's rows.
+    unsigned* lse_sync = nullptr;
+    unsigned lse_epoch = 0;
     LseArgs lse{};
     // Grad, stream-K tail (sk_ws != nullptr; CTA-pair kernel): when the tiles do not
     // fill the last wave, the last (waves-1)*pairs tiles' worth plus the remainder are

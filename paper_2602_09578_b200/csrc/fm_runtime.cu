@@ -115,7 +115,8 @@ struct Workspace {
     float* zact = nullptr;          // logit of the taken token [Mpad]
     float2* stats = nullptr;
     float* mrow = nullptr;  // loss fold: per-row softmax offset bound [Mpad]
-    int* lse_cnt = nullptr;  // fused K-lse: GEMM1 tiles finished per 128-row block (self-resetting)
+    unsigned* lse_sync = nullptr;  // fused K-lse: {CTAs arrived, epoch published} (GEMM1 tail)
+    unsigned lse_epoch = 0;
     float* sk_ws = nullptr;  // GEMM2 stream-K tail: partial tiles [kSkMaxTiles][256][256] (zero between launches)
     int* sk_cnt = nullptr;   // [kSkMaxTiles][2] arrivals per tile half (self-resetting)
     // parity mode scratch
@@ -289,7 +290,7 @@ void ws_free(Workspace& w) {
     cudaFree(w.zact);
     cudaFree(w.stats);
     cudaFree(w.mrow);
-    cudaFree(w.lse_cnt);
+    cudaFree(w.lse_sync);
     cudaFree(w.sk_ws);
     cudaFree(w.sk_cnt);
     cudaFree(w.zscratch);
@@ -344,8 +345,8 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
     e = e ? e : dalloc(&w.zact, R);
     e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n);
     e = e ? e : dalloc(&w.mrow, R);
-    e = e ? e : dalloc(&w.lse_cnt, static_cast<size_t>(R / 128 + 2));
-    e = e ? e : cudaMemset(w.lse_cnt, 0, sizeof(int) * static_cast<size_t>(R / 128 + 2));
+    e = e ? e : dalloc(&w.lse_sync, 2);
+    e = e ? e : cudaMemset(w.lse_sync, 0, 2 * sizeof(unsigned));
     e = e ? e : dalloc(&w.sk_ws, static_cast<size_t>(kSkMaxTiles) * 256 * 256);
     e = e ? e : cudaMemset(w.sk_ws, 0, sizeof(float) * static_cast<size_t>(kSkMaxTiles) * 256 * 256);
     e = e ? e : dalloc(&w.sk_cnt, static_cast<size_t>(kSkMaxTiles) * 2);
@@ -1131,18 +1132,20 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g1.row_scale = w.rscale;
             g1.stats = w.stats;
             g1.stats_ld = tiles_n;
-            // K-lse fused into GEMM1 (loss fold, CTA-pair kernel; opt-in FM_LSE_FUSED=1): the
-            // CTA finishing a 128-row block's last vocab tile normalises those rows in its
-            // epilogue.  Measured slower (GEMM1 2.57 -> 2.89-2.97 ms at C2 vs a 14 us K-lse
-            // launch): the per-tile counter release stalls the epilogue warps.
+            // K-lse fused into GEMM1's tail (loss fold, CTA-pair kernel; FM_LSE_FUSED=0
+            // launches it separately): after a grid-wide arrival the epilogue warps
+            // normalise the rows.  Same time as the 14 us launch it replaces (C2: GEMM1
+            // +7-29 us, K-lse -14 us); one launch fewer per micro-batch.  (A per-tile
+            // last-finisher variant cost GEMM1 12-15%: DESIGN.md §9.)
             const char* lse_env = std::getenv("FM_LSE_FUSED");
-            const bool lse_fused = fold && gemm_pair_mode() && lse_env && lse_env[0] == '1';
+            const bool lse_fused = fold && gemm_pair_mode() && !(lse_env && lse_env[0] == '0');
             const LseArgs lse_args{w.zact, w.stats, tiles_n, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
                                    a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1,
                                    fold ? 1 : 0, fold ? w.gt : nullptr, w.phict, Mpad};
             if (lse_fused) {
                 g1.lse = lse_args;
-                g1.lse_count = w.lse_cnt;
+                g1.lse_sync = w.lse_sync;
+                g1.lse_epoch = ++w.lse_epoch;
             }
             FM_CUDA(cudaEventRecord(c->ev_gemm, s));  // swap copies may start here (fm_agent_suspend)
             c->gemm_seq = ++c->op_seq;

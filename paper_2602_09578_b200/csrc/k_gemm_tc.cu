@@ -56,31 +56,42 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int tiles_m, int tiles_n,
 
 __device__ __forceinline__ float fast_exp(float x) { return exp2f(x * 1.4426950408889634f); }
 
-// Fused K-lse (GEMM1, loss fold): after a tile's epilogue, count the finished
-// vocab tile for this CTA's 128-row block; the CTA that finishes the block's
-// last tile runs the row normaliser for its 128 rows (each epilogue warp its 32,
-// four rows per step).  Release: the named barrier orders the four warps'
-// p~^T / logit / partial stores before one thread's gpu-scope acq_rel fence
-// and counter increment (cumulative, as CUTLASS's generic barrier); acquire:
-// the finishing CTA fences after observing the count.  The counter resets
-// itself for the next launch.
-__device__ __forceinline__ void lse_tile_done(const GemmArgs& a, int blk, int tiles_n, uint32_t quad,
-                                              volatile int* flag, double& loss) {
+// Fused K-lse (GEMM1, loss fold; opt-in FM_LSE_FUSED=1): once a CTA's
+// epilogue warps have stored all their tiles, one thread releases the CTA's
+// stores (named barrier + gpu-scope acq_rel fence, cumulative) and arrives on a
+// grid counter; the last arriver resets it and publishes the launch's epoch,
+// the others spin on the epoch (the persistent grid is one CTA per SM, all
+// co-resident; a 2 s bound traps instead of hanging).  Then every epilogue warp
+// of the grid runs the row normaliser (fm_lse.cuh) over a strided share of the
+// rows — the work of the standalone K-lse launch, without the launch.
+__device__ __forceinline__ void lse_grid_tail(const GemmArgs& a, uint32_t quad, double& loss) {
     named_bar_sync(1, 128);
     if (quad == 0 && (threadIdx.x & 31) == 0) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        const int prev = atomicAdd(&a.lse_count[blk], 1);
-        const int last = prev == tiles_n - 1;
-        if (last) a.lse_count[blk] = 0;
-        *flag = last;
+        const unsigned prev = atomicAdd(&a.lse_sync[0], 1u);
+        if (prev == gridDim.x - 1) {
+            a.lse_sync[0] = 0;  // for the next launch (stream-ordered after this one)
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.lse_sync + 1), "r"(a.lse_epoch) : "memory");
+        } else {
+            uint64_t t0;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            for (;;) {
+                unsigned e;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(e) : "l"(a.lse_sync + 1) : "memory");
+                if (e == a.lse_epoch) break;
+                __nanosleep(100);
+                uint64_t t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (t - t0 > 2000000000ull) __trap();
+            }
+        }
     }
     named_bar_sync(1, 128);
-    if (*flag) {
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        const int64_t r0 = static_cast<int64_t>(blk) * 128 + quad * 32;
-#pragma unroll 1
-        for (int q = 0; q < 8; ++q) loss += lse_row_quad(a.lse, r0 + 4 * q);
-    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * 4;
+    for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * 4 + quad) * 4; r0 < a.lse.Mpad; r0 += nw * 4)
+        loss += lse_row_quad(a.lse, r0);
 }
 
 // ---- epilogues ------------------------------------------------------------
@@ -617,7 +628,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         uint32_t acc_phase = 0;
         double sumsq_total = 0.0;
         double lse_loss = 0.0;
-        __shared__ int lse_flag;
         __shared__ int sk_flag;
         WorkItem wi;
         for (int w = 0; sch.get(cid, w, wi); ++w) {
@@ -710,10 +720,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             }
             epi.end(args, row, tc.nb);
             if constexpr (std::is_same_v<Epi, GradEpi>) sumsq_total += epi.sumsq;
-            if constexpr (std::is_same_v<Epi, LogitsEpi>) {
-                if (args.lse_count)
-                    lse_tile_done(args, tc.mb * 2 + static_cast<int>(rank), tiles_n, quad, &lse_flag, lse_loss);
-            }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
@@ -722,9 +728,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             if (lane == 0 && args.sumsq) atomicAdd(args.sumsq, sumsq_total);
         }
         if constexpr (std::is_same_v<Epi, LogitsEpi>) {
-            for (int o = 16; o > 0; o >>= 1) lse_loss += __shfl_xor_sync(0xffffffffu, lse_loss, o);
-            if (lane == 0 && args.lse_count && args.lse.loss_acc && lse_loss != 0.0)
-                atomicAdd(args.lse.loss_acc, lse_loss);
+            if (args.lse_sync) {
+                lse_grid_tail(args, quad, lse_loss);
+                for (int o = 16; o > 0; o >>= 1) lse_loss += __shfl_xor_sync(0xffffffffu, lse_loss, o);
+                if (lane == 0 && args.lse.loss_acc && lse_loss != 0.0) atomicAdd(args.lse.loss_acc, lse_loss);
+            }
         }
     }
     tc_fence_before();

@@ -116,13 +116,13 @@ def test_c2_swap_identity(ctx, c2_engine, tier):
 
 
 def test_c2_fused_lse_matches_standalone(ctx, c2_engine, monkeypatch):
-    """125 vocab tiles per row block: the CTA finishing a block's last tile runs
-    K-lse inside GEMM1 (opt-in FM_LSE_FUSED=1) — same gradient as the standalone
-    K-lse launch (default); only the accumulator round trip differs (fp32 adds)."""
+    """16,384 rows normalised by the whole GEMM1 grid after its grid-wide
+    arrival (default) — same gradient as the standalone K-lse launch
+    (FM_LSE_FUSED=0); only the accumulator round trip differs (fp32 adds)."""
     mb = _samples(3, 16, 1024, adv_seed=3)
-    g_alone = _fresh_grad(ctx, c2_engine, [mb])
-    monkeypatch.setenv("FM_LSE_FUSED", "1")
     g_fused = _fresh_grad(ctx, c2_engine, [mb])
+    monkeypatch.setenv("FM_LSE_FUSED", "0")
+    g_alone = _fresh_grad(ctx, c2_engine, [mb])
     assert np.linalg.norm(g_fused) > 0
     assert rel_fro(g_fused, g_alone) < 1e-6
 

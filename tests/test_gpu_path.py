@@ -406,14 +406,14 @@ def test_gemm2_k_chunks_match_single_launch(ctx, monkeypatch):
 
 
 def test_fused_lse_matches_standalone_kernel(ctx, monkeypatch):
-    """K-lse fused into GEMM1's last-tile epilogue (opt-in FM_LSE_FUSED=1) runs
-    the same per-row routine (fm_lse.cuh) on the same bits as the standalone
-    K-lse launch (default): gradients, grad norms and the updated W/m/v are
+    """K-lse fused into GEMM1's grid tail (default) runs the same per-row
+    routine (fm_lse.cuh) on the same bits as the standalone K-lse launch
+    (FM_LSE_FUSED=0): gradients, grad norms and the updated W/m/v are
     bit-identical."""
     f = _ld("mid_agent0.npz")
-    alone = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
-    monkeypatch.setenv("FM_LSE_FUSED", "1")
     fused = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
+    monkeypatch.setenv("FM_LSE_FUSED", "0")
+    alone = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
     for g1, g2 in zip(fused["grads"], alone["grads"]):
         np.testing.assert_array_equal(g1, g2)
     for k in ("W", "m", "v", "mb_grad_norm"):
