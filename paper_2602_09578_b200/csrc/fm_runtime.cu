@@ -1,8 +1,12 @@
 // fm_runtime.cu — C ABI implementation: device contexts, the token arena,
 // per-agent trainer state, the micro-batch pipeline
-//   K-gather -> K-GEMM1 (tcgen05) -> K-lse -> K-softmax-grad -> K-GEMM2 (tcgen05)
-// (or the fp64 parity pipeline), the fused Adam update, training-state swap
-// and the NCCL gradient all-reduce.
+//   K-gather -> K-GEMM1 (tcgen05; log-softmax numerator in the epilogue, K-lse
+//   in the grid tail) -> K-GEMM2 (tcgen05; softmax gradient folded into its
+//   operands)
+// (or the fp64 parity pipeline; FM_LOSS_FOLD=0 / FM_LSE_FUSED=0 restore the
+// separate K-softmax-grad / K-lse launches), the fused Adam update, training-
+// state swap and migration, DP gangs (fused reduce-scatter / NCCL all-reduce),
+// weight publish and the PolicyState wire format.
 //
 // Memory layout in HBM: every agent matrix is row-major
 // [V][D] (row = vocab id, col = feature; tensor.hpp:13-22):
@@ -11,8 +15,9 @@
 //   dW   f32   gradient accumulator      (4 B/param; f64 in parity mode)
 //   W16  bf16  GEMM shadow of W          (2 B/param; tensor-core mode only)
 // Per-GPU workspace, sized for the largest micro-batch (Mpad = rows rounded
-// up to 128): packed rows, Phic [Mpad][D] / Phic^T [D][Mpad] bf16, Z [Mpad][V]
-// fp32 logits, softmax partials [Mpad][V/256], G^T [V][Mpad] bf16.
+// up to 128): packed rows, Phic [Mpad][D] / Phic^T [D][Mpad] bf16 (integer
+// counts; K-lse rescales Phic^T's entries per row), p~^T [V][Mpad] bf16
+// (GEMM1's output = GEMM2's A operand), softmax partials [Mpad][V/256].
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
