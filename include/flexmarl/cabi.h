@@ -197,6 +197,12 @@ int fm_agent_poll_report(fm_agent* a, int64_t ticket, fm_report* out);
  * If grad_norm_out != NULL the call waits and writes ||grad||_F. */
 int fm_apply_update(fm_agent* a, int64_t global_batch, double lr, double beta1, double beta2,
                     double eps, double* grad_norm_out, int64_t* version_out);
+/* apply_global_update followed by suspend(FM_TIER_DEVICE) (training.hpp:435-456,
+ * 321-350), fused: K-adam writes the updated state straight into the agent's
+ * parking buffer on its GPU, so no copy-out pass runs; fm_agent_activate
+ * brings it back as after fm_agent_suspend.  Tensor-core agents outside a gang. */
+int fm_apply_update_park(fm_agent* a, int64_t global_batch, double lr, double beta1, double beta2,
+                         double eps, double* grad_norm_out, int64_t* version_out);
 
 /* ---- training-state swap (suspend / activate, training.hpp:259-350) -------
  * suspend: copy {W, m, v, accumulated gradient} to the parking tier on the

@@ -87,6 +87,7 @@ _PROTOS = {
     "fm_agent_sync": (I, [P]),
     "fm_agent_poll_report": (I, [P, I64, C.POINTER(fm_report)]),
     "fm_apply_update": (I, [P, I64, D, D, D, D, PD, PI64]),
+    "fm_apply_update_park": (I, [P, I64, D, D, D, D, PD, PI64]),
     "fm_agent_suspend": (I, [P, I, I]),
     "fm_agent_activate": (I, [P, P]),
     "fm_agent_state_checksum": (I, [P, PU64]),

@@ -99,11 +99,20 @@ cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D,
 // sum(g^2) into *gsq for the update grad_norm.  With colmax != NULL (and a
 // [V][D] shadow) it also produces K-colmax's keys from the new shadow when the
 // grid can keep every thread on fixed columns (*colmax_done tells).
+// With dst != NULL the updated w / m / v go to dst's buffers instead of in
+// place (w16 and colmax are outputs already): the swap-out fused into the
+// optimizer, which writes the new state straight into the parking buffer.
+struct AdamDst {
+    double* w;
+    float* m;
+    float* v;
+};
 template <typename G>
 cudaError_t launch_adam(double* w, float* m, float* v, G* g, __nv_bfloat16* w16, uint64_t n,
                         double lr, double b1, double b2, double eps, double bc1, double bc2,
                         int zero_grad, double* gsq, int num_sms, cudaStream_t s,
-                        int* colmax = nullptr, uint64_t D = 0, bool* colmax_done = nullptr);
+                        int* colmax = nullptr, uint64_t D = 0, bool* colmax_done = nullptr,
+                        const AdamDst* dst = nullptr);
 
 cudaError_t launch_to_bf16(const double* w, __nv_bfloat16* w16, uint64_t n, int num_sms,
                            cudaStream_t s);

@@ -1417,9 +1417,15 @@ int fm_agent_poll_report(fm_agent* a, int64_t ticket, fm_report* out) {
     return 1;
 }
 
-int fm_apply_update(fm_agent* a, int64_t G, double lr, double b1, double b2, double eps, double* grad_norm_out,
-                    int64_t* version_out) {
-    FM_GUARD_BEGIN
+static int park_reserve(fm_agent* a, fm_ctx* c, int tier, int pdev, size_t bytes);
+static size_t park_bytes_for(const fm_agent* a);
+
+// apply_global_update; with park != 0 (device tier, tensor-core agent, no gang)
+// K-adam writes the new W / m / v / W16 / colmax straight into the agent's
+// parking buffer and the agent is suspended — the swap-out fused into the
+// optimizer (no copy-out pass).
+static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, double b2, double eps,
+                             double* grad_norm_out, int64_t* version_out, bool park) {
     if (int st = check_active(a)) return st;
     if (a->samples != G)
         return fail(FM_ERR_INCOMPLETE_BATCH,
@@ -1427,6 +1433,17 @@ int fm_apply_update(fm_agent* a, int64_t G, double lr, double b1, double b2, dou
     fm_ctx* c = a->ctx;
     if (int st = set_dev(c)) return st;
     cudaStream_t s = c->stream;
+    AdamDst dst{};
+    uint8_t* pk = nullptr;
+    if (park) {
+        if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang (fm_gang_detach first)");
+        if (a->precision != FM_PRECISION_BF16_TC || !a->W16)
+            return fail(FM_ERR_INVALID_ARG, "update-and-park needs a tensor-core agent");
+        if (int st = park_reserve(a, c, FM_TIER_DEVICE, c->device, park_bytes_for(a))) return st;
+        pk = static_cast<uint8_t*>(a->park);
+        dst = AdamDst{reinterpret_cast<double*>(pk), reinterpret_cast<float*>(pk + a->P * 8),
+                      reinterpret_cast<float*>(pk + a->P * 12)};
+    }
     if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * dw_elem(a), s));
     a->step += 1;
     const double bc1 = 1.0 - std::pow(b1, static_cast<double>(a->step));  // training.hpp:42-43
@@ -1453,9 +1470,12 @@ int fm_apply_update(fm_agent* a, int64_t G, double lr, double b1, double b2, dou
     } else {
         // the next step's first GEMM2 overwrites dW, so no zeroing pass here; the new
         // shadow's column maxima (loss-fold bound) come out of the same pass
-        FM_CUDA(launch_adam<float>(a->W, a->m, a->v, static_cast<float*>(a->dW), a->W16, a->P, lr, b1, b2, eps,
-                                   bc1, bc2, 0, a->d_upd, c->num_sms, s, loss_fold_enabled() ? a->colmax : nullptr,
-                                   a->D, &cm_fused));
+        const size_t dwe = dw_elem(a);
+        __nv_bfloat16* w16_out = park ? reinterpret_cast<__nv_bfloat16*>(pk + a->P * (16 + dwe)) : a->W16;
+        int* cm_out = park ? reinterpret_cast<int*>(pk + a->P * (18 + dwe)) : a->colmax;
+        FM_CUDA(launch_adam<float>(a->W, a->m, a->v, static_cast<float*>(a->dW), w16_out, a->P, lr, b1, b2, eps,
+                                   bc1, bc2, 0, a->d_upd, c->num_sms, s, loss_fold_enabled() ? cm_out : nullptr,
+                                   a->D, &cm_fused, park ? &dst : nullptr));
     }
     count_launch();
     a->dw_valid = false;
@@ -1464,38 +1484,47 @@ int fm_apply_update(fm_agent* a, int64_t G, double lr, double b1, double b2, dou
     ++a->w16_gen;
     if (cm_fused) a->cm_gen = a->w16_gen;
     FM_CUDA(cudaMemcpyAsync(a->h_upd, a->d_upd, sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (park) {
+        // the parked state is complete when K-adam is: release the slot behind it
+        a->park_w16 = true;
+        a->cm_parked = cm_fused;
+        FM_CUDA(cudaEventRecord(a->ev_out, s));
+        agent_free_device(a, s);
+        a->active = false;
+        a->ctx = nullptr;
+    }
     if (grad_norm_out) {
         FM_CUDA(cudaStreamSynchronize(s));
         *grad_norm_out = std::sqrt(*a->h_upd);
     }
     if (version_out) *version_out = a->version;
     return FM_OK;
+}
+
+int fm_apply_update(fm_agent* a, int64_t G, double lr, double b1, double b2, double eps, double* grad_norm_out,
+                    int64_t* version_out) {
+    FM_GUARD_BEGIN
+    return apply_update_impl(a, G, lr, b1, b2, eps, grad_norm_out, version_out, false);
+    FM_GUARD_END
+}
+
+int fm_apply_update_park(fm_agent* a, int64_t G, double lr, double b1, double b2, double eps, double* grad_norm_out,
+                         int64_t* version_out) {
+    FM_GUARD_BEGIN
+    return apply_update_impl(a, G, lr, b1, b2, eps, grad_norm_out, version_out, true);
     FM_GUARD_END
 }
 
 // ---------------------------------------------------------------------------
 // training-state swap
 // ---------------------------------------------------------------------------
-int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
-    FM_GUARD_BEGIN
-    // a K-GEMM1 launched after the agent's last op (e.g. the next agent's first
-    // micro-batch) is a safe and cheap start for the copy-out: the copy engines then
-    // overlap tensor-bound GEMMs instead of the latency-bound K-gather that follows
-    // the end of the currently queued work (measured: K-gather 16 us -> 390 us
-    // beside a 2.4 GB D2D copy)
-    const bool gated = a->active && a->ctx && a->ctx->gemm_seq > a->last_seq;
-    if (int st = check_active(a)) return st;
-    if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang (fm_gang_detach first)");
-    fm_ctx* c = a->ctx;
-    if (int st = set_dev(c)) return st;
-    const size_t P = a->P;
-    const size_t dwb = a->dw_valid ? P * dw_elem(a) : 0;
-    // park layout: W | m | v | dW | W16.  The bf16 shadow travels on the HBM /
-    // NVLink tiers (a copy-engine copy is cheaper than regenerating it on the
-    // SMs); over PCIe it is regenerated from W on activation instead.
-    const bool park_w16 = a->W16 && tier != FM_TIER_HOST;
-    const size_t bytes = P * 16 + P * dw_elem(a) + (a->W16 ? P * 2 + a->D * 4 : 0);
-    const int pdev = tier == FM_TIER_PEER ? peer_device : c->device;
+// Park layout: W | m | v | dW | W16 | colmax keys.
+static size_t park_bytes_for(const fm_agent* a) {
+    return a->P * 16 + a->P * dw_elem(a) + (a->W16 ? a->P * 2 + a->D * 4 : 0);
+}
+
+// Parking buffer of `bytes` on `tier` (device pdev), reused while it fits.
+static int park_reserve(fm_agent* a, fm_ctx* c, int tier, int pdev, size_t bytes) {
     if (a->park && (a->park_tier != tier || a->park_device != pdev || a->park_bytes < bytes)) {
         FM_CUDA(cudaStreamSynchronize(c->copy_out));
         if (a->park_tier == FM_TIER_HOST) cudaFreeHost(a->park);
@@ -1530,6 +1559,30 @@ int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
         a->park_device = pdev;
         a->park_bytes = bytes;
     }
+    return FM_OK;
+}
+
+int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
+    FM_GUARD_BEGIN
+    // a K-GEMM1 launched after the agent's last op (e.g. the next agent's first
+    // micro-batch) is a safe and cheap start for the copy-out: the copy engines then
+    // overlap tensor-bound GEMMs instead of the latency-bound K-gather that follows
+    // the end of the currently queued work (measured: K-gather 16 us -> 390 us
+    // beside a 2.4 GB D2D copy)
+    const bool gated = a->active && a->ctx && a->ctx->gemm_seq > a->last_seq;
+    if (int st = check_active(a)) return st;
+    if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang (fm_gang_detach first)");
+    fm_ctx* c = a->ctx;
+    if (int st = set_dev(c)) return st;
+    const size_t P = a->P;
+    const size_t dwb = a->dw_valid ? P * dw_elem(a) : 0;
+    // park layout: W | m | v | dW | W16.  The bf16 shadow travels on the HBM /
+    // NVLink tiers (a copy-engine copy is cheaper than regenerating it on the
+    // SMs); over PCIe it is regenerated from W on activation instead.
+    const bool park_w16 = a->W16 && tier != FM_TIER_HOST;
+    const size_t bytes = park_bytes_for(a);
+    const int pdev = tier == FM_TIER_PEER ? peer_device : c->device;
+    if (int st = park_reserve(a, c, tier, pdev, bytes)) return st;
     // order the copy-out after everything the agent has queued on the compute stream
     if (gated) {
         FM_CUDA(cudaStreamWaitEvent(c->copy_out, c->ev_gemm, 0));

@@ -367,8 +367,15 @@ __global__ void __launch_bounds__(256) adam_kernel(double* __restrict__ w, float
                                                    __nv_bfloat16* __restrict__ w16, uint64_t n,
                                                    double lr, double b1, double b2, double eps,
                                                    double bc1, double bc2, int zero_grad, double* gsq,
-                                                   int* __restrict__ cm, uint64_t D) {
+                                                   int* __restrict__ cm, uint64_t D, double* w_o, float* m_o,
+                                                   float* v_o) {
     __shared__ double red[8];
+    // outputs: in place, or the parking buffer (fused swap-out)
+    if (!w_o) {
+        w_o = w;
+        m_o = m;
+        v_o = v;
+    }
     double acc = 0.0;
     // colmax fused (cm != null): the launcher sized the grid so that a thread's four
     // elements sit in the same four columns on every iteration
@@ -397,9 +404,9 @@ __global__ void __launch_bounds__(256) adam_kernel(double* __restrict__ w, float
         acc += adam_one(wv.y, mv.y, vv.y, gv[1], lr, b1, b2, eps, bc1, bc2);
         acc += adam_one(wv.z, mv.z, vv.z, gv[2], lr, b1, b2, eps, bc1, bc2);
         acc += adam_one(wv.w, mv.w, vv.w, gv[3], lr, b1, b2, eps, bc1, bc2);
-        reinterpret_cast<double4*>(w)[i] = wv;
-        reinterpret_cast<float4*>(m)[i] = mv;
-        reinterpret_cast<float4*>(v)[i] = vv;
+        reinterpret_cast<double4*>(w_o)[i] = wv;
+        reinterpret_cast<float4*>(m_o)[i] = mv;
+        reinterpret_cast<float4*>(v_o)[i] = vv;
         if (w16) {
             __nv_bfloat162 lo = __floats2bfloat162_rn(static_cast<float>(wv.x), static_cast<float>(wv.y));
             __nv_bfloat162 hi = __floats2bfloat162_rn(static_cast<float>(wv.z), static_cast<float>(wv.w));
@@ -424,8 +431,13 @@ __global__ void __launch_bounds__(256) adam_kernel(double* __restrict__ w, float
     const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (gid < n - n4 * 4) {
         const uint64_t i = n4 * 4 + gid;
-        acc += adam_one(w[i], m[i], v[i], g[i], lr, b1, b2, eps, bc1, bc2);
-        if (w16) w16[i] = __float2bfloat16_rn(static_cast<float>(w[i]));
+        double wi = w[i];
+        float mi = m[i], vi = v[i];
+        acc += adam_one(wi, mi, vi, g[i], lr, b1, b2, eps, bc1, bc2);
+        w_o[i] = wi;
+        m_o[i] = mi;
+        v_o[i] = vi;
+        if (w16) w16[i] = __float2bfloat16_rn(static_cast<float>(wi));
         if (zero_grad) g[i] = G(0);
     }
     if (cm) {
@@ -691,7 +703,7 @@ cudaError_t launch_softmax_grad(const CUtensorMap& tmP, const CUtensorMap& tmGt,
 template <typename G>
 cudaError_t launch_adam(double* w, float* m, float* v, G* g, __nv_bfloat16* w16, uint64_t n, double lr, double b1,
                         double b2, double eps, double bc1, double bc2, int zero_grad, double* gsq, int num_sms,
-                        cudaStream_t s, int* colmax, uint64_t D, bool* colmax_done) {
+                        cudaStream_t s, int* colmax, uint64_t D, bool* colmax_done, const AdamDst* dst) {
     if (colmax_done) *colmax_done = false;
     if (n == 0) return cudaSuccess;
     if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g)) & 31) return cudaErrorMisalignedAddress;
@@ -716,17 +728,19 @@ cudaError_t launch_adam(double* w, float* m, float* v, G* g, __nv_bfloat16* w16,
             blocks = want < cap ? want : cap;
         }
     }
+    if (dst && (reinterpret_cast<uintptr_t>(dst->w) & 31)) return cudaErrorMisalignedAddress;
     adam_kernel<G><<<static_cast<int>(blocks), 256, 0, s>>>(w, m, v, g, w16, n, lr, b1, b2, eps, bc1, bc2, zero_grad,
-                                                            gsq, cm, D);
+                                                            gsq, cm, D, dst ? dst->w : nullptr,
+                                                            dst ? dst->m : nullptr, dst ? dst->v : nullptr);
     if (colmax_done) *colmax_done = cm != nullptr;
     return cudaGetLastError();
 }
 template cudaError_t launch_adam<float>(double*, float*, float*, float*, __nv_bfloat16*, uint64_t, double, double,
                                         double, double, double, double, int, double*, int, cudaStream_t, int*,
-                                        uint64_t, bool*);
+                                        uint64_t, bool*, const AdamDst*);
 template cudaError_t launch_adam<double>(double*, float*, float*, double*, __nv_bfloat16*, uint64_t, double,
                                          double, double, double, double, double, int, double*, int, cudaStream_t,
-                                         int*, uint64_t, bool*);
+                                         int*, uint64_t, bool*, const AdamDst*);
 
 cudaError_t launch_adam_shard(double* w, float* m, float* v, const float* g, const float* recv, int nslots,
                               uint64_t slot_stride, __nv_bfloat16* w16, ShardPeers peers, uint64_t n, double lr,

@@ -463,3 +463,53 @@ def test_gemm2_stream_k_tail(ctx, monkeypatch, V, D_, resp):
     ref = orc.sparse_grad(V, D_, agent_seed(2048, "sk"), samples, adv, 64)
     assert rel_fro(g_sk[:, ref["cols"]], ref["grad"]) <= 2e-2
     assert abs(n_sk - ref["mb_grad_norm"]) <= 2e-2 * ref["mb_grad_norm"]
+
+
+def test_update_park_equals_update_then_suspend(ctx):
+    """fm_apply_update_park (K-adam writes W/m/v/W16/colmax straight into the
+    parking buffer) == fm_apply_update + fm_agent_suspend(device): after
+    re-activation the state checksums (W, m, v, W16), weights, moments and the
+    next step's gradient are bit-identical, and equal the resident run's."""
+    from paper_2602_09578_b200.engine import TrainingEngine
+    L = _lib.lib()
+    V, D_ = 2048, 256
+    rng = np.random.default_rng(5)
+    batches = [[([int(x) for x in rng.integers(0, V, size=8)], [int(x) for x in rng.integers(0, V, size=12)])
+                for _ in range(16)] for _ in range(8)]
+    adv = [rng.normal(size=16) for _ in range(8)]
+
+    def run(mode):
+        eng = TrainingEngine([ctx], global_batch=64, precision=_lib.PRECISION_BF16_TC)
+        try:
+            eng.add_agent("p", V, D_)
+            eng.activate("p")
+            eng.run()
+            h = eng.handle("p")
+            for step in range(2):
+                for b in range(4):
+                    k = step * 4 + b
+                    arr = (_lib.fm_sample * 16)(*[_lib.fm_sample(ctx.put(orc.encode(p)), ctx.put(orc.encode(r)), a)
+                                                  for (p, r), a in zip(batches[k], adv[k])])
+                    t = C.c_int64()
+                    _lib.check(L.fm_train_micro_batch(h, arr, 16, 64, C.byref(t)))
+                if mode == "park" and step == 0:
+                    _lib.check(L.fm_apply_update_park(h, 64, 1e-3, 0.9, 0.999, 1e-8, None, None))
+                    assert L.fm_agent_is_active(h) == 0
+                else:
+                    _lib.check(L.fm_apply_update(h, 64, 1e-3, 0.9, 0.999, 1e-8, None, None))
+                    if mode == "copy" and step == 0:
+                        _lib.check(L.fm_agent_suspend(h, _lib.TIER_DEVICE, -1))
+                if mode != "resident" and step == 0:
+                    _lib.check(L.fm_agent_activate(h, ctx.handle))
+            cs = C.c_uint64()
+            _lib.check(L.fm_agent_state_checksum(h, C.byref(cs)))
+            W = np.empty(V * D_, dtype=np.float64)
+            _lib.check(L.fm_agent_read_weights(h, W.ctypes.data))
+            return cs.value, W
+        finally:
+            eng.close()
+
+    park, copy, res = run("park"), run("copy"), run("resident")
+    assert park[0] == copy[0] == res[0]
+    np.testing.assert_array_equal(park[1], res[1])
+    assert np.any(park[1] != seeded_weights(V, D_, agent_seed(2048, "p")).reshape(-1))
