@@ -513,3 +513,31 @@ def test_update_park_equals_update_then_suspend(ctx):
     assert park[0] == copy[0] == res[0]
     np.testing.assert_array_equal(park[1], res[1])
     assert np.any(park[1] != seeded_weights(V, D_, agent_seed(2048, "p")).reshape(-1))
+
+
+def test_update_park_and_read_cols_error_paths(ctx):
+    """fm_apply_update_park keeps the reference's update errors (IncompleteBatch
+    before anything changes) and refuses a parity-mode agent; the agent stays
+    active and usable after a refused call.  fm_agent_read_grad_cols rejects
+    out-of-range columns."""
+    from paper_2602_09578_b200.engine import TrainingEngine
+    L = _lib.lib()
+    eng = TrainingEngine([ctx], global_batch=64, precision=_lib.PRECISION_PARITY_F64)
+    try:
+        eng.add_agent("e", 64, 16)
+        eng.activate("e")
+        eng.run()
+        h = eng.handle("e")
+        assert L.fm_apply_update_park(h, 64, 1e-3, 0.9, 0.999, 1e-8, None, None) == 25  # IncompleteBatch
+        arr = (_lib.fm_sample * 64)(*[_lib.fm_sample(ctx.put(orc.encode([1, 2, 3])), ctx.put(orc.encode([4, 5])), 0.5)
+                                      for _ in range(64)])
+        t = C.c_int64()
+        _lib.check(L.fm_train_micro_batch(h, arr, 64, 64, C.byref(t)))
+        assert L.fm_apply_update_park(h, 64, 1e-3, 0.9, 0.999, 1e-8, None, None) == _lib.FM_ERR_INVALID_ARG
+        assert L.fm_agent_is_active(h) == 1
+        cols = np.array([0, 16], dtype=np.int64)
+        out = np.zeros(64 * 2)
+        assert L.fm_agent_read_grad_cols(h, cols.ctypes.data, 2, out.ctypes.data) == _lib.FM_ERR_INVALID_ARG
+        _lib.check(L.fm_apply_update(h, 64, 1e-3, 0.9, 0.999, 1e-8, None, None))
+    finally:
+        eng.close()
