@@ -1,4 +1,5 @@
 #!/bin/bash
+# (experiment record: the FM_G1_POL / FM_G2_POL knobs it sets were removed after the sweep)
 # L2 eviction-priority x raster sweep at C2 (1 agent resident): one GEMM1 + one
 # GEMM2 launch under ncu (DRAM bytes, duration, SM clock) per configuration.
 set -u
