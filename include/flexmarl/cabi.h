@@ -134,6 +134,9 @@ int fm_agent_read_grad(fm_agent* a, double* g_out);
 /* selected feature columns of the gradient accumulator, [V][n_cols] row-major as f64
  * (parity tooling at full V x D, where reading all V*D is host-memory heavy) */
 int fm_agent_read_grad_cols(fm_agent* a, const int64_t* cols, int64_t n_cols, double* g_out);
+/* kernel test hook (device pointers): C[M][N] fp32 = sum_k A(m,k) B(n,k) through the
+ * tcgen05 CTA-pair GEMM, A/B K-major ([M][K] / [N][K]) or MN-major ([K][M] / [K][N]) */
+int fm_debug_gemm(fm_ctx* c, const void* A, const void* B, int a_mn, int b_mn, int M, int N, int K, float* C);
 int64_t fm_agent_version(const fm_agent* a);
 int64_t fm_agent_samples_accumulated(const fm_agent* a);
 int fm_agent_is_active(const fm_agent* a);

@@ -74,6 +74,8 @@ bool gemm_pair_mode();
 size_t gemm_smem_bytes();
 // Rows of B per TMA box: 256 (single-CTA tiles) or 128 (CTA-pair tiles, FM_GEMM_2SM != 0).
 uint32_t gemm_b_box_rows();
+cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, int a_mn, int b_mn, int M, int N,
+                              int K, float* C, int num_sms, cudaStream_t stream);
 cudaError_t gemm_tn_launch(GemmKind kind, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const GemmArgs& args, int num_sms, cudaStream_t stream);
 

@@ -196,6 +196,20 @@ __device__ __forceinline__ uint64_t umma_desc_k_sw128(uint32_t smem_addr) {
     return d;
 }
 
+// UMMA shared-memory descriptor, MN-major operand with SWIZZLE_128B: atoms of
+// 64 MN-contiguous bf16 (one 128-B row) x 8 K rows (1024 B), as TMA writes a
+// box {64 (MN), rows (K)}.  LBO = byte stride between 64-element MN atoms,
+// SBO = byte stride between 8-row K atoms (1024 B inside one box).
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t smem_addr, uint32_t lbo_bytes) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+
 // ---- clusters / CTA pairs (cta_group::2) ----------------------------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;
@@ -261,14 +275,15 @@ __device__ __forceinline__ void umma_commit_2sm(uint64_t* bar, uint16_t mask) {
         : "memory");
 }
 
-// Instruction descriptor, kind::f16: bf16 A/B, fp32 D, both K-major.
-template <int M, int N>
+// Instruction descriptor, kind::f16: bf16 A/B, fp32 D; A/B K-major unless
+// a_mn / b_mn (MN-major operand).
+template <int M, int N, bool a_mn = false, bool b_mn = false>
 __host__ __device__ constexpr uint32_t idesc_bf16_f32() {
     return (1u << 4)          // D format f32
            | (1u << 7)        // A format bf16
            | (1u << 10)       // B format bf16
-           | (0u << 15)       // A K-major
-           | (0u << 16)       // B K-major
+           | ((a_mn ? 1u : 0u) << 15)
+           | ((b_mn ? 1u : 0u) << 16)
            | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 

@@ -976,6 +976,23 @@ int fm_agent_read_grad(fm_agent* a, double* g) {
     FM_GUARD_END
 }
 
+int fm_debug_gemm(fm_ctx* c, const void* A, const void* B, int a_mn, int b_mn, int M, int N, int K, float* C) {
+    FM_GUARD_BEGIN
+    if (!c || !A || !B || !C || M <= 0 || N <= 0 || K <= 0 || M % 8 || N % 8 || K % 8)
+        return fail(FM_ERR_INVALID_ARG, "debug_gemm: bad arguments");
+    if (!gemm_pair_mode()) return fail(FM_ERR_CONFIG_ERROR, "debug_gemm needs the CTA-pair kernels");
+    if (int st = set_dev(c)) return st;
+    CUtensorMap tA, tB;
+    const bool ok = (a_mn ? make_tmap_bf16_kmajor(&tA, A, K, M, 64) : make_tmap_bf16_kmajor(&tA, A, M, K, kGemmBM)) &&
+                    (b_mn ? make_tmap_bf16_kmajor(&tB, B, K, N, 64)
+                          : make_tmap_bf16_kmajor(&tB, B, N, K, gemm_b_box_rows()));
+    if (!ok) return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    FM_CUDA(gemm_debug_launch(tA, tB, a_mn, b_mn, M, N, K, C, c->num_sms, c->stream));
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    return FM_OK;
+    FM_GUARD_END
+}
+
 int fm_agent_read_grad_cols(fm_agent* a, const int64_t* cols, int64_t n_cols, double* g) {
     FM_GUARD_BEGIN
     if (int st = check_active(a)) return st;

@@ -508,14 +508,17 @@ constexpr int P_STAGES = 6;
 constexpr uint32_t P_A_STAGE = 128 * BK * 2;    // 16 KB: this CTA's 128 rows of A
 constexpr uint32_t P_B_STAGE = 128 * BK * 2;    // 16 KB: this CTA's half of B's 256 rows
 constexpr uint32_t P_STAGE_BYTES = P_A_STAGE + P_B_STAGE;
-constexpr uint32_t kIdesc2 = idesc_bf16_f32<256, BN>();
 
 constexpr int kThreadsPair = 192;  // w0 TMA, w1 MMA, w2-5 epilogue
 
-template <class Epi>
+// kAmn / kBmn: operand stored MN-major in HBM ([K][M] / [K][N], MN contiguous);
+// each CTA's 128 MN x 64 K stage slice is then two TMA boxes {64 MN, 64 K}
+// (8 KB each, the second at +8 KB = the descriptor's LBO).
+template <class Epi, bool kAmn = false, bool kBmn = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     gemm_tn_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        GemmArgs args) {
+    constexpr uint32_t kId = idesc_bf16_f32<256, BN, kAmn, kBmn>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -575,8 +578,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                     mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t fb = mapa_shared(&full[stage], 0);
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
-                    tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, args.k0 + k * BK, arow, pol);
-                    tma_load_2d_2sm(sB + stage * P_B_STAGE, &tmB, fb, args.k0 + k * BK, brow, pol);
+                    const int kc = args.k0 + k * BK;
+                    if constexpr (kAmn) {
+                        tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, arow, kc, pol);
+                        tma_load_2d_2sm(sA + stage * P_A_STAGE + 8192, &tmA, fb, arow + 64, kc, pol);
+                    } else {
+                        tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, kc, arow, pol);
+                    }
+                    if constexpr (kBmn) {
+                        tma_load_2d_2sm(sB + stage * P_B_STAGE, &tmB, fb, brow, kc, pol);
+                        tma_load_2d_2sm(sB + stage * P_B_STAGE + 8192, &tmB, fb, brow + 64, kc, pol);
+                    } else {
+                        tma_load_2d_2sm(sB + stage * P_B_STAGE, &tmB, fb, kc, brow, pol);
+                    }
                     if (++stage == P_STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -599,12 +613,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                 for (int k = wi.kb; k < wi.ke; ++k) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint64_t adesc = umma_desc_k_sw128(smem_u32(sA + stage * P_A_STAGE));
-                    const uint64_t bdesc = umma_desc_k_sw128(smem_u32(sB + stage * P_B_STAGE));
+                    // K-major: 16 bf16 = 32 B along the swizzle row; MN-major: 16 K rows = 2 KB
+                    const uint64_t adesc = kAmn ? umma_desc_mn_sw128(smem_u32(sA + stage * P_A_STAGE), 8192)
+                                                : umma_desc_k_sw128(smem_u32(sA + stage * P_A_STAGE));
+                    const uint64_t bdesc = kBmn ? umma_desc_mn_sw128(smem_u32(sB + stage * P_B_STAGE), 8192)
+                                                : umma_desc_k_sw128(smem_u32(sB + stage * P_B_STAGE));
+                    constexpr uint64_t a_step = kAmn ? 2048 >> 4 : 2;
+                    constexpr uint64_t b_step = kBmn ? 2048 >> 4 : 2;
 #pragma unroll
                     for (int kk = 0; kk < BK / 16; ++kk)
-                        umma_bf16_2sm(d_tmem, adesc + static_cast<uint64_t>(kk * 2),
-                                      bdesc + static_cast<uint64_t>(kk * 2), kIdesc2, (k != wi.kb || kk != 0));
+                        umma_bf16_2sm(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, kId,
+                                      (k != wi.kb || kk != 0));
                     umma_commit_2sm(&empty[stage], 0x3);
                     if (++stage == P_STAGES) {
                         stage = 0;
@@ -752,6 +771,33 @@ bool use_pair_mma() {
 }
 
 }  // namespace
+
+// Test hook: C[M][N] (fp32, ld N) = sum_k A(m,k) B(n,k) with A / B either K-major
+// ([M][K] / [N][K]) or MN-major ([K][M] / [K][N]) — validates the MN-major UMMA
+// operand path against a plain reference (tests/test_gpu_path.py).
+cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, int a_mn, int b_mn, int M, int N,
+                              int K, float* C, int num_sms, cudaStream_t stream) {
+    GemmArgs args{};
+    args.M = M;
+    args.N = N;
+    args.K = K;
+    args.group_m = 8;
+    args.out = C;
+    args.ld_out = N;
+    const size_t smem = gemm_smem_bytes();
+    const int tiles = ((M + 255) / 256) * ((N + BN - 1) / BN);
+    const int pairs = num_sms / 2;
+    const int grid = 2 * (tiles < pairs ? tiles : pairs);
+    auto launch = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        kern<<<grid, kThreadsPair, smem, stream>>>(tmA, tmB, args);
+    };
+    if (a_mn && b_mn) launch(gemm_tn_2sm_kernel<GradEpi, true, true>);
+    else if (a_mn) launch(gemm_tn_2sm_kernel<GradEpi, true, false>);
+    else if (b_mn) launch(gemm_tn_2sm_kernel<GradEpi, false, true>);
+    else launch(gemm_tn_2sm_kernel<GradEpi, false, false>);
+    return cudaGetLastError();
+}
 
 // Loss-fold path (default; FM_LOSS_FOLD=0 restores the separate K-loss pass).
 bool loss_fold_enabled() {

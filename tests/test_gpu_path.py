@@ -541,3 +541,22 @@ def test_update_park_and_read_cols_error_paths(ctx):
         _lib.check(L.fm_apply_update(h, 64, 1e-3, 0.9, 0.999, 1e-8, None, None))
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (1, 0), (0, 1), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(512, 512, 256), (384, 768, 448)])
+def test_tcgen05_gemm_operand_majorness(ctx, a_mn, b_mn, M, N, K):
+    """The CTA-pair tcgen05 GEMM with K-major ([M][K] / [N][K]) or MN-major
+    ([K][M] / [K][N]) bf16 operands (SWIZZLE_128B smem descriptors) against a
+    torch fp32 product of the same bf16 values."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M + N + K + 2 * a_mn + b_mn)
+    a = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    b = torch.randn(N, K, device="cuda", generator=g).bfloat16()
+    A = a.t().contiguous() if a_mn else a
+    B = b.t().contiguous() if b_mn else b
+    C_ = torch.empty(M, N, device="cuda", dtype=torch.float32)
+    _lib.check(_lib.lib().fm_debug_gemm(ctx.handle, A.data_ptr(), B.data_ptr(), a_mn, b_mn, M, N, K, C_.data_ptr()))
+    ref = a.float() @ b.float().t()
+    err = (C_ - ref).norm() / ref.norm()
+    assert float(err) < 1e-5
