@@ -137,6 +137,11 @@ int fm_agent_read_grad_cols(fm_agent* a, const int64_t* cols, int64_t n_cols, do
 /* kernel test hook (device pointers): C[M][N] fp32 = sum_k A(m,k) B(n,k) through the
  * tcgen05 CTA-pair GEMM, A/B K-major ([M][K] / [N][K]) or MN-major ([K][M] / [K][N]) */
 int fm_debug_gemm(fm_ctx* c, const void* A, const void* B, int a_mn, int b_mn, int M, int N, int K, float* C);
+/* kernel test hook (device pointers): C[M][N] = sum over the K list of column tile
+ * n/256 of A[t][m] * B[t][n]; A [rows][M], B [rows][N] bf16 gathered by TMA gather4;
+ * klist [N/256][klist_ld] row indices, klist_iters [N/256] = list length / 64 */
+int fm_debug_gemm_klist(fm_ctx* c, const void* A, const void* B, const int32_t* klist, long long klist_ld,
+                        const int32_t* klist_iters, int rows, int M, int N, float* C);
 int64_t fm_agent_version(const fm_agent* a);
 int64_t fm_agent_samples_accumulated(const fm_agent* a);
 int fm_agent_is_active(const fm_agent* a);

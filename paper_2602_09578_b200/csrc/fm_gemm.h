@@ -61,6 +61,13 @@ struct GemmArgs {
     // each tile half runs the epilogue from it (sk_cnt[tile*2 + rank], self-resetting).
     float* sk_ws = nullptr;
     int* sk_cnt = nullptr;
+    // Grad, K-list (token-list) mode: output column tile nb sums only over the K rows
+    // klist[nb * klist_ld + 0 .. 64 * klist_iters[nb]) (row indices, padded with a
+    // zero row); both operands row-major [rows][M] / [rows][N] (MN-major),
+    // gathered four rows per TMA gather4.
+    const int32_t* klist = nullptr;
+    long long klist_ld = 0;
+    const int32_t* klist_iters = nullptr;
 };
 
 // Stream-K workspace capacity: at most 2*pairs-1 split tiles (148 SMs -> 74 pairs).
@@ -76,6 +83,11 @@ size_t gemm_smem_bytes();
 uint32_t gemm_b_box_rows();
 cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, int a_mn, int b_mn, int M, int N,
                               int K, float* C, int num_sms, cudaStream_t stream);
+// Grad GEMM over per-column-tile K lists (args.klist*), gather4 maps for A and B.
+cudaError_t gemm_klist_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int num_sms,
+                              cudaStream_t stream);
+// 2-D bf16 map over [rows][cols] with box {64, 1}, SWIZZLE_128B (TMA gather4).
+bool make_tmap_gather4(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols);
 cudaError_t gemm_tn_launch(GemmKind kind, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const GemmArgs& args, int num_sms, cudaStream_t stream);
 

@@ -244,6 +244,19 @@ __device__ __forceinline__ void tma_load_2d_2sm(void* smem_dst, const CUtensorMa
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster_addr), "r"(c0), "r"(c1), "l"(policy)
         : "memory");
 }
+// TMA gather4 (CTA pair): rows r.x..r.w (outer coordinate) x box-width columns
+// from col c0 of a 2-D map with box {64, 1}, written as four consecutive
+// 128-B rows at smem_dst (SWIZZLE_128B applied by smem address); completes on
+// the leader CTA's barrier like tma_load_2d_2sm.
+__device__ __forceinline__ void tma_gather4_2sm(void* smem_dst, const CUtensorMap* map, uint32_t bar_cluster_addr,
+                                                int32_t c0, int4 r, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster_addr), "r"(c0), "r"(r.x), "r"(r.y), "r"(r.z),
+        "r"(r.w), "l"(policy)
+        : "memory");
+}
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc_2sm(uint32_t* dst_smem) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),

@@ -86,6 +86,18 @@ bool make_tmap_bf16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, ui
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool make_tmap_gather4(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols) {
+    EncodeTiledFn f = encode_fn();
+    if (!f) return false;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint32_t box[2] = {64, 1};
+    const cuuint32_t estr[2] = {1, 1};
+    return f(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, uint32_t elem_bytes, uint64_t rows,
                   uint64_t cols, uint32_t box_rows, uint32_t box_cols) {
     EncodeTiledFn f = encode_fn();
@@ -988,6 +1000,33 @@ int fm_debug_gemm(fm_ctx* c, const void* A, const void* B, int a_mn, int b_mn, i
                           : make_tmap_bf16_kmajor(&tB, B, N, K, gemm_b_box_rows()));
     if (!ok) return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     FM_CUDA(gemm_debug_launch(tA, tB, a_mn, b_mn, M, N, K, C, c->num_sms, c->stream));
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    return FM_OK;
+    FM_GUARD_END
+}
+
+int fm_debug_gemm_klist(fm_ctx* c, const void* A, const void* B, const int32_t* klist, long long klist_ld,
+                        const int32_t* klist_iters, int rows, int M, int N, float* C) {
+    FM_GUARD_BEGIN
+    if (!c || !A || !B || !C || !klist || !klist_iters || M <= 0 || N <= 0 || rows <= 0 || M % 8 || N % 8 ||
+        klist_ld % 64)
+        return fail(FM_ERR_INVALID_ARG, "debug_gemm_klist: bad arguments");
+    if (!gemm_pair_mode()) return fail(FM_ERR_CONFIG_ERROR, "debug_gemm_klist needs the CTA-pair kernels");
+    if (int st = set_dev(c)) return st;
+    CUtensorMap tA, tB;
+    if (!make_tmap_gather4(&tA, A, rows, M) || !make_tmap_gather4(&tB, B, rows, N))
+        return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    GemmArgs g{};
+    g.M = M;
+    g.N = N;
+    g.K = 64;
+    g.group_m = 1;
+    g.out = C;
+    g.ld_out = N;
+    g.klist = klist;
+    g.klist_ld = klist_ld;
+    g.klist_iters = klist_iters;
+    FM_CUDA(gemm_klist_launch(tA, tB, g, c->num_sms, c->stream));
     FM_CUDA(cudaStreamSynchronize(c->stream));
     return FM_OK;
     FM_GUARD_END

@@ -514,10 +514,13 @@ constexpr int kThreadsPair = 192;  // w0 TMA, w1 MMA, w2-5 epilogue
 // kAmn / kBmn: operand stored MN-major in HBM ([K][M] / [K][N], MN contiguous);
 // each CTA's 128 MN x 64 K stage slice is then two TMA boxes {64 MN, 64 K}
 // (8 KB each, the second at +8 KB = the descriptor's LBO).
-template <class Epi, bool kAmn = false, bool kBmn = false>
+// kKList (Grad): both operands MN-major row-major [rows][.] gathered with TMA
+// gather4 from the output column tile's K list (args.klist*).
+template <class Epi, bool kAmn = false, bool kBmn = false, bool kKList = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     gemm_tn_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        GemmArgs args) {
+    static_assert(!kKList || (kAmn && kBmn), "K-list operands are MN-major");
     constexpr uint32_t kId = idesc_bf16_f32<256, BN, kAmn, kBmn>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -563,7 +566,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     const int nclusters = gridDim.x >> 1;
     const Sched sch(num_tiles, k_iters, nclusters, std::is_same_v<Epi, GradEpi> && args.sk_ws != nullptr);
 
-    if (warp == 0) {
+    if (warp == 0 && kKList) {
+        // ===== TMA gather producer (both CTAs; lanes 0-15 each gather one row quad) =====
+        const uint64_t pol = policy_evict_last();
+        int stage = 0;
+        uint32_t phase = 0;
+        WorkItem wi;
+        for (int w = 0; sch.get(cid, w, wi); ++w) {
+            const TileCoord tc = tile_coord(wi.tile, tiles_m, tiles_n, args.group_m);
+            const int ke = __ldg(args.klist_iters + tc.nb);
+            const int arow = tc.mb * 256 + static_cast<int>(rank) * 128;
+            const int brow = tc.nb * BN + static_cast<int>(rank) * 128;
+            const int32_t* lst = args.klist + static_cast<size_t>(tc.nb) * args.klist_ld;
+            for (int k = 0; k < ke; ++k) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                const uint32_t fb = mapa_shared(&full[stage], 0);
+                if (leader && lane == 0) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+                if (lane < 16) {
+                    const int4 t4 = __ldg(reinterpret_cast<const int4*>(lst + k * BK) + lane);
+                    uint8_t* a0 = sA + stage * P_A_STAGE + lane * 512;
+                    uint8_t* b0 = sB + stage * P_B_STAGE + lane * 512;
+                    tma_gather4_2sm(a0, &tmA, fb, arow, t4, pol);
+                    tma_gather4_2sm(a0 + 8192, &tmA, fb, arow + 64, t4, pol);
+                    tma_gather4_2sm(b0, &tmB, fb, brow, t4, pol);
+                    tma_gather4_2sm(b0 + 8192, &tmB, fb, brow + 64, t4, pol);
+                }
+                __syncwarp();
+                if (++stage == P_STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 0) {
         // ===== TMA producer (both CTAs) =====
         if (elect_one()) {
             const uint64_t pol = policy_evict_last();
@@ -607,6 +642,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             uint32_t acc_phase = 0;
             WorkItem wi;
             for (int w = 0; sch.get(cid, w, wi); ++w) {
+                if constexpr (kKList)
+                    wi.ke = __ldg(args.klist_iters + tile_coord(wi.tile, tiles_m, tiles_n, args.group_m).nb);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -796,6 +833,19 @@ cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, in
     else if (a_mn) launch(gemm_tn_2sm_kernel<GradEpi, true, false>);
     else if (b_mn) launch(gemm_tn_2sm_kernel<GradEpi, false, true>);
     else launch(gemm_tn_2sm_kernel<GradEpi, false, false>);
+    return cudaGetLastError();
+}
+
+cudaError_t gemm_klist_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int num_sms,
+                              cudaStream_t stream) {
+    const size_t smem = gemm_smem_bytes();
+    const int tiles = ((args.M + 255) / 256) * ((args.N + BN - 1) / BN);
+    if (tiles == 0) return cudaSuccess;
+    const int pairs = num_sms / 2;
+    const int grid = 2 * (tiles < pairs ? tiles : pairs);
+    auto k = gemm_tn_2sm_kernel<GradEpi, true, true, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k<<<grid, kThreadsPair, smem, stream>>>(tmA, tmB, args);
     return cudaGetLastError();
 }
 

@@ -560,3 +560,42 @@ def test_tcgen05_gemm_operand_majorness(ctx, a_mn, b_mn, M, N, K):
     ref = a.float() @ b.float().t()
     err = (C_ - ref).norm() / ref.norm()
     assert float(err) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,rows,seed", [(512, 512, 300, 0), (384, 1024, 1000, 1), (256, 256, 64, 2)])
+def test_tcgen05_gemm_token_lists(ctx, M, N, rows, seed):
+    """K-list GEMM (TMA gather4 of four K rows per lane, MN-major operands): each
+    256-wide output column tile sums over its own list of K rows, padded to a
+    multiple of 64 with a zero row — against torch on the same bf16 values.
+    Lists of different lengths (incl. one padded-only list) per tile."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    A = torch.randn(rows + 1, M, device="cuda", generator=g).bfloat16()
+    B = torch.randn(rows + 1, N, device="cuda", generator=g).bfloat16()
+    A[rows] = 0
+    B[rows] = 0
+    nt = N // 256
+    rng = np.random.default_rng(seed)
+    lists = []
+    for j in range(nt):
+        k = 0 if (j == 1 and nt > 2) else int(rng.integers(1, rows))
+        lists.append(np.sort(rng.choice(rows, size=k, replace=False)).astype(np.int32))
+    ld = int(np.ceil(max(max(len(l) for l in lists), 1) / 64) * 64)
+    kl = np.full((nt, ld), rows, dtype=np.int32)
+    iters = np.zeros(nt, dtype=np.int32)
+    for j, l in enumerate(lists):
+        kl[j, :len(l)] = l
+        iters[j] = max(1, int(np.ceil(len(l) / 64)))
+    klist = torch.tensor(kl, device="cuda")
+    kit = torch.tensor(iters, device="cuda")
+    C_ = torch.full((M, N), float("nan"), device="cuda", dtype=torch.float32)
+    _lib.check(_lib.lib().fm_debug_gemm_klist(ctx.handle, A.data_ptr(), B.data_ptr(), klist.data_ptr(), ld,
+                                              kit.data_ptr(), rows + 1, M, N, C_.data_ptr()))
+    ref = torch.zeros(M, N, device="cuda")
+    for j, l in enumerate(lists):
+        if len(l):
+            idx = torch.tensor(l, device="cuda", dtype=torch.long)
+            ref[:, 256 * j:256 * (j + 1)] = A[idx].float().t() @ B[idx][:, 256 * j:256 * (j + 1)].float()
+    assert not torch.isnan(C_).any()
+    err = (C_ - ref).norm() / ref.norm()
+    assert float(err) < 1e-5
