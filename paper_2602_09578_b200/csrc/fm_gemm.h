@@ -87,7 +87,7 @@ cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, in
 cudaError_t gemm_klist_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int num_sms,
                               cudaStream_t stream);
 // 2-D bf16 map over [rows][cols] with box {64, 1}, SWIZZLE_128B (TMA gather4).
-bool make_tmap_gather4(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols);
+bool make_tmap_gather4(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch);
 cudaError_t gemm_tn_launch(GemmKind kind, const CUtensorMap& tmA, const CUtensorMap& tmB,
                            const GemmArgs& args, int num_sms, cudaStream_t stream);
 

@@ -51,9 +51,11 @@ struct LseArgs {
     float clip_eps;
     double* loss_acc;  // += objective (nullable)
     int fold;
-    __nv_bfloat16* pexp_t;  // fold: p~^T [V][ldt]
-    __nv_bfloat16* phict;   // fold: Phic^T [D][ldt]
+    __nv_bfloat16* pexp_t;  // fold: p~^T [V][ldt]  (rowmajor: p~ [Mpad][ldt])
+    __nv_bfloat16* phict;   // fold: Phic^T [D][ldt] (rowmajor: Phic [Mpad][ld_phi])
     int64_t ldt;
+    int rowmajor = 0;  // K-list GEMM2: the fold writes go to the row-major operands
+    int64_t ld_phi = 0;
 };
 
 // K-gather: decode the selected records' token payloads straight out of the
@@ -81,13 +83,20 @@ cudaError_t launch_colmax(const __nv_bfloat16* w16, int64_t V, int64_t D, int* k
 cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int64_t M, int64_t Mpad,
                        int64_t V, const SampleDesc* sd, int64_t global_batch, RowBuffers rows,
                        const float* old_logp, float clip_eps, double* loss_acc, __nv_bfloat16* pexp_t,
-                       __nv_bfloat16* phict, int64_t ldt, cudaStream_t s);
+                       __nv_bfloat16* phict, int64_t ldt, cudaStream_t s, int rowmajor = 0, int64_t ld_phi = 0);
 
 // K-loss (fused log-softmax gradient):
 //   G^T[v][t] = coef_eff_t * (delta(v, a_t) - p~[t][v] * exp(m_tile(t, v) - lse_t))
 // p~ tiles (bf16, from GEMM1) streamed in through TMA, G^T tiles stored through TMA.
 cudaError_t launch_softmax_grad(const CUtensorMap& tmP, const CUtensorMap& tmGt, const float2* stats,
                                 int stats_ld, int64_t Mpad, int64_t V, RowBuffers rows, cudaStream_t s);
+
+// K-klist: for every 256-feature column block b of GEMM2, the rows (tokens) whose
+// context touches block b, ascending, padded with zero_row to a multiple of 64
+// (at least 64); iters[b] = padded length / 64.  One block per column block
+// (deterministic block-wide scans).
+cudaError_t launch_klist(const int4* feat4, int64_t M, int nblk, int32_t* klist, int64_t ld, int32_t* iters,
+                         int32_t zero_row, cudaStream_t s);
 
 // Parity tooling: out[v][j] = dW[v][cols[j]] (f32 or f64 accumulator).
 cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D, const int64_t* cols,

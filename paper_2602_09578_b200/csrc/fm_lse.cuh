@@ -112,13 +112,17 @@ __device__ __forceinline__ double lse_row_quad(const LseArgs& L, int64_t r0) {
         // an action outside [0, V) never matches a vocab row (policy.hpp:84-85): the
         // row still gets -c p, just no delta term
         const float sig = ce != 0.f ? __fdividef(-ce, s) : 0.f;
-        if (sl == 4 && sig != 0.f && valid)
-            L.pexp_t[static_cast<size_t>(a) * L.ldt + r] = __float2bfloat16_rn(__expf(za - m) - s);
+        if (sl == 4 && sig != 0.f && valid) {
+            const size_t i = L.rowmajor ? static_cast<size_t>(r) * L.ldt + a : static_cast<size_t>(a) * L.ldt + r;
+            L.pexp_t[i] = __float2bfloat16_rn(__expf(za - m) - s);
+        }
         if (sl < 4) {
             const int f = sl == 0 ? f4.x : sl == 1 ? f4.y : sl == 2 ? f4.z : f4.w;
-            if (f >= 0)
-                L.phict[static_cast<size_t>(f) * L.ldt + r] =
-                    __float2bfloat16_rn(sig * static_cast<float>((c4 >> (8 * sl)) & 0xFFu));
+            if (f >= 0) {
+                const size_t i =
+                    L.rowmajor ? static_cast<size_t>(r) * L.ld_phi + f : static_cast<size_t>(f) * L.ldt + r;
+                L.phict[i] = __float2bfloat16_rn(sig * static_cast<float>((c4 >> (8 * sl)) & 0xFFu));
+            }
         }
     }
     return loss;

@@ -86,11 +86,11 @@ bool make_tmap_bf16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, ui
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool make_tmap_gather4(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols) {
+bool make_tmap_gather4(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch) {
     EncodeTiledFn f = encode_fn();
     if (!f) return false;
     const cuuint64_t dims[2] = {cols, rows};
-    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint64_t strides[1] = {(pitch ? pitch : cols) * 2};
     const cuuint32_t box[2] = {64, 1};
     const cuuint32_t estr[2] = {1, 1};
     return f(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
@@ -134,6 +134,9 @@ struct Workspace {
     float* mrow = nullptr;  // loss fold: per-row softmax offset bound [Mpad]
     unsigned* lse_sync = nullptr;  // fused K-lse: {CTAs arrived, epoch published} (GEMM1 tail)
     unsigned lse_epoch = 0;
+    int32_t* klist = nullptr;  // K-list GEMM2: token lists per 256-feature block [nblk][klist_ld]
+    int32_t* kiters = nullptr;  // [nblk] list length / 64
+    int64_t klist_ld = 0;
     float* sk_ws = nullptr;  // GEMM2 stream-K tail: partial tiles [kSkMaxTiles][256][256] (zero between launches)
     int* sk_cnt = nullptr;   // [kSkMaxTiles][2] arrivals per tile half (self-resetting)
     // parity mode scratch
@@ -309,6 +312,8 @@ void ws_free(Workspace& w) {
     cudaFree(w.mrow);
     cudaFree(w.lse_sync);
     cudaFree(w.sk_ws);
+    cudaFree(w.klist);
+    cudaFree(w.kiters);
     cudaFree(w.sk_cnt);
     cudaFree(w.zscratch);
     cudaFree(w.dWmb);
@@ -355,10 +360,16 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
     e = e ? e : dalloc(&w.logp, R);
     e = e ? e : dalloc(&w.coef_eff, R);
     e = e ? e : dalloc(&w.old_logp, R);
-    e = e ? e : dalloc(&w.phic, static_cast<size_t>(R) * DD);
+    // Phic and p~ carry one extra zero row (index R): the K-list GEMM2's padding row
+    e = e ? e : dalloc(&w.phic, static_cast<size_t>(R + 1) * DD);
+    e = e ? e : cudaMemset(w.phic, 0, static_cast<size_t>(R + 1) * DD * 2);
     e = e ? e : dalloc(&w.phict, static_cast<size_t>(R) * DD);
     e = e ? e : dalloc(&w.gt, static_cast<size_t>(R) * VV);
-    e = e ? e : dalloc(&w.Pexp, static_cast<size_t>(R) * ldz);
+    e = e ? e : dalloc(&w.Pexp, static_cast<size_t>(R + 1) * ldz);
+    e = e ? e : cudaMemset(w.Pexp + static_cast<size_t>(R) * ldz, 0, ldz * 2);
+    w.klist_ld = static_cast<int64_t>(round_up(static_cast<uint64_t>(R), 64) + 64);
+    e = e ? e : dalloc(&w.klist, static_cast<size_t>((DD + 255) / 256) * w.klist_ld);
+    e = e ? e : dalloc(&w.kiters, static_cast<size_t>((DD + 255) / 256));
     e = e ? e : dalloc(&w.zact, R);
     e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n);
     e = e ? e : dalloc(&w.mrow, R);
@@ -1014,7 +1025,7 @@ int fm_debug_gemm_klist(fm_ctx* c, const void* A, const void* B, const int32_t* 
     if (!gemm_pair_mode()) return fail(FM_ERR_CONFIG_ERROR, "debug_gemm_klist needs the CTA-pair kernels");
     if (int st = set_dev(c)) return st;
     CUtensorMap tA, tB;
-    if (!make_tmap_gather4(&tA, A, rows, M) || !make_tmap_gather4(&tB, B, rows, N))
+    if (!make_tmap_gather4(&tA, A, rows, M, M) || !make_tmap_gather4(&tB, B, rows, N, N))
         return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     GemmArgs g{};
     g.M = M;
@@ -1146,6 +1157,10 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 FM_CUDA(cudaMemsetAsync(w.phict, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
             }
             const bool fold = loss_fold_enabled();
+            // K-list GEMM2 (opt-in FM_G2_KLIST=1): each 256-feature column block of the
+            // weight gradient sums only over the tokens whose context touches it
+            const char* kl_env = std::getenv("FM_G2_KLIST");
+            const bool klist = fold && gemm_pair_mode() && kl_env && kl_env[0] == '1';
             if (fold && a->cm_gen != a->w16_gen) {
                 // per-feature max of the shadow, when K-adam did not produce it (first step,
                 // set_weights, DP-gang sharded update, host-tier swap-in)
@@ -1163,6 +1178,13 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             w.phi_valid = true;
             w.phi_Mpad = Mpad;
             w.phi_D = a->D;
+            const int nblk = static_cast<int>((a->D + kGemmBN - 1) / kGemmBN);
+            if (klist) {
+                KScope k(c, K_GATHER, s);
+                FM_CUDA(launch_klist(rows.feat4, M, nblk, w.klist, w.klist_ld, w.kiters,
+                                     static_cast<int32_t>(w.rows_cap), s));
+                count_launch();
+            }
             // K-GEMM1: z = Phic * W16^T / n; epilogue stores p~ = exp(z - m) (bf16) with m the
             // row's bound (fold: transposed, GEMM2's A operand) or the tile max (K-loss path),
             // the (m, sum p~) softmax partials and the taken token's logit
@@ -1179,7 +1201,10 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g1.N = static_cast<int>(a->V);
             g1.K = static_cast<int>(a->D);
             g1.group_m = env_int("FM_G1_GROUP_M", 16);  // raster: m-tiles per group (L2 reuse)
-            if (fold) {  // p~^T straight into GEMM2's A operand buffer
+            if (klist) {  // p~ row-major: the K-list GEMM2 gathers token rows
+                g1.mrow = w.mrow;
+                g1.pexp = w.Pexp;
+            } else if (fold) {  // p~^T straight into GEMM2's A operand buffer
                 g1.mrow = w.mrow;
                 g1.pexp_t = w.gt;
                 g1.ldt = static_cast<long long>(Mpad);
@@ -1200,9 +1225,16 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             // last-finisher variant cost GEMM1 12-15%: DESIGN.md §9.)
             const char* lse_env = std::getenv("FM_LSE_FUSED");
             const bool lse_fused = fold && gemm_pair_mode() && !(lse_env && lse_env[0] == '0');
-            const LseArgs lse_args{w.zact, w.stats, tiles_n, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
-                                   a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1,
-                                   fold ? 1 : 0, fold ? w.gt : nullptr, w.phict, Mpad};
+            LseArgs lse_args{w.zact, w.stats, tiles_n, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
+                             a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1,
+                             fold ? 1 : 0, fold ? w.gt : nullptr, w.phict, Mpad};
+            if (klist) {
+                lse_args.pexp_t = w.Pexp;
+                lse_args.ldt = static_cast<int64_t>(ldz);
+                lse_args.phict = w.phic;
+                lse_args.rowmajor = 1;
+                lse_args.ld_phi = static_cast<int64_t>(a->D);
+            }
             if (lse_fused) {
                 g1.lse = lse_args;
                 g1.lse_sync = w.lse_sync;
@@ -1218,7 +1250,8 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             if (!lse_fused) {
                 KScope k(c, K_LSE, s);
                 FM_CUDA(launch_lse(w.zact, w.stats, tiles_n, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
-                                   lse_args.old_logp, a->clip_eps, scal + 1, lse_args.pexp_t, w.phict, Mpad, s));
+                                   lse_args.old_logp, a->clip_eps, scal + 1, lse_args.pexp_t, lse_args.phict,
+                                   lse_args.ldt, s, lse_args.rowmajor, lse_args.ld_phi));
             }
             // K-softmax-grad: G^T tiles (zero for padding rows) — folded into GEMM2's operands
             if (!fold) {
@@ -1269,7 +1302,17 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 const int kc = static_cast<int>(round_up(static_cast<uint64_t>(std::min(kc_env, 1 << 30)), 64));
                 const int nch = (static_cast<int>(Mpad) + kc - 1) / kc;
                 KScope k(c, K_GEMM2, s);
-                if (nch == 1) {
+                if (klist) {
+                    CUtensorMap tKA, tKB;
+                    if (!make_tmap_gather4(&tKA, w.Pexp, static_cast<uint64_t>(w.rows_cap) + 1, a->V, ldz) ||
+                        !make_tmap_gather4(&tKB, w.phic, static_cast<uint64_t>(w.rows_cap) + 1, a->D, a->D))
+                        return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+                    g2.klist = w.klist;
+                    g2.klist_ld = w.klist_ld;
+                    g2.klist_iters = w.kiters;
+                    g2.sk_ws = nullptr;
+                    FM_CUDA(gemm_klist_launch(tKA, tKB, g2, c->num_sms, s));
+                } else if (nch == 1) {
                     FM_CUDA(gemm_tn_launch(GemmKind::Grad, tGt, tPt, g2, c->num_sms, s));
                 } else {
                     FM_CUDA(cudaMemsetAsync(scal, 0xFF, sizeof(double), s));  // NaN grad norm

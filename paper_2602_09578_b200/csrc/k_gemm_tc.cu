@@ -164,6 +164,11 @@ struct LogitsEpi {
         }
         if (row >= a.M) return;
         if (nvalid <= 0) return;
+        if (a.mrow) {  // single pass (K-list fold): the taken token's logit is caught here
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (col0 + j == action && j < nvalid) a.zact[row] = __uint_as_float(r[j]) * row_scale;
+        }
         const float m = run_max;
         uint32_t pk[16];
         float s = 0.f;

@@ -666,6 +666,56 @@ __global__ void gather_cols_kernel(const T* __restrict__ src, uint64_t V, uint64
 }
 }  // namespace
 
+namespace {
+__global__ void __launch_bounds__(1024) klist_kernel(const int4* __restrict__ feat4, int64_t M, int32_t* __restrict__ klist,
+                                                     int64_t ld, int32_t* __restrict__ iters, int32_t zero_row) {
+    __shared__ int wsum[32];
+    __shared__ int tot_s;
+    const int b = blockIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t* out = klist + static_cast<size_t>(b) * ld;
+    int base = 0;
+    for (int64_t r0 = 0; r0 < M; r0 += 1024) {
+        const int64_t r = r0 + threadIdx.x;
+        bool hit = false;
+        if (r < M) {
+            const int4 q = __ldg(feat4 + r);
+            hit = (q.x >= 0 && (q.x >> 8) == b) || (q.y >= 0 && (q.y >> 8) == b) ||
+                  (q.z >= 0 && (q.z >> 8) == b) || (q.w >= 0 && (q.w >> 8) == b);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+        const int pre = __popc(bal & ((1u << lane) - 1u));
+        if (lane == 0) wsum[wid] = __popc(bal);
+        __syncthreads();
+        if (wid == 0) {
+            const int v = wsum[lane];
+            int inc = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            wsum[lane] = inc - v;
+            if (lane == 31) tot_s = inc;
+        }
+        __syncthreads();
+        if (hit) out[base + wsum[wid] + pre] = static_cast<int32_t>(r);
+        base += tot_s;
+        __syncthreads();
+    }
+    const int padded = base < 64 ? 64 : (base + 63) / 64 * 64;
+    for (int i = base + static_cast<int>(threadIdx.x); i < padded; i += blockDim.x) out[i] = zero_row;
+    if (threadIdx.x == 0) iters[b] = padded / 64;
+}
+}  // namespace
+
+cudaError_t launch_klist(const int4* feat4, int64_t M, int nblk, int32_t* klist, int64_t ld, int32_t* iters,
+                         int32_t zero_row, cudaStream_t s) {
+    if (nblk <= 0) return cudaSuccess;
+    klist_kernel<<<nblk, 1024, 0, s>>>(feat4, M, klist, ld, iters, zero_row);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D, const int64_t* cols,
                                int64_t n_cols, void* out, cudaStream_t s) {
     if (f64)
@@ -680,12 +730,14 @@ cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D,
 cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int64_t M, int64_t Mpad, int64_t V,
                        const SampleDesc* sd, int64_t global_batch, RowBuffers rows, const float* old_logp,
                        float clip_eps, double* loss_acc, __nv_bfloat16* pexp_t, __nv_bfloat16* phict,
-                       int64_t ldt, cudaStream_t s) {
+                       int64_t ldt, cudaStream_t s, int rowmajor, int64_t ld_phi) {
     if (Mpad == 0) return cudaSuccess;
     int64_t blocks = (Mpad * 8 + 255) / 256;  // 4 rows per warp
     if (blocks > 148 * 4) blocks = 148 * 4;   // persistent warps: 4 resident 256-thread blocks per SM
-    const LseArgs L{zact, stats, stats_ld, M, Mpad, V, sd, global_batch, rows, old_logp, clip_eps,
-                    loss_acc, pexp_t != nullptr, pexp_t, phict, ldt};
+    LseArgs L{zact, stats, stats_ld, M, Mpad, V, sd, global_batch, rows, old_logp, clip_eps,
+              loss_acc, pexp_t != nullptr, pexp_t, phict, ldt};
+    L.rowmajor = rowmajor;
+    L.ld_phi = ld_phi;
     lse_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(L);
     return cudaGetLastError();
 }

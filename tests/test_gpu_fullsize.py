@@ -135,8 +135,9 @@ def _host_gb():
         return 0.0
 
 
+@pytest.mark.parametrize("klist", ["0", "1"])
 @pytest.mark.parametrize("cfg_name", ["C3", "C5"])
-def test_large_policy_gradient_matches_sparse_f64_oracle(ctx, cfg_name):
+def test_large_policy_gradient_matches_sparse_f64_oracle(ctx, cfg_name, klist, monkeypatch):
     """1.05B-parameter policies (C3: V=32,000 D=32,768; C5: V=128,000 D=8,192):
     a 2-sample x 4-token micro-batch through the tensor-core path against the
     column-sparse f64 oracle (fmo_sparse_grad, pinned bit-for-bit to the dense
@@ -145,6 +146,7 @@ def test_large_policy_gradient_matches_sparse_f64_oracle(ctx, cfg_name):
     V x D gradient — matches the oracle's, so no mass lands in other columns."""
     if _host_gb() < 40:
         pytest.skip("needs ~40 GB of free host memory (seeded 1.05B-param init)")
+    monkeypatch.setenv("FM_G2_KLIST", klist)
     cfg = wl.CONFIGS[cfg_name]
     Vb, Db = cfg.vocab, cfg.feat
     s = wl.step_samples(cfg, "agent0", 0, n=2, resp_len=4)
@@ -188,3 +190,14 @@ def test_c2_stream_k_matches_plain_schedule(ctx, c2_engine, monkeypatch):
     g_sk = _fresh_grad(ctx, c2_engine, [mb])
     assert np.linalg.norm(g_dp) > 0
     assert rel_fro(g_sk, g_dp) < 1e-6
+
+
+def test_c2_token_list_gemm2_matches_dense(ctx, c2_engine, monkeypatch):
+    """C2 micro-batch through the K-list GEMM2 (16 column blocks, ~23% of the
+    16,384 tokens each) vs the dense GEMM2."""
+    mb = _samples(5, 16, 1024, adv_seed=5)
+    g_dense = _fresh_grad(ctx, c2_engine, [mb])
+    monkeypatch.setenv("FM_G2_KLIST", "1")
+    g_kl = _fresh_grad(ctx, c2_engine, [mb])
+    assert np.linalg.norm(g_dense) > 0
+    assert rel_fro(g_kl, g_dense) < 1e-5

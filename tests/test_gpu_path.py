@@ -599,3 +599,21 @@ def test_tcgen05_gemm_token_lists(ctx, M, N, rows, seed):
     assert not torch.isnan(C_).any()
     err = (C_ - ref).norm() / ref.norm()
     assert float(err) < 1e-5
+
+
+@pytest.mark.parametrize("name", ["mid_agent0", "c1_planner"])
+def test_gemm2_token_lists_match_dense(ctx, monkeypatch, name):
+    """K-list GEMM2 (FM_G2_KLIST=1: each 256-feature column block sums only the
+    tokens whose context touches it, gathered with TMA gather4) gives the dense
+    GEMM2's gradients and updates up to fp32 summation order, and the same
+    grad norms; GEMM1 then stores p~ row-major and K-lse folds into the row-major
+    operands."""
+    f = _ld(f"{name}.npz")
+    dense = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
+    monkeypatch.setenv("FM_G2_KLIST", "1")
+    kl = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
+    for g1, g2 in zip(dense["grads"], kl["grads"]):
+        assert rel_fro(g2, g1) <= 1e-5
+    np.testing.assert_allclose(kl["mb_grad_norm"], dense["mb_grad_norm"], rtol=1e-5)
+    np.testing.assert_allclose(kl["upd_grad_norm"], dense["upd_grad_norm"], rtol=1e-5)
+    assert np.array_equal(kl["poll_order"], dense["poll_order"])
