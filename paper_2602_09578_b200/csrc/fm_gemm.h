@@ -68,6 +68,12 @@ struct GemmArgs {
     const int32_t* klist = nullptr;
     long long klist_ld = 0;
     const int32_t* klist_iters = nullptr;
+    // Segmented K (token slots): column tile nb sums K rows [kseg_off[nb], +64*klist_iters[nb])
+    // of A' [K'][M] and B' [K'][256] (tile loads, MN-major).  Logits: aseg != nullptr
+    // stores each row's p~ into the A' rows slot4[row] (row-major, pitch ld_out).
+    const int32_t* kseg_off = nullptr;
+    __nv_bfloat16* aseg = nullptr;
+    const int4* slot4 = nullptr;
 };
 
 // Stream-K workspace capacity: at most 2*pairs-1 split tiles (148 SMs -> 74 pairs).
@@ -83,6 +89,9 @@ size_t gemm_smem_bytes();
 uint32_t gemm_b_box_rows();
 cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, int a_mn, int b_mn, int M, int N,
                               int K, float* C, int num_sms, cudaStream_t stream);
+// Grad GEMM over token-slot segments (args.kseg_off / klist_iters), MN-major tile maps.
+cudaError_t gemm_kseg_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int num_sms,
+                             cudaStream_t stream);
 // Grad GEMM over per-column-tile K lists (args.klist*), gather4 maps for A and B.
 cudaError_t gemm_klist_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int num_sms,
                               cudaStream_t stream);
@@ -94,7 +103,7 @@ cudaError_t gemm_tn_launch(GemmKind kind, const CUtensorMap& tmA, const CUtensor
 // Builds a 2-D bf16 K-major tensor map over a row-major [rows][cols] matrix
 // (cols contiguous), box {64, box_rows}, SWIZZLE_128B.
 bool make_tmap_bf16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols,
-                           uint32_t box_rows);
+                           uint32_t box_rows, uint64_t pitch = 0);
 // Plain (no swizzle) 2-D map, any 4/2-byte dtype, box {box_cols, box_rows}.
 bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, uint32_t elem_bytes,
                   uint64_t rows, uint64_t cols, uint32_t box_rows, uint32_t box_cols);

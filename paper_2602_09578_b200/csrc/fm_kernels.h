@@ -54,8 +54,10 @@ struct LseArgs {
     __nv_bfloat16* pexp_t;  // fold: p~^T [V][ldt]  (rowmajor: p~ [Mpad][ldt])
     __nv_bfloat16* phict;   // fold: Phic^T [D][ldt] (rowmajor: Phic [Mpad][ld_phi])
     int64_t ldt;
-    int rowmajor = 0;  // K-list GEMM2: the fold writes go to the row-major operands
+    int rowmajor = 0;  // K-list GEMM2: 1 = row-major p~ / Phic, 2 = token-slot segments
     int64_t ld_phi = 0;
+    const int4* slot4 = nullptr;   // rowmajor 2: A' row of each feature's block per token
+    __nv_bfloat16* bseg = nullptr; // rowmajor 2: B' [K'][256]
 };
 
 // K-gather: decode the selected records' token payloads straight out of the
@@ -97,6 +99,16 @@ cudaError_t launch_softmax_grad(const CUtensorMap& tmP, const CUtensorMap& tmGt,
 // (deterministic block-wide scans).
 cudaError_t launch_klist(const int4* feat4, int64_t M, int nblk, int32_t* klist, int64_t ld, int32_t* iters,
                          int32_t zero_row, cudaStream_t s);
+
+// K-slot (segmented K-list GEMM2): the tokens touching 256-feature block b get
+// consecutive rows ("slots") of a segment of A' [K'][ld_a] / B' [K'][256]; segment
+// b starts at kseg_off[b] and is padded to a multiple of 64 rows (>= 64) whose A'
+// and B' rows are zeroed.  slot4[t].c_j = the slot of feature j's block (-1 if
+// feature j is absent); B'[slot][f mod 256] = count of f.  bseg must be zero on
+// entry.  Deterministic (block-wide scans in row order).
+cudaError_t launch_kslots(const int4* feat4, const uint32_t* cnt4, int64_t M, int nblk, int32_t* kcount,
+                          int32_t* kseg_off, int32_t* kiters, int4* slot4, __nv_bfloat16* aseg, int64_t ld_a,
+                          int64_t ncols_a, __nv_bfloat16* bseg, cudaStream_t s);
 
 // Parity tooling: out[v][j] = dW[v][cols[j]] (f32 or f64 accumulator).
 cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D, const int64_t* cols,

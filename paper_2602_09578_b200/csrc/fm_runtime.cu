@@ -74,11 +74,12 @@ cudaError_t dalloc(T** p, size_t n) {
 
 namespace fm {
 
-bool make_tmap_bf16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+bool make_tmap_bf16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                           uint64_t pitch) {
     EncodeTiledFn f = encode_fn();
     if (!f) return false;
     const cuuint64_t dims[2] = {cols, rows};
-    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint64_t strides[1] = {(pitch ? pitch : cols) * 2};
     const cuuint32_t box[2] = {64, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     return f(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
@@ -134,6 +135,11 @@ struct Workspace {
     float* mrow = nullptr;  // loss fold: per-row softmax offset bound [Mpad]
     unsigned* lse_sync = nullptr;  // fused K-lse: {CTAs arrived, epoch published} (GEMM1 tail)
     unsigned lse_epoch = 0;
+    // segmented K-list GEMM2 (FM_G2_KLIST=2), allocated on first use
+    __nv_bfloat16 *aseg = nullptr, *bseg = nullptr;  // A' [kp_cap][ldz], B' [kp_cap][256]
+    int4* slot4 = nullptr;                            // [rows_cap]
+    int32_t *kcount = nullptr, *kseg_off = nullptr;   // [nblk]
+    int64_t kp_cap = 0;
     int32_t* klist = nullptr;  // K-list GEMM2: token lists per 256-feature block [nblk][klist_ld]
     int32_t* kiters = nullptr;  // [nblk] list length / 64
     int64_t klist_ld = 0;
@@ -314,6 +320,11 @@ void ws_free(Workspace& w) {
     cudaFree(w.sk_ws);
     cudaFree(w.klist);
     cudaFree(w.kiters);
+    cudaFree(w.aseg);
+    cudaFree(w.bseg);
+    cudaFree(w.slot4);
+    cudaFree(w.kcount);
+    cudaFree(w.kseg_off);
     cudaFree(w.sk_cnt);
     cudaFree(w.zscratch);
     cudaFree(w.dWmb);
@@ -386,6 +397,35 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
     w.rows_cap = R;
     w.vocab_cap = VV;
     w.feat_cap = DD;
+    return FM_OK;
+}
+
+// Token-slot segments for the segmented K-list GEMM2: every token occupies at
+// most 4 slots (one per distinct feature block), each block's segment is padded
+// to 64 rows.
+int ws_reserve_seg(fm_ctx* c) {
+    Workspace& w = c->ws;
+    const int64_t nblk = static_cast<int64_t>((w.feat_cap + 255) / 256);
+    const int64_t need = 4 * w.rows_cap + 64 * nblk;
+    if (w.aseg && w.kp_cap >= need) return FM_OK;
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(w.aseg);
+    cudaFree(w.bseg);
+    cudaFree(w.slot4);
+    cudaFree(w.kcount);
+    cudaFree(w.kseg_off);
+    w.aseg = w.bseg = nullptr;
+    w.slot4 = nullptr;
+    w.kcount = w.kseg_off = nullptr;
+    const uint64_t ldz = round_up(w.vocab_cap, 8);
+    cudaError_t e = cudaSuccess;
+    e = e ? e : dalloc(&w.aseg, static_cast<size_t>(need) * ldz);
+    e = e ? e : dalloc(&w.bseg, static_cast<size_t>(need) * 256);
+    e = e ? e : dalloc(&w.slot4, static_cast<size_t>(w.rows_cap));
+    e = e ? e : dalloc(&w.kcount, static_cast<size_t>(nblk));
+    e = e ? e : dalloc(&w.kseg_off, static_cast<size_t>(nblk));
+    if (e != cudaSuccess) return fail(FM_ERR_DEVICE_OOM, std::string("segment workspace: ") + cudaGetErrorString(e));
+    w.kp_cap = need;
     return FM_OK;
 }
 
@@ -1161,6 +1201,12 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             // weight gradient sums only over the tokens whose context touches it
             const char* kl_env = std::getenv("FM_G2_KLIST");
             const bool klist = fold && gemm_pair_mode() && kl_env && kl_env[0] == '1';
+            // segmented variant (FM_G2_KLIST=2): GEMM1 writes each token's p~ row into
+            // one slot per feature block it touches, GEMM2 tile-loads contiguous segments
+            const bool kseg = fold && gemm_pair_mode() && kl_env && kl_env[0] == '2';
+            if (kseg) {
+                if (int st = ws_reserve_seg(c)) return st;
+            }
             if (fold && a->cm_gen != a->w16_gen) {
                 // per-feature max of the shadow, when K-adam did not produce it (first step,
                 // set_weights, DP-gang sharded update, host-tier swap-in)
@@ -1185,6 +1231,13 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                                      static_cast<int32_t>(w.rows_cap), s));
                 count_launch();
             }
+            if (kseg) {
+                KScope k(c, K_GATHER, s);
+                FM_CUDA(cudaMemsetAsync(w.bseg, 0, static_cast<size_t>(w.kp_cap) * 256 * 2, s));
+                FM_CUDA(launch_kslots(rows.feat4, rows.cnt4, M, nblk, w.kcount, w.kseg_off, w.kiters, w.slot4,
+                                      w.aseg, static_cast<int64_t>(ldz), static_cast<int64_t>(ldz), w.bseg, s));
+                count_launch(2);
+            }
             // K-GEMM1: z = Phic * W16^T / n; epilogue stores p~ = exp(z - m) (bf16) with m the
             // row's bound (fold: transposed, GEMM2's A operand) or the tile max (K-loss path),
             // the (m, sum p~) softmax partials and the taken token's logit
@@ -1201,7 +1254,11 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g1.N = static_cast<int>(a->V);
             g1.K = static_cast<int>(a->D);
             g1.group_m = env_int("FM_G1_GROUP_M", 16);  // raster: m-tiles per group (L2 reuse)
-            if (klist) {  // p~ row-major: the K-list GEMM2 gathers token rows
+            if (kseg) {  // p~ rows into the token's segment slots (A')
+                g1.mrow = w.mrow;
+                g1.aseg = w.aseg;
+                g1.slot4 = w.slot4;
+            } else if (klist) {  // p~ row-major: the K-list GEMM2 gathers token rows
                 g1.mrow = w.mrow;
                 g1.pexp = w.Pexp;
             } else if (fold) {  // p~^T straight into GEMM2's A operand buffer
@@ -1234,6 +1291,13 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 lse_args.phict = w.phic;
                 lse_args.rowmajor = 1;
                 lse_args.ld_phi = static_cast<int64_t>(a->D);
+            }
+            if (kseg) {
+                lse_args.pexp_t = w.aseg;
+                lse_args.ldt = static_cast<int64_t>(ldz);
+                lse_args.rowmajor = 2;
+                lse_args.slot4 = w.slot4;
+                lse_args.bseg = w.bseg;
             }
             if (lse_fused) {
                 g1.lse = lse_args;
@@ -1302,7 +1366,16 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 const int kc = static_cast<int>(round_up(static_cast<uint64_t>(std::min(kc_env, 1 << 30)), 64));
                 const int nch = (static_cast<int>(Mpad) + kc - 1) / kc;
                 KScope k(c, K_GEMM2, s);
-                if (klist) {
+                if (kseg) {
+                    CUtensorMap tSA, tSB;
+                    if (!make_tmap_bf16_kmajor(&tSA, w.aseg, static_cast<uint64_t>(w.kp_cap), a->V, 64, ldz) ||
+                        !make_tmap_bf16_kmajor(&tSB, w.bseg, static_cast<uint64_t>(w.kp_cap), 256, 64))
+                        return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+                    g2.kseg_off = w.kseg_off;
+                    g2.klist_iters = w.kiters;
+                    g2.sk_ws = nullptr;
+                    FM_CUDA(gemm_kseg_launch(tSA, tSB, g2, c->num_sms, s));
+                } else if (klist) {
                     CUtensorMap tKA, tKB;
                     if (!make_tmap_gather4(&tKA, w.Pexp, static_cast<uint64_t>(w.rows_cap) + 1, a->V, ldz) ||
                         !make_tmap_gather4(&tKB, w.phic, static_cast<uint64_t>(w.rows_cap) + 1, a->D, a->D))

@@ -109,10 +109,18 @@ struct LogitsEpi {
     float row_scale;
     float run_max, run_sum;
     int action;
+    int4 slots;
     __device__ __forceinline__ void begin(const GemmArgs& a, int row) {
         const bool ok = row < a.M;
         row_scale = ok ? a.row_scale[row] : 0.f;
         action = ok ? a.action[row] : -1;
+        if (a.aseg) {  // distinct A' rows of this token (duplicates -> -1)
+            int4 q = ok ? a.slot4[row] : make_int4(-1, -1, -1, -1);
+            if (q.y == q.x) q.y = -1;
+            if (q.z == q.x || q.z == q.y) q.z = -1;
+            if (q.w == q.x || q.w == q.y || q.w == q.z) q.w = -1;
+            slots = q;
+        }
         run_max = a.mrow ? (ok ? a.mrow[row] : 0.f) : -INFINITY;  // fold: the row's bound, known upfront
         run_sum = 0.f;
     }
@@ -181,6 +189,24 @@ struct LogitsEpi {
             pk[j >> 1] = *reinterpret_cast<const uint32_t*>(&h);
         }
         run_sum += s;
+        if (a.aseg) {
+            const int sl[4] = {slots.x, slots.y, slots.z, slots.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (sl[q] < 0) continue;
+                __nv_bfloat16* d = a.aseg + static_cast<size_t>(sl[q]) * a.ld_out + col0;
+                if (nvalid == 32) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        reinterpret_cast<uint4*>(d)[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < nvalid) d[j] = reinterpret_cast<const __nv_bfloat16*>(pk)[j];
+                }
+            }
+            return;
+        }
         __nv_bfloat16* dst = a.pexp + static_cast<size_t>(row) * a.ld_out + col0;
         if (nvalid == 32) {
 #pragma unroll
@@ -521,11 +547,14 @@ constexpr int kThreadsPair = 192;  // w0 TMA, w1 MMA, w2-5 epilogue
 // (8 KB each, the second at +8 KB = the descriptor's LBO).
 // kKList (Grad): both operands MN-major row-major [rows][.] gathered with TMA
 // gather4 from the output column tile's K list (args.klist*).
-template <class Epi, bool kAmn = false, bool kBmn = false, bool kKList = false>
+// kSeg (Grad): both operands MN-major; column tile nb runs the K rows of its
+// token-slot segment (args.kseg_off / klist_iters); B' holds only 256 columns.
+template <class Epi, bool kAmn = false, bool kBmn = false, bool kKList = false, bool kSeg = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     gemm_tn_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        GemmArgs args) {
     static_assert(!kKList || (kAmn && kBmn), "K-list operands are MN-major");
+    static_assert(!kSeg || (kAmn && kBmn), "segment operands are MN-major");
     constexpr uint32_t kId = idesc_bf16_f32<256, BN, kAmn, kBmn>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -613,12 +642,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             for (int w = 0; sch.get(cid, w, wi); ++w) {
                 const TileCoord tc = tile_coord(wi.tile, tiles_m, tiles_n, args.group_m);
                 const int arow = tc.mb * 256 + static_cast<int>(rank) * 128;
-                const int brow = tc.nb * BN + static_cast<int>(rank) * 128;
+                const int brow = (kSeg ? 0 : tc.nb * BN) + static_cast<int>(rank) * 128;
+                int kbase = args.k0;
+                if constexpr (kSeg) {
+                    kbase = __ldg(args.kseg_off + tc.nb);
+                    wi.ke = __ldg(args.klist_iters + tc.nb);
+                }
                 for (int k = wi.kb; k < wi.ke; ++k) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t fb = mapa_shared(&full[stage], 0);
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
-                    const int kc = args.k0 + k * BK;
+                    const int kc = kbase + k * BK;
                     if constexpr (kAmn) {
                         tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, arow, kc, pol);
                         tma_load_2d_2sm(sA + stage * P_A_STAGE + 8192, &tmA, fb, arow + 64, kc, pol);
@@ -647,7 +681,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             uint32_t acc_phase = 0;
             WorkItem wi;
             for (int w = 0; sch.get(cid, w, wi); ++w) {
-                if constexpr (kKList)
+                if constexpr (kKList || kSeg)
                     wi.ke = __ldg(args.klist_iters + tile_coord(wi.tile, tiles_m, tiles_n, args.group_m).nb);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
@@ -838,6 +872,19 @@ cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, in
     else if (a_mn) launch(gemm_tn_2sm_kernel<GradEpi, true, false>);
     else if (b_mn) launch(gemm_tn_2sm_kernel<GradEpi, false, true>);
     else launch(gemm_tn_2sm_kernel<GradEpi, false, false>);
+    return cudaGetLastError();
+}
+
+cudaError_t gemm_kseg_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int num_sms,
+                             cudaStream_t stream) {
+    const size_t smem = gemm_smem_bytes();
+    const int tiles = ((args.M + 255) / 256) * ((args.N + BN - 1) / BN);
+    if (tiles == 0) return cudaSuccess;
+    const int pairs = num_sms / 2;
+    const int grid = 2 * (tiles < pairs ? tiles : pairs);
+    auto k = gemm_tn_2sm_kernel<GradEpi, true, true, false, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k<<<grid, kThreadsPair, smem, stream>>>(tmA, tmB, args);
     return cudaGetLastError();
 }
 

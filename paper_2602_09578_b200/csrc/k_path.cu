@@ -716,6 +716,127 @@ cudaError_t launch_klist(const int4* feat4, int64_t M, int nblk, int32_t* klist,
     return cudaGetLastError();
 }
 
+namespace {
+// block-wide exclusive scan of a 0/1 flag over 1024 threads; returns the rank,
+// *total gets the count (all threads)
+__device__ __forceinline__ int block_rank(bool flag, int* wsum, int* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    const int pre = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) wsum[wid] = __popc(bal);
+    __syncthreads();
+    if (wid == 0) {
+        const int v = wsum[lane];
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        wsum[lane] = inc - v;
+        if (lane == 31) wsum[32] = inc;
+    }
+    __syncthreads();
+    const int r = wsum[wid] + pre;
+    *total = wsum[32];
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ bool touches(int4 q, int b) {
+    return (q.x >= 0 && (q.x >> 8) == b) || (q.y >= 0 && (q.y >> 8) == b) || (q.z >= 0 && (q.z >> 8) == b) ||
+           (q.w >= 0 && (q.w >> 8) == b);
+}
+
+__global__ void __launch_bounds__(1024) kslot_count_kernel(const int4* __restrict__ feat4, int64_t M, int nblk,
+                                                           int32_t* __restrict__ kcount, int4* __restrict__ slot4) {
+    __shared__ int wsum[33];
+    const int b = blockIdx.x;
+    int n = 0;
+    for (int64_t r0 = 0; r0 < M; r0 += 1024) {
+        const int64_t r = r0 + threadIdx.x;
+        const bool hit = r < M && touches(__ldg(feat4 + r), b);
+        int tot;
+        block_rank(hit, wsum, &tot);
+        n += tot;
+    }
+    if (threadIdx.x == 0) kcount[b] = n;
+    for (int64_t r = static_cast<int64_t>(b) * 1024 + threadIdx.x; r < M; r += static_cast<int64_t>(nblk) * 1024)
+        slot4[r] = make_int4(-1, -1, -1, -1);
+}
+
+__global__ void __launch_bounds__(1024) kslot_place_kernel(const int4* __restrict__ feat4,
+                                                           const uint32_t* __restrict__ cnt4, int64_t M,
+                                                           const int32_t* __restrict__ kcount,
+                                                           int32_t* __restrict__ kseg_off,
+                                                           int32_t* __restrict__ kiters, int4* __restrict__ slot4,
+                                                           __nv_bfloat16* __restrict__ aseg, int64_t ld_a,
+                                                           int64_t ncols_a, __nv_bfloat16* __restrict__ bseg) {
+    __shared__ int wsum[33];
+    __shared__ int off_s;
+    const int b = blockIdx.x;
+    if (threadIdx.x == 0) {
+        int off = 0;
+        for (int i = 0; i < b; ++i) {
+            const int c = kcount[i];
+            off += c < 64 ? 64 : (c + 63) / 64 * 64;
+        }
+        off_s = off;
+    }
+    __syncthreads();
+    const int off = off_s;
+    const int len = kcount[b];
+    const int padded = len < 64 ? 64 : (len + 63) / 64 * 64;
+    if (threadIdx.x == 0) {
+        kseg_off[b] = off;
+        kiters[b] = padded / 64;
+    }
+    int base = 0;
+    for (int64_t r0 = 0; r0 < M; r0 += 1024) {
+        const int64_t r = r0 + threadIdx.x;
+        int4 q = make_int4(-1, -1, -1, -1);
+        if (r < M) q = __ldg(feat4 + r);
+        const bool hit = r < M && touches(q, b);
+        int tot;
+        const int rk = block_rank(hit, wsum, &tot);
+        if (hit) {
+            const int slot = off + base + rk;
+            const uint32_t c4 = __ldg(cnt4 + r);
+            int* sl = reinterpret_cast<int*>(slot4 + r);
+            const int f[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (f[j] >= 0 && (f[j] >> 8) == b) {
+                    sl[j] = slot;
+                    bseg[static_cast<size_t>(slot) * 256 + (f[j] & 255)] =
+                        __float2bfloat16_rn(static_cast<float>((c4 >> (8 * j)) & 0xFFu));
+                }
+            }
+        }
+        base += tot;
+    }
+    // zero the segment's padding rows of A' (B' is zero on entry)
+    const int64_t npad = padded - len;
+    const int64_t cols8 = ncols_a / 8;  // ld_a and ncols_a are multiples of 8
+    for (int64_t i = threadIdx.x; i < npad * cols8; i += blockDim.x) {
+        const int64_t rr = off + len + i / cols8, cc = (i % cols8) * 8;
+        *reinterpret_cast<uint4*>(aseg + rr * ld_a + cc) = make_uint4(0u, 0u, 0u, 0u);
+    }
+}
+}  // namespace
+
+cudaError_t launch_kslots(const int4* feat4, const uint32_t* cnt4, int64_t M, int nblk, int32_t* kcount,
+                          int32_t* kseg_off, int32_t* kiters, int4* slot4, __nv_bfloat16* aseg, int64_t ld_a,
+                          int64_t ncols_a, __nv_bfloat16* bseg, cudaStream_t s) {
+    if (nblk <= 0) return cudaSuccess;
+    kslot_count_kernel<<<nblk, 1024, 0, s>>>(feat4, M, nblk, kcount, slot4);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    kslot_place_kernel<<<nblk, 1024, 0, s>>>(feat4, cnt4, M, kcount, kseg_off, kiters, slot4, aseg, ld_a, ncols_a,
+                                             bseg);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D, const int64_t* cols,
                                int64_t n_cols, void* out, cudaStream_t s) {
     if (f64)

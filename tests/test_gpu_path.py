@@ -601,8 +601,9 @@ def test_tcgen05_gemm_token_lists(ctx, M, N, rows, seed):
     assert float(err) < 1e-5
 
 
+@pytest.mark.parametrize("mode", ["1", "2"])
 @pytest.mark.parametrize("name", ["mid_agent0", "c1_planner"])
-def test_gemm2_token_lists_match_dense(ctx, monkeypatch, name):
+def test_gemm2_token_lists_match_dense(ctx, monkeypatch, name, mode):
     """K-list GEMM2 (FM_G2_KLIST=1: each 256-feature column block sums only the
     tokens whose context touches it, gathered with TMA gather4) gives the dense
     GEMM2's gradients and updates up to fp32 summation order, and the same
@@ -610,7 +611,7 @@ def test_gemm2_token_lists_match_dense(ctx, monkeypatch, name):
     operands."""
     f = _ld(f"{name}.npz")
     dense = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
-    monkeypatch.setenv("FM_G2_KLIST", "1")
+    monkeypatch.setenv("FM_G2_KLIST", mode)
     kl = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
     for g1, g2 in zip(dense["grads"], kl["grads"]):
         assert rel_fro(g2, g1) <= 1e-5
