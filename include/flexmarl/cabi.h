@@ -134,6 +134,10 @@ int fm_agent_read_grad(fm_agent* a, double* g_out);
 /* selected feature columns of the gradient accumulator, [V][n_cols] row-major as f64
  * (parity tooling at full V x D, where reading all V*D is host-memory heavy) */
 int fm_agent_read_grad_cols(fm_agent* a, const int64_t* cols, int64_t n_cols, double* g_out);
+/* K rows the segmented K-GEMM2 launches on ctx ran since the last reset, summed
+ * over their 256-feature column blocks (executed flops = 2 * V * 256 * rows);
+ * reset != 0 zeroes the counter after reading.  0 when only dense GEMM2s ran. */
+int fm_ctx_gemm2_rows(fm_ctx* c, int64_t* rows_out, int reset);
 /* kernel test hook (device pointers): C[M][N] fp32 = sum_k A(m,k) B(n,k) through the
  * tcgen05 CTA-pair GEMM, A/B K-major ([M][K] / [N][K]) or MN-major ([K][M] / [K][N]) */
 int fm_debug_gemm(fm_ctx* c, const void* A, const void* B, int a_mn, int b_mn, int M, int N, int K, float* C);

@@ -75,6 +75,7 @@ _PROTOS = {
     "fm_agent_read_grad": (I, [P, P]),
     "fm_agent_read_grad_cols": (I, [P, P, I64, P]),
     "fm_debug_gemm": (I, [P, P, P, I, I, I, I, I, P]),
+    "fm_ctx_gemm2_rows": (I, [P, PI64, I]),
     "fm_debug_gemm_klist": (I, [P, P, P, P, I64, P, I, I, I, P]),
     "fm_agent_version": (I64, [P]),
     "fm_agent_samples_accumulated": (I64, [P]),

@@ -105,10 +105,11 @@ cudaError_t launch_klist(const int4* feat4, int64_t M, int nblk, int32_t* klist,
 // b starts at kseg_off[b] and is padded to a multiple of 64 rows (>= 64) whose A'
 // and B' rows are zeroed.  slot4[t].c_j = the slot of feature j's block (-1 if
 // feature j is absent); B'[slot][f mod 256] = count of f.  bseg must be zero on
-// entry.  Deterministic (block-wide scans in row order).
+// entry.  Deterministic (block-wide scans in row order).  rows_acc (nullable)
+// accumulates the padded segment rows (GEMM2's executed K, for the roofline).
 cudaError_t launch_kslots(const int4* feat4, const uint32_t* cnt4, int64_t M, int nblk, int32_t* kcount,
                           int32_t* kseg_off, int32_t* kiters, int4* slot4, __nv_bfloat16* aseg, int64_t ld_a,
-                          int64_t ncols_a, __nv_bfloat16* bseg, cudaStream_t s);
+                          int64_t ncols_a, __nv_bfloat16* bseg, unsigned long long* rows_acc, cudaStream_t s);
 
 // Parity tooling: out[v][j] = dW[v][cols[j]] (f32 or f64 accumulator).
 cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D, const int64_t* cols,

@@ -139,6 +139,7 @@ struct Workspace {
     __nv_bfloat16 *aseg = nullptr, *bseg = nullptr;  // A' [kp_cap][ldz], B' [kp_cap][256]
     int4* slot4 = nullptr;                            // [rows_cap]
     int32_t *kcount = nullptr, *kseg_off = nullptr;   // [nblk]
+    unsigned long long* kseg_rows = nullptr;          // executed GEMM2 K rows, accumulated
     int64_t kp_cap = 0;
     int32_t* klist = nullptr;  // K-list GEMM2: token lists per 256-feature block [nblk][klist_ld]
     int32_t* kiters = nullptr;  // [nblk] list length / 64
@@ -210,6 +211,7 @@ struct fm_ctx {
     uint64_t arena_cap = 0, arena_used = 0;
     std::unordered_map<uint64_t, uint64_t> arena_ntok;  // offset -> token count
     Workspace ws;
+    bool last_kseg = false;  // the last tensor-core micro-batch ran the segmented GEMM2
     // pinned staging (sample descriptors, host payloads) with reuse events
     uint8_t* staging[kStagingSlots] = {};
     size_t staging_cap[kStagingSlots] = {};
@@ -325,6 +327,7 @@ void ws_free(Workspace& w) {
     cudaFree(w.slot4);
     cudaFree(w.kcount);
     cudaFree(w.kseg_off);
+    cudaFree(w.kseg_rows);
     cudaFree(w.sk_cnt);
     cudaFree(w.zscratch);
     cudaFree(w.dWmb);
@@ -424,6 +427,10 @@ int ws_reserve_seg(fm_ctx* c) {
     e = e ? e : dalloc(&w.slot4, static_cast<size_t>(w.rows_cap));
     e = e ? e : dalloc(&w.kcount, static_cast<size_t>(nblk));
     e = e ? e : dalloc(&w.kseg_off, static_cast<size_t>(nblk));
+    if (!w.kseg_rows) {
+        e = e ? e : dalloc(&w.kseg_rows, 1);
+        e = e ? e : cudaMemset(w.kseg_rows, 0, sizeof(unsigned long long));
+    }
     if (e != cudaSuccess) return fail(FM_ERR_DEVICE_OOM, std::string("segment workspace: ") + cudaGetErrorString(e));
     w.kp_cap = need;
     return FM_OK;
@@ -1083,6 +1090,21 @@ int fm_debug_gemm_klist(fm_ctx* c, const void* A, const void* B, const int32_t* 
     FM_GUARD_END
 }
 
+int fm_ctx_gemm2_rows(fm_ctx* c, int64_t* rows_out, int reset) {
+    FM_GUARD_BEGIN
+    if (!c || !rows_out) return fail(FM_ERR_INVALID_ARG, "gemm2_rows: bad arguments");
+    *rows_out = 0;
+    if (!c->ws.kseg_rows) return FM_OK;
+    if (int st = set_dev(c)) return st;
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    unsigned long long v = 0;
+    FM_CUDA(cudaMemcpy(&v, c->ws.kseg_rows, sizeof(v), cudaMemcpyDeviceToHost));
+    if (reset) FM_CUDA(cudaMemset(c->ws.kseg_rows, 0, sizeof(v)));
+    *rows_out = static_cast<int64_t>(v);
+    return FM_OK;
+    FM_GUARD_END
+}
+
 int fm_agent_read_grad_cols(fm_agent* a, const int64_t* cols, int64_t n_cols, double* g) {
     FM_GUARD_BEGIN
     if (int st = check_active(a)) return st;
@@ -1199,14 +1221,21 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             const bool fold = loss_fold_enabled();
             // K-list GEMM2 (opt-in FM_G2_KLIST=1): each 256-feature column block of the
             // weight gradient sums only over the tokens whose context touches it
+            // GEMM2 over token-slot segments (default; FM_G2_KLIST=0 dense, 1 gather4 lists):
+            // each 256-feature column block of dW sums only the tokens whose context touches
+            // it — GEMM1 writes each token's p~ row into one slot per feature block it
+            // touches and GEMM2 tile-loads contiguous segments.  Falls back to the dense
+            // GEMM2 when the segment workspace does not fit.
             const char* kl_env = std::getenv("FM_G2_KLIST");
-            const bool klist = fold && gemm_pair_mode() && kl_env && kl_env[0] == '1';
-            // segmented variant (FM_G2_KLIST=2): GEMM1 writes each token's p~ row into
-            // one slot per feature block it touches, GEMM2 tile-loads contiguous segments
-            const bool kseg = fold && gemm_pair_mode() && kl_env && kl_env[0] == '2';
-            if (kseg) {
-                if (int st = ws_reserve_seg(c)) return st;
+            const char kl_mode = kl_env && kl_env[0] ? kl_env[0] : '2';
+            const bool klist = fold && gemm_pair_mode() && kl_mode == '1';
+            bool kseg = fold && gemm_pair_mode() && kl_mode == '2';
+            if (kseg && ws_reserve_seg(c) != FM_OK) {
+                kseg = false;
+                clear_error();
+                cudaGetLastError();
             }
+            c->last_kseg = kseg;
             if (fold && a->cm_gen != a->w16_gen) {
                 // per-feature max of the shadow, when K-adam did not produce it (first step,
                 // set_weights, DP-gang sharded update, host-tier swap-in)
@@ -1235,7 +1264,8 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 KScope k(c, K_GATHER, s);
                 FM_CUDA(cudaMemsetAsync(w.bseg, 0, static_cast<size_t>(w.kp_cap) * 256 * 2, s));
                 FM_CUDA(launch_kslots(rows.feat4, rows.cnt4, M, nblk, w.kcount, w.kseg_off, w.kiters, w.slot4,
-                                      w.aseg, static_cast<int64_t>(ldz), static_cast<int64_t>(ldz), w.bseg, s));
+                                      w.aseg, static_cast<int64_t>(ldz), static_cast<int64_t>(ldz), w.bseg,
+                                      w.kseg_rows, s));
                 count_launch(2);
             }
             // K-GEMM1: z = Phic * W16^T / n; epilogue stores p~ = exp(z - m) (bf16) with m the

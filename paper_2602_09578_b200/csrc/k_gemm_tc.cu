@@ -110,6 +110,7 @@ struct LogitsEpi {
     float run_max, run_sum;
     int action;
     int4 slots;
+    float* xbuf = nullptr;  // per-warp smem staging (token-slot stores)
     __device__ __forceinline__ void begin(const GemmArgs& a, int row) {
         const bool ok = row < a.M;
         row_scale = ok ? a.row_scale[row] : 0.f;
@@ -170,8 +171,12 @@ struct LogitsEpi {
             run_sum += s;
             return;
         }
+        if (nvalid <= 0) return;  // warp-uniform (col0 is the same for every lane)
+        if (a.aseg) {
+            seg_chunk(a, row, col0, nvalid, r);  // warp-cooperative: every lane takes part
+            return;
+        }
         if (row >= a.M) return;
-        if (nvalid <= 0) return;
         if (a.mrow) {  // single pass (K-list fold): the taken token's logit is caught here
 #pragma unroll
             for (int j = 0; j < 32; ++j)
@@ -189,24 +194,6 @@ struct LogitsEpi {
             pk[j >> 1] = *reinterpret_cast<const uint32_t*>(&h);
         }
         run_sum += s;
-        if (a.aseg) {
-            const int sl[4] = {slots.x, slots.y, slots.z, slots.w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (sl[q] < 0) continue;
-                __nv_bfloat16* d = a.aseg + static_cast<size_t>(sl[q]) * a.ld_out + col0;
-                if (nvalid == 32) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        reinterpret_cast<uint4*>(d)[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (j < nvalid) d[j] = reinterpret_cast<const __nv_bfloat16*>(pk)[j];
-                }
-            }
-            return;
-        }
         __nv_bfloat16* dst = a.pexp + static_cast<size_t>(row) * a.ld_out + col0;
         if (nvalid == 32) {
 #pragma unroll
@@ -218,6 +205,67 @@ struct LogitsEpi {
                 if (j < nvalid) dst[j] = reinterpret_cast<const __nv_bfloat16*>(pk)[j];
         }
     }
+    // Token-slot segments (K-list GEMM2 mode 2): p~ = exp(z - m_row) of the chunk goes
+    // to every A' row of this token (one per feature block it touches).
+    __device__ __forceinline__ void seg_chunk(const GemmArgs& a, int row, int col0, int nvalid, uint32_t (&r)[32]) {
+        const bool live = row < a.M;
+        if (live) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (col0 + j == action && j < nvalid) a.zact[row] = __uint_as_float(r[j]) * row_scale;
+        }
+        const float m = run_max;
+        uint32_t pk[16];
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+            const float p0 = (live && j < nvalid) ? fast_exp(__uint_as_float(r[j]) * row_scale - m) : 0.f;
+            const float p1 = (live && j + 1 < nvalid) ? fast_exp(__uint_as_float(r[j + 1]) * row_scale - m) : 0.f;
+            s += p0 + p1;
+            const __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+            pk[j >> 1] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        run_sum += s;
+        if (nvalid < 32) {  // ragged last vocab tile: plain per-lane stores
+            const int sl[4] = {slots.x, slots.y, slots.z, slots.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (sl[q] < 0) continue;
+                __nv_bfloat16* d = a.aseg + static_cast<size_t>(sl[q]) * a.ld_out + col0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (j < nvalid) d[j] = reinterpret_cast<const __nv_bfloat16*>(pk)[j];
+            }
+            return;
+        }
+        // Stage the warp's 32 rows x 64 B through smem, then write each (row, slot)
+        // piece with 4 lanes x 16 B: every store instruction covers 8 rows' full
+        // 32-B sectors (per-lane 16-B stores to 32 different rows left half-sector
+        // writes that L2 filled from DRAM: +5 GB reads per launch)
+        const uint32_t lane = threadIdx.x & 31;
+        uint4* xb = reinterpret_cast<uint4*>(xbuf);  // 32 rows x 5 uint4 (80-B pitch)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xb[lane * 5 + i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        __syncwarp();
+        const int part = static_cast<int>(lane & 3);
+        const uint64_t pol = policy_evict_first();  // 3.6 GB stream, read back by GEMM2 from DRAM
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const int rr = g * 8 + static_cast<int>(lane >> 2);
+            const uint4 v = xb[rr * 5 + part];
+            const int s0 = __shfl_sync(0xffffffffu, slots.x, rr), s1 = __shfl_sync(0xffffffffu, slots.y, rr);
+            const int s2 = __shfl_sync(0xffffffffu, slots.z, rr), s3 = __shfl_sync(0xffffffffu, slots.w, rr);
+            const int sl[4] = {s0, s1, s2, s3};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (sl[q] >= 0)
+                    st_global_v4_hint(reinterpret_cast<uint4*>(a.aseg + static_cast<size_t>(sl[q]) * a.ld_out + col0) + part,
+                                      v, pol);
+        }
+        __syncwarp();
+        return;
+    }
+
     __device__ __forceinline__ void end(const GemmArgs& a, int row, int nb) {
         if (row < a.M) a.stats[static_cast<size_t>(row) * a.stats_ld + nb] = make_float2(run_max, run_sum);
     }
@@ -636,6 +684,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         // ===== TMA producer (both CTAs) =====
         if (elect_one()) {
             const uint64_t pol = policy_evict_last();
+            // segmented GEMM2: each A' segment block is read by exactly one tile
+            const uint64_t pol_a = kSeg ? policy_evict_first() : pol;
             int stage = 0;
             uint32_t phase = 0;
             WorkItem wi;
@@ -654,8 +704,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
                     const int kc = kbase + k * BK;
                     if constexpr (kAmn) {
-                        tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, arow, kc, pol);
-                        tma_load_2d_2sm(sA + stage * P_A_STAGE + 8192, &tmA, fb, arow + 64, kc, pol);
+                        tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, arow, kc, pol_a);
+                        tma_load_2d_2sm(sA + stage * P_A_STAGE + 8192, &tmA, fb, arow + 64, kc, pol_a);
                     } else {
                         tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, kc, arow, pol);
                     }
@@ -718,7 +768,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         const int row_in_tile = static_cast<int>(rank * 128 + quad * 32 + lane);
         const uint32_t tempty_leader[2] = {mapa_shared(&tempty[0], 0), mapa_shared(&tempty[1], 0)};
         Epi epi;
-        if constexpr (std::is_same_v<Epi, GradEpi>) epi.xbuf = xscratch + quad * 32 * 36;
+        epi.xbuf = xscratch + quad * 32 * 36;
         int acc = 0;
         uint32_t acc_phase = 0;
         double sumsq_total = 0.0;

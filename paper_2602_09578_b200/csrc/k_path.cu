@@ -771,7 +771,8 @@ __global__ void __launch_bounds__(1024) kslot_place_kernel(const int4* __restric
                                                            int32_t* __restrict__ kseg_off,
                                                            int32_t* __restrict__ kiters, int4* __restrict__ slot4,
                                                            __nv_bfloat16* __restrict__ aseg, int64_t ld_a,
-                                                           int64_t ncols_a, __nv_bfloat16* __restrict__ bseg) {
+                                                           int64_t ncols_a, __nv_bfloat16* __restrict__ bseg,
+                                                           unsigned long long* rows_acc) {
     __shared__ int wsum[33];
     __shared__ int off_s;
     const int b = blockIdx.x;
@@ -790,6 +791,7 @@ __global__ void __launch_bounds__(1024) kslot_place_kernel(const int4* __restric
     if (threadIdx.x == 0) {
         kseg_off[b] = off;
         kiters[b] = padded / 64;
+        if (rows_acc) atomicAdd(rows_acc, static_cast<unsigned long long>(padded));
     }
     int base = 0;
     for (int64_t r0 = 0; r0 < M; r0 += 1024) {
@@ -827,13 +829,13 @@ __global__ void __launch_bounds__(1024) kslot_place_kernel(const int4* __restric
 
 cudaError_t launch_kslots(const int4* feat4, const uint32_t* cnt4, int64_t M, int nblk, int32_t* kcount,
                           int32_t* kseg_off, int32_t* kiters, int4* slot4, __nv_bfloat16* aseg, int64_t ld_a,
-                          int64_t ncols_a, __nv_bfloat16* bseg, cudaStream_t s) {
+                          int64_t ncols_a, __nv_bfloat16* bseg, unsigned long long* rows_acc, cudaStream_t s) {
     if (nblk <= 0) return cudaSuccess;
     kslot_count_kernel<<<nblk, 1024, 0, s>>>(feat4, M, nblk, kcount, slot4);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     kslot_place_kernel<<<nblk, 1024, 0, s>>>(feat4, cnt4, M, kcount, kseg_off, kiters, slot4, aseg, ld_a, ncols_a,
-                                             bseg);
+                                             bseg, rows_acc);
     return cudaGetLastError();
 }
 
