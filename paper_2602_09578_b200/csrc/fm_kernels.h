@@ -86,6 +86,7 @@ cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int
                        int64_t V, const SampleDesc* sd, int64_t global_batch, RowBuffers rows,
                        const float* old_logp, float clip_eps, double* loss_acc, __nv_bfloat16* pexp_t,
                        __nv_bfloat16* phict, int64_t ldt, cudaStream_t s, int rowmajor = 0, int64_t ld_phi = 0);
+cudaError_t launch_lse(const LseArgs& L, cudaStream_t s);
 
 // K-loss (fused log-softmax gradient):
 //   G^T[v][t] = coef_eff_t * (delta(v, a_t) - p~[t][v] * exp(m_tile(t, v) - lse_t))
@@ -105,7 +106,8 @@ cudaError_t launch_klist(const int4* feat4, int64_t M, int nblk, int32_t* klist,
 // b starts at kseg_off[b] and is padded to a multiple of 64 rows (>= 64) whose A'
 // and B' rows are zeroed.  slot4[t].c_j = the slot of feature j's block (-1 if
 // feature j is absent); B'[slot][f mod 256] = count of f.  bseg must be zero on
-// entry.  Deterministic (block-wide scans in row order).  rows_acc (nullable)
+// entry.  Deterministic (block-wide scans in row order; kcount = per-(block,
+// 1024-row chunk) counts).  rows_acc (nullable)
 // accumulates the padded segment rows (GEMM2's executed K, for the roofline).
 cudaError_t launch_kslots(const int4* feat4, const uint32_t* cnt4, int64_t M, int nblk, int32_t* kcount,
                           int32_t* kseg_off, int32_t* kiters, int4* slot4, __nv_bfloat16* aseg, int64_t ld_a,

@@ -138,7 +138,7 @@ struct Workspace {
     // segmented K-list GEMM2 (FM_G2_KLIST=2), allocated on first use
     __nv_bfloat16 *aseg = nullptr, *bseg = nullptr;  // A' [kp_cap][ldz], B' [kp_cap][256]
     int4* slot4 = nullptr;                            // [rows_cap]
-    int32_t *kcount = nullptr, *kseg_off = nullptr;   // [nblk]
+    int32_t *kcount = nullptr, *kseg_off = nullptr;   // [nblk][row chunks of 1024], [nblk]
     unsigned long long* kseg_rows = nullptr;          // executed GEMM2 K rows, accumulated
     int64_t kp_cap = 0;
     int32_t* klist = nullptr;  // K-list GEMM2: token lists per 256-feature block [nblk][klist_ld]
@@ -425,7 +425,7 @@ int ws_reserve_seg(fm_ctx* c) {
     e = e ? e : dalloc(&w.aseg, static_cast<size_t>(need) * ldz);
     e = e ? e : dalloc(&w.bseg, static_cast<size_t>(need) * 256);
     e = e ? e : dalloc(&w.slot4, static_cast<size_t>(w.rows_cap));
-    e = e ? e : dalloc(&w.kcount, static_cast<size_t>(nblk));
+    e = e ? e : dalloc(&w.kcount, static_cast<size_t>(nblk) * static_cast<size_t>((w.rows_cap + 1023) / 1024 + 1));
     e = e ? e : dalloc(&w.kseg_off, static_cast<size_t>(nblk));
     if (!w.kseg_rows) {
         e = e ? e : dalloc(&w.kseg_rows, 1);
@@ -1343,9 +1343,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             // K-lse (standalone unless fused into GEMM1's epilogue)
             if (!lse_fused) {
                 KScope k(c, K_LSE, s);
-                FM_CUDA(launch_lse(w.zact, w.stats, tiles_n, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
-                                   lse_args.old_logp, a->clip_eps, scal + 1, lse_args.pexp_t, lse_args.phict,
-                                   lse_args.ldt, s, lse_args.rowmajor, lse_args.ld_phi));
+                FM_CUDA(launch_lse(lse_args, s));
             }
             // K-softmax-grad: G^T tiles (zero for padding rows) — folded into GEMM2's operands
             if (!fold) {

@@ -748,79 +748,88 @@ __device__ __forceinline__ bool touches(int4 q, int b) {
            (q.w >= 0 && (q.w >> 8) == b);
 }
 
-__global__ void __launch_bounds__(1024) kslot_count_kernel(const int4* __restrict__ feat4, int64_t M, int nblk,
-                                                           int32_t* __restrict__ kcount, int4* __restrict__ slot4) {
+// grid (nblk, nchunk): CTA (b, c) counts the rows of chunk c (1024 rows) touching
+// block b; CTA (b, 0) also resets slot4 for its share of rows
+__global__ void __launch_bounds__(1024) kslot_count_kernel(const int4* __restrict__ feat4, int64_t M,
+                                                           int32_t* __restrict__ ccount, int4* __restrict__ slot4) {
     __shared__ int wsum[33];
-    const int b = blockIdx.x;
-    int n = 0;
-    for (int64_t r0 = 0; r0 < M; r0 += 1024) {
-        const int64_t r = r0 + threadIdx.x;
-        const bool hit = r < M && touches(__ldg(feat4 + r), b);
-        int tot;
-        block_rank(hit, wsum, &tot);
-        n += tot;
-    }
-    if (threadIdx.x == 0) kcount[b] = n;
-    for (int64_t r = static_cast<int64_t>(b) * 1024 + threadIdx.x; r < M; r += static_cast<int64_t>(nblk) * 1024)
-        slot4[r] = make_int4(-1, -1, -1, -1);
+    const int b = blockIdx.x, c = blockIdx.y;
+    const int64_t r = static_cast<int64_t>(c) * 1024 + threadIdx.x;
+    const bool hit = r < M && touches(__ldg(feat4 + r), b);
+    int tot;
+    block_rank(hit, wsum, &tot);
+    if (threadIdx.x == 0) ccount[static_cast<size_t>(b) * gridDim.y + c] = tot;
+    if (b == 0 && r < M) slot4[r] = make_int4(-1, -1, -1, -1);
 }
 
+// grid (nblk, nchunk): segment offsets from the chunk counts (block-major), ranks
+// within the chunk, slot / B' writes; the segment's padding rows of A' are zeroed
+// by the block's CTAs together
 __global__ void __launch_bounds__(1024) kslot_place_kernel(const int4* __restrict__ feat4,
                                                            const uint32_t* __restrict__ cnt4, int64_t M,
-                                                           const int32_t* __restrict__ kcount,
+                                                           const int32_t* __restrict__ ccount,
                                                            int32_t* __restrict__ kseg_off,
                                                            int32_t* __restrict__ kiters, int4* __restrict__ slot4,
                                                            __nv_bfloat16* __restrict__ aseg, int64_t ld_a,
                                                            int64_t ncols_a, __nv_bfloat16* __restrict__ bseg,
                                                            unsigned long long* rows_acc) {
     __shared__ int wsum[33];
-    __shared__ int off_s;
-    const int b = blockIdx.x;
-    if (threadIdx.x == 0) {
+    __shared__ int off_s, base_s, len_s;
+    const int b = blockIdx.x, c = blockIdx.y, nch = gridDim.y;
+    if (threadIdx.x < 32) {
+        // segment offset: padded lengths of blocks < b; base: rows of chunks < c in block b
         int off = 0;
-        for (int i = 0; i < b; ++i) {
-            const int c = kcount[i];
-            off += c < 64 ? 64 : (c + 63) / 64 * 64;
+        // per-block totals, lane-parallel over chunks
+        for (int bb = 0; bb <= b; ++bb) {
+            int t = 0;
+            for (int i = static_cast<int>(threadIdx.x); i < nch; i += 32) t += ccount[static_cast<size_t>(bb) * nch + i];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (bb < b) off += t < 64 ? 64 : (t + 63) / 64 * 64;
+            else if (threadIdx.x == 0) len_s = t;
         }
-        off_s = off;
+        int base = 0;
+        for (int i = static_cast<int>(threadIdx.x); i < c; i += 32) base += ccount[static_cast<size_t>(b) * nch + i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
+        if (threadIdx.x == 0) {
+            off_s = off;
+            base_s = base;
+        }
     }
     __syncthreads();
-    const int off = off_s;
-    const int len = kcount[b];
+    const int off = off_s, len = len_s;
     const int padded = len < 64 ? 64 : (len + 63) / 64 * 64;
-    if (threadIdx.x == 0) {
+    if (c == 0 && threadIdx.x == 0) {
         kseg_off[b] = off;
         kiters[b] = padded / 64;
         if (rows_acc) atomicAdd(rows_acc, static_cast<unsigned long long>(padded));
     }
-    int base = 0;
-    for (int64_t r0 = 0; r0 < M; r0 += 1024) {
-        const int64_t r = r0 + threadIdx.x;
-        int4 q = make_int4(-1, -1, -1, -1);
-        if (r < M) q = __ldg(feat4 + r);
-        const bool hit = r < M && touches(q, b);
-        int tot;
-        const int rk = block_rank(hit, wsum, &tot);
-        if (hit) {
-            const int slot = off + base + rk;
-            const uint32_t c4 = __ldg(cnt4 + r);
-            int* sl = reinterpret_cast<int*>(slot4 + r);
-            const int f[4] = {q.x, q.y, q.z, q.w};
+    const int64_t r = static_cast<int64_t>(c) * 1024 + threadIdx.x;
+    int4 q = make_int4(-1, -1, -1, -1);
+    if (r < M) q = __ldg(feat4 + r);
+    const bool hit = r < M && touches(q, b);
+    int tot;
+    const int rk = block_rank(hit, wsum, &tot);
+    if (hit) {
+        const int slot = off + base_s + rk;
+        const uint32_t c4 = __ldg(cnt4 + r);
+        int* sl = reinterpret_cast<int*>(slot4 + r);
+        const int f[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (f[j] >= 0 && (f[j] >> 8) == b) {
-                    sl[j] = slot;
-                    bseg[static_cast<size_t>(slot) * 256 + (f[j] & 255)] =
-                        __float2bfloat16_rn(static_cast<float>((c4 >> (8 * j)) & 0xFFu));
-                }
+        for (int j = 0; j < 4; ++j) {
+            if (f[j] >= 0 && (f[j] >> 8) == b) {
+                sl[j] = slot;
+                bseg[static_cast<size_t>(slot) * 256 + (f[j] & 255)] =
+                    __float2bfloat16_rn(static_cast<float>((c4 >> (8 * j)) & 0xFFu));
             }
         }
-        base += tot;
     }
-    // zero the segment's padding rows of A' (B' is zero on entry)
+    // zero the segment's padding rows of A' (B' is zero on entry), split over the chunks
     const int64_t npad = padded - len;
     const int64_t cols8 = ncols_a / 8;  // ld_a and ncols_a are multiples of 8
-    for (int64_t i = threadIdx.x; i < npad * cols8; i += blockDim.x) {
+    for (int64_t i = static_cast<int64_t>(c) * blockDim.x + threadIdx.x; i < npad * cols8;
+         i += static_cast<int64_t>(nch) * blockDim.x) {
         const int64_t rr = off + len + i / cols8, cc = (i % cols8) * 8;
         *reinterpret_cast<uint4*>(aseg + rr * ld_a + cc) = make_uint4(0u, 0u, 0u, 0u);
     }
@@ -831,11 +840,12 @@ cudaError_t launch_kslots(const int4* feat4, const uint32_t* cnt4, int64_t M, in
                           int32_t* kseg_off, int32_t* kiters, int4* slot4, __nv_bfloat16* aseg, int64_t ld_a,
                           int64_t ncols_a, __nv_bfloat16* bseg, unsigned long long* rows_acc, cudaStream_t s) {
     if (nblk <= 0) return cudaSuccess;
-    kslot_count_kernel<<<nblk, 1024, 0, s>>>(feat4, M, nblk, kcount, slot4);
+    const unsigned nch = static_cast<unsigned>(M > 0 ? (M + 1023) / 1024 : 1);
+    kslot_count_kernel<<<dim3(nblk, nch), 1024, 0, s>>>(feat4, M, kcount, slot4);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    kslot_place_kernel<<<nblk, 1024, 0, s>>>(feat4, cnt4, M, kcount, kseg_off, kiters, slot4, aseg, ld_a, ncols_a,
-                                             bseg, rows_acc);
+    kslot_place_kernel<<<dim3(nblk, nch), 1024, 0, s>>>(feat4, cnt4, M, kcount, kseg_off, kiters, slot4, aseg, ld_a,
+                                                        ncols_a, bseg, rows_acc);
     return cudaGetLastError();
 }
 
@@ -854,13 +864,17 @@ cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int
                        const SampleDesc* sd, int64_t global_batch, RowBuffers rows, const float* old_logp,
                        float clip_eps, double* loss_acc, __nv_bfloat16* pexp_t, __nv_bfloat16* phict,
                        int64_t ldt, cudaStream_t s, int rowmajor, int64_t ld_phi) {
-    if (Mpad == 0) return cudaSuccess;
-    int64_t blocks = (Mpad * 8 + 255) / 256;  // 4 rows per warp
-    if (blocks > 148 * 4) blocks = 148 * 4;   // persistent warps: 4 resident 256-thread blocks per SM
     LseArgs L{zact, stats, stats_ld, M, Mpad, V, sd, global_batch, rows, old_logp, clip_eps,
               loss_acc, pexp_t != nullptr, pexp_t, phict, ldt};
     L.rowmajor = rowmajor;
     L.ld_phi = ld_phi;
+    return launch_lse(L, s);
+}
+
+cudaError_t launch_lse(const LseArgs& L, cudaStream_t s) {
+    if (L.Mpad == 0) return cudaSuccess;
+    int64_t blocks = (L.Mpad * 8 + 255) / 256;  // 4 rows per warp
+    if (blocks > 148 * 4) blocks = 148 * 4;     // persistent warps: 4 resident 256-thread blocks per SM
     lse_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(L);
     return cudaGetLastError();
 }

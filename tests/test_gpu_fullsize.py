@@ -185,6 +185,7 @@ def test_c2_stream_k_matches_plain_schedule(ctx, c2_engine, monkeypatch):
     """C2's GEMM2 (2,000 tiles on 74 pairs, 256 K iterations each) with the
     stream-K tail (opt-in FM_G2_STREAMK=1) vs the plain round-robin schedule."""
     mb = _samples(4, 16, 1024, adv_seed=4)
+    monkeypatch.setenv("FM_G2_KLIST", "0")  # stream-K is an option of the dense GEMM2
     g_dp = _fresh_grad(ctx, c2_engine, [mb])
     monkeypatch.setenv("FM_G2_STREAMK", "1")
     g_sk = _fresh_grad(ctx, c2_engine, [mb])
@@ -197,6 +198,7 @@ def test_c2_token_list_gemm2_matches_dense(ctx, c2_engine, monkeypatch, mode):
     """C2 micro-batch through the K-list GEMM2 (16 column blocks, ~23% of the
     16,384 tokens each) vs the dense GEMM2."""
     mb = _samples(5, 16, 1024, adv_seed=5)
+    monkeypatch.setenv("FM_G2_KLIST", "0")
     g_dense = _fresh_grad(ctx, c2_engine, [mb])
     monkeypatch.setenv("FM_G2_KLIST", mode)
     g_kl = _fresh_grad(ctx, c2_engine, [mb])

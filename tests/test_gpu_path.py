@@ -395,6 +395,7 @@ def test_gemm2_k_chunks_match_single_launch(ctx, monkeypatch):
     default): same gradient as one launch up to fp32 summation order; the
     micro-batch grad norm (diagnostic) is reported as NaN when chunked."""
     f = _ld("mid_agent0.npz")
+    monkeypatch.setenv("FM_G2_KLIST", "0")  # K-chunks are an option of the dense GEMM2
     one = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
     monkeypatch.setenv("FM_G2_KCHUNK", "256")
     chunked = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
@@ -454,6 +455,7 @@ def test_gemm2_stream_k_tail(ctx, monkeypatch, V, D_, resp):
     samples = [([int(x) for x in rng.integers(0, V, size=8)], [int(x) for x in rng.integers(0, V, size=resp)])
                for _ in range(16)]
     adv = rng.normal(size=16)
+    monkeypatch.setenv("FM_G2_KLIST", "0")  # stream-K is an option of the dense GEMM2
     g_dp, n_dp = _train_one(ctx, V, D_, samples, adv)
     monkeypatch.setenv("FM_G2_STREAMK", "1")
     g_sk, n_sk = _train_one(ctx, V, D_, samples, adv)
@@ -610,6 +612,7 @@ def test_gemm2_token_lists_match_dense(ctx, monkeypatch, name, mode):
     grad norms; GEMM1 then stores p~ row-major and K-lse folds into the row-major
     operands."""
     f = _ld(f"{name}.npz")
+    monkeypatch.setenv("FM_G2_KLIST", "0")
     dense = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
     monkeypatch.setenv("FM_G2_KLIST", mode)
     kl = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
