@@ -1821,6 +1821,10 @@ int fm_agent_activate(fm_agent* a, fm_ctx* c) {
     const size_t P = a->P;
     // the parked copy must have landed before we read it back
     FM_CUDA(cudaStreamWaitEvent(c->copy_in, a->ev_out, 0));
+    // start the copy-in beside the latest queued K-GEMM1 (tensor-bound) rather than
+    // beside whatever runs when it is issued: the latency-bound gather / slot kernels
+    // slowed 4x next to a copy-engine burst (119 vs 28 us per micro-batch)
+    if (c->gemm_seq > 0) FM_CUDA(cudaStreamWaitEvent(c->copy_in, c->ev_gemm, 0));
 
     if (int st = agent_alloc_device(a, c, c->copy_in)) return st;
     uint8_t* p = static_cast<uint8_t*>(a->park);
