@@ -74,6 +74,11 @@ struct GemmArgs {
     const int32_t* kseg_off = nullptr;
     __nv_bfloat16* aseg = nullptr;
     const int4* slot4 = nullptr;
+    // Grad, segments with a software-gathered A (FM_G2_KLIST=3): A rows = p~ rows
+    // pexp[seg_tok[k]] (row-major, pitch ld_pexp) copied by four producer warps per
+    // CTA into the swizzled MN-major stage; B' tile-loaded as in kSeg.
+    const int32_t* seg_tok = nullptr;
+    long long ld_pexp = 0;
 };
 
 // Stream-K workspace capacity: at most 2*pairs-1 split tiles (148 SMs -> 74 pairs).
@@ -92,6 +97,8 @@ cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, in
 // Grad GEMM over token-slot segments (args.kseg_off / klist_iters), MN-major tile maps.
 cudaError_t gemm_kseg_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int num_sms,
                              cudaStream_t stream);
+// Same, A rows gathered by producer warps from args.pexp via args.seg_tok (tmA unused).
+cudaError_t gemm_kseg_swa_launch(const CUtensorMap& tmB, const GemmArgs& args, int num_sms, cudaStream_t stream);
 // Grad GEMM over per-column-tile K lists (args.klist*), gather4 maps for A and B.
 cudaError_t gemm_klist_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int num_sms,
                               cudaStream_t stream);

@@ -109,9 +109,12 @@ cudaError_t launch_klist(const int4* feat4, int64_t M, int nblk, int32_t* klist,
 // entry.  Deterministic (block-wide scans in row order; kcount = per-(block,
 // 1024-row chunk) counts).  rows_acc (nullable)
 // accumulates the padded segment rows (GEMM2's executed K, for the roofline).
+// seg_tok (nullable): the token of every slot (padding slots = zero_row) for the
+// software-gathered A; aseg may then be null (no A' rows are written).
 cudaError_t launch_kslots(const int4* feat4, const uint32_t* cnt4, int64_t M, int nblk, int32_t* kcount,
                           int32_t* kseg_off, int32_t* kiters, int4* slot4, __nv_bfloat16* aseg, int64_t ld_a,
-                          int64_t ncols_a, __nv_bfloat16* bseg, unsigned long long* rows_acc, cudaStream_t s);
+                          int64_t ncols_a, __nv_bfloat16* bseg, unsigned long long* rows_acc, int32_t* seg_tok,
+                          int32_t zero_row, cudaStream_t s);
 
 // Parity tooling: out[v][j] = dW[v][cols[j]] (f32 or f64 accumulator).
 cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D, const int64_t* cols,

@@ -112,6 +112,21 @@ __device__ __forceinline__ double lse_row_quad(const LseArgs& L, int64_t r0) {
         // an action outside [0, V) never matches a vocab row (policy.hpp:84-85): the
         // row still gets -c p, just no delta term
         const float sig = ce != 0.f ? __fdividef(-ce, s) : 0.f;
+        if (L.rowmajor == 3) {
+            // segments with a software-gathered A: p~ stays row-major (delta once per
+            // row, lane 4), the row factor goes into B' through the slot table
+            if (sl == 4 && sig != 0.f && valid)
+                L.pexp_t[static_cast<size_t>(r) * L.ldt + a] = __float2bfloat16_rn(__expf(za - m) - s);
+            if (sl < 4) {
+                const int4 s4 = L.slot4[r];
+                const int sj = sl == 0 ? s4.x : sl == 1 ? s4.y : sl == 2 ? s4.z : s4.w;
+                const int f = sl == 0 ? f4.x : sl == 1 ? f4.y : sl == 2 ? f4.z : f4.w;
+                if (f >= 0 && sj >= 0)
+                    L.bseg[static_cast<size_t>(sj) * 256 + (f & 255)] =
+                        __float2bfloat16_rn(sig * static_cast<float>((c4 >> (8 * sl)) & 0xFFu));
+            }
+            return loss;
+        }
         if (L.rowmajor == 2) {
             // token-slot segments: lane j (< 4) owns feature j — the delta goes into its
             // block's A' row (once per distinct slot), the row factor into B'

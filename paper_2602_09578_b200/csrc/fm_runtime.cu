@@ -140,6 +140,8 @@ struct Workspace {
     int4* slot4 = nullptr;                            // [rows_cap]
     int32_t *kcount = nullptr, *kseg_off = nullptr;   // [nblk][row chunks of 1024], [nblk]
     unsigned long long* kseg_rows = nullptr;          // executed GEMM2 K rows, accumulated
+    int32_t* seg_tok = nullptr;                       // [kp_cap] token of each slot (mode 3)
+    bool seg_has_a = false;                           // A' allocated (mode 2)
     int64_t kp_cap = 0;
     int32_t* klist = nullptr;  // K-list GEMM2: token lists per 256-feature block [nblk][klist_ld]
     int32_t* kiters = nullptr;  // [nblk] list length / 64
@@ -328,6 +330,7 @@ void ws_free(Workspace& w) {
     cudaFree(w.kcount);
     cudaFree(w.kseg_off);
     cudaFree(w.kseg_rows);
+    cudaFree(w.seg_tok);
     cudaFree(w.sk_cnt);
     cudaFree(w.zscratch);
     cudaFree(w.dWmb);
@@ -406,23 +409,26 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
 // Token-slot segments for the segmented K-list GEMM2: every token occupies at
 // most 4 slots (one per distinct feature block), each block's segment is padded
 // to 64 rows.
-int ws_reserve_seg(fm_ctx* c) {
+int ws_reserve_seg(fm_ctx* c, bool need_a) {
     Workspace& w = c->ws;
     const int64_t nblk = static_cast<int64_t>((w.feat_cap + 255) / 256);
     const int64_t need = 4 * w.rows_cap + 64 * nblk;
-    if (w.aseg && w.kp_cap >= need) return FM_OK;
+    if (w.bseg && w.kp_cap >= need && (w.seg_has_a || !need_a)) return FM_OK;
     FM_CUDA(cudaStreamSynchronize(c->stream));
     cudaFree(w.aseg);
     cudaFree(w.bseg);
     cudaFree(w.slot4);
     cudaFree(w.kcount);
     cudaFree(w.kseg_off);
+    cudaFree(w.seg_tok);
     w.aseg = w.bseg = nullptr;
     w.slot4 = nullptr;
-    w.kcount = w.kseg_off = nullptr;
+    w.kcount = w.kseg_off = w.seg_tok = nullptr;
+    w.seg_has_a = false;
     const uint64_t ldz = round_up(w.vocab_cap, 8);
     cudaError_t e = cudaSuccess;
-    e = e ? e : dalloc(&w.aseg, static_cast<size_t>(need) * ldz);
+    if (need_a) e = e ? e : dalloc(&w.aseg, static_cast<size_t>(need) * ldz);
+    e = e ? e : dalloc(&w.seg_tok, static_cast<size_t>(need));
     e = e ? e : dalloc(&w.bseg, static_cast<size_t>(need) * 256);
     e = e ? e : dalloc(&w.slot4, static_cast<size_t>(w.rows_cap));
     e = e ? e : dalloc(&w.kcount, static_cast<size_t>(nblk) * static_cast<size_t>((w.rows_cap + 1023) / 1024 + 1));
@@ -433,6 +439,7 @@ int ws_reserve_seg(fm_ctx* c) {
     }
     if (e != cudaSuccess) return fail(FM_ERR_DEVICE_OOM, std::string("segment workspace: ") + cudaGetErrorString(e));
     w.kp_cap = need;
+    w.seg_has_a = need_a;
     return FM_OK;
 }
 
@@ -1229,8 +1236,10 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             const char* kl_env = std::getenv("FM_G2_KLIST");
             const char kl_mode = kl_env && kl_env[0] ? kl_env[0] : '2';
             const bool klist = fold && gemm_pair_mode() && kl_mode == '1';
-            bool kseg = fold && gemm_pair_mode() && kl_mode == '2';
-            if (kseg && ws_reserve_seg(c) != FM_OK) {
+            bool kseg = fold && gemm_pair_mode() && (kl_mode == '2' || kl_mode == '3');
+            // mode 3: A rows gathered from the row-major p~ by producer warps (no A' copies)
+            const bool swa = kseg && kl_mode == '3';
+            if (kseg && ws_reserve_seg(c, !swa) != FM_OK) {
                 kseg = false;
                 clear_error();
                 cudaGetLastError();
@@ -1264,8 +1273,9 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 KScope k(c, K_GATHER, s);
                 FM_CUDA(cudaMemsetAsync(w.bseg, 0, static_cast<size_t>(w.kp_cap) * 256 * 2, s));
                 FM_CUDA(launch_kslots(rows.feat4, rows.cnt4, M, nblk, w.kcount, w.kseg_off, w.kiters, w.slot4,
-                                      w.aseg, static_cast<int64_t>(ldz), static_cast<int64_t>(ldz), w.bseg,
-                                      w.kseg_rows, s));
+                                      swa ? nullptr : w.aseg, static_cast<int64_t>(ldz), static_cast<int64_t>(ldz),
+                                      w.bseg, w.kseg_rows, swa ? w.seg_tok : nullptr,
+                                      static_cast<int32_t>(w.rows_cap), s));
                 count_launch(2);
             }
             // K-GEMM1: z = Phic * W16^T / n; epilogue stores p~ = exp(z - m) (bf16) with m the
@@ -1284,11 +1294,11 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g1.N = static_cast<int>(a->V);
             g1.K = static_cast<int>(a->D);
             g1.group_m = env_int("FM_G1_GROUP_M", 16);  // raster: m-tiles per group (L2 reuse)
-            if (kseg) {  // p~ rows into the token's segment slots (A')
+            if (kseg && !swa) {  // p~ rows into the token's segment slots (A')
                 g1.mrow = w.mrow;
                 g1.aseg = w.aseg;
                 g1.slot4 = w.slot4;
-            } else if (klist) {  // p~ row-major: the K-list GEMM2 gathers token rows
+            } else if (klist || swa) {  // p~ row-major: the K-list GEMM2 gathers token rows
                 g1.mrow = w.mrow;
                 g1.pexp = w.Pexp;
             } else if (fold) {  // p~^T straight into GEMM2's A operand buffer
@@ -1323,9 +1333,9 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 lse_args.ld_phi = static_cast<int64_t>(a->D);
             }
             if (kseg) {
-                lse_args.pexp_t = w.aseg;
+                lse_args.pexp_t = swa ? w.Pexp : w.aseg;
                 lse_args.ldt = static_cast<int64_t>(ldz);
-                lse_args.rowmajor = 2;
+                lse_args.rowmajor = swa ? 3 : 2;
                 lse_args.slot4 = w.slot4;
                 lse_args.bseg = w.bseg;
             }
@@ -1394,7 +1404,18 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 const int kc = static_cast<int>(round_up(static_cast<uint64_t>(std::min(kc_env, 1 << 30)), 64));
                 const int nch = (static_cast<int>(Mpad) + kc - 1) / kc;
                 KScope k(c, K_GEMM2, s);
-                if (kseg) {
+                if (swa) {
+                    CUtensorMap tSB;
+                    if (!make_tmap_bf16_kmajor(&tSB, w.bseg, static_cast<uint64_t>(w.kp_cap), 256, 64))
+                        return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+                    g2.kseg_off = w.kseg_off;
+                    g2.klist_iters = w.kiters;
+                    g2.seg_tok = w.seg_tok;
+                    g2.pexp = w.Pexp;
+                    g2.ld_pexp = static_cast<long long>(ldz);
+                    g2.sk_ws = nullptr;
+                    FM_CUDA(gemm_kseg_swa_launch(tSB, g2, c->num_sms, s));
+                } else if (kseg) {
                     CUtensorMap tSA, tSB;
                     if (!make_tmap_bf16_kmajor(&tSA, w.aseg, static_cast<uint64_t>(w.kp_cap), a->V, 64, ldz) ||
                         !make_tmap_bf16_kmajor(&tSB, w.bseg, static_cast<uint64_t>(w.kp_cap), 256, 64))

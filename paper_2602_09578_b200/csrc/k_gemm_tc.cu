@@ -597,12 +597,16 @@ constexpr int kThreadsPair = 192;  // w0 TMA, w1 MMA, w2-5 epilogue
 // gather4 from the output column tile's K list (args.klist*).
 // kSeg (Grad): both operands MN-major; column tile nb runs the K rows of its
 // token-slot segment (args.kseg_off / klist_iters); B' holds only 256 columns.
-template <class Epi, bool kAmn = false, bool kBmn = false, bool kKList = false, bool kSeg = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
+// kSwA (with kSeg): warps 6-9 of each CTA gather the A rows (p~ rows of the
+// segment's tokens) with 16-B loads and write them into the swizzled MN-major
+// stage; they and the B TMA arrive on the leader's full barrier (1 + 8 arrivals).
+template <class Epi, bool kAmn = false, bool kBmn = false, bool kKList = false, bool kSeg = false, bool kSwA = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSwA ? 320 : kThreadsPair, 1)
     gemm_tn_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        GemmArgs args) {
     static_assert(!kKList || (kAmn && kBmn), "K-list operands are MN-major");
     static_assert(!kSeg || (kAmn && kBmn), "segment operands are MN-major");
+    static_assert(!kSwA || kSeg, "software A gather runs the segment schedule");
     constexpr uint32_t kId = idesc_bf16_f32<256, BN, kAmn, kBmn>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -625,8 +629,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
         for (int s = 0; s < P_STAGES; ++s) {
-            mbar_init(&full[s], 1);   // the leader's producer arrives with both CTAs' tx bytes
-            mbar_init(&empty[s], 1);  // one multicast commit per consumed stage
+            mbar_init(&full[s], kSwA ? 9 : 1);  // the leader's producer arrives with both CTAs' tx bytes
+            mbar_init(&empty[s], 1);            // one multicast commit per consumed stage
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
@@ -701,9 +705,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                 for (int k = wi.kb; k < wi.ke; ++k) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t fb = mapa_shared(&full[stage], 0);
-                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], kSwA ? 2 * P_B_STAGE : 2 * P_STAGE_BYTES);
                     const int kc = kbase + k * BK;
-                    if constexpr (kAmn) {
+                    if constexpr (kSwA) {
+                        // A comes from the gather warps
+                    } else if constexpr (kAmn) {
                         tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, arow, kc, pol_a);
                         tma_load_2d_2sm(sA + stage * P_A_STAGE + 8192, &tmA, fb, arow + 64, kc, pol_a);
                     } else {
@@ -762,6 +768,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             }
         }
         __syncwarp();
+    } else if (kSwA && warp >= 6) {
+        // ===== A gather (both CTAs): warp aw copies K rows 16aw..16aw+15 of each stage =====
+        // cp.async 16-B pieces straight into the swizzled MN-major stage, one commit group
+        // per stage; a stage is released to the MMA (proxy fence + cluster arrive on the
+        // leader's full barrier) once it is two groups old, so three stages of loads are
+        // in flight per warp without staging registers.
+        const int aw = static_cast<int>(warp) - 6;
+        int stage = 0;
+        uint32_t phase = 0;
+        int pend[2] = {-1, -1};  // stages issued but not yet released (oldest first)
+        auto release_oldest = [&](bool all) {
+            if (all) asm volatile("cp.async.wait_group 0;" ::: "memory");
+            else asm volatile("cp.async.wait_group 2;" ::: "memory");
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(&full[pend[0]], 0));
+            pend[0] = pend[1];
+            pend[1] = -1;
+        };
+        WorkItem wi;
+        for (int w = 0; sch.get(cid, w, wi); ++w) {
+            const TileCoord tc = tile_coord(wi.tile, tiles_m, tiles_n, args.group_m);
+            const int arow = tc.mb * 256 + static_cast<int>(rank) * 128;
+            const int kbase = __ldg(args.kseg_off + tc.nb);
+            const int ke = __ldg(args.klist_iters + tc.nb);
+            for (int k = 0; k < ke; ++k) {
+                const int tok_l = lane < 16 ? __ldg(args.seg_tok + kbase + k * BK + 16 * aw + static_cast<int>(lane)) : 0;
+                mbar_wait(&empty[stage], phase ^ 1);
+                const uint32_t base = smem_u32(sA + stage * P_A_STAGE);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int q = static_cast<int>(lane) + 32 * i;  // 16 tokens x 16 pieces of 16 B
+                    const int t = __shfl_sync(0xffffffffu, tok_l, q >> 4);
+                    const int r = 16 * aw + (q >> 4), p = q & 15, h = p >> 3, c = p & 7;
+                    const int v0 = arow + 8 * p;
+                    const uint32_t dst = base + h * 8192 + r * 128 + ((c ^ (r & 7)) << 4);
+                    const __nv_bfloat16* src = args.pexp + static_cast<size_t>(t) * args.ld_pexp + v0;
+                    const uint32_t nbytes = v0 < args.M ? 16u : 0u;  // zero-fill past the vocab
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(nbytes)
+                                 : "memory");
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+                if (pend[1] >= 0) release_oldest(false);  // the stage issued two groups ago
+                if (pend[0] < 0) pend[0] = stage;
+                else pend[1] = stage;
+                if (++stage == P_STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        while (pend[0] >= 0) release_oldest(true);
     } else {
         // ===== epilogue warps 2..5 (both CTAs; each drains its own 128 rows) =====
         const uint32_t quad = warp & 3;
@@ -935,6 +993,18 @@ cudaError_t gemm_kseg_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, con
     auto k = gemm_tn_2sm_kernel<GradEpi, true, true, false, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     k<<<grid, kThreadsPair, smem, stream>>>(tmA, tmB, args);
+    return cudaGetLastError();
+}
+
+cudaError_t gemm_kseg_swa_launch(const CUtensorMap& tmB, const GemmArgs& args, int num_sms, cudaStream_t stream) {
+    const size_t smem = gemm_smem_bytes();
+    const int tiles = ((args.M + 255) / 256) * ((args.N + BN - 1) / BN);
+    if (tiles == 0) return cudaSuccess;
+    const int pairs = num_sms / 2;
+    const int grid = 2 * (tiles < pairs ? tiles : pairs);
+    auto k = gemm_tn_2sm_kernel<GradEpi, true, true, false, true, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k<<<grid, 320, smem, stream>>>(tmB, tmB, args);
     return cudaGetLastError();
 }
 

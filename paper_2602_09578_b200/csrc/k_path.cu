@@ -772,7 +772,8 @@ __global__ void __launch_bounds__(1024) kslot_place_kernel(const int4* __restric
                                                            int32_t* __restrict__ kiters, int4* __restrict__ slot4,
                                                            __nv_bfloat16* __restrict__ aseg, int64_t ld_a,
                                                            int64_t ncols_a, __nv_bfloat16* __restrict__ bseg,
-                                                           unsigned long long* rows_acc) {
+                                                           unsigned long long* rows_acc, int32_t* __restrict__ seg_tok,
+                                                           int32_t zero_row) {
     __shared__ int wsum[33];
     __shared__ int off_s, base_s, len_s;
     const int b = blockIdx.x, c = blockIdx.y, nch = gridDim.y;
@@ -813,6 +814,7 @@ __global__ void __launch_bounds__(1024) kslot_place_kernel(const int4* __restric
     const int rk = block_rank(hit, wsum, &tot);
     if (hit) {
         const int slot = off + base_s + rk;
+        if (seg_tok) seg_tok[slot] = static_cast<int32_t>(r);
         const uint32_t c4 = __ldg(cnt4 + r);
         int* sl = reinterpret_cast<int*>(slot4 + r);
         const int f[4] = {q.x, q.y, q.z, q.w};
@@ -825,8 +827,15 @@ __global__ void __launch_bounds__(1024) kslot_place_kernel(const int4* __restric
             }
         }
     }
-    // zero the segment's padding rows of A' (B' is zero on entry), split over the chunks
+    // zero the segment's padding rows of A' (B' is zero on entry), split over the chunks;
+    // with a software-gathered A the padding slots point at the zero row instead
     const int64_t npad = padded - len;
+    if (seg_tok) {
+        for (int64_t i = static_cast<int64_t>(c) * blockDim.x + threadIdx.x; i < npad;
+             i += static_cast<int64_t>(nch) * blockDim.x)
+            seg_tok[off + len + i] = zero_row;
+    }
+    if (!aseg) return;
     const int64_t cols8 = ncols_a / 8;  // ld_a and ncols_a are multiples of 8
     for (int64_t i = static_cast<int64_t>(c) * blockDim.x + threadIdx.x; i < npad * cols8;
          i += static_cast<int64_t>(nch) * blockDim.x) {
@@ -838,14 +847,15 @@ __global__ void __launch_bounds__(1024) kslot_place_kernel(const int4* __restric
 
 cudaError_t launch_kslots(const int4* feat4, const uint32_t* cnt4, int64_t M, int nblk, int32_t* kcount,
                           int32_t* kseg_off, int32_t* kiters, int4* slot4, __nv_bfloat16* aseg, int64_t ld_a,
-                          int64_t ncols_a, __nv_bfloat16* bseg, unsigned long long* rows_acc, cudaStream_t s) {
+                          int64_t ncols_a, __nv_bfloat16* bseg, unsigned long long* rows_acc, int32_t* seg_tok,
+                          int32_t zero_row, cudaStream_t s) {
     if (nblk <= 0) return cudaSuccess;
     const unsigned nch = static_cast<unsigned>(M > 0 ? (M + 1023) / 1024 : 1);
     kslot_count_kernel<<<dim3(nblk, nch), 1024, 0, s>>>(feat4, M, kcount, slot4);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     kslot_place_kernel<<<dim3(nblk, nch), 1024, 0, s>>>(feat4, cnt4, M, kcount, kseg_off, kiters, slot4, aseg, ld_a,
-                                                        ncols_a, bseg, rows_acc);
+                                                        ncols_a, bseg, rows_acc, seg_tok, zero_row);
     return cudaGetLastError();
 }
 

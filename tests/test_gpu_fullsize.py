@@ -135,7 +135,7 @@ def _host_gb():
         return 0.0
 
 
-@pytest.mark.parametrize("klist", ["0", "1", "2"])
+@pytest.mark.parametrize("klist", ["0", "1", "2", "3"])
 @pytest.mark.parametrize("cfg_name", ["C3", "C5"])
 def test_large_policy_gradient_matches_sparse_f64_oracle(ctx, cfg_name, klist, monkeypatch):
     """1.05B-parameter policies (C3: V=32,000 D=32,768; C5: V=128,000 D=8,192):
@@ -193,7 +193,7 @@ def test_c2_stream_k_matches_plain_schedule(ctx, c2_engine, monkeypatch):
     assert rel_fro(g_sk, g_dp) < 1e-6
 
 
-@pytest.mark.parametrize("mode", ["1", "2"])
+@pytest.mark.parametrize("mode", ["1", "2", "3"])
 def test_c2_token_list_gemm2_matches_dense(ctx, c2_engine, monkeypatch, mode):
     """C2 micro-batch through the K-list GEMM2 (16 column blocks, ~23% of the
     16,384 tokens each) vs the dense GEMM2."""

@@ -603,7 +603,7 @@ def test_tcgen05_gemm_token_lists(ctx, M, N, rows, seed):
     assert float(err) < 1e-5
 
 
-@pytest.mark.parametrize("mode", ["1", "2"])
+@pytest.mark.parametrize("mode", ["1", "2", "3"])
 @pytest.mark.parametrize("name", ["mid_agent0", "c1_planner"])
 def test_gemm2_token_lists_match_dense(ctx, monkeypatch, name, mode):
     """K-list GEMM2 (FM_G2_KLIST=1: each 256-feature column block sums only the
