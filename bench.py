@@ -1320,7 +1320,7 @@ def config_obj(cfg, args) -> dict:
             "agents": na, "vocab": cfg.vocab, "feat": cfg.feat, "micro_batch": cfg.micro_batch,
             "global_batch": cfg.global_batch, "resp_len": cfg.resp_len,
             "formulation": formulation(args),
-            "l2": "inputs larger than L2 (W16 262 MB, Z 2.1 GB per micro-batch); no flush needed",
+            "l2": "inputs larger than L2 (W16 262 MB; p~ token slots 3.8 GB per micro-batch); no flush needed",
             "parallelism": f"agent-centric placement, dp gangs of max(1, N/{na}) GPUs",
             "experience_store": getattr(args, "store", "host")}
 
