@@ -334,9 +334,52 @@ struct GradEpi {
                 return;
             }
         }
-        if (row >= a.M) return;
         const int nvalid = min(32, a.N - col0);
-        if (nvalid <= 0) return;
+        if (nvalid <= 0) return;  // warp-uniform
+        if (nvalid == 32 && xbuf) {
+            // transposed read-modify-write: stage the warp's 32 rows x 32 columns in smem,
+            // then every load / store instruction covers 4 whole 128-B rows (8 lanes x 16 B
+            // per row) instead of 32 rows x 16 B — the RMW of dW bounds GEMM2 when a tile's
+            // K range is short (C3: 128 feature blocks, ~8 K iterations per tile)
+            const uint32_t lane = threadIdx.x & 31;
+            float part = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+                const float4 acc = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                               __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                if (row < a.M) part += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
+                *reinterpret_cast<float4*>(xbuf + lane * 36 + j) = acc;
+            }
+            sumsq += static_cast<double>(part);
+            __syncwarp();
+            const int row0 = row - static_cast<int>(lane);
+            const int seg = static_cast<int>(lane & 7);
+            float4 o[8];
+            if (a.accumulate) {  // all eight loads in flight before any store
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int rg = row0 + i * 4 + static_cast<int>(lane >> 3);
+                    o[i] = rg < a.M ? __ldcg(reinterpret_cast<const float4*>(a.out + static_cast<size_t>(rg) * a.ld_out + col0) + seg)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int rr = i * 4 + static_cast<int>(lane >> 3);
+                const int rg = row0 + rr;
+                float4 q = *reinterpret_cast<const float4*>(xbuf + rr * 36 + seg * 4);
+                if (a.accumulate) {
+                    q.x += o[i].x;
+                    q.y += o[i].y;
+                    q.z += o[i].z;
+                    q.w += o[i].w;
+                }
+                if (rg < a.M) *(reinterpret_cast<float4*>(a.out + static_cast<size_t>(rg) * a.ld_out + col0) + seg) = q;
+            }
+            __syncwarp();
+            return;
+        }
+        if (row >= a.M) return;
         const float* src = a.out + static_cast<size_t>(row) * a.ld_out + col0;  // this rank's partial
         float* dst = const_cast<float*>(src);
         float part = 0.f;
