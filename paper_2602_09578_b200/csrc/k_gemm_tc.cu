@@ -522,8 +522,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int row = tc.mb * BM + row_in_tile;
-            epi.begin(args, row);
-            if constexpr (std::is_same_v<Epi, GradEpi>) epi.sumsq = 0.0;
+            if constexpr (std::is_same_v<Epi, GradEpi>) {
+                epi.begin(args, row);
+                epi.sumsq = 0.0;
+            }
             if (Epi::kTwoPass && !args.mrow) {
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
@@ -878,9 +880,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSwA ? 320 : kThread
         WorkItem wi;
         for (int w = 0; sch.get(cid, w, wi); ++w) {
             const TileCoord tc = tile_coord(wi.tile, tiles_m, tiles_n, args.group_m);
+            const int row = tc.mb * 256 + row_in_tile;
+            // per-row epilogue operands (scale, action, bound, token slots) are loaded while
+            // the accumulator is still being produced, not after it is ready
+            if constexpr (std::is_same_v<Epi, LogitsEpi>) epi.begin(args, row);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int row = tc.mb * 256 + row_in_tile;
             if constexpr (std::is_same_v<Epi, GradEpi>) {
                 if (wi.sk >= 0) {
                     // stream-K partial: add this K range's accumulator into the tile's
