@@ -18,59 +18,8 @@
 // up to 128): packed rows, Phic [Mpad][D] / Phic^T [D][Mpad] bf16 (integer
 // counts; K-lse rescales Phic^T's entries per row), p~^T [V][Mpad] bf16
 // (GEMM1's output = GEMM2's A operand), softmax partials [Mpad][V/256].
-#include <cuda.h>
-#include <cuda_bf16.h>
-#include <cuda_runtime.h>
-#include <nccl.h>
+#include "fm_state.h"
 
-#include <algorithm>
-#include <atomic>
-#include <cmath>
-#include <cstdio>
-#include <cstring>
-#include <map>
-#include <mutex>
-#include <string>
-#include <unordered_map>
-#include <vector>
-
-#include "fm_gemm.h"
-#include "fm_internal.h"
-#include "fm_kernels.h"
-
-using namespace fm;
-
-namespace {
-
-constexpr int kReportRing = 256;
-constexpr int kStagingSlots = 4;
-
-// ---- driver entry point for cuTensorMapEncodeTiled (no -lcuda link) -------
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-    static EncodeTiledFn fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeTiledFn>(p);
-    });
-    return fn;
-}
-
-template <typename T>
-cudaError_t dalloc(T** p, size_t n) {
-    *p = nullptr;
-    if (n == 0) return cudaSuccess;
-    return cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
-}
-
-}  // namespace
 
 namespace fm {
 
@@ -114,115 +63,6 @@ bool make_tmap_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, ui
 
 }  // namespace fm
 
-// ===========================================================================
-// context
-// ===========================================================================
-struct Workspace {
-    int64_t rows_cap = 0;  // Mpad capacity
-    uint64_t vocab_cap = 0, feat_cap = 0;
-    int32_t* action = nullptr;
-    int4* ctx4 = nullptr;
-    int4* feat4 = nullptr;
-    uint32_t* cnt4 = nullptr;
-    int32_t* n_ctx = nullptr;
-    int32_t* sample = nullptr;
-    float *coef = nullptr, *rscale = nullptr, *lse = nullptr, *logp = nullptr, *coef_eff = nullptr;
-    float* old_logp = nullptr;
-    __nv_bfloat16 *phic = nullptr, *phict = nullptr, *gt = nullptr;
-    __nv_bfloat16* Pexp = nullptr;  // p~ = exp(z - m_tile) [Mpad][ldz] bf16
-    float* zact = nullptr;          // logit of the taken token [Mpad]
-    float2* stats = nullptr;
-    float* mrow = nullptr;  // loss fold: per-row softmax offset bound [Mpad]
-    unsigned* lse_sync = nullptr;  // fused K-lse: {CTAs arrived, epoch published} (GEMM1 tail)
-    unsigned lse_epoch = 0;
-    // segmented K-list GEMM2 (FM_G2_KLIST=2), allocated on first use
-    __nv_bfloat16 *aseg = nullptr, *bseg = nullptr;  // A' [kp_cap][ldz], B' [kp_cap][256]
-    int4* slot4 = nullptr;                            // [rows_cap]
-    int32_t *kcount = nullptr, *kseg_off = nullptr;   // [nblk][row chunks of 1024], [nblk]
-    unsigned long long* kseg_rows = nullptr;          // executed GEMM2 K rows, accumulated
-    int32_t* seg_tok = nullptr;                       // [kp_cap] token of each slot (mode 3)
-    bool seg_has_a = false;                           // A' allocated (mode 2)
-    int64_t kp_cap = 0;
-    int32_t* klist = nullptr;  // K-list GEMM2: token lists per 256-feature block [nblk][klist_ld]
-    int32_t* kiters = nullptr;  // [nblk] list length / 64
-    int64_t klist_ld = 0;
-    float* sk_ws = nullptr;  // GEMM2 stream-K tail: partial tiles [kSkMaxTiles][256][256] (zero between launches)
-    int* sk_cnt = nullptr;   // [kSkMaxTiles][2] arrivals per tile half (self-resetting)
-    // parity mode scratch
-    int64_t prow_cap = 0;
-    uint64_t pvocab_cap = 0, pparam_cap = 0;
-    double *zscratch = nullptr, *dWmb = nullptr, *logp64 = nullptr;
-    SampleDesc* sd = nullptr;
-    int sd_cap = 0;
-    // Phic / Phic^T hold exactly the entries of the rows in the row buffers
-    // (for phi_Mpad, phi_D): the next gather erases them row by row
-    bool phi_valid = false;
-    int64_t phi_Mpad = 0;
-    uint64_t phi_D = 0;
-};
-
-// Per-kernel device timing (bench.py's roofline): event pairs recorded on the
-// launching stream around each hot-path kernel when enabled.
-enum KKind { K_GATHER = 0, K_GEMM1, K_LSE, K_SOFTMAX_GRAD, K_GEMM2, K_ADAM, K_PARITY, K_MEMSET, K_COLMAX, K_NKINDS };
-struct KTimer {
-    bool on = false;
-    std::vector<cudaEvent_t> pool;
-    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> open;
-    double ms[K_NKINDS] = {};
-    int64_t count[K_NKINDS] = {};
-    cudaEvent_t get() {
-        if (pool.empty()) {
-            cudaEvent_t e;
-            cudaEventCreate(&e);
-            return e;
-        }
-        cudaEvent_t e = pool.back();
-        pool.pop_back();
-        return e;
-    }
-};
-
-// One training slot: the device home of an active agent's {W, m, v, dW, W16}.
-// Slots are allocated once and recycled across activate/suspend (the
-// reference's training_slots, config.hpp:89); reuse is ordered on the GPU by
-// the event recorded after the previous tenant's copy-out.
-struct Slot {
-    void* base = nullptr;
-    size_t cap = 0;
-    bool busy = false;
-    cudaEvent_t ev_free = nullptr;
-};
-
-struct fm_ctx {
-    int device = 0;
-    KTimer kt;
-    std::vector<Slot*> slots;
-    cudaEvent_t t0 = nullptr, t1 = nullptr;
-    int num_sms = 148;
-    cudaStream_t stream = nullptr;    // compute
-    cudaStream_t copy_in = nullptr;   // swap-in (H2D / D2D / P2P)
-    cudaStream_t copy_out = nullptr;  // swap-out
-    // the latest K-GEMM1 launch on the compute stream (swap copies start there, see
-    // fm_agent_suspend) and the op sequence numbers that say what it follows
-    cudaEvent_t ev_gemm = nullptr;
-    std::map<std::string, void*> ipc_cache;  // peer buffers mapped over NVLink (slots, gang receive buffers)
-    std::vector<std::pair<size_t, void*>> recv_pool;  // gang receive buffers + barrier tokens, recycled
-    std::unordered_map<void*, size_t> pool_sizes;
-    uint64_t op_seq = 0, gemm_seq = 0;
-    uint8_t* arena = nullptr;
-    uint64_t arena_cap = 0, arena_used = 0;
-    std::unordered_map<uint64_t, uint64_t> arena_ntok;  // offset -> token count
-    Workspace ws;
-    bool last_kseg = false;  // the last tensor-core micro-batch ran the segmented GEMM2
-    // pinned staging (sample descriptors, host payloads) with reuse events
-    uint8_t* staging[kStagingSlots] = {};
-    size_t staging_cap[kStagingSlots] = {};
-    cudaEvent_t staging_ev[kStagingSlots] = {};
-    int staging_next = 0;
-    // arena region reserved for the end-to-end host path
-    uint64_t e2e_off = 0, e2e_cap = 0;
-};
-
 namespace fm {
 uint64_t arena_token_count(const fm_ctx* ctx, uint64_t offset, bool* found) {
     auto it = ctx->arena_ntok.find(offset);
@@ -231,7 +71,7 @@ uint64_t arena_token_count(const fm_ctx* ctx, uint64_t offset, bool* found) {
 }
 }  // namespace fm
 
-namespace {
+namespace fm {
 
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
@@ -534,28 +374,8 @@ RowBuffers row_buffers(Workspace& w) {
     return r;
 }
 
-// RAII event pair around one launch (no-op unless kernel timing is on).
-struct KScope {
-    fm_ctx* c;
-    int kind;
-    cudaStream_t s;
-    cudaEvent_t e0 = nullptr;
-    KScope(fm_ctx* c_, int k, cudaStream_t s_) : c(c_), kind(k), s(s_) {
-        if (c->kt.on) {
-            e0 = c->kt.get();
-            cudaEventRecord(e0, s);
-        }
-    }
-    ~KScope() {
-        if (e0) {
-            cudaEvent_t e1 = c->kt.get();
-            cudaEventRecord(e1, s);
-            c->kt.open.push_back({kind, {e0, e1}});
-        }
-    }
-};
 
-}  // namespace
+}  // namespace fm
 
 extern "C" {
 
@@ -750,93 +570,7 @@ uint64_t fm_arena_used(const fm_ctx* c) { return c->arena_used; }
 
 }  // extern "C"
 
-// ===========================================================================
-// agents
-// ===========================================================================
-// DP gang of an agent with the fused reduce-scatter: V rows are
-// split into g contiguous, 256-row-aligned shards; during the step's last
-// micro-batch GEMM2 writes the partials of rows owned by another rank into
-// that rank's receive slot over NVLink (IPC-mapped), then each rank runs the
-// sharded Adam on its rows and writes the new bf16 rows into every peer's
-// W16.  Two 1-element NCCL all-reduces on the compute stream serve as the
-// device-side barriers (after the exchange; the update grad-norm reduction
-// after Adam), so no host round trip or spin-wait is involved.
-#define FM_NCCL(expr)                                                                          \
-    do {                                                                                       \
-        ncclResult_t _r = (expr);                                                              \
-        if (_r != ncclSuccess) return fail(FM_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
-    } while (0)
-
-struct fm_comm;
-struct GangState;
-static ncclComm_t gang_comm(GangState* gs);
-struct GangState {
-    fm_comm* comm = nullptr;
-    int rank = 0, g = 1;
-    int64_t lo[9] = {};          // row boundaries of the shards
-    float* recv = nullptr;       // [g-1][own_rows][D] partials from the peers
-    float* peer_slot[8] = {};    // my slot inside peer o's receive buffer
-    __nv_bfloat16* peer_w16[8] = {};
-    uint8_t* peer_base[8] = {};  // peer o's training slot (same layout as ours)
-    int* d_token = nullptr;      // 1-int all-reduce used as a device barrier
-    bool connected = false;
-};
-
-struct fm_agent {
-    fm_ctx* ctx = nullptr;  // GPU the agent is bound to (null while suspended)
-    std::string name;
-    uint64_t V = 0, D = 0, P = 0;
-    int precision = FM_PRECISION_BF16_TC;
-    // device state
-    double* W = nullptr;
-    float* m = nullptr;
-    float* v = nullptr;
-    void* dW = nullptr;  // float (TC) or double (parity)
-    __nv_bfloat16* W16 = nullptr;
-    int* colmax = nullptr;          // K-colmax keys of W16 [D] (loss-fold softmax bound)
-    uint64_t w16_gen = 0;           // bumped whenever W16 is rewritten
-    uint64_t cm_gen = ~0ull;        // the W16 generation colmax describes
-    bool cm_parked = false;         // the parked copy carries a valid colmax
-    bool dw_valid = false;  // dW holds this step's partial sum
-    bool pending_in = false;  // a swap-in copy the next use must wait for
-    bool park_w16 = false;    // the parked copy includes the bf16 shadow
-    int64_t step = 0, version = 0, samples = 0;
-    // reports
-    double* d_scalars = nullptr;  // [kReportRing][2]: sumsq, loss
-    uint64_t last_seq = 0;        // ctx op sequence number of the agent's last compute op
-    double* h_scalars = nullptr;  // pinned mirror
-    cudaEvent_t ev[kReportRing] = {};
-    int64_t rep_tokens[kReportRing] = {};
-    int64_t rep_bs[kReportRing] = {};
-    int64_t next_ticket = 0;
-    bool dp = false;
-    int shard_rank = 0, shard_count = 1;  // token-balanced DP shard of every micro-batch
-    double* d_upd = nullptr;  // update sum g^2
-    double* h_upd = nullptr;
-    int64_t last_rows = 0;
-    // PPO clip
-    float clip_eps = 0.f;
-    bool have_old_logp = false;
-    // swap
-    bool active = false;
-    int park_tier = -1;
-    int park_device = -1;
-    void* park = nullptr;  // W | m | v | dW   (host pinned or device)
-    size_t park_bytes = 0;
-    cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_compute = nullptr;
-    cudaEvent_t ev_ipc = nullptr;  // interprocess: the source's work before a migration is done
-    bool lent = false;             // exported by migration; slot reserved until migrate_release
-    Slot* slot = nullptr;
-    GangState* gang = nullptr;
-};
-
-// Device-side barrier across the gang (defined with the NCCL section below).
-static int gang_barrier(fm_agent* a);
-// Copies a full [V][D] state buffer (slot offset off, elem bytes/param) to dst
-// (host or device), gathering a DP gang's row shards (defined below).
-static int copy_state(fm_agent* a, size_t off, size_t elem, void* dst, cudaStream_t s);
-
-namespace {
+namespace fm {
 
 size_t dw_elem(const fm_agent* a) { return a->precision == FM_PRECISION_PARITY_F64 ? 8 : 4; }
 
@@ -922,7 +656,7 @@ int check_active(fm_agent* a) {
     return FM_OK;
 }
 
-}  // namespace
+}  // namespace fm
 
 extern "C" {
 
@@ -1638,8 +1372,6 @@ int fm_agent_poll_report(fm_agent* a, int64_t ticket, fm_report* out) {
     return 1;
 }
 
-static int park_reserve(fm_agent* a, fm_ctx* c, int tier, int pdev, size_t bytes);
-static size_t park_bytes_for(const fm_agent* a);
 
 // apply_global_update; with park != 0 (device tier, tensor-core agent, no gang)
 // K-adam writes the new W / m / v / W16 / colmax straight into the agent's
@@ -1736,316 +1468,9 @@ int fm_apply_update_park(fm_agent* a, int64_t G, double lr, double b1, double b2
     FM_GUARD_END
 }
 
-// ---------------------------------------------------------------------------
-// training-state swap
-// ---------------------------------------------------------------------------
-// Park layout: W | m | v | dW | W16 | colmax keys.
-static size_t park_bytes_for(const fm_agent* a) {
-    return a->P * 16 + a->P * dw_elem(a) + (a->W16 ? a->P * 2 + a->D * 4 : 0);
-}
+}  // extern "C"
 
-// Parking buffer of `bytes` on `tier` (device pdev), reused while it fits.
-static int park_reserve(fm_agent* a, fm_ctx* c, int tier, int pdev, size_t bytes) {
-    if (a->park && (a->park_tier != tier || a->park_device != pdev || a->park_bytes < bytes)) {
-        FM_CUDA(cudaStreamSynchronize(c->copy_out));
-        if (a->park_tier == FM_TIER_HOST) cudaFreeHost(a->park);
-        else {
-            cudaSetDevice(a->park_device);
-            cudaFree(a->park);
-            cudaSetDevice(c->device);
-        }
-        a->park = nullptr;
-    }
-    if (!a->park) {
-        if (tier == FM_TIER_HOST) {
-            if (cudaHostAlloc(&a->park, bytes, cudaHostAllocDefault) != cudaSuccess)
-                return fail(FM_ERR_HOST_OOM, "pinned parking buffer");
-        } else if (tier == FM_TIER_DEVICE || tier == FM_TIER_PEER) {
-            if (tier == FM_TIER_PEER) {
-                int can = 0;
-                FM_CUDA(cudaDeviceCanAccessPeer(&can, c->device, pdev));
-                if (!can) return fail(FM_ERR_CONFIG_ERROR, "no peer access to device " + std::to_string(pdev));
-                cudaError_t pe = cudaDeviceEnablePeerAccess(pdev, 0);
-                if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) FM_CUDA(pe);
-                cudaGetLastError();
-                FM_CUDA(cudaSetDevice(pdev));
-            }
-            const cudaError_t e = cudaMalloc(&a->park, bytes);
-            FM_CUDA(cudaSetDevice(c->device));
-            if (e != cudaSuccess) return fail(FM_ERR_DEVICE_OOM, "parking buffer");
-        } else {
-            return fail(FM_ERR_INVALID_ARG, "unknown tier");
-        }
-        a->park_tier = tier;
-        a->park_device = pdev;
-        a->park_bytes = bytes;
-    }
-    return FM_OK;
-}
-
-int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
-    FM_GUARD_BEGIN
-    // a K-GEMM1 launched after the agent's last op (e.g. the next agent's first
-    // micro-batch) is a safe and cheap start for the copy-out: the copy engines then
-    // overlap tensor-bound GEMMs instead of the latency-bound K-gather that follows
-    // the end of the currently queued work (measured: K-gather 16 us -> 390 us
-    // beside a 2.4 GB D2D copy)
-    const bool gated = a->active && a->ctx && a->ctx->gemm_seq > a->last_seq;
-    if (int st = check_active(a)) return st;
-    if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang (fm_gang_detach first)");
-    fm_ctx* c = a->ctx;
-    if (int st = set_dev(c)) return st;
-    const size_t P = a->P;
-    const size_t dwb = a->dw_valid ? P * dw_elem(a) : 0;
-    // park layout: W | m | v | dW | W16.  The bf16 shadow travels on the HBM /
-    // NVLink tiers (a copy-engine copy is cheaper than regenerating it on the
-    // SMs); over PCIe it is regenerated from W on activation instead.
-    const bool park_w16 = a->W16 && tier != FM_TIER_HOST;
-    const size_t bytes = park_bytes_for(a);
-    const int pdev = tier == FM_TIER_PEER ? peer_device : c->device;
-    if (int st = park_reserve(a, c, tier, pdev, bytes)) return st;
-    // order the copy-out after everything the agent has queued on the compute stream
-    if (gated) {
-        FM_CUDA(cudaStreamWaitEvent(c->copy_out, c->ev_gemm, 0));
-    } else {
-        FM_CUDA(cudaEventRecord(a->ev_compute, c->stream));
-        FM_CUDA(cudaStreamWaitEvent(c->copy_out, a->ev_compute, 0));
-    }
-    uint8_t* p = static_cast<uint8_t*>(a->park);
-    auto cp = [&](void* dst, const void* src, size_t n) -> cudaError_t {
-        if (tier == FM_TIER_PEER) return cudaMemcpyPeerAsync(dst, pdev, src, c->device, n, c->copy_out);
-        return cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, c->copy_out);
-    };
-    FM_CUDA(cp(p, a->W, P * 8));
-    FM_CUDA(cp(p + P * 8, a->m, P * 4));
-    FM_CUDA(cp(p + P * 12, a->v, P * 4));
-    if (dwb) FM_CUDA(cp(p + P * 16, a->dW, dwb));  // only mid-step gradients travel
-    if (park_w16) FM_CUDA(cp(p + P * (16 + dw_elem(a)), a->W16, P * 2));
-    a->park_w16 = park_w16;
-    a->cm_parked = park_w16 && a->cm_gen == a->w16_gen;
-    if (a->cm_parked) FM_CUDA(cp(p + P * (18 + dw_elem(a)), a->colmax, a->D * 4));
-    FM_CUDA(cudaEventRecord(a->ev_out, c->copy_out));
-    agent_free_device(a, c->copy_out);
-    a->active = false;
-    a->ctx = nullptr;
-    a->park_device = pdev;
-    return FM_OK;
-    FM_GUARD_END
-}
-
-int fm_agent_activate(fm_agent* a, fm_ctx* c) {
-    FM_GUARD_BEGIN
-    if (a->active) return fail(FM_ERR_CONFIG_ERROR, a->name + " already active");
-    if (a->lent) return fail(FM_ERR_CONFIG_ERROR, a->name + " was migrated away (fm_agent_migrate_release)");
-    if (!c) return fail(FM_ERR_NO_DEVICE, "null context");
-    if (int st = set_dev(c)) return st;
-    const size_t P = a->P;
-    // the parked copy must have landed before we read it back
-    FM_CUDA(cudaStreamWaitEvent(c->copy_in, a->ev_out, 0));
-    // start the copy-in beside the latest queued K-GEMM1 (tensor-bound) rather than
-    // beside whatever runs when it is issued: the latency-bound gather / slot kernels
-    // slowed 4x next to a copy-engine burst (119 vs 28 us per micro-batch)
-    if (c->gemm_seq > 0) FM_CUDA(cudaStreamWaitEvent(c->copy_in, c->ev_gemm, 0));
-
-    if (int st = agent_alloc_device(a, c, c->copy_in)) return st;
-    uint8_t* p = static_cast<uint8_t*>(a->park);
-    const bool peer = a->park_tier != FM_TIER_HOST && a->park_device != c->device;
-    if (peer) {
-        int can = 0;
-        FM_CUDA(cudaDeviceCanAccessPeer(&can, c->device, a->park_device));
-        if (!can) return fail(FM_ERR_CONFIG_ERROR, "no peer access to parking device");
-        cudaError_t pe = cudaDeviceEnablePeerAccess(a->park_device, 0);
-        if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) FM_CUDA(pe);
-        cudaGetLastError();
-    }
-    auto cp = [&](void* dst, const void* src, size_t n) -> cudaError_t {
-        if (peer) return cudaMemcpyPeerAsync(dst, c->device, src, a->park_device, n, c->copy_in);
-        return cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, c->copy_in);
-    };
-    FM_CUDA(cp(a->W, p, P * 8));
-    FM_CUDA(cp(a->m, p + P * 8, P * 4));
-    FM_CUDA(cp(a->v, p + P * 12, P * 4));
-    if (a->dw_valid) FM_CUDA(cp(a->dW, p + P * 16, P * dw_elem(a)));
-    if (a->W16 && a->park_w16) {
-        FM_CUDA(cp(a->W16, p + P * (16 + dw_elem(a)), P * 2));
-    } else if (a->W16) {
-        FM_CUDA(launch_to_bf16(a->W, a->W16, P, c->num_sms, c->copy_in));  // shadow regenerated
-        count_launch();
-    }
-    if (a->W16 && a->park_w16 && a->cm_parked) FM_CUDA(cp(a->colmax, p + P * (18 + dw_elem(a)), a->D * 4));
-    FM_CUDA(cudaEventRecord(a->ev_in, c->copy_in));
-    ++a->w16_gen;
-    if (a->W16 && a->park_w16 && a->cm_parked) a->cm_gen = a->w16_gen;
-    a->pending_in = true;  // consumers wait lazily (check_active)
-    a->ctx = c;
-    a->active = true;
-    return FM_OK;
-    FM_GUARD_END
-}
-
-// ---- cross-process migration over NVLink (location-agnostic swap between GPUs) ----
-// The sender lends its live training slot: it exports CUDA IPC handles of the
-// slot and of an interprocess event recorded on its compute stream after the
-// agent's queued work, and stops using the agent.  The receiver maps the slot
-// (mappings are cached per context: slots are recycled, so after the first hop
-// a migration is just the copy) and pulls the state into its own slot with
-// copy-engine NVLink peer copies on its copy stream.  No park copy on the
-// source.  The sender returns the slot to its pool with fm_agent_migrate_release
-// once the receiver's import has returned (training.hpp:259-350 with a
-// placement change; SURVEY §8e "agents <-> GPUs").
-namespace {
-struct MigrateBlob {
-    uint32_t magic;  // 'FMMG'
-    int32_t precision;
-    uint64_t V, D;
-    int32_t src_device;
-    uint8_t dw_valid, cm_valid, pad0, pad1;
-    int64_t step, version, samples;
-    uint64_t off_w, off_m, off_v, off_dw, off_w16, off_cm;  // within the slot
-    cudaIpcMemHandle_t mem;
-    cudaIpcEventHandle_t ev;
-};
-constexpr uint32_t kMigrateMagic = 0x474d4d46u;
-}  // namespace
-
-static int migrate_export_impl(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64_t* len, bool share);
-
-int fm_agent_migrate_export(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64_t* len) {
-    return migrate_export_impl(a, blob_out, cap, len, false);
-}
-
-// Same blob, but the agent stays active here: several processes may import it
-// (a DP gang forming around the agent); the caller enqueues no work for it
-// until every importer returned.
-int fm_agent_share_export(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64_t* len) {
-    return migrate_export_impl(a, blob_out, cap, len, true);
-}
-
-static int migrate_export_impl(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64_t* len, bool share) {
-    FM_GUARD_BEGIN
-    *len = sizeof(MigrateBlob);
-    if (!blob_out) return FM_OK;
-    if (cap < sizeof(MigrateBlob)) return fail(FM_ERR_INVALID_ARG, "blob buffer too small");
-    if (int st = check_active(a)) return st;
-    if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang (fm_gang_detach first)");
-    fm_ctx* c = a->ctx;
-    if (int st = set_dev(c)) return st;
-    if (!a->ev_ipc) FM_CUDA(cudaEventCreateWithFlags(&a->ev_ipc, cudaEventDisableTiming | cudaEventInterprocess));
-    FM_CUDA(cudaEventRecord(a->ev_ipc, c->stream));  // after everything queued for the agent
-    const uint8_t* base = static_cast<const uint8_t*>(a->slot->base);
-    auto off = [&](const void* q) { return static_cast<uint64_t>(static_cast<const uint8_t*>(q) - base); };
-    MigrateBlob b{};
-    b.magic = kMigrateMagic;
-    b.precision = a->precision;
-    b.V = a->V;
-    b.D = a->D;
-    b.src_device = c->device;
-    b.dw_valid = a->dw_valid;
-    b.cm_valid = a->W16 && a->cm_gen == a->w16_gen;
-    b.step = a->step;
-    b.version = a->version;
-    b.samples = a->samples;
-    b.off_w = off(a->W);
-    b.off_m = off(a->m);
-    b.off_v = off(a->v);
-    b.off_dw = off(a->dW);
-    b.off_w16 = a->W16 ? off(a->W16) : 0;
-    b.off_cm = a->colmax ? off(a->colmax) : 0;
-    FM_CUDA(cudaIpcGetMemHandle(&b.mem, a->slot->base));
-    FM_CUDA(cudaIpcGetEventHandle(&b.ev, a->ev_ipc));
-    std::memcpy(blob_out, &b, sizeof(b));
-    if (!share) {
-        a->active = false;  // lent: the slot stays reserved until fm_agent_migrate_release
-        a->lent = true;
-    }
-    return FM_OK;
-    FM_GUARD_END
-}
-
-int fm_agent_migrate_release(fm_agent* a) {
-    FM_GUARD_BEGIN
-    if (!a->lent) return fail(FM_ERR_CONFIG_ERROR, a->name + " was not exported");
-    fm_ctx* c = a->ctx;
-    if (int st = set_dev(c)) return st;
-    agent_free_device(a, c->stream);
-    a->lent = false;
-    a->ctx = nullptr;
-    a->dw_valid = false;
-    return FM_OK;
-    FM_GUARD_END
-}
-
-int fm_agent_migrate_import(fm_agent* a, fm_ctx* c, const uint8_t* blob, uint64_t len) {
-    FM_GUARD_BEGIN
-    if (len != sizeof(MigrateBlob)) return fail(FM_ERR_INVALID_ARG, "migration blob size mismatch");
-    MigrateBlob b;
-    std::memcpy(&b, blob, sizeof(b));
-    if (b.magic != kMigrateMagic) return fail(FM_ERR_INVALID_ARG, "not a migration blob");
-    if (b.V != a->V || b.D != a->D || b.precision != a->precision)
-        return fail(FM_ERR_CONFIG_ERROR, "migration blob describes another model shape/precision");
-    if (!a->active || a->ctx != c) return fail(FM_ERR_INACTIVE_GROUP, a->name + " must be active on the target GPU");
-    if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang");
-    if (int st = set_dev(c)) return st;
-    void* src = nullptr;
-    if (int st = ipc_open_cached(c, b.mem, &src)) return st;
-    cudaEvent_t ev = nullptr;
-    FM_CUDA(cudaIpcOpenEventHandle(&ev, b.ev));
-    // after everything already queued on the agent's slot, and after the source's queued work
-    FM_CUDA(cudaEventRecord(a->ev_compute, c->stream));
-    FM_CUDA(cudaStreamWaitEvent(c->copy_in, a->ev_compute, 0));
-    FM_CUDA(cudaStreamWaitEvent(c->copy_in, ev, 0));
-    const size_t P = a->P;
-    const uint8_t* p = static_cast<const uint8_t*>(src);
-    auto cp = [&](void* dst, uint64_t off, size_t n) {
-        return cudaMemcpyPeerAsync(dst, c->device, p + off, b.src_device, n, c->copy_in);
-    };
-    FM_CUDA(cp(a->W, b.off_w, P * 8));
-    FM_CUDA(cp(a->m, b.off_m, P * 4));
-    FM_CUDA(cp(a->v, b.off_v, P * 4));
-    if (b.dw_valid) FM_CUDA(cp(a->dW, b.off_dw, P * dw_elem(a)));
-    if (a->W16) FM_CUDA(cp(a->W16, b.off_w16, P * 2));
-    if (a->W16 && b.cm_valid) FM_CUDA(cp(a->colmax, b.off_cm, a->D * 4));
-    FM_CUDA(cudaEventRecord(a->ev_in, c->copy_in));
-    a->dw_valid = b.dw_valid;
-    a->step = b.step;
-    a->version = b.version;
-    a->samples = b.samples;
-    ++a->w16_gen;
-    a->cm_gen = (a->W16 && b.cm_valid) ? a->w16_gen : ~0ull;
-    a->pending_in = true;  // consumers wait lazily (check_active)
-    // the source may release its slot once this returns
-    FM_CUDA(cudaEventSynchronize(a->ev_in));
-    cudaEventDestroy(ev);
-    return FM_OK;
-    FM_GUARD_END
-}
-
-int fm_agent_state_checksum(fm_agent* a, uint64_t* out) {
-    FM_GUARD_BEGIN
-    if (int st = check_active(a)) return st;
-    if (int st = set_dev(a->ctx)) return st;
-    FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
-    const size_t P = a->P;
-    std::vector<uint8_t> buf(P * (16 + dw_elem(a)));
-    FM_CUDA(cudaMemcpy(buf.data(), a->W, P * 8, cudaMemcpyDeviceToHost));
-    FM_CUDA(cudaMemcpy(buf.data() + P * 8, a->m, P * 4, cudaMemcpyDeviceToHost));
-    FM_CUDA(cudaMemcpy(buf.data() + P * 12, a->v, P * 4, cudaMemcpyDeviceToHost));
-    if (a->dw_valid) FM_CUDA(cudaMemcpy(buf.data() + P * 16, a->dW, P * dw_elem(a), cudaMemcpyDeviceToHost));
-    else std::fill(buf.begin() + P * 16, buf.end(), 0);
-    uint64_t h = 0xcbf29ce484222325ULL;
-    for (uint8_t b : buf) {
-        h ^= b;
-        h *= 0x100000001b3ULL;
-    }
-    for (int64_t x : {a->step, a->version, a->samples}) {
-        h ^= static_cast<uint64_t>(x);
-        h *= 0x100000001b3ULL;
-    }
-    *out = h;
-    return FM_OK;
-    FM_GUARD_END
-}
-
+extern "C" {
 // ---------------------------------------------------------------------------
 // GRPO advantages on device
 // ---------------------------------------------------------------------------
@@ -2070,666 +1495,6 @@ int fm_group_advantages(fm_ctx* c, const double* rewards, const int32_t* seg_off
     FM_CUDA(cudaFreeAsync(dr, s));
     FM_CUDA(cudaFreeAsync(dout, s));
     FM_CUDA(cudaFreeAsync(doff, s));
-    FM_CUDA(cudaStreamSynchronize(s));
-    return FM_OK;
-    FM_GUARD_END
-}
-
-// ---------------------------------------------------------------------------
-// NCCL gang
-// ---------------------------------------------------------------------------
-struct fm_comm {
-    ncclComm_t comm = nullptr;
-    int nranks = 1, rank = 0;
-    fm_ctx* ctx = nullptr;
-};
-
-#define FM_NCCL(expr)                                                                          \
-    do {                                                                                       \
-        ncclResult_t _r = (expr);                                                              \
-        if (_r != ncclSuccess) return fail(FM_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r)); \
-    } while (0)
-
-int fm_comm_unique_id(uint8_t out[128]) {
-    ncclUniqueId id;
-    FM_NCCL(ncclGetUniqueId(&id));
-    static_assert(sizeof(id) == 128, "ncclUniqueId size");
-    std::memcpy(out, &id, 128);
-    return FM_OK;
-}
-
-int fm_comm_create(fm_ctx* c, const uint8_t id_bytes[128], int nranks, int rank, fm_comm** out) {
-    FM_GUARD_BEGIN
-    if (int st = set_dev(c)) return st;
-    ncclUniqueId id;
-    std::memcpy(&id, id_bytes, 128);
-    auto* cm = new fm_comm();
-    cm->nranks = nranks;
-    cm->rank = rank;
-    cm->ctx = c;
-    const ncclResult_t r = ncclCommInitRank(&cm->comm, nranks, id, rank);
-    if (r != ncclSuccess) {
-        delete cm;
-        return fail(FM_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
-    }
-    *out = cm;
-    return FM_OK;
-    FM_GUARD_END
-}
-
-int fm_comm_destroy(fm_comm* c) {
-    if (!c) return FM_OK;
-    if (c->comm) ncclCommDestroy(c->comm);
-    delete c;
-    return FM_OK;
-}
-
-}  // extern "C"
-
-static ncclComm_t gang_comm(GangState* gs) { return gs->comm->comm; }
-
-static int gang_barrier(fm_agent* a) {
-    GangState* gs = a->gang;
-    FM_NCCL(ncclAllReduce(gs->d_token, gs->d_token, 1, ncclInt32, ncclSum, gs->comm->comm, a->ctx->stream));
-    return FM_OK;
-}
-
-namespace {
-struct GangBlob {
-    int32_t rank;
-    int32_t pad;
-    cudaIpcMemHandle_t recv;
-    cudaIpcMemHandle_t slot;
-    uint64_t w16_off;
-};
-}  // namespace
-
-extern "C" {
-
-// Puts the agent into a DP gang with the fused reduce-scatter (see GangState).
-// Writes this rank's export blob (IPC handles of its receive buffer and of
-// its training slot's bf16 shadow) for the caller to all-gather across the
-// gang and hand to fm_gang_connect.  The agent must stay resident (no
-// suspend) while attached.
-int fm_gang_attach(fm_agent* a, fm_comm* cm, uint8_t* blob_out, uint64_t cap, uint64_t* len) {
-    FM_GUARD_BEGIN
-    *len = sizeof(GangBlob);
-    if (!blob_out) return FM_OK;
-    if (cap < sizeof(GangBlob)) return fail(FM_ERR_INVALID_ARG, "blob buffer too small");
-    if (int st = check_active(a)) return st;
-    if (a->precision != FM_PRECISION_BF16_TC) return fail(FM_ERR_CONFIG_ERROR, "gang exchange needs the tensor-core path");
-    if (cm->ctx != a->ctx) return fail(FM_ERR_CONFIG_ERROR, "communicator bound to another GPU");
-    if (cm->nranks < 2 || cm->nranks > 8) return fail(FM_ERR_CONFIG_ERROR, "gang size must be 2..8");
-    if (!gemm_pair_mode()) return fail(FM_ERR_CONFIG_ERROR, "gang exchange needs the CTA-pair GEMM (FM_GEMM_2SM)");
-    if (int st = set_dev(a->ctx)) return st;
-    auto* gs = new GangState();
-    gs->comm = cm;
-    gs->rank = cm->rank;
-    gs->g = cm->nranks;
-    const int64_t tiles = static_cast<int64_t>((a->V + 255) / 256);
-    for (int o = 0; o <= gs->g; ++o)
-        gs->lo[o] = std::min<int64_t>(static_cast<int64_t>(a->V), (tiles * o / gs->g) * 256);
-    int64_t max_rows = 0;
-    for (int o = 0; o < gs->g; ++o) max_rows = std::max(max_rows, gs->lo[o + 1] - gs->lo[o]);
-    const int64_t own = gs->lo[gs->rank + 1] - gs->lo[gs->rank];
-    const size_t rbytes = static_cast<size_t>(gs->g - 1) * std::max<int64_t>(own, 1) * a->D * 4;
-    fm_ctx* c = a->ctx;
-    void* rb = nullptr;
-    void* tk = nullptr;
-    if (int st = pool_take(c, rbytes, &rb)) {
-        delete gs;
-        return st;
-    }
-    if (int st = pool_take(c, 256, &tk)) {
-        pool_give(c, rb);
-        delete gs;
-        return st;
-    }
-    gs->recv = static_cast<float*>(rb);
-    gs->d_token = static_cast<int*>(tk);
-    FM_CUDA(cudaMemset(gs->d_token, 0, sizeof(int)));
-    GangBlob b{};
-    b.rank = gs->rank;
-    FM_CUDA(cudaIpcGetMemHandle(&b.recv, gs->recv));
-    FM_CUDA(cudaIpcGetMemHandle(&b.slot, a->slot->base));
-    b.w16_off = static_cast<uint64_t>(reinterpret_cast<uint8_t*>(a->W16) - static_cast<uint8_t*>(a->slot->base));
-    std::memcpy(blob_out, &b, sizeof(b));
-    a->gang = gs;
-    a->shard_rank = gs->rank;  // token-balanced row shards of every micro-batch
-    a->shard_count = gs->g;
-    a->dp = true;
-    return FM_OK;
-    FM_GUARD_END
-}
-
-// blobs: the gang's export blobs in rank order (nranks x blob_len bytes).
-int fm_gang_connect(fm_agent* a, const uint8_t* blobs, uint64_t blob_len) {
-    FM_GUARD_BEGIN
-    GangState* gs = a->gang;
-    if (!gs) return fail(FM_ERR_CONFIG_ERROR, "fm_gang_attach first");
-    if (blob_len != sizeof(GangBlob)) return fail(FM_ERR_INVALID_ARG, "blob size mismatch");
-    if (int st = set_dev(a->ctx)) return st;
-    for (int o = 0; o < gs->g; ++o) {
-        GangBlob b;
-        std::memcpy(&b, blobs + o * blob_len, sizeof(b));
-        if (b.rank != o) return fail(FM_ERR_INVALID_ARG, "blobs must be in rank order");
-        if (o == gs->rank) continue;
-        void* rbase = nullptr;
-        void* sbase = nullptr;
-        if (int st = ipc_open_cached(a->ctx, b.recv, &rbase)) return st;
-        if (int st = ipc_open_cached(a->ctx, b.slot, &sbase)) return st;
-        // my slot in o's receive buffer: senders in rank order, skipping o itself
-        const int idx = gs->rank < o ? gs->rank : gs->rank - 1;
-        const int64_t o_rows = gs->lo[o + 1] - gs->lo[o];
-        gs->peer_slot[o] = static_cast<float*>(rbase) + static_cast<size_t>(idx) * o_rows * a->D;
-        gs->peer_w16[o] = reinterpret_cast<__nv_bfloat16*>(static_cast<uint8_t*>(sbase) + b.w16_off);
-        gs->peer_base[o] = static_cast<uint8_t*>(sbase);
-    }
-    gs->connected = true;
-    return FM_OK;
-    FM_GUARD_END
-}
-
-}  // extern "C"
-
-// A DP-gang agent maintains W / m / v only on its own row shard (the sharded
-// K-adam); the other rows live in the owners' slots, mapped over NVLink at
-// connect.  Outside a gang this is one contiguous copy.
-static int copy_state(fm_agent* a, size_t off, size_t elem, void* dst, cudaStream_t s) {
-    const uint8_t* mine = static_cast<const uint8_t*>(a->slot->base) + off;
-    GangState* gs = a->gang;
-    if (!gs || !gs->connected) {
-        FM_CUDA(cudaMemcpyAsync(dst, mine, a->P * elem, cudaMemcpyDefault, s));
-        return FM_OK;
-    }
-    const size_t row = a->D * elem;
-    for (int o = 0; o < gs->g; ++o) {
-        const int64_t r0 = gs->lo[o], r1 = gs->lo[o + 1];
-        if (r1 <= r0) continue;
-        const uint8_t* src = (o == gs->rank ? mine : gs->peer_base[o] + off) + static_cast<size_t>(r0) * row;
-        FM_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + static_cast<size_t>(r0) * row, src,
-                                static_cast<size_t>(r1 - r0) * row, cudaMemcpyDefault, s));
-    }
-    return FM_OK;
-}
-
-extern "C" {
-
-// Pulls every peer's W / m / v rows into this rank's slot over NVLink (the gang's
-// sharded Adam keeps only the own rows current there), so that after
-// fm_gang_detach this rank holds the agent's whole training state.  The bf16
-// shadow is replicated already.  Caller: all gang ranks idle (host barrier).
-int fm_gang_gather_state(fm_agent* a) {
-    FM_GUARD_BEGIN
-    if (int st = check_active(a)) return st;
-    GangState* gs = a->gang;
-    if (!gs || !gs->connected) return fail(FM_ERR_CONFIG_ERROR, a->name + " is not in a connected DP gang");
-    fm_ctx* c = a->ctx;
-    if (int st = set_dev(c)) return st;
-    const size_t offs[3] = {0, slot_off_m(a), slot_off_v(a)};
-    const size_t elems[3] = {8, 4, 4};
-    for (int k = 0; k < 3; ++k) {
-        const size_t row = a->D * elems[k];
-        uint8_t* mine = static_cast<uint8_t*>(a->slot->base) + offs[k];
-        for (int o = 0; o < gs->g; ++o) {
-            const int64_t r0 = gs->lo[o], r1 = gs->lo[o + 1];
-            if (o == gs->rank || r1 <= r0) continue;
-            FM_CUDA(cudaMemcpyAsync(mine + static_cast<size_t>(r0) * row,
-                                    gs->peer_base[o] + offs[k] + static_cast<size_t>(r0) * row,
-                                    static_cast<size_t>(r1 - r0) * row, cudaMemcpyDefault, c->stream));
-        }
-    }
-    FM_CUDA(cudaStreamSynchronize(c->stream));
-    return FM_OK;
-    FM_GUARD_END
-}
-
-int fm_gang_detach(fm_agent* a) {
-    GangState* gs = a->gang;
-    if (!gs) return FM_OK;
-    if (a->ctx) {
-        cudaSetDevice(a->ctx->device);
-        cudaStreamSynchronize(a->ctx->stream);
-    }
-    // mappings stay in the context's cache; the buffers go back to its pool
-    if (a->ctx) {
-        pool_give(a->ctx, gs->recv);
-        pool_give(a->ctx, gs->d_token);
-    } else {
-        cudaFree(gs->recv);
-        cudaFree(gs->d_token);
-    }
-    delete gs;
-    a->gang = nullptr;
-    a->shard_rank = 0;
-    a->shard_count = 1;
-    a->dp = false;
-    return FM_OK;
-}
-
-int fm_agent_allreduce_grad(fm_agent* a, fm_comm* cm) {
-    if (int st = check_active(a)) return st;
-    if (a->gang && a->gang->connected) return FM_OK;  // already reduced inside the last GEMM2
-    if (cm->ctx != a->ctx) return fail(FM_ERR_CONFIG_ERROR, "communicator bound to another GPU");
-    fm_ctx* c = a->ctx;
-    if (int st = set_dev(c)) return st;
-    if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * dw_elem(a), c->stream));
-    a->dw_valid = true;
-    a->dp = cm->nranks > 1;
-    FM_NCCL(ncclAllReduce(a->dW, a->dW, a->P, a->precision == FM_PRECISION_PARITY_F64 ? ncclFloat64 : ncclFloat32,
-                          ncclSum, cm->comm, c->stream));
-    return FM_OK;
-}
-
-}  // extern "C"
-
-// ===========================================================================
-// §8f next rows: weight publish / rollout sync (f1) and the byte-compatible
-// PolicyState wire format (f2)
-// ===========================================================================
-struct fm_weights {
-    int device = -1;
-    void* buf = nullptr;
-    uint64_t rows = 0, cols = 0;
-    int dtype = 0;  // 0 f64, 1 f32, 2 bf16, 3 f64 transposed [D][V] (rollout layout)
-    int64_t version = 0;
-    uint64_t nbytes = 0;
-};
-
-namespace {
-__global__ void f64_to_f32_kernel(const double* __restrict__ w, float* __restrict__ o, uint64_t n) {
-    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
-        o[i] = static_cast<float>(w[i]);
-}
-size_t dtype_bytes(int dt) { return dt == 0 || dt == 3 ? 8 : dt == 1 ? 4 : 2; }
-
-// W [V][D] -> Wt [D][V] through 32 x 32 shared-memory tiles (both sides coalesced)
-__global__ void transpose_f64_kernel(const double* __restrict__ w, double* __restrict__ wt, uint64_t V, uint64_t D) {
-    __shared__ double tile[32][33];
-    const uint64_t d0 = static_cast<uint64_t>(blockIdx.x) * 32, v0 = static_cast<uint64_t>(blockIdx.y) * 32;
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const uint64_t v = v0 + r, d = d0 + threadIdx.x;
-        if (v < V && d < D) tile[r][threadIdx.x] = w[v * D + d];
-    }
-    __syncthreads();
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const uint64_t d = d0 + r, v = v0 + threadIdx.x;
-        if (v < V && d < D) wt[d * V + v] = tile[threadIdx.x][r];
-    }
-}
-
-void put_u64(std::vector<uint8_t>& v, uint64_t x) {
-    const size_t o = v.size();
-    v.resize(o + 8);
-    std::memcpy(v.data() + o, &x, 8);
-}
-}  // namespace
-
-extern "C" {
-
-int fm_weights_alloc(fm_ctx* c, uint64_t rows, uint64_t cols, int dtype, fm_weights** out) {
-    FM_GUARD_BEGIN
-    if (dtype < 0 || dtype > 3)
-        return fail(FM_ERR_INVALID_ARG, "dtype must be 0 (f64), 1 (f32), 2 (bf16) or 3 (f64 transposed)");
-    if (int st = set_dev(c)) return st;
-    auto* w = new fm_weights();
-    w->device = c->device;
-    w->rows = rows;
-    w->cols = cols;
-    w->dtype = dtype;
-    w->nbytes = rows * cols * dtype_bytes(dtype);
-    if (cudaMalloc(&w->buf, w->nbytes) != cudaSuccess) {
-        cudaGetLastError();
-        delete w;
-        return fail(FM_ERR_DEVICE_OOM, "weights buffer");
-    }
-    *out = w;
-    return FM_OK;
-    FM_GUARD_END
-}
-
-// publish_weights (training.hpp:459-467): the agent's current W as ONE
-// contiguous device buffer — pack_weights' single-tensor layout (offset 0,
-// shape V x D, object_store.hpp:258-273) — stamped with the agent version.
-// dtype 0 reproduces the reference payload byte-for-byte; 2 (bf16) is the
-// rollout copy the paper's contiguous-buffer sync ships.
-int fm_publish_weights(fm_agent* a, int dtype, fm_weights** out) {
-    FM_GUARD_BEGIN
-    if (int st = check_active(a)) return st;
-    if (int st = fm_weights_alloc(a->ctx, a->V, a->D, dtype, out)) return st;
-    if (int st = fm_publish_into(a, *out)) {
-        fm_weights_destroy(*out);
-        *out = nullptr;
-        return st;
-    }
-    return FM_OK;
-    FM_GUARD_END
-}
-
-// Republish into an existing buffer (same agent dims; dtype taken from w): the
-// steady-state path, no allocation.
-int fm_publish_into(fm_agent* a, fm_weights* w) {
-    FM_GUARD_BEGIN
-    if (int st = check_active(a)) return st;
-    fm_ctx* c = a->ctx;
-    if (int st = set_dev(c)) return st;
-    if (w->rows != a->V || w->cols != a->D) return fail(FM_ERR_CONFIG_ERROR, "weights buffer shape mismatch");
-    if (w->device != c->device) return fail(FM_ERR_CONFIG_ERROR, "weights buffer on another GPU");
-    const int dtype = w->dtype;
-    w->version = a->version;
-    cudaStream_t s = c->stream;
-    const bool sharded = a->gang && a->gang->connected;  // f64 master rows live on their owners
-    if (dtype == 0) {
-        if (int st = copy_state(a, 0, 8, w->buf, s)) return st;
-    } else if (dtype == 1) {
-        double* src = a->W;
-        if (sharded) {
-            FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&src), a->P * 8, s));
-            if (int st = copy_state(a, 0, 8, src, s)) return st;
-        }
-        f64_to_f32_kernel<<<c->num_sms * 8, 256, 0, s>>>(src, static_cast<float*>(w->buf), a->P);
-        FM_CUDA(cudaGetLastError());
-        count_launch();
-        if (sharded) FM_CUDA(cudaFreeAsync(src, s));
-    } else if (dtype == 3) {
-        // rollout layout: one feature's weights over the vocabulary are contiguous, so the
-        // generator's per-token column reads coalesce
-        double* src = a->W;
-        if (sharded) {
-            FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&src), a->P * 8, s));
-            if (int st = copy_state(a, 0, 8, src, s)) return st;
-        }
-        const dim3 grid(static_cast<unsigned>((a->D + 31) / 32), static_cast<unsigned>((a->V + 31) / 32));
-        transpose_f64_kernel<<<grid, dim3(32, 8), 0, s>>>(src, static_cast<double*>(w->buf), a->V, a->D);
-        FM_CUDA(cudaGetLastError());
-        count_launch();
-        if (sharded) FM_CUDA(cudaFreeAsync(src, s));
-    } else if (a->W16) {
-        // the bf16 shadow IS bf16(W) (same double -> float -> bf16 rounding; full replica in a gang)
-        FM_CUDA(cudaMemcpyAsync(w->buf, a->W16, a->P * 2, cudaMemcpyDeviceToDevice, s));
-    } else {
-        FM_CUDA(launch_to_bf16(a->W, static_cast<__nv_bfloat16*>(w->buf), a->P, c->num_sms, s));
-        count_launch();
-    }
-    FM_CUDA(cudaStreamSynchronize(s));
-    return FM_OK;
-    FM_GUARD_END
-}
-
-int fm_weights_info(const fm_weights* w, int64_t* version, uint64_t* rows, uint64_t* cols, int* dtype,
-                    uint64_t* nbytes, int* device) {
-    if (version) *version = w->version;
-    if (rows) *rows = w->rows;
-    if (cols) *cols = w->cols;
-    if (dtype) *dtype = w->dtype;
-    if (nbytes) *nbytes = w->nbytes;
-    if (device) *device = w->device;
-    return FM_OK;
-}
-
-// One Get per consumer (rollout.hpp:510-541 sync_agent): a single contiguous
-// copy into `dst` — host memory (dst_device = -1) or any GPU of this process
-// (peer GPUs over NVLink via cudaMemcpyPeer).
-int fm_weights_get(const fm_weights* w, void* dst, int dst_device) {
-    FM_GUARD_BEGIN
-    // synchronous: returns when the copy has landed (the caller may free or
-    // republish the source right after); the caller's current device is kept
-    int prev = 0;
-    FM_CUDA(cudaGetDevice(&prev));
-    struct Restore {
-        int d;
-        ~Restore() { cudaSetDevice(d); }
-    } restore{prev};
-    FM_CUDA(cudaSetDevice(w->device));
-    if (dst_device < 0) {
-        FM_CUDA(cudaMemcpy(dst, w->buf, w->nbytes, cudaMemcpyDeviceToHost));
-    } else if (dst_device == w->device) {
-        FM_CUDA(cudaMemcpy(dst, w->buf, w->nbytes, cudaMemcpyDeviceToDevice));
-        FM_CUDA(cudaDeviceSynchronize());
-    } else {
-        int can = 0;
-        FM_CUDA(cudaDeviceCanAccessPeer(&can, dst_device, w->device));
-        FM_CUDA(cudaSetDevice(dst_device));
-        if (can) {
-            cudaError_t pe = cudaDeviceEnablePeerAccess(w->device, 0);
-            if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) FM_CUDA(pe);
-            cudaGetLastError();
-        }
-        // one NVLink copy on a private stream of the consumer GPU
-        cudaStream_t st;
-        FM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        const cudaError_t e = cudaMemcpyPeerAsync(dst, dst_device, w->buf, w->device, w->nbytes, st);
-        const cudaError_t e2 = e == cudaSuccess ? cudaStreamSynchronize(st) : e;
-        cudaStreamDestroy(st);
-        FM_CUDA(e2);
-    }
-    return FM_OK;
-    FM_GUARD_END
-}
-
-// Weight sync to every rank of a communicator in one collective (NCCL over
-// NVLink/NVSwitch): the root's published buffer -> each rank's buffer.
-int fm_weights_broadcast(fm_weights* w, fm_comm* cm, int root) {
-    FM_GUARD_BEGIN
-    FM_CUDA(cudaSetDevice(w->device));
-    if (w->device != cm->ctx->device) return fail(FM_ERR_CONFIG_ERROR, "weights and communicator on different GPUs");
-    const ncclDataType_t dt = w->dtype == 0 ? ncclFloat64 : w->dtype == 1 ? ncclFloat32 : ncclBfloat16;
-    int64_t ver = w->version;
-    int64_t* dver = nullptr;
-    FM_CUDA(cudaMalloc(&dver, sizeof(int64_t)));
-    FM_CUDA(cudaMemcpy(dver, &ver, sizeof(int64_t), cudaMemcpyHostToDevice));
-    FM_NCCL(ncclGroupStart());
-    FM_NCCL(ncclBroadcast(w->buf, w->buf, w->rows * w->cols, dt, root, cm->comm, cm->ctx->stream));
-    FM_NCCL(ncclBroadcast(dver, dver, 1, ncclInt64, root, cm->comm, cm->ctx->stream));
-    FM_NCCL(ncclGroupEnd());
-    FM_CUDA(cudaStreamSynchronize(cm->ctx->stream));
-    FM_CUDA(cudaMemcpy(&ver, dver, sizeof(int64_t), cudaMemcpyDeviceToHost));
-    cudaFree(dver);
-    w->version = ver;
-    return FM_OK;
-    FM_GUARD_END
-}
-
-int fm_weights_destroy(fm_weights* w) {
-    if (!w) return FM_OK;
-    cudaSetDevice(w->device);
-    cudaFree(w->buf);
-    delete w;
-    return FM_OK;
-}
-
-// PolicyState::serialize (training.hpp:107-133), byte for byte: u64 version,
-// step_count, samples_accumulated, vocab, feat; W, m, v as (u64 rows, u64
-// cols, f64 data); u64 cache_n; entries.  The reference caches one V x D term
-// per sample; this engine keeps only their sum, so a pending step is written
-// as ONE entry with key ("__sum__", 0, 0, version) holding sum(term) =
-// -G * dW, which the reference's canonical reduction turns back into the same
-// gradient.  With no pending gradient (the usual swap point) the bytes are
-// identical to the reference's.
-int fm_agent_serialize(fm_agent* a, int64_t global_batch, uint8_t* out, uint64_t cap, uint64_t* len) {
-    FM_GUARD_BEGIN
-    if (int st = check_active(a)) return st;
-    fm_ctx* c = a->ctx;
-    if (int st = set_dev(c)) return st;
-    FM_CUDA(cudaStreamSynchronize(c->stream));
-    const uint64_t P = a->P;
-    const bool pending = a->samples > 0 && a->dw_valid;
-    const uint64_t need = 5 * 8 + 3 * (16 + 8 * P) + 8 + (pending ? (8 + 7 + 24 + 16 + 8 * P) : 0);
-    *len = need;
-    if (!out) return FM_OK;
-    if (cap < need) return fail(FM_ERR_LAYOUT_OUT_OF_BOUNDS, "serialize buffer too small");
-    std::vector<uint8_t> head;
-    for (uint64_t x : {static_cast<uint64_t>(a->version), static_cast<uint64_t>(a->step),
-                       static_cast<uint64_t>(a->samples), a->V, a->D})
-        put_u64(head, x);
-    uint8_t* p = out;
-    std::memcpy(p, head.data(), head.size());
-    p += head.size();
-    auto put_hdr = [&](uint64_t r, uint64_t cc) {
-        std::memcpy(p, &r, 8);
-        std::memcpy(p + 8, &cc, 8);
-        p += 16;
-    };
-    put_hdr(a->V, a->D);
-    if (int st = copy_state(a, 0, 8, p, c->stream)) return st;  // gathers a gang's row shards
-    FM_CUDA(cudaStreamSynchronize(c->stream));
-    p += P * 8;
-    std::vector<float> tmp(P);
-    for (size_t off : {slot_off_m(a), slot_off_v(a)}) {  // fp32 moments widen exactly to f64
-        put_hdr(a->V, a->D);
-        if (int st = copy_state(a, off, 4, tmp.data(), c->stream)) return st;
-        FM_CUDA(cudaStreamSynchronize(c->stream));
-        if (a->step == 0) std::fill(tmp.begin(), tmp.end(), 0.f);
-        double* d = reinterpret_cast<double*>(p);
-        for (uint64_t i = 0; i < P; ++i) {
-            const double x = tmp[i];
-            std::memcpy(d + i, &x, 8);
-        }
-        p += P * 8;
-    }
-    const uint64_t cache_n = pending ? 1 : 0;
-    std::memcpy(p, &cache_n, 8);
-    p += 8;
-    if (pending) {
-        const char key[] = "__sum__";
-        const uint64_t klen = 7, zero = 0, ver = static_cast<uint64_t>(a->version);
-        std::memcpy(p, &klen, 8);
-        std::memcpy(p + 8, key, 7);
-        p += 15;
-        std::memcpy(p, &zero, 8);
-        std::memcpy(p + 8, &zero, 8);
-        std::memcpy(p + 16, &ver, 8);
-        p += 24;
-        put_hdr(a->V, a->D);
-        std::vector<double> g(P);
-        if (int st = fm_agent_read_grad(a, g.data())) return st;
-        const double scale = -static_cast<double>(global_batch);
-        for (uint64_t i = 0; i < P; ++i) g[i] *= scale;
-        std::memcpy(p, g.data(), P * 8);
-        p += P * 8;
-    }
-    return FM_OK;
-    FM_GUARD_END
-}
-
-// PolicyState::deserialize (training.hpp:135-164) into this agent's device
-// state.  Matrix dims are read rows-then-cols in the defined order (the
-// reference's unspecified argument evaluation at :146 transposes them).
-int fm_agent_deserialize(fm_agent* a, int64_t global_batch, const uint8_t* in, uint64_t len) {
-    FM_GUARD_BEGIN
-    if (int st = check_active(a)) return st;
-    fm_ctx* c = a->ctx;
-    if (int st = set_dev(c)) return st;
-    uint64_t pos = 0;
-    auto rd = [&](uint64_t* x) -> bool {
-        if (pos + 8 > len) return false;
-        std::memcpy(x, in + pos, 8);
-        pos += 8;
-        return true;
-    };
-    uint64_t version, step, samples, vocab, feat;
-    if (!rd(&version) || !rd(&step) || !rd(&samples) || !rd(&vocab) || !rd(&feat))
-        return fail(FM_ERR_LAYOUT_OUT_OF_BOUNDS, "truncated header");
-    if (vocab != a->V || feat != a->D) return fail(FM_ERR_CONFIG_ERROR, "state dims differ from the agent's");
-    const uint64_t P = a->P;
-    std::vector<double> mats[3];
-    for (int k = 0; k < 3; ++k) {
-        uint64_t r, cc;
-        if (!rd(&r) || !rd(&cc)) return fail(FM_ERR_LAYOUT_OUT_OF_BOUNDS, "truncated matrix header");
-        if (r * cc != P || pos + 8 * P > len) return fail(FM_ERR_LAYOUT_OUT_OF_BOUNDS, "matrix size");
-        mats[k].resize(P);
-        std::memcpy(mats[k].data(), in + pos, 8 * P);
-        pos += 8 * P;
-    }
-    uint64_t cache_n;
-    if (!rd(&cache_n)) return fail(FM_ERR_LAYOUT_OUT_OF_BOUNDS, "truncated cache count");
-    std::vector<double> sum(cache_n ? P : 0, 0.0);
-    for (uint64_t e = 0; e < cache_n; ++e) {
-        uint64_t klen, turns, traj, ver, r, cc;
-        if (!rd(&klen) || pos + klen > len) return fail(FM_ERR_LAYOUT_OUT_OF_BOUNDS, "cache key");
-        pos += klen;
-        if (!rd(&turns) || !rd(&traj) || !rd(&ver) || !rd(&r) || !rd(&cc) || r * cc != P || pos + 8 * P > len)
-            return fail(FM_ERR_LAYOUT_OUT_OF_BOUNDS, "cache entry");
-        const double* d = reinterpret_cast<const double*>(in + pos);
-        for (uint64_t i = 0; i < P; ++i) {
-            double x;
-            std::memcpy(&x, d + i, 8);
-            sum[i] += x;
-        }
-        pos += 8 * P;
-    }
-    cudaStream_t s = c->stream;
-    FM_CUDA(cudaStreamSynchronize(s));
-    FM_CUDA(cudaMemcpy(a->W, mats[0].data(), P * 8, cudaMemcpyHostToDevice));
-    std::vector<float> f(P);
-    for (int k = 1; k < 3; ++k) {
-        for (uint64_t i = 0; i < P; ++i) f[i] = static_cast<float>(mats[k][i]);
-        FM_CUDA(cudaMemcpy(k == 1 ? a->m : a->v, f.data(), P * 4, cudaMemcpyHostToDevice));
-    }
-    if (cache_n) {  // accumulator = -(1/G) * sum(term)   (training.hpp:444-446)
-        const double scale = -1.0 / static_cast<double>(global_batch);
-        if (a->precision == FM_PRECISION_PARITY_F64) {
-            for (uint64_t i = 0; i < P; ++i) sum[i] *= scale;
-            FM_CUDA(cudaMemcpy(a->dW, sum.data(), P * 8, cudaMemcpyHostToDevice));
-        } else {
-            for (uint64_t i = 0; i < P; ++i) f[i] = static_cast<float>(sum[i] * scale);
-            FM_CUDA(cudaMemcpy(a->dW, f.data(), P * 4, cudaMemcpyHostToDevice));
-        }
-        a->dw_valid = true;
-    } else {
-        a->dw_valid = false;
-    }
-    if (a->W16) {
-        FM_CUDA(launch_to_bf16(a->W, a->W16, P, c->num_sms, s));
-        count_launch();
-        ++a->w16_gen;
-    }
-    FM_CUDA(cudaStreamSynchronize(s));
-    a->version = static_cast<int64_t>(version);
-    a->step = static_cast<int64_t>(step);
-    a->samples = static_cast<int64_t>(samples);
-    return FM_OK;
-    FM_GUARD_END
-}
-
-// §8f-3: PolicyModel::generate (policy.hpp:119-130) for n requests on the GPU
-// from a published f64 weight buffer; seeds are the per-request token seeds
-// (rollout.hpp:638-645).  Host arrays in and out.
-int fm_generate(fm_ctx* c, const fm_weights* w, const int32_t* prompts, const int32_t* prompt_off, int n,
-                int max_tokens, const uint64_t* seeds, int32_t* out_tokens, double* out_logp, int32_t* out_len) {
-    FM_GUARD_BEGIN
-    if (w->dtype != 0 && w->dtype != 3)
-        return fail(FM_ERR_CONFIG_ERROR, "generation reads f64 weights (publish with dtype 0 or 3)");
-    if (w->device != c->device) return fail(FM_ERR_CONFIG_ERROR, "weights live on another GPU (fm_weights_get)");
-    if (n <= 0 || max_tokens <= 0) return FM_OK;
-    if (int st = set_dev(c)) return st;
-    cudaStream_t s = c->stream;
-    const int np = prompt_off[n];
-    int32_t *dp = nullptr, *doff = nullptr, *dtok = nullptr, *dlen = nullptr;
-    uint64_t* dseed = nullptr;
-    double *dz = nullptr, *dlp = nullptr;
-    const size_t nt = static_cast<size_t>(n) * max_tokens;
-    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dp), std::max(np, 1) * 4, s));
-    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&doff), (n + 1) * 4, s));
-    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dseed), n * 8, s));
-    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dz), static_cast<size_t>(n) * w->rows * 8, s));
-    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dtok), nt * 4, s));
-    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dlp), nt * 8, s));
-    FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dlen), n * 4, s));
-    if (np) FM_CUDA(cudaMemcpyAsync(dp, prompts, np * 4, cudaMemcpyHostToDevice, s));
-    FM_CUDA(cudaMemcpyAsync(doff, prompt_off, (n + 1) * 4, cudaMemcpyHostToDevice, s));
-    FM_CUDA(cudaMemcpyAsync(dseed, seeds, n * 8, cudaMemcpyHostToDevice, s));
-    FM_CUDA(launch_generate(static_cast<const double*>(w->buf), w->dtype == 3, w->rows, w->cols, dp, doff, n,
-                            max_tokens, dseed, dz, dtok, dlp, dlen, s));
-    count_launch();
-    FM_CUDA(cudaMemcpyAsync(out_tokens, dtok, nt * 4, cudaMemcpyDeviceToHost, s));
-    FM_CUDA(cudaMemcpyAsync(out_logp, dlp, nt * 8, cudaMemcpyDeviceToHost, s));
-    FM_CUDA(cudaMemcpyAsync(out_len, dlen, n * 4, cudaMemcpyDeviceToHost, s));
-    for (void* p : {static_cast<void*>(dp), static_cast<void*>(doff), static_cast<void*>(dseed),
-                    static_cast<void*>(dz), static_cast<void*>(dtok), static_cast<void*>(dlp),
-                    static_cast<void*>(dlen)})
-        FM_CUDA(cudaFreeAsync(p, s));
     FM_CUDA(cudaStreamSynchronize(s));
     return FM_OK;
     FM_GUARD_END
