@@ -640,3 +640,24 @@ def test_gemm2_rows_counter(ctx, monkeypatch):
     run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
     _lib.check(L.fm_ctx_gemm2_rows(ctx.handle, C.byref(rows), 1))
     assert rows.value == 0
+
+
+@pytest.mark.parametrize("V,D_,n_samples,resp", [(300, 200, 5, 7), (1000, 520, 16, 33), (4100, 96, 3, 2),
+                                                 (520, 1000, 16, 64)])
+def test_token_slot_segments_odd_shapes(ctx, monkeypatch, V, D_, n_samples, resp):
+    """Segmented GEMM2 on ragged shapes — V and D not multiples of 256 (partial
+    last vocab tile / feature block), blocks no token touches, tokens whose
+    features share a block, tiny micro-batches — against the dense GEMM2 and
+    the f64 oracle."""
+    rng = np.random.default_rng(V * 7 + D_)
+    samples = [([int(x) for x in rng.integers(0, 3 * V, size=int(rng.integers(0, 6)))],
+                [int(x) for x in rng.integers(0, V, size=resp)]) for _ in range(n_samples)]
+    adv = rng.normal(size=n_samples)
+    monkeypatch.setenv("FM_G2_KLIST", "0")
+    g_dense, n_dense = _train_one(ctx, V, D_, samples, adv)
+    monkeypatch.setenv("FM_G2_KLIST", "2")
+    g_seg, n_seg = _train_one(ctx, V, D_, samples, adv)
+    assert rel_fro(g_seg, g_dense) < 1e-5
+    assert abs(n_seg - n_dense) <= 1e-5 * max(n_dense, 1e-30)
+    ref = orc.sparse_grad(V, D_, agent_seed(2048, "sk"), samples, adv, 64)
+    assert rel_fro(g_seg[:, ref["cols"]], ref["grad"]) <= 2e-2
