@@ -155,7 +155,8 @@ struct ShardPeers {
 cudaError_t launch_adam_shard(double* w, float* m, float* v, const float* g, const float* recv, int nslots,
                               uint64_t slot_stride, __nv_bfloat16* w16, ShardPeers peers, uint64_t n,
                               double lr, double b1, double b2, double eps, double bc1, double bc2,
-                              double* gsq, int num_sms, cudaStream_t s);
+                              double* gsq, int num_sms, cudaStream_t s, int* colmax = nullptr, uint64_t D = 0,
+                              bool* colmax_done = nullptr);
 
 // K-adv (training.hpp:54-67): one warp per reward group, fp64 shuffle reductions.
 cudaError_t launch_group_advantages(const double* rewards, const int32_t* seg_off, int nseg,

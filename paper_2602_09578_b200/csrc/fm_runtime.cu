@@ -1417,9 +1417,20 @@ static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, doubl
             if (o != gs->rank) peers.w16[peers.n++] = gs->peer_w16[o] + off;
         FM_CUDA(launch_adam_shard(a->W + off, a->m + off, a->v + off, static_cast<float*>(a->dW) + off, gs->recv,
                                   gs->g - 1, n_own, a->W16 + off, peers, n_own, lr, b1, b2, eps, bc1, bc2, a->d_upd,
-                                  c->num_sms, s));
+                                  c->num_sms, s, loss_fold_enabled() ? a->colmax : nullptr, a->D, &cm_fused));
         // global grad norm^2; doubles as the barrier after the peers' W16 writes
         FM_NCCL(ncclAllReduce(a->d_upd, a->d_upd, 1, ncclFloat64, ncclSum, gang_comm(gs), s));
+        // the shards' partial column maxima of the new shadow -> the loss-fold bound.  Every
+        // rank takes part in the all-reduce (a rank whose shard could not fuse the partial
+        // max computes it over its rows first), so the collective sequence never diverges.
+        if (loss_fold_enabled()) {
+            if (!cm_fused && r1 > r0)
+                FM_CUDA(launch_colmax(a->W16 + off, r1 - r0, static_cast<int64_t>(a->D), a->colmax, c->num_sms, s));
+            else if (!cm_fused)  // no rows here: the neutral key (below any finite value)
+                FM_CUDA(cudaMemsetAsync(a->colmax, 0x80, a->D * sizeof(int), s));
+            FM_NCCL(ncclAllReduce(a->colmax, a->colmax, a->D, ncclInt32, ncclMax, gang_comm(gs), s));
+            cm_fused = true;
+        }
     } else {
         // the next step's first GEMM2 overwrites dW, so no zeroing pass here; the new
         // shadow's column maxima (loss-fold bound) come out of the same pass

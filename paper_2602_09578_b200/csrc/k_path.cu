@@ -465,9 +465,10 @@ __global__ void __launch_bounds__(256) adam_shard_kernel(double* __restrict__ w,
                                                          uint64_t slot_stride, __nv_bfloat16* __restrict__ w16,
                                                          ShardPeers peers, uint64_t n, double lr, double b1,
                                                          double b2, double eps, double bc1, double bc2,
-                                                         double* gsq) {
+                                                         double* gsq, int* __restrict__ cm, uint64_t D) {
     __shared__ double red[8];
     double acc = 0.0;
+    float cmx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // partial colmax of this rank's rows
     const AdamF cf(lr, b1, b2, eps, bc1, bc2);
     auto adam_one = [&](double& w_, float& m_, float& v_, float g_, double, double, double, double, double,
                         double) -> double { return adam_f32(w_, m_, v_, g_, cf); };
@@ -499,6 +500,21 @@ __global__ void __launch_bounds__(256) adam_shard_kernel(double* __restrict__ w,
         pk.y = *reinterpret_cast<uint32_t*>(&hi);
         reinterpret_cast<uint2*>(w16)[i] = pk;
         for (int p = 0; p < peers.n; ++p) reinterpret_cast<uint2*>(peers.w16[p])[i] = pk;
+        if (cm) {
+            const float2 a = __bfloat1622float2(lo), b = __bfloat1622float2(hi);
+            cmx[0] = fmaxf(cmx[0], a.x);
+            cmx[1] = fmaxf(cmx[1], a.y);
+            cmx[2] = fmaxf(cmx[2], b.x);
+            cmx[3] = fmaxf(cmx[3], b.y);
+        }
+    }
+    if (cm) {
+        const uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+        if (i0 < n4) {
+            const uint64_t c0 = (4 * i0) % D;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) atomicMax(cm + c0 + j, fkey(cmx[j]));
+        }
     }
     const uint64_t gid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (gid < n - n4 * 4) {
@@ -944,13 +960,32 @@ template cudaError_t launch_adam<double>(double*, float*, float*, double*, __nv_
 cudaError_t launch_adam_shard(double* w, float* m, float* v, const float* g, const float* recv, int nslots,
                               uint64_t slot_stride, __nv_bfloat16* w16, ShardPeers peers, uint64_t n, double lr,
                               double b1, double b2, double eps, double bc1, double bc2, double* gsq, int num_sms,
-                              cudaStream_t s) {
+                              cudaStream_t s, int* colmax, uint64_t D, bool* colmax_done) {
+    if (colmax_done) *colmax_done = false;
     if (n == 0) return cudaSuccess;
     const uint64_t want = (n / 4 + 255) / 256;
     const uint64_t cap = static_cast<uint64_t>(num_sms) * 8;
-    const int blocks = static_cast<int>(want < 1 ? 1 : (want > cap ? cap : want));
-    adam_shard_kernel<<<blocks, 256, 0, s>>>(w, m, v, g, recv, nslots, slot_stride, w16, peers, n, lr, b1, b2, eps,
-                                             bc1, bc2, gsq);
+    uint64_t blocks = want < 1 ? 1 : (want > cap ? cap : want);
+    int* cm = nullptr;
+    if (colmax && D % 4 == 0 && n % D == 0) {
+        // partial colmax of this shard (fixed columns per thread, as in launch_adam)
+        if (want > blocks) {
+            uint64_t q = D, r = 1024;
+            while (r) { const uint64_t t = q % r; q = r; r = t; }
+            const uint64_t mult = D / q;
+            blocks = blocks / mult * mult;
+        }
+        if (blocks > 0) {
+            cm = colmax;
+            cudaError_t e = cudaMemsetAsync(colmax, 0x80, D * sizeof(int), s);
+            if (e != cudaSuccess) return e;
+        } else {
+            blocks = want < cap ? want : cap;
+        }
+    }
+    adam_shard_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(w, m, v, g, recv, nslots, slot_stride, w16, peers, n,
+                                                               lr, b1, b2, eps, bc1, bc2, gsq, cm, D);
+    if (colmax_done) *colmax_done = cm != nullptr;
     return cudaGetLastError();
 }
 
