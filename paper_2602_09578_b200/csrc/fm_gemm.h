@@ -79,6 +79,7 @@ struct GemmArgs {
     // CTA into the swizzled MN-major stage; B' tile-loaded as in kSeg.
     const int32_t* seg_tok = nullptr;
     long long ld_pexp = 0;
+    int dbg_nostore = 0;  // timing diagnostics only: skip the token-slot global stores
 };
 
 // Stream-K workspace capacity: at most 2*pairs-1 split tiles (148 SMs -> 74 pairs).

@@ -92,7 +92,8 @@ cudaError_t launch_lse(const LseArgs& L, cudaStream_t s);
 //   G^T[v][t] = coef_eff_t * (delta(v, a_t) - p~[t][v] * exp(m_tile(t, v) - lse_t))
 // p~ tiles (bf16, from GEMM1) streamed in through TMA, G^T tiles stored through TMA.
 cudaError_t launch_softmax_grad(const CUtensorMap& tmP, const CUtensorMap& tmGt, const float2* stats,
-                                int stats_ld, int64_t Mpad, int64_t V, RowBuffers rows, cudaStream_t s);
+                                int stats_ld, int64_t Mpad, int64_t V, RowBuffers rows, cudaStream_t s,
+                                int part_cols = 256);
 
 // K-klist: for every 256-feature column block b of GEMM2, the rows (tokens) whose
 // context touches block b, ascending, padded with zero_row to a multiple of 64

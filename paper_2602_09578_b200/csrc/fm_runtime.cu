@@ -228,7 +228,7 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
     e = e ? e : dalloc(&w.klist, static_cast<size_t>((DD + 255) / 256) * w.klist_ld);
     e = e ? e : dalloc(&w.kiters, static_cast<size_t>((DD + 255) / 256));
     e = e ? e : dalloc(&w.zact, R);
-    e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n);
+    e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n * 2);  // GEMM1 partials per tile half
     e = e ? e : dalloc(&w.mrow, R);
     e = e ? e : dalloc(&w.lse_sync, 2);
     e = e ? e : cudaMemset(w.lse_sync, 0, 2 * sizeof(unsigned));
@@ -1023,6 +1023,10 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 !make_tmap_bf16_kmajor(&tPt, w.phict, a->D, Mpad, gemm_b_box_rows()))
                 return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
             const int tiles_n = static_cast<int>((a->V + kGemmBN - 1) / kGemmBN);
+            // the CTA-pair GEMM1 drains a tile with two warps per row (column halves): one
+            // softmax partial per half
+            const int parts = gemm_pair_mode() ? 2 : 1;
+            const int stats_ld = tiles_n * parts;
             GemmArgs g1{};
             g1.M = static_cast<int>(M);
             g1.N = static_cast<int>(a->V);
@@ -1032,6 +1036,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 g1.mrow = w.mrow;
                 g1.aseg = w.aseg;
                 g1.slot4 = w.slot4;
+                g1.dbg_nostore = std::getenv("FM_DBG_G1_NOSTORE") ? 1 : 0;
             } else if (klist || swa) {  // p~ row-major: the K-list GEMM2 gathers token rows
                 g1.mrow = w.mrow;
                 g1.pexp = w.Pexp;
@@ -1048,7 +1053,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g1.ld_out = static_cast<long long>(ldz);
             g1.row_scale = w.rscale;
             g1.stats = w.stats;
-            g1.stats_ld = tiles_n;
+            g1.stats_ld = stats_ld;
             // K-lse fused into GEMM1's tail (loss fold, CTA-pair kernel; FM_LSE_FUSED=0
             // launches it separately): after a grid-wide arrival the epilogue warps
             // normalise the rows.  Same time as the 14 us launch it replaces (C2: GEMM1
@@ -1056,7 +1061,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             // last-finisher variant cost GEMM1 12-15%: DESIGN.md §9.)
             const char* lse_env = std::getenv("FM_LSE_FUSED");
             const bool lse_fused = fold && gemm_pair_mode() && !(lse_env && lse_env[0] == '0');
-            LseArgs lse_args{w.zact, w.stats, tiles_n, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
+            LseArgs lse_args{w.zact, w.stats, stats_ld, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
                              a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1,
                              fold ? 1 : 0, fold ? w.gt : nullptr, w.phict, Mpad};
             if (klist) {
@@ -1092,7 +1097,8 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             // K-softmax-grad: G^T tiles (zero for padding rows) — folded into GEMM2's operands
             if (!fold) {
                 KScope k(c, K_SOFTMAX_GRAD, s);
-                FM_CUDA(launch_softmax_grad(tP, tGt, w.stats, tiles_n, Mpad, static_cast<int64_t>(a->V), rows, s));
+                FM_CUDA(launch_softmax_grad(tP, tGt, w.stats, stats_ld, Mpad, static_cast<int64_t>(a->V), rows, s,
+                                            kGemmBN / parts));
             }
             // K-GEMM2: dW (+)= G^T * Phic ; first contribution of the step overwrites
             // (fold: A = p~'^T, B = Phic^T scaled per row by K-lse — the same product)

@@ -64,9 +64,9 @@ __device__ __forceinline__ float fast_exp(float x) { return exp2f(x * 1.44269504
 // co-resident; a 2 s bound traps instead of hanging).  Then every epilogue warp
 // of the grid runs the row normaliser (fm_lse.cuh) over a strided share of the
 // rows — the work of the standalone K-lse launch, without the launch.
-__device__ __forceinline__ void lse_grid_tail(const GemmArgs& a, uint32_t quad, double& loss) {
-    named_bar_sync(1, 128);
-    if (quad == 0 && (threadIdx.x & 31) == 0) {
+__device__ __forceinline__ void lse_grid_tail(const GemmArgs& a, int ew, int n_ew, double& loss) {
+    named_bar_sync(1, 32 * n_ew);
+    if (ew == 0 && (threadIdx.x & 31) == 0) {
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
         const unsigned prev = atomicAdd(&a.lse_sync[0], 1u);
         if (prev == gridDim.x - 1) {
@@ -87,10 +87,10 @@ __device__ __forceinline__ void lse_grid_tail(const GemmArgs& a, uint32_t quad, 
             }
         }
     }
-    named_bar_sync(1, 128);
+    named_bar_sync(1, 32 * n_ew);
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    const int64_t nw = static_cast<int64_t>(gridDim.x) * 4;
-    for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * 4 + quad) * 4; r0 < a.lse.Mpad; r0 += nw * 4)
+    const int64_t nw = static_cast<int64_t>(gridDim.x) * n_ew;
+    for (int64_t r0 = (static_cast<int64_t>(blockIdx.x) * n_ew + ew) * 4; r0 < a.lse.Mpad; r0 += nw * 4)
         loss += lse_row_quad(a.lse, r0);
 }
 
@@ -258,7 +258,7 @@ struct LogitsEpi {
             const int sl[4] = {s0, s1, s2, s3};
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-                if (sl[q] >= 0)
+                if (sl[q] >= 0 && !a.dbg_nostore)
                     st_global_v4_hint(reinterpret_cast<uint4*>(a.aseg + static_cast<size_t>(sl[q]) * a.ld_out + col0) + part,
                                       v, pol);
         }
@@ -646,13 +646,17 @@ constexpr int kThreadsPair = 192;  // w0 TMA, w1 MMA, w2-5 epilogue
 // segment's tokens) with 16-B loads and write them into the swizzled MN-major
 // stage; they and the B TMA arrive on the leader's full barrier (1 + 8 arrivals).
 template <class Epi, bool kAmn = false, bool kBmn = false, bool kKList = false, bool kSeg = false, bool kSwA = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSwA ? 320 : kThreadsPair, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((kSwA || std::is_same_v<Epi, LogitsEpi>) ? 320 : kThreadsPair, 1)
     gemm_tn_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        GemmArgs args) {
     static_assert(!kKList || (kAmn && kBmn), "K-list operands are MN-major");
     static_assert(!kSeg || (kAmn && kBmn), "segment operands are MN-major");
     static_assert(!kSwA || kSeg, "software A gather runs the segment schedule");
     constexpr uint32_t kId = idesc_bf16_f32<256, BN, kAmn, kBmn>();
+    // GEMM1 drains each accumulator with 8 epilogue warps (two per TMEM lane quadrant,
+    // each half the columns): its epilogue (exp, p~ stores) is the long one
+    constexpr int kEW = std::is_same_v<Epi, LogitsEpi> ? 8 : 4;
+    constexpr int kSplit = kEW / 4;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -679,7 +683,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSwA ? 320 : kThread
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is the one used)
+            mbar_init(&tempty[i], 2 * kEW);  // epilogue warps x 2 CTAs (leader's copy is the one used)
         }
         fence_barrier_init();
     }
@@ -866,12 +870,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSwA ? 320 : kThread
         }
         while (pend[0] >= 0) release_oldest(true);
     } else {
-        // ===== epilogue warps 2..5 (both CTAs; each drains its own 128 rows) =====
-        const uint32_t quad = warp & 3;
+        // ===== epilogue warps 2..(1+kEW) (both CTAs; each CTA drains its own 128 rows) =====
+        const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
+        const int ew = static_cast<int>(warp) - 2;
+        const int half = ew / 4;         // column part of the tile (kSplit parts)
+        constexpr int kCh = BN / 32 / kSplit;
+        const int c0 = half * kCh, c1 = c0 + kCh;
         const int row_in_tile = static_cast<int>(rank * 128 + quad * 32 + lane);
         const uint32_t tempty_leader[2] = {mapa_shared(&tempty[0], 0), mapa_shared(&tempty[1], 0)};
         Epi epi;
-        epi.xbuf = xscratch + quad * 32 * 36;
+        epi.xbuf = std::is_same_v<Epi, LogitsEpi> ? xscratch + ew * 32 * 20 : xscratch + quad * 32 * 36;
         int acc = 0;
         uint32_t acc_phase = 0;
         double sumsq_total = 0.0;
@@ -947,7 +955,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSwA ? 320 : kThread
             if constexpr (std::is_same_v<Epi, GradEpi>) epi.sumsq = 0.0;
             if (Epi::kTwoPass && !args.mrow) {
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = c0; c < c1; ++c) {
                     uint32_t r[32];
                     tmem_ld_32x32b_x32(tmem_base + ((quad * 32u) << 16) + static_cast<uint32_t>(acc * BN + c * 32), r);
                     tmem_ld_wait();
@@ -955,11 +963,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSwA ? 320 : kThread
                 }
             }
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = c0; c < c1; ++c) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + ((quad * 32u) << 16) + static_cast<uint32_t>(acc * BN + c * 32), r);
                 tmem_ld_wait();
-                if (c == BN / 32 - 1) {
+                if (c == c1 - 1) {
                     // the accumulator is fully in registers: hand TMEM back to the MMA
                     // warp before the last chunk's math and stores (relaxed: no wait
                     // for this warp's outstanding global stores)
@@ -969,7 +977,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSwA ? 320 : kThread
                 }
                 epi.chunk(args, row, tc.nb * BN + c * 32, r);
             }
-            epi.end(args, row, tc.nb);
+            epi.end(args, row, tc.nb * kSplit + half);  // softmax partials per column part
             if constexpr (std::is_same_v<Epi, GradEpi>) sumsq_total += epi.sumsq;
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
@@ -980,7 +988,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kSwA ? 320 : kThread
         }
         if constexpr (std::is_same_v<Epi, LogitsEpi>) {
             if (args.lse_sync) {
-                lse_grid_tail(args, quad, lse_loss);
+                lse_grid_tail(args, ew, kEW, lse_loss);
                 for (int o = 16; o > 0; o >>= 1) lse_loss += __shfl_xor_sync(0xffffffffu, lse_loss, o);
                 if (lane == 0 && args.lse.loss_acc && lse_loss != 0.0) atomicAdd(args.lse.loss_acc, lse_loss);
             }
@@ -1080,7 +1088,7 @@ bool loss_fold_enabled() {
 
 
 size_t gemm_smem_bytes() {
-    return use_pair_mma() ? P_STAGES * P_STAGE_BYTES + 1024 + 512 + 4 * 32 * 36 * 4
+    return use_pair_mma() ? P_STAGES * P_STAGE_BYTES + 1024 + 512 + 8 * 32 * 20 * 4  // >= 4 x 32 x 36 fp32
                           : STAGES * STAGE_BYTES + 1024 + 256;
 }
 
@@ -1099,7 +1107,7 @@ cudaError_t gemm_tn_launch(GemmKind kind, const CUtensorMap& tmA, const CUtensor
         if (kind == GemmKind::Logits) {
             auto k = gemm_tn_2sm_kernel<LogitsEpi>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            k<<<grid, kThreadsPair, smem, stream>>>(tmA, tmB, args);
+            k<<<grid, 320, smem, stream>>>(tmA, tmB, args);  // 8 epilogue warps
         } else {
             auto k = gemm_tn_2sm_kernel<GradEpi>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

@@ -257,7 +257,7 @@ constexpr uint32_t kSgGBytes = kSgRows * kSgCols * 2;  // 16 KB bf16 G^T tile (s
 __global__ void __launch_bounds__(256) softmax_grad_kernel(const __grid_constant__ CUtensorMap tmP,
                                                            const __grid_constant__ CUtensorMap tmGt,
                                                            const float2* __restrict__ stats, int stats_ld,
-                                                           RowBuffers rows) {
+                                                           RowBuffers rows, int part_cols) {
     extern __shared__ uint8_t raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(256) softmax_grad_kernel(const __grid_constant
 
     const int v0 = blockIdx.x * kSgCols;
     const int r0 = blockIdx.y * kSgRows;
-    const int tile = v0 / 256;  // GEMM1's 256-wide softmax-partial tile holding these columns
+    const int tile = v0 / part_cols;  // GEMM1's softmax partial (per tile, or per tile half) holding these columns
     const int tid = threadIdx.x;
     if (tid == 0) {
         tma_prefetch(&tmP);
@@ -906,12 +906,12 @@ cudaError_t launch_lse(const LseArgs& L, cudaStream_t s) {
 }
 
 cudaError_t launch_softmax_grad(const CUtensorMap& tmP, const CUtensorMap& tmGt, const float2* stats, int stats_ld,
-                                int64_t Mpad, int64_t V, RowBuffers rows, cudaStream_t s) {
+                                int64_t Mpad, int64_t V, RowBuffers rows, cudaStream_t s, int part_cols) {
     if (Mpad == 0) return cudaSuccess;
     const size_t smem = 1024 + kSgPBytes + kSgGBytes + 16 + kSgRows * 12;
     cudaFuncSetAttribute(softmax_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     dim3 grid(static_cast<unsigned>((V + kSgCols - 1) / kSgCols), static_cast<unsigned>(Mpad / kSgRows));
-    softmax_grad_kernel<<<grid, 256, smem, s>>>(tmP, tmGt, stats, stats_ld, rows);
+    softmax_grad_kernel<<<grid, 256, smem, s>>>(tmP, tmGt, stats, stats_ld, rows, part_cols);
     return cudaGetLastError();
 }
 
