@@ -80,6 +80,9 @@ struct GemmArgs {
     const int32_t* seg_tok = nullptr;
     long long ld_pexp = 0;
     int dbg_nostore = 0;  // timing diagnostics only: skip the token-slot global stores
+    // Logits (CTA pair): drain each accumulator with 8 epilogue warps (softmax partials
+    // per column half: stats_ld = 2 x tiles) instead of 4
+    int epi_wide = 0;
 };
 
 // Stream-K workspace capacity: at most 2*pairs-1 split tiles (148 SMs -> 74 pairs).

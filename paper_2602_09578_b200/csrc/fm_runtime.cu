@@ -1023,9 +1023,13 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 !make_tmap_bf16_kmajor(&tPt, w.phict, a->D, Mpad, gemm_b_box_rows()))
                 return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
             const int tiles_n = static_cast<int>((a->V + kGemmBN - 1) / kGemmBN);
-            // the CTA-pair GEMM1 drains a tile with two warps per row (column halves): one
-            // softmax partial per half
-            const int parts = gemm_pair_mode() ? 2 : 1;
+            // short-K GEMM1 (D <= 4,096: 64 K iterations per tile) is epilogue-bound, so its
+            // tiles are drained by 8 warps, two per row (column halves, one softmax partial
+            // each): C2 GEMM1 3.2 -> 2.9 ms; with longer K (C3/C5) 4 warps measured 5-7%
+            // fewer cycles (FM_G1_EPI_WARPS=4/8 overrides)
+            const int epi_w = env_int("FM_G1_EPI_WARPS", a->D <= 4096 ? 8 : 4);
+            const bool wide = gemm_pair_mode() && epi_w == 8;
+            const int parts = wide ? 2 : 1;
             const int stats_ld = tiles_n * parts;
             GemmArgs g1{};
             g1.M = static_cast<int>(M);
@@ -1054,6 +1058,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g1.row_scale = w.rscale;
             g1.stats = w.stats;
             g1.stats_ld = stats_ld;
+            g1.epi_wide = wide ? 1 : 0;
             // K-lse fused into GEMM1's tail (loss fold, CTA-pair kernel; FM_LSE_FUSED=0
             // launches it separately): after a grid-wide arrival the epilogue warps
             // normalise the rows.  Same time as the 14 us launch it replaces (C2: GEMM1

@@ -645,17 +645,19 @@ constexpr int kThreadsPair = 192;  // w0 TMA, w1 MMA, w2-5 epilogue
 // kSwA (with kSeg): warps 6-9 of each CTA gather the A rows (p~ rows of the
 // segment's tokens) with 16-B loads and write them into the swizzled MN-major
 // stage; they and the B TMA arrive on the leader's full barrier (1 + 8 arrivals).
-template <class Epi, bool kAmn = false, bool kBmn = false, bool kKList = false, bool kSeg = false, bool kSwA = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((kSwA || std::is_same_v<Epi, LogitsEpi>) ? 320 : kThreadsPair, 1)
+template <class Epi, bool kAmn = false, bool kBmn = false, bool kKList = false, bool kSeg = false, bool kSwA = false,
+          int kEpiW = 4>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((kSwA || kEpiW == 8) ? 320 : kThreadsPair, 1)
     gemm_tn_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        GemmArgs args) {
     static_assert(!kKList || (kAmn && kBmn), "K-list operands are MN-major");
     static_assert(!kSeg || (kAmn && kBmn), "segment operands are MN-major");
     static_assert(!kSwA || kSeg, "software A gather runs the segment schedule");
     constexpr uint32_t kId = idesc_bf16_f32<256, BN, kAmn, kBmn>();
-    // GEMM1 drains each accumulator with 8 epilogue warps (two per TMEM lane quadrant,
-    // each half the columns): its epilogue (exp, p~ stores) is the long one
-    constexpr int kEW = std::is_same_v<Epi, LogitsEpi> ? 8 : 4;
+    // kEpiW = 8: the accumulator is drained by two warps per TMEM lane quadrant, each
+    // half the columns — GEMM1 with short K (its exp + p~ slot stores outlast the MMAs)
+    static_assert(kEpiW == 4 || (kEpiW == 8 && std::is_same_v<Epi, LogitsEpi>), "8 epilogue warps: GEMM1 only");
+    constexpr int kEW = kEpiW;
     constexpr int kSplit = kEW / 4;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -879,7 +881,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((kSwA || std::is_sam
         const int row_in_tile = static_cast<int>(rank * 128 + quad * 32 + lane);
         const uint32_t tempty_leader[2] = {mapa_shared(&tempty[0], 0), mapa_shared(&tempty[1], 0)};
         Epi epi;
-        epi.xbuf = std::is_same_v<Epi, LogitsEpi> ? xscratch + ew * 32 * 20 : xscratch + quad * 32 * 36;
+        epi.xbuf = kEW == 8 ? xscratch + ew * 32 * 20 : xscratch + quad * 32 * 36;
         int acc = 0;
         uint32_t acc_phase = 0;
         double sumsq_total = 0.0;
@@ -1105,9 +1107,15 @@ cudaError_t gemm_tn_launch(GemmKind kind, const CUtensorMap& tmA, const CUtensor
         const int pairs = num_sms / 2;
         const int grid = 2 * (tiles < pairs ? tiles : pairs);
         if (kind == GemmKind::Logits) {
-            auto k = gemm_tn_2sm_kernel<LogitsEpi>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            k<<<grid, 320, smem, stream>>>(tmA, tmB, args);  // 8 epilogue warps
+            if (args.epi_wide) {  // 8 epilogue warps
+                auto k = gemm_tn_2sm_kernel<LogitsEpi, false, false, false, false, false, 8>;
+                cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                k<<<grid, 320, smem, stream>>>(tmA, tmB, args);
+            } else {
+                auto k = gemm_tn_2sm_kernel<LogitsEpi>;
+                cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+                k<<<grid, kThreadsPair, smem, stream>>>(tmA, tmB, args);
+            }
         } else {
             auto k = gemm_tn_2sm_kernel<GradEpi>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
