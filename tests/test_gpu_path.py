@@ -417,10 +417,11 @@ def test_fused_lse_matches_standalone_kernel(ctx, monkeypatch):
     alone = run_fixture(ctx, f, _lib.PRECISION_BF16_TC)
     for g1, g2 in zip(fused["grads"], alone["grads"]):
         np.testing.assert_array_equal(g1, g2)
-    for k in ("W", "m", "v", "mb_grad_norm"):
+    for k in ("W", "m", "v"):
         np.testing.assert_array_equal(fused[k], alone[k])
-    # K-adam's norm reduction adds in atomic order
-    np.testing.assert_allclose(fused["upd_grad_norm"], alone["upd_grad_norm"], rtol=1e-12)
+    # the norms are sums of per-warp partials added in atomic order
+    for k in ("mb_grad_norm", "upd_grad_norm"):
+        np.testing.assert_allclose(fused[k], alone[k], rtol=1e-12)
     assert rel_fro(fused["grads"][0], _oracle_grad_step0(f)) <= 2e-2
 
 
