@@ -32,7 +32,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-KINDS = ["gather", "gemm1", "lse", "softmax_grad", "gemm2", "adam", "parity", "memset", "colmax"]
+KINDS = ["gather", "stats", "lse", "band", "gemm2", "adam", "parity", "memset"]
 
 
 def log(*a):
@@ -370,47 +370,50 @@ def run_ours(args, dist: Dist) -> dict | None:
     agent_tokens = len(agents) * G * cfg.resp_len * args.steps
     value = agent_tokens / (max_ms / 1e3)
 
-    # --- roofline of the dominant kernel + the HBM-bound kernels
+    # --- roofline of the dominant kernel + every hot-path kernel
     peaks = load_peaks()
     M_local = rows_per_mb / len(place[mine[0]]) if mine else 0
     V, Dm, P = cfg.vocab, cfg.feat, cfg.params
-    flops_gemm = 2.0 * M_local * V * Dm  # per launch (2VD per trained token)
-    Mpad = int(np.ceil(M_local / 128) * 128)
-    bytes_sg = 4.0 * V * Mpad            # read p~ bf16 + write G^T bf16
-    bytes_adam = 38.0 * P                # r: w8 m4 v4 g4; w: w8 m4 v4 shadow2
+    n_mb = G // cfg.micro_batch
+    # context positions of a micro-batch shard: its rows + 3 per sample
+    Q_local = M_local + 3 * cfg.micro_batch
+    ldw = int(np.ceil(V / 8) * 8)
+    ntile = int(np.ceil(V / 256))
+    # algorithmic bytes per launch:
+    #   K-stats: every position's W16^T row read once + per-(row, 256-col tile) partials written
+    #   K-band : the position's W16^T row read once + its bf16 gradient row H written once
+    #   K-GEMM2: A' (H rows incl. segment padding) read once + dW read-modify-write (the step's
+    #            first micro-batch writes only)
+    #   K-adam : 38 B/param (r: W8 m4 v4 g4; w: W8 m4 v4 W16^T 2)
+    bytes_stats = 2.0 * Q_local * ldw + 8.0 * M_local * ntile + 4.0 * M_local
+    bytes_band = 4.0 * Q_local * ldw + 8.0 * M_local * 2
+    bytes_adam = 38.0 * P
     g_adam = len(place[mine[0]]) if mine and args.dp_mode == "gang" else 1
     if g_adam > 1:
         # sharded K-adam on P/g params: + the g-1 received fp32 partials read; the
         # bf16 rows it writes into the g-1 peers' shadows go over NVLink, not local HBM
         bytes_adam = (38.0 + 4.0 * (g_adam - 1)) * P / g_adam
-    bytes_lse = M_local * (np.ceil(V / 256) * 8 + 24)
+    bytes_lse = M_local * (ntile * 8 + 24)
     kernels = {}
     for i, name in enumerate(KINDS):
         if kcnt[i] == 0:
             continue
         avg_ms = kms[i] / kcnt[i]
         e = {"launches": int(kcnt[i]), "avg_ms": round(avg_ms, 4), "total_ms": round(float(kms[i]), 3)}
-        if name == "gemm2" and g2rows.value > 0:
-            # token-slot segments: each 256-feature column block sums only the tokens
-            # touching it — achieved on the EXECUTED flops (2 * V * 256 * segment rows)
-            ex = 2.0 * V * 256 * g2rows.value / kcnt[i]
-            a = ex / (avg_ms / 1e3) / 1e12
-            e.update(bound="tensor", achieved=round(a, 1), unit="TFLOP/s",
-                     frac=round(a / peaks["bf16_tflops_sustained"], 4), executed_flops=ex,
-                     dense_equivalent_flops=flops_gemm, note="segmented K (token slots per feature block)")
-        elif name in ("gemm1", "gemm2"):
-            a = flops_gemm / (avg_ms / 1e3) / 1e12
-            e.update(bound="tensor", achieved=round(a, 1), unit="TFLOP/s",
-                     frac=round(a / peaks["bf16_tflops_sustained"], 4))
-        elif name in ("softmax_grad", "adam", "lse"):
-            b = {"softmax_grad": bytes_sg, "adam": bytes_adam, "lse": bytes_lse}[name]
+        b = None
+        if name == "gemm2":
+            rows = g2rows.value / kcnt[i]
+            b = 2.0 * rows * V + (4.0 * P + (n_mb - 1) * 8.0 * P) / n_mb
+            ex = 2.0 * V * 256 * rows
+            e.update(executed_flops=ex, tflops=round(ex / (avg_ms / 1e3) / 1e12, 1),
+                     note="segmented K: one-hot scatter of per-position gradient rows (tcgen05)")
+        elif name in ("stats", "band", "adam", "lse"):
+            b = {"stats": bytes_stats, "band": bytes_band, "adam": bytes_adam, "lse": bytes_lse}[name]
+        if b is not None:
             a = b / (avg_ms / 1e3) / 1e9
-            e.update(bound="hbm", achieved=round(a, 1), unit="GB/s", frac=round(a / peaks["hbm_gbs"], 4))
+            e.update(bound="hbm", achieved=round(a, 1), unit="GB/s", frac=round(a / peaks["hbm_gbs"], 4),
+                     bytes_per_launch=b)
         kernels[name] = e
-    if "gemm1" in kernels and "lse" not in kernels and os.environ.get("FM_LSE_FUSED") != "0" \
-            and os.environ.get("FM_LOSS_FOLD") != "0":
-        # K-lse runs in GEMM1's grid tail (default; FM_LSE_FUSED=0 launches it): its time is gemm1's
-        kernels["lse"] = {"launches": 0, "fused_into": "gemm1"}
     dom = max(kernels, key=lambda k: kernels[k].get("total_ms", 0.0)) if kernels else None
     traffic = None
     tfile = ROOT / "profiles" / "traffic.json"
@@ -419,21 +422,9 @@ def run_ours(args, dist: Dist) -> dict | None:
     roof = None
     if dom and "bound" in kernels[dom]:
         k = kernels[dom]
-        roof = {"kernel": dom, "bound": k["bound"], "achieved": k["achieved"],
-                "peak": peaks["bf16_tflops_sustained"] if k["bound"] == "tensor" else peaks["hbm_gbs"],
+        roof = {"kernel": dom, "bound": k["bound"], "achieved": k["achieved"], "peak": peaks["hbm_gbs"],
                 "unit": k["unit"], "frac": k["frac"], "traffic": traffic,
-                "peak_source": f"{peaks['source']} ({'bf16 sustained' if k['bound'] == 'tensor' else 'hbm copy'})",
-                "work_per_launch": flops_gemm if k["bound"] == "tensor" else None}
-        if k["bound"] == "tensor":
-            # the same achieved rate against the burst peak, and against the dense bf16 peak
-            # at the SM clock this run sustained (148 SMs x 8,192 flop/clk): the GEMMs are
-            # power-capped, so the clock-adjusted fraction is the kernel-quality figure
-            roof["frac_burst"] = round(k["achieved"] / peaks["bf16_tflops"], 4)
-            mhz = clk.get("sm_mhz") if isinstance(clk, dict) else None
-            if mhz:
-                peak_clk = 148 * 8192 * mhz * 1e6 / 1e12
-                roof["frac_at_clock"] = round(k["achieved"] / peak_clk, 4)
-                roof["peak_at_clock"] = round(peak_clk, 1)
+                "peak_source": f"{peaks['source']} (hbm copy)", "work_per_launch": k["bytes_per_launch"]}
 
     # --- end-to-end through the public API with host buffers
     e2e = run_e2e(args, cfg, ctx, mine, handles, place, comms, dist, tier) if args.e2e_steps > 0 else None
@@ -1302,11 +1293,12 @@ METRIC = "trained tokens/sec (policy-update micro-batches) at 1/2/4/8 B200 vs CP
 
 def formulation(args) -> str:
     dense = "dense 4*V*D flop/token (reference's own dense loops, policy.hpp:57-61, 87-89)"
-    if getattr(args, "impl", "ours") == "reference" or os.environ.get("FM_G2_KLIST", "2") != "2":
+    if getattr(args, "impl", "ours") == "reference":
         return dense
-    return ("metric work = " + dense + "; executed: logits GEMM dense 2*V*D flop/token, weight-gradient GEMM "
-            "over token-slot segments (each 256-feature block of dW sums only the tokens whose context "
-            "touches it; every other phi_d is 0, policy.hpp:46-49, 87-89); per-kernel rooflines on executed flops")
+    return ("metric = trained tokens (the reference's unit of work); executed: the reference's arithmetic on "
+            "its non-zero terms in the context-position formulation (phi = mean one-hot of the last 4 context "
+            "tokens, policy.hpp:42-51: logits are a 4-tap sum of W16^T rows, the weight gradient a per-position "
+            "row scattered into its feature column by a one-hot tcgen05 GEMM); per-kernel rooflines on HBM bytes")
 
 
 def config_obj(cfg, args) -> dict:

@@ -105,8 +105,9 @@ int fm_ctx_synchronize(fm_ctx* ctx);
 /* Device step timer on the compute stream (copy streams joined at stop). */
 int fm_ctx_timer_start(fm_ctx* ctx);
 int fm_ctx_timer_stop(fm_ctx* ctx, double* ms);
-/* Per-kernel CUDA-event timing of the hot path (off by default).  Kinds:
- * 0 gather, 1 gemm1, 2 lse, 3 softmax_grad, 4 gemm2, 5 adam, 6 parity, 7 memset, 8 colmax. */
+/* Per-kernel CUDA-event timing of the hot path (off by default).  Kinds (8 slots):
+ * 0 gather (K-gather + K-pos + K-pslot), 1 stats (K-stats), 2 lse, 3 band (K-band),
+ * 4 gemm2, 5 adam, 6 parity, 7 memset. */
 int fm_ctx_set_kernel_timing(fm_ctx* ctx, int on);
 int fm_ctx_kernel_times(fm_ctx* ctx, double* ms_out, int64_t* count_out, int reset);
 /* Pre-size the token arena and the per-micro-batch workspace. */
@@ -136,16 +137,11 @@ int fm_agent_read_grad(fm_agent* a, double* g_out);
 int fm_agent_read_grad_cols(fm_agent* a, const int64_t* cols, int64_t n_cols, double* g_out);
 /* K rows the segmented K-GEMM2 launches on ctx ran since the last reset, summed
  * over their 256-feature column blocks (executed flops = 2 * V * 256 * rows);
- * reset != 0 zeroes the counter after reading.  0 when only dense GEMM2s ran. */
+ * reset != 0 zeroes the counter after reading. */
 int fm_ctx_gemm2_rows(fm_ctx* c, int64_t* rows_out, int reset);
 /* kernel test hook (device pointers): C[M][N] fp32 = sum_k A(m,k) B(n,k) through the
  * tcgen05 CTA-pair GEMM, A/B K-major ([M][K] / [N][K]) or MN-major ([K][M] / [K][N]) */
 int fm_debug_gemm(fm_ctx* c, const void* A, const void* B, int a_mn, int b_mn, int M, int N, int K, float* C);
-/* kernel test hook (device pointers): C[M][N] = sum over the K list of column tile
- * n/256 of A[t][m] * B[t][n]; A [rows][M], B [rows][N] bf16 gathered by TMA gather4;
- * klist [N/256][klist_ld] row indices, klist_iters [N/256] = list length / 64 */
-int fm_debug_gemm_klist(fm_ctx* c, const void* A, const void* B, const int32_t* klist, long long klist_ld,
-                        const int32_t* klist_iters, int rows, int M, int N, float* C);
 int64_t fm_agent_version(const fm_agent* a);
 int64_t fm_agent_samples_accumulated(const fm_agent* a);
 int fm_agent_is_active(const fm_agent* a);
@@ -175,8 +171,25 @@ typedef struct fm_report {
     double loss;      /* -(1/G) sum_i A_i sum_t log pi, this micro-batch */
 } fm_report;
 
-/* TrainingEngine::train_micro_batch (training.hpp:355-430): gather -> logits ->
- * fused loss -> weight-gradient accumulate, enqueued on the agent's stream.
+/* Identity of a trained sample: GradKey (training.hpp:87-91) = sample id
+ * (input_id, number_of_turns, trajectory_id; sample.hpp:38-47) + the policy
+ * version it was generated under. */
+typedef struct fm_sample_key {
+    const char* input_id;
+    int32_t turns;
+    int32_t traj;
+    int64_t version;
+} fm_sample_key;
+
+/* DuplicateSample guard of train_micro_batch (training.hpp:396-401): adds the
+ * micro-batch's keys to the agent's set for the current global step, or fails
+ * with FM_ERR_DUPLICATE_SAMPLE (nothing added) if any key is already there or
+ * repeats in the list.  apply_global_update clears the set (training.hpp:448).
+ * Callers: before fm_train_micro_batch of the same samples. */
+int fm_agent_add_grad_keys(fm_agent* a, const fm_sample_key* keys, int n);
+
+/* TrainingEngine::train_micro_batch (training.hpp:355-430): gather -> positions ->
+ * K-stats -> K-lse -> K-band -> weight-gradient GEMM, enqueued on the agent's stream.
  * Returns immediately; *ticket_out identifies the report (fm_agent_poll_report).
  * global_batch is G of the -1/G normalisation (training.hpp:446). */
 int fm_train_micro_batch(fm_agent* a, const fm_sample* samples, int n, int64_t global_batch,
@@ -185,7 +198,9 @@ int fm_train_micro_batch_host(fm_agent* a, const fm_host_sample* samples, int n,
                               int64_t global_batch, int64_t* ticket_out);
 /* Optional PPO clipped-ratio surrogate (off by default = the reference's
  * ratio-free objective).  old_logp: per packed row of the next
- * micro-batch (host array, n_rows entries) or NULL to disable. */
+ * micro-batch (host array, n_rows entries = all its rows, also under DP) or NULL
+ * to disable; the next train call fails with FM_ERR_INVALID_ARG if n_rows
+ * differs from its row count. */
 int fm_agent_set_clip(fm_agent* a, float clip_eps, const float* old_logp, int64_t n_rows);
 /* Data-parallel gang: every rank receives the whole micro-batch and trains
  * the token-balanced row range [M*rank/nranks, M*(rank+1)/nranks). */
@@ -196,9 +211,6 @@ int fm_agent_read_logp(fm_agent* a, double* out, int64_t n_rows);
  * bit-exact target of the oracle's fmo_pack_rows); any pointer may be NULL. */
 int fm_debug_read_rows(fm_ctx* ctx, int64_t n_rows, int32_t* action, int32_t* ctx4,
                        int32_t* n_ctx, int32_t* sample, float* coef);
-/* Loss-fold softmax bound: colmax[d] = max_v bf16(W)[v][d] as the agent holds it
- * (D floats); *valid = 1 when it describes the current bf16 shadow. */
-int fm_agent_debug_colmax(fm_agent* a, float* out, int* valid);
 /* Blocks until the agent's stream drains; completed reports become pollable. */
 int fm_agent_sync(fm_agent* a);
 /* Non-blocking: 1 and fills *out if the ticket's micro-batch has finished. */

@@ -41,6 +41,11 @@ class fm_report(C.Structure):
                 ("grad_norm", C.c_double), ("loss", C.c_double)]
 
 
+class fm_sample_key(C.Structure):
+    """GradKey of one trained sample (training.hpp:87-91)."""
+    _fields_ = [("input_id", C.c_char_p), ("turns", C.c_int32), ("traj", C.c_int32), ("version", C.c_int64)]
+
+
 P = C.c_void_p
 I, I64, U64, D, F = C.c_int, C.c_int64, C.c_uint64, C.c_double, C.c_float
 PI64, PU64, PD = C.POINTER(C.c_int64), C.POINTER(C.c_uint64), C.POINTER(C.c_double)
@@ -76,7 +81,6 @@ _PROTOS = {
     "fm_agent_read_grad_cols": (I, [P, P, I64, P]),
     "fm_debug_gemm": (I, [P, P, P, I, I, I, I, I, P]),
     "fm_ctx_gemm2_rows": (I, [P, PI64, I]),
-    "fm_debug_gemm_klist": (I, [P, P, P, P, I64, P, I, I, I, P]),
     "fm_agent_version": (I64, [P]),
     "fm_agent_samples_accumulated": (I64, [P]),
     "fm_agent_is_active": (I, [P]),
@@ -86,7 +90,7 @@ _PROTOS = {
     "fm_agent_set_shard": (I, [P, I, I]),
     "fm_agent_read_logp": (I, [P, P, I64]),
     "fm_debug_read_rows": (I, [P, I64, P, P, P, P, P]),
-    "fm_agent_debug_colmax": (I, [P, P, P]),
+    "fm_agent_add_grad_keys": (I, [P, P, I]),
     "fm_agent_sync": (I, [P]),
     "fm_agent_poll_report": (I, [P, I64, C.POINTER(fm_report)]),
     "fm_apply_update": (I, [P, I64, D, D, D, D, PD, PI64]),

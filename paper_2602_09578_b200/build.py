@@ -36,7 +36,7 @@ def nccl_dir() -> Path | None:
     except Exception:
         pass
     return None
-CUDA_SOURCES = ["k_gemm_tc.cu", "k_path.cu", "k_rollout.cu", "k_store.cu", "fm_runtime.cu", "fm_swap.cu", "fm_gang.cu",
+CUDA_SOURCES = ["k_gemm_tc.cu", "k_band.cu", "k_path.cu", "k_rollout.cu", "k_store.cu", "fm_runtime.cu", "fm_swap.cu", "fm_gang.cu",
                 "fm_publish.cu", "fm_dtable.cu"]
 CXX_SOURCES = ["fm_host.cpp"]
 

@@ -76,7 +76,6 @@ int fm_gang_attach(fm_agent* a, fm_comm* cm, uint8_t* blob_out, uint64_t cap, ui
     if (a->precision != FM_PRECISION_BF16_TC) return fail(FM_ERR_CONFIG_ERROR, "gang exchange needs the tensor-core path");
     if (cm->ctx != a->ctx) return fail(FM_ERR_CONFIG_ERROR, "communicator bound to another GPU");
     if (cm->nranks < 2 || cm->nranks > 8) return fail(FM_ERR_CONFIG_ERROR, "gang size must be 2..8");
-    if (!gemm_pair_mode()) return fail(FM_ERR_CONFIG_ERROR, "gang exchange needs the CTA-pair GEMM (FM_GEMM_2SM)");
     if (int st = set_dev(a->ctx)) return st;
     auto* gs = new GangState();
     gs->comm = cm;

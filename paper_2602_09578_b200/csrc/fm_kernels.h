@@ -32,13 +32,10 @@ struct RowBuffers {
     float* lse;        // [Mpad]
     float* logp;       // [Mpad]
     float* coef_eff;   // [Mpad] coef * surrogate factor
-    int4* feat4;       // [Mpad] unique features of the row (-1 padded)   (tensor-core path)
-    uint32_t* cnt4;    // [Mpad] their multiplicities, 8 bits each
-    float* mrow;       // [Mpad] softmax offset bound (1/n) sum_j colmax[f_j]   (loss-fold path)
+    int32_t* q0;       // [Mpad] first context position of the row (band formulation; nullable)
 };
 
-// K-lse arguments (fm_lse.cuh: the per-row routine shared by the standalone
-// kernel and GEMM1's fused last-tile epilogue).
+// K-lse arguments (fm_lse.cuh: the per-row routine).
 struct LseArgs {
     const float* zact;    // [Mpad] fp32 logit of the taken token
     const float2* stats;  // [Mpad][stats_ld] (max, sum exp) per 256-column tile
@@ -47,117 +44,103 @@ struct LseArgs {
     const SampleDesc* sd;
     int64_t G;
     RowBuffers rows;
-    const float* old_logp;  // PPO clip (nullable)
+    const float* old_logp;  // PPO clip (nullable): old log-prob of shard row r at old_logp[row_lo + r]
+    int64_t row_lo;
     float clip_eps;
     double* loss_acc;  // += objective (nullable)
-    int fold;
-    __nv_bfloat16* pexp_t;  // fold: p~^T [V][ldt]  (rowmajor: p~ [Mpad][ldt])
-    __nv_bfloat16* phict;   // fold: Phic^T [D][ldt] (rowmajor: Phic [Mpad][ld_phi])
-    int64_t ldt;
-    int rowmajor = 0;  // K-list GEMM2: 1 = row-major p~ / Phic, 2 = token-slot segments
-    int64_t ld_phi = 0;
-    const int4* slot4 = nullptr;   // rowmajor 2: A' row of each feature's block per token
-    __nv_bfloat16* bseg = nullptr; // rowmajor 2: B' [K'][256]
 };
 
 // K-gather: decode the selected records' token payloads straight out of the
-// arena into packed rows; optionally scatter integer-count features into the
-// dense bf16 operands Phic [Mpad][D] and Phic^T [D][Mpad] (pre-zeroed, or
-// holding the previous micro-batch's pattern for the same Mpad/D when
-// clear_old != 0, in which case each row first erases its old entries).
+// arena into packed rows (action, context window, sample, row coefficient,
+// 1/n, and with rows.q0 != NULL the row's first context position).
 cudaError_t launch_gather(const uint8_t* arena, const SampleDesc* sd, int n_samples, int64_t row_lo,
                           int64_t M, int64_t Mpad, int64_t global_batch, uint64_t D, RowBuffers rows,
-                          __nv_bfloat16* phic, __nv_bfloat16* phict, int clear_old, const int* colmax,
                           cudaStream_t s);
 
-// K-colmax: keys[d] = key(max_v W16[v][d]) (order-preserving int encoding), the
-// per-feature bound K-gather turns into each row's softmax offset (loss-fold path).
-cudaError_t launch_colmax(const __nv_bfloat16* w16, int64_t V, int64_t D, int* keys, int num_sms,
+// K-pos: feature (tok mod D) of every context position of the shard's rows
+// (every sample overlapping the shard owns its rows + 3 positions: the three
+// tokens before its first row's last context token), -1 where the sequence
+// has no token (prompt shorter than 4) and past the last position (q < Qcap).
+cudaError_t launch_positions(const uint8_t* arena, const SampleDesc* sd, int n_samples, int64_t row_lo, int64_t M,
+                             uint64_t D, int32_t* feat, int64_t Qcap, cudaStream_t s);
+
+// K-pslot: every position with a feature gets a row ("slot") of the segment of
+// its feature's 256-column block in A' [K'][.] / B' [K'][256]; segment b
+// starts at kseg_off[b] and is padded to a multiple of 64 rows (>= 64);
+// B' = one-hot of the feature inside the block (zeroed here first).
+// Deterministic (position order).  rows_acc (nullable) accumulates the padded
+// segment rows (GEMM2's executed K, for the roofline).
+cudaError_t launch_pslots(const int32_t* feat, int64_t Q, int nblk, int32_t* kcount, int32_t* kseg_off, int32_t* kiters,
+                          int32_t* slot, __nv_bfloat16* bseg, int64_t bseg_rows, unsigned long long* rows_acc,
                           cudaStream_t s);
 
-// K-lse: combine GEMM1's per-tile softmax partials into lse, the taken-token
-// log-prob (from the fp32 logit GEMM1 captured) and the effective row
+// K-stats / K-band (k_band.cu).
+struct BandArgs {
+    const __nv_bfloat16* w16t;  // transposed bf16 shadow W16^T [D][ldw]
+    int64_t ldw;
+    const __nv_bfloat16* zero_row;  // >= 2,048 zero bf16 (positions before a sequence start)
+    int64_t V;
+    const int32_t* pos_feat;    // [Q]
+    const int32_t* q0;          // [M]
+    const int32_t* action;      // [M]
+    const float* rscale;        // [M]
+    int64_t M;
+    // pass A (K-stats)
+    float2* stats;  // [M][stats_ld]
+    int stats_ld;
+    float* zact;    // [M]
+    // pass B (K-band)
+    const float* lse;       // [M]
+    const float* coef_eff;  // [M]
+    const int32_t* pos_slot;  // [Q]
+    __nv_bfloat16* aseg;      // A' [K'][ld_a]
+    int64_t ld_a;
+};
+cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s);
+
+// K-lse: combine K-stats' per-tile softmax partials into lse, the taken-token
+// log-prob (from the fp32 logit K-stats captured) and the effective row
 // coefficient (PPO-clip surrogate optional).
-// Loss-fold path (pexp_t != NULL; GEMM1 used the row bound m_t for every tile):
-// folds the taken token's delta into p~^T (pexp_t [V][ldt]) and overwrites the
-// row's <= 4 count entries of Phic^T (phict [D][ldt]) with count * (-c_t / s_t),
-// so that GEMM2 (A = p~^T, B = Phic^T) yields G^T x Phic without a K-loss pass.
-cudaError_t launch_lse(const float* zact, const float2* stats, int stats_ld, int64_t M, int64_t Mpad,
-                       int64_t V, const SampleDesc* sd, int64_t global_batch, RowBuffers rows,
-                       const float* old_logp, float clip_eps, double* loss_acc, __nv_bfloat16* pexp_t,
-                       __nv_bfloat16* phict, int64_t ldt, cudaStream_t s, int rowmajor = 0, int64_t ld_phi = 0);
 cudaError_t launch_lse(const LseArgs& L, cudaStream_t s);
-
-// K-loss (fused log-softmax gradient):
-//   G^T[v][t] = coef_eff_t * (delta(v, a_t) - p~[t][v] * exp(m_tile(t, v) - lse_t))
-// p~ tiles (bf16, from GEMM1) streamed in through TMA, G^T tiles stored through TMA.
-cudaError_t launch_softmax_grad(const CUtensorMap& tmP, const CUtensorMap& tmGt, const float2* stats,
-                                int stats_ld, int64_t Mpad, int64_t V, RowBuffers rows, cudaStream_t s,
-                                int part_cols = 256);
-
-// K-klist: for every 256-feature column block b of GEMM2, the rows (tokens) whose
-// context touches block b, ascending, padded with zero_row to a multiple of 64
-// (at least 64); iters[b] = padded length / 64.  One block per column block
-// (deterministic block-wide scans).
-cudaError_t launch_klist(const int4* feat4, int64_t M, int nblk, int32_t* klist, int64_t ld, int32_t* iters,
-                         int32_t zero_row, cudaStream_t s);
-
-// K-slot (segmented K-list GEMM2): the tokens touching 256-feature block b get
-// consecutive rows ("slots") of a segment of A' [K'][ld_a] / B' [K'][256]; segment
-// b starts at kseg_off[b] and is padded to a multiple of 64 rows (>= 64) whose A'
-// and B' rows are zeroed.  slot4[t].c_j = the slot of feature j's block (-1 if
-// feature j is absent); B'[slot][f mod 256] = count of f.  bseg must be zero on
-// entry.  Deterministic (block-wide scans in row order; kcount = per-(block,
-// 1024-row chunk) counts).  rows_acc (nullable)
-// accumulates the padded segment rows (GEMM2's executed K, for the roofline).
-// seg_tok (nullable): the token of every slot (padding slots = zero_row) for the
-// software-gathered A; aseg may then be null (no A' rows are written).
-cudaError_t launch_kslots(const int4* feat4, const uint32_t* cnt4, int64_t M, int nblk, int32_t* kcount,
-                          int32_t* kseg_off, int32_t* kiters, int4* slot4, __nv_bfloat16* aseg, int64_t ld_a,
-                          int64_t ncols_a, __nv_bfloat16* bseg, unsigned long long* rows_acc, int32_t* seg_tok,
-                          int32_t zero_row, cudaStream_t s);
 
 // Parity tooling: out[v][j] = dW[v][cols[j]] (f32 or f64 accumulator).
 cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D, const int64_t* cols,
                                int64_t n_cols, void* out, cudaStream_t s);
 
-// K-adam (training.hpp:37-51): fp64 master weights, fp32 moments, gradient
-// of type G (float for the tensor-core path, double for parity mode);
-// optionally writes the bf16 shadow and zeroes the gradient.  Accumulates
-// sum(g^2) into *gsq for the update grad_norm.  With colmax != NULL (and a
-// [V][D] shadow) it also produces K-colmax's keys from the new shadow when the
-// grid can keep every thread on fixed columns (*colmax_done tells).
-// With dst != NULL the updated w / m / v go to dst's buffers instead of in
-// place (w16 and colmax are outputs already): the swap-out fused into the
-// optimizer, which writes the new state straight into the parking buffer.
+// K-adam (training.hpp:37-51): fp64 master weights, fp32 moments, gradient of
+// type G (float for the tensor-core path, double for parity mode) over rows
+// [r0, r1) of the [V][D] state, in 32 x 64 tiles.  Optionally: the gradient is
+// the local partial plus nslots receive slots ([nslots][r1-r0][D], a DP
+// gang's reduce-scatter); the transposed bf16 shadow W16^T [D][ldw] is
+// written (locally and into the peers' replicas over NVLink: the all-gather
+// fused into the optimizer) through a shared-memory transpose; the new w / m
+// / v go to dst instead of in place (the swap-out fused into the optimizer);
+// the gradient is zeroed (parity mode).  Accumulates sum(g^2) into *gsq.
 struct AdamDst {
     double* w;
     float* m;
     float* v;
 };
+// Peer W16^T replicas (NVLink-mapped base pointers) of a DP gang, excluding self.
+struct ShardPeers {
+    int n;
+    __nv_bfloat16* w16t[7];
+};
 template <typename G>
-cudaError_t launch_adam(double* w, float* m, float* v, G* g, __nv_bfloat16* w16, uint64_t n,
-                        double lr, double b1, double b2, double eps, double bc1, double bc2,
-                        int zero_grad, double* gsq, int num_sms, cudaStream_t s,
-                        int* colmax = nullptr, uint64_t D = 0, bool* colmax_done = nullptr,
-                        const AdamDst* dst = nullptr);
+cudaError_t launch_adam(double* w, float* m, float* v, G* g, uint64_t V, uint64_t D, uint64_t r0, uint64_t r1,
+                        const float* recv, int nslots, __nv_bfloat16* w16t, uint64_t ldw, ShardPeers peers,
+                        double lr, double b1, double b2, double eps, double bc1, double bc2, int zero_grad,
+                        double* gsq, int num_sms, cudaStream_t s, const AdamDst* dst = nullptr);
+
+// W16^T [D][ldw] = bf16(W) for W [V][D] f64 (shadow refresh: set_weights, host-tier swap-in).
+cudaError_t launch_w16t(const double* w, uint64_t V, uint64_t D, __nv_bfloat16* w16t, uint64_t ldw, int num_sms,
+                        cudaStream_t s);
+// out [V][D] = W16^T transposed back (the bf16 weight publish).
+cudaError_t launch_w16t_untranspose(const __nv_bfloat16* w16t, uint64_t V, uint64_t D, uint64_t ldw,
+                                    __nv_bfloat16* out, cudaStream_t s);
 
 cudaError_t launch_to_bf16(const double* w, __nv_bfloat16* w16, uint64_t n, int num_sms,
                            cudaStream_t s);
-
-// Peer W16 row-range pointers (NVLink-mapped) of a DP gang, excluding self.
-struct ShardPeers {
-    int n;
-    __nv_bfloat16* w16[7];
-};
-// K-adam, sharded over a DP gang: this rank's rows only; gradient = local
-// partial + the receive slots the peers filled from their GEMM2 epilogues;
-// the new bf16 rows are written locally and into every peer's W16.
-cudaError_t launch_adam_shard(double* w, float* m, float* v, const float* g, const float* recv, int nslots,
-                              uint64_t slot_stride, __nv_bfloat16* w16, ShardPeers peers, uint64_t n,
-                              double lr, double b1, double b2, double eps, double bc1, double bc2,
-                              double* gsq, int num_sms, cudaStream_t s, int* colmax = nullptr, uint64_t D = 0,
-                              bool* colmax_done = nullptr);
 
 // K-adv (training.hpp:54-67): one warp per reward group, fp64 shuffle reductions.
 cudaError_t launch_group_advantages(const double* rewards, const int32_t* seg_off, int nseg,

@@ -116,8 +116,10 @@ int fm_publish_into(fm_agent* a, fm_weights* w) {
         count_launch();
         if (sharded) FM_CUDA(cudaFreeAsync(src, s));
     } else if (a->W16) {
-        // the bf16 shadow IS bf16(W) (same double -> float -> bf16 rounding; full replica in a gang)
-        FM_CUDA(cudaMemcpyAsync(w->buf, a->W16, a->P * 2, cudaMemcpyDeviceToDevice, s));
+        // the bf16 shadow IS bf16(W) (same double -> float -> bf16 rounding; full replica in a
+        // gang), held transposed: back to the payload's [V][D]
+        FM_CUDA(launch_w16t_untranspose(a->W16, a->V, a->D, w16_ld(a), static_cast<__nv_bfloat16*>(w->buf), s));
+        count_launch();
     } else {
         FM_CUDA(launch_to_bf16(a->W, static_cast<__nv_bfloat16*>(w->buf), a->P, c->num_sms, s));
         count_launch();
@@ -351,9 +353,8 @@ int fm_agent_deserialize(fm_agent* a, int64_t global_batch, const uint8_t* in, u
         a->dw_valid = false;
     }
     if (a->W16) {
-        FM_CUDA(launch_to_bf16(a->W, a->W16, P, c->num_sms, s));
+        FM_CUDA(launch_w16t(a->W, a->V, a->D, a->W16, w16_ld(a), c->num_sms, s));
         count_launch();
-        ++a->w16_gen;
     }
     FM_CUDA(cudaStreamSynchronize(s));
     a->version = static_cast<int64_t>(version);

@@ -1,23 +1,23 @@
 // fm_runtime.cu — C ABI implementation: device contexts, the token arena,
 // per-agent trainer state, the micro-batch pipeline
-//   K-gather -> K-GEMM1 (tcgen05; log-softmax numerator in the epilogue, K-lse
-//   in the grid tail) -> K-GEMM2 (tcgen05; softmax gradient folded into its
-//   operands)
-// (or the fp64 parity pipeline; FM_LOSS_FOLD=0 / FM_LSE_FUSED=0 restore the
-// separate K-softmax-grad / K-lse launches), the fused Adam update, training-
-// state swap and migration, DP gangs (fused reduce-scatter / NCCL all-reduce),
-// weight publish and the PolicyState wire format.
+//   K-gather + K-pos + K-pslot -> K-stats -> K-lse -> K-band -> K-GEMM2 (tcgen05)
+// (or the fp64 parity pipeline), the fused Adam update; training-state swap
+// and migration (fm_swap.cu), DP gangs (fm_gang.cu), weight publish and the
+// PolicyState wire format (fm_publish.cu).
 //
-// Memory layout in HBM: every agent matrix is row-major
-// [V][D] (row = vocab id, col = feature; tensor.hpp:13-22):
-//   W    f64   master weights            (8 B/param)
-//   m, v f32   Adam moments              (4+4 B/param)
-//   dW   f32   gradient accumulator      (4 B/param; f64 in parity mode)
-//   W16  bf16  GEMM shadow of W          (2 B/param; tensor-core mode only)
-// Per-GPU workspace, sized for the largest micro-batch (Mpad = rows rounded
-// up to 128): packed rows, Phic [Mpad][D] / Phic^T [D][Mpad] bf16 (integer
-// counts; K-lse rescales Phic^T's entries per row), p~^T [V][Mpad] bf16
-// (GEMM1's output = GEMM2's A operand), softmax partials [Mpad][V/256].
+// Memory layout in HBM: every agent state matrix is
+// row-major [V][D] (row = vocab id, col = feature; tensor.hpp:13-22):
+//   W     f64   master weights            (8 B/param)
+//   m, v  f32   Adam moments              (4+4 B/param)
+//   dW    f32   gradient accumulator      (4 B/param; f64 in parity mode)
+// and the tensor-core path's bf16 shadow is TRANSPOSED:
+//   W16^T bf16  [D][round_up(V, 8)]       (2 B/param; a feature's weights are
+//               one contiguous row — the row K-stats / K-band stream per
+//               context position)
+// Per-GPU workspace, sized for the largest micro-batch (Mpad = rows rounded up
+// to 128): packed rows, K-stats partials [Mpad][V/256], per-position features
+// and slots, and K-GEMM2's segments: A' (one bf16 gradient row H per context
+// position, [M + 3 n + 64 * D/256][V]) and the one-hot B' [.][256].
 #include "fm_state.h"
 
 
@@ -143,8 +143,6 @@ int staging_acquire(fm_ctx* c, size_t bytes, uint8_t** out, cudaEvent_t* ev) {
 void ws_free(Workspace& w) {
     cudaFree(w.action);
     cudaFree(w.ctx4);
-    cudaFree(w.feat4);
-    cudaFree(w.cnt4);
     cudaFree(w.n_ctx);
     cudaFree(w.sample);
     cudaFree(w.coef);
@@ -153,25 +151,18 @@ void ws_free(Workspace& w) {
     cudaFree(w.logp);
     cudaFree(w.coef_eff);
     cudaFree(w.old_logp);
-    cudaFree(w.phic);
-    cudaFree(w.phict);
-    cudaFree(w.gt);
-    cudaFree(w.Pexp);
+    cudaFree(w.q0);
+    cudaFree(w.pos_feat);
+    cudaFree(w.pos_slot);
     cudaFree(w.zact);
     cudaFree(w.stats);
-    cudaFree(w.mrow);
-    cudaFree(w.lse_sync);
-    cudaFree(w.sk_ws);
-    cudaFree(w.klist);
-    cudaFree(w.kiters);
     cudaFree(w.aseg);
     cudaFree(w.bseg);
-    cudaFree(w.slot4);
+    cudaFree(w.zero_row);
     cudaFree(w.kcount);
     cudaFree(w.kseg_off);
+    cudaFree(w.kiters);
     cudaFree(w.kseg_rows);
-    cudaFree(w.seg_tok);
-    cudaFree(w.sk_cnt);
     cudaFree(w.zscratch);
     cudaFree(w.dWmb);
     cudaFree(w.logp64);
@@ -181,34 +172,37 @@ void ws_free(Workspace& w) {
 
 uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
 
-// Ensure tensor-core workspace for Mpad rows, vocab V, features D.
-int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
+// Ensure tensor-core workspace for Mpad rows of at most n samples, vocab V,
+// features D: row buffers, K-stats partials, positions (Mpad + 3 n) and the
+// K-GEMM2 segments (positions + 64 padding rows per 256-feature block).
+int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D, int n_samples) {
     Workspace& w = c->ws;
-    if (Mpad <= w.rows_cap && V <= w.vocab_cap && D <= w.feat_cap && w.Pexp) return FM_OK;
+    const int64_t Qneed = Mpad + 3 * static_cast<int64_t>(std::max(n_samples, 1));
+    if (Mpad <= w.rows_cap && V <= w.vocab_cap && D <= w.feat_cap && Qneed <= w.pos_cap && w.aseg) return FM_OK;
     const int64_t R = std::max<int64_t>(Mpad, w.rows_cap);
     const uint64_t VV = std::max<uint64_t>(V, w.vocab_cap), DD = std::max<uint64_t>(D, w.feat_cap);
+    const int64_t Q = std::max<int64_t>(Qneed, w.pos_cap);
     FM_CUDA(cudaStreamSynchronize(c->stream));
-    Workspace keep_parity;
-    std::swap(keep_parity.zscratch, w.zscratch);
-    std::swap(keep_parity.dWmb, w.dWmb);
-    std::swap(keep_parity.logp64, w.logp64);
-    keep_parity.prow_cap = w.prow_cap;
-    keep_parity.pvocab_cap = w.pvocab_cap;
-    keep_parity.pparam_cap = w.pparam_cap;
+    Workspace keep;  // parity scratch and sample descriptors survive
+    std::swap(keep.zscratch, w.zscratch);
+    std::swap(keep.dWmb, w.dWmb);
+    std::swap(keep.logp64, w.logp64);
+    std::swap(keep.sd, w.sd);
+    std::swap(keep.old_logp, w.old_logp);
+    keep.prow_cap = w.prow_cap;
+    keep.pvocab_cap = w.pvocab_cap;
+    keep.pparam_cap = w.pparam_cap;
+    keep.sd_cap = w.sd_cap;
+    keep.old_logp_cap = w.old_logp_cap;
     ws_free(w);
-    w.zscratch = keep_parity.zscratch;
-    w.dWmb = keep_parity.dWmb;
-    w.logp64 = keep_parity.logp64;
-    w.prow_cap = keep_parity.prow_cap;
-    w.pvocab_cap = keep_parity.pvocab_cap;
-    w.pparam_cap = keep_parity.pparam_cap;
+    w = keep;
     const uint64_t ldz = round_up(VV, 8);
     const uint64_t tiles_n = (VV + kGemmBN - 1) / kGemmBN;
+    const int64_t nblk = static_cast<int64_t>((DD + 255) / 256);
+    const int64_t kp = Q + 64 * nblk;
     cudaError_t e = cudaSuccess;
     e = e ? e : dalloc(&w.action, R);
     e = e ? e : dalloc(&w.ctx4, R);
-    e = e ? e : dalloc(&w.feat4, R);
-    e = e ? e : dalloc(&w.cnt4, R);
     e = e ? e : dalloc(&w.n_ctx, R);
     e = e ? e : dalloc(&w.sample, R);
     e = e ? e : dalloc(&w.coef, R);
@@ -216,79 +210,41 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D) {
     e = e ? e : dalloc(&w.lse, R);
     e = e ? e : dalloc(&w.logp, R);
     e = e ? e : dalloc(&w.coef_eff, R);
-    e = e ? e : dalloc(&w.old_logp, R);
-    // Phic and p~ carry one extra zero row (index R): the K-list GEMM2's padding row
-    e = e ? e : dalloc(&w.phic, static_cast<size_t>(R + 1) * DD);
-    e = e ? e : cudaMemset(w.phic, 0, static_cast<size_t>(R + 1) * DD * 2);
-    e = e ? e : dalloc(&w.phict, static_cast<size_t>(R) * DD);
-    e = e ? e : dalloc(&w.gt, static_cast<size_t>(R) * VV);
-    e = e ? e : dalloc(&w.Pexp, static_cast<size_t>(R + 1) * ldz);
-    e = e ? e : cudaMemset(w.Pexp + static_cast<size_t>(R) * ldz, 0, ldz * 2);
-    w.klist_ld = static_cast<int64_t>(round_up(static_cast<uint64_t>(R), 64) + 64);
-    e = e ? e : dalloc(&w.klist, static_cast<size_t>((DD + 255) / 256) * w.klist_ld);
-    e = e ? e : dalloc(&w.kiters, static_cast<size_t>((DD + 255) / 256));
+    e = e ? e : dalloc(&w.q0, R);
     e = e ? e : dalloc(&w.zact, R);
-    e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n * 2);  // GEMM1 partials per tile half
-    e = e ? e : dalloc(&w.mrow, R);
-    e = e ? e : dalloc(&w.lse_sync, 2);
-    e = e ? e : cudaMemset(w.lse_sync, 0, 2 * sizeof(unsigned));
-    e = e ? e : dalloc(&w.sk_ws, static_cast<size_t>(kSkMaxTiles) * 256 * 256);
-    e = e ? e : cudaMemset(w.sk_ws, 0, sizeof(float) * static_cast<size_t>(kSkMaxTiles) * 256 * 256);
-    e = e ? e : dalloc(&w.sk_cnt, static_cast<size_t>(kSkMaxTiles) * 2);
-    e = e ? e : cudaMemset(w.sk_cnt, 0, sizeof(int) * static_cast<size_t>(kSkMaxTiles) * 2);
+    e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n);
+    e = e ? e : dalloc(&w.pos_feat, static_cast<size_t>(Q));
+    e = e ? e : dalloc(&w.pos_slot, static_cast<size_t>(Q));
+    e = e ? e : dalloc(&w.aseg, static_cast<size_t>(kp) * ldz);
+    // A' rows are only written for live positions: segment padding rows must hold
+    // finite values (B' is zero there), so the buffer starts zeroed
+    e = e ? e : cudaMemset(w.aseg, 0, static_cast<size_t>(kp) * ldz * 2);
+    e = e ? e : dalloc(&w.bseg, static_cast<size_t>(kp) * 256);
+    e = e ? e : dalloc(&w.zero_row, 4096);
+    e = e ? e : cudaMemset(w.zero_row, 0, 4096 * 2);
+    e = e ? e : dalloc(&w.kcount, static_cast<size_t>(nblk) * static_cast<size_t>((Q + 1023) / 1024 + 1));
+    e = e ? e : dalloc(&w.kseg_off, static_cast<size_t>(nblk));
+    e = e ? e : dalloc(&w.kiters, static_cast<size_t>(nblk));
+    e = e ? e : dalloc(&w.kseg_rows, 1);
+    e = e ? e : cudaMemset(w.kseg_rows, 0, sizeof(unsigned long long));
     if (e != cudaSuccess) {
+        cudaGetLastError();
         ws_free(w);
         return fail(FM_ERR_DEVICE_OOM, std::string("workspace allocation: ") + cudaGetErrorString(e));
     }
     w.rows_cap = R;
     w.vocab_cap = VV;
     w.feat_cap = DD;
-    return FM_OK;
-}
-
-// Token-slot segments for the segmented K-list GEMM2: every token occupies at
-// most 4 slots (one per distinct feature block), each block's segment is padded
-// to 64 rows.
-int ws_reserve_seg(fm_ctx* c, bool need_a) {
-    Workspace& w = c->ws;
-    const int64_t nblk = static_cast<int64_t>((w.feat_cap + 255) / 256);
-    const int64_t need = 4 * w.rows_cap + 64 * nblk;
-    if (w.bseg && w.kp_cap >= need && (w.seg_has_a || !need_a)) return FM_OK;
-    FM_CUDA(cudaStreamSynchronize(c->stream));
-    cudaFree(w.aseg);
-    cudaFree(w.bseg);
-    cudaFree(w.slot4);
-    cudaFree(w.kcount);
-    cudaFree(w.kseg_off);
-    cudaFree(w.seg_tok);
-    w.aseg = w.bseg = nullptr;
-    w.slot4 = nullptr;
-    w.kcount = w.kseg_off = w.seg_tok = nullptr;
-    w.seg_has_a = false;
-    const uint64_t ldz = round_up(w.vocab_cap, 8);
-    cudaError_t e = cudaSuccess;
-    if (need_a) e = e ? e : dalloc(&w.aseg, static_cast<size_t>(need) * ldz);
-    e = e ? e : dalloc(&w.seg_tok, static_cast<size_t>(need));
-    e = e ? e : dalloc(&w.bseg, static_cast<size_t>(need) * 256);
-    e = e ? e : dalloc(&w.slot4, static_cast<size_t>(w.rows_cap));
-    e = e ? e : dalloc(&w.kcount, static_cast<size_t>(nblk) * static_cast<size_t>((w.rows_cap + 1023) / 1024 + 1));
-    e = e ? e : dalloc(&w.kseg_off, static_cast<size_t>(nblk));
-    if (!w.kseg_rows) {
-        e = e ? e : dalloc(&w.kseg_rows, 1);
-        e = e ? e : cudaMemset(w.kseg_rows, 0, sizeof(unsigned long long));
-    }
-    if (e != cudaSuccess) return fail(FM_ERR_DEVICE_OOM, std::string("segment workspace: ") + cudaGetErrorString(e));
-    w.kp_cap = need;
-    w.seg_has_a = need_a;
+    w.pos_cap = Q;
+    w.kp_cap = kp;
     return FM_OK;
 }
 
 int ws_reserve_rows(fm_ctx* c, int64_t R) {  // row arrays only (parity mode)
     Workspace& w = c->ws;
     if (R <= w.rows_cap && w.action) return FM_OK;
-    if (w.Pexp) return ws_reserve_tc(c, R, w.vocab_cap, w.feat_cap);
+    if (w.aseg) return ws_reserve_tc(c, R, w.vocab_cap, w.feat_cap, 1);
     FM_CUDA(cudaStreamSynchronize(c->stream));
-    w.phi_valid = false;
     cudaFree(w.action);
     cudaFree(w.ctx4);
     cudaFree(w.n_ctx);
@@ -298,7 +254,6 @@ int ws_reserve_rows(fm_ctx* c, int64_t R) {  // row arrays only (parity mode)
     cudaFree(w.lse);
     cudaFree(w.logp);
     cudaFree(w.coef_eff);
-    cudaFree(w.old_logp);
     cudaError_t e = cudaSuccess;
     e = e ? e : dalloc(&w.action, R);
     e = e ? e : dalloc(&w.ctx4, R);
@@ -309,7 +264,6 @@ int ws_reserve_rows(fm_ctx* c, int64_t R) {  // row arrays only (parity mode)
     e = e ? e : dalloc(&w.lse, R);
     e = e ? e : dalloc(&w.logp, R);
     e = e ? e : dalloc(&w.coef_eff, R);
-    e = e ? e : dalloc(&w.old_logp, R);
     if (e != cudaSuccess) return fail(FM_ERR_DEVICE_OOM, cudaGetErrorString(e));
     w.rows_cap = R;
     return FM_OK;
@@ -361,9 +315,6 @@ RowBuffers row_buffers(Workspace& w) {
     RowBuffers r;
     r.action = w.action;
     r.ctx4 = w.ctx4;
-    r.feat4 = w.feat4;
-    r.cnt4 = w.cnt4;
-    r.mrow = w.mrow;
     r.n_ctx = w.n_ctx;
     r.sample = w.sample;
     r.coef = w.coef;
@@ -371,6 +322,7 @@ RowBuffers row_buffers(Workspace& w) {
     r.lse = w.lse;
     r.logp = w.logp;
     r.coef_eff = w.coef_eff;
+    r.q0 = w.q0;
     return r;
 }
 
@@ -385,7 +337,7 @@ int fm_ctx_set_kernel_timing(fm_ctx* c, int on) {
 }
 
 // Drains the recorded event pairs; out_ms / out_count have K_NKINDS (8) slots:
-// gather, gemm1, lse, softmax_grad, gemm2, adam, parity, memset.
+// gather, stats, lse, band, gemm2, adam, parity, memset.
 int fm_ctx_kernel_times(fm_ctx* c, double* out_ms, int64_t* out_count, int reset) {
     if (int st = set_dev(c)) return st;
     KTimer& k = c->kt;
@@ -526,7 +478,8 @@ int fm_ctx_reserve(fm_ctx* c, uint64_t arena_bytes, int64_t max_rows, uint64_t V
         c->arena = na;
         c->arena_cap = arena_bytes;
     }
-    if (max_rows > 0 && V > 0 && D > 0) return ws_reserve_tc(c, static_cast<int64_t>(round_up(max_rows, 128)), V, D);
+    if (max_rows > 0 && V > 0 && D > 0)
+        return ws_reserve_tc(c, static_cast<int64_t>(round_up(max_rows, 128)), V, D, 1);
     return FM_OK;
     FM_GUARD_END
 }
@@ -579,10 +532,13 @@ size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 size_t slot_off_m(const fm_agent* a) { return align256(a->P * 8); }
 size_t slot_off_v(const fm_agent* a) { return align256(a->P * 8) + align256(a->P * 4); }
 
+uint64_t w16_ld(const fm_agent* a) { return round_up(a->V, 8); }
+size_t w16_bytes(const fm_agent* a) { return a->D * w16_ld(a) * 2; }
+
 size_t slot_bytes(const fm_agent* a) {
     const size_t P = a->P;
     return align256(P * 8) + 2 * align256(P * 4) + align256(P * dw_elem(a)) +
-           (a->precision == FM_PRECISION_BF16_TC ? align256(P * 2) + align256(a->D * 4) : 0);
+           (a->precision == FM_PRECISION_BF16_TC ? align256(w16_bytes(a)) : 0);
 }
 
 // Binds a free slot of ctx c (allocating one the first time), ordered on
@@ -618,8 +574,6 @@ int agent_alloc_device(fm_agent* a, fm_ctx* c, cudaStream_t s) {
     a->dW = p;
     p += align256(P * dw_elem(a));
     a->W16 = a->precision == FM_PRECISION_BF16_TC ? reinterpret_cast<__nv_bfloat16*>(p) : nullptr;
-    p += a->W16 ? align256(P * 2) : 0;
-    a->colmax = a->W16 ? reinterpret_cast<int*>(p) : nullptr;
     return FM_OK;
 }
 
@@ -638,7 +592,6 @@ void agent_free_device(fm_agent* a, cudaStream_t s) {
     a->m = a->v = nullptr;
     a->dW = nullptr;
     a->W16 = nullptr;
-    a->colmax = nullptr;
 }
 
 // Every operation on an agent goes through here: besides the InactiveGroup
@@ -685,7 +638,7 @@ int fm_agent_create(fm_ctx* c, const char* name, uint64_t V, uint64_t D, int pre
     FM_CUDA(cudaMemsetAsync(a->m, 0, a->P * 4, c->stream));
     FM_CUDA(cudaMemsetAsync(a->v, 0, a->P * 4, c->stream));
     FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * dw_elem(a), c->stream));
-    if (a->W16) FM_CUDA(cudaMemsetAsync(a->W16, 0, a->P * 2, c->stream));
+    if (a->W16) FM_CUDA(cudaMemsetAsync(a->W16, 0, w16_bytes(a), c->stream));
     FM_CUDA(cudaMalloc(&a->d_scalars, kReportRing * 2 * sizeof(double)));
     FM_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&a->h_scalars), kReportRing * 2 * sizeof(double), 0));
     FM_CUDA(cudaMalloc(&a->d_upd, sizeof(double)));
@@ -738,9 +691,8 @@ int fm_agent_set_weights(fm_agent* a, const double* W) {
     if (int st = set_dev(c)) return st;
     FM_CUDA(cudaMemcpyAsync(a->W, W, a->P * 8, cudaMemcpyHostToDevice, c->stream));
     if (a->W16) {
-        FM_CUDA(launch_to_bf16(a->W, a->W16, a->P, c->num_sms, c->stream));
+        FM_CUDA(launch_w16t(a->W, a->V, a->D, a->W16, w16_ld(a), c->num_sms, c->stream));
         count_launch();
-        ++a->w16_gen;
     }
     FM_CUDA(cudaStreamSynchronize(c->stream));
     return FM_OK;
@@ -791,41 +743,12 @@ int fm_debug_gemm(fm_ctx* c, const void* A, const void* B, int a_mn, int b_mn, i
     FM_GUARD_BEGIN
     if (!c || !A || !B || !C || M <= 0 || N <= 0 || K <= 0 || M % 8 || N % 8 || K % 8)
         return fail(FM_ERR_INVALID_ARG, "debug_gemm: bad arguments");
-    if (!gemm_pair_mode()) return fail(FM_ERR_CONFIG_ERROR, "debug_gemm needs the CTA-pair kernels");
     if (int st = set_dev(c)) return st;
     CUtensorMap tA, tB;
-    const bool ok = (a_mn ? make_tmap_bf16_kmajor(&tA, A, K, M, 64) : make_tmap_bf16_kmajor(&tA, A, M, K, kGemmBM)) &&
-                    (b_mn ? make_tmap_bf16_kmajor(&tB, B, K, N, 64)
-                          : make_tmap_bf16_kmajor(&tB, B, N, K, gemm_b_box_rows()));
+    const bool ok = (a_mn ? make_tmap_bf16_kmajor(&tA, A, K, M, 64) : make_tmap_bf16_kmajor(&tA, A, M, K, 128)) &&
+                    (b_mn ? make_tmap_bf16_kmajor(&tB, B, K, N, 64) : make_tmap_bf16_kmajor(&tB, B, N, K, 128));
     if (!ok) return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     FM_CUDA(gemm_debug_launch(tA, tB, a_mn, b_mn, M, N, K, C, c->num_sms, c->stream));
-    FM_CUDA(cudaStreamSynchronize(c->stream));
-    return FM_OK;
-    FM_GUARD_END
-}
-
-int fm_debug_gemm_klist(fm_ctx* c, const void* A, const void* B, const int32_t* klist, long long klist_ld,
-                        const int32_t* klist_iters, int rows, int M, int N, float* C) {
-    FM_GUARD_BEGIN
-    if (!c || !A || !B || !C || !klist || !klist_iters || M <= 0 || N <= 0 || rows <= 0 || M % 8 || N % 8 ||
-        klist_ld % 64)
-        return fail(FM_ERR_INVALID_ARG, "debug_gemm_klist: bad arguments");
-    if (!gemm_pair_mode()) return fail(FM_ERR_CONFIG_ERROR, "debug_gemm_klist needs the CTA-pair kernels");
-    if (int st = set_dev(c)) return st;
-    CUtensorMap tA, tB;
-    if (!make_tmap_gather4(&tA, A, rows, M, M) || !make_tmap_gather4(&tB, B, rows, N, N))
-        return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    GemmArgs g{};
-    g.M = M;
-    g.N = N;
-    g.K = 64;
-    g.group_m = 1;
-    g.out = C;
-    g.ld_out = N;
-    g.klist = klist;
-    g.klist_ld = klist_ld;
-    g.klist_iters = klist_iters;
-    FM_CUDA(gemm_klist_launch(tA, tB, g, c->num_sms, c->stream));
     FM_CUDA(cudaStreamSynchronize(c->stream));
     return FM_OK;
     FM_GUARD_END
@@ -886,17 +809,32 @@ int fm_agent_is_active(const fm_agent* a) { return a->active ? 1 : 0; }
 
 int fm_agent_set_clip(fm_agent* a, float clip_eps, const float* old_logp, int64_t n_rows) {
     if (int st = check_active(a)) return st;
-    fm_ctx* c = a->ctx;
-    if (int st = set_dev(c)) return st;
+    if (n_rows < 0 || (n_rows > 0 && !old_logp)) return fail(FM_ERR_INVALID_ARG, "bad old log-prob array");
     a->clip_eps = clip_eps;
-    a->have_old_logp = false;
-    if (old_logp && clip_eps > 0.f) {
-        if (int st = ws_reserve_rows(c, static_cast<int64_t>(round_up(n_rows, 128)))) return st;
-        FM_CUDA(cudaMemcpyAsync(c->ws.old_logp, old_logp, n_rows * 4, cudaMemcpyHostToDevice, c->stream));
-        FM_CUDA(cudaStreamSynchronize(c->stream));
-        a->have_old_logp = true;
-    }
+    a->old_logp.clear();
+    if (old_logp && clip_eps > 0.f) a->old_logp.assign(old_logp, old_logp + n_rows);  // uploaded by train_impl
     return FM_OK;
+}
+
+// DuplicateSample guard (training.hpp:396-401): the step's GradKey set.  All
+// keys are checked (against the set and each other) before any is inserted.
+int fm_agent_add_grad_keys(fm_agent* a, const fm_sample_key* keys, int n) {
+    FM_GUARD_BEGIN
+    if (n < 0 || (n > 0 && !keys)) return fail(FM_ERR_INVALID_ARG, "bad key list");
+    std::vector<std::tuple<std::string, int, int, int64_t>> add;
+    add.reserve(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+        auto k = std::make_tuple(std::string(keys[i].input_id ? keys[i].input_id : ""), keys[i].turns, keys[i].traj,
+                                 keys[i].version);
+        if (a->grad_keys.count(k) || std::find(add.begin(), add.end(), k) != add.end())
+            return fail(FM_ERR_DUPLICATE_SAMPLE, "gradient already cached for " + std::get<0>(k) + "/" +
+                                                     std::to_string(std::get<1>(k)) + "/" +
+                                                     std::to_string(std::get<2>(k)));
+        add.push_back(std::move(k));
+    }
+    for (auto& k : add) a->grad_keys.insert(std::move(k));
+    return FM_OK;
+    FM_GUARD_END
 }
 
 int fm_agent_set_shard(fm_agent* a, int rank, int nranks) {
@@ -922,9 +860,13 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
     Workspace& w = c->ws;
     cudaStream_t s = c->stream;
     const bool tc = a->precision == FM_PRECISION_BF16_TC;
+    const bool clip = !a->old_logp.empty() && a->clip_eps > 0.f;
+    if (clip && static_cast<int64_t>(a->old_logp.size()) != M_total)
+        return fail(FM_ERR_INVALID_ARG, "old log-probs given for " + std::to_string(a->old_logp.size()) +
+                                            " rows, the micro-batch has " + std::to_string(M_total));
     const int64_t Mpad = tc ? static_cast<int64_t>(round_up(static_cast<uint64_t>(M), 128)) : M;
     if (tc) {
-        if (int st = ws_reserve_tc(c, std::max<int64_t>(Mpad, 128), a->V, a->D)) return st;
+        if (int st = ws_reserve_tc(c, std::max<int64_t>(Mpad, 128), a->V, a->D, n)) return st;
     } else {
         if (int st = ws_reserve_parity(c, M, a->V, a->P)) return st;
     }
@@ -942,6 +884,21 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
         FM_CUDA(cudaMemcpyAsync(w.sd, stg, sizeof(SampleDesc) * n, cudaMemcpyHostToDevice, s));
         FM_CUDA(cudaEventRecord(sev, s));
     }
+    if (clip) {  // after the workspace reserve (which may reallocate)
+        if (w.old_logp_cap < M_total) {
+            FM_CUDA(cudaStreamSynchronize(s));
+            cudaFree(w.old_logp);
+            w.old_logp = nullptr;
+            if (dalloc(&w.old_logp, static_cast<size_t>(M_total))) return fail(FM_ERR_DEVICE_OOM, "old log-probs");
+            w.old_logp_cap = M_total;
+        }
+        uint8_t* stg;
+        cudaEvent_t sev;
+        if (int st = staging_acquire(c, M_total * 4, &stg, &sev)) return st;
+        std::memcpy(stg, a->old_logp.data(), M_total * 4);
+        FM_CUDA(cudaMemcpyAsync(w.old_logp, stg, M_total * 4, cudaMemcpyHostToDevice, s));
+        FM_CUDA(cudaEventRecord(sev, s));
+    }
 
     const int64_t ticket = a->next_ticket++;
     const int slot = static_cast<int>(ticket % kReportRing);
@@ -953,184 +910,69 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
     if (M > 0) {
         if (tc) {
             const uint64_t ldz = round_up(a->V, 8);
-            const bool reuse = w.phi_valid && w.phi_Mpad == Mpad && w.phi_D == a->D;
-            if (!reuse) {
-                KScope k(c, K_MEMSET, s);
-                FM_CUDA(cudaMemsetAsync(w.phic, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
-                FM_CUDA(cudaMemsetAsync(w.phict, 0, static_cast<size_t>(Mpad) * a->D * 2, s));
-            }
-            const bool fold = loss_fold_enabled();
-            // K-list GEMM2 (opt-in FM_G2_KLIST=1): each 256-feature column block of the
-            // weight gradient sums only over the tokens whose context touches it
-            // GEMM2 over token-slot segments (default; FM_G2_KLIST=0 dense, 1 gather4 lists):
-            // each 256-feature column block of dW sums only the tokens whose context touches
-            // it — GEMM1 writes each token's p~ row into one slot per feature block it
-            // touches and GEMM2 tile-loads contiguous segments.  Falls back to the dense
-            // GEMM2 when the segment workspace does not fit.
-            const char* kl_env = std::getenv("FM_G2_KLIST");
-            const char kl_mode = kl_env && kl_env[0] ? kl_env[0] : '2';
-            const bool klist = fold && gemm_pair_mode() && kl_mode == '1';
-            bool kseg = fold && gemm_pair_mode() && (kl_mode == '2' || kl_mode == '3');
-            // mode 3: A rows gathered from the row-major p~ by producer warps (no A' copies)
-            const bool swa = kseg && kl_mode == '3';
-            if (kseg && ws_reserve_seg(c, !swa) != FM_OK) {
-                kseg = false;
-                clear_error();
-                cudaGetLastError();
-            }
-            c->last_kseg = kseg;
-            if (fold && a->cm_gen != a->w16_gen) {
-                // per-feature max of the shadow, when K-adam did not produce it (first step,
-                // set_weights, DP-gang sharded update, host-tier swap-in)
-                KScope k(c, K_COLMAX, s);
-                FM_CUDA(launch_colmax(a->W16, static_cast<int64_t>(a->V), static_cast<int64_t>(a->D), a->colmax,
-                                      c->num_sms, s));
-                a->cm_gen = a->w16_gen;
-                count_launch();
-            }
+            const int64_t Qcap = Mpad + 3 * static_cast<int64_t>(n);
+            const int nblk = static_cast<int>((a->D + 255) / 256);
             {
+                // K-gather (rows, q0) + K-pos (position features) + K-pslot (segment slots,
+                // one-hot B')
                 KScope k(c, K_GATHER, s);
-                FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, Mpad, G, a->D, rows, w.phic, w.phict,
-                                      reuse ? 1 : 0, fold ? a->colmax : nullptr, s));
+                FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, Mpad, G, a->D, rows, s));
+                FM_CUDA(launch_positions(c->arena, w.sd, n, row_lo, M, a->D, w.pos_feat, Qcap, s));
+                FM_CUDA(launch_pslots(w.pos_feat, Qcap, nblk, w.kcount, w.kseg_off, w.kiters, w.pos_slot, w.bseg,
+                                      w.kp_cap, w.kseg_rows, s));
+                count_launch(4);
             }
-            w.phi_valid = true;
-            w.phi_Mpad = Mpad;
-            w.phi_D = a->D;
-            const int nblk = static_cast<int>((a->D + kGemmBN - 1) / kGemmBN);
-            if (klist) {
-                KScope k(c, K_GATHER, s);
-                FM_CUDA(launch_klist(rows.feat4, M, nblk, w.klist, w.klist_ld, w.kiters,
-                                     static_cast<int32_t>(w.rows_cap), s));
-                count_launch();
-            }
-            if (kseg) {
-                KScope k(c, K_GATHER, s);
-                FM_CUDA(cudaMemsetAsync(w.bseg, 0, static_cast<size_t>(w.kp_cap) * 256 * 2, s));
-                FM_CUDA(launch_kslots(rows.feat4, rows.cnt4, M, nblk, w.kcount, w.kseg_off, w.kiters, w.slot4,
-                                      swa ? nullptr : w.aseg, static_cast<int64_t>(ldz), static_cast<int64_t>(ldz),
-                                      w.bseg, w.kseg_rows, swa ? w.seg_tok : nullptr,
-                                      static_cast<int32_t>(w.rows_cap), s));
-                count_launch(2);
-            }
-            // K-GEMM1: z = Phic * W16^T / n; epilogue stores p~ = exp(z - m) (bf16) with m the
-            // row's bound (fold: transposed, GEMM2's A operand) or the tile max (K-loss path),
-            // the (m, sum p~) softmax partials and the taken token's logit
-            CUtensorMap tA, tB, tP, tGt, tPt;
-            if (!make_tmap_bf16_kmajor(&tA, w.phic, Mpad, a->D, kGemmBM) ||
-                !make_tmap_bf16_kmajor(&tB, a->W16, a->V, a->D, gemm_b_box_rows()) ||
-                !make_tmap_2d(&tP, w.Pexp, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Mpad, ldz, 64, 128) ||
-                !make_tmap_bf16_kmajor(&tGt, w.gt, a->V, Mpad, kGemmBM) ||
-                !make_tmap_bf16_kmajor(&tPt, w.phict, a->D, Mpad, gemm_b_box_rows()))
-                return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-            const int tiles_n = static_cast<int>((a->V + kGemmBN - 1) / kGemmBN);
-            // short-K GEMM1 (D <= 4,096: 64 K iterations per tile) is epilogue-bound, so its
-            // tiles are drained by 8 warps, two per row (column halves, one softmax partial
-            // each): C2 GEMM1 3.2 -> 2.9 ms; with longer K (C3/C5) 4 warps measured 5-7%
-            // fewer cycles (FM_G1_EPI_WARPS=4/8 overrides)
-            const int epi_w = env_int("FM_G1_EPI_WARPS", a->D <= 4096 ? 8 : 4);
-            const bool wide = gemm_pair_mode() && epi_w == 8;
-            const int parts = wide ? 2 : 1;
-            const int stats_ld = tiles_n * parts;
-            GemmArgs g1{};
-            g1.M = static_cast<int>(M);
-            g1.N = static_cast<int>(a->V);
-            g1.K = static_cast<int>(a->D);
-            g1.group_m = env_int("FM_G1_GROUP_M", 16);  // raster: m-tiles per group (L2 reuse)
-            if (kseg && !swa) {  // p~ rows into the token's segment slots (A')
-                g1.mrow = w.mrow;
-                g1.aseg = w.aseg;
-                g1.slot4 = w.slot4;
-                g1.dbg_nostore = std::getenv("FM_DBG_G1_NOSTORE") ? 1 : 0;
-            } else if (klist || swa) {  // p~ row-major: the K-list GEMM2 gathers token rows
-                g1.mrow = w.mrow;
-                g1.pexp = w.Pexp;
-            } else if (fold) {  // p~^T straight into GEMM2's A operand buffer
-                g1.mrow = w.mrow;
-                g1.pexp_t = w.gt;
-                g1.ldt = static_cast<long long>(Mpad);
-                g1.store_rows = static_cast<int>(Mpad);
-            } else {
-                g1.pexp = w.Pexp;
-            }
-            g1.zact = w.zact;
-            g1.action = w.action;
-            g1.ld_out = static_cast<long long>(ldz);
-            g1.row_scale = w.rscale;
-            g1.stats = w.stats;
-            g1.stats_ld = stats_ld;
-            g1.epi_wide = wide ? 1 : 0;
-            // K-lse fused into GEMM1's tail (loss fold, CTA-pair kernel; FM_LSE_FUSED=0
-            // launches it separately): after a grid-wide arrival the epilogue warps
-            // normalise the rows.  Same time as the 14 us launch it replaces (C2: GEMM1
-            // +7-29 us, K-lse -14 us); one launch fewer per micro-batch.  (A per-tile
-            // last-finisher variant cost GEMM1 12-15%: DESIGN.md §9.)
-            const char* lse_env = std::getenv("FM_LSE_FUSED");
-            const bool lse_fused = fold && gemm_pair_mode() && !(lse_env && lse_env[0] == '0');
-            LseArgs lse_args{w.zact, w.stats, stats_ld, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
-                             a->have_old_logp ? w.old_logp : nullptr, a->clip_eps, scal + 1,
-                             fold ? 1 : 0, fold ? w.gt : nullptr, w.phict, Mpad};
-            if (klist) {
-                lse_args.pexp_t = w.Pexp;
-                lse_args.ldt = static_cast<int64_t>(ldz);
-                lse_args.phict = w.phic;
-                lse_args.rowmajor = 1;
-                lse_args.ld_phi = static_cast<int64_t>(a->D);
-            }
-            if (kseg) {
-                lse_args.pexp_t = swa ? w.Pexp : w.aseg;
-                lse_args.ldt = static_cast<int64_t>(ldz);
-                lse_args.rowmajor = swa ? 3 : 2;
-                lse_args.slot4 = w.slot4;
-                lse_args.bseg = w.bseg;
-            }
-            if (lse_fused) {
-                g1.lse = lse_args;
-                g1.lse_sync = w.lse_sync;
-                g1.lse_epoch = ++w.lse_epoch;
-            }
+            BandArgs ba{};
+            ba.w16t = a->W16;
+            ba.ldw = static_cast<int64_t>(w16_ld(a));
+            ba.zero_row = w.zero_row;
+            ba.V = static_cast<int64_t>(a->V);
+            ba.pos_feat = w.pos_feat;
+            ba.q0 = w.q0;
+            ba.action = w.action;
+            ba.rscale = w.rscale;
+            ba.M = M;
+            ba.stats = w.stats;
+            ba.stats_ld = static_cast<int>((a->V + 255) / 256);
+            ba.zact = w.zact;
+            ba.lse = w.lse;
+            ba.coef_eff = w.coef_eff;
+            ba.pos_slot = w.pos_slot;
+            ba.aseg = w.aseg;
+            ba.ld_a = static_cast<int64_t>(ldz);
             FM_CUDA(cudaEventRecord(c->ev_gemm, s));  // swap copies may start here (fm_agent_suspend)
             c->gemm_seq = ++c->op_seq;
             {
-                KScope k(c, K_GEMM1, s);
-                FM_CUDA(gemm_tn_launch(GemmKind::Logits, tA, tB, g1, c->num_sms, s));
+                // K-stats: per-(row, 256-column tile) softmax partials + the taken token's logit
+                KScope k(c, K_STATS, s);
+                FM_CUDA(launch_band(ba, false, s));
             }
-            // K-lse (standalone unless fused into GEMM1's epilogue)
-            if (!lse_fused) {
+            {
                 KScope k(c, K_LSE, s);
-                FM_CUDA(launch_lse(lse_args, s));
+                LseArgs L{w.zact, w.stats, ba.stats_ld, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
+                          clip ? w.old_logp : nullptr, row_lo, a->clip_eps, scal + 1};
+                FM_CUDA(launch_lse(L, s));
             }
-            // K-softmax-grad: G^T tiles (zero for padding rows) — folded into GEMM2's operands
-            if (!fold) {
-                KScope k(c, K_SOFTMAX_GRAD, s);
-                FM_CUDA(launch_softmax_grad(tP, tGt, w.stats, stats_ld, Mpad, static_cast<int64_t>(a->V), rows, s,
-                                            kGemmBN / parts));
+            {
+                // K-band: per-position gradient rows H into the feature blocks' A' segments
+                KScope k(c, K_BAND, s);
+                FM_CUDA(launch_band(ba, true, s));
             }
-            // K-GEMM2: dW (+)= G^T * Phic ; first contribution of the step overwrites
-            // (fold: A = p~'^T, B = Phic^T scaled per row by K-lse — the same product)
+            // K-GEMM2: dW[v][f] (+)= sum over block(f)'s positions of H[q][v] * onehot[q][f];
+            // the first contribution of the step overwrites
             GemmArgs g2{};
             g2.M = static_cast<int>(a->V);
             g2.N = static_cast<int>(a->D);
-            g2.K = static_cast<int>(Mpad);
-            // raster: when B = Phic^T (D x Mpad bf16) is about L2-sized (C2: 134 MB) run all
-            // D/256 column tiles of a vocab row block together (group 1) so p~^T is read
-            // from DRAM once (ncu: 6.6 vs 7.0 GB, 2.22 vs 2.26 ms; profiles/r01_g2_sweep.jsonl);
-            // a larger B (C3/C5: 1.07 GB) would be re-read per row block, so group 8 there
-            const double b_bytes = 2.0 * static_cast<double>(a->D) * static_cast<double>(Mpad);
-            g2.group_m = env_int("FM_G2_GROUP_M", b_bytes <= 160e6 ? 1 : 8);
+            g2.K = 0;
+            // raster: the 256-feature column tiles of a vocab row block run together, so the
+            // row block's dW stripe and A' columns stay L2-local
+            g2.group_m = env_int("FM_G2_GROUP_M", 1);
             g2.out = static_cast<float*>(a->dW);
             g2.ld_out = static_cast<long long>(a->D);
             g2.accumulate = a->dw_valid ? 1 : 0;
             g2.sumsq = scal;
-            {
-                // stream-K tail (opt-in FM_G2_STREAMK=1): C2's 2,000 tiles on 74 pairs leave a
-                // last wave of 2 tiles; split the last 76 tiles' K ranges evenly instead.
-                // Measured within noise of the plain schedule at C2 (2.676 vs 2.670 ms).
-                const char* sk_env = std::getenv("FM_G2_STREAMK");
-                if (gemm_pair_mode() && c->num_sms / 2 <= kSkMaxTiles / 2 && sk_env && sk_env[0] == '1') {
-                    g2.sk_ws = w.sk_ws;
-                    g2.sk_cnt = w.sk_cnt;
-                }
-            }
+            g2.kseg_off = w.kseg_off;
+            g2.kseg_iters = w.kiters;
             const bool exchange = a->gang && a->gang->connected && a->samples + n == G;
             if (exchange) {  // last micro-batch of the step: reduce-scatter inside the epilogue
                 GangState* gs = a->gang;
@@ -1140,69 +982,20 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 for (int o = 0; o < gs->g; ++o) g2.xpeer[o] = gs->peer_slot[o];
             }
             {
-                // Long K (rows of the micro-batch): optionally launch K-chunks of FM_G2_KCHUNK
-                // rows in sequence, each accumulating into dW, so concurrent tiles stay within
-                // one chunk's operands (L2 reuse).  Off by default: at C5 N=1 (K = 65,536) the
-                // A/B on one box was within noise (profiles/r01_kchunk.jsonl).  When chunked
-                // the micro-batch grad norm spans several accumulations and reads NaN.
-                const int kc_env = env_int("FM_G2_KCHUNK", 1 << 30);  // default: one launch
-                const int kc = static_cast<int>(round_up(static_cast<uint64_t>(std::min(kc_env, 1 << 30)), 64));
-                const int nch = (static_cast<int>(Mpad) + kc - 1) / kc;
                 KScope k(c, K_GEMM2, s);
-                if (swa) {
-                    CUtensorMap tSB;
-                    if (!make_tmap_bf16_kmajor(&tSB, w.bseg, static_cast<uint64_t>(w.kp_cap), 256, 64))
-                        return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-                    g2.kseg_off = w.kseg_off;
-                    g2.klist_iters = w.kiters;
-                    g2.seg_tok = w.seg_tok;
-                    g2.pexp = w.Pexp;
-                    g2.ld_pexp = static_cast<long long>(ldz);
-                    g2.sk_ws = nullptr;
-                    FM_CUDA(gemm_kseg_swa_launch(tSB, g2, c->num_sms, s));
-                } else if (kseg) {
-                    CUtensorMap tSA, tSB;
-                    if (!make_tmap_bf16_kmajor(&tSA, w.aseg, static_cast<uint64_t>(w.kp_cap), a->V, 64, ldz) ||
-                        !make_tmap_bf16_kmajor(&tSB, w.bseg, static_cast<uint64_t>(w.kp_cap), 256, 64))
-                        return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-                    g2.kseg_off = w.kseg_off;
-                    g2.klist_iters = w.kiters;
-                    g2.sk_ws = nullptr;
-                    FM_CUDA(gemm_kseg_launch(tSA, tSB, g2, c->num_sms, s));
-                } else if (klist) {
-                    CUtensorMap tKA, tKB;
-                    if (!make_tmap_gather4(&tKA, w.Pexp, static_cast<uint64_t>(w.rows_cap) + 1, a->V, ldz) ||
-                        !make_tmap_gather4(&tKB, w.phic, static_cast<uint64_t>(w.rows_cap) + 1, a->D, a->D))
-                        return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-                    g2.klist = w.klist;
-                    g2.klist_ld = w.klist_ld;
-                    g2.klist_iters = w.kiters;
-                    g2.sk_ws = nullptr;
-                    FM_CUDA(gemm_klist_launch(tKA, tKB, g2, c->num_sms, s));
-                } else if (nch == 1) {
-                    FM_CUDA(gemm_tn_launch(GemmKind::Grad, tGt, tPt, g2, c->num_sms, s));
-                } else {
-                    FM_CUDA(cudaMemsetAsync(scal, 0xFF, sizeof(double), s));  // NaN grad norm
-                    for (int ch = 0; ch < nch; ++ch) {
-                        GemmArgs gc = g2;
-                        gc.k0 = ch * kc;
-                        gc.K = std::min(kc, static_cast<int>(Mpad) - gc.k0);
-                        gc.accumulate = (a->dw_valid || ch > 0) ? 1 : 0;
-                        gc.sumsq = nullptr;
-                        if (ch + 1 < nch) gc.xg = 0;  // the gang exchange rides on the last chunk
-                        FM_CUDA(gemm_tn_launch(GemmKind::Grad, tGt, tPt, gc, c->num_sms, s));
-                    }
-                    count_launch(nch - 1);
-                }
+                CUtensorMap tSA, tSB;
+                if (!make_tmap_bf16_kmajor(&tSA, w.aseg, static_cast<uint64_t>(w.kp_cap), a->V, 64, ldz) ||
+                    !make_tmap_bf16_kmajor(&tSB, w.bseg, static_cast<uint64_t>(w.kp_cap), 256, 64))
+                    return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+                FM_CUDA(gemm_kseg_launch(tSA, tSB, g2, c->num_sms, s));
             }
             if (exchange) {
                 a->dw_valid = true;
                 if (int st = gang_barrier(a)) return st;  // every rank's partials have landed
             }
-            count_launch(fold ? (lse_fused ? 3 : 4) : 5);
+            count_launch(4);
         } else {
-            w.phi_valid = false;  // the row buffers no longer describe Phic's contents
-            FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, M, G, a->D, rows, nullptr, nullptr, 0, nullptr, s));
+            FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, M, G, a->D, rows, s));
             if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * 8, s));
             KScope k(c, K_PARITY, s);
             FM_CUDA(launch_parity_rows(a->W, a->V, a->D, M, rows, w.sd, G, w.zscratch, w.dWmb, w.logp64,
@@ -1218,16 +1011,16 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
         if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * 4, s));
         for (int o = 0; o < gs->g; ++o) {
             if (o == gs->rank) continue;
-            const size_t rows = static_cast<size_t>(gs->lo[o + 1] - gs->lo[o]);
+            const size_t rows_o = static_cast<size_t>(gs->lo[o + 1] - gs->lo[o]);
             FM_CUDA(cudaMemcpyAsync(gs->peer_slot[o], static_cast<float*>(a->dW) + gs->lo[o] * a->D,
-                                    rows * a->D * 4, cudaMemcpyDeviceToDevice, s));
+                                    rows_o * a->D * 4, cudaMemcpyDeviceToDevice, s));
         }
         a->dw_valid = true;
         if (int st = gang_barrier(a)) return st;
     }
-    a->have_old_logp = false;  // old log-probs apply to one micro-batch
+    a->old_logp.clear();  // old log-probs apply to one micro-batch
     a->last_rows = M;
-    a->last_seq = ++c->op_seq;  // its own GEMM1 mark precedes this micro-batch's GEMM2
+    a->last_seq = ++c->op_seq;  // its own K-stats mark precedes this micro-batch's GEMM2
     FM_CUDA(cudaMemcpyAsync(a->h_scalars + 2 * slot, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     FM_CUDA(cudaEventRecord(a->ev[slot], s));
     a->rep_tokens[slot] = M;
@@ -1344,23 +1137,6 @@ int fm_debug_read_rows(fm_ctx* c, int64_t n, int32_t* action, int32_t* ctx4, int
     return FM_OK;
 }
 
-int fm_agent_debug_colmax(fm_agent* a, float* out, int* valid) {
-    FM_GUARD_BEGIN
-    if (int st = check_active(a)) return st;
-    if (!a->colmax) return fail(FM_ERR_CONFIG_ERROR, "no bf16 shadow (parity precision)");
-    if (int st = set_dev(a->ctx)) return st;
-    FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
-    std::vector<int> keys(a->D);
-    FM_CUDA(cudaMemcpy(keys.data(), a->colmax, a->D * 4, cudaMemcpyDeviceToHost));
-    for (uint64_t d = 0; d < a->D; ++d) {
-        const int k = keys[d] >= 0 ? keys[d] : keys[d] ^ 0x7fffffff;
-        std::memcpy(out + d, &k, 4);
-    }
-    if (valid) *valid = a->cm_gen == a->w16_gen ? 1 : 0;
-    return FM_OK;
-    FM_GUARD_END
-}
-
 int fm_agent_sync(fm_agent* a) {
     if (!a->ctx) return FM_OK;
     if (int st = set_dev(a->ctx)) return st;
@@ -1385,7 +1161,7 @@ int fm_agent_poll_report(fm_agent* a, int64_t ticket, fm_report* out) {
 
 
 // apply_global_update; with park != 0 (device tier, tensor-core agent, no gang)
-// K-adam writes the new W / m / v / W16 / colmax straight into the agent's
+// K-adam writes the new W / m / v / W16^T straight into the agent's
 // parking buffer and the agent is suspended — the swap-out fused into the
 // optimizer (no copy-out pass).
 static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, double b2, double eps,
@@ -1413,56 +1189,42 @@ static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, doubl
     const double bc1 = 1.0 - std::pow(b1, static_cast<double>(a->step));  // training.hpp:42-43
     const double bc2 = 1.0 - std::pow(b2, static_cast<double>(a->step));
     FM_CUDA(cudaMemsetAsync(a->d_upd, 0, sizeof(double), s));
-    bool cm_fused = false;
     KScope ks(c, K_ADAM, s);
+    const ShardPeers none{};
     if (a->precision == FM_PRECISION_PARITY_F64) {
-        FM_CUDA(launch_adam<double>(a->W, a->m, a->v, static_cast<double*>(a->dW), nullptr, a->P, lr, b1, b2, eps,
-                                    bc1, bc2, 1, a->d_upd, c->num_sms, s));
+        FM_CUDA(launch_adam<double>(a->W, a->m, a->v, static_cast<double*>(a->dW), a->V, a->D, 0, a->V, nullptr, 0,
+                                    nullptr, 0, none, lr, b1, b2, eps, bc1, bc2, 1, a->d_upd, c->num_sms, s));
     } else if (a->gang && a->gang->connected) {
-        // sharded Adam over this rank's rows; W16 rows all-gathered by peer stores
+        // sharded Adam over this rank's rows (gradient = local partial + the peers'
+        // receive slots); the new W16^T columns of those rows go to every replica
         GangState* gs = a->gang;
-        const int64_t r0 = gs->lo[gs->rank], r1 = gs->lo[gs->rank + 1];
-        const uint64_t off = static_cast<uint64_t>(r0) * a->D, n_own = static_cast<uint64_t>(r1 - r0) * a->D;
+        const uint64_t r0 = static_cast<uint64_t>(gs->lo[gs->rank]), r1 = static_cast<uint64_t>(gs->lo[gs->rank + 1]);
         ShardPeers peers{};
         for (int o = 0; o < gs->g; ++o)
-            if (o != gs->rank) peers.w16[peers.n++] = gs->peer_w16[o] + off;
-        FM_CUDA(launch_adam_shard(a->W + off, a->m + off, a->v + off, static_cast<float*>(a->dW) + off, gs->recv,
-                                  gs->g - 1, n_own, a->W16 + off, peers, n_own, lr, b1, b2, eps, bc1, bc2, a->d_upd,
-                                  c->num_sms, s, loss_fold_enabled() ? a->colmax : nullptr, a->D, &cm_fused));
-        // global grad norm^2; doubles as the barrier after the peers' W16 writes
+            if (o != gs->rank) peers.w16t[peers.n++] = gs->peer_w16[o];
+        FM_CUDA(launch_adam<float>(a->W, a->m, a->v, static_cast<float*>(a->dW), a->V, a->D, r0, r1, gs->recv,
+                                   gs->g - 1, a->W16, w16_ld(a), peers, lr, b1, b2, eps, bc1, bc2, 0, a->d_upd,
+                                   c->num_sms, s));
+        // global grad norm^2; doubles as the barrier after the peers' W16^T writes
         FM_NCCL(ncclAllReduce(a->d_upd, a->d_upd, 1, ncclFloat64, ncclSum, gang_comm(gs), s));
-        // the shards' partial column maxima of the new shadow -> the loss-fold bound.  Every
-        // rank takes part in the all-reduce (a rank whose shard could not fuse the partial
-        // max computes it over its rows first), so the collective sequence never diverges.
-        if (loss_fold_enabled()) {
-            if (!cm_fused && r1 > r0)
-                FM_CUDA(launch_colmax(a->W16 + off, r1 - r0, static_cast<int64_t>(a->D), a->colmax, c->num_sms, s));
-            else if (!cm_fused)  // no rows here: the neutral key (below any finite value)
-                FM_CUDA(cudaMemsetAsync(a->colmax, 0x80, a->D * sizeof(int), s));
-            FM_NCCL(ncclAllReduce(a->colmax, a->colmax, a->D, ncclInt32, ncclMax, gang_comm(gs), s));
-            cm_fused = true;
-        }
     } else {
-        // the next step's first GEMM2 overwrites dW, so no zeroing pass here; the new
-        // shadow's column maxima (loss-fold bound) come out of the same pass
+        // the next step's first GEMM2 overwrites dW, so no zeroing pass here; with park the
+        // new state goes straight into the parking buffer
         const size_t dwe = dw_elem(a);
         __nv_bfloat16* w16_out = park ? reinterpret_cast<__nv_bfloat16*>(pk + a->P * (16 + dwe)) : a->W16;
-        int* cm_out = park ? reinterpret_cast<int*>(pk + a->P * (18 + dwe)) : a->colmax;
-        FM_CUDA(launch_adam<float>(a->W, a->m, a->v, static_cast<float*>(a->dW), w16_out, a->P, lr, b1, b2, eps,
-                                   bc1, bc2, 0, a->d_upd, c->num_sms, s, loss_fold_enabled() ? cm_out : nullptr,
-                                   a->D, &cm_fused, park ? &dst : nullptr));
+        FM_CUDA(launch_adam<float>(a->W, a->m, a->v, static_cast<float*>(a->dW), a->V, a->D, 0, a->V, nullptr, 0,
+                                   w16_out, w16_ld(a), none, lr, b1, b2, eps, bc1, bc2, 0, a->d_upd, c->num_sms, s,
+                                   park ? &dst : nullptr));
     }
     count_launch();
     a->dw_valid = false;
     a->samples = 0;
     a->version += 1;
-    ++a->w16_gen;
-    if (cm_fused) a->cm_gen = a->w16_gen;
+    a->grad_keys.clear();
     FM_CUDA(cudaMemcpyAsync(a->h_upd, a->d_upd, sizeof(double), cudaMemcpyDeviceToHost, s));
     if (park) {
         // the parked state is complete when K-adam is: release the slot behind it
         a->park_w16 = true;
-        a->cm_parked = cm_fused;
         FM_CUDA(cudaEventRecord(a->ev_out, s));
         agent_free_device(a, s);
         a->active = false;

@@ -18,7 +18,9 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
 #include <string>
+#include <tuple>
 #include <unordered_map>
 #include <vector>
 
@@ -66,48 +68,37 @@ struct Workspace {
     uint64_t vocab_cap = 0, feat_cap = 0;
     int32_t* action = nullptr;
     int4* ctx4 = nullptr;
-    int4* feat4 = nullptr;
-    uint32_t* cnt4 = nullptr;
     int32_t* n_ctx = nullptr;
     int32_t* sample = nullptr;
     float *coef = nullptr, *rscale = nullptr, *lse = nullptr, *logp = nullptr, *coef_eff = nullptr;
     float* old_logp = nullptr;
-    __nv_bfloat16 *phic = nullptr, *phict = nullptr, *gt = nullptr;
-    __nv_bfloat16* Pexp = nullptr;  // p~ = exp(z - m_tile) [Mpad][ldz] bf16
-    float* zact = nullptr;          // logit of the taken token [Mpad]
-    float2* stats = nullptr;
-    float* mrow = nullptr;  // loss fold: per-row softmax offset bound [Mpad]
-    unsigned* lse_sync = nullptr;  // fused K-lse: {CTAs arrived, epoch published} (GEMM1 tail)
-    unsigned lse_epoch = 0;
-    // segmented K-list GEMM2 (FM_G2_KLIST=2), allocated on first use
-    __nv_bfloat16 *aseg = nullptr, *bseg = nullptr;  // A' [kp_cap][ldz], B' [kp_cap][256]
-    int4* slot4 = nullptr;                            // [rows_cap]
-    int32_t *kcount = nullptr, *kseg_off = nullptr;   // [nblk][row chunks of 1024], [nblk]
-    unsigned long long* kseg_rows = nullptr;          // executed GEMM2 K rows, accumulated
-    int32_t* seg_tok = nullptr;                       // [kp_cap] token of each slot (mode 3)
-    bool seg_has_a = false;                           // A' allocated (mode 2)
+    int64_t old_logp_cap = 0;
+    // band formulation (k_band.cu): per row its first context position, per
+    // position its feature and its A'/B' slot
+    int32_t* q0 = nullptr;
+    int32_t *pos_feat = nullptr, *pos_slot = nullptr;
+    int64_t pos_cap = 0;
+    float* zact = nullptr;   // logit of the taken token [Mpad]
+    float2* stats = nullptr; // K-stats partials [Mpad][ceil(V/256)]
+    // segments of K-GEMM2: A' = per-position gradient rows H [kp_cap][ldz] bf16,
+    // B' = one-hot [kp_cap][256] bf16
+    __nv_bfloat16 *aseg = nullptr, *bseg = nullptr;
+    __nv_bfloat16* zero_row = nullptr;  // 2,048 zeros: the W16^T "row" of a missing position
+    int32_t *kcount = nullptr, *kseg_off = nullptr, *kiters = nullptr;
+    unsigned long long* kseg_rows = nullptr;  // executed GEMM2 K rows, accumulated
     int64_t kp_cap = 0;
-    int32_t* klist = nullptr;  // K-list GEMM2: token lists per 256-feature block [nblk][klist_ld]
-    int32_t* kiters = nullptr;  // [nblk] list length / 64
-    int64_t klist_ld = 0;
-    float* sk_ws = nullptr;  // GEMM2 stream-K tail: partial tiles [kSkMaxTiles][256][256] (zero between launches)
-    int* sk_cnt = nullptr;   // [kSkMaxTiles][2] arrivals per tile half (self-resetting)
     // parity mode scratch
     int64_t prow_cap = 0;
     uint64_t pvocab_cap = 0, pparam_cap = 0;
     double *zscratch = nullptr, *dWmb = nullptr, *logp64 = nullptr;
     SampleDesc* sd = nullptr;
     int sd_cap = 0;
-    // Phic / Phic^T hold exactly the entries of the rows in the row buffers
-    // (for phi_Mpad, phi_D): the next gather erases them row by row
-    bool phi_valid = false;
-    int64_t phi_Mpad = 0;
-    uint64_t phi_D = 0;
 };
 
 // Per-kernel device timing (bench.py's roofline): event pairs recorded on the
 // launching stream around each hot-path kernel when enabled.
-enum KKind { K_GATHER = 0, K_GEMM1, K_LSE, K_SOFTMAX_GRAD, K_GEMM2, K_ADAM, K_PARITY, K_MEMSET, K_COLMAX, K_NKINDS };
+// gather = K-gather + K-pos + K-pslot; stats = K-stats (pass A); band = K-band (pass B)
+enum KKind { K_GATHER = 0, K_STATS, K_LSE, K_BAND, K_GEMM2, K_ADAM, K_PARITY, K_MEMSET, K_NKINDS };
 struct KTimer {
     bool on = false;
     std::vector<cudaEvent_t> pool;
@@ -126,7 +117,7 @@ struct KTimer {
     }
 };
 
-// One training slot: the device home of an active agent's {W, m, v, dW, W16}.
+// One training slot: the device home of an active agent's {W, m, v, dW, W16^T}.
 // Slots are allocated once and recycled across activate/suspend (the
 // reference's training_slots, config.hpp:89); reuse is ordered on the GPU by
 // the event recorded after the previous tenant's copy-out.
@@ -146,7 +137,7 @@ struct fm_ctx {
     cudaStream_t stream = nullptr;    // compute
     cudaStream_t copy_in = nullptr;   // swap-in (H2D / D2D / P2P)
     cudaStream_t copy_out = nullptr;  // swap-out
-    // the latest K-GEMM1 launch on the compute stream (swap copies start there, see
+    // the latest K-stats launch on the compute stream (swap copies start there, see
     // fm_agent_suspend) and the op sequence numbers that say what it follows
     cudaEvent_t ev_gemm = nullptr;
     std::map<std::string, void*> ipc_cache;  // peer buffers mapped over NVLink (slots, gang receive buffers)
@@ -157,7 +148,6 @@ struct fm_ctx {
     uint64_t arena_cap = 0, arena_used = 0;
     std::unordered_map<uint64_t, uint64_t> arena_ntok;  // offset -> token count
     Workspace ws;
-    bool last_kseg = false;  // the last tensor-core micro-batch ran the segmented GEMM2
     // pinned staging (sample descriptors, host payloads) with reuse events
     uint8_t* staging[kStagingSlots] = {};
     size_t staging_cap[kStagingSlots] = {};
@@ -199,7 +189,7 @@ struct KScope {
 // micro-batch GEMM2 writes the partials of rows owned by another rank into
 // that rank's receive slot over NVLink (IPC-mapped), then each rank runs the
 // sharded Adam on its rows and writes the new bf16 rows into every peer's
-// W16.  Two 1-element NCCL all-reduces on the compute stream serve as the
+// W16^T.  Two 1-element NCCL all-reduces on the compute stream serve as the
 // device-side barriers (after the exchange; the update grad-norm reduction
 // after Adam), so no host round trip or spin-wait is involved.
 #define FM_NCCL(expr)                                                                          \
@@ -233,11 +223,7 @@ struct fm_agent {
     float* m = nullptr;
     float* v = nullptr;
     void* dW = nullptr;  // float (TC) or double (parity)
-    __nv_bfloat16* W16 = nullptr;
-    int* colmax = nullptr;          // K-colmax keys of W16 [D] (loss-fold softmax bound)
-    uint64_t w16_gen = 0;           // bumped whenever W16 is rewritten
-    uint64_t cm_gen = ~0ull;        // the W16 generation colmax describes
-    bool cm_parked = false;         // the parked copy carries a valid colmax
+    __nv_bfloat16* W16 = nullptr;   // transposed bf16 shadow W16^T [D][ldw] (tensor-core mode)
     bool dw_valid = false;  // dW holds this step's partial sum
     bool pending_in = false;  // a swap-in copy the next use must wait for
     bool park_w16 = false;    // the parked copy includes the bf16 shadow
@@ -255,9 +241,12 @@ struct fm_agent {
     double* d_upd = nullptr;  // update sum g^2
     double* h_upd = nullptr;
     int64_t last_rows = 0;
-    // PPO clip
+    // PPO clip: old log-probs of the next micro-batch's packed rows (host copy,
+    // uploaded by train_impl after the workspace is reserved)
     float clip_eps = 0.f;
-    bool have_old_logp = false;
+    std::vector<float> old_logp;
+    // GradKey bookkeeping of the current global step (training.hpp:87-91, 396-401)
+    std::set<std::tuple<std::string, int, int, int64_t>> grad_keys;
     // swap
     bool active = false;
     int park_tier = -1;
@@ -304,8 +293,7 @@ void pool_give(fm_ctx* c, void* p);
 int staging_acquire(fm_ctx* c, size_t bytes, uint8_t** out, cudaEvent_t* ev);
 void ws_free(Workspace& w);
 uint64_t round_up(uint64_t x, uint64_t m);
-int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D);
-int ws_reserve_seg(fm_ctx* c, bool need_a);
+int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D, int n_samples);
 int ws_reserve_rows(fm_ctx* c, int64_t R);
 int ws_reserve_parity(fm_ctx* c, int64_t M, uint64_t V, uint64_t P);
 int ws_reserve_sd(fm_ctx* c, int n);
@@ -315,6 +303,8 @@ size_t align256(size_t x);
 size_t slot_off_m(const fm_agent* a);
 size_t slot_off_v(const fm_agent* a);
 size_t slot_bytes(const fm_agent* a);
+uint64_t w16_ld(const fm_agent* a);     // row pitch of W16^T: V rounded up to 8
+size_t w16_bytes(const fm_agent* a);    // D * w16_ld * 2
 int agent_alloc_device(fm_agent* a, fm_ctx* c, cudaStream_t s);
 void agent_free_device(fm_agent* a, cudaStream_t s);
 int check_active(fm_agent* a);
@@ -322,7 +312,7 @@ int check_active(fm_agent* a);
 
 // ---- parking buffers (fm_swap.cu), also written by the fused update-and-park ----
 extern "C" {
-// Park layout: W | m | v | dW | W16 | colmax keys.
+// Park layout: W | m | v | dW | W16^T.
 size_t park_bytes_for(const fm_agent* a);
 // Parking buffer of `bytes` on `tier` (device pdev), reused while it fits.
 int park_reserve(fm_agent* a, fm_ctx* c, int tier, int pdev, size_t bytes);

@@ -6,9 +6,9 @@ extern "C" {
 // ---------------------------------------------------------------------------
 // training-state swap
 // ---------------------------------------------------------------------------
-// Park layout: W | m | v | dW | W16 | colmax keys.
+// Park layout: W | m | v | dW | W16^T.
 size_t park_bytes_for(const fm_agent* a) {
-    return a->P * 16 + a->P * dw_elem(a) + (a->W16 ? a->P * 2 + a->D * 4 : 0);
+    return a->P * 16 + a->P * dw_elem(a) + (a->W16 ? w16_bytes(a) : 0);
 }
 
 // Parking buffer of `bytes` on `tier` (device pdev), reused while it fits.
@@ -52,11 +52,11 @@ int park_reserve(fm_agent* a, fm_ctx* c, int tier, int pdev, size_t bytes) {
 
 int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
     FM_GUARD_BEGIN
-    // a K-GEMM1 launched after the agent's last op (e.g. the next agent's first
+    // a K-stats launched after the agent's last op (e.g. the next agent's first
     // micro-batch) is a safe and cheap start for the copy-out: the copy engines then
-    // overlap tensor-bound GEMMs instead of the latency-bound K-gather that follows
-    // the end of the currently queued work (measured: K-gather 16 us -> 390 us
-    // beside a 2.4 GB D2D copy)
+    // overlap the streaming passes instead of the latency-bound K-gather that follows
+    // the end of the currently queued work (measured with the earlier GEMM1 pipeline:
+    // K-gather 16 us -> 390 us beside a 2.4 GB D2D copy)
     const bool gated = a->active && a->ctx && a->ctx->gemm_seq > a->last_seq;
     if (int st = check_active(a)) return st;
     if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang (fm_gang_detach first)");
@@ -64,7 +64,7 @@ int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
     if (int st = set_dev(c)) return st;
     const size_t P = a->P;
     const size_t dwb = a->dw_valid ? P * dw_elem(a) : 0;
-    // park layout: W | m | v | dW | W16.  The bf16 shadow travels on the HBM /
+    // park layout: W | m | v | dW | W16^T.  The bf16 shadow travels on the HBM /
     // NVLink tiers (a copy-engine copy is cheaper than regenerating it on the
     // SMs); over PCIe it is regenerated from W on activation instead.
     const bool park_w16 = a->W16 && tier != FM_TIER_HOST;
@@ -87,10 +87,8 @@ int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
     FM_CUDA(cp(p + P * 8, a->m, P * 4));
     FM_CUDA(cp(p + P * 12, a->v, P * 4));
     if (dwb) FM_CUDA(cp(p + P * 16, a->dW, dwb));  // only mid-step gradients travel
-    if (park_w16) FM_CUDA(cp(p + P * (16 + dw_elem(a)), a->W16, P * 2));
+    if (park_w16) FM_CUDA(cp(p + P * (16 + dw_elem(a)), a->W16, w16_bytes(a)));
     a->park_w16 = park_w16;
-    a->cm_parked = park_w16 && a->cm_gen == a->w16_gen;
-    if (a->cm_parked) FM_CUDA(cp(p + P * (18 + dw_elem(a)), a->colmax, a->D * 4));
     FM_CUDA(cudaEventRecord(a->ev_out, c->copy_out));
     agent_free_device(a, c->copy_out);
     a->active = false;
@@ -109,9 +107,9 @@ int fm_agent_activate(fm_agent* a, fm_ctx* c) {
     const size_t P = a->P;
     // the parked copy must have landed before we read it back
     FM_CUDA(cudaStreamWaitEvent(c->copy_in, a->ev_out, 0));
-    // start the copy-in beside the latest queued K-GEMM1 (tensor-bound) rather than
-    // beside whatever runs when it is issued: the latency-bound gather / slot kernels
-    // slowed 4x next to a copy-engine burst (119 vs 28 us per micro-batch)
+    // start the copy-in beside the latest queued K-stats rather than beside whatever
+    // runs when it is issued: the latency-bound gather / slot kernels slowed 4x next to
+    // a copy-engine burst (119 vs 28 us per micro-batch, earlier GEMM1 pipeline)
     if (c->gemm_seq > 0) FM_CUDA(cudaStreamWaitEvent(c->copy_in, c->ev_gemm, 0));
 
     if (int st = agent_alloc_device(a, c, c->copy_in)) return st;
@@ -134,15 +132,12 @@ int fm_agent_activate(fm_agent* a, fm_ctx* c) {
     FM_CUDA(cp(a->v, p + P * 12, P * 4));
     if (a->dw_valid) FM_CUDA(cp(a->dW, p + P * 16, P * dw_elem(a)));
     if (a->W16 && a->park_w16) {
-        FM_CUDA(cp(a->W16, p + P * (16 + dw_elem(a)), P * 2));
+        FM_CUDA(cp(a->W16, p + P * (16 + dw_elem(a)), w16_bytes(a)));
     } else if (a->W16) {
-        FM_CUDA(launch_to_bf16(a->W, a->W16, P, c->num_sms, c->copy_in));  // shadow regenerated
+        FM_CUDA(launch_w16t(a->W, a->V, a->D, a->W16, w16_ld(a), c->num_sms, c->copy_in));  // shadow regenerated
         count_launch();
     }
-    if (a->W16 && a->park_w16 && a->cm_parked) FM_CUDA(cp(a->colmax, p + P * (18 + dw_elem(a)), a->D * 4));
     FM_CUDA(cudaEventRecord(a->ev_in, c->copy_in));
-    ++a->w16_gen;
-    if (a->W16 && a->park_w16 && a->cm_parked) a->cm_gen = a->w16_gen;
     a->pending_in = true;  // consumers wait lazily (check_active)
     a->ctx = c;
     a->active = true;
@@ -166,9 +161,9 @@ struct MigrateBlob {
     int32_t precision;
     uint64_t V, D;
     int32_t src_device;
-    uint8_t dw_valid, cm_valid, pad0, pad1;
+    uint8_t dw_valid, pad0, pad1, pad2;
     int64_t step, version, samples;
-    uint64_t off_w, off_m, off_v, off_dw, off_w16, off_cm;  // within the slot
+    uint64_t off_w, off_m, off_v, off_dw, off_w16;  // within the slot
     cudaIpcMemHandle_t mem;
     cudaIpcEventHandle_t ev;
 };
@@ -208,7 +203,6 @@ static int migrate_export_impl(fm_agent* a, uint8_t* blob_out, uint64_t cap, uin
     b.D = a->D;
     b.src_device = c->device;
     b.dw_valid = a->dw_valid;
-    b.cm_valid = a->W16 && a->cm_gen == a->w16_gen;
     b.step = a->step;
     b.version = a->version;
     b.samples = a->samples;
@@ -217,7 +211,6 @@ static int migrate_export_impl(fm_agent* a, uint8_t* blob_out, uint64_t cap, uin
     b.off_v = off(a->v);
     b.off_dw = off(a->dW);
     b.off_w16 = a->W16 ? off(a->W16) : 0;
-    b.off_cm = a->colmax ? off(a->colmax) : 0;
     FM_CUDA(cudaIpcGetMemHandle(&b.mem, a->slot->base));
     FM_CUDA(cudaIpcGetEventHandle(&b.ev, a->ev_ipc));
     std::memcpy(blob_out, &b, sizeof(b));
@@ -270,15 +263,12 @@ int fm_agent_migrate_import(fm_agent* a, fm_ctx* c, const uint8_t* blob, uint64_
     FM_CUDA(cp(a->m, b.off_m, P * 4));
     FM_CUDA(cp(a->v, b.off_v, P * 4));
     if (b.dw_valid) FM_CUDA(cp(a->dW, b.off_dw, P * dw_elem(a)));
-    if (a->W16) FM_CUDA(cp(a->W16, b.off_w16, P * 2));
-    if (a->W16 && b.cm_valid) FM_CUDA(cp(a->colmax, b.off_cm, a->D * 4));
+    if (a->W16) FM_CUDA(cp(a->W16, b.off_w16, w16_bytes(a)));
     FM_CUDA(cudaEventRecord(a->ev_in, c->copy_in));
     a->dw_valid = b.dw_valid;
     a->step = b.step;
     a->version = b.version;
     a->samples = b.samples;
-    ++a->w16_gen;
-    a->cm_gen = (a->W16 && b.cm_valid) ? a->w16_gen : ~0ull;
     a->pending_in = true;  // consumers wait lazily (check_active)
     // the source may release its slot once this returns
     FM_CUDA(cudaEventSynchronize(a->ev_in));

@@ -1,0 +1,472 @@
+// k_band.cu — the policy's two products in the context-position ("band")
+// formulation:
+//
+// phi_t (policy.hpp:42-51) is the mean one-hot of the LAST FOUR context
+// tokens, and the context grows by one token per trained row
+// (training.hpp:389-393), so row t's logits are a 4-tap sliding sum over
+// context POSITIONS:
+//
+//   z_t[v] = (1/n_t) * sum_{k<4} W[v][feat(q0_t + k)]          (policy.hpp:57-61)
+//
+// where position q holds the context token at that place of the sample's
+// sequence (prompt ++ response) and feat = tok mod D.  Every position's row
+// X[q][:] = W16^T[feat(q)][:] is a contiguous row of the transposed bf16
+// shadow, so each row costs ONE new 2·V-byte row read (the other three are
+// the previous rows' positions, kept in registers) — an HBM-streaming
+// stencil, not a GEMM: the dense Phi·W^T would spend D/4 multiply-adds per
+// useful one.  The weight gradient (policy.hpp:83-90) likewise becomes, per
+// position,
+//
+//   H[q][v] = sum_{t: q in ctx(t)} c_t (delta(v, a_t) - p_t[v])  (c_t = -A/(G n_t))
+//   dW[v][feat(q)] += H[q][v]
+//
+// H rows go to the A' segment of their feature's 256-column block (one row
+// per position — the token-slot layout stored every p~ row 3.6x), and the
+// tcgen05 segmented GEMM2 (k_gemm_tc.cu) scatters them into dW's columns
+// with a one-hot B'.
+//
+//   K-pos     positions of the micro-batch shard: feat[q] (prompt tail +
+//             response prefix of every sample), q0[row]       (codec.hpp:24-30)
+//   K-pslot   A'/B' slot of every position in its feature block's segment
+//   K-stats   pass A: per-(row, 256-column tile) softmax partials (max, sum)
+//             and the taken token's fp32 logit                (policy.hpp:62-70)
+//   K-band    pass B: p = exp(z - lse) (lse from K-lse), the per-row
+//             log-softmax gradient folded into the per-position H rows
+//                                                             (policy.hpp:83-90, training.hpp:394)
+//
+// Both passes stream the W16^T rows through a shared-memory ring filled by
+// one producer thread with 1-D bulk copies (cp.async.bulk, mbarrier
+// completion); eight consumer warps each own 256 vocabulary columns (eight
+// per lane).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+#include <type_traits>
+
+#include "fm_kernels.h"
+#include "fm_ptx.cuh"
+
+namespace fm {
+
+namespace {
+
+constexpr int kBandConsumers = 256;                  // 8 warps x 32 lanes x 8 columns
+constexpr int kBandThreads = kBandConsumers + 32;    // + the producer warp
+constexpr int kBandCols = kBandConsumers * 8;        // 2,048 vocabulary columns per CTA
+constexpr int kBandStages = 12;
+constexpr int kBandStageBytes = kBandCols * 2;       // 4 KB of one W16^T row
+constexpr int kBandRows = 128;                       // trained rows per CTA
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ int token_of(uint64_t x) {  // static_cast<Token>(u64), codec.hpp:28
+    return static_cast<int>(static_cast<uint32_t>(x));
+}
+__device__ __forceinline__ int32_t feature_of(int tok, uint64_t D) {  // policy.hpp:48
+    return static_cast<int32_t>(static_cast<uint64_t>(static_cast<int64_t>(tok)) % D);
+}
+
+// sample holding global row gr: the last s with row_start[s] <= gr (rows are in poll order)
+__device__ __forceinline__ int sample_of_row(const SampleDesc* sd, int n, int64_t gr) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sd[mid].row_start <= gr) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// First position of sample s in the shard: every sample overlapping the shard
+// owns (its rows in the shard) + 3 consecutive positions.
+__device__ __forceinline__ int64_t pos_base(const SampleDesc* sd, int s, int s_first, int64_t row_lo) {
+    const int64_t rs = sd[s].row_start - row_lo;
+    return (rs > 0 ? rs : 0) + 3 * static_cast<int64_t>(s - s_first);
+}
+
+__global__ void __launch_bounds__(256) positions_kernel(const uint8_t* __restrict__ arena,
+                                                        const SampleDesc* __restrict__ sd, int n, int64_t row_lo,
+                                                        int64_t M, uint64_t D, int32_t* __restrict__ feat,
+                                                        int64_t Qcap) {
+    const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (q >= Qcap) return;
+    int32_t f = -1;
+    if (M > 0 && n > 0) {
+        const int s_first = sample_of_row(sd, n, row_lo);
+        int lo = s_first, hi = n - 1;  // last sample whose first position is <= q
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pos_base(sd, mid, s_first, row_lo) <= q) lo = mid;
+            else hi = mid - 1;
+        }
+        const SampleDesc d = sd[lo];
+        const int64_t a = d.row_start > row_lo ? d.row_start : row_lo;
+        const int64_t e = d.row_start + d.resp_n < row_lo + M ? d.row_start + d.resp_n : row_lo + M;
+        const int64_t k = q - pos_base(sd, lo, s_first, row_lo);
+        if (e > a && k < (e - a) + 3) {
+            // position k of the shard's part of the sample = sequence index prompt_n - 4 + ja + k
+            const int64_t seq = static_cast<int64_t>(d.prompt_n) - 4 + (a - d.row_start) + k;
+            if (seq >= 0) {
+                const uint64_t* P = reinterpret_cast<const uint64_t*>(arena + d.prompt_off + 8);
+                const uint64_t* R = reinterpret_cast<const uint64_t*>(arena + d.resp_off + 8);
+                const int tok = token_of(seq < d.prompt_n ? __ldg(P + seq) : __ldg(R + (seq - d.prompt_n)));
+                f = feature_of(tok, D);
+            }
+        }
+    }
+    feat[q] = f;
+}
+
+// ---- K-pslot ---------------------------------------------------------------
+// block-wide exclusive scan of a 0/1 flag over 1024 threads; returns the rank,
+// *total gets the count (all threads)
+__device__ __forceinline__ int block_rank(bool flag, int* wsum, int* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    const int pre = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) wsum[wid] = __popc(bal);
+    __syncthreads();
+    if (wid == 0) {
+        const int v = wsum[lane];
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        wsum[lane] = inc - v;
+        if (lane == 31) wsum[32] = inc;
+    }
+    __syncthreads();
+    const int r = wsum[wid] + pre;
+    *total = wsum[32];
+    __syncthreads();
+    return r;
+}
+
+// grid (nblk, chunks of 1024 positions): CTA (b, c) counts chunk c's positions
+// whose feature lies in block b; CTA (b = 0, c) resets their slots
+__global__ void __launch_bounds__(1024) pslot_count_kernel(const int32_t* __restrict__ feat, int64_t Q,
+                                                           int32_t* __restrict__ ccount, int32_t* __restrict__ slot) {
+    __shared__ int wsum[33];
+    const int b = blockIdx.x, c = blockIdx.y;
+    const int64_t q = static_cast<int64_t>(c) * 1024 + threadIdx.x;
+    const int32_t f = q < Q ? __ldg(feat + q) : -1;
+    int tot;
+    block_rank(f >= 0 && (f >> 8) == b, wsum, &tot);
+    if (threadIdx.x == 0) ccount[static_cast<size_t>(b) * gridDim.y + c] = tot;
+    if (b == 0 && q < Q) slot[q] = -1;
+}
+
+// grid (nblk, chunks): segment offsets from the chunk counts (block-major,
+// every segment padded to a multiple of 64 rows, at least 64), the position's
+// rank in its segment (position order: deterministic) and its one-hot B' row.
+__global__ void __launch_bounds__(1024) pslot_place_kernel(const int32_t* __restrict__ feat, int64_t Q,
+                                                           const int32_t* __restrict__ ccount,
+                                                           int32_t* __restrict__ kseg_off,
+                                                           int32_t* __restrict__ kiters, int32_t* __restrict__ slot,
+                                                           __nv_bfloat16* __restrict__ bseg,
+                                                           unsigned long long* rows_acc) {
+    __shared__ int wsum[33];
+    __shared__ int off_s, base_s, len_s;
+    const int b = blockIdx.x, c = blockIdx.y, nch = gridDim.y;
+    if (threadIdx.x < 32) {
+        int off = 0;
+        for (int bb = 0; bb <= b; ++bb) {
+            int t = 0;
+            for (int i = static_cast<int>(threadIdx.x); i < nch; i += 32) t += ccount[static_cast<size_t>(bb) * nch + i];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (bb < b) off += t < 64 ? 64 : (t + 63) / 64 * 64;
+            else if (threadIdx.x == 0) len_s = t;
+        }
+        int base = 0;
+        for (int i = static_cast<int>(threadIdx.x); i < c; i += 32) base += ccount[static_cast<size_t>(b) * nch + i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
+        if (threadIdx.x == 0) {
+            off_s = off;
+            base_s = base;
+        }
+    }
+    __syncthreads();
+    const int off = off_s, len = len_s;
+    if (c == 0 && threadIdx.x == 0) {
+        const int padded = len < 64 ? 64 : (len + 63) / 64 * 64;
+        kseg_off[b] = off;
+        kiters[b] = padded / 64;
+        if (rows_acc) atomicAdd(rows_acc, static_cast<unsigned long long>(padded));
+    }
+    const int64_t q = static_cast<int64_t>(c) * 1024 + threadIdx.x;
+    const int32_t f = q < Q ? __ldg(feat + q) : -1;
+    const bool hit = f >= 0 && (f >> 8) == b;
+    int tot;
+    const int rk = block_rank(hit, wsum, &tot);
+    if (hit) {
+        const int s = off + base_s + rk;
+        slot[q] = s;
+        bseg[static_cast<size_t>(s) * 256 + (f & 255)] = __float2bfloat16_rn(1.f);
+    }
+}
+
+// ---- K-stats / K-band ------------------------------------------------------
+__device__ __forceinline__ void unpack8(uint4 u, float (&x)[8]) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        x[2 * i] = __uint_as_float(w[i] << 16);
+        x[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&x)[8]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+        w[i] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Grid (vocabulary slices of 2,048 columns, chunks of kBandRows rows).
+// kGrad = false: pass A (K-stats) over rows [ra, rb).
+// kGrad = true:  pass B (K-band): rows [ra - 3, rb) so that every position in
+// [q0[ra], q0[rb]) (the chunk's emission range) has all of its rows.
+// Shared memory: the W16^T row ring, its full / empty barriers, and the
+// chunk's per-row metadata (q0, action, 1/n; pass B: lse, coefficient).
+constexpr int kMetaRows = kBandRows + 4;
+constexpr size_t kBandSmem = kBandStages * kBandStageBytes + 2 * kBandStages * sizeof(uint64_t) +
+                             5 * kMetaRows * sizeof(int32_t);
+
+template <bool kGrad>
+__global__ void __launch_bounds__(kBandThreads) band_kernel(const BandArgs A) {
+    extern __shared__ __align__(128) uint8_t band_smem[];
+    uint8_t (*ring)[kBandStageBytes] = reinterpret_cast<uint8_t (*)[kBandStageBytes]>(band_smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(band_smem + kBandStages * kBandStageBytes);
+    uint64_t* empty = full + kBandStages;
+    int32_t* m_q0 = reinterpret_cast<int32_t*>(empty + kBandStages);
+    int32_t* m_act = m_q0 + kMetaRows;
+    float* m_rs = reinterpret_cast<float*>(m_act + kMetaRows);
+    float* m_lse = m_rs + kMetaRows;
+    float* m_ce = m_lse + kMetaRows;
+    const int tid = static_cast<int>(threadIdx.x);
+    const int lane = tid & 31;
+    const int64_t v0 = static_cast<int64_t>(blockIdx.x) * kBandCols;
+    const int64_t ra = static_cast<int64_t>(blockIdx.y) * kBandRows;
+    if (ra >= A.M) return;
+    const int64_t rb = ra + kBandRows < A.M ? ra + kBandRows : A.M;
+    const int64_t rstart = kGrad ? (ra >= 3 ? ra - 3 : 0) : ra;
+    const int nrows = static_cast<int>(rb - rstart);
+    if (tid == 0) {
+        for (int s = 0; s < kBandStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kBandConsumers / 32);
+        }
+        fence_barrier_init();
+    }
+    // the rows' metadata, once per CTA (off the per-row critical path)
+    for (int i = tid; i <= nrows; i += kBandThreads) {
+        const int64_t r = rstart + i;
+        m_q0[i] = r < A.M ? __ldg(A.q0 + r) : INT32_MAX;
+        if (i < nrows) {
+            m_act[i] = __ldg(A.action + r);
+            m_rs[i] = __ldg(A.rscale + r);
+            if constexpr (kGrad) {
+                m_lse[i] = __ldg(A.lse + r);
+                m_ce[i] = __ldg(A.coef_eff + r);
+            }
+        }
+    }
+    __syncthreads();
+    const int64_t qa = m_q0[0];
+    const int64_t qb = static_cast<int64_t>(m_q0[nrows - 1]) + 4;
+    const int nq = static_cast<int>(qb - qa);
+
+    if (tid >= kBandConsumers) {
+        // ===== producer warp: lane 0 streams the positions' W16^T row slices; the
+        // positions' features are fetched 32 at a time, one group ahead =====
+        const int64_t cols = A.ldw - v0 < kBandCols ? A.ldw - v0 : kBandCols;
+        const uint32_t bytes = static_cast<uint32_t>(cols) * 2u;
+        const __nv_bfloat16* base = A.w16t + v0;
+        int32_t f_next = lane < nq ? __ldg(A.pos_feat + qa + lane) : -1;
+        for (int k0 = 0; k0 < nq; k0 += 32) {
+            const int32_t f_cur = f_next;
+            f_next = k0 + 32 + lane < nq ? __ldg(A.pos_feat + qa + k0 + 32 + lane) : -1;
+            const int kn = nq - k0 < 32 ? nq - k0 : 32;
+            for (int j = 0; j < kn; ++j) {
+                const int k = k0 + j;
+                const int st = k % kBandStages;
+                if (k >= kBandStages) mbar_wait(&empty[st], static_cast<uint32_t>((k / kBandStages) - 1) & 1u);
+                const int32_t f = __shfl_sync(0xffffffffu, f_cur, j);
+                if (lane == 0) {
+                    // a position before the sequence start reads the zero row
+                    const __nv_bfloat16* src = f >= 0 ? base + static_cast<int64_t>(f) * A.ldw : A.zero_row;
+                    mbar_arrive_expect_tx(&full[st], bytes);
+                    bulk_load(ring[st], src, bytes, &full[st]);
+                }
+                __syncwarp();
+            }
+        }
+        return;
+    }
+
+    // ===== consumers =====
+    const int warp = tid >> 5;
+    const int64_t c0 = v0 + static_cast<int64_t>(tid) * 8;
+    const int nvalid = A.V - c0 >= 8 ? 8 : (A.V - c0 > 0 ? static_cast<int>(A.V - c0) : 0);
+    const int tile = static_cast<int>(blockIdx.x) * (kBandCols / 256) + warp;
+    float xr[4][8];
+    float acc[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            xr[i][j] = 0.f;
+            acc[i][j] = 0.f;
+        }
+    int ri = 0;                  // next row (index into the metadata)
+    int64_t next_end = qa + 3;   // its last position
+    int64_t elo = 0, ehi = 0;
+    // pass B: slots of the positions being flushed, 32 at a time (one group ahead)
+    int64_t sg = 0;
+    int32_t s_cur = -1, s_next = -1;
+    if constexpr (kGrad) {
+        elo = m_q0[ra - rstart];
+        ehi = rb < A.M ? static_cast<int64_t>(m_q0[nrows]) : qb;
+        sg = elo & ~static_cast<int64_t>(31);
+        s_cur = sg + lane < qb ? __ldg(A.pos_slot + sg + lane) : -1;
+        s_next = sg + 32 + lane < qb ? __ldg(A.pos_slot + sg + 32 + lane) : -1;
+    }
+
+    auto row = [&](int i, int64_t rr) {
+        const float rs = m_rs[i];
+        const int act = m_act[i];
+        float z[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) z[j] = rs * ((xr[0][j] + xr[1][j]) + (xr[2][j] + xr[3][j]));
+        if constexpr (!kGrad) {
+            float mx = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (j < nvalid) mx = fmaxf(mx, z[j]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            float sum = 0.f;
+            if (mx != -INFINITY) {
+                const float mo = mx * kLog2e;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (j < nvalid) sum += exp2f(fmaf(z[j], kLog2e, -mo));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            if (lane == 0 && mx != -INFINITY) A.stats[rr * A.stats_ld + tile] = make_float2(mx, sum);
+            if (act >= c0 && act < c0 + nvalid) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (act - c0 == j) A.zact[rr] = z[j];
+            }
+        } else {
+            const float ce = m_ce[i];
+            if (ce != 0.f) {  // zero-advantage rows contribute nothing (training.hpp:394)
+                const float lo = m_lse[i] * kLog2e;
+                float g[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) g[j] = j < nvalid ? -ce * exp2f(fmaf(z[j], kLog2e, -lo)) : 0.f;
+                if (act >= c0 && act < c0 + nvalid) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (act - c0 == j) g[j] += ce;
+                }
+#pragma unroll
+                for (int i2 = 0; i2 < 4; ++i2)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[i2][j] += g[j];
+            }
+        }
+    };
+
+    // one position step; S = q & 3 is static so the rings stay in registers
+    auto step = [&](int64_t q, auto Sc) {
+        constexpr int S = decltype(Sc)::value;
+        if (q >= qa && q < qb) {
+            const int k = static_cast<int>(q - qa);
+            const int st = k % kBandStages;
+            mbar_wait(&full[st], static_cast<uint32_t>(k / kBandStages) & 1u);
+            const uint4 u = *reinterpret_cast<const uint4*>(&ring[st][tid * 16]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            unpack8(u, xr[S]);
+            if constexpr (kGrad) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[S][j] = 0.f;
+            }
+            if (q == next_end) {  // the row whose four positions end here
+                row(ri, rstart + ri);
+                ++ri;
+                next_end = static_cast<int64_t>(m_q0[ri]) + 3;  // INT32_MAX + 3 past the last row
+            }
+        }
+        if constexpr (kGrad) {
+            // position q - 3 has all its rows now (a later row starts at >= q - 2)
+            const int64_t p = q - 3;
+            if (p >= elo && p < ehi) {
+                if (p >= sg + 32) {  // next group of slots (warp-uniform)
+                    sg += 32;
+                    s_cur = s_next;
+                    s_next = sg + 32 + lane < qb ? __ldg(A.pos_slot + sg + 32 + lane) : -1;
+                }
+                const int32_t sl = __shfl_sync(0xffffffffu, s_cur, static_cast<int>(p - sg));
+                if (sl >= 0 && nvalid > 0)
+                    *reinterpret_cast<uint4*>(A.aseg + static_cast<int64_t>(sl) * A.ld_a + c0) = pack8(acc[(S + 1) & 3]);
+            }
+        }
+    };
+    const int64_t qend = kGrad ? qb + 3 : qb;
+    for (int64_t qq = qa & ~static_cast<int64_t>(3); qq < qend; qq += 4) {
+        step(qq, std::integral_constant<int, 0>{});
+        step(qq + 1, std::integral_constant<int, 1>{});
+        step(qq + 2, std::integral_constant<int, 2>{});
+        step(qq + 3, std::integral_constant<int, 3>{});
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_positions(const uint8_t* arena, const SampleDesc* sd, int n_samples, int64_t row_lo, int64_t M,
+                             uint64_t D, int32_t* feat, int64_t Qcap, cudaStream_t s) {
+    if (Qcap == 0) return cudaSuccess;
+    positions_kernel<<<static_cast<unsigned>((Qcap + 255) / 256), 256, 0, s>>>(arena, sd, n_samples, row_lo, M, D,
+                                                                              feat, Qcap);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pslots(const int32_t* feat, int64_t Q, int nblk, int32_t* kcount, int32_t* kseg_off, int32_t* kiters,
+                          int32_t* slot, __nv_bfloat16* bseg, int64_t bseg_rows, unsigned long long* rows_acc,
+                          cudaStream_t s) {
+    if (nblk <= 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(bseg, 0, static_cast<size_t>(bseg_rows) * 256 * 2, s);
+    if (e != cudaSuccess) return e;
+    const unsigned nch = static_cast<unsigned>(Q > 0 ? (Q + 1023) / 1024 : 1);
+    pslot_count_kernel<<<dim3(nblk, nch), 1024, 0, s>>>(feat, Q, kcount, slot);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    pslot_place_kernel<<<dim3(nblk, nch), 1024, 0, s>>>(feat, Q, kcount, kseg_off, kiters, slot, bseg, rows_acc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s) {
+    if (A.M <= 0) return cudaSuccess;
+    const dim3 grid(static_cast<unsigned>((A.V + kBandCols - 1) / kBandCols),
+                    static_cast<unsigned>((A.M + kBandRows - 1) / kBandRows));
+    auto k = grad ? band_kernel<true> : band_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBandSmem));
+    if (e != cudaSuccess) return e;
+    k<<<grid, kBandThreads, kBandSmem, s>>>(A);
+    return cudaGetLastError();
+}
+
+}  // namespace fm

@@ -598,6 +598,12 @@ class TrainingEngine:
         if min(schema.column_index(c) for c in ("prompt", "response", "advantage")) < 0:
             raise MarlsimError(13, "trainer needs prompt/response/advantage columns")
         n = len(batch.samples)
+        # DuplicateSample guard (training.hpp:396-401), before anything is enqueued
+        ids = [s.sample_id.input_id.encode() for s in batch.samples]
+        keys = (_lib.fm_sample_key * max(n, 1))(*[
+            _lib.fm_sample_key(ids[i], s.sample_id.number_of_turns, s.sample_id.trajectory_id, s.policy_version)
+            for i, s in enumerate(batch.samples)])
+        check(lib().fm_agent_add_grad_keys(g.handle, keys, n))
         ticket = C.c_int64()
         if batch.dtable is not None:  # polled on the device: descriptors stay in HBM
             check(lib().fm_train_polled(g.handle, batch.dtable, batch.poll_id, self.global_batch, C.byref(ticket)))
