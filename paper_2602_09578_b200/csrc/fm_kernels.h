@@ -33,12 +33,14 @@ struct RowBuffers {
     float* logp;       // [Mpad]
     float* coef_eff;   // [Mpad] coef * surrogate factor
     int32_t* q0;       // [Mpad] first context position of the row (band formulation; nullable)
+    float* mrow;       // [Mpad] softmax bound (1/n) sum_k fmax[f_k] >= max_v z (with fmax)
+    const float* fmax; // [D] per-feature maximum of the bf16 shadow (nullable: no bounds)
 };
 
-// K-lse arguments (fm_lse.cuh: the per-row routine).
+// K-lse arguments.
 struct LseArgs {
     const float* zact;    // [Mpad] fp32 logit of the taken token
-    const float2* stats;  // [Mpad][stats_ld] (max, sum exp) per 256-column tile
+    const float* stats;   // [stats_ld][Mpad] partial sums of exp(z - mrow) (K-stats)
     int stats_ld;
     int64_t M, Mpad, V;
     const SampleDesc* sd;
@@ -61,6 +63,10 @@ cudaError_t launch_gather(const uint8_t* arena, const SampleDesc* sd, int n_samp
 // (every sample overlapping the shard owns its rows + 3 positions: the three
 // tokens before its first row's last context token), -1 where the sequence
 // has no token (prompt shorter than 4) and past the last position (q < Qcap).
+// K-fmax: fmax[f] = max_v W16^T[f][v] (the per-feature bound K-gather sums into
+// every row's softmax offset), one CTA per feature row.
+cudaError_t launch_fmax(const __nv_bfloat16* w16t, int64_t D, int64_t V, int64_t ldw, float* fmax, cudaStream_t s);
+
 cudaError_t launch_positions(const uint8_t* arena, const SampleDesc* sd, int n_samples, int64_t row_lo, int64_t M,
                              uint64_t D, int32_t* feat, int64_t Qcap, cudaStream_t s);
 
@@ -84,9 +90,11 @@ struct BandArgs {
     const int32_t* q0;          // [M]
     const int32_t* action;      // [M]
     const float* rscale;        // [M]
+    const float* mrow;          // [M] softmax bound of the row
     int64_t M;
+    int64_t ld_stats;           // row pitch of stats (Mpad)
     // pass A (K-stats)
-    float2* stats;  // [M][stats_ld]
+    float* stats;   // [stats_ld][ld_stats] partial sums of exp(z - mrow)
     int stats_ld;
     float* zact;    // [M]
     // pass B (K-band)
@@ -97,10 +105,12 @@ struct BandArgs {
     int64_t ld_a;
 };
 cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s);
+// K-stats partials per row (one per consumer warp of every vocabulary slice).
+int band_stats_ld(int64_t V);
 
-// K-lse: combine K-stats' per-tile softmax partials into lse, the taken-token
+// K-lse: lse = mrow + log(sum of K-stats' partial sums), the taken-token
 // log-prob (from the fp32 logit K-stats captured) and the effective row
-// coefficient (PPO-clip surrogate optional).
+// coefficient (PPO-clip surrogate optional).  One lane per row.
 cudaError_t launch_lse(const LseArgs& L, cudaStream_t s);
 
 // Parity tooling: out[v][j] = dW[v][cols[j]] (f32 or f64 accumulator).

@@ -355,6 +355,7 @@ int fm_agent_deserialize(fm_agent* a, int64_t global_batch, const uint8_t* in, u
     if (a->W16) {
         FM_CUDA(launch_w16t(a->W, a->V, a->D, a->W16, w16_ld(a), c->num_sms, s));
         count_launch();
+        a->fmax_valid = false;
     }
     FM_CUDA(cudaStreamSynchronize(s));
     a->version = static_cast<int64_t>(version);

@@ -152,6 +152,7 @@ void ws_free(Workspace& w) {
     cudaFree(w.coef_eff);
     cudaFree(w.old_logp);
     cudaFree(w.q0);
+    cudaFree(w.mrow);
     cudaFree(w.pos_feat);
     cudaFree(w.pos_slot);
     cudaFree(w.zact);
@@ -197,7 +198,7 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D, int n_samples
     ws_free(w);
     w = keep;
     const uint64_t ldz = round_up(VV, 8);
-    const uint64_t tiles_n = (VV + kGemmBN - 1) / kGemmBN;
+    const uint64_t tiles_n = static_cast<uint64_t>(band_stats_ld(static_cast<int64_t>(VV))) + 8;
     const int64_t nblk = static_cast<int64_t>((DD + 255) / 256);
     const int64_t kp = Q + 64 * nblk;
     cudaError_t e = cudaSuccess;
@@ -211,8 +212,9 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D, int n_samples
     e = e ? e : dalloc(&w.logp, R);
     e = e ? e : dalloc(&w.coef_eff, R);
     e = e ? e : dalloc(&w.q0, R);
+    e = e ? e : dalloc(&w.mrow, R);
     e = e ? e : dalloc(&w.zact, R);
-    e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n);
+    e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n);  // [tiles][R] partial sums
     e = e ? e : dalloc(&w.pos_feat, static_cast<size_t>(Q));
     e = e ? e : dalloc(&w.pos_slot, static_cast<size_t>(Q));
     e = e ? e : dalloc(&w.aseg, static_cast<size_t>(kp) * ldz);
@@ -323,6 +325,8 @@ RowBuffers row_buffers(Workspace& w) {
     r.logp = w.logp;
     r.coef_eff = w.coef_eff;
     r.q0 = w.q0;
+    r.mrow = w.mrow;
+    r.fmax = nullptr;
     return r;
 }
 
@@ -538,7 +542,7 @@ size_t w16_bytes(const fm_agent* a) { return a->D * w16_ld(a) * 2; }
 size_t slot_bytes(const fm_agent* a) {
     const size_t P = a->P;
     return align256(P * 8) + 2 * align256(P * 4) + align256(P * dw_elem(a)) +
-           (a->precision == FM_PRECISION_BF16_TC ? align256(w16_bytes(a)) : 0);
+           (a->precision == FM_PRECISION_BF16_TC ? align256(w16_bytes(a)) + align256(a->D * 4) : 0);
 }
 
 // Binds a free slot of ctx c (allocating one the first time), ordered on
@@ -574,6 +578,9 @@ int agent_alloc_device(fm_agent* a, fm_ctx* c, cudaStream_t s) {
     a->dW = p;
     p += align256(P * dw_elem(a));
     a->W16 = a->precision == FM_PRECISION_BF16_TC ? reinterpret_cast<__nv_bfloat16*>(p) : nullptr;
+    p += a->W16 ? align256(w16_bytes(a)) : 0;
+    a->fmax = a->W16 ? reinterpret_cast<float*>(p) : nullptr;
+    a->fmax_valid = false;
     return FM_OK;
 }
 
@@ -592,6 +599,8 @@ void agent_free_device(fm_agent* a, cudaStream_t s) {
     a->m = a->v = nullptr;
     a->dW = nullptr;
     a->W16 = nullptr;
+    a->fmax = nullptr;
+    a->fmax_valid = false;
 }
 
 // Every operation on an agent goes through here: besides the InactiveGroup
@@ -693,6 +702,7 @@ int fm_agent_set_weights(fm_agent* a, const double* W) {
     if (a->W16) {
         FM_CUDA(launch_w16t(a->W, a->V, a->D, a->W16, w16_ld(a), c->num_sms, c->stream));
         count_launch();
+        a->fmax_valid = false;
     }
     FM_CUDA(cudaStreamSynchronize(c->stream));
     return FM_OK;
@@ -912,9 +922,19 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             const uint64_t ldz = round_up(a->V, 8);
             const int64_t Qcap = Mpad + 3 * static_cast<int64_t>(n);
             const int nblk = static_cast<int>((a->D + 255) / 256);
+            if (!a->fmax_valid) {
+                // per-feature maxima of the shadow (the rows' softmax bounds), once per
+                // shadow generation (update, set_weights, swap-in, migration)
+                KScope k(c, K_GATHER, s);
+                FM_CUDA(launch_fmax(a->W16, static_cast<int64_t>(a->D), static_cast<int64_t>(a->V),
+                                    static_cast<int64_t>(w16_ld(a)), a->fmax, s));
+                a->fmax_valid = true;
+                count_launch();
+            }
+            rows.fmax = a->fmax;
             {
-                // K-gather (rows, q0) + K-pos (position features) + K-pslot (segment slots,
-                // one-hot B')
+                // K-gather (rows, q0, bounds) + K-pos (position features) + K-pslot (segment
+                // slots, one-hot B')
                 KScope k(c, K_GATHER, s);
                 FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, Mpad, G, a->D, rows, s));
                 FM_CUDA(launch_positions(c->arena, w.sd, n, row_lo, M, a->D, w.pos_feat, Qcap, s));
@@ -931,9 +951,11 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             ba.q0 = w.q0;
             ba.action = w.action;
             ba.rscale = w.rscale;
+            ba.mrow = w.mrow;
             ba.M = M;
+            ba.ld_stats = Mpad;
             ba.stats = w.stats;
-            ba.stats_ld = static_cast<int>((a->V + 255) / 256);
+            ba.stats_ld = band_stats_ld(static_cast<int64_t>(a->V));
             ba.zact = w.zact;
             ba.lse = w.lse;
             ba.coef_eff = w.coef_eff;
@@ -1221,6 +1243,7 @@ static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, doubl
     a->samples = 0;
     a->version += 1;
     a->grad_keys.clear();
+    a->fmax_valid = false;  // the shadow changed
     FM_CUDA(cudaMemcpyAsync(a->h_upd, a->d_upd, sizeof(double), cudaMemcpyDeviceToHost, s));
     if (park) {
         // the parked state is complete when K-adam is: release the slot behind it

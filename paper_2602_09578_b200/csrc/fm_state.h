@@ -79,7 +79,8 @@ struct Workspace {
     int32_t *pos_feat = nullptr, *pos_slot = nullptr;
     int64_t pos_cap = 0;
     float* zact = nullptr;   // logit of the taken token [Mpad]
-    float2* stats = nullptr; // K-stats partials [Mpad][ceil(V/256)]
+    float* mrow = nullptr;   // per-row softmax bound (1/n) sum_k fmax[f_k] [Mpad]
+    float* stats = nullptr;  // K-stats partial sums exp(z - mrow), [stats_ld][Mpad]
     // segments of K-GEMM2: A' = per-position gradient rows H [kp_cap][ldz] bf16,
     // B' = one-hot [kp_cap][256] bf16
     __nv_bfloat16 *aseg = nullptr, *bseg = nullptr;
@@ -224,6 +225,8 @@ struct fm_agent {
     float* v = nullptr;
     void* dW = nullptr;  // float (TC) or double (parity)
     __nv_bfloat16* W16 = nullptr;   // transposed bf16 shadow W16^T [D][ldw] (tensor-core mode)
+    float* fmax = nullptr;          // fmax[f] = max_v W16^T[f][v] (K-stats' per-row softmax bound)
+    bool fmax_valid = false;        // fmax describes the current shadow
     bool dw_valid = false;  // dW holds this step's partial sum
     bool pending_in = false;  // a swap-in copy the next use must wait for
     bool park_w16 = false;    // the parked copy includes the bf16 shadow

@@ -138,6 +138,7 @@ int fm_agent_activate(fm_agent* a, fm_ctx* c) {
         count_launch();
     }
     FM_CUDA(cudaEventRecord(a->ev_in, c->copy_in));
+    a->fmax_valid = false;
     a->pending_in = true;  // consumers wait lazily (check_active)
     a->ctx = c;
     a->active = true;
@@ -269,6 +270,7 @@ int fm_agent_migrate_import(fm_agent* a, fm_ctx* c, const uint8_t* blob, uint64_
     a->step = b.step;
     a->version = b.version;
     a->samples = b.samples;
+    a->fmax_valid = false;
     a->pending_in = true;  // consumers wait lazily (check_active)
     // the source may release its slot once this returns
     FM_CUDA(cudaEventSynchronize(a->ev_in));

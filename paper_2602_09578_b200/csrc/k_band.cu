@@ -53,12 +53,14 @@ namespace fm {
 
 namespace {
 
-constexpr int kBandConsumers = 256;                  // 8 warps x 32 lanes x 8 columns
+constexpr int kBandConsumers = 256;                  // 8 consumer warps
 constexpr int kBandThreads = kBandConsumers + 32;    // + the producer warp
-constexpr int kBandCols = kBandConsumers * 8;        // 2,048 vocabulary columns per CTA
 constexpr int kBandStages = 12;
-constexpr int kBandStageBytes = kBandCols * 2;       // 4 KB of one W16^T row
 constexpr int kBandRows = 128;                       // trained rows per CTA
+// columns per lane: 8 * kV.  Both passes run 8 with two CTAs (18 warps) per SM:
+// 16 columns per lane (measured: K-stats 0.43-0.53 ms vs 0.33 ms at C2) needs
+// more registers than two CTAs leave and drops to one CTA per SM.
+constexpr int kStatsV = 1, kGradV = 1;
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ int token_of(uint64_t x) {  // static_cast<Token>(u64), codec.hpp:28
@@ -117,6 +119,32 @@ __global__ void __launch_bounds__(256) positions_kernel(const uint8_t* __restric
         }
     }
     feat[q] = f;
+}
+
+// ---- K-fmax: per-feature maxima of the shadow ----------------------------------
+__global__ void __launch_bounds__(256) fmax_kernel(const __nv_bfloat16* __restrict__ w16t, int64_t V, int64_t ldw,
+                                                   float* __restrict__ fmax) {
+    __shared__ float red[8];
+    const __nv_bfloat16* row = w16t + static_cast<int64_t>(blockIdx.x) * ldw;
+    float m = -INFINITY;
+    const int64_t v8 = V / 8;
+    for (int64_t i = threadIdx.x; i < v8; i += blockDim.x) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(row) + i);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            m = fmaxf(m, fmaxf(__uint_as_float(w[k] << 16), __uint_as_float(w[k] & 0xffff0000u)));
+    }
+    for (int64_t v = v8 * 8 + threadIdx.x; v < V; v += blockDim.x) m = fmaxf(m, __bfloat162float(row[v]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = red[0];
+        for (int k = 1; k < 8; ++k) t = fmaxf(t, red[k]);
+        fmax[blockIdx.x] = t;
+    }
 }
 
 // ---- K-pslot ---------------------------------------------------------------
@@ -212,54 +240,67 @@ __global__ void __launch_bounds__(1024) pslot_place_kernel(const int32_t* __rest
 }
 
 // ---- K-stats / K-band ------------------------------------------------------
-__device__ __forceinline__ void unpack8(uint4 u, float (&x)[8]) {
+// 8 bf16 -> 4 fp32 pairs (exact)
+__device__ __forceinline__ void unpack8(uint4 u, float2 (&x)[4]) {
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        x[2 * i] = __uint_as_float(w[i] << 16);
-        x[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
-    }
+    for (int i = 0; i < 4; ++i) x[i] = make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xffff0000u));
 }
 
-__device__ __forceinline__ uint4 pack8(const float (&x)[8]) {
+__device__ __forceinline__ uint4 pack8(const float2 (&x)[4]) {
     uint32_t w[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const __nv_bfloat162 h = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+        const __nv_bfloat162 h = __floats2bfloat162_rn(x[i].x, x[i].y);
         w[i] = *reinterpret_cast<const uint32_t*>(&h);
     }
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// Grid (vocabulary slices of 2,048 columns, chunks of kBandRows rows).
+// 2^x, one MUFU op (inputs <= 0 here; results below 2^-126 flush to zero)
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Grid (vocabulary slices of 2,048 * kV columns, chunks of kBandRows rows).
 // kGrad = false: pass A (K-stats) over rows [ra, rb).
 // kGrad = true:  pass B (K-band): rows [ra - 3, rb) so that every position in
 // [q0[ra], q0[rb]) (the chunk's emission range) has all of its rows.
 // Shared memory: the W16^T row ring, its full / empty barriers, and the
 // chunk's per-row metadata (q0, action, 1/n; pass B: lse, coefficient).
 constexpr int kMetaRows = kBandRows + 4;
-constexpr size_t kBandSmem = kBandStages * kBandStageBytes + 2 * kBandStages * sizeof(uint64_t) +
-                             5 * kMetaRows * sizeof(int32_t);
+constexpr int kRedPitch = 33;  // per-warp [32 rows][32 lanes] partial sums, padded (conflict-free transpose)
+template <bool kGrad, int kV>
+constexpr size_t band_smem_bytes() {
+    return kBandStages * kBandConsumers * 16 * kV + 2 * kBandStages * sizeof(uint64_t) +
+           5 * kMetaRows * sizeof(int32_t) + (kGrad ? 0 : (kBandConsumers / 32) * 32 * kRedPitch * sizeof(float));
+}
 
-template <bool kGrad>
-__global__ void __launch_bounds__(kBandThreads) band_kernel(const BandArgs A) {
+template <bool kGrad, int kV, int kMinBlocks>
+__global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const BandArgs A) {
+    constexpr int kCols = kBandConsumers * 8 * kV;   // vocabulary columns per CTA
+    constexpr int kStage = kCols * 2;                // bytes of one position's W16^T slice
+    constexpr int kP = 4 * kV;                       // fp32 pairs per lane
     extern __shared__ __align__(128) uint8_t band_smem[];
-    uint8_t (*ring)[kBandStageBytes] = reinterpret_cast<uint8_t (*)[kBandStageBytes]>(band_smem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(band_smem + kBandStages * kBandStageBytes);
+    uint8_t* ring = band_smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(band_smem + kBandStages * kStage);
     uint64_t* empty = full + kBandStages;
     int32_t* m_q0 = reinterpret_cast<int32_t*>(empty + kBandStages);
     int32_t* m_act = m_q0 + kMetaRows;
     float* m_rs = reinterpret_cast<float*>(m_act + kMetaRows);
-    float* m_lse = m_rs + kMetaRows;
+    float* m_lse = m_rs + kMetaRows;  // pass A: the rows' softmax bounds
     float* m_ce = m_lse + kMetaRows;
+    float* redbuf = m_ce + kMetaRows;  // pass A: per-warp [32][kRedPitch]
     const int tid = static_cast<int>(threadIdx.x);
     const int lane = tid & 31;
-    const int64_t v0 = static_cast<int64_t>(blockIdx.x) * kBandCols;
-    const int64_t ra = static_cast<int64_t>(blockIdx.y) * kBandRows;
+    const int64_t v0 = static_cast<int64_t>(blockIdx.x) * kCols;
+    const int ra = static_cast<int>(blockIdx.y) * kBandRows;
     if (ra >= A.M) return;
-    const int64_t rb = ra + kBandRows < A.M ? ra + kBandRows : A.M;
-    const int64_t rstart = kGrad ? (ra >= 3 ? ra - 3 : 0) : ra;
-    const int nrows = static_cast<int>(rb - rstart);
+    const int rb = ra + kBandRows < A.M ? ra + kBandRows : static_cast<int>(A.M);
+    const int rstart = kGrad ? (ra >= 3 ? ra - 3 : 0) : ra;
+    const int nrows = rb - rstart;
     if (tid == 0) {
         for (int s = 0; s < kBandStages; ++s) {
             mbar_init(&full[s], 1);
@@ -269,164 +310,254 @@ __global__ void __launch_bounds__(kBandThreads) band_kernel(const BandArgs A) {
     }
     // the rows' metadata, once per CTA (off the per-row critical path)
     for (int i = tid; i <= nrows; i += kBandThreads) {
-        const int64_t r = rstart + i;
-        m_q0[i] = r < A.M ? __ldg(A.q0 + r) : INT32_MAX;
+        const int r = rstart + i;
+        m_q0[i] = r < A.M ? __ldg(A.q0 + r) : INT32_MAX - 8;
         if (i < nrows) {
             m_act[i] = __ldg(A.action + r);
             m_rs[i] = __ldg(A.rscale + r);
             if constexpr (kGrad) {
                 m_lse[i] = __ldg(A.lse + r);
                 m_ce[i] = __ldg(A.coef_eff + r);
+            } else {
+                m_lse[i] = __ldg(A.mrow + r);
             }
         }
     }
     __syncthreads();
-    const int64_t qa = m_q0[0];
-    const int64_t qb = static_cast<int64_t>(m_q0[nrows - 1]) + 4;
-    const int nq = static_cast<int>(qb - qa);
+    const int qa = m_q0[0];
+    const int qb = m_q0[nrows - 1] + 4;
+    const int nq = qb - qa;
 
-    if (tid >= kBandConsumers) {
+    // warp-uniform role split (the broadcast tells the compiler so: no divergent
+    // shuffle fallbacks in the consumers)
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+    if (warp >= kBandConsumers / 32) {
         // ===== producer warp: lane 0 streams the positions' W16^T row slices; the
         // positions' features are fetched 32 at a time, one group ahead =====
-        const int64_t cols = A.ldw - v0 < kBandCols ? A.ldw - v0 : kBandCols;
+        const int64_t cols = A.ldw - v0 < kCols ? A.ldw - v0 : kCols;
         const uint32_t bytes = static_cast<uint32_t>(cols) * 2u;
         const __nv_bfloat16* base = A.w16t + v0;
         int32_t f_next = lane < nq ? __ldg(A.pos_feat + qa + lane) : -1;
+        int st = 0;
+        uint32_t ph = 0;
         for (int k0 = 0; k0 < nq; k0 += 32) {
             const int32_t f_cur = f_next;
             f_next = k0 + 32 + lane < nq ? __ldg(A.pos_feat + qa + k0 + 32 + lane) : -1;
             const int kn = nq - k0 < 32 ? nq - k0 : 32;
             for (int j = 0; j < kn; ++j) {
-                const int k = k0 + j;
-                const int st = k % kBandStages;
-                if (k >= kBandStages) mbar_wait(&empty[st], static_cast<uint32_t>((k / kBandStages) - 1) & 1u);
+                if (k0 + j >= kBandStages) mbar_wait(&empty[st], ph ^ 1u);
                 const int32_t f = __shfl_sync(0xffffffffu, f_cur, j);
                 if (lane == 0) {
                     // a position before the sequence start reads the zero row
                     const __nv_bfloat16* src = f >= 0 ? base + static_cast<int64_t>(f) * A.ldw : A.zero_row;
                     mbar_arrive_expect_tx(&full[st], bytes);
-                    bulk_load(ring[st], src, bytes, &full[st]);
+                    bulk_load(ring + st * kStage, src, bytes, &full[st]);
                 }
                 __syncwarp();
+                if (++st == kBandStages) {
+                    st = 0;
+                    ph ^= 1u;
+                }
             }
         }
         return;
     }
 
-    // ===== consumers =====
-    const int warp = tid >> 5;
-    const int64_t c0 = v0 + static_cast<int64_t>(tid) * 8;
-    const int nvalid = A.V - c0 >= 8 ? 8 : (A.V - c0 > 0 ? static_cast<int>(A.V - c0) : 0);
-    const int tile = static_cast<int>(blockIdx.x) * (kBandCols / 256) + warp;
-    float xr[4][8];
-    float acc[4][8];
+    // ===== consumers: lane = kV runs of 8 consecutive columns, as fp32 pairs =====
+    // run i of lane l covers columns v0 + (i * kBandConsumers + tid) * 8 .. + 8, so every
+    // shared-memory read of the warp is 512 contiguous bytes
+    int nv[kV];   // valid columns of each run (8, or fewer at the vocabulary's end)
+    int64_t cb[kV];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < kV; ++i) {
+        cb[i] = v0 + (static_cast<int64_t>(i) * kBandConsumers + tid) * 8;
+        nv[i] = A.V - cb[i] >= 8 ? 8 : (A.V - cb[i] > 0 ? static_cast<int>(A.V - cb[i]) : 0);
+    }
+    bool full_lane = true;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            xr[i][j] = 0.f;
-            acc[i][j] = 0.f;
+    for (int i = 0; i < kV; ++i) full_lane = full_lane && nv[i] == 8;
+    const bool warp_full = __all_sync(0xffffffffu, full_lane);
+    const int tile = static_cast<int>(blockIdx.x) * (kBandConsumers / 32) + warp;  // the warp's stats column
+    // per position q: xp = X[q-1] (previous position's row), pr[q & 3] = X[q-1] + X[q];
+    // the row ending at q sums pr[(q-2) & 3] + pr[q & 3] = X[q-3] + X[q-2] + X[q-1] + X[q]
+    float2 xp[kP], pr[4][kP], gr[4][kP];
+#pragma unroll
+    for (int j = 0; j < kP; ++j) {
+        xp[j] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            pr[i][j] = make_float2(0.f, 0.f);
+            if constexpr (kGrad) gr[i][j] = make_float2(0.f, 0.f);
         }
-    int ri = 0;                  // next row (index into the metadata)
-    int64_t next_end = qa + 3;   // its last position
-    int64_t elo = 0, ehi = 0;
+    }
+    int ri = 0;            // next row (index into the metadata)
+    int next_end = qa + 3; // its last position
+    int st = 0;
+    uint32_t ph = 0;
+    int elo = 0, ehi = 0;
     // pass B: slots of the positions being flushed, 32 at a time (one group ahead)
-    int64_t sg = 0;
+    int sg = 0;
     int32_t s_cur = -1, s_next = -1;
     if constexpr (kGrad) {
         elo = m_q0[ra - rstart];
-        ehi = rb < A.M ? static_cast<int64_t>(m_q0[nrows]) : qb;
-        sg = elo & ~static_cast<int64_t>(31);
+        ehi = rb < A.M ? m_q0[nrows] : qb;
+        sg = elo & ~31;
         s_cur = sg + lane < qb ? __ldg(A.pos_slot + sg + lane) : -1;
         s_next = sg + 32 + lane < qb ? __ldg(A.pos_slot + sg + 32 + lane) : -1;
     }
-
-    auto row = [&](int i, int64_t rr) {
-        const float rs = m_rs[i];
-        const int act = m_act[i];
-        float z[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) z[j] = rs * ((xr[0][j] + xr[1][j]) + (xr[2][j] + xr[3][j]));
-        if constexpr (!kGrad) {
-            float mx = -INFINITY;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if (j < nvalid) mx = fmaxf(mx, z[j]);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            float sum = 0.f;
-            if (mx != -INFINITY) {
-                const float mo = mx * kLog2e;
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (j < nvalid) sum += exp2f(fmaf(z[j], kLog2e, -mo));
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-            if (lane == 0 && mx != -INFINITY) A.stats[rr * A.stats_ld + tile] = make_float2(mx, sum);
-            if (act >= c0 && act < c0 + nvalid) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    if (act - c0 == j) A.zact[rr] = z[j];
-            }
-        } else {
-            const float ce = m_ce[i];
-            if (ce != 0.f) {  // zero-advantage rows contribute nothing (training.hpp:394)
-                const float lo = m_lse[i] * kLog2e;
-                float g[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) g[j] = j < nvalid ? -ce * exp2f(fmaf(z[j], kLog2e, -lo)) : 0.f;
-                if (act >= c0 && act < c0 + nvalid) {
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        if (act - c0 == j) g[j] += ce;
-                }
-#pragma unroll
-                for (int i2 = 0; i2 < 4; ++i2)
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[i2][j] += g[j];
-            }
-        }
+    auto valid = [&](int j, int h) {  // element 2j + h of the lane's pairs
+        return warp_full || 2 * (j & 3) + h < nv[j >> 2];
     };
 
     // one position step; S = q & 3 is static so the rings stay in registers
-    auto step = [&](int64_t q, auto Sc) {
+    auto step = [&](int q, auto Sc) {
         constexpr int S = decltype(Sc)::value;
         if (q >= qa && q < qb) {
-            const int k = static_cast<int>(q - qa);
-            const int st = k % kBandStages;
-            mbar_wait(&full[st], static_cast<uint32_t>(k / kBandStages) & 1u);
-            const uint4 u = *reinterpret_cast<const uint4*>(&ring[st][tid * 16]);
+            mbar_wait(&full[st], ph);
+            uint4 u[kV];
+#pragma unroll
+            for (int i = 0; i < kV; ++i)
+                u[i] = *reinterpret_cast<const uint4*>(ring + st * kStage + (i * kBandConsumers + tid) * 16);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
-            unpack8(u, xr[S]);
-            if constexpr (kGrad) {
+            if (++st == kBandStages) {
+                st = 0;
+                ph ^= 1u;
+            }
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[S][j] = 0.f;
+            for (int i = 0; i < kV; ++i) {
+                float2 x[4];
+                unpack8(u[i], x);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    pr[S][4 * i + j] = __fadd2_rn(xp[4 * i + j], x[j]);
+                    xp[4 * i + j] = x[j];
+                }
             }
             if (q == next_end) {  // the row whose four positions end here
-                row(ri, rstart + ri);
+                const int i = ri;
+                const float rs = m_rs[i];
+                const int act = m_act[i];
+                float2 z4[kP];  // sum of the row's four position rows
+#pragma unroll
+                for (int j = 0; j < kP; ++j) z4[j] = __fadd2_rn(pr[(S + 2) & 3][j], pr[S][j]);
+                const float c = rs * kLog2e;  // z = rs * z4 (rs >= 0), exponents in base 2
+                if constexpr (!kGrad) {
+                    // partial sum of exp(z - mrow) over the lane's columns (mrow >= every z of
+                    // the row: no max reduction), parked in shared memory; every 32 rows the
+                    // warp transposes them and lane l adds up row l's 32 lane partials
+                    const float2 cc = make_float2(c, c);
+                    const float lo = -m_lse[i] * kLog2e;
+                    const float2 off = make_float2(lo, lo);
+                    float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int j = 0; j < kP; ++j) {
+                        const float2 y = __ffma2_rn(z4[j], cc, off);
+                        float2 e = make_float2(ex2(y.x), ex2(y.y));
+                        if (!warp_full) {
+                            if (!valid(j, 0)) e.x = 0.f;
+                            if (!valid(j, 1)) e.y = 0.f;
+                        }
+                        s2 = __fadd2_rn(s2, e);
+                    }
+                    float* rb_w = redbuf + warp * 32 * kRedPitch;
+                    rb_w[(i & 31) * kRedPitch + lane] = s2.x + s2.y;
+                    const int rr = rstart + i;
+#pragma unroll
+                    for (int r2 = 0; r2 < kV; ++r2) {
+                        const int64_t d = act - cb[r2];
+                        if (d >= 0 && d < nv[r2]) {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                if (d == 2 * j) A.zact[rr] = rs * z4[4 * r2 + j].x;
+                                if (d == 2 * j + 1) A.zact[rr] = rs * z4[4 * r2 + j].y;
+                            }
+                        }
+                    }
+                    if ((i & 31) == 31 || i == nrows - 1) {
+                        __syncwarp();
+                        const int i0 = i & ~31;
+                        if (i0 + lane <= i) {
+                            const float* src = rb_w + lane * kRedPitch;
+                            float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+#pragma unroll
+                            for (int k = 0; k < 32; k += 4) {
+                                t0 += src[k];
+                                t1 += src[k + 1];
+                                t2 += src[k + 2];
+                                t3 += src[k + 3];
+                            }
+                            A.stats[static_cast<int64_t>(tile) * A.ld_stats + rstart + i0 + lane] = (t0 + t1) + (t2 + t3);
+                        }
+                        __syncwarp();
+                    }
+                } else {
+                    const float ce = m_ce[i];
+                    // g = ce (delta(v, a) - exp(z - lse)); zero-advantage rows give 0 (training.hpp:394)
+                    const float2 cc = make_float2(c, c);
+                    const float lo = -m_lse[i] * kLog2e;
+                    const float2 off = make_float2(lo, lo), nce = make_float2(-ce, -ce);
+#pragma unroll
+                    for (int j = 0; j < kP; ++j) {
+                        const float2 y = __ffma2_rn(z4[j], cc, off);
+                        float2 g = __fmul2_rn(make_float2(ex2(y.x), ex2(y.y)), nce);
+                        if (!warp_full) {
+                            if (!valid(j, 0)) g.x = 0.f;
+                            if (!valid(j, 1)) g.y = 0.f;
+                        }
+                        gr[S][j] = g;
+                    }
+#pragma unroll
+                    for (int r2 = 0; r2 < kV; ++r2) {
+                        const int64_t d = act - cb[r2];
+                        if (d >= 0 && d < nv[r2]) {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                if (d == 2 * j) gr[S][4 * r2 + j].x += ce;
+                                if (d == 2 * j + 1) gr[S][4 * r2 + j].y += ce;
+                            }
+                        }
+                    }
+                }
                 ++ri;
-                next_end = static_cast<int64_t>(m_q0[ri]) + 3;  // INT32_MAX + 3 past the last row
+                next_end = m_q0[ri] + 3;
+            } else if constexpr (kGrad) {
+#pragma unroll
+                for (int j = 0; j < kP; ++j) gr[S][j] = make_float2(0.f, 0.f);  // no row ends here
             }
+        } else if constexpr (kGrad) {
+#pragma unroll
+            for (int j = 0; j < kP; ++j) gr[S][j] = make_float2(0.f, 0.f);  // past the last position
         }
         if constexpr (kGrad) {
-            // position q - 3 has all its rows now (a later row starts at >= q - 2)
-            const int64_t p = q - 3;
+            // position p = q - 3 is touched exactly by the rows ending at p .. p + 3: the
+            // four g-ring slots.  H[p] = their sum.
+            const int p = q - 3;
             if (p >= elo && p < ehi) {
                 if (p >= sg + 32) {  // next group of slots (warp-uniform)
                     sg += 32;
                     s_cur = s_next;
                     s_next = sg + 32 + lane < qb ? __ldg(A.pos_slot + sg + 32 + lane) : -1;
                 }
-                const int32_t sl = __shfl_sync(0xffffffffu, s_cur, static_cast<int>(p - sg));
-                if (sl >= 0 && nvalid > 0)
-                    *reinterpret_cast<uint4*>(A.aseg + static_cast<int64_t>(sl) * A.ld_a + c0) = pack8(acc[(S + 1) & 3]);
+                const int32_t sl = __shfl_sync(0xffffffffu, s_cur, p - sg);
+                if (sl >= 0) {
+#pragma unroll
+                    for (int i = 0; i < kV; ++i) {
+                        if (nv[i] > 0) {
+                            float2 h[4];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                h[j] = __fadd2_rn(__fadd2_rn(gr[0][4 * i + j], gr[1][4 * i + j]),
+                                                  __fadd2_rn(gr[2][4 * i + j], gr[3][4 * i + j]));
+                            *reinterpret_cast<uint4*>(A.aseg + static_cast<int64_t>(sl) * A.ld_a + cb[i]) = pack8(h);
+                        }
+                    }
+                }
             }
         }
     };
-    const int64_t qend = kGrad ? qb + 3 : qb;
-    for (int64_t qq = qa & ~static_cast<int64_t>(3); qq < qend; qq += 4) {
+    const int qend = kGrad ? qb + 3 : qb;
+    for (int qq = qa & ~3; qq < qend; qq += 4) {
         step(qq, std::integral_constant<int, 0>{});
         step(qq + 1, std::integral_constant<int, 1>{});
         step(qq + 2, std::integral_constant<int, 2>{});
@@ -444,6 +575,12 @@ cudaError_t launch_positions(const uint8_t* arena, const SampleDesc* sd, int n_s
     return cudaGetLastError();
 }
 
+cudaError_t launch_fmax(const __nv_bfloat16* w16t, int64_t D, int64_t V, int64_t ldw, float* fmax, cudaStream_t s) {
+    if (D == 0) return cudaSuccess;
+    fmax_kernel<<<static_cast<unsigned>(D), 256, 0, s>>>(w16t, V, ldw, fmax);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pslots(const int32_t* feat, int64_t Q, int nblk, int32_t* kcount, int32_t* kseg_off, int32_t* kiters,
                           int32_t* slot, __nv_bfloat16* bseg, int64_t bseg_rows, unsigned long long* rows_acc,
                           cudaStream_t s) {
@@ -458,15 +595,24 @@ cudaError_t launch_pslots(const int32_t* feat, int64_t Q, int nblk, int32_t* kco
     return cudaGetLastError();
 }
 
+int band_stats_ld(int64_t V) {
+    const int64_t cols = kBandConsumers * 8 * kStatsV;
+    return static_cast<int>((V + cols - 1) / cols) * (kBandConsumers / 32);
+}
+
 cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s) {
     if (A.M <= 0) return cudaSuccess;
-    const dim3 grid(static_cast<unsigned>((A.V + kBandCols - 1) / kBandCols),
-                    static_cast<unsigned>((A.M + kBandRows - 1) / kBandRows));
-    auto k = grad ? band_kernel<true> : band_kernel<false>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kBandSmem));
-    if (e != cudaSuccess) return e;
-    k<<<grid, kBandThreads, kBandSmem, s>>>(A);
-    return cudaGetLastError();
+    if (A.M + 3 * A.M >= INT32_MAX - 16) return cudaErrorInvalidValue;  // positions are int32
+    auto go = [&](auto kern, int cols, size_t smem) {
+        const dim3 grid(static_cast<unsigned>((A.V + cols - 1) / cols),
+                        static_cast<unsigned>((A.M + kBandRows - 1) / kBandRows));
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        kern<<<grid, kBandThreads, smem, s>>>(A);
+        return cudaGetLastError();
+    };
+    if (grad) return go(band_kernel<true, kGradV, 2>, kBandConsumers * 8 * kGradV, band_smem_bytes<true, kGradV>());
+    return go(band_kernel<false, kStatsV, 2>, kBandConsumers * 8 * kStatsV, band_smem_bytes<false, kStatsV>());
 }
 
 }  // namespace fm

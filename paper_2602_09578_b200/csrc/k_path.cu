@@ -15,7 +15,6 @@
 #include <cstdint>
 
 #include "fm_kernels.h"
-#include "fm_lse.cuh"
 #include "fm_ptx.cuh"
 
 namespace fm {
@@ -75,7 +74,7 @@ constexpr int kMaxSamplesSmem = 1024;
 __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__ arena,
                                                      const SampleDesc* __restrict__ sd, int n_samples,
                                                      int64_t row_lo, int64_t M, int64_t Mpad, int64_t G,
-                                                     RowBuffers rows) {
+                                                     uint64_t D, RowBuffers rows) {
     __shared__ int64_t s_start[kMaxSamplesSmem];
     const bool in_smem = n_samples <= kMaxSamplesSmem;  // larger micro-batches search global memory
     if (in_smem)
@@ -101,6 +100,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
         rows.sample[r] = -1;
         rows.coef[r] = 0.f;
         rows.rscale[r] = 0.f;
+        if (rows.fmax) rows.mrow[r] = 0.f;
         return;
     }
     const int64_t gr = row_lo + r;
@@ -125,7 +125,19 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
     rows.n_ctx[r] = n;
     rows.sample[r] = lo;
     rows.coef[r] = n ? static_cast<float>(-d.adv / (static_cast<double>(G) * static_cast<double>(n))) : 0.f;
-    rows.rscale[r] = n ? static_cast<float>(1.0 / static_cast<double>(n)) : 0.f;
+    const float rs = n ? static_cast<float>(1.0 / static_cast<double>(n)) : 0.f;
+    rows.rscale[r] = rs;
+    if (rows.fmax) {
+        // softmax bound of the row, summed in K-stats' order over its four positions (the
+        // first 4 - n are empty): fp32 addition is monotone, so mrow >= every logit
+        float fm[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int j = k - (4 - n);
+            fm[k] = j >= 0 ? __ldg(rows.fmax + feature_of(ctx[j], D)) : 0.f;
+        }
+        rows.mrow[r] = rs * ((fm[0] + fm[1]) + (fm[2] + fm[3]));
+    }
     if (rows.q0) {
         // band formulation (k_band.cu): every sample overlapping the shard owns its rows + 3
         // positions; this row's four context positions start at q0
@@ -138,15 +150,51 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
 // ---------------------------------------------------------------------------
 // K-lse
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) lse_kernel(LseArgs L) {
-    // Four rows per warp (8 lanes per row, fm_lse.cuh), persistent over row quads.
-    // The kernel is latency/issue bound (1 KB of partials per row at C2).
+// One lane per row: the partial sums of the row's vocabulary slices are
+// [stats_ld][Mpad], so a warp's 32 rows read 128 contiguous bytes per slice.
+__global__ void __launch_bounds__(256) lse_kernel(const LseArgs L) {
     __shared__ double red[8];
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     double loss = 0.0;
-    for (int64_t r0 = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 4; r0 < L.Mpad;
-         r0 += nwarps * 4)
-        loss += lse_row_quad(L, r0);
+    if (r < L.Mpad) {
+        const RowBuffers& rows = L.rows;
+        if (r >= L.M) {  // padding rows
+            rows.lse[r] = 0.f;
+            rows.logp[r] = 0.f;
+            rows.coef_eff[r] = 0.f;
+        } else {
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+            int t = 0;
+            for (; t + 4 <= L.stats_ld; t += 4) {
+                s0 += __ldg(L.stats + static_cast<int64_t>(t) * L.Mpad + r);
+                s1 += __ldg(L.stats + static_cast<int64_t>(t + 1) * L.Mpad + r);
+                s2 += __ldg(L.stats + static_cast<int64_t>(t + 2) * L.Mpad + r);
+                s3 += __ldg(L.stats + static_cast<int64_t>(t + 3) * L.Mpad + r);
+            }
+            for (; t < L.stats_ld; ++t) s0 += __ldg(L.stats + static_cast<int64_t>(t) * L.Mpad + r);
+            const float sum = (s0 + s1) + (s2 + s3);
+            const int a = rows.action[r];
+            const double adv = L.sd[rows.sample[r]].adv;
+            const float lse = rows.mrow[r] + __logf(sum);
+            const bool valid = a >= 0 && a < L.V;
+            const float lp = valid ? L.zact[r] - lse : 0.f;  // policy.hpp:72-75, fp32 logit
+            float ce = rows.coef[r];
+            if (L.old_logp && L.clip_eps > 0.f) {
+                // PPO clipped-ratio surrogate min(rho*A, clip(rho,1-e,1+e)*A): the
+                // gradient flows (scaled by rho) only through the unclipped branch.
+                const float rho = __expf(lp - L.old_logp[L.row_lo + r]);
+                const bool active = adv >= 0.0 ? rho <= 1.f + L.clip_eps : rho >= 1.f - L.clip_eps;
+                ce = active ? ce * rho : 0.f;
+            }
+            rows.lse[r] = lse;
+            rows.logp[r] = lp;
+            rows.coef_eff[r] = ce;
+            loss = valid ? -(adv / static_cast<double>(L.G)) * static_cast<double>(lp) : 0.0;
+            // the bound keeps sum >= exp(max z - mrow); a vanishing sum would mean the bound
+            // overshot the logits by ~87: report NaN rather than a silently wrong gradient
+            if (!(sum >= 1e-30f) || !isfinite(sum)) loss = __longlong_as_double(0x7ff8000000000000ll);
+        }
+    }
     if (L.loss_acc) {
         const double tot = block_sum(loss, red);
         if (threadIdx.x == 0 && tot != 0.0) atomicAdd(L.loss_acc, tot);
@@ -508,10 +556,9 @@ __global__ void parity_fold_kernel(double* __restrict__ dW, double* __restrict__
 // ---------------------------------------------------------------------------
 cudaError_t launch_gather(const uint8_t* arena, const SampleDesc* sd, int n_samples, int64_t row_lo, int64_t M,
                           int64_t Mpad, int64_t global_batch, uint64_t D, RowBuffers rows, cudaStream_t s) {
-    (void)D;
     if (Mpad == 0) return cudaSuccess;
     const int blocks = static_cast<int>((Mpad + 255) / 256);
-    gather_kernel<<<blocks, 256, 0, s>>>(arena, sd, n_samples, row_lo, M, Mpad, global_batch, rows);
+    gather_kernel<<<blocks, 256, 0, s>>>(arena, sd, n_samples, row_lo, M, Mpad, global_batch, D, rows);
     return cudaGetLastError();
 }
 
@@ -539,9 +586,7 @@ cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D,
 
 cudaError_t launch_lse(const LseArgs& L, cudaStream_t s) {
     if (L.Mpad == 0) return cudaSuccess;
-    int64_t blocks = (L.Mpad * 8 + 255) / 256;  // 4 rows per warp
-    if (blocks > 148 * 4) blocks = 148 * 4;     // persistent warps: 4 resident 256-thread blocks per SM
-    lse_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(L);
+    lse_kernel<<<static_cast<unsigned>((L.Mpad + 255) / 256), 256, 0, s>>>(L);
     return cudaGetLastError();
 }
 
