@@ -132,6 +132,8 @@ int fm_agent_read_weights(fm_agent* a, double* W_out);
 int fm_agent_read_moments(fm_agent* a, float* m_out, float* v_out, int64_t* step_out);
 /* gradient accumulator (V*D, as f64) — the reduced -1/G * sum term of training.hpp:444-446 */
 int fm_agent_read_grad(fm_agent* a, double* g_out);
+/* the same, as the device holds it (fp32, tensor-core agents): V*D floats, half the host memory */
+int fm_agent_read_grad_f32(fm_agent* a, float* g_out);
 /* selected feature columns of the gradient accumulator, [V][n_cols] row-major as f64
  * (parity tooling at full V x D, where reading all V*D is host-memory heavy) */
 int fm_agent_read_grad_cols(fm_agent* a, const int64_t* cols, int64_t n_cols, double* g_out);

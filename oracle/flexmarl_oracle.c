@@ -444,3 +444,260 @@ int64_t fmo_sparse_grad(uint64_t V, uint64_t D, uint64_t seed, int n_samples, co
     free(term);
     return nc;
 }
+
+
+/* ---------------------------------------------------------------------------
+ * Full-size gradient of one global step, multi-threaded (TEST INFRASTRUCTURE:
+ * the full-size parity tests' checker).  The reference's own arithmetic —
+ * training.hpp:378-395 (per-sample term over the response tokens, scaled by
+ * the advantage), 417 (micro-batch grad norm), 444-446 (canonical sum, -1/G);
+ * policy.hpp:42-51 (featurize), 54-70 (probabilities), 79-91 (gradient) —
+ * restricted, as in fmo_sparse_grad, to the non-zero features (skipping a
+ * +-0 addend never changes an IEEE sum that starts at +0), so every element
+ * is bit-identical to the dense sequential oracle (fmo_run_agent's last_grad).
+ * Parallel without changing any summation order:
+ *   pass 1, threads over tokens: each token's softmax max and denominator
+ *           (sequential over v, as policy.hpp:62-69);
+ *   pass 2, threads over vocabulary blocks: every (v, d) element is owned by
+ *           one thread, which walks the samples and tokens in order.
+ * Wt is W transposed, [D][V] f64 (a feature's weights contiguous); gradT_out
+ * is [D][V] = -(1/G) sum_s A_s term_s; mb_norm_out (nullable) gets
+ * ||sum_{s in mb} A_s term_s||_F / G per micro-batch of mb samples
+ * (training.hpp:417).  Returns 0, or -1 on allocation failure. */
+#include <pthread.h>
+
+typedef struct {
+    uint64_t V, D;
+    const double* Wt;
+    int n_samples;
+    const int* tok;           /* all sequences (prompt ++ response) back to back */
+    const int64_t* seq_off;   /* [n_samples + 1] */
+    const int64_t* prompt_n;  /* [n_samples] */
+    const int64_t* row_off;   /* [n_samples + 1]: first trained row of each sample */
+    const double* adv;
+    int64_t G;
+    int mb;
+    double* zmax;   /* [rows] */
+    double* denom;  /* [rows] */
+    double* gradT;
+    double* mbT;    /* nullable */
+    double* mb_ss;  /* [threads][n_mb] */
+    int n_mb;
+    int threads;
+} StepCtx;
+
+typedef struct {
+    StepCtx* c;
+    int id;
+} StepArg;
+
+/* phi of row t of sample s: the distinct features of its context, ascending,
+ * with their summed weights (policy.hpp:46-49: phi[tok mod D] += 1/n in
+ * context order); returns their number */
+static int row_phi(const StepCtx* c, int s, int64_t t, int64_t* f, double* w) {
+    const int* seq = c->tok + c->seq_off[s];
+    const int64_t len = c->prompt_n[s] + t, n = len < 4 ? len : 4;
+    int nf = 0;
+    if (n == 0) return 0;
+    const double wt = 1.0 / (double)n;
+    for (int64_t i = len - n; i < len; ++i) {
+        const int64_t d = (int64_t)((uint64_t)(int64_t)seq[i] % c->D);
+        int k = 0;
+        while (k < nf && f[k] != d) ++k;
+        if (k == nf) {
+            f[nf] = d;
+            w[nf] = 0.0;
+            ++nf;
+        }
+        w[k] += wt;
+    }
+    for (int a = 1; a < nf; ++a) /* ascending features (the d loop of policy.hpp:57-61) */
+        for (int b = a; b > 0 && f[b - 1] > f[b]; --b) {
+            int64_t tf = f[b];
+            f[b] = f[b - 1];
+            f[b - 1] = tf;
+            double tw = w[b];
+            w[b] = w[b - 1];
+            w[b - 1] = tw;
+        }
+    return nf;
+}
+
+static inline double row_logit(const StepCtx* c, uint64_t v, int nf, const int64_t* f, const double* w) {
+    double acc = 0.0;
+    for (int k = 0; k < nf; ++k) acc += c->Wt[(uint64_t)f[k] * c->V + v] * w[k];
+    return acc;
+}
+
+static void* step_pass1(void* p) {
+    StepArg* a = (StepArg*)p;
+    StepCtx* c = a->c;
+    const int64_t rows = c->row_off[c->n_samples];
+    int s = 0;
+    for (int64_t r = a->id; r < rows; r += c->threads) {
+        while (c->row_off[s + 1] <= r) ++s;
+        int64_t f[4];
+        double w[4];
+        const int nf = row_phi(c, s, r - c->row_off[s], f, w);
+        double zmax = row_logit(c, 0, nf, f, w);
+        for (uint64_t v = 1; v < c->V; ++v) {
+            const double z = row_logit(c, v, nf, f, w);
+            if (z > zmax) zmax = z;
+        }
+        double den = 0.0;
+        for (uint64_t v = 0; v < c->V; ++v) den += exp(row_logit(c, v, nf, f, w) - zmax);
+        c->zmax[r] = zmax;
+        c->denom[r] = den;
+    }
+    return NULL;
+}
+
+static void* step_pass2(void* p) {
+    StepArg* a = (StepArg*)p;
+    StepCtx* c = a->c;
+    const uint64_t V = c->V;
+    const uint64_t v0 = V * (uint64_t)a->id / (uint64_t)c->threads, v1 = V * (uint64_t)(a->id + 1) / (uint64_t)c->threads;
+    const uint64_t nb = v1 - v0;
+    if (nb == 0) return NULL;
+    /* the current sample's term, compacted to its touched features: [slot][nb] */
+    int64_t max_rows = 0;
+    for (int s = 0; s < c->n_samples; ++s)
+        if (c->row_off[s + 1] - c->row_off[s] > max_rows) max_rows = c->row_off[s + 1] - c->row_off[s];
+    const int64_t max_feat = 4 * max_rows + 4;
+    double* term = (double*)calloc((size_t)max_feat * nb, sizeof(double));
+    int64_t* feat_of_slot = (int64_t*)malloc((size_t)max_feat * sizeof(int64_t));
+    double* ss = c->mb_ss + (size_t)a->id * (size_t)c->n_mb;
+    for (int s = 0; s < c->n_samples; ++s) {
+        const int64_t nr = c->row_off[s + 1] - c->row_off[s];
+        int nslot = 0;
+        for (int64_t t = 0; t < nr; ++t) {
+            const int64_t r = c->row_off[s] + t;
+            int64_t f[4];
+            double w[4];
+            const int nf = row_phi(c, s, t, f, w);
+            int slot[4];
+            for (int k = 0; k < nf; ++k) {
+                int q = 0;
+                while (q < nslot && feat_of_slot[q] != f[k]) ++q;
+                if (q == nslot) {
+                    feat_of_slot[nslot++] = f[k];
+                    memset(term + (size_t)q * nb, 0, nb * sizeof(double));
+                }
+                slot[k] = q;
+            }
+            const int action = c->tok[c->seq_off[s] + c->prompt_n[s] + t];
+            const double zmax = c->zmax[r], den = c->denom[r];
+            for (uint64_t v = v0; v < v1; ++v) {
+                const double pv = exp(row_logit(c, v, nf, f, w) - zmax) / den; /* policy.hpp:62-69 */
+                const double coef = ((int)v == action ? 1.0 : 0.0) - pv;       /* policy.hpp:84-86 */
+                if (coef == 0.0) continue;
+                for (int k = 0; k < nf; ++k) term[(size_t)slot[k] * nb + (v - v0)] += coef * w[k];
+            }
+        }
+        /* term *= A; canonical sum into the gradient and the micro-batch sum */
+        const double A = c->adv[s];
+        const int k_mb = s / c->mb;
+        for (int q = 0; q < nslot; ++q) {
+            double* g = c->gradT + (uint64_t)feat_of_slot[q] * V + v0;
+            double* mbr = c->mbT ? c->mbT + (uint64_t)feat_of_slot[q] * V + v0 : NULL;
+            const double* tq = term + (size_t)q * nb;
+            for (uint64_t i = 0; i < nb; ++i) {
+                const double x = tq[i] * A;
+                g[i] += x;
+                if (mbr) mbr[i] += x;
+            }
+        }
+        if (c->mbT && (s % c->mb == c->mb - 1 || s == c->n_samples - 1)) {
+            /* micro-batch done: its sum of squares over this block, then reset */
+            double acc = 0.0;
+            for (uint64_t d = 0; d < c->D; ++d) {
+                double* mbr = c->mbT + d * V + v0;
+                for (uint64_t i = 0; i < nb; ++i) {
+                    acc += mbr[i] * mbr[i];
+                    mbr[i] = 0.0;
+                }
+            }
+            ss[k_mb] = acc;
+        }
+    }
+    free(term);
+    free(feat_of_slot);
+    return NULL;
+}
+
+int fmo_step_grad(uint64_t V, uint64_t D, const double* Wt, int n_samples, const uint8_t* payloads,
+                  const int64_t* prompt_off, const int64_t* resp_off, const double* adv, int64_t G, int mb,
+                  int threads, double* gradT_out, double* mb_norm_out) {
+    if (threads < 1) threads = 1;
+    StepCtx c;
+    memset(&c, 0, sizeof(c));
+    c.V = V;
+    c.D = D;
+    c.Wt = Wt;
+    c.n_samples = n_samples;
+    c.adv = adv;
+    c.G = G;
+    c.mb = mb > 0 ? mb : n_samples;
+    c.threads = threads;
+    int64_t* seq_off = (int64_t*)malloc((size_t)(n_samples + 1) * sizeof(int64_t));
+    int64_t* pn = (int64_t*)malloc((size_t)(n_samples + 1) * sizeof(int64_t));
+    int64_t* row_off = (int64_t*)malloc((size_t)(n_samples + 1) * sizeof(int64_t));
+    seq_off[0] = 0;
+    row_off[0] = 0;
+    for (int s = 0; s < n_samples; ++s) {
+        const uint64_t np = fmo_decode_tokens(payloads + prompt_off[s], NULL);
+        const uint64_t nr = fmo_decode_tokens(payloads + resp_off[s], NULL);
+        pn[s] = (int64_t)np;
+        seq_off[s + 1] = seq_off[s] + (int64_t)(np + nr);
+        row_off[s + 1] = row_off[s] + (int64_t)nr;
+    }
+    int* tok = (int*)malloc((size_t)(seq_off[n_samples] + 1) * sizeof(int));
+    for (int s = 0; s < n_samples; ++s) {
+        fmo_decode_tokens(payloads + prompt_off[s], tok + seq_off[s]);
+        fmo_decode_tokens(payloads + resp_off[s], tok + seq_off[s] + pn[s]);
+    }
+    const int64_t rows = row_off[n_samples];
+    c.tok = tok;
+    c.seq_off = seq_off;
+    c.prompt_n = pn;
+    c.row_off = row_off;
+    c.zmax = (double*)malloc((size_t)(rows + 1) * sizeof(double));
+    c.denom = (double*)malloc((size_t)(rows + 1) * sizeof(double));
+    c.n_mb = (n_samples + c.mb - 1) / c.mb;
+    c.mb_ss = (double*)calloc((size_t)threads * (size_t)(c.n_mb + 1), sizeof(double));
+    c.gradT = gradT_out;
+    memset(gradT_out, 0, V * D * sizeof(double));
+    c.mbT = mb_norm_out ? (double*)calloc(V * D, sizeof(double)) : NULL;
+    int rc = 0;
+    if (!c.zmax || !c.denom || !c.mb_ss || (mb_norm_out && !c.mbT)) rc = -1;
+    pthread_t* th = (pthread_t*)malloc((size_t)threads * sizeof(pthread_t));
+    StepArg* args = (StepArg*)malloc((size_t)threads * sizeof(StepArg));
+    if (rc == 0) {
+        for (int i = 0; i < threads; ++i) {
+            args[i].c = &c;
+            args[i].id = i;
+            pthread_create(&th[i], NULL, step_pass1, &args[i]);
+        }
+        for (int i = 0; i < threads; ++i) pthread_join(th[i], NULL);
+        for (int i = 0; i < threads; ++i) pthread_create(&th[i], NULL, step_pass2, &args[i]);
+        for (int i = 0; i < threads; ++i) pthread_join(th[i], NULL);
+        for (uint64_t i = 0; i < V * D; ++i) gradT_out[i] *= -1.0 / (double)G; /* training.hpp:446 */
+        if (mb_norm_out)
+            for (int k = 0; k < c.n_mb; ++k) {
+                double acc = 0.0;
+                for (int i = 0; i < threads; ++i) acc += c.mb_ss[(size_t)i * (size_t)c.n_mb + k];
+                mb_norm_out[k] = sqrt(acc) / (double)G;
+            }
+    }
+    free(th);
+    free(args);
+    free(c.mbT);
+    free(c.mb_ss);
+    free(c.zmax);
+    free(c.denom);
+    free(tok);
+    free(seq_off);
+    free(pn);
+    free(row_off);
+    return rc;
+}

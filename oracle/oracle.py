@@ -77,6 +77,8 @@ def olib() -> C.CDLL:
         L.fmo_run_agent.argtypes = [U64, U64, I64, I64, I, P, P, P, P, D, D, D, D, P, P, P, P, P, P, P]
         L.fmo_sparse_grad.restype = I64
         L.fmo_sparse_grad.argtypes = [U64, U64, U64, I, P, P, P, P, I64, I64, P, P, P]
+        L.fmo_step_grad.restype = I
+        L.fmo_step_grad.argtypes = [U64, U64, P, I, P, P, P, P, I64, I, I, P, P]
         _o = L
     return _o
 
@@ -248,6 +250,24 @@ def sparse_grad(V, D_, seed, samples, advantages, G, max_cols=4096) -> dict:
                                 _p(cols), _p(grad), _p(mbn))
     assert nc >= 0, "too many feature columns"
     return dict(cols=cols[:nc].copy(), grad=grad[:V * nc].reshape(V, nc).copy(), mb_grad_norm=float(mbn[0]))
+
+
+def step_grad(V, D_, Wt, samples, advantages, G, mb=16, threads=0, mb_norms=True) -> dict:
+    """Full-size gradient of one global step (fmo_step_grad): gradT [D][V]
+    = -(1/G) sum_s A_s term_s, bit-identical to run_agent's dense arithmetic,
+    and the per-micro-batch grad norms.  Wt = W transposed [D][V] f64."""
+    import os
+    buf, poff, roff = pack_payloads(samples)
+    adv = np.ascontiguousarray(advantages, dtype=np.float64)
+    Wt = np.ascontiguousarray(Wt, dtype=np.float64)
+    gradT = np.empty((D_, V), dtype=np.float64)
+    nmb = (len(samples) + mb - 1) // mb
+    norms = np.zeros(nmb) if mb_norms else None
+    th = threads or max(1, min(64, os.cpu_count() or 1))
+    rc = olib().fmo_step_grad(V, D_, _p(Wt), len(samples), _p(buf), _p(poff), _p(roff), _p(adv), G, mb, th,
+                              _p(gradT), _p(norms) if mb_norms else None)
+    assert rc == 0, "fmo_step_grad: allocation failed"
+    return dict(gradT=gradT, mb_grad_norms=norms)
 
 
 # ---------------------------------------------------------------------------

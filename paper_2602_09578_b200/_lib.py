@@ -78,6 +78,7 @@ _PROTOS = {
     "fm_agent_read_weights": (I, [P, P]),
     "fm_agent_read_moments": (I, [P, P, P, PI64]),
     "fm_agent_read_grad": (I, [P, P]),
+    "fm_agent_read_grad_f32": (I, [P, P]),
     "fm_agent_read_grad_cols": (I, [P, P, I64, P]),
     "fm_debug_gemm": (I, [P, P, P, I, I, I, I, I, P]),
     "fm_ctx_gemm2_rows": (I, [P, PI64, I]),

@@ -749,6 +749,21 @@ int fm_agent_read_grad(fm_agent* a, double* g) {
     FM_GUARD_END
 }
 
+int fm_agent_read_grad_f32(fm_agent* a, float* g) {
+    FM_GUARD_BEGIN
+    if (int st = check_active(a)) return st;
+    if (a->precision != FM_PRECISION_BF16_TC) return fail(FM_ERR_CONFIG_ERROR, "fp32 accumulator: tensor-core agents");
+    if (int st = set_dev(a->ctx)) return st;
+    FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
+    if (!a->dw_valid) {
+        std::fill(g, g + a->P, 0.f);
+        return FM_OK;
+    }
+    FM_CUDA(cudaMemcpy(g, a->dW, a->P * 4, cudaMemcpyDeviceToHost));
+    return FM_OK;
+    FM_GUARD_END
+}
+
 int fm_debug_gemm(fm_ctx* c, const void* A, const void* B, int a_mn, int b_mn, int M, int N, int K, float* C) {
     FM_GUARD_BEGIN
     if (!c || !A || !B || !C || M <= 0 || N <= 0 || K <= 0 || M % 8 || N % 8 || K % 8)

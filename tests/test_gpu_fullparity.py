@@ -1,0 +1,230 @@
+"""Post-update parity at the benchmark configurations, over ALL V x D.
+
+The checker is fmo_step_grad (oracle/flexmarl_oracle.c): the reference's f64
+arithmetic for one global step (training.hpp:378-395, 417, 444-446;
+policy.hpp:42-91), bit-identical to the dense sequential restatement
+(tests/test_oracle.py pins it) and multi-threaded over tokens / vocabulary
+blocks without changing any summation order, so a full C2 step (64 x 1,024
+tokens at V=32,000, D=4,096) is seconds of host time.  Adam is the oracle's
+fmo_adam_step (training.hpp:37-51).
+
+  * C2: two full global steps through the default path (4 micro-batches of
+    16 x 1,024 tokens each, K-stats / K-band / segmented K-GEMM2, K-adam with
+    the fused update-and-park and a device-tier swap-in between the steps):
+    every step's gradient, the micro-batch and update grad norms, and after the
+    two steps delta-W, m and v over all 131M parameters.
+  * C3 (V=32,000, D=32,768) and C5 (V=128,000, D=8,192), 1.05B parameters:
+    one full global step (C3) / one full 16 x 4,096-token micro-batch (C5):
+    the whole gradient and the grad norms, and delta-W of the update.
+
+Contract (BF16_TC, SURVEY.md §8c / DESIGN.md §6): gradient rel-Frobenius
+<= 2e-2 and cosine >= 0.999; grad norms rel <= 2e-2; delta-W rel-Frobenius
+<= 5e-2 with <= 1% of elements off by more than 0.5 * lr * steps (Adam
+amplifies a sign flip of a near-zero gradient element to 2 * lr); m, v
+rel-Frobenius <= 5e-2.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_2602_09578_b200 import _lib
+from paper_2602_09578_b200 import workload as wl
+from paper_2602_09578_b200.engine import TrainingEngine, agent_seed, seeded_weights
+
+pytestmark = pytest.mark.gpu
+LR, B1, B2, EPS = 1e-6, 0.9, 0.999, 1e-8
+
+
+def _host_gb():
+    try:
+        import psutil
+        return psutil.virtual_memory().available / 2**30
+    except Exception:
+        return 0.0
+
+
+def rel_fro(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def cosine(a, b):
+    return float(np.vdot(a, b) / (np.linalg.norm(a) * np.linalg.norm(b)))
+
+
+def _with_advantages(samples):
+    """GRPO advantages per group of the reference (training.hpp:54-67), f64."""
+    off = wl.group_offsets(samples)
+    r = np.array([s.reward for s in samples])
+    for a, b in zip(off[:-1], off[1:]):
+        for s, x in zip(samples[a:b], orc.group_advantages(r[a:b])):
+            s.advantage = float(x)
+    return samples
+
+
+def _gpu_step(ctx, h, samples, G, mb):
+    L = _lib.lib()
+    tickets = []
+    for k in range(0, len(samples), mb):
+        b = samples[k:k + mb]
+        arr = (_lib.fm_sample * len(b))(*[_lib.fm_sample(ctx.put(x.prompt_payload), ctx.put(x.response_payload),
+                                                         x.advantage) for x in b])
+        t = C.c_int64()
+        _lib.check(L.fm_train_micro_batch(h, arr, len(b), G, C.byref(t)))
+        tickets.append(t.value)
+    _lib.check(L.fm_agent_sync(h))
+    norms = []
+    for t in tickets:
+        rep = _lib.fm_report()
+        assert L.fm_agent_poll_report(h, t, C.byref(rep)) == 1
+        norms.append(rep.grad_norm)
+    return np.array(norms)
+
+
+def _read_grad(h, V, D):
+    g = np.empty(V * D, dtype=np.float32)
+    _lib.check(_lib.lib().fm_agent_read_grad_f32(h, g.ctypes.data))
+    return g.reshape(V, D)
+
+
+def _check_grad(g, gradT, label):
+    """GPU fp32 gradient [V][D] vs the oracle's [D][V], column blocks at a time."""
+    V, D = g.shape
+    num = den = dot = ng = 0.0
+    for d0 in range(0, D, 1024):
+        ref = gradT[d0:d0 + 1024].T.astype(np.float64)
+        x = g[:, d0:d0 + 1024].astype(np.float64)
+        num += float(np.sum((x - ref) ** 2))
+        den += float(np.sum(ref ** 2))
+        dot += float(np.sum(x * ref))
+        ng += float(np.sum(x ** 2))
+    rel, cos = np.sqrt(num / den), dot / np.sqrt(ng * den)
+    print(f"{label}: gradient rel-Fro {rel:.3e} cos {cos:.6f}")
+    assert rel <= 2e-2
+    assert cos >= 0.999
+    return rel
+
+
+def _engine(ctx, V, D, agent):
+    eng = TrainingEngine([ctx], global_batch=64, precision=_lib.PRECISION_BF16_TC, park_tier=_lib.TIER_DEVICE)
+    eng.add_agent(agent, V, D)
+    eng.activate(agent)
+    eng.run()
+    return eng
+
+
+def test_c2_two_global_steps_match_reference(ctx):
+    if _host_gb() < 12:
+        pytest.skip("needs ~12 GB of free host memory")
+    cfg = wl.CONFIGS["C2"]
+    V, D, G, mb, agent = cfg.vocab, cfg.feat, cfg.global_batch, cfg.micro_batch, "agent0"
+    L = _lib.lib()
+    ctx.reset_arena()
+    eng = _engine(ctx, V, D, agent)
+    try:
+        h = eng.handle(agent)
+        W0 = seeded_weights(V, D, agent_seed(cfg.seed, agent)).reshape(V, D)
+        W = W0.copy()
+        m = np.zeros_like(W)
+        v = np.zeros_like(W)
+        st = 0
+        for step in range(2):
+            samples = _with_advantages(wl.step_samples(cfg, agent, step))
+            ref = orc.step_grad(V, D, np.ascontiguousarray(W.T), [(x.prompt, x.response) for x in samples],
+                                [x.advantage for x in samples], G, mb=mb)
+            norms = _gpu_step(ctx, h, samples, G, mb)
+            _check_grad(_read_grad(h, V, D), ref["gradT"], f"C2 step {step}")
+            print(f"C2 step {step}: micro-batch grad norms {norms} vs {ref['mb_grad_norms']}")
+            np.testing.assert_allclose(norms, ref["mb_grad_norms"], rtol=2e-2)
+            gn = C.c_double()
+            # the default path's update: K-adam writes the new state into the parking
+            # buffer (device tier), the next step activates it again (swap-in)
+            _lib.check(L.fm_apply_update_park(h, G, LR, B1, B2, EPS, C.byref(gn), None))
+            _lib.check(L.fm_agent_activate(h, ctx.handle))
+            g = np.ascontiguousarray(ref["gradT"].T)
+            del ref
+            st_arr = np.array([st], dtype=np.int64)
+            orc.olib().fmo_adam_step(orc._p(W), orc._p(m), orc._p(v), orc._p(st_arr), orc._p(g), W.size,
+                                     LR, B1, B2, EPS)
+            st = int(st_arr[0])
+            upd = float(np.linalg.norm(g))
+            print(f"C2 step {step}: update grad norm {gn.value:.6e} vs {upd:.6e}")
+            assert abs(gn.value - upd) <= 2e-2 * upd
+            del g
+        Wg = np.empty(V * D)
+        mg = np.empty(V * D, dtype=np.float32)
+        vg = np.empty(V * D, dtype=np.float32)
+        step_out = C.c_int64()
+        _lib.check(L.fm_agent_read_weights(h, Wg.ctypes.data))
+        _lib.check(L.fm_agent_read_moments(h, mg.ctypes.data, vg.ctypes.data, C.byref(step_out)))
+        assert step_out.value == 2 and L.fm_agent_version(h) == 2
+        dW = Wg.reshape(V, D) - W0
+        dW_ref = W - W0
+        rel = rel_fro(dW, dW_ref)
+        off = float(np.mean(np.abs(dW - dW_ref) > 0.5 * LR * 2))
+        rm = rel_fro(mg.reshape(V, D).astype(np.float64), m)
+        rv = rel_fro(vg.reshape(V, D).astype(np.float64), v)
+        print(f"C2 after 2 steps: delta-W rel-Fro {rel:.3e}, elements off {off:.2e}, m {rm:.3e}, v {rv:.3e}")
+        assert rel <= 5e-2
+        assert off <= 1e-2
+        assert rm <= 5e-2 and rv <= 5e-2
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("cfg_name", ["C3", "C5"])
+def test_1b_policy_full_step_matches_reference(ctx, cfg_name):
+    """1.05B parameters: C3 one full global step (64 x 1,024 tokens), C5 one
+    full micro-batch (16 x 4,096 tokens; a full C5 step is 4x the oracle time)."""
+    if _host_gb() < 40:
+        pytest.skip("needs ~40 GB of free host memory (1.05B-parameter f64 oracle)")
+    cfg = wl.CONFIGS[cfg_name]
+    V, D, G, mb, agent = cfg.vocab, cfg.feat, cfg.global_batch, cfg.micro_batch, "agent0"
+    n = G if cfg_name == "C3" else mb
+    L = _lib.lib()
+    ctx.reset_arena()
+    samples = _with_advantages(wl.step_samples(cfg, agent, 0))[:n]
+    W0 = seeded_weights(V, D, agent_seed(cfg.seed, agent)).reshape(V, D)
+    Wt = np.ascontiguousarray(W0.T)
+    del W0
+    ref = orc.step_grad(V, D, Wt, [(x.prompt, x.response) for x in samples], [x.advantage for x in samples], G,
+                        mb=mb)
+    del Wt
+    eng = _engine(ctx, V, D, agent)
+    try:
+        h = eng.handle(agent)
+        norms = _gpu_step(ctx, h, samples, G, mb)
+        print(f"{cfg_name}: micro-batch grad norms {norms} vs {ref['mb_grad_norms']}")
+        np.testing.assert_allclose(norms, ref["mb_grad_norms"], rtol=2e-2)
+        g = _read_grad(h, V, D)
+        _check_grad(g, ref["gradT"], cfg_name)
+        del g
+        if n < G:  # a partial step cannot be applied (IncompleteBatch); the gradient is the check
+            return
+        gn = C.c_double()
+        _lib.check(L.fm_apply_update(h, G, LR, B1, B2, EPS, C.byref(gn), None))
+        upd = float(np.sqrt(np.sum(ref["gradT"] ** 2)))
+        print(f"{cfg_name}: update grad norm {gn.value:.6e} vs {upd:.6e}")
+        assert abs(gn.value - upd) <= 2e-2 * upd
+        # one Adam step from zero moments: delta-W = -lr * g / (|g| + eps) (training.hpp:37-51)
+        Wg = np.empty(V * D)
+        _lib.check(L.fm_agent_read_weights(h, Wg.ctypes.data))
+        Wg = Wg.reshape(V, D)
+        Wg -= seeded_weights(V, D, agent_seed(cfg.seed, agent)).reshape(V, D)
+        num = den = 0.0
+        off = 0
+        for d0 in range(0, D, 1024):
+            gr = ref["gradT"][d0:d0 + 1024].T
+            dref = -LR * gr / (np.abs(gr) + EPS)
+            x = Wg[:, d0:d0 + 1024]
+            num += float(np.sum((x - dref) ** 2))
+            den += float(np.sum(dref ** 2))
+            off += int(np.count_nonzero(np.abs(x - dref) > 0.5 * LR))
+        rel, frac = np.sqrt(num / den), off / (V * D)
+        print(f"{cfg_name}: delta-W rel-Fro {rel:.3e}, elements off {frac:.2e}")
+        assert rel <= 5e-2
+        assert frac <= 1e-2
+    finally:
+        eng.close()
