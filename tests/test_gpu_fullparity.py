@@ -17,11 +17,14 @@ fmo_adam_step (training.hpp:37-51).
     one full global step (C3) / one full 16 x 4,096-token micro-batch (C5):
     the whole gradient and the grad norms, and delta-W of the update.
 
-Contract (BF16_TC, SURVEY.md §8c / DESIGN.md §6): gradient rel-Frobenius
-<= 2e-2 and cosine >= 0.999; grad norms rel <= 2e-2; delta-W rel-Frobenius
-<= 5e-2 with <= 1% of elements off by more than 0.5 * lr * steps (Adam
-amplifies a sign flip of a near-zero gradient element to 2 * lr); m, v
-rel-Frobenius <= 5e-2.
+Contract (BF16_TC at full size): gradient rel-Frobenius
+<= 1e-2 and cosine >= 0.9999; grad norms rel <= 5e-3; delta-W
+rel-Frobenius <= 2e-2 with <= 0.1% of elements off by more than
+0.5 * lr * steps (Adam amplifies a sign flip of a near-zero gradient element
+to 2 * lr); m, v rel-Frobenius <= 2e-2.  Measured on a B200
+(profiles/r02_fullparity_gpu.log): gradient 1.6-1.7e-3, norms <= 1.1e-3,
+delta-W 5.8e-3 (C3) / 8.0e-3 (C2, two steps), elements off <= 2.1e-7,
+m 1.7e-3, v 3.5e-3.
 """
 import ctypes as C
 import os
@@ -102,8 +105,8 @@ def _check_grad(g, gradT, label):
         ng += float(np.sum(x ** 2))
     rel, cos = np.sqrt(num / den), dot / np.sqrt(ng * den)
     print(f"{label}: gradient rel-Fro {rel:.3e} cos {cos:.6f}")
-    assert rel <= 2e-2
-    assert cos >= 0.999
+    assert rel <= 1e-2
+    assert cos >= 0.9999
     return rel
 
 
@@ -137,7 +140,7 @@ def test_c2_two_global_steps_match_reference(ctx):
             norms = _gpu_step(ctx, h, samples, G, mb)
             _check_grad(_read_grad(h, V, D), ref["gradT"], f"C2 step {step}")
             print(f"C2 step {step}: micro-batch grad norms {norms} vs {ref['mb_grad_norms']}")
-            np.testing.assert_allclose(norms, ref["mb_grad_norms"], rtol=2e-2)
+            np.testing.assert_allclose(norms, ref["mb_grad_norms"], rtol=5e-3)
             gn = C.c_double()
             # the default path's update: K-adam writes the new state into the parking
             # buffer (device tier), the next step activates it again (swap-in)
@@ -151,7 +154,7 @@ def test_c2_two_global_steps_match_reference(ctx):
             st = int(st_arr[0])
             upd = float(np.linalg.norm(g))
             print(f"C2 step {step}: update grad norm {gn.value:.6e} vs {upd:.6e}")
-            assert abs(gn.value - upd) <= 2e-2 * upd
+            assert abs(gn.value - upd) <= 5e-3 * upd
             del g
         Wg = np.empty(V * D)
         mg = np.empty(V * D, dtype=np.float32)
@@ -167,9 +170,9 @@ def test_c2_two_global_steps_match_reference(ctx):
         rm = rel_fro(mg.reshape(V, D).astype(np.float64), m)
         rv = rel_fro(vg.reshape(V, D).astype(np.float64), v)
         print(f"C2 after 2 steps: delta-W rel-Fro {rel:.3e}, elements off {off:.2e}, m {rm:.3e}, v {rv:.3e}")
-        assert rel <= 5e-2
-        assert off <= 1e-2
-        assert rm <= 5e-2 and rv <= 5e-2
+        assert rel <= 2e-2
+        assert off <= 1e-3
+        assert rm <= 2e-2 and rv <= 2e-2
     finally:
         eng.close()
 
@@ -197,7 +200,7 @@ def test_1b_policy_full_step_matches_reference(ctx, cfg_name):
         h = eng.handle(agent)
         norms = _gpu_step(ctx, h, samples, G, mb)
         print(f"{cfg_name}: micro-batch grad norms {norms} vs {ref['mb_grad_norms']}")
-        np.testing.assert_allclose(norms, ref["mb_grad_norms"], rtol=2e-2)
+        np.testing.assert_allclose(norms, ref["mb_grad_norms"], rtol=5e-3)
         g = _read_grad(h, V, D)
         _check_grad(g, ref["gradT"], cfg_name)
         del g
@@ -207,7 +210,7 @@ def test_1b_policy_full_step_matches_reference(ctx, cfg_name):
         _lib.check(L.fm_apply_update(h, G, LR, B1, B2, EPS, C.byref(gn), None))
         upd = float(np.sqrt(np.sum(ref["gradT"] ** 2)))
         print(f"{cfg_name}: update grad norm {gn.value:.6e} vs {upd:.6e}")
-        assert abs(gn.value - upd) <= 2e-2 * upd
+        assert abs(gn.value - upd) <= 5e-3 * upd
         # one Adam step from zero moments: delta-W = -lr * g / (|g| + eps) (training.hpp:37-51)
         Wg = np.empty(V * D)
         _lib.check(L.fm_agent_read_weights(h, Wg.ctypes.data))
@@ -224,7 +227,7 @@ def test_1b_policy_full_step_matches_reference(ctx, cfg_name):
             off += int(np.count_nonzero(np.abs(x - dref) > 0.5 * LR))
         rel, frac = np.sqrt(num / den), off / (V * D)
         print(f"{cfg_name}: delta-W rel-Fro {rel:.3e}, elements off {frac:.2e}")
-        assert rel <= 5e-2
-        assert frac <= 1e-2
+        assert rel <= 2e-2
+        assert frac <= 1e-3
     finally:
         eng.close()
