@@ -213,6 +213,10 @@ int fm_agent_read_logp(fm_agent* a, double* out, int64_t n_rows);
  * bit-exact target of the oracle's fmo_pack_rows); any pointer may be NULL. */
 int fm_debug_read_rows(fm_ctx* ctx, int64_t n_rows, int32_t* action, int32_t* ctx4,
                        int32_t* n_ctx, int32_t* sample, float* coef);
+/* Context positions of the last tensor-core micro-batch on ctx (the band
+ * formulation): each row's first position, each position's
+ * feature (tok mod D, -1 before a sequence start) and K-GEMM2 segment slot. */
+int fm_debug_read_positions(fm_ctx* ctx, int64_t n_rows, int32_t* q0, int64_t n_pos, int32_t* feat, int32_t* slot);
 /* Blocks until the agent's stream drains; completed reports become pollable. */
 int fm_agent_sync(fm_agent* a);
 /* Non-blocking: 1 and fills *out if the ticket's micro-batch has finished. */

@@ -34,7 +34,7 @@ def build(ref: bool = True) -> None:
     """Builds the restatement, and _ref when the reference sources exist."""
     targets = ["liboracle"]
     if ref and REF_INC.exists():
-        targets.append("ref")
+        targets += ["ref", "orch"]  # orch: the drop-in harness (needs the native library, built first)
     subprocess.run(["make", "-s", "-C", str(HERE), *targets], check=True)
 
 

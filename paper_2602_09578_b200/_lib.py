@@ -91,6 +91,7 @@ _PROTOS = {
     "fm_agent_set_shard": (I, [P, I, I]),
     "fm_agent_read_logp": (I, [P, P, I64]),
     "fm_debug_read_rows": (I, [P, I64, P, P, P, P, P]),
+    "fm_debug_read_positions": (I, [P, I64, P, I64, P, P]),
     "fm_agent_add_grad_keys": (I, [P, P, I]),
     "fm_agent_sync": (I, [P]),
     "fm_agent_poll_report": (I, [P, I64, C.POINTER(fm_report)]),

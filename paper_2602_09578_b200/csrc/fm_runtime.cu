@@ -1174,6 +1174,17 @@ int fm_debug_read_rows(fm_ctx* c, int64_t n, int32_t* action, int32_t* ctx4, int
     return FM_OK;
 }
 
+int fm_debug_read_positions(fm_ctx* c, int64_t n_rows, int32_t* q0, int64_t n_pos, int32_t* feat, int32_t* slot) {
+    if (int st = set_dev(c)) return st;
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    if (n_rows > c->ws.rows_cap || n_pos > c->ws.pos_cap || !c->ws.q0)
+        return fail(FM_ERR_INVALID_ARG, "more rows / positions than the workspace holds");
+    if (q0) FM_CUDA(cudaMemcpy(q0, c->ws.q0, n_rows * 4, cudaMemcpyDeviceToHost));
+    if (feat) FM_CUDA(cudaMemcpy(feat, c->ws.pos_feat, n_pos * 4, cudaMemcpyDeviceToHost));
+    if (slot) FM_CUDA(cudaMemcpy(slot, c->ws.pos_slot, n_pos * 4, cudaMemcpyDeviceToHost));
+    return FM_OK;
+}
+
 int fm_agent_sync(fm_agent* a) {
     if (!a->ctx) return FM_OK;
     if (int st = set_dev(a->ctx)) return st;

@@ -231,3 +231,69 @@ def test_1b_policy_full_step_matches_reference(ctx, cfg_name):
         assert frac <= 1e-3
     finally:
         eng.close()
+
+
+def test_c2_gather_and_positions_bit_exact(ctx):
+    """K-gather and K-pos at the C2 shape (one 16 x 1,024-token micro-batch,
+    and the same micro-batch cut into 3 DP shards): packed rows bit-exact
+    against the oracle's fmo_pack_rows; every row's first context position,
+    every position's feature and the segment slots (one per live position,
+    grouped by 256-feature block, position order inside a block) against a
+    numpy restatement of the layout."""
+    cfg = wl.CONFIGS["C2"]
+    V, D, G = cfg.vocab, cfg.feat, cfg.global_batch
+    L = _lib.lib()
+    samples = _with_advantages(wl.step_samples(cfg, "agent0", 0))[:16]
+    ctx.reset_arena()
+    for nranks in (1, 3):
+        for rank in range(nranks):
+            eng = _engine(ctx, V, D, "agent0")
+            try:
+                h = eng.handle("agent0")
+                _lib.check(L.fm_agent_set_shard(h, rank, nranks))
+                _gpu_step(ctx, h, samples, G, 16)
+                want = orc.pack_rows([(x.prompt, x.response) for x in samples], [x.advantage for x in samples], G)
+                Mt = len(want["action"])
+                lo, hi = Mt * rank // nranks, Mt * (rank + 1) // nranks
+                M = hi - lo
+                got = {k: np.zeros(M, np.int32) for k in ("action", "n_ctx", "sample")}
+                got["ctx4"] = np.zeros((M, 4), np.int32)
+                got["coef"] = np.zeros(M, np.float32)
+                _lib.check(L.fm_debug_read_rows(ctx.handle, M, got["action"].ctypes.data, got["ctx4"].ctypes.data,
+                                                got["n_ctx"].ctypes.data, got["sample"].ctypes.data,
+                                                got["coef"].ctypes.data))
+                for k in ("action", "ctx4", "n_ctx", "sample"):
+                    assert np.array_equal(got[k], want[k][lo:hi]), k
+                assert np.array_equal(got["coef"].view(np.uint32), want["coef"][lo:hi].view(np.uint32))
+                # positions: every sample overlapping the shard owns its rows + 3 positions
+                starts = np.cumsum([0] + [len(x.response) for x in samples])
+                q0_want, feat_want = [], []
+                for si, x in enumerate(samples):
+                    a, b = max(starts[si], lo), min(starts[si + 1], hi)
+                    if b <= a:
+                        continue
+                    ja, seq = a - starts[si], np.concatenate([x.prompt, x.response])
+                    base = len(feat_want)
+                    q0_want += [base + t for t in range(b - a)]
+                    for k in range(b - a + 3):
+                        sq = len(x.prompt) - 4 + ja + k
+                        feat_want.append(int(np.int64(seq[sq]) % D) if sq >= 0 else -1)
+                Q = len(feat_want)
+                q0 = np.zeros(M, np.int32)
+                feat = np.zeros(Q, np.int32)
+                slot = np.zeros(Q, np.int32)
+                _lib.check(L.fm_debug_read_positions(ctx.handle, M, q0.ctypes.data, Q, feat.ctypes.data,
+                                                     slot.ctypes.data))
+                assert np.array_equal(q0, np.array(q0_want, np.int32))
+                assert np.array_equal(feat, np.array(feat_want, np.int32))
+                fw = np.array(feat_want)
+                live = fw >= 0
+                assert np.all(slot[~live] == -1)
+                # slots: block-major, position order within a block, segments padded to 64
+                off = 0
+                for blk in range((D + 255) // 256):
+                    qs = np.nonzero(live & (fw // 256 == blk))[0]
+                    assert np.array_equal(slot[qs], off + np.arange(len(qs)))
+                    off += max(64, -(-len(qs) // 64) * 64)
+            finally:
+                eng.close()
