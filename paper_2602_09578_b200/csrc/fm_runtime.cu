@@ -656,6 +656,7 @@ int fm_agent_create(fm_ctx* c, const char* name, uint64_t V, uint64_t D, int pre
     FM_CUDA(cudaEventCreateWithFlags(&a->ev_in, cudaEventDisableTiming));
     FM_CUDA(cudaEventCreateWithFlags(&a->ev_out, cudaEventDisableTiming));
     FM_CUDA(cudaEventCreateWithFlags(&a->ev_compute, cudaEventDisableTiming));
+    a->ev_device = c->device;
     a->active = true;
     *out = a;
     return FM_OK;

@@ -258,6 +258,7 @@ struct fm_agent {
     size_t park_bytes = 0;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_compute = nullptr;
     cudaEvent_t ev_ipc = nullptr;  // interprocess: the source's work before a migration is done
+    int ev_device = -1;            // the device the agent's events were created on
     bool lent = false;             // exported by migration; slot reserved until migrate_release
     Slot* slot = nullptr;
     GangState* gang = nullptr;

@@ -105,8 +105,37 @@ int fm_agent_activate(fm_agent* a, fm_ctx* c) {
     if (!c) return fail(FM_ERR_NO_DEVICE, "null context");
     if (int st = set_dev(c)) return st;
     const size_t P = a->P;
-    // the parked copy must have landed before we read it back
+    // the parked copy must have landed before we read it back (a cross-device wait when
+    // the agent comes back on another GPU)
     FM_CUDA(cudaStreamWaitEvent(c->copy_in, a->ev_out, 0));
+    if (a->ev_device != c->device) {
+        // CUDA events can only be recorded on their own device's streams: re-create the
+        // agent's events on the new GPU once everything recorded on the old ones is done
+        for (int i = 0; i < kReportRing; ++i) FM_CUDA(cudaEventSynchronize(a->ev[i]));
+        FM_CUDA(cudaEventSynchronize(a->ev_out));
+        for (int i = 0; i < kReportRing; ++i) {
+            cudaEventDestroy(a->ev[i]);
+            FM_CUDA(cudaEventCreateWithFlags(&a->ev[i], cudaEventDisableTiming));
+        }
+        cudaEventDestroy(a->ev_in);
+        cudaEventDestroy(a->ev_out);
+        cudaEventDestroy(a->ev_compute);
+        FM_CUDA(cudaEventCreateWithFlags(&a->ev_in, cudaEventDisableTiming));
+        FM_CUDA(cudaEventCreateWithFlags(&a->ev_out, cudaEventDisableTiming));
+        FM_CUDA(cudaEventCreateWithFlags(&a->ev_compute, cudaEventDisableTiming));
+        if (a->ev_ipc) {
+            cudaEventDestroy(a->ev_ipc);
+            a->ev_ipc = nullptr;
+        }
+        // the report / update scalars the kernels write live on the agent's GPU too
+        cudaFree(a->d_scalars);
+        cudaFree(a->d_upd);
+        a->d_scalars = nullptr;
+        a->d_upd = nullptr;
+        FM_CUDA(cudaMalloc(&a->d_scalars, kReportRing * 2 * sizeof(double)));
+        FM_CUDA(cudaMalloc(&a->d_upd, sizeof(double)));
+        a->ev_device = c->device;
+    }
     // start the copy-in beside the latest queued K-stats rather than beside whatever
     // runs when it is issued: the latency-bound gather / slot kernels slowed 4x next to
     // a copy-engine burst (119 vs 28 us per micro-batch, earlier GEMM1 pipeline)

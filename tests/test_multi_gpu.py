@@ -36,3 +36,66 @@ def test_cross_process_migration():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout, r.stdout[-3000:]
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("back_on", [0, 1])
+def test_peer_tier_swap_identity(back_on):
+    """FM_TIER_PEER (training.hpp:321-350 / 259-317 with the state parked in a
+    peer GPU's HBM over NVLink, cudaMemcpyPeerAsync on the copy streams): an
+    agent with a mid-step gradient suspended from GPU 0 into GPU 1's HBM and
+    re-activated on GPU 0 or GPU 1 has a bit-identical state checksum, and the
+    next micro-batch gives the same gradient as an agent that never moved."""
+    import ctypes as C
+
+    import numpy as np
+
+    from oracle import oracle as orc
+    from paper_2602_09578_b200 import _lib
+    from paper_2602_09578_b200.engine import Context
+    L = _lib.lib()
+    V, D = 2048, 256
+    rng = np.random.default_rng(3)
+    W0 = np.ascontiguousarray(rng.normal(size=(V, D)) * 0.5)
+    batches = [[(rng.integers(0, V, size=6).astype(np.int32), rng.integers(0, V, size=40).astype(np.int32))
+                for _ in range(16)] for _ in range(2)]
+    advs = [rng.normal(size=16) for _ in range(2)]
+    ctxs = [Context(0), Context(1)]
+
+    def train(h, ctx, k):
+        arr = (_lib.fm_sample * 16)(*[_lib.fm_sample(ctx.put(orc.encode(p)), ctx.put(orc.encode(r)), a)
+                                      for (p, r), a in zip(batches[k], advs[k])])
+        t = C.c_int64()
+        _lib.check(L.fm_train_micro_batch(h, arr, 16, 64, C.byref(t)))
+
+    def checksum(h):
+        cs = C.c_uint64()
+        _lib.check(L.fm_agent_state_checksum(h, C.byref(cs)))
+        return cs.value
+
+    hs = []
+    try:
+        for name in (b"moved", b"stayed"):
+            h = C.c_void_p()
+            _lib.check(L.fm_agent_create(ctxs[0].handle, name, V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
+            _lib.check(L.fm_agent_set_weights(h, W0.ctypes.data))
+            hs.append(h)
+            train(h, ctxs[0], 0)
+        moved, stayed = hs
+        before = checksum(moved)
+        assert before == checksum(stayed)
+        _lib.check(L.fm_agent_suspend(moved, _lib.TIER_PEER, 1))
+        _lib.check(L.fm_agent_activate(moved, ctxs[back_on].handle))
+        assert checksum(moved) == before
+        train(moved, ctxs[back_on], 1)
+        train(stayed, ctxs[0], 1)
+        g_m = np.empty(V * D)
+        g_s = np.empty(V * D)
+        _lib.check(L.fm_agent_read_grad(moved, g_m.ctypes.data))
+        _lib.check(L.fm_agent_read_grad(stayed, g_s.ctypes.data))
+        np.testing.assert_array_equal(g_m, g_s)
+    finally:
+        for h in hs:
+            L.fm_agent_destroy(h)
+        for c in ctxs:
+            c.close()
