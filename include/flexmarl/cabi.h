@@ -169,7 +169,7 @@ typedef struct fm_report {
     int64_t ticket;
     int64_t tokens;
     int64_t batch_size;
-    double grad_norm; /* ||sum_mb A_i term_i|| / G (training.hpp:417); NaN under DP */
+    double grad_norm; /* ||sum_mb A_i term_i|| / G (training.hpp:417); NaN under DP unless fm_agent_set_dp_norms */
     double loss;      /* -(1/G) sum_i A_i sum_t log pi, this micro-batch */
 } fm_report;
 
@@ -311,6 +311,12 @@ int fm_group_advantages(fm_ctx* ctx, const double* rewards, const int32_t* seg_o
 int fm_comm_unique_id(uint8_t out[128]);
 int fm_comm_create(fm_ctx* ctx, const uint8_t id[128], int nranks, int rank, fm_comm** out);
 int fm_comm_destroy(fm_comm* c);
+/* Exact per-micro-batch grad norm under DP (training.hpp:417), opt-in
+ * diagnostic: each micro-batch's contribution is all-reduced over `c` (the
+ * gang's communicator) and measured, so fm_report.grad_norm is the reference's
+ * value instead of NaN.  Costs a P-float all-reduce per micro-batch.  NULL
+ * turns it off.  Collective: every rank of the gang calls it. */
+int fm_agent_set_dp_norms(fm_agent* a, fm_comm* c);
 /* Sum the agent's gradient accumulator across the gang (before fm_apply_update).
  * A no-op for agents attached with fm_gang_attach (reduced inside GEMM2). */
 int fm_agent_allreduce_grad(fm_agent* a, fm_comm* c);

@@ -110,6 +110,7 @@ _PROTOS = {
     "fm_comm_create": (I, [P, P, I, I, C.POINTER(P)]),
     "fm_comm_destroy": (I, [P]),
     "fm_agent_allreduce_grad": (I, [P, P]),
+    "fm_agent_set_dp_norms": (I, [P, P]),
     "fm_gang_attach": (I, [P, P, P, U64, PU64]),
     "fm_gang_connect": (I, [P, P, U64]),
     "fm_gang_detach": (I, [P]),

@@ -149,6 +149,11 @@ cudaError_t launch_w16t(const double* w, uint64_t V, uint64_t D, __nv_bfloat16* 
 cudaError_t launch_w16t_untranspose(const __nv_bfloat16* w16t, uint64_t V, uint64_t D, uint64_t ldw,
                                     __nv_bfloat16* out, cudaStream_t s);
 
+// dst = (accumulate ? dst : 0) + src, n floats.
+cudaError_t launch_axpy_init(float* dst, const float* src, uint64_t n, int accumulate, int num_sms, cudaStream_t s);
+// *out += sum(x^2) over n floats (fp64 accumulation).
+cudaError_t launch_sumsq(const float* x, uint64_t n, double* out, int num_sms, cudaStream_t s);
+
 cudaError_t launch_to_bf16(const double* w, __nv_bfloat16* w16, uint64_t n, int num_sms,
                            cudaStream_t s);
 

@@ -168,6 +168,7 @@ void ws_free(Workspace& w) {
     cudaFree(w.dWmb);
     cudaFree(w.logp64);
     cudaFree(w.sd);
+    cudaFree(w.dpn);
     w = Workspace{};
 }
 
@@ -190,6 +191,8 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D, int n_samples
     std::swap(keep.logp64, w.logp64);
     std::swap(keep.sd, w.sd);
     std::swap(keep.old_logp, w.old_logp);
+    std::swap(keep.dpn, w.dpn);
+    keep.dpn_cap = w.dpn_cap;
     keep.prow_cap = w.prow_cap;
     keep.pvocab_cap = w.pvocab_cap;
     keep.pparam_cap = w.pparam_cap;
@@ -872,6 +875,63 @@ int fm_agent_set_shard(fm_agent* a, int rank, int nranks) {
 }
 
 // ---------------------------------------------------------------------------
+// DP helpers
+// ---------------------------------------------------------------------------
+namespace {
+int ws_reserve_dpnorm(fm_ctx* c, uint64_t P) {
+    Workspace& w = c->ws;
+    if (w.dpn_cap >= P) return FM_OK;
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(w.dpn);
+    w.dpn = nullptr;
+    if (dalloc(&w.dpn, P)) return fail(FM_ERR_DEVICE_OOM, "DP grad-norm scratch");
+    w.dpn_cap = P;
+    return FM_OK;
+}
+
+// A gang rank's partials of the peers' rows, shipped with plain NVLink copies
+// into their receive slots, then the gang barrier.
+int gang_copy_exchange(fm_agent* a) {
+    fm_ctx* c = a->ctx;
+    cudaStream_t s = c->stream;
+    GangState* gs = a->gang;
+    if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * 4, s));
+    for (int o = 0; o < gs->g; ++o) {
+        if (o == gs->rank) continue;
+        const size_t rows_o = static_cast<size_t>(gs->lo[o + 1] - gs->lo[o]);
+        FM_CUDA(cudaMemcpyAsync(gs->peer_slot[o], static_cast<float*>(a->dW) + gs->lo[o] * a->D,
+                                rows_o * a->D * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    a->dw_valid = true;
+    return gang_barrier(a);
+}
+
+// Exact DP micro-batch grad norm: dW (+)= this rank's contribution (w.dpn), the
+// contributions summed over the ranks (NCCL all-reduce over NVLink) and their
+// sum of squares into scal[0]; then a gang's exchange if this was the step's
+// last micro-batch.
+int dp_norm_finish(fm_agent* a, double* scal, bool last) {
+    fm_ctx* c = a->ctx;
+    cudaStream_t s = c->stream;
+    Workspace& w = c->ws;
+    FM_CUDA(launch_axpy_init(static_cast<float*>(a->dW), w.dpn, a->P, a->dw_valid ? 1 : 0, c->num_sms, s));
+    a->dw_valid = true;
+    FM_NCCL(ncclAllReduce(w.dpn, w.dpn, a->P, ncclFloat32, ncclSum, a->norm_comm->comm, s));
+    FM_CUDA(launch_sumsq(w.dpn, a->P, scal, c->num_sms, s));
+    count_launch(2);
+    if (last && a->gang && a->gang->connected) return gang_copy_exchange(a);
+    return FM_OK;
+}
+}  // namespace
+
+extern "C" int fm_agent_set_dp_norms(fm_agent* a, fm_comm* comm) {
+    if (comm && comm->ctx != a->ctx) return fail(FM_ERR_CONFIG_ERROR, "communicator bound to another GPU");
+    if (comm && a->precision != FM_PRECISION_BF16_TC) return fail(FM_ERR_CONFIG_ERROR, "tensor-core agents only");
+    a->norm_comm = comm;
+    return FM_OK;
+}
+
+// ---------------------------------------------------------------------------
 // the micro-batch pipeline
 // ---------------------------------------------------------------------------
 // hsd: host descriptors (staged H2D), or dsd: descriptors already in HBM (the
@@ -1011,7 +1071,17 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g2.sumsq = scal;
             g2.kseg_off = w.kseg_off;
             g2.kseg_iters = w.kiters;
-            const bool exchange = a->gang && a->gang->connected && a->samples + n == G;
+            // exact micro-batch grad norm under DP (opt-in, fm_agent_set_dp_norms): GEMM2 writes
+            // this rank's contribution to a scratch, which is added to dW, all-reduced and
+            // measured (training.hpp:417); a gang's exchange then runs as plain copies
+            const bool dp_norms = a->norm_comm != nullptr;
+            const bool exchange = !dp_norms && a->gang && a->gang->connected && a->samples + n == G;
+            if (dp_norms) {
+                if (int st = ws_reserve_dpnorm(c, a->P)) return st;
+                g2.out = w.dpn;
+                g2.accumulate = 0;
+                g2.sumsq = nullptr;
+            }
             if (exchange) {  // last micro-batch of the step: reduce-scatter inside the epilogue
                 GangState* gs = a->gang;
                 g2.xg = gs->g;
@@ -1031,6 +1101,9 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 a->dw_valid = true;
                 if (int st = gang_barrier(a)) return st;  // every rank's partials have landed
             }
+            if (dp_norms) {
+                if (int st = dp_norm_finish(a, scal, a->samples + n == G)) return st;
+            }
             count_launch(4);
         } else {
             FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, M, G, a->D, rows, s));
@@ -1042,19 +1115,15 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             count_launch(3);
         }
         a->dw_valid = true;
+    } else if (tc && a->norm_comm) {
+        // no rows here: a zero contribution still joins the collective
+        if (int st = ws_reserve_dpnorm(c, a->P)) return st;
+        FM_CUDA(cudaMemsetAsync(w.dpn, 0, a->P * 4, s));
+        if (int st = dp_norm_finish(a, scal, a->samples + n == G)) return st;
     } else if (a->gang && a->gang->connected && a->samples + n == G) {
         // this rank got no rows of the step's last micro-batch: ship its partials
         // for the peers' rows with plain NVLink copies, then join the barrier
-        GangState* gs = a->gang;
-        if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * 4, s));
-        for (int o = 0; o < gs->g; ++o) {
-            if (o == gs->rank) continue;
-            const size_t rows_o = static_cast<size_t>(gs->lo[o + 1] - gs->lo[o]);
-            FM_CUDA(cudaMemcpyAsync(gs->peer_slot[o], static_cast<float*>(a->dW) + gs->lo[o] * a->D,
-                                    rows_o * a->D * 4, cudaMemcpyDeviceToDevice, s));
-        }
-        a->dw_valid = true;
-        if (int st = gang_barrier(a)) return st;
+        if (int st = gang_copy_exchange(a)) return st;
     }
     a->old_logp.clear();  // old log-probs apply to one micro-batch
     a->last_rows = M;
@@ -1203,7 +1272,9 @@ int fm_agent_poll_report(fm_agent* a, int64_t ticket, fm_report* out) {
     out->ticket = ticket;
     out->tokens = a->rep_tokens[slot];
     out->batch_size = a->rep_bs[slot];
-    out->grad_norm = a->dp ? NAN : std::sqrt(a->h_scalars[2 * slot]);
+    // under DP the rank's own sum of squares is not the micro-batch's: NaN unless the
+    // exact reduction is on (fm_agent_set_dp_norms)
+    out->grad_norm = (a->dp && !a->norm_comm) ? NAN : std::sqrt(a->h_scalars[2 * slot]);
     out->loss = a->h_scalars[2 * slot + 1];
     return 1;
 }

@@ -94,6 +94,8 @@ struct Workspace {
     double *zscratch = nullptr, *dWmb = nullptr, *logp64 = nullptr;
     SampleDesc* sd = nullptr;
     int sd_cap = 0;
+    float* dpn = nullptr;  // exact DP grad norm: this micro-batch's contribution [P]
+    uint64_t dpn_cap = 0;
 };
 
 // Per-kernel device timing (bench.py's roofline): event pairs recorded on the
@@ -259,6 +261,7 @@ struct fm_agent {
     cudaEvent_t ev_in = nullptr, ev_out = nullptr, ev_compute = nullptr;
     cudaEvent_t ev_ipc = nullptr;  // interprocess: the source's work before a migration is done
     int ev_device = -1;            // the device the agent's events were created on
+    fm_comm* norm_comm = nullptr;  // exact DP micro-batch grad norms over this communicator
     bool lent = false;             // exported by migration; slot reserved until migrate_release
     Slot* slot = nullptr;
     GangState* gang = nullptr;

@@ -437,6 +437,33 @@ __global__ void w16t_untranspose_kernel(const __nv_bfloat16* __restrict__ w16t, 
     }
 }
 
+__global__ void axpy_init_kernel(float* __restrict__ dst, const float* __restrict__ src, uint64_t n4, int acc) {
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 x = reinterpret_cast<const float4*>(src)[i];
+        if (acc) {
+            const float4 d = reinterpret_cast<const float4*>(dst)[i];
+            x.x += d.x;
+            x.y += d.y;
+            x.z += d.z;
+            x.w += d.w;
+        }
+        reinterpret_cast<float4*>(dst)[i] = x;
+    }
+}
+
+__global__ void sumsq_kernel(const float* __restrict__ x, uint64_t n, double* out) {
+    __shared__ double red[8];
+    double acc = 0.0;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double v = x[i];
+        acc += v * v;
+    }
+    const double tot = block_sum(acc, red);
+    if (threadIdx.x == 0) atomicAdd(out, tot);
+}
+
 __global__ void to_bf16_kernel(const double* __restrict__ w, __nv_bfloat16* __restrict__ w16, uint64_t n) {
     const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -631,6 +658,19 @@ cudaError_t launch_w16t_untranspose(const __nv_bfloat16* w16t, uint64_t V, uint6
     if (V == 0 || D == 0) return cudaSuccess;
     const dim3 grid(static_cast<unsigned>((V + 31) / 32), static_cast<unsigned>((D + 31) / 32));
     w16t_untranspose_kernel<<<grid, dim3(32, 8), 0, s>>>(w16t, V, D, ldw, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_axpy_init(float* dst, const float* src, uint64_t n, int accumulate, int num_sms, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    if (n % 4) return cudaErrorInvalidValue;
+    axpy_init_kernel<<<num_sms * 8, 256, 0, s>>>(dst, src, n / 4, accumulate);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sumsq(const float* x, uint64_t n, double* out, int num_sms, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    sumsq_kernel<<<num_sms * 8, 256, 0, s>>>(x, n, out);
     return cudaGetLastError();
 }
 

@@ -84,6 +84,8 @@ def gang_vs_allreduce(ctx, comm, rank, world) -> bool:
 
 def main():
     mode = sys.argv[1] if len(sys.argv) > 1 else "allreduce"
+    # "norms": exact per-micro-batch grad norms under DP (fm_agent_set_dp_norms)
+    exact_norms = len(sys.argv) > 2 and sys.argv[2] == "norms"
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -116,8 +118,10 @@ def main():
         _lib.check(L.fm_gang_connect(h, allb, n.value))
     else:
         _lib.check(L.fm_agent_set_shard(h, rank, world))
+    if exact_norms:
+        _lib.check(L.fm_agent_set_dp_norms(h, comm))
     po = f["poll_order"]
-    grads, norms = [], []
+    grads, norms, tickets = [], [], []
     for u in range(U):
         for b in range(G // mb):
             idx = po[u * G + b * mb: u * G + (b + 1) * mb]
@@ -126,6 +130,7 @@ def main():
                                                          float(f["adv"][i])) for i in idx])
             t = C.c_int64()
             _lib.check(L.fm_train_micro_batch(h, arr, mb, G, C.byref(t)))
+            tickets.append(t.value)
         _lib.check(L.fm_agent_allreduce_grad(h, comm))  # no-op in gang mode
         if mode == "allreduce":
             g = np.empty(V * D)
@@ -134,6 +139,13 @@ def main():
         gn = C.c_double()
         _lib.check(L.fm_apply_update(h, G, 1e-6, 0.9, 0.999, 1e-8, C.byref(gn), None))
         norms.append(gn.value)
+    _lib.check(L.fm_agent_sync(h))
+    mbn = []
+    for t in tickets:
+        rep = _lib.fm_report()
+        assert L.fm_agent_poll_report(h, t, C.byref(rep)) == 1
+        mbn.append(rep.grad_norm)
+    mbn = np.array(mbn)
     W = np.empty(V * D)
     _lib.check(L.fm_agent_read_weights(h, W.ctypes.data))
     W = W.reshape(V, D)
@@ -173,6 +185,12 @@ def main():
             e_g = rel_fro(grads[0], _oracle_grad_step0(f))
             ok = ok and e_g <= 2e-2
             msg += f", grad rel {e_g:.3e}"
+        if exact_norms:  # the reference's micro-batch grad norms (training.hpp:417), not NaN
+            e_m = float(np.max(np.abs(mbn - f["mb_grad_norm"]) / f["mb_grad_norm"]))
+            ok = ok and e_m <= 2e-2
+            msg += f", micro-batch grad-norm rel {e_m:.3e}"
+        else:
+            ok = ok and bool(np.all(np.isnan(mbn)))
         print(msg + (" -> OK" if ok else " -> FAIL"), flush=True)
     same = True
     if mode == "allreduce":  # replicas must hold identical weights after the replicated update
