@@ -39,11 +39,15 @@ struct GemmArgs {
 
 size_t gemm_smem_bytes();
 // Test hook: fp32 C = A * B^T with either operand K- or MN-major.
-cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, int a_mn, int b_mn, int M, int N,
-                              int K, float* C, int num_sms, cudaStream_t stream);
+// tmC: the output's fp32 map (make_tmap_f32_out) for the TMA reduce-add / store epilogue.
+cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, int a_mn,
+                              int b_mn, int M, int N, int K, float* C, int num_sms, cudaStream_t stream);
 // K-GEMM2 over segments (args.kseg_off / kseg_iters), MN-major tile maps.
-cudaError_t gemm_kseg_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int num_sms,
-                             cudaStream_t stream);
+cudaError_t gemm_kseg_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                             const GemmArgs& args, int num_sms, cudaStream_t stream);
+// fp32 [rows][cols] (row pitch `pitch` elements, a multiple of 4) with box {32, 32},
+// SWIZZLE_128B: the GEMM epilogue's per-warp output tile.
+bool make_tmap_f32_out(CUtensorMap* map, const float* base, uint64_t rows, uint64_t cols, uint64_t pitch);
 
 // Builds a 2-D bf16 tensor map over a row-major [rows][cols] matrix (cols
 // contiguous, row pitch `pitch` elements), box {64, box_rows}, SWIZZLE_128B.

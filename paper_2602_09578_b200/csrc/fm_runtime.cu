@@ -36,6 +36,18 @@ bool make_tmap_bf16_kmajor(CUtensorMap* map, const void* base, uint64_t rows, ui
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool make_tmap_f32_out(CUtensorMap* map, const float* base, uint64_t rows, uint64_t cols, uint64_t pitch) {
+    EncodeTiledFn f = encode_fn();
+    if (!f || (pitch & 3)) return false;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {pitch * 4};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    return f(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_tmap_gather4(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t pitch) {
     EncodeTiledFn f = encode_fn();
     if (!f) return false;
@@ -773,11 +785,12 @@ int fm_debug_gemm(fm_ctx* c, const void* A, const void* B, int a_mn, int b_mn, i
     if (!c || !A || !B || !C || M <= 0 || N <= 0 || K <= 0 || M % 8 || N % 8 || K % 8)
         return fail(FM_ERR_INVALID_ARG, "debug_gemm: bad arguments");
     if (int st = set_dev(c)) return st;
-    CUtensorMap tA, tB;
+    CUtensorMap tA, tB, tC;
     const bool ok = (a_mn ? make_tmap_bf16_kmajor(&tA, A, K, M, 64) : make_tmap_bf16_kmajor(&tA, A, M, K, 128)) &&
-                    (b_mn ? make_tmap_bf16_kmajor(&tB, B, K, N, 64) : make_tmap_bf16_kmajor(&tB, B, N, K, 128));
+                    (b_mn ? make_tmap_bf16_kmajor(&tB, B, K, N, 64) : make_tmap_bf16_kmajor(&tB, B, N, K, 128)) &&
+                    make_tmap_f32_out(&tC, C, M, N, N);
     if (!ok) return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    FM_CUDA(gemm_debug_launch(tA, tB, a_mn, b_mn, M, N, K, C, c->num_sms, c->stream));
+    FM_CUDA(gemm_debug_launch(tA, tB, tC, a_mn, b_mn, M, N, K, C, c->num_sms, c->stream));
     FM_CUDA(cudaStreamSynchronize(c->stream));
     return FM_OK;
     FM_GUARD_END
@@ -1091,11 +1104,12 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             }
             {
                 KScope k(c, K_GEMM2, s);
-                CUtensorMap tSA, tSB;
+                CUtensorMap tSA, tSB, tC;
                 if (!make_tmap_bf16_kmajor(&tSA, w.aseg, static_cast<uint64_t>(w.kp_cap), a->V, 64, ldz) ||
-                    !make_tmap_bf16_kmajor(&tSB, w.bseg, static_cast<uint64_t>(w.kp_cap), 256, 64))
+                    !make_tmap_bf16_kmajor(&tSB, w.bseg, static_cast<uint64_t>(w.kp_cap), 256, 64) ||
+                    !make_tmap_f32_out(&tC, g2.out, a->V, a->D, a->D))
                     return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-                FM_CUDA(gemm_kseg_launch(tSA, tSB, g2, c->num_sms, s));
+                FM_CUDA(gemm_kseg_launch(tSA, tSB, tC, g2, c->num_sms, s));
             }
             if (exchange) {
                 a->dw_valid = true;

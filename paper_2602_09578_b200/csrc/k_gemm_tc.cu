@@ -58,7 +58,39 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int tiles_m, int tiles_n,
 
 struct GradEpi {
     double sumsq;
-    float* xbuf = nullptr;  // per-warp 32 x 36 fp32 smem staging
+    float* xbuf = nullptr;  // per-warp 32 x 36 fp32 smem staging (exchange mode)
+    uint8_t* stage = nullptr;  // per-warp 2 x 4 KB SWIZZLE_128B staging of the TMA epilogue
+    const CUtensorMap* tmc = nullptr;
+    int nstaged = 0;
+
+    // Local rows: the warp's 32 rows x 32 columns go through shared memory (SWIZZLE_128B,
+    // the TMA map's layout) and one TMA op adds them into dW in L2 (store for the
+    // step's first micro-batch) — no SM round trip for the read-modify-write; two
+    // staging buffers, so a chunk's staging overlaps the previous chunk's TMA.
+    __device__ __forceinline__ void tma_chunk(const GemmArgs& a, int row, int col0, uint32_t (&r)[32]) {
+        const uint32_t lane = threadIdx.x & 31;
+        uint8_t* buf = stage + (nstaged & 1) * 4096;
+        if (lane == 0) tma_store_wait_read<1>();  // the op that used this buffer has read it
+        __syncwarp();
+        float part = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float4 acc = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
+                                           __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
+            part += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
+            *reinterpret_cast<float4*>(buf + lane * 128 + ((k ^ (lane & 7)) << 4)) = acc;
+        }
+        sumsq += static_cast<double>(part);  // rows / columns past the matrix hold exact zeros
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            const int row0 = row - static_cast<int>(lane);
+            if (a.accumulate) tma_reduce_add_2d(tmc, buf, col0, row0);
+            else tma_store_2d(tmc, buf, col0, row0);
+            tma_store_commit();
+        }
+        ++nstaged;
+    }
 
     // Warp-cooperative: lane = row holds 32 columns; transpose through smem so
     // each store instruction writes 4 whole 128-B rows (8 lanes x 16 B per
@@ -115,6 +147,10 @@ struct GradEpi {
                 remote_chunk(a, row, col0, r, o);
                 return;
             }
+        }
+        if (tmc) {
+            tma_chunk(a, row, col0, r);
+            return;
         }
         const int nvalid = min(32, a.N - col0);
         if (nvalid <= 0) return;  // warp-uniform
@@ -194,7 +230,7 @@ struct GradEpi {
     }
 };
 
-constexpr int P_STAGES = 6;
+constexpr int P_STAGES = 5;
 constexpr uint32_t P_A_STAGE = 128 * BK * 2;    // 16 KB: this CTA's 128 rows of A
 constexpr uint32_t P_B_STAGE = 128 * BK * 2;    // 16 KB: this CTA's half of B's 256 rows
 constexpr uint32_t P_STAGE_BYTES = P_A_STAGE + P_B_STAGE;
@@ -209,7 +245,7 @@ constexpr int kThreadsPair = 192;  // w0 TMA, w1 MMA, w2-5 epilogue
 template <bool kAmn, bool kBmn, bool kSeg>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     gemm_grad_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     GemmArgs args) {
+                     const __grid_constant__ CUtensorMap tmC, GemmArgs args) {
     static_assert(!kSeg || (kAmn && kBmn), "segment operands are MN-major");
     constexpr uint32_t kId = idesc_bf16_f32<256, BN, kAmn, kBmn>();
     extern __shared__ uint8_t smem_raw[];
@@ -223,6 +259,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     float* xscratch = reinterpret_cast<float*>(tmem_slot + 4);  // 4 warps x 32 x 36 fp32 (16-B aligned)
+    // TMA epilogue staging: 4 warps x 2 x 4 KB, 1024-B aligned (SWIZZLE_128B atoms)
+    uint8_t* tstage = smem + ((P_STAGES * P_STAGE_BYTES + 512 + 4 * 32 * 36 * 4 + 1023) & ~1023u);
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
@@ -232,6 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
+        tma_prefetch(&tmC);
         for (int s = 0; s < P_STAGES; ++s) {
             mbar_init(&full[s], 1);   // the leader's producer arrives with both CTAs' tx bytes
             mbar_init(&empty[s], 1);  // one multicast commit per consumed stage
@@ -341,6 +380,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         const uint32_t tempty_leader[2] = {mapa_shared(&tempty[0], 0), mapa_shared(&tempty[1], 0)};
         GradEpi epi;
         epi.xbuf = xscratch + quad * 32 * 36;
+        epi.stage = tstage + quad * 8192;
+        epi.tmc = &tmC;
         int acc = 0;
         uint32_t acc_phase = 0;
         double sumsq_total = 0.0;
@@ -371,6 +412,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         }
         for (int o = 16; o > 0; o >>= 1) sumsq_total += __shfl_xor_sync(0xffffffffu, sumsq_total, o);
         if (lane == 0 && args.sumsq) atomicAdd(args.sumsq, sumsq_total);
+        if (lane == 0) tma_store_wait<0>();  // every reduce / store of this warp has completed
     }
     tc_fence_before();
     cluster_sync();
@@ -381,8 +423,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
 }
 
 template <bool kAmn, bool kBmn, bool kSeg>
-cudaError_t launch_grad(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int num_sms,
-                        cudaStream_t stream) {
+cudaError_t launch_grad(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmArgs& args,
+                        int num_sms, cudaStream_t stream) {
     const size_t smem = gemm_smem_bytes();
     const int tiles = ((args.M + 255) / 256) * ((args.N + BN - 1) / BN);
     if (tiles == 0) return cudaSuccess;
@@ -391,7 +433,7 @@ cudaError_t launch_grad(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
     auto k = gemm_grad_kernel<kAmn, kBmn, kSeg>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    k<<<grid, kThreadsPair, smem, stream>>>(tmA, tmB, args);
+    k<<<grid, kThreadsPair, smem, stream>>>(tmA, tmB, tmC, args);
     return cudaGetLastError();
 }
 
@@ -400,8 +442,8 @@ cudaError_t launch_grad(const CUtensorMap& tmA, const CUtensorMap& tmB, const Ge
 // Test hook: C[M][N] (fp32, ld N) = sum_k A(m,k) B(n,k) with A / B either K-major
 // ([M][K] / [N][K]) or MN-major ([K][M] / [K][N]) — validates the MN-major UMMA
 // operand path against a plain reference (tests/test_gpu_path.py).
-cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, int a_mn, int b_mn, int M, int N,
-                              int K, float* C, int num_sms, cudaStream_t stream) {
+cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, int a_mn,
+                              int b_mn, int M, int N, int K, float* C, int num_sms, cudaStream_t stream) {
     GemmArgs args{};
     args.M = M;
     args.N = N;
@@ -409,17 +451,19 @@ cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, in
     args.group_m = 8;
     args.out = C;
     args.ld_out = N;
-    if (a_mn && b_mn) return launch_grad<true, true, false>(tmA, tmB, args, num_sms, stream);
-    if (a_mn) return launch_grad<true, false, false>(tmA, tmB, args, num_sms, stream);
-    if (b_mn) return launch_grad<false, true, false>(tmA, tmB, args, num_sms, stream);
-    return launch_grad<false, false, false>(tmA, tmB, args, num_sms, stream);
+    if (a_mn && b_mn) return launch_grad<true, true, false>(tmA, tmB, tmC, args, num_sms, stream);
+    if (a_mn) return launch_grad<true, false, false>(tmA, tmB, tmC, args, num_sms, stream);
+    if (b_mn) return launch_grad<false, true, false>(tmA, tmB, tmC, args, num_sms, stream);
+    return launch_grad<false, false, false>(tmA, tmB, tmC, args, num_sms, stream);
 }
 
-cudaError_t gemm_kseg_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, int num_sms,
-                             cudaStream_t stream) {
-    return launch_grad<true, true, true>(tmA, tmB, args, num_sms, stream);
+cudaError_t gemm_kseg_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                             const GemmArgs& args, int num_sms, cudaStream_t stream) {
+    return launch_grad<true, true, true>(tmA, tmB, tmC, args, num_sms, stream);
 }
 
-size_t gemm_smem_bytes() { return P_STAGES * P_STAGE_BYTES + 1024 + 512 + 4 * 32 * 36 * 4; }
+size_t gemm_smem_bytes() {
+    return 1024 + ((P_STAGES * P_STAGE_BYTES + 512 + 4 * 32 * 36 * 4 + 1023) & ~static_cast<size_t>(1023)) + 4 * 8192;
+}
 
 }  // namespace fm
