@@ -1245,6 +1245,81 @@ def reference_sample(cfg, tokens_per_thread: int, threads: int, update_s: float 
     return {"value": value, "t_train_s": t_train, "t_update_s": t_upd, "wall_s": wall, "tokens": tok}
 
 
+def host_info() -> dict:
+    """The box the CPU numbers were taken on."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        ram = int(open("/proc/meminfo").read().split("MemTotal:")[1].split()[0]) / 2**20
+    except Exception:
+        ram = 0.0
+    return {"nproc": os.cpu_count() or 1, "cpu_model": model, "ram_gb": round(ram, 1)}
+
+
+def reference_processes(cfg, tokens: int, procs: int, update_s: float | None = None) -> dict:
+    """P independent reference processes, process i pinned to
+    core i with taskset: each drives the compiled reference ExperienceStore +
+    TrainingEngine on one sample of `tokens` response tokens at the full V x D
+    (bench.py --ref-worker).  Aggregate = all processes' tokens / the slowest
+    process's training time, + the update amortised over a real global step."""
+    import shutil
+    import subprocess
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--ref-worker", "--config", cfg.name, "--ref-tokens", str(tokens)]
+    if update_s is not None:
+        cmd += ["--ref-skip-update"]
+    ncpu = os.cpu_count() or 1
+    tset = shutil.which("taskset")
+    ps = [subprocess.Popen(([tset, "-c", str(i % ncpu)] if tset else []) + cmd + ["--ref-id", str(i)],
+                           stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for i in range(procs)]
+    outs = []
+    for p in ps:
+        o, e = p.communicate(timeout=3600)
+        if p.returncode != 0:
+            raise RuntimeError(f"reference worker failed: {e[-500:]}")
+        outs.append(json.loads(o.strip().splitlines()[-1]))
+    t_train = max(r["t_train"] for r in outs)
+    t_upd = max(r["t_update"] for r in outs) if update_s is None else update_s
+    tok = procs * tokens
+    per_tok_upd = t_upd / (cfg.global_batch * cfg.resp_len)
+    return {"value": tok / (t_train + per_tok_upd * tokens), "t_train_s": t_train, "t_update_s": t_upd,
+            "tokens": tok, "pinned": bool(tset)}
+
+
+def ref_worker(args) -> None:
+    """One reference process (see reference_processes): prints its timings."""
+    from oracle import oracle as orc
+    from paper_2602_09578_b200 import workload as wl
+    cfg = wl.CONFIGS[args.config]
+    s = wl.step_samples(cfg, cfg.agents[0], 0, n=1, resp_len=args.ref_tokens)[0]
+    r = orc.ref_run_agent(f"cpu{args.ref_id}", cfg.vocab, cfg.feat, cfg.seed, 1, 1, 1, [s.input_id], [0], [0], [0],
+                          [(s.prompt, s.response)], [0.5], want_state=False, skip_update=args.ref_skip_update)
+    emit({"t_train": r["t_train"], "t_update": r["t_update"]})
+
+
+def cpu_baseline_record(cfg, tokens: int, steps: int = 1) -> dict:
+    """The reference on the box's host cores: P = min(nproc, RAM-bound) independent
+    pinned processes (the value), and 1 pinned process (the single-core number)."""
+    P = ref_threads(cfg)
+    one = reference_processes(cfg, tokens, 1)
+    upd = one["t_update_s"]
+    runs = [reference_processes(cfg, tokens, P, update_s=upd) for _ in range(max(1, steps))]
+    v = float(np.mean([r["value"] for r in runs]))
+    return {"value": v, "unit": "trained tokens/s", "cores": P, "kind": "reference",
+            "sample": (f"{P} independent processes pinned to cores 0..{P - 1} (taskset), each 1 sample x {tokens} "
+                       f"tokens at V={cfg.vocab}, D={cfg.feat} through the compiled reference ExperienceStore + "
+                       f"TrainingEngine; apply_global_update timed once and amortised over "
+                       f"{cfg.global_batch}x{cfg.resp_len} tokens"),
+            "one_core": {"value": one["value"], "unit": "trained tokens/s",
+                         "sample": f"1 process pinned to core 0, 1 sample x {tokens} tokens, same amortisation"},
+            "host": host_info(), "ms_per_step": float(np.mean([r["t_train_s"] for r in runs])) * 1e3}
+
+
 def ref_threads(cfg) -> int:
     n = os.cpu_count() or 1
     try:
@@ -1264,26 +1339,13 @@ def run_reference(args, dist: Dist):
     if not orc.ref_available():
         emit({"impl": "reference", "unavailable": "oracle/_ref/libmarlsim_ref.so not built"})
         return
-    threads = ref_threads(cfg)
-    tpt = args.ref_tokens
-    vals = []
-    upd = None
-    for i in range(args.warmup + args.steps):
-        r = reference_sample(cfg, tpt, threads, update_s=upd)
-        upd = r["t_update_s"]  # measured in the first (warm-up) step, reused after
-        if i >= args.warmup:
-            vals.append(r)
-    v = float(np.mean([r["value"] for r in vals]))
-    ms_step = float(np.mean([r["t_train_s"] for r in vals])) * 1e3
-    sample = (f"{threads} threads x 1 sample x {tpt} tokens at V={cfg.vocab}, D={cfg.feat} per step "
-              f"(fresh reference TrainingEngine per thread; apply_global_update timed and amortised over "
-              f"{cfg.global_batch}x{cfg.resp_len} tokens)")
+    # warm-up: the single-core run (also measures the update) stands in for it
+    cb = cpu_baseline_record(cfg, args.ref_tokens, steps=args.steps)
+    v = cb["value"]
     out = {"metric": METRIC, "value": v, "unit": "trained tokens/s", "n_gpus": args.gpus, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-           "config": config_obj(cfg, args),
-           "cpu_baseline": {"value": v, "unit": "trained tokens/s", "cores": threads, "kind": "reference",
-                            "sample": sample},
+           "warmup": args.warmup, "ms_per_step": cb.pop("ms_per_step"), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": config_obj(cfg, args), "cpu_baseline": cb,
            "e2e": {"value": v, "unit": "trained tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(out)
 
@@ -1338,6 +1400,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--ref-tokens", type=int, default=4, help="reference tokens per thread per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-worker", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--ref-id", type=int, default=0, help=argparse.SUPPRESS)
+    ap.add_argument("--ref-skip-update", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--host-breakdown", action="store_true")
     ap.add_argument("--agents", type=int, default=0, help="use only the first K agents of the config")
     ap.add_argument("--dp-mode", default="gang", choices=["gang", "allreduce"],
@@ -1356,6 +1421,9 @@ def main():
     ap.add_argument("--c4-phase-epochs", type=int, default=0,
                     help="C4 drifting core: epochs per phase (0 = fixed core; dynamic defaults to 2)")
     args = ap.parse_args()
+    if args.ref_worker:  # one pinned reference process of the CPU baseline
+        ref_worker(args)
+        return
     dist = Dist()
     try:
         if args.impl == "reference":
@@ -1401,11 +1469,8 @@ def main():
         if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
             from oracle import oracle as orc
             if orc.ref_available():
-                th = ref_threads(cfg)
-                r = reference_sample(cfg, args.ref_tokens, th)
-                cpu = {"value": r["value"], "unit": "trained tokens/s", "cores": th, "kind": "reference",
-                       "sample": f"{th} threads x 1 sample x {args.ref_tokens} tokens at V={cfg.vocab}, "
-                                 f"D={cfg.feat}, apply_global_update amortised ({r['wall_s']:.1f} s wall)"}
+                cpu = cpu_baseline_record(cfg, args.ref_tokens)
+                cpu.pop("ms_per_step", None)
         if dist.rank == 0:
             out = {"metric": METRIC, "value": res["value"], "unit": "trained tokens/s", "n_gpus": dist.world,
                    "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["max_ms"] / args.steps,
