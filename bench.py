@@ -1112,7 +1112,7 @@ def run_migrate(args, dist) -> None:
         holder = dst
     t_best = dist.bcast_obj(min(times) if times else None, src=1)
     t_best = min(x for x in (t_best, dist.bcast_obj(min(times) if times else None, src=0)) if x is not None)
-    nbytes = V * D * (8 + 4 + 4 + 4 + 2) + D * 4  # W f64, m, v, pending dW, bf16 shadow, colmax
+    nbytes = V * D * (8 + 4 + 4 + 4 + 2) + D * 4  # W f64, m, v, pending dW, bf16 shadow, fmax
     if dist.rank == 0:
         emit({"row": "agent migration (cross-process, NVLink)", "config": args.config, "params": V * D,
               "state_bytes": nbytes, "best_ms": round(t_best * 1e3, 3),
@@ -1374,7 +1374,7 @@ def config_obj(cfg, args) -> dict:
             "agents": na, "vocab": cfg.vocab, "feat": cfg.feat, "micro_batch": cfg.micro_batch,
             "global_batch": cfg.global_batch, "resp_len": cfg.resp_len,
             "formulation": formulation(args),
-            "l2": "inputs larger than L2 (W16 262 MB; p~ token slots 3.8 GB per micro-batch); no flush needed",
+            "l2": "inputs larger than L2 (W16^T 262 MB, gradient segments 1.1 GB per micro-batch, 2.4 GB of state per agent); no flush needed",
             "parallelism": f"agent-centric placement, dp gangs of max(1, N/{na}) GPUs",
             "experience_store": getattr(args, "store", "host")}
 

@@ -629,7 +629,7 @@ int check_active(fm_agent* a) {
         FM_CUDA(cudaStreamWaitEvent(a->ctx->stream, a->ev_in, 0));
         a->pending_in = false;
     }
-    a->last_seq = ++a->ctx->op_seq;  // everything this op enqueues follows any earlier GEMM1 mark
+    a->last_seq = ++a->ctx->op_seq;  // everything this op enqueues follows any earlier K-stats mark
     return FM_OK;
 }
 

@@ -133,7 +133,7 @@ def test_tensor_core_path_matches_reference(ctx):
 
 
 def test_tensor_core_kernels_vs_torch_fp32(ctx):
-    """One micro-batch through K-gather/K-GEMM1/K-lse/K-softmax-grad/K-GEMM2
+    """One micro-batch through K-gather/K-pos/K-stats/K-lse/K-band/K-GEMM2
     against a plain torch fp32 restatement of the same dense op on the same
     bf16-rounded operands (V=1000 exercises the N-tile tail)."""
     import torch
@@ -428,7 +428,7 @@ def test_gemm2_partial_waves(ctx, V, D_, resp):
 
 
 def test_update_park_equals_update_then_suspend(ctx):
-    """fm_apply_update_park (K-adam writes W/m/v/W16/colmax straight into the
+    """fm_apply_update_park (K-adam writes W/m/v/W16^T straight into the
     parking buffer) == fm_apply_update + fm_agent_suspend(device): after
     re-activation the state checksums (W, m, v, W16), weights, moments and the
     next step's gradient are bit-identical, and equal the resident run's."""
