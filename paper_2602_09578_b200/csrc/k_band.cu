@@ -272,10 +272,14 @@ __device__ __forceinline__ float ex2(float x) {
 // chunk's per-row metadata (q0, action, 1/n; pass B: lse, coefficient).
 constexpr int kMetaRows = kBandRows + 4;
 constexpr int kRedPitch = 33;  // per-warp [32 rows][32 lanes] partial sums, padded (conflict-free transpose)
+// Positions of a chunk the branch-free loop indexes directly (4 per row covers
+// samples of >= 1 row; longer spans — many empty samples — take the general loop).
+constexpr int kMaxQ = 4 * (kBandRows + 4) + 8;
 template <bool kGrad, int kV>
 constexpr size_t band_smem_bytes() {
     return kBandStages * kBandConsumers * 16 * kV + 2 * kBandStages * sizeof(uint64_t) +
-           5 * kMetaRows * sizeof(int32_t) + (kGrad ? 0 : (kBandConsumers / 32) * 32 * kRedPitch * sizeof(float));
+           5 * kMetaRows * sizeof(int32_t) + (kGrad ? 0 : (kBandConsumers / 32) * 32 * kRedPitch * sizeof(float)) +
+           kMaxQ * sizeof(int32_t);
 }
 
 template <bool kGrad, int kV, int kMinBlocks>
@@ -293,6 +297,8 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
     float* m_lse = m_rs + kMetaRows;  // pass A: the rows' softmax bounds
     float* m_ce = m_lse + kMetaRows;
     float* redbuf = m_ce + kMetaRows;  // pass A: per-warp [32][kRedPitch]
+    // position k of the chunk -> the row whose four positions end there, or -1
+    int32_t* m_end = reinterpret_cast<int32_t*>(redbuf + (kGrad ? 0 : (kBandConsumers / 32) * 32 * kRedPitch));
     const int tid = static_cast<int>(threadIdx.x);
     const int lane = tid & 31;
     const int64_t v0 = static_cast<int64_t>(blockIdx.x) * kCols;
@@ -327,6 +333,13 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
     const int qa = m_q0[0];
     const int qb = m_q0[nrows - 1] + 4;
     const int nq = qb - qa;
+    const bool fast = kV == 1 && nq + 8 <= kMaxQ;  // uniform
+    if (fast) {
+        for (int k = tid; k < kMaxQ; k += kBandThreads) m_end[k] = -1;
+        __syncthreads();
+        for (int i = tid; i < nrows; i += kBandThreads) m_end[m_q0[i] + 3 - qa] = i;
+        __syncthreads();
+    }
 
     // warp-uniform role split (the broadcast tells the compiler so: no divergent
     // shuffle fallbacks in the consumers)
@@ -557,11 +570,149 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
         }
     };
     const int qend = kGrad ? qb + 3 : qb;
-    for (int qq = qa & ~3; qq < qend; qq += 4) {
-        step(qq, std::integral_constant<int, 0>{});
-        step(qq + 1, std::integral_constant<int, 1>{});
-        step(qq + 2, std::integral_constant<int, 2>{});
-        step(qq + 3, std::integral_constant<int, 3>{});
+    if (!fast) {
+        for (int qq = qa & ~3; qq < qend; qq += 4) {
+            step(qq, std::integral_constant<int, 0>{});
+            step(qq + 1, std::integral_constant<int, 1>{});
+            step(qq + 2, std::integral_constant<int, 2>{});
+            step(qq + 3, std::integral_constant<int, 3>{});
+        }
+        return;
+    }
+    if constexpr (kV == 1) {
+        // Branch-free body over 4 positions: wait for and read all four ring stages first,
+        // then run the four positions' arithmetic as one straight-line block (the row math
+        // unconditionally, zero-weighted where no row ends), so the compiler interleaves
+        // four independent dependency chains instead of serialising position after position.
+        const int d_act0 = static_cast<int>(cb[0] - v0);  // this lane's first column within the slice
+        for (int qq = qa & ~3; qq < qend; qq += 4) {
+            uint4 u[4];
+            int stg[4];
+            bool in[4];
+#pragma unroll
+            for (int S = 0; S < 4; ++S) {
+                const int q = qq + S;
+                in[S] = q >= qa && q < qb;
+                u[S] = make_uint4(0u, 0u, 0u, 0u);
+                stg[S] = st;
+                if (in[S]) {
+                    mbar_wait(&full[st], ph);
+                    u[S] = *reinterpret_cast<const uint4*>(ring + st * kStage + tid * 16);
+                    if (++st == kBandStages) {
+                        st = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+                for (int S = 0; S < 4; ++S)
+                    if (in[S]) mbar_arrive(&empty[stg[S]]);
+            }
+#pragma unroll
+            for (int S = 0; S < 4; ++S) {
+                const int q = qq + S;
+                float2 x[4];
+                unpack8(u[S], x);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    pr[S][j] = __fadd2_rn(xp[j], x[j]);
+                    xp[j] = x[j];
+                }
+                const int k = q - qa;
+                const int i = in[S] ? m_end[k] : -1;
+                const int ii = i < 0 ? 0 : i;
+                const float rs = m_rs[ii];
+                const int dact = m_act[ii] - static_cast<int>(v0) - d_act0;  // action column - this lane's first
+                float2 z4[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) z4[j] = __fadd2_rn(pr[(S + 2) & 3][j], pr[S][j]);
+                const float c = rs * kLog2e;
+                const float2 cc = make_float2(c, c);
+                if constexpr (!kGrad) {
+                    const float lo = -m_lse[ii] * kLog2e;  // the row's softmax bound
+                    const float2 off = make_float2(lo, lo);
+                    float2 s2 = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float2 y = __ffma2_rn(z4[j], cc, off);
+                        float2 e = make_float2(ex2(y.x), ex2(y.y));
+                        if (!warp_full) {
+                            if (!valid(j, 0)) e.x = 0.f;
+                            if (!valid(j, 1)) e.y = 0.f;
+                        }
+                        s2 = __fadd2_rn(s2, e);
+                    }
+                    if (i >= 0) {
+                        float* rb_w = redbuf + warp * 32 * kRedPitch;
+                        rb_w[(i & 31) * kRedPitch + lane] = s2.x + s2.y;
+                        if (static_cast<unsigned>(dact) < static_cast<unsigned>(nv[0])) {
+                            const int rr = rstart + i;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                if (dact == 2 * j) A.zact[rr] = rs * z4[j].x;
+                                if (dact == 2 * j + 1) A.zact[rr] = rs * z4[j].y;
+                            }
+                        }
+                        if ((i & 31) == 31 || i == nrows - 1) {
+                            __syncwarp();
+                            const int i0 = i & ~31;
+                            if (i0 + lane <= i) {
+                                const float* src = rb_w + lane * kRedPitch;
+                                float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+#pragma unroll
+                                for (int kk = 0; kk < 32; kk += 4) {
+                                    t0 += src[kk];
+                                    t1 += src[kk + 1];
+                                    t2 += src[kk + 2];
+                                    t3 += src[kk + 3];
+                                }
+                                A.stats[static_cast<int64_t>(tile) * A.ld_stats + rstart + i0 + lane] =
+                                    (t0 + t1) + (t2 + t3);
+                            }
+                            __syncwarp();
+                        }
+                    }
+                } else {
+                    // g = ce (delta(v, a) - exp(z - lse)); ce = 0 where no row ends (and for
+                    // zero-advantage rows, training.hpp:394).  Columns past V hold garbage that
+                    // is never stored: no masks.
+                    const float ce = i >= 0 ? m_ce[ii] : 0.f;
+                    const float lo = i >= 0 ? -m_lse[ii] * kLog2e : -1e30f;  // no row: exp -> +0
+                    const float2 off = make_float2(lo, lo), nce = make_float2(-ce, -ce);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float2 y = __ffma2_rn(z4[j], cc, off);
+                        gr[S][j] = __fmul2_rn(make_float2(ex2(y.x), ex2(y.y)), nce);
+                    }
+                    if (static_cast<unsigned>(dact) < 8u) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            if (dact == 2 * j) gr[S][j].x += ce;
+                            if (dact == 2 * j + 1) gr[S][j].y += ce;
+                        }
+                    }
+                    // position p = q - 3 is touched exactly by the rows ending at p .. p + 3
+                    const int p = q - 3;
+                    if (p >= elo && p < ehi) {
+                        if (p >= sg + 32) {  // next group of slots (warp-uniform)
+                            sg += 32;
+                            s_cur = s_next;
+                            s_next = sg + 32 + lane < qb ? __ldg(A.pos_slot + sg + 32 + lane) : -1;
+                        }
+                        const int32_t sl = __shfl_sync(0xffffffffu, s_cur, p - sg);
+                        if (sl >= 0 && nv[0] > 0) {
+                            float2 h[4];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                h[j] = __fadd2_rn(__fadd2_rn(gr[0][j], gr[1][j]), __fadd2_rn(gr[2][j], gr[3][j]));
+                            *reinterpret_cast<uint4*>(A.aseg + static_cast<int64_t>(sl) * A.ld_a + cb[0]) = pack8(h);
+                        }
+                    }
+                }
+            }
+        }
     }
 }
 
