@@ -585,6 +585,11 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
         // unconditionally, zero-weighted where no row ends), so the compiler interleaves
         // four independent dependency chains instead of serialising position after position.
         const int d_act0 = static_cast<int>(cb[0] - v0);  // this lane's first column within the slice
+        int rows_done = 0, flushed = 0;  // pass A: rows whose partials are parked / summed
+        // two instances of the loop: warps whose columns are all inside the vocabulary skip
+        // pass A's per-column masks (only the last slice's boundary warp needs them)
+        auto fast_loop = [&](auto FullTag) {
+        constexpr bool kFull = decltype(FullTag)::value;
         for (int qq = qa & ~3; qq < qend; qq += 4) {
             uint4 u[4];
             int stg[4];
@@ -638,42 +643,24 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
                     for (int j = 0; j < 4; ++j) {
                         const float2 y = __ffma2_rn(z4[j], cc, off);
                         float2 e = make_float2(ex2(y.x), ex2(y.y));
-                        if (!warp_full) {
+                        if constexpr (!kFull) {
                             if (!valid(j, 0)) e.x = 0.f;
                             if (!valid(j, 1)) e.y = 0.f;
                         }
                         s2 = __fadd2_rn(s2, e);
                     }
-                    if (i >= 0) {
-                        float* rb_w = redbuf + warp * 32 * kRedPitch;
-                        rb_w[(i & 31) * kRedPitch + lane] = s2.x + s2.y;
-                        if (static_cast<unsigned>(dact) < static_cast<unsigned>(nv[0])) {
-                            const int rr = rstart + i;
+                    // partial sum parked in the warp's 32-row ring (slot i & 31); the
+                    // halves are summed once per 4-position body (below)
+                    if (i >= 0) redbuf[warp * 32 * kRedPitch + (i & 31) * kRedPitch + lane] = s2.x + s2.y;
+                    if (i >= 0 && static_cast<unsigned>(dact) < static_cast<unsigned>(nv[0])) {
+                        const int rr = rstart + i;
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                if (dact == 2 * j) A.zact[rr] = rs * z4[j].x;
-                                if (dact == 2 * j + 1) A.zact[rr] = rs * z4[j].y;
-                            }
-                        }
-                        if ((i & 31) == 31 || i == nrows - 1) {
-                            __syncwarp();
-                            const int i0 = i & ~31;
-                            if (i0 + lane <= i) {
-                                const float* src = rb_w + lane * kRedPitch;
-                                float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
-#pragma unroll
-                                for (int kk = 0; kk < 32; kk += 4) {
-                                    t0 += src[kk];
-                                    t1 += src[kk + 1];
-                                    t2 += src[kk + 2];
-                                    t3 += src[kk + 3];
-                                }
-                                A.stats[static_cast<int64_t>(tile) * A.ld_stats + rstart + i0 + lane] =
-                                    (t0 + t1) + (t2 + t3);
-                            }
-                            __syncwarp();
+                        for (int j = 0; j < 4; ++j) {
+                            if (dact == 2 * j) A.zact[rr] = rs * z4[j].x;
+                            if (dact == 2 * j + 1) A.zact[rr] = rs * z4[j].y;
                         }
                     }
+                    if (i >= 0) rows_done = i + 1;
                 } else {
                     // g = ce (delta(v, a) - exp(z - lse)); ce = 0 where no row ends (and for
                     // zero-advantage rows, training.hpp:394).  Columns past V hold garbage that
@@ -712,7 +699,33 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
                     }
                 }
             }
+            if constexpr (!kGrad) {
+                // a body ends <= 4 rows, so <= 19 rows are ever parked: every completed
+                // 16-row group (and the tail after the last body), lanes 0-15 add up its rows' 32 lane partials (transposed read of the padded
+                // ring, conflict-free) into the warp's stats column
+                while (rows_done - flushed >= 16 || (qq + 4 >= qend && rows_done > flushed)) {
+                    __syncwarp();
+                    const int n = rows_done - flushed < 16 ? rows_done - flushed : 16;
+                    if (lane < n) {
+                        const float* src = redbuf + warp * 32 * kRedPitch + ((flushed + lane) & 31) * kRedPitch;
+                        float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+#pragma unroll
+                        for (int kk = 0; kk < 32; kk += 4) {
+                            t0 += src[kk];
+                            t1 += src[kk + 1];
+                            t2 += src[kk + 2];
+                            t3 += src[kk + 3];
+                        }
+                        A.stats[static_cast<int64_t>(tile) * A.ld_stats + rstart + flushed + lane] = (t0 + t1) + (t2 + t3);
+                    }
+                    flushed += n;
+                    __syncwarp();
+                }
+            }
         }
+        };
+        if (warp_full) fast_loop(std::true_type{});
+        else fast_loop(std::false_type{});
     }
 }
 

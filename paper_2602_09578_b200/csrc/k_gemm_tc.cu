@@ -57,7 +57,7 @@ __device__ __forceinline__ TileCoord tile_coord(int t, int tiles_m, int tiles_n,
 // ---- epilogue ---------------------------------------------------------------
 
 struct GradEpi {
-    double sumsq;
+    float sumsq;  // this tile's sum of squares (fp32 per tile, fp64 across tiles)
     float* xbuf = nullptr;  // per-warp 32 x 36 fp32 smem staging (exchange mode)
     uint8_t* stage = nullptr;  // per-warp 2 x 4 KB SWIZZLE_128B staging of the TMA epilogue
     const CUtensorMap* tmc = nullptr;
@@ -80,7 +80,7 @@ struct GradEpi {
             part += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
             *reinterpret_cast<float4*>(buf + lane * 128 + ((k ^ (lane & 7)) << 4)) = acc;
         }
-        sumsq += static_cast<double>(part);  // rows / columns past the matrix hold exact zeros
+        sumsq += part;  // rows / columns past the matrix hold exact zeros
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -117,7 +117,7 @@ struct GradEpi {
             }
             *reinterpret_cast<float4*>(xbuf + lane * 36 + j) = acc;
         }
-        sumsq += static_cast<double>(part);
+        sumsq += part;
         __syncwarp();
         const int row0 = row - static_cast<int>(lane);
         const int seg = static_cast<int>(lane & 7);
@@ -168,7 +168,7 @@ struct GradEpi {
                 if (row < a.M) part += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
                 *reinterpret_cast<float4*>(xbuf + lane * 36 + j) = acc;
             }
-            sumsq += static_cast<double>(part);
+            sumsq += part;
             __syncwarp();
             const int row0 = row - static_cast<int>(lane);
             const int seg = static_cast<int>(lane & 7);
@@ -226,7 +226,7 @@ struct GradEpi {
                 }
             }
         }
-        sumsq += static_cast<double>(part);
+        sumsq += part;
     }
 };
 
@@ -390,7 +390,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             const int row = tc.mb * 256 + row_in_tile;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            epi.sumsq = 0.0;
+            epi.sumsq = 0.f;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t r[32];
@@ -406,7 +406,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                 }
                 epi.chunk(args, row, tc.nb * BN + c * 32, r);
             }
-            sumsq_total += epi.sumsq;
+            sumsq_total += static_cast<double>(epi.sumsq);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
