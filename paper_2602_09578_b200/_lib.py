@@ -10,7 +10,8 @@ import ctypes as C
 import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_native" / "libflexmarl_b200.so"
+LIB_PATH = Path(__file__).resolve().parent / "_native" / (
+    "libflexmarl_b200_debug.so" if os.environ.get("FLEXMARL_DEBUG_LIB") == "1" else "libflexmarl_b200.so")
 
 # fm_status (cabi.h) — 1..28 are marlsim::ErrorCode + 1 (errors.hpp:10-39)
 ERROR_NAMES = [

@@ -21,6 +21,10 @@ CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_native"
 LIB = OUT_DIR / "libflexmarl_b200.so"
 OBJ_DIR = ROOT / "build" / "obj"
+# debug variant: device-side bounds checks (FM_DCHECK, fm_ptx.cuh) in place of
+# compute-sanitizer, which the GPU pool does not offer; loaded with FLEXMARL_DEBUG_LIB=1
+LIB_DEBUG = OUT_DIR / "libflexmarl_b200_debug.so"
+OBJ_DIR_DEBUG = ROOT / "build" / "obj_debug"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -57,8 +61,8 @@ def _flags() -> list[str]:
     ]
 
 
-def _compile(src: Path, obj: Path, verbose: bool) -> None:
-    cmd = [nvcc(), *ARCH, *_flags(), "-c", str(src), "-o", str(obj)]
+def _compile(src: Path, obj: Path, verbose: bool, debug: bool = False) -> None:
+    cmd = [nvcc(), *ARCH, *_flags(), *(["-DFM_DEBUG_CHECKS"] if debug else []), "-c", str(src), "-o", str(obj)]
     if src.suffix == ".cu":
         cmd.insert(1, "-Xptxas=-v") if verbose else None
     if verbose:
@@ -77,33 +81,34 @@ def _stale(outp: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    OBJ_DIR.mkdir(parents=True, exist_ok=True)
+def build(verbose: bool = False, force: bool = False, debug: bool = False) -> Path:
+    obj_dir, lib = (OBJ_DIR_DEBUG, LIB_DEBUG) if debug else (OBJ_DIR, LIB)
+    obj_dir.mkdir(parents=True, exist_ok=True)
     OUT_DIR.mkdir(parents=True, exist_ok=True)
     headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + list((ROOT / "include").rglob("*.h"))
     jobs = []
     objs = []
     for name in CUDA_SOURCES + CXX_SOURCES:
         src = CSRC / name
-        obj = OBJ_DIR / (name + ".o")
+        obj = obj_dir / (name + ".o")
         objs.append(obj)
         if force or _stale(obj, [src, *headers]):
             jobs.append((src, obj))
     with cf.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
-        for f in [ex.submit(_compile, s, o, verbose) for s, o in jobs]:
+        for f in [ex.submit(_compile, s, o, verbose, debug) for s, o in jobs]:
             f.result()
-    if force or jobs or _stale(LIB, objs):
+    if force or jobs or _stale(lib, objs):
         nd = nccl_dir()
         link = ([f"-L{nd / 'lib'}", "-l:libnccl.so.2", "-Xlinker", f"-rpath,{nd / 'lib'}"] if nd
                 else ["-lnccl"])
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), *link]
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(lib), *map(str, objs), *link]
         if verbose:
             print(" ".join(cmd), flush=True)
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed\n{res.stdout}\n{res.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, debug="--debug" in sys.argv))

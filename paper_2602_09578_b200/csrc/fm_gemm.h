@@ -35,6 +35,7 @@ struct GemmArgs {
     // A' [K'][M] and B' [K'][256] (tile loads, MN-major).
     const int32_t* kseg_off = nullptr;
     const int32_t* kseg_iters = nullptr;
+    long long dbg_krows = 0;  // rows of A' / B' (debug-build bounds checks; 0 = unchecked)
 };
 
 size_t gemm_smem_bytes();

@@ -103,6 +103,7 @@ struct BandArgs {
     const int32_t* pos_slot;  // [Q]
     __nv_bfloat16* aseg;      // A' [K'][ld_a]
     int64_t ld_a;
+    int64_t dbg_kp = 0, dbg_D = 0;  // A' rows and features (debug-build bounds checks)
 };
 cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s);
 // K-stats partials per row (one per consumer warp of every vocabulary slice).

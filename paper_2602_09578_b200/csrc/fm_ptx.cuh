@@ -8,6 +8,25 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+// Device-side bounds checks of the debug build (build.py --debug ->
+// _native/libflexmarl_b200_debug.so, FLEXMARL_DEBUG_LIB=1): compute-sanitizer is
+// closed on the GPU pool, so the indices the kernels derive from data (slots,
+// positions, features, rows) are checked here instead.  No-ops otherwise.
+#ifdef FM_DEBUG_CHECKS
+#include <cstdio>
+#define FM_DCHECK(c)                                                                     \
+    do {                                                                                 \
+        if (!(c)) {                                                                      \
+            printf("FM_DCHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);              \
+            __trap();                                                                    \
+        }                                                                                \
+    } while (0)
+#else
+#define FM_DCHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 namespace fm {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -1051,6 +1051,8 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             ba.pos_slot = w.pos_slot;
             ba.aseg = w.aseg;
             ba.ld_a = static_cast<int64_t>(ldz);
+            ba.dbg_kp = w.kp_cap;
+            ba.dbg_D = static_cast<int64_t>(a->D);
             FM_CUDA(cudaEventRecord(c->ev_gemm, s));  // swap copies may start here (fm_agent_suspend)
             c->gemm_seq = ++c->op_seq;
             {
@@ -1084,6 +1086,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             g2.sumsq = scal;
             g2.kseg_off = w.kseg_off;
             g2.kseg_iters = w.kiters;
+            g2.dbg_krows = w.kp_cap;
             // exact micro-batch grad norm under DP (opt-in, fm_agent_set_dp_norms): GEMM2 writes
             // this rank's contribution to a scratch, which is added to dW, all-reduced and
             // measured (training.hpp:417); a gang's exchange then runs as plain copies

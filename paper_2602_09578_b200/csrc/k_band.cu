@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(1024) pslot_place_kernel(const int32_t* __rest
                                                            int32_t* __restrict__ kseg_off,
                                                            int32_t* __restrict__ kiters, int32_t* __restrict__ slot,
                                                            __nv_bfloat16* __restrict__ bseg,
-                                                           unsigned long long* rows_acc) {
+                                                           unsigned long long* rows_acc, int64_t kp_cap) {
     __shared__ int wsum[33];
     __shared__ int off_s, base_s, len_s;
     const int b = blockIdx.x, c = blockIdx.y, nch = gridDim.y;
@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(1024) pslot_place_kernel(const int32_t* __rest
     const int rk = block_rank(hit, wsum, &tot);
     if (hit) {
         const int s = off + base_s + rk;
+        FM_DCHECK(s >= 0 && s < kp_cap);
         slot[q] = s;
         bseg[static_cast<size_t>(s) * 256 + (f & 255)] = __float2bfloat16_rn(1.f);
     }
@@ -337,7 +338,10 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
     if (fast) {
         for (int k = tid; k < kMaxQ; k += kBandThreads) m_end[k] = -1;
         __syncthreads();
-        for (int i = tid; i < nrows; i += kBandThreads) m_end[m_q0[i] + 3 - qa] = i;
+        for (int i = tid; i < nrows; i += kBandThreads) {
+            FM_DCHECK(m_q0[i] + 3 - qa >= 0 && m_q0[i] + 3 - qa < nq);
+            m_end[m_q0[i] + 3 - qa] = i;
+        }
         __syncthreads();
     }
 
@@ -364,6 +368,7 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
                     // a position before the sequence start reads the zero row
                     const __nv_bfloat16* src = f >= 0 ? base + static_cast<int64_t>(f) * A.ldw : A.zero_row;
                     mbar_arrive_expect_tx(&full[st], bytes);
+                    FM_DCHECK(f < A.dbg_D);
                     bulk_load(ring + st * kStage, src, bytes, &full[st]);
                 }
                 __syncwarp();
@@ -562,6 +567,7 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
                             for (int j = 0; j < 4; ++j)
                                 h[j] = __fadd2_rn(__fadd2_rn(gr[0][4 * i + j], gr[1][4 * i + j]),
                                                   __fadd2_rn(gr[2][4 * i + j], gr[3][4 * i + j]));
+                            FM_DCHECK(sl < A.dbg_kp && cb[i] + 8 <= A.ld_a);
                             *reinterpret_cast<uint4*>(A.aseg + static_cast<int64_t>(sl) * A.ld_a + cb[i]) = pack8(h);
                         }
                     }
@@ -694,6 +700,7 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
 #pragma unroll
                             for (int j = 0; j < 4; ++j)
                                 h[j] = __fadd2_rn(__fadd2_rn(gr[0][j], gr[1][j]), __fadd2_rn(gr[2][j], gr[3][j]));
+                            FM_DCHECK(sl < A.dbg_kp && cb[0] + 8 <= A.ld_a);
                             *reinterpret_cast<uint4*>(A.aseg + static_cast<int64_t>(sl) * A.ld_a + cb[0]) = pack8(h);
                         }
                     }
@@ -716,6 +723,7 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
                             t2 += src[kk + 2];
                             t3 += src[kk + 3];
                         }
+                        FM_DCHECK(tile < A.stats_ld && rstart + flushed + lane < A.M);
                         A.stats[static_cast<int64_t>(tile) * A.ld_stats + rstart + flushed + lane] = (t0 + t1) + (t2 + t3);
                     }
                     flushed += n;
@@ -755,7 +763,8 @@ cudaError_t launch_pslots(const int32_t* feat, int64_t Q, int nblk, int32_t* kco
     pslot_count_kernel<<<dim3(nblk, nch), 1024, 0, s>>>(feat, Q, kcount, slot);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    pslot_place_kernel<<<dim3(nblk, nch), 1024, 0, s>>>(feat, Q, kcount, kseg_off, kiters, slot, bseg, rows_acc);
+    pslot_place_kernel<<<dim3(nblk, nch), 1024, 0, s>>>(feat, Q, kcount, kseg_off, kiters, slot, bseg, rows_acc,
+                                                       bseg_rows);
     return cudaGetLastError();
 }
 

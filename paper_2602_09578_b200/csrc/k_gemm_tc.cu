@@ -310,6 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                 if constexpr (kSeg) {
                     kbase = __ldg(args.kseg_off + tc.nb);
                     ke = __ldg(args.kseg_iters + tc.nb);
+                    FM_DCHECK(args.dbg_krows == 0 || kbase + static_cast<long long>(ke) * BK <= args.dbg_krows);
                 }
                 for (int k = 0; k < ke; ++k) {
                     mbar_wait(&empty[stage], phase ^ 1);
