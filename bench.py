@@ -175,6 +175,11 @@ def placement(agents, world):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+def gang_mode_id(args) -> int:
+    """fm_gang_attach_mode's mode: 1 = vocabulary-parallel gang, 0 = token shards."""
+    return 1 if getattr(args, "dp_mode", "vocab") == "vocab" else 0
+
+
 def run_ours(args, dist: Dist) -> dict | None:
     from paper_2602_09578_b200 import _lib
     from paper_2602_09578_b200 import workload as wl
@@ -234,16 +239,17 @@ def run_ours(args, dist: Dist) -> dict | None:
         h = handles.get(a)
         blob = b""
         if h is not None:
-            if args.dp_mode == "gang":
+            if args.dp_mode in ("gang", "vocab"):
+                gm = 1 if args.dp_mode == "vocab" else 0
                 n = C.c_uint64()
-                check(L.fm_gang_attach(h, comms[a], None, 0, C.byref(n)))
+                check(L.fm_gang_attach_mode(h, comms[a], gm, None, 0, C.byref(n)))
                 buf = (C.c_uint8 * n.value)()
-                check(L.fm_gang_attach(h, comms[a], buf, n.value, C.byref(n)))
+                check(L.fm_gang_attach_mode(h, comms[a], gm, buf, n.value, C.byref(n)))
                 blob = bytes(buf)
             else:
                 check(L.fm_agent_set_shard(h, gang.index(dist.rank), len(gang)))
         blobs = dist.all_gather_obj(blob)
-        if h is not None and args.dp_mode == "gang":
+        if h is not None and args.dp_mode in ("gang", "vocab"):
             gang_blobs = b"".join(blobs[r] for r in gang)
             check(L.fm_gang_connect(h, gang_blobs, len(blob)))
 
@@ -372,8 +378,17 @@ def run_ours(args, dist: Dist) -> dict | None:
 
     # --- roofline of the dominant kernel + every hot-path kernel
     peaks = load_peaks()
-    M_local = rows_per_mb / len(place[mine[0]]) if mine else 0
+    g_mine = len(place[mine[0]]) if mine else 1
+    vocab_par = args.dp_mode == "vocab" and g_mine > 1
+    # token shards: each rank trains 1/g of the rows over the whole vocabulary;
+    # vocabulary gang: every row over this rank's 256-aligned column range
+    M_local = rows_per_mb / (1 if vocab_par else g_mine) if mine else 0
     V, Dm, P = cfg.vocab, cfg.feat, cfg.params
+    if vocab_par:
+        tiles = (V + 255) // 256
+        r = place[mine[0]].index(dist.rank)
+        V = min(V, tiles * (r + 1) // g_mine * 256) - min(V, tiles * r // g_mine * 256)
+        P = V * Dm
     n_mb = G // cfg.micro_batch
     # context positions of a micro-batch shard: its rows + 3 per sample
     Q_local = M_local + 3 * cfg.micro_batch
@@ -520,9 +535,9 @@ def run_c4(args, dist: Dist) -> dict:
         blob = b""
         if a in handles:
             n = C.c_uint64()
-            check(L.fm_gang_attach(handles[a], comms[a], None, 0, C.byref(n)))
+            check(L.fm_gang_attach_mode(handles[a], comms[a], gang_mode_id(args), None, 0, C.byref(n)))
             buf = (C.c_uint8 * n.value)()
-            check(L.fm_gang_attach(handles[a], comms[a], buf, n.value, C.byref(n)))
+            check(L.fm_gang_attach_mode(handles[a], comms[a], gang_mode_id(args), buf, n.value, C.byref(n)))
             blob = bytes(buf)
         blobs = dist.all_gather_obj(blob)
         if a in handles:
@@ -706,9 +721,9 @@ def run_c4_dynamic(args, dist: Dist) -> dict:
             h = comm_cache[key]
             comms[a] = h
             n = C.c_uint64()
-            check(L.fm_gang_attach(handles[a], h, None, 0, C.byref(n)))
+            check(L.fm_gang_attach_mode(handles[a], h, gang_mode_id(args), None, 0, C.byref(n)))
             buf = (C.c_uint8 * n.value)()
-            check(L.fm_gang_attach(handles[a], h, buf, n.value, C.byref(n)))
+            check(L.fm_gang_attach_mode(handles[a], h, gang_mode_id(args), buf, n.value, C.byref(n)))
             blob = bytes(buf)
         blobs = dist.all_gather_obj(blob)
         if me in gang:
@@ -1376,6 +1391,9 @@ def config_obj(cfg, args) -> dict:
             "formulation": formulation(args),
             "l2": "inputs larger than L2 (W16^T 262 MB, gradient segments 1.1 GB per micro-batch, 2.4 GB of state per agent); no flush needed",
             "parallelism": f"agent-centric placement, dp gangs of max(1, N/{na}) GPUs",
+            "dp_mode": {"gang": "token shards + fused GEMM2 reduce-scatter over NVLink + sharded Adam",
+                        "vocab": "vocabulary-parallel gang: column shards + per-row softmax all-reduce",
+                        "allreduce": "token shards + NCCL all-reduce + replicated Adam"}[getattr(args, "dp_mode", "vocab")],
             "experience_store": getattr(args, "store", "host")}
 
 
@@ -1405,8 +1423,10 @@ def main():
     ap.add_argument("--ref-skip-update", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--host-breakdown", action="store_true")
     ap.add_argument("--agents", type=int, default=0, help="use only the first K agents of the config")
-    ap.add_argument("--dp-mode", default="gang", choices=["gang", "allreduce"],
-                    help="gang: fused GEMM2 reduce-scatter over NVLink + sharded Adam; allreduce: NCCL")
+    ap.add_argument("--dp-mode", default="vocab", choices=["gang", "vocab", "allreduce"],
+                    help="gang: token shards, fused GEMM2 reduce-scatter over NVLink + sharded Adam; "
+                         "vocab: vocabulary-parallel gang (column shards, per-row softmax all-reduce); "
+                         "allreduce: token shards + NCCL all-reduce + replicated Adam")
     ap.add_argument("--store", default="host", choices=["host", "device"],
                     help="experience store: host control plane (default) or the on-device table (§8f-4)")
     ap.add_argument("--next", action="store_true", help="measure the SURVEY §8f next rows (one GPU)")

@@ -327,6 +327,15 @@ int fm_agent_allreduce_grad(fm_agent* a, fm_comm* c);
  * connect.  While attached the agent trains token-balanced row shards and its
  * master W / m / v rows outside its own shard are not maintained. */
 int fm_gang_attach(fm_agent* a, fm_comm* c, uint8_t* blob_out, uint64_t cap, uint64_t* len);
+/* Same with a mode: 0 = the token-sharded gang above; 1 = vocabulary-parallel:
+ * every rank trains ALL rows of each micro-batch on its vocabulary range of
+ * 256-row shards — K-stats / K-band on its columns, K-GEMM2 / K-adam on its rows
+ * of dW / W, its own W16^T columns — so no partial gradients cross NVLink; per
+ * micro-batch the rows' partial softmax sums and taken-token logits (2 floats per
+ * row) and the squared gradient norm are all-reduced (the micro-batch grad norm
+ * is the reference's, training.hpp:417).  The per-feature softmax bound is
+ * max-all-reduced once per update.  Same blob / connect / detach protocol. */
+int fm_gang_attach_mode(fm_agent* a, fm_comm* c, int mode, uint8_t* blob_out, uint64_t cap, uint64_t* len);
 int fm_gang_connect(fm_agent* a, const uint8_t* blobs, uint64_t blob_len);
 int fm_gang_detach(fm_agent* a);
 /* Before a gang dissolves: pull the peers' W / m / v rows (the sharded Adam keeps

@@ -113,6 +113,7 @@ _PROTOS = {
     "fm_agent_allreduce_grad": (I, [P, P]),
     "fm_agent_set_dp_norms": (I, [P, P]),
     "fm_gang_attach": (I, [P, P, P, U64, PU64]),
+    "fm_gang_attach_mode": (I, [P, P, I, P, U64, PU64]),
     "fm_gang_connect": (I, [P, P, U64]),
     "fm_gang_detach": (I, [P]),
     "fm_publish_weights": (I, [P, I, C.POINTER(P)]),

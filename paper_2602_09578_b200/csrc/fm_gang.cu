@@ -68,7 +68,12 @@ extern "C" {
 // gang and hand to fm_gang_connect.  The agent must stay resident (no
 // suspend) while attached.
 int fm_gang_attach(fm_agent* a, fm_comm* cm, uint8_t* blob_out, uint64_t cap, uint64_t* len) {
+    return fm_gang_attach_mode(a, cm, 0, blob_out, cap, len);
+}
+
+int fm_gang_attach_mode(fm_agent* a, fm_comm* cm, int mode, uint8_t* blob_out, uint64_t cap, uint64_t* len) {
     FM_GUARD_BEGIN
+    if (mode != 0 && mode != 1) return fail(FM_ERR_INVALID_ARG, "gang mode must be 0 (token shards) or 1 (vocabulary)");
     *len = sizeof(GangBlob);
     if (!blob_out) return FM_OK;
     if (cap < sizeof(GangBlob)) return fail(FM_ERR_INVALID_ARG, "blob buffer too small");
@@ -87,7 +92,9 @@ int fm_gang_attach(fm_agent* a, fm_comm* cm, uint8_t* blob_out, uint64_t cap, ui
     int64_t max_rows = 0;
     for (int o = 0; o < gs->g; ++o) max_rows = std::max(max_rows, gs->lo[o + 1] - gs->lo[o]);
     const int64_t own = gs->lo[gs->rank + 1] - gs->lo[gs->rank];
-    const size_t rbytes = static_cast<size_t>(gs->g - 1) * std::max<int64_t>(own, 1) * a->D * 4;
+    gs->vocab = mode == 1;
+    // the vocabulary-parallel gang exchanges no partial gradients: a token receive buffer only
+    const size_t rbytes = gs->vocab ? 256 : static_cast<size_t>(gs->g - 1) * std::max<int64_t>(own, 1) * a->D * 4;
     fm_ctx* c = a->ctx;
     void* rb = nullptr;
     void* tk = nullptr;
@@ -110,9 +117,11 @@ int fm_gang_attach(fm_agent* a, fm_comm* cm, uint8_t* blob_out, uint64_t cap, ui
     b.w16_off = static_cast<uint64_t>(reinterpret_cast<uint8_t*>(a->W16) - static_cast<uint8_t*>(a->slot->base));
     std::memcpy(blob_out, &b, sizeof(b));
     a->gang = gs;
-    a->shard_rank = gs->rank;  // token-balanced row shards of every micro-batch
-    a->shard_count = gs->g;
-    a->dp = true;
+    // token-balanced row shards of every micro-batch (mode 0); mode 1 trains every row
+    a->shard_rank = gs->vocab ? 0 : gs->rank;
+    a->shard_count = gs->vocab ? 1 : gs->g;
+    a->dp = !gs->vocab;  // the vocabulary-parallel gang reports exact micro-batch grad norms
+    a->fmax_valid = false;
     return FM_OK;
     FM_GUARD_END
 }
@@ -136,7 +145,7 @@ int fm_gang_connect(fm_agent* a, const uint8_t* blobs, uint64_t blob_len) {
         // my slot in o's receive buffer: senders in rank order, skipping o itself
         const int idx = gs->rank < o ? gs->rank : gs->rank - 1;
         const int64_t o_rows = gs->lo[o + 1] - gs->lo[o];
-        gs->peer_slot[o] = static_cast<float*>(rbase) + static_cast<size_t>(idx) * o_rows * a->D;
+        gs->peer_slot[o] = gs->vocab ? nullptr : static_cast<float*>(rbase) + static_cast<size_t>(idx) * o_rows * a->D;
         gs->peer_w16[o] = reinterpret_cast<__nv_bfloat16*>(static_cast<uint8_t*>(sbase) + b.w16_off);
         gs->peer_base[o] = static_cast<uint8_t*>(sbase);
     }
@@ -194,6 +203,11 @@ int fm_gang_gather_state(fm_agent* a) {
                                     static_cast<size_t>(r1 - r0) * row, cudaMemcpyDefault, c->stream));
         }
     }
+    if (gs->vocab && a->W16) {
+        // each rank kept only its own W16^T columns: rebuild the whole shadow from W
+        FM_CUDA(launch_w16t(a->W, a->V, a->D, a->W16, w16_ld(a), c->num_sms, c->stream));
+        a->fmax_valid = false;
+    }
     FM_CUDA(cudaStreamSynchronize(c->stream));
     return FM_OK;
     FM_GUARD_END
@@ -219,6 +233,7 @@ int fm_gang_detach(fm_agent* a) {
     a->shard_rank = 0;
     a->shard_count = 1;
     a->dp = false;
+    a->fmax_valid = false;
     return FM_OK;
 }
 

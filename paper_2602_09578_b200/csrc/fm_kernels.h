@@ -50,6 +50,10 @@ struct LseArgs {
     int64_t row_lo;
     float clip_eps;
     double* loss_acc;  // += objective (nullable)
+    // vocabulary-parallel gang: partial_out != NULL -> write [row sum, taken logit] as
+    // [2][Mpad] and stop (for the all-reduce); sum_in != NULL -> take them from there
+    float* partial_out = nullptr;
+    const float* sum_in = nullptr;
 };
 
 // K-gather: decode the selected records' token payloads straight out of the
@@ -104,6 +108,9 @@ struct BandArgs {
     __nv_bfloat16* aseg;      // A' [K'][ld_a]
     int64_t ld_a;
     int64_t dbg_kp = 0, dbg_D = 0;  // A' rows and features (debug-build bounds checks)
+    // vocabulary-parallel gang: w16t and aseg point at this rank's first column, V is its
+    // range's width and actions are taken relative to col_base
+    int64_t col_base = 0;
 };
 cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s);
 // K-stats partials per row (one per consumer warp of every vocabulary slice).

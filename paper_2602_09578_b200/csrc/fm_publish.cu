@@ -115,11 +115,19 @@ int fm_publish_into(fm_agent* a, fm_weights* w) {
         FM_CUDA(cudaGetLastError());
         count_launch();
         if (sharded) FM_CUDA(cudaFreeAsync(src, s));
-    } else if (a->W16) {
+    } else if (a->W16 && !(sharded && a->gang->vocab)) {
         // the bf16 shadow IS bf16(W) (same double -> float -> bf16 rounding; full replica in a
-        // gang), held transposed: back to the payload's [V][D]
+        // token gang), held transposed: back to the payload's [V][D]
         FM_CUDA(launch_w16t_untranspose(a->W16, a->V, a->D, w16_ld(a), static_cast<__nv_bfloat16*>(w->buf), s));
         count_launch();
+    } else if (sharded) {
+        // vocabulary gang: each rank holds its own shadow columns only — from the owners' W rows
+        double* src = nullptr;
+        FM_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&src), a->P * 8, s));
+        if (int st = copy_state(a, 0, 8, src, s)) return st;
+        FM_CUDA(launch_to_bf16(src, static_cast<__nv_bfloat16*>(w->buf), a->P, c->num_sms, s));
+        count_launch();
+        FM_CUDA(cudaFreeAsync(src, s));
     } else {
         FM_CUDA(launch_to_bf16(a->W, static_cast<__nv_bfloat16*>(w->buf), a->P, c->num_sms, s));
         count_launch();

@@ -181,6 +181,7 @@ void ws_free(Workspace& w) {
     cudaFree(w.logp64);
     cudaFree(w.sd);
     cudaFree(w.dpn);
+    cudaFree(w.lse_red);
     w = Workspace{};
 }
 
@@ -205,6 +206,8 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D, int n_samples
     std::swap(keep.old_logp, w.old_logp);
     std::swap(keep.dpn, w.dpn);
     keep.dpn_cap = w.dpn_cap;
+    std::swap(keep.lse_red, w.lse_red);
+    keep.lse_red_cap = w.lse_red_cap;
     keep.prow_cap = w.prow_cap;
     keep.pvocab_cap = w.pvocab_cap;
     keep.pparam_cap = w.pparam_cap;
@@ -745,6 +748,22 @@ int fm_agent_read_moments(fm_agent* a, float* m, float* v, int64_t* step) {
     return FM_OK;
 }
 
+}  // extern "C"
+
+// fp32 dW to the host; a vocabulary gang's rows live with their owners
+static int read_dw_f32(fm_agent* a, float* g) {
+    if (a->gang && a->gang->connected && a->gang->vocab) {
+        const size_t off = static_cast<size_t>(static_cast<uint8_t*>(a->dW) - static_cast<uint8_t*>(a->slot->base));
+        if (int st = copy_state(a, off, 4, g, a->ctx->stream)) return st;
+        FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
+        return FM_OK;
+    }
+    FM_CUDA(cudaMemcpy(g, a->dW, a->P * 4, cudaMemcpyDeviceToHost));
+    return FM_OK;
+}
+
+extern "C" {
+
 int fm_agent_read_grad(fm_agent* a, double* g) {
     FM_GUARD_BEGIN
     if (int st = check_active(a)) return st;
@@ -758,7 +777,7 @@ int fm_agent_read_grad(fm_agent* a, double* g) {
         FM_CUDA(cudaMemcpy(g, a->dW, a->P * 8, cudaMemcpyDeviceToHost));
     } else {
         std::vector<float> tmp(a->P);
-        FM_CUDA(cudaMemcpy(tmp.data(), a->dW, a->P * 4, cudaMemcpyDeviceToHost));
+        if (int st = read_dw_f32(a, tmp.data())) return st;
         for (uint64_t i = 0; i < a->P; ++i) g[i] = tmp[i];
     }
     return FM_OK;
@@ -775,7 +794,7 @@ int fm_agent_read_grad_f32(fm_agent* a, float* g) {
         std::fill(g, g + a->P, 0.f);
         return FM_OK;
     }
-    FM_CUDA(cudaMemcpy(g, a->dW, a->P * 4, cudaMemcpyDeviceToHost));
+    if (int st = read_dw_f32(a, g)) return st;
     return FM_OK;
     FM_GUARD_END
 }
@@ -902,6 +921,17 @@ int ws_reserve_dpnorm(fm_ctx* c, uint64_t P) {
     return FM_OK;
 }
 
+int ws_reserve_lsered(fm_ctx* c, int64_t Mpad) {
+    Workspace& w = c->ws;
+    if (w.lse_red_cap >= Mpad) return FM_OK;
+    FM_CUDA(cudaStreamSynchronize(c->stream));
+    cudaFree(w.lse_red);
+    w.lse_red = nullptr;
+    if (dalloc(&w.lse_red, static_cast<size_t>(2 * Mpad))) return fail(FM_ERR_DEVICE_OOM, "vocabulary-gang lse scratch");
+    w.lse_red_cap = Mpad;
+    return FM_OK;
+}
+
 // A gang rank's partials of the peers' rows, shipped with plain NVLink copies
 // into their receive slots, then the gang barrier.
 int gang_copy_exchange(fm_agent* a) {
@@ -1011,12 +1041,18 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             const uint64_t ldz = round_up(a->V, 8);
             const int64_t Qcap = Mpad + 3 * static_cast<int64_t>(n);
             const int nblk = static_cast<int>((a->D + 255) / 256);
+            // vocabulary-parallel gang: this rank's columns [c0, c1) of every row
+            GangState* vg = (a->gang && a->gang->connected && a->gang->vocab) ? a->gang : nullptr;
+            const int64_t c0 = vg ? vg->lo[vg->rank] : 0;
+            const int64_t c1 = vg ? vg->lo[vg->rank + 1] : static_cast<int64_t>(a->V);
             if (!a->fmax_valid) {
                 // per-feature maxima of the shadow (the rows' softmax bounds), once per
-                // shadow generation (update, set_weights, swap-in, migration)
+                // shadow generation (update, set_weights, swap-in, migration); a vocabulary
+                // gang takes the max over its ranks' column ranges
                 KScope k(c, K_GATHER, s);
-                FM_CUDA(launch_fmax(a->W16, static_cast<int64_t>(a->D), static_cast<int64_t>(a->V),
+                FM_CUDA(launch_fmax(a->W16 + c0, static_cast<int64_t>(a->D), c1 - c0,
                                     static_cast<int64_t>(w16_ld(a)), a->fmax, s));
+                if (vg) FM_NCCL(ncclAllReduce(a->fmax, a->fmax, a->D, ncclFloat32, ncclMax, gang_comm(vg), s));
                 a->fmax_valid = true;
                 count_launch();
             }
@@ -1032,10 +1068,11 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 count_launch(4);
             }
             BandArgs ba{};
-            ba.w16t = a->W16;
+            ba.w16t = a->W16 + c0;
             ba.ldw = static_cast<int64_t>(w16_ld(a));
             ba.zero_row = w.zero_row;
-            ba.V = static_cast<int64_t>(a->V);
+            ba.V = c1 - c0;
+            ba.col_base = c0;
             ba.pos_feat = w.pos_feat;
             ba.q0 = w.q0;
             ba.action = w.action;
@@ -1044,29 +1081,46 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             ba.M = M;
             ba.ld_stats = Mpad;
             ba.stats = w.stats;
-            ba.stats_ld = band_stats_ld(static_cast<int64_t>(a->V));
+            ba.stats_ld = band_stats_ld(c1 - c0);
             ba.zact = w.zact;
             ba.lse = w.lse;
             ba.coef_eff = w.coef_eff;
             ba.pos_slot = w.pos_slot;
-            ba.aseg = w.aseg;
+            ba.aseg = w.aseg + c0;
             ba.ld_a = static_cast<int64_t>(ldz);
             ba.dbg_kp = w.kp_cap;
             ba.dbg_D = static_cast<int64_t>(a->D);
             FM_CUDA(cudaEventRecord(c->ev_gemm, s));  // swap copies may start here (fm_agent_suspend)
             c->gemm_seq = ++c->op_seq;
+            const bool cols = c1 > c0;  // (a vocabulary-gang rank may own no columns)
             {
                 // K-stats: per-(row, 256-column tile) softmax partials + the taken token's logit
                 KScope k(c, K_STATS, s);
-                FM_CUDA(launch_band(ba, false, s));
+                if (vg) FM_CUDA(cudaMemsetAsync(w.zact, 0, Mpad * 4, s));  // the action's owner writes it
+                if (cols) FM_CUDA(launch_band(ba, false, s));
             }
             {
                 KScope k(c, K_LSE, s);
                 LseArgs L{w.zact, w.stats, ba.stats_ld, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
                           clip ? w.old_logp : nullptr, row_lo, a->clip_eps, scal + 1};
+                if (vg) {
+                    // vocabulary gang: per row (sum over my columns, taken logit or 0), summed
+                    // over the gang, then every rank finishes the same lse / log-prob / coef
+                    if (int st = ws_reserve_lsered(c, Mpad)) return st;
+                    LseArgs P = L;
+                    P.partial_out = w.lse_red;
+                    P.loss_acc = nullptr;
+                    if (cols) {
+                        FM_CUDA(launch_lse(P, s));
+                    } else {
+                        FM_CUDA(cudaMemsetAsync(w.lse_red, 0, 2 * Mpad * 4, s));
+                    }
+                    FM_NCCL(ncclAllReduce(w.lse_red, w.lse_red, 2 * Mpad, ncclFloat32, ncclSum, gang_comm(vg), s));
+                    L.sum_in = w.lse_red;
+                }
                 FM_CUDA(launch_lse(L, s));
             }
-            {
+            if (cols) {
                 // K-band: per-position gradient rows H into the feature blocks' A' segments
                 KScope k(c, K_BAND, s);
                 FM_CUDA(launch_band(ba, true, s));
@@ -1074,13 +1128,13 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             // K-GEMM2: dW[v][f] (+)= sum over block(f)'s positions of H[q][v] * onehot[q][f];
             // the first contribution of the step overwrites
             GemmArgs g2{};
-            g2.M = static_cast<int>(a->V);
+            g2.M = static_cast<int>(c1 - c0);
             g2.N = static_cast<int>(a->D);
             g2.K = 0;
             // raster: the 256-feature column tiles of a vocab row block run together, so the
             // row block's dW stripe and A' columns stay L2-local
             g2.group_m = env_int("FM_G2_GROUP_M", 1);
-            g2.out = static_cast<float*>(a->dW);
+            g2.out = static_cast<float*>(a->dW) + static_cast<size_t>(c0) * a->D;
             g2.ld_out = static_cast<long long>(a->D);
             g2.accumulate = a->dw_valid ? 1 : 0;
             g2.sumsq = scal;
@@ -1091,7 +1145,8 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             // this rank's contribution to a scratch, which is added to dW, all-reduced and
             // measured (training.hpp:417); a gang's exchange then runs as plain copies
             const bool dp_norms = a->norm_comm != nullptr;
-            const bool exchange = !dp_norms && a->gang && a->gang->connected && a->samples + n == G;
+            const bool exchange = !dp_norms && !vg && a->gang && a->gang->connected && a->samples + n == G;
+            if (dp_norms && vg) return fail(FM_ERR_CONFIG_ERROR, "a vocabulary gang reports exact norms already");
             if (dp_norms) {
                 if (int st = ws_reserve_dpnorm(c, a->P)) return st;
                 g2.out = w.dpn;
@@ -1108,11 +1163,16 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             {
                 KScope k(c, K_GEMM2, s);
                 CUtensorMap tSA, tSB, tC;
-                if (!make_tmap_bf16_kmajor(&tSA, w.aseg, static_cast<uint64_t>(w.kp_cap), a->V, 64, ldz) ||
-                    !make_tmap_bf16_kmajor(&tSB, w.bseg, static_cast<uint64_t>(w.kp_cap), 256, 64) ||
-                    !make_tmap_f32_out(&tC, g2.out, a->V, a->D, a->D))
-                    return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-                FM_CUDA(gemm_kseg_launch(tSA, tSB, tC, g2, c->num_sms, s));
+                const uint64_t mc = static_cast<uint64_t>(c1 - c0);
+                if (cols) {
+                    if (!make_tmap_bf16_kmajor(&tSA, w.aseg + c0, static_cast<uint64_t>(w.kp_cap), mc, 64, ldz) ||
+                        !make_tmap_bf16_kmajor(&tSB, w.bseg, static_cast<uint64_t>(w.kp_cap), 256, 64) ||
+                        !make_tmap_f32_out(&tC, g2.out, mc, a->D, a->D))
+                        return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+                    FM_CUDA(gemm_kseg_launch(tSA, tSB, tC, g2, c->num_sms, s));
+                }
+                // the micro-batch's grad norm^2 over the whole vocabulary (training.hpp:417)
+                if (vg) FM_NCCL(ncclAllReduce(scal, scal, 1, ncclFloat64, ncclSum, gang_comm(vg), s));
             }
             if (exchange) {
                 a->dw_valid = true;
@@ -1137,7 +1197,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
         if (int st = ws_reserve_dpnorm(c, a->P)) return st;
         FM_CUDA(cudaMemsetAsync(w.dpn, 0, a->P * 4, s));
         if (int st = dp_norm_finish(a, scal, a->samples + n == G)) return st;
-    } else if (a->gang && a->gang->connected && a->samples + n == G) {
+    } else if (a->gang && a->gang->connected && !a->gang->vocab && a->samples + n == G) {
         // this rank got no rows of the step's last micro-batch: ship its partials
         // for the peers' rows with plain NVLink copies, then join the barrier
         if (int st = gang_copy_exchange(a)) return st;
@@ -1336,12 +1396,15 @@ static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, doubl
         // receive slots); the new W16^T columns of those rows go to every replica
         GangState* gs = a->gang;
         const uint64_t r0 = static_cast<uint64_t>(gs->lo[gs->rank]), r1 = static_cast<uint64_t>(gs->lo[gs->rank + 1]);
+        // (vocabulary gang: the rows' gradient is complete here and only this rank reads
+        // their W16^T columns — no receive slots, no peer writes)
         ShardPeers peers{};
-        for (int o = 0; o < gs->g; ++o)
-            if (o != gs->rank) peers.w16t[peers.n++] = gs->peer_w16[o];
-        FM_CUDA(launch_adam<float>(a->W, a->m, a->v, static_cast<float*>(a->dW), a->V, a->D, r0, r1, gs->recv,
-                                   gs->g - 1, a->W16, w16_ld(a), peers, lr, b1, b2, eps, bc1, bc2, 0, a->d_upd,
-                                   c->num_sms, s));
+        if (!gs->vocab)
+            for (int o = 0; o < gs->g; ++o)
+                if (o != gs->rank) peers.w16t[peers.n++] = gs->peer_w16[o];
+        FM_CUDA(launch_adam<float>(a->W, a->m, a->v, static_cast<float*>(a->dW), a->V, a->D, r0, r1,
+                                   gs->vocab ? nullptr : gs->recv, gs->vocab ? 0 : gs->g - 1, a->W16, w16_ld(a),
+                                   peers, lr, b1, b2, eps, bc1, bc2, 0, a->d_upd, c->num_sms, s));
         // global grad norm^2; doubles as the barrier after the peers' W16^T writes
         FM_NCCL(ncclAllReduce(a->d_upd, a->d_upd, 1, ncclFloat64, ncclSum, gang_comm(gs), s));
     } else {

@@ -96,6 +96,8 @@ struct Workspace {
     int sd_cap = 0;
     float* dpn = nullptr;  // exact DP grad norm: this micro-batch's contribution [P]
     uint64_t dpn_cap = 0;
+    float* lse_red = nullptr;  // vocabulary gang: per-row (sum, taken logit) partials [2][cap]
+    int64_t lse_red_cap = 0;
 };
 
 // Per-kernel device timing (bench.py's roofline): event pairs recorded on the
@@ -214,6 +216,13 @@ struct GangState {
     uint8_t* peer_base[8] = {};  // peer o's training slot (same layout as ours)
     int* d_token = nullptr;      // 1-int all-reduce used as a device barrier
     bool connected = false;
+    // vocabulary-parallel mode (fm_gang_attach_mode 1): every rank trains ALL rows of
+    // each micro-batch on its vocabulary range [lo[rank], lo[rank+1]) — K-stats /
+    // K-band on those columns, K-GEMM2 and K-adam on those rows of dW / W, its own
+    // W16^T columns; per micro-batch only the rows' partial softmax sums and the taken
+    // tokens' logits are all-reduced (2 x Mpad floats), plus the micro-batch's
+    // squared gradient norm.  No bulk NVLink traffic, no receive buffers.
+    bool vocab = false;
 };
 
 struct fm_agent {

@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
         const int r = rstart + i;
         m_q0[i] = r < A.M ? __ldg(A.q0 + r) : INT32_MAX - 8;
         if (i < nrows) {
-            m_act[i] = __ldg(A.action + r);
+            m_act[i] = __ldg(A.action + r) - static_cast<int32_t>(A.col_base);  // this range's column
             m_rs[i] = __ldg(A.rscale + r);
             if constexpr (kGrad) {
                 m_lse[i] = __ldg(A.lse + r);

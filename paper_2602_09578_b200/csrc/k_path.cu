@@ -159,25 +159,42 @@ __global__ void __launch_bounds__(256) lse_kernel(const LseArgs L) {
     if (r < L.Mpad) {
         const RowBuffers& rows = L.rows;
         if (r >= L.M) {  // padding rows
+            if (L.partial_out) {
+                L.partial_out[r] = 0.f;
+                L.partial_out[L.Mpad + r] = 0.f;
+                return;
+            }
             rows.lse[r] = 0.f;
             rows.logp[r] = 0.f;
             rows.coef_eff[r] = 0.f;
         } else {
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-            int t = 0;
-            for (; t + 4 <= L.stats_ld; t += 4) {
-                s0 += __ldg(L.stats + static_cast<int64_t>(t) * L.Mpad + r);
-                s1 += __ldg(L.stats + static_cast<int64_t>(t + 1) * L.Mpad + r);
-                s2 += __ldg(L.stats + static_cast<int64_t>(t + 2) * L.Mpad + r);
-                s3 += __ldg(L.stats + static_cast<int64_t>(t + 3) * L.Mpad + r);
+            float sum, za;
+            if (L.sum_in) {  // vocabulary gang: the all-reduced row sum and taken logit
+                sum = L.sum_in[r];
+                za = L.sum_in[L.Mpad + r];
+            } else {
+                float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+                int t = 0;
+                for (; t + 4 <= L.stats_ld; t += 4) {
+                    s0 += __ldg(L.stats + static_cast<int64_t>(t) * L.Mpad + r);
+                    s1 += __ldg(L.stats + static_cast<int64_t>(t + 1) * L.Mpad + r);
+                    s2 += __ldg(L.stats + static_cast<int64_t>(t + 2) * L.Mpad + r);
+                    s3 += __ldg(L.stats + static_cast<int64_t>(t + 3) * L.Mpad + r);
+                }
+                for (; t < L.stats_ld; ++t) s0 += __ldg(L.stats + static_cast<int64_t>(t) * L.Mpad + r);
+                sum = (s0 + s1) + (s2 + s3);
+                za = L.zact[r];
+                if (L.partial_out) {  // this rank's columns only: to the all-reduce
+                    L.partial_out[r] = sum;
+                    L.partial_out[L.Mpad + r] = za;
+                    return;
+                }
             }
-            for (; t < L.stats_ld; ++t) s0 += __ldg(L.stats + static_cast<int64_t>(t) * L.Mpad + r);
-            const float sum = (s0 + s1) + (s2 + s3);
             const int a = rows.action[r];
             const double adv = L.sd[rows.sample[r]].adv;
             const float lse = rows.mrow[r] + __logf(sum);
             const bool valid = a >= 0 && a < L.V;
-            const float lp = valid ? L.zact[r] - lse : 0.f;  // policy.hpp:72-75, fp32 logit
+            const float lp = valid ? za - lse : 0.f;  // policy.hpp:72-75, fp32 logit
             float ce = rows.coef[r];
             if (L.old_logp && L.clip_eps > 0.f) {
                 // PPO clipped-ratio surrogate min(rho*A, clip(rho,1-e,1+e)*A): the

@@ -1,10 +1,13 @@
 """Multi-GPU data-parallel parity (run under torchrun, >= 2 GPUs).
 
 Every rank of one gang trains its token-balanced shard of each polled
-micro-batch of the V=256/D=64 golden fixture (2 global steps).  Two modes:
+micro-batch of the V=256/D=64 golden fixture (2 global steps).  Three modes:
   allreduce  NCCL all-reduce of dW + replicated Adam (`fm_agent_allreduce_grad`)
   gang       fused GEMM2 -> reduce-scatter over NVLink peer memory + sharded
              Adam with the bf16 all-gather fused in (`fm_gang_attach/connect`)
+  vocab      vocabulary-parallel gang (`fm_gang_attach_mode(.., 1, ..)`): every
+             rank trains every row on its 256-aligned vocabulary columns; the
+             softmax sums are all-reduced per row, dW / Adam stay column-local
 Rank 0 checks delta-W (assembled from the owners' rows in gang mode) and the
 update grad norms against the compiled-reference golden run, with the same
 tolerances as the 1-GPU tensor-core path."""
@@ -29,7 +32,17 @@ from fixture_runner import payload  # noqa: E402
 from test_gpu_path import _oracle_grad_step0, rel_fro  # noqa: E402
 
 
-def gang_vs_allreduce(ctx, comm, rank, world) -> bool:
+def _attach(L, h, comm, world, gmode):
+    n = C.c_uint64()
+    _lib.check(L.fm_gang_attach_mode(h, comm, gmode, None, 0, C.byref(n)))
+    blob = (C.c_uint8 * n.value)()
+    _lib.check(L.fm_gang_attach_mode(h, comm, gmode, blob, n.value, C.byref(n)))
+    blobs = [None] * world
+    dist.all_gather_object(blobs, bytes(blob))
+    _lib.check(L.fm_gang_connect(h, b"".join(blobs), n.value))
+
+
+def gang_vs_allreduce(ctx, comm, rank, world, gang_mode="gang") -> bool:
     """V = 1000 (4 GEMM2 row tiles, so every rank owns rows): one global step
     through the fused gang path and through all-reduce + replicated Adam from
     the same W0 must give the same update (different summation order only)."""
@@ -41,18 +54,12 @@ def gang_vs_allreduce(ctx, comm, rank, world) -> bool:
     batches = [[(rng.integers(0, V, 5).astype(np.int32), rng.integers(0, V, 70).astype(np.int32), float(a))
                 for a in rng.normal(size=mb)] for _ in range(G // mb)]
     outs = {}
-    for mode in ("allreduce", "gang"):
+    for mode in ("allreduce", gang_mode):
         h = C.c_void_p()
         _lib.check(L.fm_agent_create(ctx.handle, mode.encode(), V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
         _lib.check(L.fm_agent_set_weights(h, np.ascontiguousarray(W0).ctypes.data))
-        if mode == "gang":
-            n = C.c_uint64()
-            _lib.check(L.fm_gang_attach(h, comm, None, 0, C.byref(n)))
-            blob = (C.c_uint8 * n.value)()
-            _lib.check(L.fm_gang_attach(h, comm, blob, n.value, C.byref(n)))
-            blobs = [None] * world
-            dist.all_gather_object(blobs, bytes(blob))
-            _lib.check(L.fm_gang_connect(h, b"".join(blobs), n.value))
+        if mode != "allreduce":
+            _attach(L, h, comm, world, 1 if mode == "vocab" else 0)
         else:
             _lib.check(L.fm_agent_set_shard(h, rank, world))
         for bt in batches:
@@ -65,7 +72,7 @@ def gang_vs_allreduce(ctx, comm, rank, world) -> bool:
         W = np.empty(V * D)
         _lib.check(L.fm_agent_read_weights(h, W.ctypes.data))
         W = W.reshape(V, D)
-        if mode == "gang":
+        if mode != "allreduce":
             tiles = (V + 255) // 256
             lo = [min(V, (tiles * o // world) * 256) for o in range(world + 1)]
             parts = [None] * world
@@ -73,12 +80,12 @@ def gang_vs_allreduce(ctx, comm, rank, world) -> bool:
             W = torch.cat(parts).numpy()
         outs[mode] = (W - W0, gn.value)
         L.fm_agent_destroy(h)
-    e = rel_fro(outs["gang"][0], outs["allreduce"][0])
-    en = abs(outs["gang"][1] - outs["allreduce"][1]) / outs["allreduce"][1]
+    e = rel_fro(outs[gang_mode][0], outs["allreduce"][0])
+    en = abs(outs[gang_mode][1] - outs["allreduce"][1]) / outs["allreduce"][1]
     good = e < 1e-2 and en < 1e-4
     if rank == 0:
-        print(f"gang vs allreduce (V=1000): dW rel {e:.3e}, grad-norm rel {en:.3e} -> {'OK' if good else 'FAIL'}",
-              flush=True)
+        print(f"{gang_mode} vs allreduce (V=1000): dW rel {e:.3e}, grad-norm rel {en:.3e} -> "
+              f"{'OK' if good else 'FAIL'}", flush=True)
     return good
 
 
@@ -107,15 +114,8 @@ def main():
     _lib.check(L.fm_agent_set_weights(h, W0.ctypes.data))
     tiles = (V + 255) // 256
     lo = [min(V, (tiles * o // world) * 256) for o in range(world + 1)]
-    if mode == "gang":
-        n = C.c_uint64()
-        _lib.check(L.fm_gang_attach(h, comm, None, 0, C.byref(n)))
-        blob = (C.c_uint8 * n.value)()
-        _lib.check(L.fm_gang_attach(h, comm, blob, n.value, C.byref(n)))
-        blobs = [None] * world
-        dist.all_gather_object(blobs, bytes(blob))
-        allb = b"".join(blobs)
-        _lib.check(L.fm_gang_connect(h, allb, n.value))
+    if mode in ("gang", "vocab"):
+        _attach(L, h, comm, world, 1 if mode == "vocab" else 0)
     else:
         _lib.check(L.fm_agent_set_shard(h, rank, world))
     if exact_norms:
@@ -132,7 +132,7 @@ def main():
             _lib.check(L.fm_train_micro_batch(h, arr, mb, G, C.byref(t)))
             tickets.append(t.value)
         _lib.check(L.fm_agent_allreduce_grad(h, comm))  # no-op in gang mode
-        if mode == "allreduce":
+        if mode in ("allreduce", "vocab"):  # (vocab: read_grad assembles the owners' rows)
             g = np.empty(V * D)
             _lib.check(L.fm_agent_read_grad(h, g.ctypes.data))
             grads.append(g.reshape(V, D))
@@ -150,7 +150,7 @@ def main():
     _lib.check(L.fm_agent_read_weights(h, W.ctypes.data))
     W = W.reshape(V, D)
     full_ok = True
-    if mode == "gang":  # each rank maintains only its own rows of the master weights
+    if mode in ("gang", "vocab"):  # each rank maintains only its own rows of the master weights
         mine = torch.tensor(W[lo[rank]:lo[rank + 1]].copy())
         parts = [None] * world
         dist.all_gather_object(parts, mine)
@@ -185,7 +185,7 @@ def main():
             e_g = rel_fro(grads[0], _oracle_grad_step0(f))
             ok = ok and e_g <= 2e-2
             msg += f", grad rel {e_g:.3e}"
-        if exact_norms:  # the reference's micro-batch grad norms (training.hpp:417), not NaN
+        if exact_norms or mode == "vocab":  # the reference's micro-batch grad norms (training.hpp:417)
             e_m = float(np.max(np.abs(mbn - f["mb_grad_norm"]) / f["mb_grad_norm"]))
             ok = ok and e_m <= 2e-2
             msg += f", micro-batch grad-norm rel {e_m:.3e}"
@@ -201,8 +201,8 @@ def main():
         if not same:
             print(f"rank {rank}: weights diverged from rank 0", flush=True)
     L.fm_agent_destroy(h)
-    if mode == "gang":
-        ok = ok and gang_vs_allreduce(ctx, comm, rank, world)
+    if mode in ("gang", "vocab"):
+        ok = ok and gang_vs_allreduce(ctx, comm, rank, world, mode)
     L.fm_comm_destroy(comm)
     ctx.close()
     okt = torch.tensor([1 if (ok and same and full_ok) else 0])

@@ -20,16 +20,24 @@ def _ngpu():
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
 @pytest.mark.parametrize("mode,norms,port", [("allreduce", "", 29511), ("gang", "", 29512),
-                                           ("allreduce", "norms", 29514), ("gang", "norms", 29515)])
-def test_dp_gang_parity(mode, norms, port):
+                                           ("allreduce", "norms", 29514), ("gang", "norms", 29515),
+                                           ("vocab", "", 29516)])
+def test_dp_gang_parity(mode, norms, port, n=2):
     """DP gang of 2 vs the reference golden run; with "norms" the exact
-    per-micro-batch grad norms (fm_agent_set_dp_norms) against the reference's."""
-    n = 2
+    per-micro-batch grad norms (fm_agent_set_dp_norms) against the reference's;
+    "vocab" is the vocabulary-parallel gang (exact norms by construction)."""
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
                         "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "tests" / "dp_check.py"),
                         mode] + ([norms] if norms else []), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs >= 4 GPUs")
+@pytest.mark.parametrize("mode,port", [("gang", 29517), ("vocab", 29518)])
+def test_dp_gang_parity_4(mode, port):
+    """The same checks with a gang of 4 (V=1000: one 256-row tile per rank)."""
+    test_dp_gang_parity(mode, "", port, n=4)
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
