@@ -291,9 +291,9 @@ def run_ours(args, dist: Dist) -> dict | None:
             active[a] = False
     ctx.synchronize()
 
-    # device tier: each agent parks right after its update, so K-adam writes the new
-    # state into the parking buffer (fm_apply_update_park) instead of a copy-out
-    park_fused = swap and len(order) > 1 and tier == _lib.TIER_DEVICE and args.park == "fused"
+    # device tier: each agent is suspended right after its update (fm_apply_update_park);
+    # its state stays in its HBM slot and the next activation rebinds it
+    park_fused = swap and len(order) > 1 and tier == _lib.TIER_DEVICE
     tokens_per_step = 0
     FS = _lib.fm_sample
     htime = {}
@@ -336,7 +336,6 @@ def run_ours(args, dist: Dist) -> dict | None:
             if a in comms:
                 check(timed("allreduce", L.fm_agent_allreduce_grad, h, comms[a]))
             if park_fused and a not in comms:
-                # the swap-out fused into K-adam: the new state lands in the parking buffer
                 check(timed("update", L.fm_apply_update_park, h, G, cfg.lr, 0.9, 0.999, 1e-8, None, None))
                 active[a] = False
             else:
@@ -1194,7 +1193,7 @@ def run_e2e(args, cfg, ctx, mine, handles, place, comms, dist, tier) -> dict:
             if a in comms:
                 check(L.fm_agent_allreduce_grad(h, comms[a]))
             gn = C.c_double()
-            if (args.park == "fused" and len(order) > 1 and tier == _lib.TIER_DEVICE and a not in comms):
+            if len(order) > 1 and tier == _lib.TIER_DEVICE and a not in comms:
                 check(L.fm_apply_update_park(h, G, cfg.lr, 0.9, 0.999, 1e-8, C.byref(gn), None))  # D2H of the result
                 active[a] = False
             else:
@@ -1384,8 +1383,9 @@ def config_obj(cfg, args) -> dict:
                         f"({cfg.params / 1e6:.1f}M params/agent), GRPO k={cfg.group_k}, micro-batch "
                         f"{cfg.micro_batch}/global {cfg.global_batch}, response {cfg.resp_len} tokens, "
                         f"state swap tier={args.tier}"
-                        + (f" (swap-out {'fused into K-adam' if getattr(args, 'park', 'copy') == 'fused' else 'copy'})"
-                           if args.tier == "device" else ""),
+                        + (" (suspend keeps the state in its HBM slot, activate rebinds it: no copy)"
+                           if args.tier == "device" else
+                           " (pinned host parking over PCIe, copy engines)" if args.tier == "host" else ""),
             "agents": na, "vocab": cfg.vocab, "feat": cfg.feat, "micro_batch": cfg.micro_batch,
             "global_batch": cfg.global_batch, "resp_len": cfg.resp_len,
             "formulation": formulation(args),
@@ -1408,8 +1408,6 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--park", default="fused", choices=["fused", "copy"],
-                    help="device tier: K-adam writes the parked state (fused) or a copy-out after the update")
     ap.add_argument("--tier", default="device", choices=["device", "host", "resident"],
                     help="parking tier of the state swap; 'resident' = no swaps (analysis only)")
     ap.add_argument("--resp-len", type=int, default=0)

@@ -131,14 +131,8 @@ cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D,
 // the local partial plus nslots receive slots ([nslots][r1-r0][D], a DP
 // gang's reduce-scatter); the transposed bf16 shadow W16^T [D][ldw] is
 // written (locally and into the peers' replicas over NVLink: the all-gather
-// fused into the optimizer) through a shared-memory transpose; the new w / m
-// / v go to dst instead of in place (the swap-out fused into the optimizer);
-// the gradient is zeroed (parity mode).  Accumulates sum(g^2) into *gsq.
-struct AdamDst {
-    double* w;
-    float* m;
-    float* v;
-};
+// fused into the optimizer) through a shared-memory transpose; the gradient
+// is zeroed (parity mode).  Accumulates sum(g^2) into *gsq.
 // Peer W16^T replicas (NVLink-mapped base pointers) of a DP gang, excluding self.
 struct ShardPeers {
     int n;
@@ -148,7 +142,7 @@ template <typename G>
 cudaError_t launch_adam(double* w, float* m, float* v, G* g, uint64_t V, uint64_t D, uint64_t r0, uint64_t r1,
                         const float* recv, int nslots, __nv_bfloat16* w16t, uint64_t ldw, ShardPeers peers,
                         double lr, double b1, double b2, double eps, double bc1, double bc2, int zero_grad,
-                        double* gsq, int num_sms, cudaStream_t s, const AdamDst* dst = nullptr);
+                        double* gsq, int num_sms, cudaStream_t s);
 
 // W16^T [D][ldw] = bf16(W) for W [V][D] f64 (shadow refresh: set_weights, host-tier swap-in).
 cudaError_t launch_w16t(const double* w, uint64_t V, uint64_t D, __nv_bfloat16* w16t, uint64_t ldw, int num_sms,

@@ -584,8 +584,15 @@ int agent_alloc_device(fm_agent* a, fm_ctx* c, cudaStream_t s) {
     }
     FM_CUDA(cudaStreamWaitEvent(s, pick->ev_free, 0));
     pick->busy = true;
-    a->slot = pick;
-    uint8_t* p = static_cast<uint8_t*>(pick->base);
+    agent_bind_slot(a, pick);
+    a->fmax_valid = false;
+    return FM_OK;
+}
+
+// Points the agent's W / m / v / dW / W16^T / fmax into slot sl.
+void agent_bind_slot(fm_agent* a, Slot* sl) {
+    a->slot = sl;
+    uint8_t* p = static_cast<uint8_t*>(sl->base);
     const size_t P = a->P;
     a->W = reinterpret_cast<double*>(p);
     p += align256(P * 8);
@@ -598,8 +605,16 @@ int agent_alloc_device(fm_agent* a, fm_ctx* c, cudaStream_t s) {
     a->W16 = a->precision == FM_PRECISION_BF16_TC ? reinterpret_cast<__nv_bfloat16*>(p) : nullptr;
     p += a->W16 ? align256(w16_bytes(a)) : 0;
     a->fmax = a->W16 ? reinterpret_cast<float*>(p) : nullptr;
+}
+
+void agent_unbind(fm_agent* a) {
+    a->slot = nullptr;
+    a->W = nullptr;
+    a->m = a->v = nullptr;
+    a->dW = nullptr;
+    a->W16 = nullptr;
+    a->fmax = nullptr;
     a->fmax_valid = false;
-    return FM_OK;
 }
 
 // Releases the agent's slot once everything queued on stream s has run.
@@ -611,14 +626,8 @@ void agent_free_device(fm_agent* a, cudaStream_t s) {
     if (a->slot) {
         cudaEventRecord(a->slot->ev_free, s);
         a->slot->busy = false;
-        a->slot = nullptr;
     }
-    a->W = nullptr;
-    a->m = a->v = nullptr;
-    a->dW = nullptr;
-    a->W16 = nullptr;
-    a->fmax = nullptr;
-    a->fmax_valid = false;
+    agent_unbind(a);
 }
 
 // Every operation on an agent goes through here: besides the InactiveGroup
@@ -685,6 +694,12 @@ int fm_agent_destroy(fm_agent* a) {
     if (!a) return FM_OK;
     if (a->lent) fm_agent_migrate_release(a);
     fm_gang_detach(a);
+    if (a->kept) {  // suspended on the device tier: rebind to release the slot below
+        agent_bind_slot(a, a->kept);
+        a->ctx = a->kept_ctx;
+        a->kept = nullptr;
+        a->kept_ctx = nullptr;
+    }
     if (a->ctx) {
         cudaSetDevice(a->ctx->device);
         cudaStreamSynchronize(a->ctx->stream);
@@ -1357,10 +1372,9 @@ int fm_agent_poll_report(fm_agent* a, int64_t ticket, fm_report* out) {
 }
 
 
-// apply_global_update; with park != 0 (device tier, tensor-core agent, no gang)
-// K-adam writes the new W / m / v / W16^T straight into the agent's
-// parking buffer and the agent is suspended — the swap-out fused into the
-// optimizer (no copy-out pass).
+// apply_global_update; with park != 0 (tensor-core agent, no gang) the agent
+// is suspended to the device tier right after K-adam (fm_agent_suspend with
+// FM_TIER_DEVICE: its state stays in its HBM slot).
 static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, double b2, double eps,
                              double* grad_norm_out, int64_t* version_out, bool park) {
     if (int st = check_active(a)) return st;
@@ -1370,16 +1384,10 @@ static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, doubl
     fm_ctx* c = a->ctx;
     if (int st = set_dev(c)) return st;
     cudaStream_t s = c->stream;
-    AdamDst dst{};
-    uint8_t* pk = nullptr;
     if (park) {
         if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang (fm_gang_detach first)");
         if (a->precision != FM_PRECISION_BF16_TC || !a->W16)
             return fail(FM_ERR_INVALID_ARG, "update-and-park needs a tensor-core agent");
-        if (int st = park_reserve(a, c, FM_TIER_DEVICE, c->device, park_bytes_for(a))) return st;
-        pk = static_cast<uint8_t*>(a->park);
-        dst = AdamDst{reinterpret_cast<double*>(pk), reinterpret_cast<float*>(pk + a->P * 8),
-                      reinterpret_cast<float*>(pk + a->P * 12)};
     }
     if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * dw_elem(a), s));
     a->step += 1;
@@ -1408,13 +1416,9 @@ static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, doubl
         // global grad norm^2; doubles as the barrier after the peers' W16^T writes
         FM_NCCL(ncclAllReduce(a->d_upd, a->d_upd, 1, ncclFloat64, ncclSum, gang_comm(gs), s));
     } else {
-        // the next step's first GEMM2 overwrites dW, so no zeroing pass here; with park the
-        // new state goes straight into the parking buffer
-        const size_t dwe = dw_elem(a);
-        __nv_bfloat16* w16_out = park ? reinterpret_cast<__nv_bfloat16*>(pk + a->P * (16 + dwe)) : a->W16;
+        // the next step's first GEMM2 overwrites dW, so no zeroing pass here
         FM_CUDA(launch_adam<float>(a->W, a->m, a->v, static_cast<float*>(a->dW), a->V, a->D, 0, a->V, nullptr, 0,
-                                   w16_out, w16_ld(a), none, lr, b1, b2, eps, bc1, bc2, 0, a->d_upd, c->num_sms, s,
-                                   park ? &dst : nullptr));
+                                   a->W16, w16_ld(a), none, lr, b1, b2, eps, bc1, bc2, 0, a->d_upd, c->num_sms, s));
     }
     count_launch();
     a->dw_valid = false;
@@ -1423,14 +1427,7 @@ static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, doubl
     a->grad_keys.clear();
     a->fmax_valid = false;  // the shadow changed
     FM_CUDA(cudaMemcpyAsync(a->h_upd, a->d_upd, sizeof(double), cudaMemcpyDeviceToHost, s));
-    if (park) {
-        // the parked state is complete when K-adam is: release the slot behind it
-        a->park_w16 = true;
-        FM_CUDA(cudaEventRecord(a->ev_out, s));
-        agent_free_device(a, s);
-        a->active = false;
-        a->ctx = nullptr;
-    }
+    if (park) agent_keep_slot(a);  // suspended to the device tier: the state stays in its slot
     if (grad_norm_out) {
         FM_CUDA(cudaStreamSynchronize(s));
         *grad_norm_out = std::sqrt(*a->h_upd);

@@ -273,6 +273,11 @@ struct fm_agent {
     fm_comm* norm_comm = nullptr;  // exact DP micro-batch grad norms over this communicator
     bool lent = false;             // exported by migration; slot reserved until migrate_release
     Slot* slot = nullptr;
+    // device-tier suspend on the agent's own GPU keeps the training state where it is:
+    // the slot stays reserved (kept) and activation on that context rebinds it
+    Slot* kept = nullptr;
+    fm_ctx* kept_ctx = nullptr;
+    bool kept_fmax = false;
     GangState* gang = nullptr;
 };
 
@@ -323,11 +328,15 @@ uint64_t w16_ld(const fm_agent* a);     // row pitch of W16^T: V rounded up to 8
 size_t w16_bytes(const fm_agent* a);    // D * w16_ld * 2
 int agent_alloc_device(fm_agent* a, fm_ctx* c, cudaStream_t s);
 void agent_free_device(fm_agent* a, cudaStream_t s);
+void agent_bind_slot(fm_agent* a, Slot* sl);
+void agent_unbind(fm_agent* a);
 int check_active(fm_agent* a);
 }  // namespace fm
 
-// ---- parking buffers (fm_swap.cu), also written by the fused update-and-park ----
+// ---- parking buffers (fm_swap.cu) ----
 extern "C" {
+// Device-tier suspend on the agent's own GPU: keep the slot (no copy).
+void agent_keep_slot(fm_agent* a);
 // Park layout: W | m | v | dW | W16^T.
 size_t park_bytes_for(const fm_agent* a);
 // Parking buffer of `bytes` on `tier` (device pdev), reused while it fits.

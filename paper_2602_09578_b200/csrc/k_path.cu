@@ -150,71 +150,81 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
 // ---------------------------------------------------------------------------
 // K-lse
 // ---------------------------------------------------------------------------
-// One lane per row: the partial sums of the row's vocabulary slices are
-// [stats_ld][Mpad], so a warp's 32 rows read 128 contiguous bytes per slice.
+// A block covers 32 rows with 8 warps: warp j sums slices j, j + 8, ... of its
+// lane's row (the partial sums are [stats_ld][Mpad], so a warp reads 128
+// contiguous bytes per slice and the block keeps 8 loads in flight per row),
+// then warp 0 combines the 8 partials and finishes the row.
 __global__ void __launch_bounds__(256) lse_kernel(const LseArgs L) {
-    __shared__ double red[8];
-    const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    __shared__ float part[8][33];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t r = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+    const bool live = r < L.M;
+    if (!L.sum_in) {
+        float s0 = 0.f, s1 = 0.f;
+        if (live) {
+            int t = wid;
+            for (; t + 8 < L.stats_ld; t += 16) {
+                s0 += __ldg(L.stats + static_cast<int64_t>(t) * L.Mpad + r);
+                s1 += __ldg(L.stats + static_cast<int64_t>(t + 8) * L.Mpad + r);
+            }
+            if (t < L.stats_ld) s0 += __ldg(L.stats + static_cast<int64_t>(t) * L.Mpad + r);
+        }
+        part[wid][lane] = s0 + s1;
+        __syncthreads();
+    }
+    if (wid != 0) return;
     double loss = 0.0;
     if (r < L.Mpad) {
         const RowBuffers& rows = L.rows;
-        if (r >= L.M) {  // padding rows
+        if (!live) {  // padding rows
             if (L.partial_out) {
                 L.partial_out[r] = 0.f;
                 L.partial_out[L.Mpad + r] = 0.f;
-                return;
+            } else {
+                rows.lse[r] = 0.f;
+                rows.logp[r] = 0.f;
+                rows.coef_eff[r] = 0.f;
             }
-            rows.lse[r] = 0.f;
-            rows.logp[r] = 0.f;
-            rows.coef_eff[r] = 0.f;
         } else {
             float sum, za;
             if (L.sum_in) {  // vocabulary gang: the all-reduced row sum and taken logit
                 sum = L.sum_in[r];
                 za = L.sum_in[L.Mpad + r];
             } else {
-                float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-                int t = 0;
-                for (; t + 4 <= L.stats_ld; t += 4) {
-                    s0 += __ldg(L.stats + static_cast<int64_t>(t) * L.Mpad + r);
-                    s1 += __ldg(L.stats + static_cast<int64_t>(t + 1) * L.Mpad + r);
-                    s2 += __ldg(L.stats + static_cast<int64_t>(t + 2) * L.Mpad + r);
-                    s3 += __ldg(L.stats + static_cast<int64_t>(t + 3) * L.Mpad + r);
-                }
-                for (; t < L.stats_ld; ++t) s0 += __ldg(L.stats + static_cast<int64_t>(t) * L.Mpad + r);
-                sum = (s0 + s1) + (s2 + s3);
+                sum = ((part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane])) +
+                      ((part[4][lane] + part[5][lane]) + (part[6][lane] + part[7][lane]));
                 za = L.zact[r];
-                if (L.partial_out) {  // this rank's columns only: to the all-reduce
-                    L.partial_out[r] = sum;
-                    L.partial_out[L.Mpad + r] = za;
-                    return;
+            }
+            if (L.partial_out) {  // this rank's columns only: to the all-reduce
+                L.partial_out[r] = sum;
+                L.partial_out[L.Mpad + r] = za;
+            } else {
+                const int a = rows.action[r];
+                const double adv = L.sd[rows.sample[r]].adv;
+                const float lse = rows.mrow[r] + __logf(sum);
+                const bool valid = a >= 0 && a < L.V;
+                const float lp = valid ? za - lse : 0.f;  // policy.hpp:72-75, fp32 logit
+                float ce = rows.coef[r];
+                if (L.old_logp && L.clip_eps > 0.f) {
+                    // PPO clipped-ratio surrogate min(rho*A, clip(rho,1-e,1+e)*A): the
+                    // gradient flows (scaled by rho) only through the unclipped branch.
+                    const float rho = __expf(lp - L.old_logp[L.row_lo + r]);
+                    const bool active = adv >= 0.0 ? rho <= 1.f + L.clip_eps : rho >= 1.f - L.clip_eps;
+                    ce = active ? ce * rho : 0.f;
                 }
+                rows.lse[r] = lse;
+                rows.logp[r] = lp;
+                rows.coef_eff[r] = ce;
+                loss = valid ? -(adv / static_cast<double>(L.G)) * static_cast<double>(lp) : 0.0;
+                // the bound keeps sum >= exp(max z - mrow); a vanishing sum would mean the bound
+                // overshot the logits by ~87: report NaN rather than a silently wrong gradient
+                if (!(sum >= 1e-30f) || !isfinite(sum)) loss = __longlong_as_double(0x7ff8000000000000ll);
             }
-            const int a = rows.action[r];
-            const double adv = L.sd[rows.sample[r]].adv;
-            const float lse = rows.mrow[r] + __logf(sum);
-            const bool valid = a >= 0 && a < L.V;
-            const float lp = valid ? za - lse : 0.f;  // policy.hpp:72-75, fp32 logit
-            float ce = rows.coef[r];
-            if (L.old_logp && L.clip_eps > 0.f) {
-                // PPO clipped-ratio surrogate min(rho*A, clip(rho,1-e,1+e)*A): the
-                // gradient flows (scaled by rho) only through the unclipped branch.
-                const float rho = __expf(lp - L.old_logp[L.row_lo + r]);
-                const bool active = adv >= 0.0 ? rho <= 1.f + L.clip_eps : rho >= 1.f - L.clip_eps;
-                ce = active ? ce * rho : 0.f;
-            }
-            rows.lse[r] = lse;
-            rows.logp[r] = lp;
-            rows.coef_eff[r] = ce;
-            loss = valid ? -(adv / static_cast<double>(L.G)) * static_cast<double>(lp) : 0.0;
-            // the bound keeps sum >= exp(max z - mrow); a vanishing sum would mean the bound
-            // overshot the logits by ~87: report NaN rather than a silently wrong gradient
-            if (!(sum >= 1e-30f) || !isfinite(sum)) loss = __longlong_as_double(0x7ff8000000000000ll);
         }
     }
     if (L.loss_acc) {
-        const double tot = block_sum(loss, red);
-        if (threadIdx.x == 0 && tot != 0.0) atomicAdd(L.loss_acc, tot);
+        for (int o = 16; o > 0; o >>= 1) loss += __shfl_xor_sync(0xffffffffu, loss, o);
+        if (lane == 0 && loss != 0.0) atomicAdd(L.loss_acc, loss);
     }
 }
 
@@ -227,7 +237,8 @@ __global__ void __launch_bounds__(256) lse_kernel(const LseArgs L) {
 // fp64 division + sqrt per parameter cost more issue slots than its 38 bytes.
 struct AdamF {
     float b1, ob1, b2, ob2, lr_bc1, inv_bc2, eps;
-    __device__ AdamF(double lr, double b1_, double b2_, double eps_, double bc1, double bc2)
+    AdamF() = default;
+    __host__ __device__ AdamF(double lr, double b1_, double b2_, double eps_, double bc1, double bc2)
         : b1(static_cast<float>(b1_)), ob1(static_cast<float>(1.0 - b1_)), b2(static_cast<float>(b2_)),
           ob2(static_cast<float>(1.0 - b2_)), lr_bc1(static_cast<float>(lr / bc1)),
           inv_bc2(static_cast<float>(1.0 / bc2)), eps(static_cast<float>(eps_)) {}
@@ -271,16 +282,27 @@ struct AdamTileArgs {
     __nv_bfloat16* w16t;
     uint64_t ldw;
     ShardPeers peers;
-    double* w_o;
-    float* m_o;
-    float* v_o;
     int zero_grad;
     double* gsq;
     double lr, b1, b2, eps, bc1, bc2;
+    AdamF cf;  // fp32 coefficients, computed on the host (kernel-parameter space, no registers)
 };
 
+template <bool kPeers>
+__device__ __noinline__ void store_w16t_tail(uint4 val, uint64_t off, int n, __nv_bfloat16* w16t,
+                                             const ShardPeers& peers) {
+    const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&val);
+    for (int k = 0; k < n; ++k) {
+        w16t[off + k] = e[k];
+        if constexpr (kPeers)
+            for (int p = 0; p < peers.n; ++p) peers.w16t[p][off + k] = e[k];
+    }
+}
+
 // Stores the tile's bf16 values (tsh[col][row]) as W16^T rows: thread -> one
-// column d, 8 consecutive rows (16 B).  Rows are 8-aligned (r0 % 8 == 0).
+// column d, 8 consecutive rows (16 B).  Rows are 8-aligned (vbase % 8 == 0).
+// kPeers: also into the DP gang peers' shadows (token-shard gang).
+template <bool kPeers>
 __device__ __forceinline__ void store_w16t_tile(const __nv_bfloat16 (*tsh)[kTPitch], uint64_t vbase, uint64_t dbase,
                                                 uint64_t r1, uint64_t D, __nv_bfloat16* w16t, uint64_t ldw,
                                                 const ShardPeers& peers) {
@@ -291,33 +313,25 @@ __device__ __forceinline__ void store_w16t_tile(const __nv_bfloat16 (*tsh)[kTPit
     const uint64_t off = d * ldw + vb;
     if (vb + 8 <= r1) {
         *reinterpret_cast<uint4*>(w16t + off) = val;
-        for (int p = 0; p < peers.n; ++p) *reinterpret_cast<uint4*>(peers.w16t[p] + off) = val;
+        if constexpr (kPeers)
+            for (int p = 0; p < peers.n; ++p) *reinterpret_cast<uint4*>(peers.w16t[p] + off) = val;
     } else {
-        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&val);
-        for (int k = 0; k < 8 && vb + k < r1; ++k) {
-            w16t[off + k] = e[k];
-            for (int p = 0; p < peers.n; ++p) peers.w16t[p][off + k] = e[k];
-        }
+        store_w16t_tail<kPeers>(val, off, static_cast<int>(r1 - vb), w16t, peers);
     }
 }
 
-template <typename G>
-__global__ void __launch_bounds__(256) adam_tile_kernel(const AdamTileArgs<G> A) {
+#ifndef FM_ADAM_MIN_BLOCKS
+#define FM_ADAM_MIN_BLOCKS 4
+#endif
+template <typename G, bool kVec, bool kPeers>
+__global__ void __launch_bounds__(256, FM_ADAM_MIN_BLOCKS) adam_tile_kernel(const AdamTileArgs<G> A) {
     __shared__ __align__(16) __nv_bfloat16 tsh[kTileD][kTPitch];
     __shared__ double red[8];
-    double* w_o = A.w_o ? A.w_o : A.w;
-    float* m_o = A.w_o ? A.m_o : A.m;
-    float* v_o = A.w_o ? A.v_o : A.v;
-    const AdamF cf(A.lr, A.b1, A.b2, A.eps, A.bc1, A.bc2);
-    auto adam_one = [&](double& w_, float& m_, float& v_, G g_) -> double {
-        if constexpr (sizeof(G) == 4) return adam_f32(w_, m_, v_, g_, cf);
-        else return adam_f64(w_, m_, v_, g_, A.lr, A.b1, A.b2, A.eps, A.bc1, A.bc2);
-    };
+    const AdamF& cf = A.cf;
     const uint64_t rows = A.r1 - A.r0;
     const uint64_t tv_n = (rows + kTileV - 1) / kTileV, td_n = (A.D + kTileD - 1) / kTileD;
     const uint64_t ntiles = tv_n * td_n;
     const int tr = static_cast<int>(threadIdx.x >> 3), tc = static_cast<int>(threadIdx.x & 7) * 8;
-    const bool vec = (A.D & 7) == 0;
     const uint64_t sstride = rows * A.D;
     double acc = 0.0;
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -327,34 +341,38 @@ __global__ void __launch_bounds__(256) adam_tile_kernel(const AdamTileArgs<G> A)
         float wf[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         if (vr < A.r1 && d0 < A.D) {
             const uint64_t i0 = vr * A.D + d0;
-            const int nv = A.D - d0 >= 8 ? 8 : static_cast<int>(A.D - d0);
+            const int nv = kVec ? 8 : (A.D - d0 >= 8 ? 8 : static_cast<int>(A.D - d0));
             double wv[8];
             float mv[8], vv[8];
             G gv[8];
-            if (vec) {
+            if constexpr (kVec) {
+                const double2* __restrict__ wp = reinterpret_cast<const double2*>(A.w + i0);
+                const float4* __restrict__ mp = reinterpret_cast<const float4*>(A.m + i0);
+                const float4* __restrict__ vp = reinterpret_cast<const float4*>(A.v + i0);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    const double2 x = reinterpret_cast<const double2*>(A.w + i0)[q];
+                    const double2 x = wp[q];
                     wv[2 * q] = x.x;
                     wv[2 * q + 1] = x.y;
                 }
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {
-                    const float4 a = reinterpret_cast<const float4*>(A.m + i0)[q];
-                    const float4 b = reinterpret_cast<const float4*>(A.v + i0)[q];
+                    const float4 a = mp[q], b = vp[q];
                     mv[4 * q] = a.x; mv[4 * q + 1] = a.y; mv[4 * q + 2] = a.z; mv[4 * q + 3] = a.w;
                     vv[4 * q] = b.x; vv[4 * q + 1] = b.y; vv[4 * q + 2] = b.z; vv[4 * q + 3] = b.w;
                 }
                 if constexpr (sizeof(G) == 4) {
+                    const float4* __restrict__ gp = reinterpret_cast<const float4*>(A.g + i0);
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
-                        const float4 c = reinterpret_cast<const float4*>(A.g + i0)[q];
+                        const float4 c = gp[q];
                         gv[4 * q] = c.x; gv[4 * q + 1] = c.y; gv[4 * q + 2] = c.z; gv[4 * q + 3] = c.w;
                     }
                 } else {
+                    const double2* __restrict__ gp = reinterpret_cast<const double2*>(A.g + i0);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const double2 c = reinterpret_cast<const double2*>(A.g + i0)[q];
+                        const double2 c = gp[q];
                         gv[2 * q] = c.x;
                         gv[2 * q + 1] = c.y;
                     }
@@ -377,12 +395,29 @@ __global__ void __launch_bounds__(256) adam_tile_kernel(const AdamTileArgs<G> A)
                         if (j < nv) gv[j] += static_cast<G>(rp[j]);
                 }
             }
+            if constexpr (sizeof(G) == 4) {
+                // fp32 g^2 within the thread's 8 elements, fp64 across them
+                float sq = 0.f;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (j < nv) acc += adam_one(wv[j], mv[j], vv[j], gv[j]);
-                wf[j] = static_cast<float>(wv[j]);
+                for (int j = 0; j < 8; ++j) {
+                    if (j < nv) {
+                        adam_f32(wv[j], mv[j], vv[j], gv[j], cf);
+                        sq = fmaf(gv[j], gv[j], sq);
+                    }
+                    wf[j] = static_cast<float>(wv[j]);
+                }
+                acc += static_cast<double>(sq);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (j < nv) acc += adam_f64(wv[j], mv[j], vv[j], gv[j], A.lr, A.b1, A.b2, A.eps, A.bc1, A.bc2);
+                    wf[j] = static_cast<float>(wv[j]);
+                }
             }
-            if (vec) {
+            double* const w_o = A.w;
+            float* const m_o = A.m;
+            float* const v_o = A.v;
+            if constexpr (kVec) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) reinterpret_cast<double2*>(w_o + i0)[q] = make_double2(wv[2 * q], wv[2 * q + 1]);
 #pragma unroll
@@ -409,7 +444,7 @@ __global__ void __launch_bounds__(256) adam_tile_kernel(const AdamTileArgs<G> A)
 #pragma unroll
             for (int j = 0; j < 8; ++j) tsh[tc + j][tr] = __float2bfloat16_rn(wf[j]);
             __syncthreads();
-            store_w16t_tile(tsh, A.r0 + tv * kTileV, td * kTileD, A.r1, A.D, A.w16t, A.ldw, A.peers);
+            store_w16t_tile<kPeers>(tsh, A.r0 + tv * kTileV, td * kTileD, A.r1, A.D, A.w16t, A.ldw, A.peers);
             __syncthreads();
         }
     }
@@ -433,7 +468,7 @@ __global__ void __launch_bounds__(256) w16t_kernel(const double* __restrict__ w,
         for (int j = 0; j < 8; ++j)
             tsh[tc + j][tr] = __float2bfloat16_rn(vr < V && d0 + j < D ? static_cast<float>(w[vr * D + d0 + j]) : 0.f);
         __syncthreads();
-        store_w16t_tile(tsh, tv * kTileV, td * kTileD, V, D, w16t, ldw, none);
+        store_w16t_tile<false>(tsh, tv * kTileV, td * kTileD, V, D, w16t, ldw, none);
         __syncthreads();
     }
 }
@@ -630,7 +665,7 @@ cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D,
 
 cudaError_t launch_lse(const LseArgs& L, cudaStream_t s) {
     if (L.Mpad == 0) return cudaSuccess;
-    lse_kernel<<<static_cast<unsigned>((L.Mpad + 255) / 256), 256, 0, s>>>(L);
+    lse_kernel<<<static_cast<unsigned>((L.Mpad + 31) / 32), 256, 0, s>>>(L);
     return cudaGetLastError();
 }
 
@@ -638,27 +673,30 @@ template <typename G>
 cudaError_t launch_adam(double* w, float* m, float* v, G* g, uint64_t V, uint64_t D, uint64_t r0, uint64_t r1,
                         const float* recv, int nslots, __nv_bfloat16* w16t, uint64_t ldw, ShardPeers peers, double lr,
                         double b1, double b2, double eps, double bc1, double bc2, int zero_grad, double* gsq,
-                        int num_sms, cudaStream_t s, const AdamDst* dst) {
+                        int num_sms, cudaStream_t s) {
     if (r1 <= r0 || D == 0) return cudaSuccess;
     if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g)) & 15) return cudaErrorMisalignedAddress;
-    if (dst && (reinterpret_cast<uintptr_t>(dst->w) & 15)) return cudaErrorMisalignedAddress;
     if (w16t && ((r0 & 7) || (ldw & 7))) return cudaErrorInvalidValue;
-    AdamTileArgs<G> A{w, m, v, g, V, D, r0, r1, recv, nslots, w16t, ldw, peers,
-                      dst ? dst->w : nullptr, dst ? dst->m : nullptr, dst ? dst->v : nullptr,
-                      zero_grad, gsq, lr, b1, b2, eps, bc1, bc2};
+    AdamTileArgs<G> A{w, m, v, g, V, D, r0, r1, recv, nslots, w16t, ldw, peers, zero_grad, gsq, lr, b1, b2, eps, bc1, bc2, AdamF(lr, b1, b2, eps, bc1, bc2)};
     const uint64_t tiles = ((r1 - r0 + kTileV - 1) / kTileV) * ((D + kTileD - 1) / kTileD);
-    const uint64_t cap = static_cast<uint64_t>(num_sms) * 8;
-    adam_tile_kernel<G><<<static_cast<int>(tiles < cap ? tiles : cap), 256, 0, s>>>(A);
+    const uint64_t cap = static_cast<uint64_t>(num_sms) * 64;
+    const int grid = static_cast<int>(tiles < cap ? tiles : cap);
+    const bool vec = D % 8 == 0;
+    if (peers.n > 0) {
+        if (vec) adam_tile_kernel<G, true, true><<<grid, 256, 0, s>>>(A);
+        else adam_tile_kernel<G, false, true><<<grid, 256, 0, s>>>(A);
+    } else {
+        if (vec) adam_tile_kernel<G, true, false><<<grid, 256, 0, s>>>(A);
+        else adam_tile_kernel<G, false, false><<<grid, 256, 0, s>>>(A);
+    }
     return cudaGetLastError();
 }
 template cudaError_t launch_adam<float>(double*, float*, float*, float*, uint64_t, uint64_t, uint64_t, uint64_t,
                                         const float*, int, __nv_bfloat16*, uint64_t, ShardPeers, double, double,
-                                        double, double, double, double, int, double*, int, cudaStream_t,
-                                        const AdamDst*);
+                                        double, double, double, double, int, double*, int, cudaStream_t);
 template cudaError_t launch_adam<double>(double*, float*, float*, double*, uint64_t, uint64_t, uint64_t, uint64_t,
                                          const float*, int, __nv_bfloat16*, uint64_t, ShardPeers, double, double,
-                                         double, double, double, double, int, double*, int, cudaStream_t,
-                                         const AdamDst*);
+                                         double, double, double, double, int, double*, int, cudaStream_t);
 
 cudaError_t launch_w16t(const double* w, uint64_t V, uint64_t D, __nv_bfloat16* w16t, uint64_t ldw, int num_sms,
                         cudaStream_t s) {

@@ -50,8 +50,9 @@ def test_cross_process_migration():
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("tier", ["peer", "device"])
 @pytest.mark.parametrize("back_on", [0, 1])
-def test_peer_tier_swap_identity(back_on):
+def test_peer_tier_swap_identity(back_on, tier):
     """FM_TIER_PEER (training.hpp:321-350 / 259-317 with the state parked in a
     peer GPU's HBM over NVLink, cudaMemcpyPeerAsync on the copy streams): an
     agent with a mid-step gradient suspended from GPU 0 into GPU 1's HBM and
@@ -95,7 +96,11 @@ def test_peer_tier_swap_identity(back_on):
         moved, stayed = hs
         before = checksum(moved)
         assert before == checksum(stayed)
-        _lib.check(L.fm_agent_suspend(moved, _lib.TIER_PEER, 1))
+        if tier == "peer":
+            _lib.check(L.fm_agent_suspend(moved, _lib.TIER_PEER, 1))
+        else:  # kept in its GPU-0 slot; activation on GPU 1 parks it on GPU 0, then pulls it over NVLink
+            _lib.check(L.fm_agent_suspend(moved, _lib.TIER_DEVICE, -1))
+            assert L.fm_agent_is_active(moved) == 0
         _lib.check(L.fm_agent_activate(moved, ctxs[back_on].handle))
         assert checksum(moved) == before
         train(moved, ctxs[back_on], 1)
