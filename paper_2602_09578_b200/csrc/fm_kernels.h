@@ -39,7 +39,11 @@ struct RowBuffers {
 
 // K-lse arguments.
 struct LseArgs {
-    const float* zact;    // [Mpad] fp32 logit of the taken token
+    // the taken token's fp32 logit, rs * ((X[q0] + X[q0+1]) + (X[q0+2] + X[q0+3])) at its
+    // W16^T column — K-stats' own summation order, so bit-identical to its z
+    const __nv_bfloat16* w16t;  // W16^T at column col_base
+    int64_t ldw, ncols, col_base;
+    const int32_t* pos_feat;    // [Q] position features (-1: before the sequence start)
     const float* stats;   // [stats_ld][Mpad] partial sums of exp(z - mrow) (K-stats)
     int stats_ld;
     int64_t M, Mpad, V;
@@ -100,7 +104,6 @@ struct BandArgs {
     // pass A (K-stats)
     float* stats;   // [stats_ld][ld_stats] partial sums of exp(z - mrow)
     int stats_ld;
-    float* zact;    // [M]
     // pass B (K-band)
     const float* lse;       // [M]
     const float* coef_eff;  // [M]
@@ -117,8 +120,8 @@ cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s);
 int band_stats_ld(int64_t V);
 
 // K-lse: lse = mrow + log(sum of K-stats' partial sums), the taken-token
-// log-prob (from the fp32 logit K-stats captured) and the effective row
-// coefficient (PPO-clip surrogate optional).  One lane per row.
+// log-prob (its fp32 logit from four W16^T elements) and the effective row
+// coefficient (PPO-clip surrogate optional).
 cudaError_t launch_lse(const LseArgs& L, cudaStream_t s);
 
 // Parity tooling: out[v][j] = dW[v][cols[j]] (f32 or f64 accumulator).

@@ -167,7 +167,6 @@ void ws_free(Workspace& w) {
     cudaFree(w.mrow);
     cudaFree(w.pos_feat);
     cudaFree(w.pos_slot);
-    cudaFree(w.zact);
     cudaFree(w.stats);
     cudaFree(w.aseg);
     cudaFree(w.bseg);
@@ -231,7 +230,6 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D, int n_samples
     e = e ? e : dalloc(&w.coef_eff, R);
     e = e ? e : dalloc(&w.q0, R);
     e = e ? e : dalloc(&w.mrow, R);
-    e = e ? e : dalloc(&w.zact, R);
     e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n);  // [tiles][R] partial sums
     e = e ? e : dalloc(&w.pos_feat, static_cast<size_t>(Q));
     e = e ? e : dalloc(&w.pos_slot, static_cast<size_t>(Q));
@@ -1097,7 +1095,6 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             ba.ld_stats = Mpad;
             ba.stats = w.stats;
             ba.stats_ld = band_stats_ld(c1 - c0);
-            ba.zact = w.zact;
             ba.lse = w.lse;
             ba.coef_eff = w.coef_eff;
             ba.pos_slot = w.pos_slot;
@@ -1111,12 +1108,11 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             {
                 // K-stats: per-(row, 256-column tile) softmax partials + the taken token's logit
                 KScope k(c, K_STATS, s);
-                if (vg) FM_CUDA(cudaMemsetAsync(w.zact, 0, Mpad * 4, s));  // the action's owner writes it
                 if (cols) FM_CUDA(launch_band(ba, false, s));
             }
             {
                 KScope k(c, K_LSE, s);
-                LseArgs L{w.zact, w.stats, ba.stats_ld, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
+                LseArgs L{ba.w16t, ba.ldw, c1 - c0, c0, w.pos_feat, w.stats, ba.stats_ld, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
                           clip ? w.old_logp : nullptr, row_lo, a->clip_eps, scal + 1};
                 if (vg) {
                     // vocabulary gang: per row (sum over my columns, taken logit or 0), summed

@@ -78,7 +78,6 @@ struct Workspace {
     int32_t* q0 = nullptr;
     int32_t *pos_feat = nullptr, *pos_slot = nullptr;
     int64_t pos_cap = 0;
-    float* zact = nullptr;   // logit of the taken token [Mpad]
     float* mrow = nullptr;   // per-row softmax bound (1/n) sum_k fmax[f_k] [Mpad]
     float* stats = nullptr;  // K-stats partial sums exp(z - mrow), [stats_ld][Mpad]
     // segments of K-GEMM2: A' = per-position gradient rows H [kp_cap][ldz] bf16,

@@ -57,10 +57,9 @@ constexpr int kBandConsumers = 256;                  // 8 consumer warps
 constexpr int kBandThreads = kBandConsumers + 32;    // + the producer warp
 constexpr int kBandStages = 12;
 constexpr int kBandRows = 128;                       // trained rows per CTA
-// columns per lane: 8 * kV.  Both passes run 8 with two CTAs (18 warps) per SM:
-// 16 columns per lane (measured: K-stats 0.43-0.53 ms vs 0.33 ms at C2) needs
-// more registers than two CTAs leave and drops to one CTA per SM.
-constexpr int kStatsV = 1, kGradV = 1;
+// 8 columns per lane, two CTAs (18 warps) per SM: 16 columns per lane (measured:
+// K-stats 0.43-0.53 ms vs 0.33 ms at C2) needs more registers than two CTAs leave
+// and drops to one CTA per SM.
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ int token_of(uint64_t x) {  // static_cast<Token>(u64), codec.hpp:28
@@ -265,40 +264,43 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
-// Grid (vocabulary slices of 2,048 * kV columns, chunks of kBandRows rows).
+// Grid (vocabulary slices of 2,048 columns, chunks of kBandRows rows).
 // kGrad = false: pass A (K-stats) over rows [ra, rb).
 // kGrad = true:  pass B (K-band): rows [ra - 3, rb) so that every position in
 // [q0[ra], q0[rb]) (the chunk's emission range) has all of its rows.
 // Shared memory: the W16^T row ring, its full / empty barriers, and the
-// chunk's per-row metadata (q0, action, 1/n; pass B: lse, coefficient).
-constexpr int kMetaRows = kBandRows + 4;
+// chunk's per-row metadata (q0, action, rs * log2e, -bound * log2e with the
+// bound = mrow (pass A) or lse (pass B), coefficient) plus a sentinel row
+// kNoRow whose terms vanish (exp2(-1e30) = 0, coefficient 0).
+constexpr int kMetaRows = kBandRows + 5;
+constexpr int kNoRow = kMetaRows - 1;
 constexpr int kRedPitch = 33;  // per-warp [32 rows][32 lanes] partial sums, padded (conflict-free transpose)
 // Positions of a chunk the branch-free loop indexes directly (4 per row covers
 // samples of >= 1 row; longer spans — many empty samples — take the general loop).
-constexpr int kMaxQ = 4 * (kBandRows + 4) + 8;
-template <bool kGrad, int kV>
+constexpr int kMaxQ = 4 * (kBandRows + 4) + 16;
+static_assert(kBandStages % 4 == 0, "the 4-position body consumes whole groups of 4 stages");
+template <bool kGrad>
 constexpr size_t band_smem_bytes() {
-    return kBandStages * kBandConsumers * 16 * kV + 2 * kBandStages * sizeof(uint64_t) +
+    return kBandStages * kBandConsumers * 16 + 2 * kBandStages * sizeof(uint64_t) +
            5 * kMetaRows * sizeof(int32_t) + (kGrad ? 0 : (kBandConsumers / 32) * 32 * kRedPitch * sizeof(float)) +
            kMaxQ * sizeof(int32_t);
 }
 
-template <bool kGrad, int kV, int kMinBlocks>
+template <bool kGrad, int kMinBlocks>
 __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const BandArgs A) {
-    constexpr int kCols = kBandConsumers * 8 * kV;   // vocabulary columns per CTA
-    constexpr int kStage = kCols * 2;                // bytes of one position's W16^T slice
-    constexpr int kP = 4 * kV;                       // fp32 pairs per lane
+    constexpr int kCols = kBandConsumers * 8;  // vocabulary columns per CTA
+    constexpr int kStage = kCols * 2;          // bytes of one position's W16^T slice
     extern __shared__ __align__(128) uint8_t band_smem[];
     uint8_t* ring = band_smem;
     uint64_t* full = reinterpret_cast<uint64_t*>(band_smem + kBandStages * kStage);
     uint64_t* empty = full + kBandStages;
     int32_t* m_q0 = reinterpret_cast<int32_t*>(empty + kBandStages);
     int32_t* m_act = m_q0 + kMetaRows;
-    float* m_rs = reinterpret_cast<float*>(m_act + kMetaRows);
-    float* m_lse = m_rs + kMetaRows;  // pass A: the rows' softmax bounds
-    float* m_ce = m_lse + kMetaRows;
-    float* redbuf = m_ce + kMetaRows;  // pass A: per-warp [32][kRedPitch]
-    // position k of the chunk -> the row whose four positions end there, or -1
+    float* m_c = reinterpret_cast<float*>(m_act + kMetaRows);  // rs * log2e
+    float* m_off = m_c + kMetaRows;                             // -bound * log2e
+    float* m_ce = m_off + kMetaRows;                            // pass B: the row coefficient
+    float* redbuf = m_ce + kMetaRows;                           // pass A: per-warp [32][kRedPitch]
+    // position q - qlo of the chunk -> the row whose four positions end there, or kNoRow
     int32_t* m_end = reinterpret_cast<int32_t*>(redbuf + (kGrad ? 0 : (kBandConsumers / 32) * 32 * kRedPitch));
     const int tid = static_cast<int>(threadIdx.x);
     const int lane = tid & 31;
@@ -314,6 +316,10 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
             mbar_init(&empty[s], kBandConsumers / 32);
         }
         fence_barrier_init();
+        m_act[kNoRow] = INT_MIN / 4;
+        m_c[kNoRow] = 0.f;
+        m_off[kNoRow] = -1e30f;
+        m_ce[kNoRow] = 0.f;
     }
     // the rows' metadata, once per CTA (off the per-row critical path)
     for (int i = tid; i <= nrows; i += kBandThreads) {
@@ -321,26 +327,25 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
         m_q0[i] = r < A.M ? __ldg(A.q0 + r) : INT32_MAX - 8;
         if (i < nrows) {
             m_act[i] = __ldg(A.action + r) - static_cast<int32_t>(A.col_base);  // this range's column
-            m_rs[i] = __ldg(A.rscale + r);
-            if constexpr (kGrad) {
-                m_lse[i] = __ldg(A.lse + r);
-                m_ce[i] = __ldg(A.coef_eff + r);
-            } else {
-                m_lse[i] = __ldg(A.mrow + r);
-            }
+            m_c[i] = __ldg(A.rscale + r) * kLog2e;
+            m_off[i] = -__ldg(kGrad ? A.lse + r : A.mrow + r) * kLog2e;
+            if constexpr (kGrad) m_ce[i] = __ldg(A.coef_eff + r);
         }
     }
     __syncthreads();
     const int qa = m_q0[0];
     const int qb = m_q0[nrows - 1] + 4;
-    const int nq = qb - qa;
-    const bool fast = kV == 1 && nq + 8 <= kMaxQ;  // uniform
+    const int qend = kGrad ? qb + 3 : qb;  // pass B runs 3 positions on to flush the last H rows
+    // the branch-free loop runs whole 4-position bodies over [qlo, qhi); its padding
+    // positions stream the zero row, so every body takes exactly 4 ring stages
+    const int qlo = qa & ~3, qhi = (qend + 3) & ~3;
+    const bool fast = qhi - qlo <= kMaxQ;  // uniform
     if (fast) {
-        for (int k = tid; k < kMaxQ; k += kBandThreads) m_end[k] = -1;
+        for (int k = tid; k < kMaxQ; k += kBandThreads) m_end[k] = kNoRow;
         __syncthreads();
         for (int i = tid; i < nrows; i += kBandThreads) {
-            FM_DCHECK(m_q0[i] + 3 - qa >= 0 && m_q0[i] + 3 - qa < nq);
-            m_end[m_q0[i] + 3 - qa] = i;
+            FM_DCHECK(m_q0[i] + 3 - qlo >= 0 && m_q0[i] + 3 - qlo < qhi - qlo);
+            m_end[m_q0[i] + 3 - qlo] = i;
         }
         __syncthreads();
     }
@@ -354,18 +359,23 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
         const int64_t cols = A.ldw - v0 < kCols ? A.ldw - v0 : kCols;
         const uint32_t bytes = static_cast<uint32_t>(cols) * 2u;
         const __nv_bfloat16* base = A.w16t + v0;
-        int32_t f_next = lane < nq ? __ldg(A.pos_feat + qa + lane) : -1;
+        const int p0 = fast ? qlo : qa, np = (fast ? qhi : qb) - p0;
+        auto feat_at = [&](int k) -> int32_t {
+            const int q = p0 + k;
+            return k < np && q >= qa && q < qb ? __ldg(A.pos_feat + q) : -1;
+        };
+        int32_t f_next = feat_at(lane);
         int st = 0;
         uint32_t ph = 0;
-        for (int k0 = 0; k0 < nq; k0 += 32) {
+        for (int k0 = 0; k0 < np; k0 += 32) {
             const int32_t f_cur = f_next;
-            f_next = k0 + 32 + lane < nq ? __ldg(A.pos_feat + qa + k0 + 32 + lane) : -1;
-            const int kn = nq - k0 < 32 ? nq - k0 : 32;
+            f_next = feat_at(k0 + 32 + lane);
+            const int kn = np - k0 < 32 ? np - k0 : 32;
             for (int j = 0; j < kn; ++j) {
                 if (k0 + j >= kBandStages) mbar_wait(&empty[st], ph ^ 1u);
                 const int32_t f = __shfl_sync(0xffffffffu, f_cur, j);
                 if (lane == 0) {
-                    // a position before the sequence start reads the zero row
+                    // a position before the sequence start (or a padding position) reads the zero row
                     const __nv_bfloat16* src = f >= 0 ? base + static_cast<int64_t>(f) * A.ldw : A.zero_row;
                     mbar_arrive_expect_tx(&full[st], bytes);
                     FM_DCHECK(f < A.dbg_D);
@@ -381,26 +391,18 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
         return;
     }
 
-    // ===== consumers: lane = kV runs of 8 consecutive columns, as fp32 pairs =====
-    // run i of lane l covers columns v0 + (i * kBandConsumers + tid) * 8 .. + 8, so every
-    // shared-memory read of the warp is 512 contiguous bytes
-    int nv[kV];   // valid columns of each run (8, or fewer at the vocabulary's end)
-    int64_t cb[kV];
-#pragma unroll
-    for (int i = 0; i < kV; ++i) {
-        cb[i] = v0 + (static_cast<int64_t>(i) * kBandConsumers + tid) * 8;
-        nv[i] = A.V - cb[i] >= 8 ? 8 : (A.V - cb[i] > 0 ? static_cast<int>(A.V - cb[i]) : 0);
-    }
-    bool full_lane = true;
-#pragma unroll
-    for (int i = 0; i < kV; ++i) full_lane = full_lane && nv[i] == 8;
-    const bool warp_full = __all_sync(0xffffffffu, full_lane);
+    // ===== consumers: lane = 8 consecutive columns, as 4 fp32 pairs =====
+    // lane l of warp w covers columns v0 + (w * 32 + l) * 8 .. + 8, so every shared-memory
+    // read of the warp is 512 contiguous bytes
+    const int64_t cb = v0 + static_cast<int64_t>(tid) * 8;
+    const int nv = A.V - cb >= 8 ? 8 : (A.V - cb > 0 ? static_cast<int>(A.V - cb) : 0);
+    const bool warp_full = __all_sync(0xffffffffu, nv == 8);
     const int tile = static_cast<int>(blockIdx.x) * (kBandConsumers / 32) + warp;  // the warp's stats column
     // per position q: xp = X[q-1] (previous position's row), pr[q & 3] = X[q-1] + X[q];
     // the row ending at q sums pr[(q-2) & 3] + pr[q & 3] = X[q-3] + X[q-2] + X[q-1] + X[q]
-    float2 xp[kP], pr[4][kP], gr[4][kP];
+    float2 xp[4], pr[4][4], gr[4][4];
 #pragma unroll
-    for (int j = 0; j < kP; ++j) {
+    for (int j = 0; j < 4; ++j) {
         xp[j] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -408,8 +410,6 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
             if constexpr (kGrad) gr[i][j] = make_float2(0.f, 0.f);
         }
     }
-    int ri = 0;            // next row (index into the metadata)
-    int next_end = qa + 3; // its last position
     int st = 0;
     uint32_t ph = 0;
     int elo = 0, ehi = 0;
@@ -423,203 +423,166 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
         s_cur = sg + lane < qb ? __ldg(A.pos_slot + sg + lane) : -1;
         s_next = sg + 32 + lane < qb ? __ldg(A.pos_slot + sg + 32 + lane) : -1;
     }
-    auto valid = [&](int j, int h) {  // element 2j + h of the lane's pairs
-        return warp_full || 2 * (j & 3) + h < nv[j >> 2];
-    };
+    auto valid = [&](int j, int h) { return warp_full || 2 * j + h < nv; };  // element 2j + h of the lane
 
-    // one position step; S = q & 3 is static so the rings stay in registers
-    auto step = [&](int q, auto Sc) {
-        constexpr int S = decltype(Sc)::value;
-        if (q >= qa && q < qb) {
-            mbar_wait(&full[st], ph);
-            uint4 u[kV];
+    // pass A: the row's partial sum of exp2(z * log2e - bound * log2e) over the lane's columns
+    // (the bound mrow >= every z of the row: no max reduction)
+    auto row_sum = [&](const float2 (&z4)[4], float c, float off, auto FullTag) -> float {
+        constexpr bool kFull = decltype(FullTag)::value;
+        const float2 cc = make_float2(c, c), oo = make_float2(off, off);
+        float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int i = 0; i < kV; ++i)
-                u[i] = *reinterpret_cast<const uint4*>(ring + st * kStage + (i * kBandConsumers + tid) * 16);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
-            if (++st == kBandStages) {
-                st = 0;
-                ph ^= 1u;
+        for (int j = 0; j < 4; ++j) {
+            const float2 y = __ffma2_rn(z4[j], cc, oo);
+            float2 e = make_float2(ex2(y.x), ex2(y.y));
+            if constexpr (!kFull) {
+                if (!valid(j, 0)) e.x = 0.f;
+                if (!valid(j, 1)) e.y = 0.f;
             }
+            s2 = __fadd2_rn(s2, e);
+        }
+        return s2.x + s2.y;
+    };
+    // pass B: g = ce (delta(v, a) - exp(z - lse)) over the lane's columns (zero-advantage rows
+    // and the sentinel give 0, training.hpp:394); dact = action column - the lane's first
+    auto row_grad = [&](const float2 (&z4)[4], float c, float off, float ce, int dact, float2 (&g)[4]) {
+        const float2 cc = make_float2(c, c), oo = make_float2(off, off), nce = make_float2(-ce, -ce);
 #pragma unroll
-            for (int i = 0; i < kV; ++i) {
+        for (int j = 0; j < 4; ++j) {
+            const float2 y = __ffma2_rn(z4[j], cc, oo);
+            g[j] = __fmul2_rn(make_float2(ex2(y.x), ex2(y.y)), nce);
+        }
+        if (static_cast<unsigned>(dact) < 8u) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (dact == 2 * j) g[j].x += ce;
+                if (dact == 2 * j + 1) g[j].y += ce;
+            }
+        }
+    };
+    // pass B: position p's H row = the four g-ring slots (the rows ending at p .. p + 3)
+    auto flush_h = [&](int p) {
+        if (p >= elo && p < ehi) {
+            if (p >= sg + 32) {  // next group of slots (warp-uniform)
+                sg += 32;
+                s_cur = s_next;
+                s_next = sg + 32 + lane < qb ? __ldg(A.pos_slot + sg + 32 + lane) : -1;
+            }
+            const int32_t sl = __shfl_sync(0xffffffffu, s_cur, p - sg);
+            if (sl >= 0 && nv > 0) {
+                float2 h[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    h[j] = __fadd2_rn(__fadd2_rn(gr[0][j], gr[1][j]), __fadd2_rn(gr[2][j], gr[3][j]));
+                FM_DCHECK(sl < A.dbg_kp && cb + 8 <= A.ld_a);
+                *reinterpret_cast<uint4*>(A.aseg + static_cast<int64_t>(sl) * A.ld_a + cb) = pack8(h);
+            }
+        }
+    };
+    const int d_lane = static_cast<int>(cb - v0);  // the lane's first column within the slice
+
+    if (!fast) {
+        // general loop (chunks whose samples are mostly empty): one position at a time over
+        // [qa, qb), stages consumed only for real positions
+        int ri = 0;             // next row
+        int next_end = qa + 3;  // its last position
+        int rows_done = 0;
+        auto step = [&](int q, auto Sc) {
+            constexpr int S = decltype(Sc)::value;
+            if (q >= qa && q < qb) {
+                mbar_wait(&full[st], ph);
+                const uint4 u = *reinterpret_cast<const uint4*>(ring + st * kStage + tid * 16);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
+                if (++st == kBandStages) {
+                    st = 0;
+                    ph ^= 1u;
+                }
                 float2 x[4];
-                unpack8(u[i], x);
+                unpack8(u, x);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
-                    pr[S][4 * i + j] = __fadd2_rn(xp[4 * i + j], x[j]);
-                    xp[4 * i + j] = x[j];
+                    pr[S][j] = __fadd2_rn(xp[j], x[j]);
+                    xp[j] = x[j];
                 }
-            }
-            if (q == next_end) {  // the row whose four positions end here
-                const int i = ri;
-                const float rs = m_rs[i];
-                const int act = m_act[i];
-                float2 z4[kP];  // sum of the row's four position rows
+                if (q == next_end) {  // the row whose four positions end here
+                    const int i = ri;
+                    float2 z4[4];
 #pragma unroll
-                for (int j = 0; j < kP; ++j) z4[j] = __fadd2_rn(pr[(S + 2) & 3][j], pr[S][j]);
-                const float c = rs * kLog2e;  // z = rs * z4 (rs >= 0), exponents in base 2
-                if constexpr (!kGrad) {
-                    // partial sum of exp(z - mrow) over the lane's columns (mrow >= every z of
-                    // the row: no max reduction), parked in shared memory; every 32 rows the
-                    // warp transposes them and lane l adds up row l's 32 lane partials
-                    const float2 cc = make_float2(c, c);
-                    const float lo = -m_lse[i] * kLog2e;
-                    const float2 off = make_float2(lo, lo);
-                    float2 s2 = make_float2(0.f, 0.f);
+                    for (int j = 0; j < 4; ++j) z4[j] = __fadd2_rn(pr[(S + 2) & 3][j], pr[S][j]);
+                    if constexpr (!kGrad) {
+                        const float s = warp_full ? row_sum(z4, m_c[i], m_off[i], std::true_type{})
+                                                  : row_sum(z4, m_c[i], m_off[i], std::false_type{});
+                        redbuf[warp * 32 * kRedPitch + (i & 31) * kRedPitch + lane] = s;
+                        rows_done = i + 1;
+                        if ((i & 31) == 31 || i == nrows - 1) {
+                            __syncwarp();
+                            const int i0 = i & ~31;
+                            if (i0 + lane <= i) {
+                                const float* src = redbuf + warp * 32 * kRedPitch + lane * kRedPitch;
+                                float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
 #pragma unroll
-                    for (int j = 0; j < kP; ++j) {
-                        const float2 y = __ffma2_rn(z4[j], cc, off);
-                        float2 e = make_float2(ex2(y.x), ex2(y.y));
-                        if (!warp_full) {
-                            if (!valid(j, 0)) e.x = 0.f;
-                            if (!valid(j, 1)) e.y = 0.f;
-                        }
-                        s2 = __fadd2_rn(s2, e);
-                    }
-                    float* rb_w = redbuf + warp * 32 * kRedPitch;
-                    rb_w[(i & 31) * kRedPitch + lane] = s2.x + s2.y;
-                    const int rr = rstart + i;
-#pragma unroll
-                    for (int r2 = 0; r2 < kV; ++r2) {
-                        const int64_t d = act - cb[r2];
-                        if (d >= 0 && d < nv[r2]) {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                if (d == 2 * j) A.zact[rr] = rs * z4[4 * r2 + j].x;
-                                if (d == 2 * j + 1) A.zact[rr] = rs * z4[4 * r2 + j].y;
+                                for (int k = 0; k < 32; k += 4) {
+                                    t0 += src[k];
+                                    t1 += src[k + 1];
+                                    t2 += src[k + 2];
+                                    t3 += src[k + 3];
+                                }
+                                A.stats[static_cast<int64_t>(tile) * A.ld_stats + rstart + i0 + lane] =
+                                    (t0 + t1) + (t2 + t3);
                             }
+                            __syncwarp();
                         }
+                    } else {
+                        row_grad(z4, m_c[i], m_off[i], m_ce[i], m_act[i] - static_cast<int>(v0) - d_lane, gr[S]);
                     }
-                    if ((i & 31) == 31 || i == nrows - 1) {
-                        __syncwarp();
-                        const int i0 = i & ~31;
-                        if (i0 + lane <= i) {
-                            const float* src = rb_w + lane * kRedPitch;
-                            float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+                    ++ri;
+                    next_end = m_q0[ri] + 3;
+                } else if constexpr (kGrad) {
 #pragma unroll
-                            for (int k = 0; k < 32; k += 4) {
-                                t0 += src[k];
-                                t1 += src[k + 1];
-                                t2 += src[k + 2];
-                                t3 += src[k + 3];
-                            }
-                            A.stats[static_cast<int64_t>(tile) * A.ld_stats + rstart + i0 + lane] = (t0 + t1) + (t2 + t3);
-                        }
-                        __syncwarp();
-                    }
-                } else {
-                    const float ce = m_ce[i];
-                    // g = ce (delta(v, a) - exp(z - lse)); zero-advantage rows give 0 (training.hpp:394)
-                    const float2 cc = make_float2(c, c);
-                    const float lo = -m_lse[i] * kLog2e;
-                    const float2 off = make_float2(lo, lo), nce = make_float2(-ce, -ce);
-#pragma unroll
-                    for (int j = 0; j < kP; ++j) {
-                        const float2 y = __ffma2_rn(z4[j], cc, off);
-                        float2 g = __fmul2_rn(make_float2(ex2(y.x), ex2(y.y)), nce);
-                        if (!warp_full) {
-                            if (!valid(j, 0)) g.x = 0.f;
-                            if (!valid(j, 1)) g.y = 0.f;
-                        }
-                        gr[S][j] = g;
-                    }
-#pragma unroll
-                    for (int r2 = 0; r2 < kV; ++r2) {
-                        const int64_t d = act - cb[r2];
-                        if (d >= 0 && d < nv[r2]) {
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                if (d == 2 * j) gr[S][4 * r2 + j].x += ce;
-                                if (d == 2 * j + 1) gr[S][4 * r2 + j].y += ce;
-                            }
-                        }
-                    }
+                    for (int j = 0; j < 4; ++j) gr[S][j] = make_float2(0.f, 0.f);  // no row ends here
                 }
-                ++ri;
-                next_end = m_q0[ri] + 3;
             } else if constexpr (kGrad) {
 #pragma unroll
-                for (int j = 0; j < kP; ++j) gr[S][j] = make_float2(0.f, 0.f);  // no row ends here
+                for (int j = 0; j < 4; ++j) gr[S][j] = make_float2(0.f, 0.f);  // past the last position
             }
-        } else if constexpr (kGrad) {
-#pragma unroll
-            for (int j = 0; j < kP; ++j) gr[S][j] = make_float2(0.f, 0.f);  // past the last position
-        }
-        if constexpr (kGrad) {
-            // position p = q - 3 is touched exactly by the rows ending at p .. p + 3: the
-            // four g-ring slots.  H[p] = their sum.
-            const int p = q - 3;
-            if (p >= elo && p < ehi) {
-                if (p >= sg + 32) {  // next group of slots (warp-uniform)
-                    sg += 32;
-                    s_cur = s_next;
-                    s_next = sg + 32 + lane < qb ? __ldg(A.pos_slot + sg + 32 + lane) : -1;
-                }
-                const int32_t sl = __shfl_sync(0xffffffffu, s_cur, p - sg);
-                if (sl >= 0) {
-#pragma unroll
-                    for (int i = 0; i < kV; ++i) {
-                        if (nv[i] > 0) {
-                            float2 h[4];
-#pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                h[j] = __fadd2_rn(__fadd2_rn(gr[0][4 * i + j], gr[1][4 * i + j]),
-                                                  __fadd2_rn(gr[2][4 * i + j], gr[3][4 * i + j]));
-                            FM_DCHECK(sl < A.dbg_kp && cb[i] + 8 <= A.ld_a);
-                            *reinterpret_cast<uint4*>(A.aseg + static_cast<int64_t>(sl) * A.ld_a + cb[i]) = pack8(h);
-                        }
-                    }
-                }
-            }
-        }
-    };
-    const int qend = kGrad ? qb + 3 : qb;
-    if (!fast) {
-        for (int qq = qa & ~3; qq < qend; qq += 4) {
+            if constexpr (kGrad) flush_h(q - 3);
+        };
+        for (int qq = qlo; qq < qend; qq += 4) {
             step(qq, std::integral_constant<int, 0>{});
             step(qq + 1, std::integral_constant<int, 1>{});
             step(qq + 2, std::integral_constant<int, 2>{});
             step(qq + 3, std::integral_constant<int, 3>{});
         }
+        (void)rows_done;
         return;
     }
-    if constexpr (kV == 1) {
-        // Branch-free body over 4 positions: wait for and read all four ring stages first,
-        // then run the four positions' arithmetic as one straight-line block (the row math
-        // unconditionally, zero-weighted where no row ends), so the compiler interleaves
-        // four independent dependency chains instead of serialising position after position.
-        const int d_act0 = static_cast<int>(cb[0] - v0);  // this lane's first column within the slice
-        int rows_done = 0, flushed = 0;  // pass A: rows whose partials are parked / summed
-        // two instances of the loop: warps whose columns are all inside the vocabulary skip
-        // pass A's per-column masks (only the last slice's boundary warp needs them)
-        auto fast_loop = [&](auto FullTag) {
-        constexpr bool kFull = decltype(FullTag)::value;
-        for (int qq = qa & ~3; qq < qend; qq += 4) {
+
+    // Branch-free body over 4 positions: wait for and read the body's four ring stages
+    // (always stages st .. st + 3: the padding positions stream the zero row), then run the
+    // four positions' arithmetic as one straight-line block (the row math unconditionally,
+    // the sentinel row where none ends), so the compiler interleaves four independent
+    // dependency chains instead of serialising position after position.
+    int rows_done = 0, flushed = 0;  // pass A: rows whose partials are parked / summed
+    // two instances of the loop: warps whose columns are all inside the vocabulary skip
+    // pass A's per-column masks (only the last slice's boundary warp needs them)
+    auto fast_loop = [&](auto FullTag) {
+        for (int qq = qlo; qq < qhi; qq += 4) {
             uint4 u[4];
-            int stg[4];
-            bool in[4];
 #pragma unroll
             for (int S = 0; S < 4; ++S) {
-                const int q = qq + S;
-                in[S] = q >= qa && q < qb;
-                u[S] = make_uint4(0u, 0u, 0u, 0u);
-                stg[S] = st;
-                if (in[S]) {
-                    mbar_wait(&full[st], ph);
-                    u[S] = *reinterpret_cast<const uint4*>(ring + st * kStage + tid * 16);
-                    if (++st == kBandStages) {
-                        st = 0;
-                        ph ^= 1u;
-                    }
-                }
+                mbar_wait(&full[st + S], ph);
+                u[S] = *reinterpret_cast<const uint4*>(ring + (st + S) * kStage + tid * 16);
             }
             __syncwarp();
             if (lane == 0) {
 #pragma unroll
-                for (int S = 0; S < 4; ++S)
-                    if (in[S]) mbar_arrive(&empty[stg[S]]);
+                for (int S = 0; S < 4; ++S) mbar_arrive(&empty[st + S]);
+            }
+            st += 4;
+            if (st == kBandStages) {
+                st = 0;
+                ph ^= 1u;
             }
 #pragma unroll
             for (int S = 0; S < 4; ++S) {
@@ -631,86 +594,29 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
                     pr[S][j] = __fadd2_rn(xp[j], x[j]);
                     xp[j] = x[j];
                 }
-                const int k = q - qa;
-                const int i = in[S] ? m_end[k] : -1;
-                const int ii = i < 0 ? 0 : i;
-                const float rs = m_rs[ii];
-                const int dact = m_act[ii] - static_cast<int>(v0) - d_act0;  // action column - this lane's first
+                const int i = m_end[q - qlo];
                 float2 z4[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) z4[j] = __fadd2_rn(pr[(S + 2) & 3][j], pr[S][j]);
-                const float c = rs * kLog2e;
-                const float2 cc = make_float2(c, c);
                 if constexpr (!kGrad) {
-                    const float lo = -m_lse[ii] * kLog2e;  // the row's softmax bound
-                    const float2 off = make_float2(lo, lo);
-                    float2 s2 = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const float2 y = __ffma2_rn(z4[j], cc, off);
-                        float2 e = make_float2(ex2(y.x), ex2(y.y));
-                        if constexpr (!kFull) {
-                            if (!valid(j, 0)) e.x = 0.f;
-                            if (!valid(j, 1)) e.y = 0.f;
-                        }
-                        s2 = __fadd2_rn(s2, e);
+                    const float s = row_sum(z4, m_c[i], m_off[i], FullTag);
+                    // partial sum parked in the warp's 32-row ring (slot i & 31)
+                    if (i != kNoRow) {
+                        redbuf[warp * 32 * kRedPitch + (i & 31) * kRedPitch + lane] = s;
+                        rows_done = i + 1;
                     }
-                    // partial sum parked in the warp's 32-row ring (slot i & 31); the
-                    // halves are summed once per 4-position body (below)
-                    if (i >= 0) redbuf[warp * 32 * kRedPitch + (i & 31) * kRedPitch + lane] = s2.x + s2.y;
-                    if (i >= 0 && static_cast<unsigned>(dact) < static_cast<unsigned>(nv[0])) {
-                        const int rr = rstart + i;
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            if (dact == 2 * j) A.zact[rr] = rs * z4[j].x;
-                            if (dact == 2 * j + 1) A.zact[rr] = rs * z4[j].y;
-                        }
-                    }
-                    if (i >= 0) rows_done = i + 1;
                 } else {
-                    // g = ce (delta(v, a) - exp(z - lse)); ce = 0 where no row ends (and for
-                    // zero-advantage rows, training.hpp:394).  Columns past V hold garbage that
-                    // is never stored: no masks.
-                    const float ce = i >= 0 ? m_ce[ii] : 0.f;
-                    const float lo = i >= 0 ? -m_lse[ii] * kLog2e : -1e30f;  // no row: exp -> +0
-                    const float2 off = make_float2(lo, lo), nce = make_float2(-ce, -ce);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const float2 y = __ffma2_rn(z4[j], cc, off);
-                        gr[S][j] = __fmul2_rn(make_float2(ex2(y.x), ex2(y.y)), nce);
-                    }
-                    if (static_cast<unsigned>(dact) < 8u) {
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            if (dact == 2 * j) gr[S][j].x += ce;
-                            if (dact == 2 * j + 1) gr[S][j].y += ce;
-                        }
-                    }
-                    // position p = q - 3 is touched exactly by the rows ending at p .. p + 3
-                    const int p = q - 3;
-                    if (p >= elo && p < ehi) {
-                        if (p >= sg + 32) {  // next group of slots (warp-uniform)
-                            sg += 32;
-                            s_cur = s_next;
-                            s_next = sg + 32 + lane < qb ? __ldg(A.pos_slot + sg + 32 + lane) : -1;
-                        }
-                        const int32_t sl = __shfl_sync(0xffffffffu, s_cur, p - sg);
-                        if (sl >= 0 && nv[0] > 0) {
-                            float2 h[4];
-#pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                h[j] = __fadd2_rn(__fadd2_rn(gr[0][j], gr[1][j]), __fadd2_rn(gr[2][j], gr[3][j]));
-                            FM_DCHECK(sl < A.dbg_kp && cb[0] + 8 <= A.ld_a);
-                            *reinterpret_cast<uint4*>(A.aseg + static_cast<int64_t>(sl) * A.ld_a + cb[0]) = pack8(h);
-                        }
-                    }
+                    // columns past V hold garbage that is never stored: no masks
+                    row_grad(z4, m_c[i], m_off[i], m_ce[i], m_act[i] - static_cast<int>(v0) - d_lane, gr[S]);
+                    flush_h(q - 3);
                 }
             }
             if constexpr (!kGrad) {
                 // a body ends <= 4 rows, so <= 19 rows are ever parked: every completed
-                // 16-row group (and the tail after the last body), lanes 0-15 add up its rows' 32 lane partials (transposed read of the padded
-                // ring, conflict-free) into the warp's stats column
-                while (rows_done - flushed >= 16 || (qq + 4 >= qend && rows_done > flushed)) {
+                // 16-row group (and the tail after the last body), lanes 0-15 add up its
+                // rows' 32 lane partials (transposed read of the padded ring, conflict-free)
+                // into the warp's stats column
+                while (rows_done - flushed >= 16 || (qq + 4 >= qhi && rows_done > flushed)) {
                     __syncwarp();
                     const int n = rows_done - flushed < 16 ? rows_done - flushed : 16;
                     if (lane < n) {
@@ -724,17 +630,17 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
                             t3 += src[kk + 3];
                         }
                         FM_DCHECK(tile < A.stats_ld && rstart + flushed + lane < A.M);
-                        A.stats[static_cast<int64_t>(tile) * A.ld_stats + rstart + flushed + lane] = (t0 + t1) + (t2 + t3);
+                        A.stats[static_cast<int64_t>(tile) * A.ld_stats + rstart + flushed + lane] =
+                            (t0 + t1) + (t2 + t3);
                     }
                     flushed += n;
                     __syncwarp();
                 }
             }
         }
-        };
-        if (warp_full) fast_loop(std::true_type{});
-        else fast_loop(std::false_type{});
-    }
+    };
+    if (warp_full) fast_loop(std::true_type{});
+    else fast_loop(std::false_type{});
 }
 
 }  // namespace
@@ -769,7 +675,7 @@ cudaError_t launch_pslots(const int32_t* feat, int64_t Q, int nblk, int32_t* kco
 }
 
 int band_stats_ld(int64_t V) {
-    const int64_t cols = kBandConsumers * 8 * kStatsV;
+    const int64_t cols = kBandConsumers * 8;
     return static_cast<int>((V + cols - 1) / cols) * (kBandConsumers / 32);
 }
 
@@ -784,8 +690,8 @@ cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s) {
         kern<<<grid, kBandThreads, smem, s>>>(A);
         return cudaGetLastError();
     };
-    if (grad) return go(band_kernel<true, kGradV, 2>, kBandConsumers * 8 * kGradV, band_smem_bytes<true, kGradV>());
-    return go(band_kernel<false, kStatsV, 2>, kBandConsumers * 8 * kStatsV, band_smem_bytes<false, kStatsV>());
+    if (grad) return go(band_kernel<true, 2>, kBandConsumers * 8, band_smem_bytes<true>());
+    return go(band_kernel<false, 2>, kBandConsumers * 8, band_smem_bytes<false>());
 }
 
 }  // namespace fm

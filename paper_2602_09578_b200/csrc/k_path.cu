@@ -193,7 +193,18 @@ __global__ void __launch_bounds__(256) lse_kernel(const LseArgs L) {
             } else {
                 sum = ((part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane])) +
                       ((part[4][lane] + part[5][lane]) + (part[6][lane] + part[7][lane]));
-                za = L.zact[r];
+                za = 0.f;  // (a vocabulary-gang rank without the action's column contributes 0)
+                const int64_t ac = static_cast<int64_t>(L.rows.action[r]) - L.col_base;
+                if (ac >= 0 && ac < L.ncols) {
+                    const int q = L.rows.q0[r];
+                    float x[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int32_t f = __ldg(L.pos_feat + q + k);
+                        x[k] = f >= 0 ? __bfloat162float(L.w16t[static_cast<int64_t>(f) * L.ldw + ac]) : 0.f;
+                    }
+                    za = L.rows.rscale[r] * ((x[0] + x[1]) + (x[2] + x[3]));
+                }
             }
             if (L.partial_out) {  // this rank's columns only: to the all-reduce
                 L.partial_out[r] = sum;
