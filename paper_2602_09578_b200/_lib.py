@@ -12,6 +12,8 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "_native" / (
     "libflexmarl_b200_debug.so" if os.environ.get("FLEXMARL_DEBUG_LIB") == "1" else "libflexmarl_b200.so")
+if os.environ.get("FLEXMARL_LIB"):  # A/B measurement of a variant build (tools/variant_libs.sh)
+    LIB_PATH = Path(os.environ["FLEXMARL_LIB"]).resolve()
 
 # fm_status (cabi.h) — 1..28 are marlsim::ErrorCode + 1 (errors.hpp:10-39)
 ERROR_NAMES = [
