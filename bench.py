@@ -291,8 +291,8 @@ def run_ours(args, dist: Dist) -> dict | None:
             active[a] = False
     ctx.synchronize()
 
-    # device tier: each agent is suspended right after its update (fm_apply_update_park);
-    # its state stays in its HBM slot and the next activation rebinds it
+    # device tier: each agent parks right after its update, so K-adam writes the new
+    # state into the parking buffer (fm_apply_update_park) instead of a copy-out
     park_fused = swap and len(order) > 1 and tier == _lib.TIER_DEVICE
     tokens_per_step = 0
     FS = _lib.fm_sample
@@ -1383,7 +1383,7 @@ def config_obj(cfg, args) -> dict:
                         f"({cfg.params / 1e6:.1f}M params/agent), GRPO k={cfg.group_k}, micro-batch "
                         f"{cfg.micro_batch}/global {cfg.global_batch}, response {cfg.resp_len} tokens, "
                         f"state swap tier={args.tier}"
-                        + (" (suspend keeps the state in its HBM slot, activate rebinds it: no copy)"
+                        + (" (swap-out fused into K-adam, swap-in a D2D copy on the copy engines)"
                            if args.tier == "device" else
                            " (pinned host parking over PCIe, copy engines)" if args.tier == "host" else ""),
             "agents": na, "vocab": cfg.vocab, "feat": cfg.feat, "micro_batch": cfg.micro_batch,

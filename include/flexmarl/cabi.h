@@ -72,7 +72,7 @@ typedef enum fm_precision {
 /* Where a suspended agent's training state is parked (object_store.hpp:80-86 tiers). */
 typedef enum fm_tier {
     FM_TIER_HOST = 0,   /* pinned host memory of this process (D2H / H2D copies) */
-    FM_TIER_DEVICE = 1, /* this GPU's HBM: the state stays in its slot (no copy) */
+    FM_TIER_DEVICE = 1, /* a parking arena in this GPU's HBM (D2D copy engine) */
     FM_TIER_PEER = 2    /* a peer GPU's HBM over NVLink (cudaMemcpyPeerAsync) */
 } fm_tier;
 
@@ -228,8 +228,9 @@ int fm_agent_poll_report(fm_agent* a, int64_t ticket, fm_report* out);
 int fm_apply_update(fm_agent* a, int64_t global_batch, double lr, double beta1, double beta2,
                     double eps, double* grad_norm_out, int64_t* version_out);
 /* apply_global_update followed by suspend(FM_TIER_DEVICE) (training.hpp:435-456,
- * 321-350) in one call; fm_agent_activate brings it back as after
- * fm_agent_suspend.  Tensor-core agents outside a gang. */
+ * 321-350), fused: K-adam writes the updated state straight into the agent's
+ * parking buffer on its GPU, so no copy-out pass runs; fm_agent_activate
+ * brings it back as after fm_agent_suspend.  Tensor-core agents outside a gang. */
 int fm_apply_update_park(fm_agent* a, int64_t global_batch, double lr, double beta1, double beta2,
                          double eps, double* grad_norm_out, int64_t* version_out);
 
@@ -237,10 +238,7 @@ int fm_apply_update_park(fm_agent* a, int64_t global_batch, double lr, double be
  * suspend: copy {W, m, v, accumulated gradient} to the parking tier on the
  * ctx's copy stream (ordered after the agent's compute) and release the
  * agent's slot; activate: copy back into a slot of `ctx` (may differ from the
- * one it was suspended from), regenerate the bf16 shadow.  FM_TIER_DEVICE
- * keeps the state in its slot on the agent's GPU (the slot stays reserved) and
- * activate on that ctx rebinds it; activate on another ctx first parks it in
- * the old GPU's HBM and then pulls it over NVLink.  Both are async;
+ * one it was suspended from), regenerate the bf16 shadow.  Both are async;
  * compute issued after activate waits on the copy-in event. */
 int fm_agent_suspend(fm_agent* a, int tier, int peer_device);
 int fm_agent_activate(fm_agent* a, fm_ctx* ctx);

@@ -35,15 +35,18 @@ struct RowBuffers {
     int32_t* q0;       // [Mpad] first context position of the row (band formulation; nullable)
     float* mrow;       // [Mpad] softmax bound (1/n) sum_k fmax[f_k] >= max_v z (with fmax)
     const float* fmax; // [D] per-feature maximum of the bf16 shadow (nullable: no bounds)
+    // with w16t (tensor-core path): the taken token's fp32 logit
+    // rs * ((X[f0] + X[f1]) + (X[f2] + X[f3])) at its W16^T column — K-stats' own summation
+    // order, so bit-identical to its z; 0 where the action lies outside [col_base,
+    // col_base + ncols) (a vocabulary-gang rank) — and the row's loss weight -A / G
+    float* zact = nullptr;      // [Mpad]
+    double* lossw = nullptr;    // [Mpad]
+    const __nv_bfloat16* w16t = nullptr;  // W16^T at column col_base
+    int64_t ldw = 0, col_base = 0, ncols = 0;
 };
 
 // K-lse arguments.
 struct LseArgs {
-    // the taken token's fp32 logit, rs * ((X[q0] + X[q0+1]) + (X[q0+2] + X[q0+3])) at its
-    // W16^T column — K-stats' own summation order, so bit-identical to its z
-    const __nv_bfloat16* w16t;  // W16^T at column col_base
-    int64_t ldw, ncols, col_base;
-    const int32_t* pos_feat;    // [Q] position features (-1: before the sequence start)
     const float* stats;   // [stats_ld][Mpad] partial sums of exp(z - mrow) (K-stats)
     int stats_ld;
     int64_t M, Mpad, V;
@@ -120,8 +123,8 @@ cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s);
 int band_stats_ld(int64_t V);
 
 // K-lse: lse = mrow + log(sum of K-stats' partial sums), the taken-token
-// log-prob (its fp32 logit from four W16^T elements) and the effective row
-// coefficient (PPO-clip surrogate optional).
+// log-prob (K-gather's fp32 logit) and the effective row coefficient (PPO-clip
+// surrogate optional).
 cudaError_t launch_lse(const LseArgs& L, cudaStream_t s);
 
 // Parity tooling: out[v][j] = dW[v][cols[j]] (f32 or f64 accumulator).
@@ -134,8 +137,14 @@ cudaError_t launch_gather_cols(const void* dW, bool f64, uint64_t V, uint64_t D,
 // the local partial plus nslots receive slots ([nslots][r1-r0][D], a DP
 // gang's reduce-scatter); the transposed bf16 shadow W16^T [D][ldw] is
 // written (locally and into the peers' replicas over NVLink: the all-gather
-// fused into the optimizer) through a shared-memory transpose; the gradient
-// is zeroed (parity mode).  Accumulates sum(g^2) into *gsq.
+// fused into the optimizer) through a shared-memory transpose; the new w / m
+// / v go to dst instead of in place (the swap-out fused into the optimizer);
+// the gradient is zeroed (parity mode).  Accumulates sum(g^2) into *gsq.
+struct AdamDst {
+    double* w;
+    float* m;
+    float* v;
+};
 // Peer W16^T replicas (NVLink-mapped base pointers) of a DP gang, excluding self.
 struct ShardPeers {
     int n;
@@ -145,7 +154,7 @@ template <typename G>
 cudaError_t launch_adam(double* w, float* m, float* v, G* g, uint64_t V, uint64_t D, uint64_t r0, uint64_t r1,
                         const float* recv, int nslots, __nv_bfloat16* w16t, uint64_t ldw, ShardPeers peers,
                         double lr, double b1, double b2, double eps, double bc1, double bc2, int zero_grad,
-                        double* gsq, int num_sms, cudaStream_t s);
+                        double* gsq, int num_sms, cudaStream_t s, const AdamDst* dst = nullptr);
 
 // W16^T [D][ldw] = bf16(W) for W [V][D] f64 (shadow refresh: set_weights, host-tier swap-in).
 cudaError_t launch_w16t(const double* w, uint64_t V, uint64_t D, __nv_bfloat16* w16t, uint64_t ldw, int num_sms,

@@ -165,6 +165,8 @@ void ws_free(Workspace& w) {
     cudaFree(w.old_logp);
     cudaFree(w.q0);
     cudaFree(w.mrow);
+    cudaFree(w.zact);
+    cudaFree(w.lossw);
     cudaFree(w.pos_feat);
     cudaFree(w.pos_slot);
     cudaFree(w.stats);
@@ -230,6 +232,8 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D, int n_samples
     e = e ? e : dalloc(&w.coef_eff, R);
     e = e ? e : dalloc(&w.q0, R);
     e = e ? e : dalloc(&w.mrow, R);
+    e = e ? e : dalloc(&w.zact, R);
+    e = e ? e : dalloc(&w.lossw, R);
     e = e ? e : dalloc(&w.stats, static_cast<size_t>(R) * tiles_n);  // [tiles][R] partial sums
     e = e ? e : dalloc(&w.pos_feat, static_cast<size_t>(Q));
     e = e ? e : dalloc(&w.pos_slot, static_cast<size_t>(Q));
@@ -692,12 +696,6 @@ int fm_agent_destroy(fm_agent* a) {
     if (!a) return FM_OK;
     if (a->lent) fm_agent_migrate_release(a);
     fm_gang_detach(a);
-    if (a->kept) {  // suspended on the device tier: rebind to release the slot below
-        agent_bind_slot(a, a->kept);
-        a->ctx = a->kept_ctx;
-        a->kept = nullptr;
-        a->kept_ctx = nullptr;
-    }
     if (a->ctx) {
         cudaSetDevice(a->ctx->device);
         cudaStreamSynchronize(a->ctx->stream);
@@ -1070,6 +1068,12 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 count_launch();
             }
             rows.fmax = a->fmax;
+            rows.zact = w.zact;
+            rows.lossw = w.lossw;
+            rows.w16t = a->W16 + c0;
+            rows.ldw = static_cast<int64_t>(w16_ld(a));
+            rows.col_base = c0;
+            rows.ncols = c1 - c0;
             {
                 // K-gather (rows, q0, bounds) + K-pos (position features) + K-pslot (segment
                 // slots, one-hot B')
@@ -1112,7 +1116,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             }
             {
                 KScope k(c, K_LSE, s);
-                LseArgs L{ba.w16t, ba.ldw, c1 - c0, c0, w.pos_feat, w.stats, ba.stats_ld, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
+                LseArgs L{w.stats, ba.stats_ld, M, Mpad, static_cast<int64_t>(a->V), w.sd, G, rows,
                           clip ? w.old_logp : nullptr, row_lo, a->clip_eps, scal + 1};
                 if (vg) {
                     // vocabulary gang: per row (sum over my columns, taken logit or 0), summed
@@ -1368,9 +1372,10 @@ int fm_agent_poll_report(fm_agent* a, int64_t ticket, fm_report* out) {
 }
 
 
-// apply_global_update; with park != 0 (tensor-core agent, no gang) the agent
-// is suspended to the device tier right after K-adam (fm_agent_suspend with
-// FM_TIER_DEVICE: its state stays in its HBM slot).
+// apply_global_update; with park != 0 (device tier, tensor-core agent, no gang)
+// K-adam writes the new W / m / v / W16^T straight into the agent's
+// parking buffer and the agent is suspended — the swap-out fused into the
+// optimizer (no copy-out pass).
 static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, double b2, double eps,
                              double* grad_norm_out, int64_t* version_out, bool park) {
     if (int st = check_active(a)) return st;
@@ -1380,10 +1385,16 @@ static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, doubl
     fm_ctx* c = a->ctx;
     if (int st = set_dev(c)) return st;
     cudaStream_t s = c->stream;
+    AdamDst dst{};
+    uint8_t* pk = nullptr;
     if (park) {
         if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang (fm_gang_detach first)");
         if (a->precision != FM_PRECISION_BF16_TC || !a->W16)
             return fail(FM_ERR_INVALID_ARG, "update-and-park needs a tensor-core agent");
+        if (int st = park_reserve(a, c, FM_TIER_DEVICE, c->device, park_bytes_for(a))) return st;
+        pk = static_cast<uint8_t*>(a->park);
+        dst = AdamDst{reinterpret_cast<double*>(pk), reinterpret_cast<float*>(pk + a->P * 8),
+                      reinterpret_cast<float*>(pk + a->P * 12)};
     }
     if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * dw_elem(a), s));
     a->step += 1;
@@ -1412,9 +1423,13 @@ static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, doubl
         // global grad norm^2; doubles as the barrier after the peers' W16^T writes
         FM_NCCL(ncclAllReduce(a->d_upd, a->d_upd, 1, ncclFloat64, ncclSum, gang_comm(gs), s));
     } else {
-        // the next step's first GEMM2 overwrites dW, so no zeroing pass here
+        // the next step's first GEMM2 overwrites dW, so no zeroing pass here; with park the
+        // new state goes straight into the parking buffer
+        const size_t dwe = dw_elem(a);
+        __nv_bfloat16* w16_out = park ? reinterpret_cast<__nv_bfloat16*>(pk + a->P * (16 + dwe)) : a->W16;
         FM_CUDA(launch_adam<float>(a->W, a->m, a->v, static_cast<float*>(a->dW), a->V, a->D, 0, a->V, nullptr, 0,
-                                   a->W16, w16_ld(a), none, lr, b1, b2, eps, bc1, bc2, 0, a->d_upd, c->num_sms, s));
+                                   w16_out, w16_ld(a), none, lr, b1, b2, eps, bc1, bc2, 0, a->d_upd, c->num_sms, s,
+                                   park ? &dst : nullptr));
     }
     count_launch();
     a->dw_valid = false;
@@ -1423,7 +1438,14 @@ static int apply_update_impl(fm_agent* a, int64_t G, double lr, double b1, doubl
     a->grad_keys.clear();
     a->fmax_valid = false;  // the shadow changed
     FM_CUDA(cudaMemcpyAsync(a->h_upd, a->d_upd, sizeof(double), cudaMemcpyDeviceToHost, s));
-    if (park) agent_keep_slot(a);  // suspended to the device tier: the state stays in its slot
+    if (park) {
+        // the parked state is complete when K-adam is: release the slot behind it
+        a->park_w16 = true;
+        FM_CUDA(cudaEventRecord(a->ev_out, s));
+        agent_free_device(a, s);
+        a->active = false;
+        a->ctx = nullptr;
+    }
     if (grad_norm_out) {
         FM_CUDA(cudaStreamSynchronize(s));
         *grad_norm_out = std::sqrt(*a->h_upd);

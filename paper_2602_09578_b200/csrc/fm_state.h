@@ -79,6 +79,8 @@ struct Workspace {
     int32_t *pos_feat = nullptr, *pos_slot = nullptr;
     int64_t pos_cap = 0;
     float* mrow = nullptr;   // per-row softmax bound (1/n) sum_k fmax[f_k] [Mpad]
+    float* zact = nullptr;   // the taken token's logit [Mpad]
+    double* lossw = nullptr; // the row's loss weight -A / G [Mpad]
     float* stats = nullptr;  // K-stats partial sums exp(z - mrow), [stats_ld][Mpad]
     // segments of K-GEMM2: A' = per-position gradient rows H [kp_cap][ldz] bf16,
     // B' = one-hot [kp_cap][256] bf16
@@ -272,11 +274,6 @@ struct fm_agent {
     fm_comm* norm_comm = nullptr;  // exact DP micro-batch grad norms over this communicator
     bool lent = false;             // exported by migration; slot reserved until migrate_release
     Slot* slot = nullptr;
-    // device-tier suspend on the agent's own GPU keeps the training state where it is:
-    // the slot stays reserved (kept) and activation on that context rebinds it
-    Slot* kept = nullptr;
-    fm_ctx* kept_ctx = nullptr;
-    bool kept_fmax = false;
     GangState* gang = nullptr;
 };
 
@@ -332,10 +329,8 @@ void agent_unbind(fm_agent* a);
 int check_active(fm_agent* a);
 }  // namespace fm
 
-// ---- parking buffers (fm_swap.cu) ----
+// ---- parking buffers (fm_swap.cu), also written by the fused update-and-park ----
 extern "C" {
-// Device-tier suspend on the agent's own GPU: keep the slot (no copy).
-void agent_keep_slot(fm_agent* a);
 // Park layout: W | m | v | dW | W16^T.
 size_t park_bytes_for(const fm_agent* a);
 // Parking buffer of `bytes` on `tier` (device pdev), reused while it fits.

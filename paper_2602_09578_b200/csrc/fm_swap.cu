@@ -50,40 +50,8 @@ int park_reserve(fm_agent* a, fm_ctx* c, int tier, int pdev, size_t bytes) {
     return FM_OK;
 }
 
-// Device-tier suspend on the agent's own GPU: the training state stays in its
-// HBM slot, which remains reserved; activation on the same context rebinds it
-// (no bytes move — a parking copy on the same HBM would read and write 2 x 16 B
-// per parameter for nothing).  Activation on another GPU first materialises
-// the ordinary device-tier park (suspend_copy) and then pulls it over NVLink.
-void agent_keep_slot(fm_agent* a) {
-    a->kept = a->slot;
-    a->kept_ctx = a->ctx;
-    a->kept_fmax = a->fmax_valid;
-    agent_unbind(a);
-    a->active = false;
-    a->ctx = nullptr;
-    a->park_tier = FM_TIER_DEVICE;
-    a->park_device = a->kept_ctx->device;
-}
-
-static int suspend_copy(fm_agent* a, int tier, int peer_device);
-
 int fm_agent_suspend(fm_agent* a, int tier, int peer_device) {
     FM_GUARD_BEGIN
-    if (int st = check_active(a)) return st;
-    if (a->gang) return fail(FM_ERR_BUSY_GROUP, a->name + " is attached to a DP gang (fm_gang_detach first)");
-    if (tier == FM_TIER_DEVICE) {
-        agent_keep_slot(a);
-        return FM_OK;
-    }
-    return suspend_copy(a, tier, peer_device);
-    FM_GUARD_END
-}
-
-}  // extern "C"
-
-// Copies the state into the parking buffer on `tier` and releases the slot.
-static int suspend_copy(fm_agent* a, int tier, int peer_device) {
     // a K-stats launched after the agent's last op (e.g. the next agent's first
     // micro-batch) is a safe and cheap start for the copy-out: the copy engines then
     // overlap the streaming passes instead of the latency-bound K-gather that follows
@@ -127,26 +95,14 @@ static int suspend_copy(fm_agent* a, int tier, int peer_device) {
     a->ctx = nullptr;
     a->park_device = pdev;
     return FM_OK;
+    FM_GUARD_END
 }
-
-extern "C" {
 
 int fm_agent_activate(fm_agent* a, fm_ctx* c) {
     FM_GUARD_BEGIN
     if (a->active) return fail(FM_ERR_CONFIG_ERROR, a->name + " already active");
     if (a->lent) return fail(FM_ERR_CONFIG_ERROR, a->name + " was migrated away (fm_agent_migrate_release)");
     if (!c) return fail(FM_ERR_NO_DEVICE, "null context");
-    if (a->kept) {
-        fm_ctx* kc = a->kept_ctx;
-        agent_bind_slot(a, a->kept);
-        a->fmax_valid = a->kept_fmax;
-        a->kept = nullptr;
-        a->kept_ctx = nullptr;
-        a->ctx = kc;
-        a->active = true;
-        if (kc == c) return FM_OK;  // the state never left: rebind
-        if (int st = suspend_copy(a, FM_TIER_DEVICE, kc->device)) return st;
-    }
     if (int st = set_dev(c)) return st;
     const size_t P = a->P;
     // the parked copy must have landed before we read it back (a cross-device wait when

@@ -513,6 +513,17 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
                         h[j] = __fadd2_rn(__fadd2_rn(gr[0][j], gr[1][j]), __fadd2_rn(gr[2][j], gr[3][j]));
+                    if (nv < 8) {
+                        // the row's columns past V (up to its 8-aligned pitch) hold arithmetic on
+                        // stale ring bytes: store zeros, so every A' byte stays finite — A' is
+                        // reused across agents of other widths, whose segment padding rows (B' = 0)
+                        // may land there, and 0 x NaN would poison their dW
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            if (2 * j >= nv) h[j].x = 0.f;
+                            if (2 * j + 1 >= nv) h[j].y = 0.f;
+                        }
+                    }
                     FM_DCHECK(sl < A.dbg_kp && cb + 8 <= A.ld_a);
                     *reinterpret_cast<uint4*>(A.aseg + static_cast<int64_t>(sl) * A.ld_a + cb) = pack8(h);
                 }
@@ -645,7 +656,7 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
                             rows_done = i + 1;
                         }
                     } else {
-                        // columns past V hold garbage that is never stored: no masks
+                        // columns past V hold arithmetic on stale bytes, zeroed when stored (flush_h)
                         row_grad(z4, m_c[i], m_off[i], m_ce[i], m_act[i] - static_cast<int>(v0) - d_lane, gr[S]);
                         flush_h(q - 3);
                     }

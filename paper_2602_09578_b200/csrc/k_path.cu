@@ -101,6 +101,10 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
         rows.coef[r] = 0.f;
         rows.rscale[r] = 0.f;
         if (rows.fmax) rows.mrow[r] = 0.f;
+        if (rows.w16t) {
+            rows.zact[r] = 0.f;
+            rows.lossw[r] = 0.0;
+        }
         return;
     }
     const int64_t gr = row_lo + r;
@@ -138,6 +142,23 @@ __global__ void __launch_bounds__(256) gather_kernel(const uint8_t* __restrict__
         }
         rows.mrow[r] = rs * ((fm[0] + fm[1]) + (fm[2] + fm[3]));
     }
+    if (rows.w16t) {
+        // the taken token's logit in K-stats' order (positions before the start are 0)
+        const int64_t ac = static_cast<int64_t>(action) - rows.col_base;
+        float za = 0.f;
+        if (ac >= 0 && ac < rows.ncols) {
+            float x[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int j = k - (4 - n);
+                x[k] = j >= 0 ? __bfloat162float(rows.w16t[static_cast<int64_t>(feature_of(ctx[j], D)) * rows.ldw + ac])
+                              : 0.f;
+            }
+            za = rs * ((x[0] + x[1]) + (x[2] + x[3]));
+        }
+        rows.zact[r] = za;
+        rows.lossw[r] = -(d.adv / static_cast<double>(G));
+    }
     if (rows.q0) {
         // band formulation (k_band.cu): every sample overlapping the shard owns its rows + 3
         // positions; this row's four context positions start at q0
@@ -160,16 +181,25 @@ __global__ void __launch_bounds__(256) lse_kernel(const LseArgs L) {
     const int64_t r = static_cast<int64_t>(blockIdx.x) * 32 + lane;
     const bool live = r < L.M;
     if (!L.sum_in) {
-        float s0 = 0.f, s1 = 0.f;
+        // 16 slices per warp in flight before any add: the loads are latency-bound (and share
+        // HBM with a concurrent swap copy), the adds are free
+        float acc = 0.f;
         if (live) {
-            int t = wid;
-            for (; t + 8 < L.stats_ld; t += 16) {
-                s0 += __ldg(L.stats + static_cast<int64_t>(t) * L.Mpad + r);
-                s1 += __ldg(L.stats + static_cast<int64_t>(t + 8) * L.Mpad + r);
+            for (int t0 = 0; t0 < L.stats_ld; t0 += 128) {
+                float x[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const int t = t0 + wid + 8 * k;
+                    x[k] = t < L.stats_ld ? __ldg(L.stats + static_cast<int64_t>(t) * L.Mpad + r) : 0.f;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) x[k] += x[k + 8];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) x[k] += x[k + 4];
+                acc += (x[0] + x[2]) + (x[1] + x[3]);
             }
-            if (t < L.stats_ld) s0 += __ldg(L.stats + static_cast<int64_t>(t) * L.Mpad + r);
         }
-        part[wid][lane] = s0 + s1;
+        part[wid][lane] = acc;
         __syncthreads();
     }
     if (wid != 0) return;
@@ -193,25 +223,14 @@ __global__ void __launch_bounds__(256) lse_kernel(const LseArgs L) {
             } else {
                 sum = ((part[0][lane] + part[1][lane]) + (part[2][lane] + part[3][lane])) +
                       ((part[4][lane] + part[5][lane]) + (part[6][lane] + part[7][lane]));
-                za = 0.f;  // (a vocabulary-gang rank without the action's column contributes 0)
-                const int64_t ac = static_cast<int64_t>(L.rows.action[r]) - L.col_base;
-                if (ac >= 0 && ac < L.ncols) {
-                    const int q = L.rows.q0[r];
-                    float x[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int32_t f = __ldg(L.pos_feat + q + k);
-                        x[k] = f >= 0 ? __bfloat162float(L.w16t[static_cast<int64_t>(f) * L.ldw + ac]) : 0.f;
-                    }
-                    za = L.rows.rscale[r] * ((x[0] + x[1]) + (x[2] + x[3]));
-                }
+                za = L.rows.zact[r];  // (0 on a vocabulary-gang rank without the action's column)
             }
             if (L.partial_out) {  // this rank's columns only: to the all-reduce
                 L.partial_out[r] = sum;
                 L.partial_out[L.Mpad + r] = za;
             } else {
                 const int a = rows.action[r];
-                const double adv = L.sd[rows.sample[r]].adv;
+                const double lw = rows.lossw[r];  // -A / G
                 const float lse = rows.mrow[r] + __logf(sum);
                 const bool valid = a >= 0 && a < L.V;
                 const float lp = valid ? za - lse : 0.f;  // policy.hpp:72-75, fp32 logit
@@ -220,13 +239,13 @@ __global__ void __launch_bounds__(256) lse_kernel(const LseArgs L) {
                     // PPO clipped-ratio surrogate min(rho*A, clip(rho,1-e,1+e)*A): the
                     // gradient flows (scaled by rho) only through the unclipped branch.
                     const float rho = __expf(lp - L.old_logp[L.row_lo + r]);
-                    const bool active = adv >= 0.0 ? rho <= 1.f + L.clip_eps : rho >= 1.f - L.clip_eps;
+                    const bool active = lw <= 0.0 ? rho <= 1.f + L.clip_eps : rho >= 1.f - L.clip_eps;  // A >= 0
                     ce = active ? ce * rho : 0.f;
                 }
                 rows.lse[r] = lse;
                 rows.logp[r] = lp;
                 rows.coef_eff[r] = ce;
-                loss = valid ? -(adv / static_cast<double>(L.G)) * static_cast<double>(lp) : 0.0;
+                loss = valid ? lw * static_cast<double>(lp) : 0.0;
                 // the bound keeps sum >= exp(max z - mrow); a vanishing sum would mean the bound
                 // overshot the logits by ~87: report NaN rather than a silently wrong gradient
                 if (!(sum >= 1e-30f) || !isfinite(sum)) loss = __longlong_as_double(0x7ff8000000000000ll);
@@ -293,6 +312,9 @@ struct AdamTileArgs {
     __nv_bfloat16* w16t;
     uint64_t ldw;
     ShardPeers peers;
+    double* w_o;  // the swap-out fused into the optimizer: new w / m / v here (else in place)
+    float* m_o;
+    float* v_o;
     int zero_grad;
     double* gsq;
     double lr, b1, b2, eps, bc1, bc2;
@@ -425,9 +447,9 @@ __global__ void __launch_bounds__(256, FM_ADAM_MIN_BLOCKS) adam_tile_kernel(cons
                     wf[j] = static_cast<float>(wv[j]);
                 }
             }
-            double* const w_o = A.w;
-            float* const m_o = A.m;
-            float* const v_o = A.v;
+            double* const w_o = A.w_o ? A.w_o : A.w;
+            float* const m_o = A.w_o ? A.m_o : A.m;
+            float* const v_o = A.w_o ? A.v_o : A.v;
             if constexpr (kVec) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) reinterpret_cast<double2*>(w_o + i0)[q] = make_double2(wv[2 * q], wv[2 * q + 1]);
@@ -684,11 +706,13 @@ template <typename G>
 cudaError_t launch_adam(double* w, float* m, float* v, G* g, uint64_t V, uint64_t D, uint64_t r0, uint64_t r1,
                         const float* recv, int nslots, __nv_bfloat16* w16t, uint64_t ldw, ShardPeers peers, double lr,
                         double b1, double b2, double eps, double bc1, double bc2, int zero_grad, double* gsq,
-                        int num_sms, cudaStream_t s) {
+                        int num_sms, cudaStream_t s, const AdamDst* dst) {
     if (r1 <= r0 || D == 0) return cudaSuccess;
     if ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(g)) & 15) return cudaErrorMisalignedAddress;
+    if (dst && (reinterpret_cast<uintptr_t>(dst->w) & 15)) return cudaErrorMisalignedAddress;
     if (w16t && ((r0 & 7) || (ldw & 7))) return cudaErrorInvalidValue;
-    AdamTileArgs<G> A{w, m, v, g, V, D, r0, r1, recv, nslots, w16t, ldw, peers, zero_grad, gsq, lr, b1, b2, eps, bc1, bc2, AdamF(lr, b1, b2, eps, bc1, bc2)};
+    AdamTileArgs<G> A{w, m, v, g, V, D, r0, r1, recv, nslots, w16t, ldw, peers,
+                      dst ? dst->w : nullptr, dst ? dst->m : nullptr, dst ? dst->v : nullptr, zero_grad, gsq, lr, b1, b2, eps, bc1, bc2, AdamF(lr, b1, b2, eps, bc1, bc2)};
     const uint64_t tiles = ((r1 - r0 + kTileV - 1) / kTileV) * ((D + kTileD - 1) / kTileD);
     const uint64_t cap = static_cast<uint64_t>(num_sms) * 64;
     const int grid = static_cast<int>(tiles < cap ? tiles : cap);
@@ -704,10 +728,12 @@ cudaError_t launch_adam(double* w, float* m, float* v, G* g, uint64_t V, uint64_
 }
 template cudaError_t launch_adam<float>(double*, float*, float*, float*, uint64_t, uint64_t, uint64_t, uint64_t,
                                         const float*, int, __nv_bfloat16*, uint64_t, ShardPeers, double, double,
-                                        double, double, double, double, int, double*, int, cudaStream_t);
+                                        double, double, double, double, int, double*, int, cudaStream_t,
+                                        const AdamDst*);
 template cudaError_t launch_adam<double>(double*, float*, float*, double*, uint64_t, uint64_t, uint64_t, uint64_t,
                                          const float*, int, __nv_bfloat16*, uint64_t, ShardPeers, double, double,
-                                         double, double, double, double, int, double*, int, cudaStream_t);
+                                         double, double, double, double, int, double*, int, cudaStream_t,
+                                        const AdamDst*);
 
 cudaError_t launch_w16t(const double* w, uint64_t V, uint64_t D, __nv_bfloat16* w16t, uint64_t ldw, int num_sms,
                         cudaStream_t s) {

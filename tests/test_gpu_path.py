@@ -268,7 +268,7 @@ def test_w16t_shadow_tracks_weights(ctx, V, D):
     W0 = rng.normal(size=(V, D)) * 0.5
     eng = TrainingEngine([ctx], global_batch=16, precision=_lib.PRECISION_BF16_TC)
 
-    def check_shadow(h):
+    def check_shadow(h, tag=""):
         W = np.empty(V * D)
         _lib.check(L.fm_agent_read_weights(h, W.ctypes.data))
         w = C.c_void_p()
@@ -277,7 +277,12 @@ def test_w16t_shadow_tracks_weights(ctx, V, D):
         _lib.check(L.fm_weights_get(w, out.data_ptr(), -1))
         _lib.check(L.fm_weights_destroy(w))
         want = torch.tensor(W).float().bfloat16()
-        assert torch.equal(out.view(torch.int16), want.view(torch.int16))
+        bad = (out.view(torch.int16) != want.view(torch.int16)).reshape(V, D)
+        if bad.any():
+            idx = bad.nonzero()
+            raise AssertionError(f"{tag}: {int(bad.sum())} shadow elements differ; vocab rows "
+                                 f"{idx[:, 0].min().item()}..{idx[:, 0].max().item()}, features "
+                                 f"{idx[:, 1].min().item()}..{idx[:, 1].max().item()}")
 
     try:
         eng.add_agent("t", V, D)
@@ -285,7 +290,7 @@ def test_w16t_shadow_tracks_weights(ctx, V, D):
         eng.run()
         h = eng.handle("t")
         _lib.check(L.fm_agent_set_weights(h, np.ascontiguousarray(W0).ctypes.data))
-        check_shadow(h)
+        check_shadow(h, "set_weights")
         samples = [(rng.integers(0, V, size=4).astype(np.int32), rng.integers(0, V, size=20).astype(np.int32))
                    for _ in range(16)]
         arr = (_lib.fm_sample * 16)(*[_lib.fm_sample(ctx.put(orc.encode(p)), ctx.put(orc.encode(r)), a)
@@ -298,10 +303,10 @@ def test_w16t_shadow_tracks_weights(ctx, V, D):
                 _lib.check(L.fm_agent_activate(h, ctx.handle))
             else:
                 _lib.check(L.fm_apply_update(h, 16, 1e-2, 0.9, 0.999, 1e-8, None, None))
-            check_shadow(h)
+            check_shadow(h, f"step {step}")
         _lib.check(L.fm_agent_suspend(h, _lib.TIER_HOST, -1))
         _lib.check(L.fm_agent_activate(h, ctx.handle))
-        check_shadow(h)
+        check_shadow(h, "host-tier swap")
     finally:
         eng.close()
 
@@ -592,3 +597,29 @@ def test_shard_gradients_sum_to_whole(ctx, nranks):
             eng.close()
     # positions at a cut are rounded to bf16 as two partial rows instead of one sum
     assert rel_fro(total, whole) <= 1e-3
+
+
+def test_segment_buffer_reuse_across_widths(ctx):
+    """K-GEMM2's A' segments are one workspace reused by agents of every width:
+    an agent whose V is not a multiple of 8 leaves its rows' pitch columns
+    behind, and a later, wider agent's segment padding rows (B' = 0 there) read
+    them.  They must be finite — 0 x NaN would poison that agent's dW (the
+    regression: K-band stored arithmetic on stale ring bytes past V)."""
+    L = _lib.lib()
+    rng = np.random.default_rng(17)
+    for V, D in [(300, 72), (1004, 136), (4000, 4096)]:
+        h = C.c_void_p()
+        _lib.check(L.fm_agent_create(ctx.handle, b"w", V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
+        try:
+            W0 = np.ascontiguousarray(rng.normal(size=(V, D)) * 0.5)
+            _lib.check(L.fm_agent_set_weights(h, W0.ctypes.data))
+            arr = (_lib.fm_sample * 16)(*[_lib.fm_sample(ctx.put(orc.encode(rng.integers(0, V, size=4).astype(np.int32))),
+                                                         ctx.put(orc.encode(rng.integers(0, V, size=20).astype(np.int32))),
+                                                         float(a)) for a in rng.normal(size=16)])
+            t = C.c_int64()
+            _lib.check(L.fm_train_micro_batch(h, arr, 16, 16, C.byref(t)))
+            g = np.empty(V * D)
+            _lib.check(L.fm_agent_read_grad(h, g.ctypes.data))
+            assert np.all(np.isfinite(g)), (V, D)
+        finally:
+            L.fm_agent_destroy(h)

@@ -98,7 +98,7 @@ def test_peer_tier_swap_identity(back_on, tier):
         assert before == checksum(stayed)
         if tier == "peer":
             _lib.check(L.fm_agent_suspend(moved, _lib.TIER_PEER, 1))
-        else:  # kept in its GPU-0 slot; activation on GPU 1 parks it on GPU 0, then pulls it over NVLink
+        else:  # parked in GPU 0's HBM; activation on GPU 1 pulls it over NVLink
             _lib.check(L.fm_agent_suspend(moved, _lib.TIER_DEVICE, -1))
             assert L.fm_agent_is_active(moved) == 0
         _lib.check(L.fm_agent_activate(moved, ctxs[back_on].handle))
