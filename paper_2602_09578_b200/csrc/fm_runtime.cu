@@ -1106,8 +1106,6 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             ba.ld_a = static_cast<int64_t>(ldz);
             ba.dbg_kp = w.kp_cap;
             ba.dbg_D = static_cast<int64_t>(a->D);
-            FM_CUDA(cudaEventRecord(c->ev_gemm, s));  // swap copies may start here (fm_agent_suspend)
-            c->gemm_seq = ++c->op_seq;
             const bool cols = c1 > c0;  // (a vocabulary-gang rank may own no columns)
             {
                 // K-stats: per-(row, 256-column tile) softmax partials + the taken token's logit
@@ -1135,6 +1133,11 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 }
                 FM_CUDA(launch_lse(L, s));
             }
+            // swap copies (fm_agent_suspend / fm_agent_activate) may start here: beside the
+            // streaming K-band / K-GEMM2 / next K-stats rather than the latency-bound K-lse
+            // (0.013 -> 0.09 ms next to a 2.4 GB copy-engine copy)
+            FM_CUDA(cudaEventRecord(c->ev_gemm, s));
+            c->gemm_seq = ++c->op_seq;
             if (cols) {
                 // K-band: per-position gradient rows H into the feature blocks' A' segments
                 KScope k(c, K_BAND, s);
