@@ -417,7 +417,10 @@ def run_ours(args, dist: Dist) -> dict | None:
         b = None
         if name == "gemm2":
             rows = g2rows.value / kcnt[i]
-            b = 2.0 * rows * V + (4.0 * P + (n_mb - 1) * 8.0 * P) / n_mb
+            # launches per agent-step: 1 when the step's micro-batches are batched into one
+            # K-GEMM2 (dW written once), else n_mb (the first stores, the rest add)
+            lps = max(1.0, kcnt[i] / (args.steps * max(1, len(mine))))
+            b = 2.0 * rows * V + (4.0 * P + (lps - 1) * 8.0 * P) / lps
             ex = 2.0 * V * 256 * rows
             e.update(executed_flops=ex, tflops=round(ex / (avg_ms / 1e3) / 1e12, 1),
                      note="segmented K: one-hot scatter of per-position gradient rows (tcgen05)")

@@ -13,6 +13,7 @@ namespace fm {
 
 constexpr int kGemmBN = 256;
 constexpr int kGemmBK = 64;
+constexpr int kGemmMaxBatch = 4;  // micro-batches one K-GEMM2 launch can reduce
 
 // C[M][N] (+)= sum_k A(m, k) * B(n, k) on the CTA-pair tcgen05 kernel; A / B
 // bf16, K-major ([M][K] / [N][K], TMA boxes {64, 128}) or MN-major ([K][M] /
@@ -36,6 +37,24 @@ struct GemmArgs {
     const int32_t* kseg_off = nullptr;
     const int32_t* kseg_iters = nullptr;
     long long dbg_krows = 0;  // rows of A' / B' (debug-build bounds checks; 0 = unchecked)
+    // Batched micro-batches (segmented path, no exchange): every output tile runs nmb
+    // units back to back, unit u over micro-batch u's segments (maps.a[u] / maps.b[u],
+    // kseg_off_b[u] / kseg_iters_b[u]) into the other TMEM buffer, and its epilogue adds
+    // sum(acc^2) into sumsq_b[u] and the tile into dW (store for u = 0 without
+    // accumulate) — the tile's dW stays in L2 between its units.  nmb = 1: the fields
+    // above.
+    int nmb = 1;
+    const int32_t* kseg_off_b[kGemmMaxBatch] = {};
+    const int32_t* kseg_iters_b[kGemmMaxBatch] = {};
+    double* sumsq_b[kGemmMaxBatch] = {};
+};
+
+// The kernel's tensor maps (a __grid_constant__ parameter): A / B of every batched
+// unit and the fp32 output map.
+struct GemmMaps {
+    CUtensorMap a[kGemmMaxBatch];
+    CUtensorMap b[kGemmMaxBatch];
+    CUtensorMap c;
 };
 
 size_t gemm_smem_bytes();
@@ -43,9 +62,9 @@ size_t gemm_smem_bytes();
 // tmC: the output's fp32 map (make_tmap_f32_out) for the TMA reduce-add / store epilogue.
 cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, int a_mn,
                               int b_mn, int M, int N, int K, float* C, int num_sms, cudaStream_t stream);
-// K-GEMM2 over segments (args.kseg_off / kseg_iters), MN-major tile maps.
-cudaError_t gemm_kseg_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
-                             const GemmArgs& args, int num_sms, cudaStream_t stream);
+// K-GEMM2 over segments, MN-major tile maps: nmb = 1 (args.kseg_off / kseg_iters /
+// sumsq, maps.a[0] / b[0]) or a batch of micro-batches (the _b arrays).
+cudaError_t gemm_kseg_launch(const GemmMaps& maps, const GemmArgs& args, int num_sms, cudaStream_t stream);
 // fp32 [rows][cols] (row pitch `pitch` elements, a multiple of 4) with box {32, 32},
 // SWIZZLE_128B: the GEMM epilogue's per-warp output tile.
 bool make_tmap_f32_out(CUtensorMap* map, const float* base, uint64_t rows, uint64_t cols, uint64_t pitch);

@@ -172,6 +172,12 @@ void ws_free(Workspace& w) {
     cudaFree(w.stats);
     cudaFree(w.aseg);
     cudaFree(w.bseg);
+    for (auto& x : w.xset) {
+        cudaFree(x.aseg);
+        cudaFree(x.bseg);
+        cudaFree(x.kseg_off);
+        cudaFree(x.kiters);
+    }
     cudaFree(w.zero_row);
     cudaFree(w.kcount);
     cudaFree(w.kseg_off);
@@ -188,6 +194,11 @@ void ws_free(Workspace& w) {
 
 uint64_t round_up(uint64_t x, uint64_t m) { return (x + m - 1) / m * m; }
 
+Workspace::SegSet seg_set(Workspace& w, int k) {
+    if (k == 0) return Workspace::SegSet{w.aseg, w.bseg, w.kseg_off, w.kiters};
+    return w.xset[k - 1];
+}
+
 // Ensure tensor-core workspace for Mpad rows of at most n samples, vocab V,
 // features D: row buffers, K-stats partials, positions (Mpad + 3 n) and the
 // K-GEMM2 segments (positions + 64 padding rows per 256-feature block).
@@ -195,6 +206,7 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D, int n_samples
     Workspace& w = c->ws;
     const int64_t Qneed = Mpad + 3 * static_cast<int64_t>(std::max(n_samples, 1));
     if (Mpad <= w.rows_cap && V <= w.vocab_cap && D <= w.feat_cap && Qneed <= w.pos_cap && w.aseg) return FM_OK;
+    if (int st = ctx_flush(c)) return st;  // deferred K-GEMM2s read the segment sets
     const int64_t R = std::max<int64_t>(Mpad, w.rows_cap);
     const uint64_t VV = std::max<uint64_t>(V, w.vocab_cap), DD = std::max<uint64_t>(D, w.feat_cap);
     const int64_t Q = std::max<int64_t>(Qneed, w.pos_cap);
@@ -253,6 +265,30 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D, int n_samples
         cudaGetLastError();
         ws_free(w);
         return fail(FM_ERR_DEVICE_OOM, std::string("workspace allocation: ") + cudaGetErrorString(e));
+    }
+    // further segment sets for the per-step batched K-GEMM2 while HBM allows: each
+    // must leave a quarter of the device free (a set is ~1.1 GB at C2, 17 GB at C5)
+    w.nsets = 1;
+    const size_t set_bytes = static_cast<size_t>(kp) * ldz * 2 + static_cast<size_t>(kp) * 256 * 2 + 8 * nblk;
+    for (int k = 0; k < kGemmMaxBatch - 1; ++k) {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess || fr < set_bytes + tot / 4) break;
+        Workspace::SegSet& x = w.xset[k];
+        cudaError_t ex = dalloc(&x.aseg, static_cast<size_t>(kp) * ldz);
+        ex = ex ? ex : cudaMemset(x.aseg, 0, static_cast<size_t>(kp) * ldz * 2);  // finite padding rows
+        ex = ex ? ex : dalloc(&x.bseg, static_cast<size_t>(kp) * 256);
+        ex = ex ? ex : dalloc(&x.kseg_off, static_cast<size_t>(nblk));
+        ex = ex ? ex : dalloc(&x.kiters, static_cast<size_t>(nblk));
+        if (ex != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(x.aseg);
+            cudaFree(x.bseg);
+            cudaFree(x.kseg_off);
+            cudaFree(x.kiters);
+            x = Workspace::SegSet{};
+            break;
+        }
+        w.nsets = k + 2;
     }
     w.rows_cap = R;
     w.vocab_cap = VV;
@@ -401,6 +437,7 @@ int fm_ctx_timer_start(fm_ctx* c) {
 
 int fm_ctx_timer_stop(fm_ctx* c, double* ms) {
     if (int st = set_dev(c)) return st;
+    if (int st = ctx_flush(c)) return st;  // queued K-GEMM2s belong to the timed work
     cudaEvent_t j;
     FM_CUDA(cudaEventCreateWithFlags(&j, cudaEventDisableTiming));
     for (cudaStream_t cs : {c->copy_in, c->copy_out}) {
@@ -484,6 +521,7 @@ int fm_ctx_num_sms(const fm_ctx* c) { return c->num_sms; }
 
 int fm_ctx_synchronize(fm_ctx* c) {
     if (int st = set_dev(c)) return st;
+    if (int st = ctx_flush(c)) return st;
     FM_CUDA(cudaStreamSynchronize(c->stream));
     FM_CUDA(cudaStreamSynchronize(c->copy_in));
     FM_CUDA(cudaStreamSynchronize(c->copy_out));
@@ -636,8 +674,10 @@ void agent_free_device(fm_agent* a, cudaStream_t s) {
 // check it inserts the lazy dependency on a pending swap-in, so that an
 // activate() prefetch never stalls other agents' work on the shared compute
 // stream — only this agent's first use waits for its copy-in.
-int check_active(fm_agent* a) {
+int check_active(fm_agent* a, bool flush) {
     if (!a->active || !a->ctx) return fail(FM_ERR_INACTIVE_GROUP, a->name);
+    if (flush && a->ctx->pend_agent == a)
+        if (int st = agent_flush(a)) return st;
     if (a->pending_in) {
         FM_CUDA(cudaSetDevice(a->ctx->device));
         FM_CUDA(cudaStreamWaitEvent(a->ctx->stream, a->ev_in, 0));
@@ -695,6 +735,10 @@ int fm_agent_create(fm_ctx* c, const char* name, uint64_t V, uint64_t D, int pre
 int fm_agent_destroy(fm_agent* a) {
     if (!a) return FM_OK;
     if (a->lent) fm_agent_migrate_release(a);
+    if (a->ctx && a->ctx->pend_agent == a) {  // queued reductions die with the agent
+        a->ctx->npend = 0;
+        a->ctx->pend_agent = nullptr;
+    }
     fm_gang_detach(a);
     if (a->ctx) {
         cudaSetDevice(a->ctx->device);
@@ -880,7 +924,7 @@ int64_t fm_agent_samples_accumulated(const fm_agent* a) { return a->samples; }
 int fm_agent_is_active(const fm_agent* a) { return a->active ? 1 : 0; }
 
 int fm_agent_set_clip(fm_agent* a, float clip_eps, const float* old_logp, int64_t n_rows) {
-    if (int st = check_active(a)) return st;
+    if (int st = check_active(a, false)) return st;
     if (n_rows < 0 || (n_rows > 0 && !old_logp)) return fail(FM_ERR_INVALID_ARG, "bad old log-prob array");
     a->clip_eps = clip_eps;
     a->old_logp.clear();
@@ -987,6 +1031,118 @@ extern "C" int fm_agent_set_dp_norms(fm_agent* a, fm_comm* comm) {
 
 // ---------------------------------------------------------------------------
 // the micro-batch pipeline
+}  // extern "C"
+
+namespace fm {
+// ---------------------------------------------------------------------------
+// K-GEMM2 over the agent's queued micro-batches (c->pend, in order): one launch
+// in which every dW tile runs its units back to back (the tile stays in L2
+// between them, so the step's dW is written to HBM once instead of read and
+// written per micro-batch), then each micro-batch's report (its grad norm^2
+// from the epilogue, its loss from K-lse) goes to the host.  exchange /
+// dp_norms (one queued micro-batch): the token-shard gang's fused
+// reduce-scatter / the exact DP norm of the step's micro-batch.
+static int gemm2_flush(fm_agent* a, bool exchange, bool dp_norms, bool step_last) {
+    fm_ctx* c = a->ctx;
+    if (c->pend_agent != a || c->npend == 0) return FM_OK;
+    Workspace& w = c->ws;
+    cudaStream_t s = c->stream;
+    if ((exchange || dp_norms) && c->npend != 1) return fail(FM_ERR_CONFIG_ERROR, "batched reduction with an exchange");
+    GangState* vg = (a->gang && a->gang->connected && a->gang->vocab) ? a->gang : nullptr;
+    const int64_t c0 = vg ? vg->lo[vg->rank] : 0;
+    const int64_t c1 = vg ? vg->lo[vg->rank + 1] : static_cast<int64_t>(a->V);
+    const uint64_t ldz = round_up(a->V, 8);
+    const int nmb = c->npend;
+    GemmArgs g2{};
+    g2.M = static_cast<int>(c1 - c0);
+    g2.N = static_cast<int>(a->D);
+    g2.K = 0;
+    // raster: the 256-feature column tiles of a vocab row block run together, so the
+    // row block's dW stripe and A' columns stay L2-local
+    g2.group_m = env_int("FM_G2_GROUP_M", 1);
+    g2.out = static_cast<float*>(a->dW) + static_cast<size_t>(c0) * a->D;
+    g2.ld_out = static_cast<long long>(a->D);
+    g2.accumulate = a->dw_valid ? 1 : 0;
+    g2.dbg_krows = w.kp_cap;
+    g2.nmb = nmb;
+    for (int u = 0; u < nmb; ++u) {
+        const Workspace::SegSet S = seg_set(w, c->pend[u].set);
+        g2.kseg_off_b[u] = S.kseg_off;
+        g2.kseg_iters_b[u] = S.kiters;
+        g2.sumsq_b[u] = a->d_scalars + 2 * c->pend[u].slot;
+    }
+    g2.kseg_off = g2.kseg_off_b[0];
+    g2.kseg_iters = g2.kseg_iters_b[0];
+    g2.sumsq = g2.sumsq_b[0];
+    double* scal0 = g2.sumsq_b[0];
+    // exact micro-batch grad norm under DP (opt-in, fm_agent_set_dp_norms): GEMM2 writes
+    // this rank's contribution to a scratch, which is added to dW, all-reduced and
+    // measured (training.hpp:417); a gang's exchange then runs as plain copies
+    if (dp_norms) {
+        if (int st = ws_reserve_dpnorm(c, a->P)) return st;
+        g2.out = w.dpn;
+        g2.accumulate = 0;
+        g2.sumsq = nullptr;
+        g2.sumsq_b[0] = nullptr;
+    }
+    if (exchange) {  // last micro-batch of the step: reduce-scatter inside the epilogue
+        GangState* gs = a->gang;
+        g2.xg = gs->g;
+        g2.xrank = gs->rank;
+        for (int o = 0; o <= gs->g; ++o) g2.xlo[o] = static_cast<int>(gs->lo[o]);
+        for (int o = 0; o < gs->g; ++o) g2.xpeer[o] = gs->peer_slot[o];
+    }
+    {
+        KScope k(c, K_GEMM2, s);
+        const uint64_t mc = static_cast<uint64_t>(c1 - c0);
+        if (mc > 0) {
+            GemmMaps maps{};
+            for (int u = 0; u < nmb; ++u) {
+                const Workspace::SegSet S = seg_set(w, c->pend[u].set);
+                if (!make_tmap_bf16_kmajor(&maps.a[u], S.aseg + c0, static_cast<uint64_t>(w.kp_cap), mc, 64, ldz) ||
+                    !make_tmap_bf16_kmajor(&maps.b[u], S.bseg, static_cast<uint64_t>(w.kp_cap), 256, 64))
+                    return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+            }
+            if (!make_tmap_f32_out(&maps.c, g2.out, mc, a->D, a->D))
+                return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+            FM_CUDA(gemm_kseg_launch(maps, g2, c->num_sms, s));
+            count_launch();
+        }
+        // each micro-batch's grad norm^2 over the whole vocabulary (training.hpp:417)
+        if (vg)
+            for (int u = 0; u < nmb; ++u)
+                FM_NCCL(ncclAllReduce(g2.sumsq_b[u], g2.sumsq_b[u], 1, ncclFloat64, ncclSum, gang_comm(vg), s));
+    }
+    if (exchange) {
+        a->dw_valid = true;
+        if (int st = gang_barrier(a)) return st;  // every rank's partials have landed
+    }
+    if (dp_norms) {
+        if (int st = dp_norm_finish(a, scal0, step_last)) return st;
+    }
+    a->dw_valid = true;
+    for (int u = 0; u < nmb; ++u) {
+        const int slot = c->pend[u].slot;
+        FM_CUDA(cudaMemcpyAsync(a->h_scalars + 2 * slot, a->d_scalars + 2 * slot, 2 * sizeof(double),
+                                cudaMemcpyDeviceToHost, s));
+        FM_CUDA(cudaEventRecord(a->ev[slot], s));
+    }
+    c->npend = 0;
+    c->pend_agent = nullptr;
+    return FM_OK;
+}
+
+int agent_flush(fm_agent* a) {
+    if (!a->ctx || a->ctx->pend_agent != a) return FM_OK;
+    if (int st = set_dev(a->ctx)) return st;
+    return gemm2_flush(a, false, false, false);
+}
+
+int ctx_flush(fm_ctx* c) { return c->pend_agent ? agent_flush(c->pend_agent) : FM_OK; }
+}  // namespace fm
+
+extern "C" {
+
 // ---------------------------------------------------------------------------
 // hsd: host descriptors (staged H2D), or dsd: descriptors already in HBM (the
 // on-device experience table's poll), ready when `dsd_ready` completes.
@@ -1005,6 +1161,9 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
         return fail(FM_ERR_INVALID_ARG, "old log-probs given for " + std::to_string(a->old_logp.size()) +
                                             " rows, the micro-batch has " + std::to_string(M_total));
     const int64_t Mpad = tc ? static_cast<int64_t>(round_up(static_cast<uint64_t>(M), 128)) : M;
+    // the workspace's segment sets serve one agent's deferred K-GEMM2 at a time
+    if (c->pend_agent && c->pend_agent != a)
+        if (int st = agent_flush(c->pend_agent)) return st;
     if (tc) {
         if (int st = ws_reserve_tc(c, std::max<int64_t>(Mpad, 128), a->V, a->D, n)) return st;
     } else {
@@ -1046,6 +1205,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
     double* scal = a->d_scalars + 2 * slot;
     FM_CUDA(cudaMemsetAsync(scal, 0, 2 * sizeof(double), s));
     RowBuffers rows = row_buffers(w);
+    bool queued = false;  // the report is produced by the (possibly deferred) K-GEMM2
 
     if (M > 0) {
         if (tc) {
@@ -1067,6 +1227,16 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 a->fmax_valid = true;
                 count_launch();
             }
+            // this micro-batch's segment set: the next free one while the step's reductions
+            // are batched (a DP exchange / exact DP norms need each micro-batch's dW at once)
+            const bool dp_norms = a->norm_comm != nullptr;
+            if (dp_norms && vg) return fail(FM_ERR_CONFIG_ERROR, "a vocabulary gang reports exact norms already");
+            const bool step_last = a->samples + n == G;
+            const bool batch = !dp_norms && !(a->gang && !vg) && w.nsets > 1;
+            if (!batch && c->npend)
+                if (int st = agent_flush(a)) return st;
+            const int kset = c->npend;
+            const Workspace::SegSet S = seg_set(w, kset);
             rows.fmax = a->fmax;
             rows.zact = w.zact;
             rows.lossw = w.lossw;
@@ -1080,7 +1250,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 KScope k(c, K_GATHER, s);
                 FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, Mpad, G, a->D, rows, s));
                 FM_CUDA(launch_positions(c->arena, w.sd, n, row_lo, M, a->D, w.pos_feat, Qcap, s));
-                FM_CUDA(launch_pslots(w.pos_feat, Qcap, nblk, w.kcount, w.kseg_off, w.kiters, w.pos_slot, w.bseg,
+                FM_CUDA(launch_pslots(w.pos_feat, Qcap, nblk, w.kcount, S.kseg_off, S.kiters, w.pos_slot, S.bseg,
                                       w.kp_cap, w.kseg_rows, s));
                 count_launch(4);
             }
@@ -1102,7 +1272,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             ba.lse = w.lse;
             ba.coef_eff = w.coef_eff;
             ba.pos_slot = w.pos_slot;
-            ba.aseg = w.aseg + c0;
+            ba.aseg = S.aseg + c0;
             ba.ld_a = static_cast<int64_t>(ldz);
             ba.dbg_kp = w.kp_cap;
             ba.dbg_D = static_cast<int64_t>(a->D);
@@ -1143,63 +1313,17 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 KScope k(c, K_BAND, s);
                 FM_CUDA(launch_band(ba, true, s));
             }
-            // K-GEMM2: dW[v][f] (+)= sum over block(f)'s positions of H[q][v] * onehot[q][f];
-            // the first contribution of the step overwrites
-            GemmArgs g2{};
-            g2.M = static_cast<int>(c1 - c0);
-            g2.N = static_cast<int>(a->D);
-            g2.K = 0;
-            // raster: the 256-feature column tiles of a vocab row block run together, so the
-            // row block's dW stripe and A' columns stay L2-local
-            g2.group_m = env_int("FM_G2_GROUP_M", 1);
-            g2.out = static_cast<float*>(a->dW) + static_cast<size_t>(c0) * a->D;
-            g2.ld_out = static_cast<long long>(a->D);
-            g2.accumulate = a->dw_valid ? 1 : 0;
-            g2.sumsq = scal;
-            g2.kseg_off = w.kseg_off;
-            g2.kseg_iters = w.kiters;
-            g2.dbg_krows = w.kp_cap;
-            // exact micro-batch grad norm under DP (opt-in, fm_agent_set_dp_norms): GEMM2 writes
-            // this rank's contribution to a scratch, which is added to dW, all-reduced and
-            // measured (training.hpp:417); a gang's exchange then runs as plain copies
-            const bool dp_norms = a->norm_comm != nullptr;
-            const bool exchange = !dp_norms && !vg && a->gang && a->gang->connected && a->samples + n == G;
-            if (dp_norms && vg) return fail(FM_ERR_CONFIG_ERROR, "a vocabulary gang reports exact norms already");
-            if (dp_norms) {
-                if (int st = ws_reserve_dpnorm(c, a->P)) return st;
-                g2.out = w.dpn;
-                g2.accumulate = 0;
-                g2.sumsq = nullptr;
+            // K-GEMM2 (dW[v][f] (+)= sum over block(f)'s positions of H[q][v] * onehot[q][f]):
+            // queued; it runs when the batch is full, at the step's last micro-batch, or when
+            // anything needs this agent's dW or reports (check_active, sync, poll)
+            c->pend[c->npend++] = fm_ctx::PendingMB{kset, slot};
+            c->pend_agent = a;
+            queued = true;
+            count_launch(3);
+            if (!batch || c->npend == w.nsets || step_last) {
+                const bool exchange = !dp_norms && !vg && a->gang && a->gang->connected && step_last;
+                if (int st = gemm2_flush(a, exchange, dp_norms, step_last)) return st;
             }
-            if (exchange) {  // last micro-batch of the step: reduce-scatter inside the epilogue
-                GangState* gs = a->gang;
-                g2.xg = gs->g;
-                g2.xrank = gs->rank;
-                for (int o = 0; o <= gs->g; ++o) g2.xlo[o] = static_cast<int>(gs->lo[o]);
-                for (int o = 0; o < gs->g; ++o) g2.xpeer[o] = gs->peer_slot[o];
-            }
-            {
-                KScope k(c, K_GEMM2, s);
-                CUtensorMap tSA, tSB, tC;
-                const uint64_t mc = static_cast<uint64_t>(c1 - c0);
-                if (cols) {
-                    if (!make_tmap_bf16_kmajor(&tSA, w.aseg + c0, static_cast<uint64_t>(w.kp_cap), mc, 64, ldz) ||
-                        !make_tmap_bf16_kmajor(&tSB, w.bseg, static_cast<uint64_t>(w.kp_cap), 256, 64) ||
-                        !make_tmap_f32_out(&tC, g2.out, mc, a->D, a->D))
-                        return fail(FM_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-                    FM_CUDA(gemm_kseg_launch(tSA, tSB, tC, g2, c->num_sms, s));
-                }
-                // the micro-batch's grad norm^2 over the whole vocabulary (training.hpp:417)
-                if (vg) FM_NCCL(ncclAllReduce(scal, scal, 1, ncclFloat64, ncclSum, gang_comm(vg), s));
-            }
-            if (exchange) {
-                a->dw_valid = true;
-                if (int st = gang_barrier(a)) return st;  // every rank's partials have landed
-            }
-            if (dp_norms) {
-                if (int st = dp_norm_finish(a, scal, a->samples + n == G)) return st;
-            }
-            count_launch(4);
         } else {
             FM_CUDA(launch_gather(c->arena, w.sd, n, row_lo, M, M, G, a->D, rows, s));
             if (!a->dw_valid) FM_CUDA(cudaMemsetAsync(a->dW, 0, a->P * 8, s));
@@ -1208,8 +1332,8 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                                        scal + 1, s));
             FM_CUDA(launch_parity_fold(static_cast<double*>(a->dW), w.dWmb, a->P, scal, c->num_sms, s));
             count_launch(3);
+            a->dw_valid = true;
         }
-        a->dw_valid = true;
     } else if (tc && a->norm_comm) {
         // no rows here: a zero contribution still joins the collective
         if (int st = ws_reserve_dpnorm(c, a->P)) return st;
@@ -1223,8 +1347,10 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
     a->old_logp.clear();  // old log-probs apply to one micro-batch
     a->last_rows = M;
     a->last_seq = ++c->op_seq;  // its own K-stats mark precedes this micro-batch's GEMM2
-    FM_CUDA(cudaMemcpyAsync(a->h_scalars + 2 * slot, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    FM_CUDA(cudaEventRecord(a->ev[slot], s));
+    if (!queued) {
+        FM_CUDA(cudaMemcpyAsync(a->h_scalars + 2 * slot, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        FM_CUDA(cudaEventRecord(a->ev[slot], s));
+    }
     a->rep_tokens[slot] = M;
     a->rep_bs[slot] = n;
     a->samples += n;
@@ -1234,7 +1360,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
 
 int fm_train_micro_batch(fm_agent* a, const fm_sample* samples, int n, int64_t G, int64_t* ticket_out) {
     FM_GUARD_BEGIN
-    if (int st = check_active(a)) return st;
+    if (int st = check_active(a, false)) return st;
     if (n < 0 || (n > 0 && !samples)) return fail(FM_ERR_INVALID_ARG, "bad sample list");
     if (G <= 0) return fail(FM_ERR_CONFIG_ERROR, "global batch must be positive");
     if (int st = set_dev(a->ctx)) return st;
@@ -1261,7 +1387,7 @@ int fm_train_micro_batch(fm_agent* a, const fm_sample* samples, int n, int64_t G
 // reusable arena region inside the call (H2D on the compute stream).
 int fm_train_micro_batch_host(fm_agent* a, const fm_host_sample* samples, int n, int64_t G, int64_t* ticket_out) {
     FM_GUARD_BEGIN
-    if (int st = check_active(a)) return st;
+    if (int st = check_active(a, false)) return st;
     if (n < 0 || (n > 0 && !samples)) return fail(FM_ERR_INVALID_ARG, "bad sample list");
     if (G <= 0) return fail(FM_ERR_CONFIG_ERROR, "global batch must be positive");
     fm_ctx* c = a->ctx;
@@ -1310,7 +1436,7 @@ int fm_train_micro_batch_host(fm_agent* a, const fm_host_sample* samples, int n,
 
 int fm_agent_read_logp(fm_agent* a, double* out, int64_t n_rows) {
     FM_GUARD_BEGIN
-    if (int st = check_active(a)) return st;
+    if (int st = check_active(a, false)) return st;
     fm_ctx* c = a->ctx;
     if (int st = set_dev(c)) return st;
     FM_CUDA(cudaStreamSynchronize(c->stream));
@@ -1353,6 +1479,7 @@ int fm_debug_read_positions(fm_ctx* c, int64_t n_rows, int32_t* q0, int64_t n_po
 int fm_agent_sync(fm_agent* a) {
     if (!a->ctx) return FM_OK;
     if (int st = set_dev(a->ctx)) return st;
+    if (int st = agent_flush(a)) return st;
     FM_CUDA(cudaStreamSynchronize(a->ctx->stream));
     return FM_OK;
 }
@@ -1361,6 +1488,13 @@ int fm_agent_poll_report(fm_agent* a, int64_t ticket, fm_report* out) {
     if (ticket < 0 || ticket >= a->next_ticket || ticket < a->next_ticket - kReportRing)
         return fail(FM_ERR_INVALID_ARG, "unknown or expired ticket");
     const int slot = static_cast<int>(ticket % kReportRing);
+    if (a->ctx && a->ctx->pend_agent == a) {  // its K-GEMM2 is still queued: run it now
+        for (int u = 0; u < a->ctx->npend; ++u)
+            if (a->ctx->pend[u].slot == slot) {
+                if (int st = agent_flush(a)) return st;
+                break;
+            }
+    }
     const cudaError_t q = cudaEventQuery(a->ev[slot]);
     if (q == cudaErrorNotReady) return 0;
     if (q != cudaSuccess) return fail(FM_ERR_CUDA, cudaGetErrorString(q));
@@ -1514,7 +1648,7 @@ cudaStream_t ctx_stream(const fm_ctx* c) { return c->stream; }
 uint8_t* ctx_arena(const fm_ctx* c) { return c->arena; }
 int ctx_staging(fm_ctx* c, size_t bytes, uint8_t** out, cudaEvent_t* ev) { return staging_acquire(c, bytes, out, ev); }
 fm_ctx* agent_ctx(const fm_agent* a) { return a->ctx; }
-int agent_check_active(fm_agent* a) { return check_active(a); }
+int agent_check_active(fm_agent* a) { return check_active(a, false); }  // (train entry: no flush)
 
 int ctx_arena_alloc(fm_ctx* c, uint64_t bytes, uint64_t* off_out) {
     if (int st = set_dev(c)) return st;
@@ -1531,7 +1665,7 @@ int ctx_arena_alloc(fm_ctx* c, uint64_t bytes, uint64_t* off_out) {
 int train_device_desc(fm_agent* a, const SampleDesc* dsd, int n, int64_t M_total, int64_t G, cudaEvent_t ready,
                       int64_t* ticket_out) {
     FM_GUARD_BEGIN
-    if (int st = check_active(a)) return st;
+    if (int st = check_active(a, false)) return st;
     if (G <= 0) return fail(FM_ERR_CONFIG_ERROR, "global batch must be positive");
     if (int st = set_dev(a->ctx)) return st;
     return train_impl(a, nullptr, n, M_total, G, ticket_out, dsd, ready);

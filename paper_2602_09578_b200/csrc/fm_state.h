@@ -95,6 +95,14 @@ struct Workspace {
     double *zscratch = nullptr, *dWmb = nullptr, *logp64 = nullptr;
     SampleDesc* sd = nullptr;
     int sd_cap = 0;
+    // K-GEMM2 segment sets 1 .. nsets-1 (set 0 = aseg / bseg / kseg_off / kiters above):
+    // the micro-batches of a step whose reduction is batched into one K-GEMM2
+    struct SegSet {
+        __nv_bfloat16 *aseg = nullptr, *bseg = nullptr;
+        int32_t *kseg_off = nullptr, *kiters = nullptr;
+    };
+    SegSet xset[kGemmMaxBatch - 1];
+    int nsets = 1;
     float* dpn = nullptr;  // exact DP grad norm: this micro-batch's contribution [P]
     uint64_t dpn_cap = 0;
     float* lse_red = nullptr;  // vocabulary gang: per-row (sum, taken logit) partials [2][cap]
@@ -146,6 +154,14 @@ struct fm_ctx {
     // the latest K-stats launch on the compute stream (swap copies start there, see
     // fm_agent_suspend) and the op sequence numbers that say what it follows
     cudaEvent_t ev_gemm = nullptr;
+    // micro-batches of pend_agent whose K-GEMM2 is batched (deferred): their segment
+    // set in the workspace and report slot; agent_flush runs them as one launch
+    struct PendingMB {
+        int set, slot;
+    };
+    fm_agent* pend_agent = nullptr;
+    PendingMB pend[kGemmMaxBatch];
+    int npend = 0;
     std::map<std::string, void*> ipc_cache;  // peer buffers mapped over NVLink (slots, gang receive buffers)
     std::vector<std::pair<size_t, void*>> recv_pool;  // gang receive buffers + barrier tokens, recycled
     std::unordered_map<void*, size_t> pool_sizes;
@@ -326,7 +342,11 @@ int agent_alloc_device(fm_agent* a, fm_ctx* c, cudaStream_t s);
 void agent_free_device(fm_agent* a, cudaStream_t s);
 void agent_bind_slot(fm_agent* a, Slot* sl);
 void agent_unbind(fm_agent* a);
-int check_active(fm_agent* a);
+// flush = true: first run the agent's deferred K-GEMM2 (its dW and reports are complete)
+int check_active(fm_agent* a, bool flush = true);
+// the deferred K-GEMM2 of the agent / of whichever agent has one pending on the context
+int agent_flush(fm_agent* a);
+int ctx_flush(fm_ctx* c);
 }  // namespace fm
 
 // ---- parking buffers (fm_swap.cu), also written by the fused update-and-park ----

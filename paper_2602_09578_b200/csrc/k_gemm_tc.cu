@@ -62,6 +62,7 @@ struct GradEpi {
     uint8_t* stage = nullptr;  // per-warp 2 x 4 KB SWIZZLE_128B staging of the TMA epilogue
     const CUtensorMap* tmc = nullptr;
     int nstaged = 0;
+    int accumulate = 0;  // this unit adds into dW (else stores)
 
     // Local rows: the warp's 32 rows x 32 columns go through shared memory (SWIZZLE_128B,
     // the TMA map's layout) and one TMA op adds them into dW in L2 (store for the
@@ -85,7 +86,7 @@ struct GradEpi {
         __syncwarp();
         if (lane == 0) {
             const int row0 = row - static_cast<int>(lane);
-            if (a.accumulate) tma_reduce_add_2d(tmc, buf, col0, row0);
+            if (accumulate) tma_reduce_add_2d(tmc, buf, col0, row0);
             else tma_store_2d(tmc, buf, col0, row0);
             tma_store_commit();
         }
@@ -107,7 +108,7 @@ struct GradEpi {
                                      __uint_as_float(r[j + 3]));
             if (vrow && j < nvalid) {
                 part += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
-                if (a.accumulate) {
+                if (accumulate) {
                     const float4 o4 = *reinterpret_cast<const float4*>(src + j);
                     acc.x += o4.x;
                     acc.y += o4.y;
@@ -173,7 +174,7 @@ struct GradEpi {
             const int row0 = row - static_cast<int>(lane);
             const int seg = static_cast<int>(lane & 7);
             float4 o[8];
-            if (a.accumulate) {  // all eight loads in flight before any store
+            if (accumulate) {  // all eight loads in flight before any store
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const int rg = row0 + i * 4 + static_cast<int>(lane >> 3);
@@ -186,7 +187,7 @@ struct GradEpi {
                 const int rr = i * 4 + static_cast<int>(lane >> 3);
                 const int rg = row0 + rr;
                 float4 q = *reinterpret_cast<const float4*>(xbuf + rr * 36 + seg * 4);
-                if (a.accumulate) {
+                if (accumulate) {
                     q.x += o[i].x;
                     q.y += o[i].y;
                     q.z += o[i].z;
@@ -207,7 +208,7 @@ struct GradEpi {
                 float4 acc = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
                                          __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
                 part += acc.x * acc.x + acc.y * acc.y + acc.z * acc.z + acc.w * acc.w;
-                if (a.accumulate) {
+                if (accumulate) {
                     const float4 o4 = *reinterpret_cast<const float4*>(src + j);
                     acc.x += o4.x;
                     acc.y += o4.y;
@@ -222,7 +223,7 @@ struct GradEpi {
                 if (j < nvalid) {
                     const float acc = __uint_as_float(r[j]);
                     part += acc * acc;
-                    dst[j] = a.accumulate ? src[j] + acc : acc;
+                    dst[j] = accumulate ? src[j] + acc : acc;
                 }
             }
         }
@@ -244,8 +245,7 @@ constexpr int kThreadsPair = 192;  // w0 TMA, w1 MMA, w2-5 epilogue
 // (args.kseg_off / kseg_iters); B' holds only 256 columns.
 template <bool kAmn, bool kBmn, bool kSeg>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
-    gemm_grad_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmC, GemmArgs args) {
+    gemm_grad_kernel(const __grid_constant__ GemmMaps maps, GemmArgs args) {
     static_assert(!kSeg || (kAmn && kBmn), "segment operands are MN-major");
     constexpr uint32_t kId = idesc_bf16_f32<256, BN, kAmn, kBmn>();
     extern __shared__ uint8_t smem_raw[];
@@ -266,11 +266,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     const uint32_t lane = lane_id();
     const uint32_t rank = cluster_ctarank();
     const bool leader = rank == 0;
+    // units per output tile: the batched micro-batches (segmented path) or 1
+    const int nmb = kSeg ? args.nmb : 1;
 
     if (warp == 0 && lane == 0) {
-        tma_prefetch(&tmA);
-        tma_prefetch(&tmB);
-        tma_prefetch(&tmC);
+        for (int u = 0; u < nmb; ++u) {
+            tma_prefetch(&maps.a[u]);
+            tma_prefetch(&maps.b[u]);
+        }
+        tma_prefetch(&maps.c);
         for (int s = 0; s < P_STAGES; ++s) {
             mbar_init(&full[s], 1);   // the leader's producer arrives with both CTAs' tx bytes
             mbar_init(&empty[s], 1);  // one multicast commit per consumed stage
@@ -293,6 +297,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     const int k_iters = (args.K + BK - 1) / BK;
     const int cid = blockIdx.x >> 1;
     const int nclusters = gridDim.x >> 1;
+    // K iterations of unit u of column tile nb
+    auto unit_iters = [&](int u, int nb) -> int {
+        if constexpr (kSeg) return __ldg(args.kseg_iters_b[u] + nb);
+        else return k_iters;
+    };
 
     if (warp == 0) {
         // ===== TMA producer (both CTAs) =====
@@ -306,32 +315,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                 const TileCoord tc = tile_coord(t, tiles_m, tiles_n, args.group_m);
                 const int arow = tc.mb * 256 + static_cast<int>(rank) * 128;
                 const int brow = (kSeg ? 0 : tc.nb * BN) + static_cast<int>(rank) * 128;
-                int kbase = 0, ke = k_iters;
-                if constexpr (kSeg) {
-                    kbase = __ldg(args.kseg_off + tc.nb);
-                    ke = __ldg(args.kseg_iters + tc.nb);
-                    FM_DCHECK(args.dbg_krows == 0 || kbase + static_cast<long long>(ke) * BK <= args.dbg_krows);
-                }
-                for (int k = 0; k < ke; ++k) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    const uint32_t fb = mapa_shared(&full[stage], 0);
-                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
-                    const int kc = kbase + k * BK;
-                    if constexpr (kAmn) {
-                        tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, arow, kc, pol_a);
-                        tma_load_2d_2sm(sA + stage * P_A_STAGE + 8192, &tmA, fb, arow + 64, kc, pol_a);
-                    } else {
-                        tma_load_2d_2sm(sA + stage * P_A_STAGE, &tmA, fb, kc, arow, pol);
+                for (int u = 0; u < nmb; ++u) {
+                    const CUtensorMap* tmA = &maps.a[u];
+                    const CUtensorMap* tmB = &maps.b[u];
+                    int kbase = 0;
+                    const int ke = unit_iters(u, tc.nb);
+                    if constexpr (kSeg) {
+                        kbase = __ldg(args.kseg_off_b[u] + tc.nb);
+                        FM_DCHECK(args.dbg_krows == 0 || kbase + static_cast<long long>(ke) * BK <= args.dbg_krows);
                     }
-                    if constexpr (kBmn) {
-                        tma_load_2d_2sm(sB + stage * P_B_STAGE, &tmB, fb, brow, kc, pol);
-                        tma_load_2d_2sm(sB + stage * P_B_STAGE + 8192, &tmB, fb, brow + 64, kc, pol);
-                    } else {
-                        tma_load_2d_2sm(sB + stage * P_B_STAGE, &tmB, fb, kc, brow, pol);
-                    }
-                    if (++stage == P_STAGES) {
-                        stage = 0;
-                        phase ^= 1;
+                    for (int k = 0; k < ke; ++k) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        const uint32_t fb = mapa_shared(&full[stage], 0);
+                        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * P_STAGE_BYTES);
+                        const int kc = kbase + k * BK;
+                        if constexpr (kAmn) {
+                            tma_load_2d_2sm(sA + stage * P_A_STAGE, tmA, fb, arow, kc, pol_a);
+                            tma_load_2d_2sm(sA + stage * P_A_STAGE + 8192, tmA, fb, arow + 64, kc, pol_a);
+                        } else {
+                            tma_load_2d_2sm(sA + stage * P_A_STAGE, tmA, fb, kc, arow, pol);
+                        }
+                        if constexpr (kBmn) {
+                            tma_load_2d_2sm(sB + stage * P_B_STAGE, tmB, fb, brow, kc, pol);
+                            tma_load_2d_2sm(sB + stage * P_B_STAGE + 8192, tmB, fb, brow + 64, kc, pol);
+                        } else {
+                            tma_load_2d_2sm(sB + stage * P_B_STAGE, tmB, fb, kc, brow, pol);
+                        }
+                        if (++stage == P_STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
                     }
                 }
             }
@@ -344,33 +357,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int t = cid; t < num_tiles; t += nclusters) {
-                int ke = k_iters;
-                if constexpr (kSeg) ke = __ldg(args.kseg_iters + tile_coord(t, tiles_m, tiles_n, args.group_m).nb);
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
-                tc_fence_after();
-                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-                for (int k = 0; k < ke; ++k) {
-                    mbar_wait(&full[stage], phase);
+                const int nb = tile_coord(t, tiles_m, tiles_n, args.group_m).nb;
+                for (int u = 0; u < nmb; ++u) {
+                    const int ke = unit_iters(u, nb);
+                    mbar_wait(&tempty[acc], acc_phase ^ 1);
                     tc_fence_after();
-                    // K-major: 16 bf16 = 32 B along the swizzle row; MN-major: 16 K rows = 2 KB
-                    const uint64_t adesc = kAmn ? umma_desc_mn_sw128(smem_u32(sA + stage * P_A_STAGE), 8192)
-                                                : umma_desc_k_sw128(smem_u32(sA + stage * P_A_STAGE));
-                    const uint64_t bdesc = kBmn ? umma_desc_mn_sw128(smem_u32(sB + stage * P_B_STAGE), 8192)
-                                                : umma_desc_k_sw128(smem_u32(sB + stage * P_B_STAGE));
-                    constexpr uint64_t a_step = kAmn ? 2048 >> 4 : 2;
-                    constexpr uint64_t b_step = kBmn ? 2048 >> 4 : 2;
+                    const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+                    for (int k = 0; k < ke; ++k) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        // K-major: 16 bf16 = 32 B along the swizzle row; MN-major: 16 K rows = 2 KB
+                        const uint64_t adesc = kAmn ? umma_desc_mn_sw128(smem_u32(sA + stage * P_A_STAGE), 8192)
+                                                    : umma_desc_k_sw128(smem_u32(sA + stage * P_A_STAGE));
+                        const uint64_t bdesc = kBmn ? umma_desc_mn_sw128(smem_u32(sB + stage * P_B_STAGE), 8192)
+                                                    : umma_desc_k_sw128(smem_u32(sB + stage * P_B_STAGE));
+                        constexpr uint64_t a_step = kAmn ? 2048 >> 4 : 2;
+                        constexpr uint64_t b_step = kBmn ? 2048 >> 4 : 2;
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk)
-                        umma_bf16_2sm(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, kId, (k != 0 || kk != 0));
-                    umma_commit_2sm(&empty[stage], 0x3);
-                    if (++stage == P_STAGES) {
-                        stage = 0;
-                        phase ^= 1;
+                        for (int kk = 0; kk < BK / 16; ++kk)
+                            umma_bf16_2sm(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, kId,
+                                          (k != 0 || kk != 0));
+                        umma_commit_2sm(&empty[stage], 0x3);
+                        if (++stage == P_STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
                     }
+                    umma_commit_2sm(&tfull[acc], 0x3);
+                    acc ^= 1;
+                    if (acc == 0) acc_phase ^= 1;
                 }
-                umma_commit_2sm(&tfull[acc], 0x3);
-                acc ^= 1;
-                if (acc == 0) acc_phase ^= 1;
             }
         }
         __syncwarp();
@@ -382,37 +398,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
         GradEpi epi;
         epi.xbuf = xscratch + quad * 32 * 36;
         epi.stage = tstage + quad * 8192;
-        epi.tmc = &tmC;
+        epi.tmc = &maps.c;
         int acc = 0;
         uint32_t acc_phase = 0;
-        double sumsq_total = 0.0;
+        double sq[kGemmMaxBatch] = {};  // per unit (micro-batch), fp64 across tiles
         for (int t = cid; t < num_tiles; t += nclusters) {
             const TileCoord tc = tile_coord(t, tiles_m, tiles_n, args.group_m);
             const int row = tc.mb * 256 + row_in_tile;
-            mbar_wait(&tfull[acc], acc_phase);
-            tc_fence_after();
-            epi.sumsq = 0.f;
+            for (int u = 0; u < nmb; ++u) {
+                mbar_wait(&tfull[acc], acc_phase);
+                tc_fence_after();
+                epi.sumsq = 0.f;
+                epi.accumulate = (u > 0 || args.accumulate) ? 1 : 0;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                tmem_ld_32x32b_x32(tmem_base + ((quad * 32u) << 16) + static_cast<uint32_t>(acc * BN + c * 32), r);
-                tmem_ld_wait();
-                if (c == BN / 32 - 1) {
-                    // the accumulator is fully in registers: hand TMEM back to the MMA
-                    // warp before the last chunk's stores (relaxed: no wait for this
-                    // warp's outstanding global stores)
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader[acc]);
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld_32x32b_x32(tmem_base + ((quad * 32u) << 16) + static_cast<uint32_t>(acc * BN + c * 32), r);
+                    tmem_ld_wait();
+                    if (c == BN / 32 - 1) {
+                        // the accumulator is fully in registers: hand TMEM back to the MMA
+                        // warp before the last chunk's stores (relaxed: no wait for this
+                        // warp's outstanding global stores)
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader[acc]);
+                    }
+                    epi.chunk(args, row, tc.nb * BN + c * 32, r);
                 }
-                epi.chunk(args, row, tc.nb * BN + c * 32, r);
+#pragma unroll
+                for (int j = 0; j < kGemmMaxBatch; ++j)
+                    if (j == u) sq[j] += static_cast<double>(epi.sumsq);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
             }
-            sumsq_total += static_cast<double>(epi.sumsq);
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
         }
-        for (int o = 16; o > 0; o >>= 1) sumsq_total += __shfl_xor_sync(0xffffffffu, sumsq_total, o);
-        if (lane == 0 && args.sumsq) atomicAdd(args.sumsq, sumsq_total);
+#pragma unroll
+        for (int j = 0; j < kGemmMaxBatch; ++j) {
+            double v = sq[j];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            double* dst = kSeg ? args.sumsq_b[j] : (j == 0 ? args.sumsq : nullptr);
+            if (lane == 0 && j < nmb && dst) atomicAdd(dst, v);
+        }
         if (lane == 0) tma_store_wait<0>();  // every reduce / store of this warp has completed
     }
     tc_fence_before();
@@ -424,8 +450,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
 }
 
 template <bool kAmn, bool kBmn, bool kSeg>
-cudaError_t launch_grad(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC, const GemmArgs& args,
-                        int num_sms, cudaStream_t stream) {
+cudaError_t launch_grad(const GemmMaps& maps, const GemmArgs& args, int num_sms, cudaStream_t stream) {
     const size_t smem = gemm_smem_bytes();
     const int tiles = ((args.M + 255) / 256) * ((args.N + BN - 1) / BN);
     if (tiles == 0) return cudaSuccess;
@@ -434,7 +459,7 @@ cudaError_t launch_grad(const CUtensorMap& tmA, const CUtensorMap& tmB, const CU
     auto k = gemm_grad_kernel<kAmn, kBmn, kSeg>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    k<<<grid, kThreadsPair, smem, stream>>>(tmA, tmB, tmC, args);
+    k<<<grid, kThreadsPair, smem, stream>>>(maps, args);
     return cudaGetLastError();
 }
 
@@ -452,15 +477,26 @@ cudaError_t gemm_debug_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, co
     args.group_m = 8;
     args.out = C;
     args.ld_out = N;
-    if (a_mn && b_mn) return launch_grad<true, true, false>(tmA, tmB, tmC, args, num_sms, stream);
-    if (a_mn) return launch_grad<true, false, false>(tmA, tmB, tmC, args, num_sms, stream);
-    if (b_mn) return launch_grad<false, true, false>(tmA, tmB, tmC, args, num_sms, stream);
-    return launch_grad<false, false, false>(tmA, tmB, tmC, args, num_sms, stream);
+    GemmMaps maps{};
+    maps.a[0] = tmA;
+    maps.b[0] = tmB;
+    maps.c = tmC;
+    if (a_mn && b_mn) return launch_grad<true, true, false>(maps, args, num_sms, stream);
+    if (a_mn) return launch_grad<true, false, false>(maps, args, num_sms, stream);
+    if (b_mn) return launch_grad<false, true, false>(maps, args, num_sms, stream);
+    return launch_grad<false, false, false>(maps, args, num_sms, stream);
 }
 
-cudaError_t gemm_kseg_launch(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
-                             const GemmArgs& args, int num_sms, cudaStream_t stream) {
-    return launch_grad<true, true, true>(tmA, tmB, tmC, args, num_sms, stream);
+cudaError_t gemm_kseg_launch(const GemmMaps& maps, const GemmArgs& args_in, int num_sms, cudaStream_t stream) {
+    GemmArgs args = args_in;
+    if (args.nmb < 1 || args.nmb > kGemmMaxBatch) return cudaErrorInvalidValue;
+    if (args.nmb > 1 && args.xg > 1) return cudaErrorInvalidValue;  // the exchange is per micro-batch
+    if (args.nmb == 1) {  // the single-micro-batch fields
+        args.kseg_off_b[0] = args.kseg_off;
+        args.kseg_iters_b[0] = args.kseg_iters;
+        args.sumsq_b[0] = args.sumsq;
+    }
+    return launch_grad<true, true, true>(maps, args, num_sms, stream);
 }
 
 size_t gemm_smem_bytes() {
