@@ -191,7 +191,11 @@ typedef struct fm_sample_key {
 int fm_agent_add_grad_keys(fm_agent* a, const fm_sample_key* keys, int n);
 
 /* TrainingEngine::train_micro_batch (training.hpp:355-430): gather -> positions ->
- * K-stats -> K-lse -> K-band -> weight-gradient GEMM, enqueued on the agent's stream.
+ * K-stats -> K-lse -> K-band enqueued on the agent's stream; the weight-gradient
+ * GEMM is queued and runs once for the step's queued micro-batches (at the step's
+ * last micro-batch, when 4 are queued, or when anything needs the agent's dW or a
+ * queued report: fm_agent_sync, fm_agent_poll_report of that ticket, any other
+ * call on the agent, another agent's micro-batch on the context).
  * Returns immediately; *ticket_out identifies the report (fm_agent_poll_report).
  * global_batch is G of the -1/G normalisation (training.hpp:446). */
 int fm_train_micro_batch(fm_agent* a, const fm_sample* samples, int n, int64_t global_batch,
@@ -217,9 +221,11 @@ int fm_debug_read_rows(fm_ctx* ctx, int64_t n_rows, int32_t* action, int32_t* ct
  * formulation): each row's first position, each position's
  * feature (tok mod D, -1 before a sequence start) and K-GEMM2 segment slot. */
 int fm_debug_read_positions(fm_ctx* ctx, int64_t n_rows, int32_t* q0, int64_t n_pos, int32_t* feat, int32_t* slot);
-/* Blocks until the agent's stream drains; completed reports become pollable. */
+/* Runs the agent's queued gradient GEMM, then blocks until its stream drains;
+ * every report becomes pollable. */
 int fm_agent_sync(fm_agent* a);
-/* Non-blocking: 1 and fills *out if the ticket's micro-batch has finished. */
+/* Non-blocking: 1 and fills *out if the ticket's micro-batch has finished (a
+ * queued gradient GEMM of that micro-batch is launched first). */
 int fm_agent_poll_report(fm_agent* a, int64_t ticket, fm_report* out);
 
 /* apply_global_update (training.hpp:435-456): IncompleteBatch unless
