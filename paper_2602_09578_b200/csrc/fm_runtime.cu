@@ -256,7 +256,8 @@ int ws_reserve_tc(fm_ctx* c, int64_t Mpad, uint64_t V, uint64_t D, int n_samples
     e = e ? e : dalloc(&w.bseg, static_cast<size_t>(kp) * 256);
     e = e ? e : dalloc(&w.zero_row, 4096);
     e = e ? e : cudaMemset(w.zero_row, 0, 4096 * 2);
-    e = e ? e : dalloc(&w.kcount, static_cast<size_t>(nblk) * static_cast<size_t>((Q + 1023) / 1024 + 1));
+    // chunk counts and their per-(block, chunk) bases (K-pslot)
+    e = e ? e : dalloc(&w.kcount, 2 * static_cast<size_t>(nblk) * static_cast<size_t>((Q + 1023) / 1024 + 1));
     e = e ? e : dalloc(&w.kseg_off, static_cast<size_t>(nblk));
     e = e ? e : dalloc(&w.kiters, static_cast<size_t>(nblk));
     e = e ? e : dalloc(&w.kseg_rows, 1);
