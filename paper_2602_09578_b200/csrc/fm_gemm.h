@@ -44,6 +44,7 @@ struct GemmArgs {
     // accumulate) — the tile's dW stays in L2 between its units.  nmb = 1: the fields
     // above.
     int nmb = 1;
+    int snap = 0;  // batched units share one accumulator (short segments; see gemm_grad_kernel's kSnap)
     const int32_t* kseg_off_b[kGemmMaxBatch] = {};
     const int32_t* kseg_iters_b[kGemmMaxBatch] = {};
     double* sumsq_b[kGemmMaxBatch] = {};

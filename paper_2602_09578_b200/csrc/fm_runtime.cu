@@ -1066,6 +1066,11 @@ static int gemm2_flush(fm_agent* a, bool exchange, bool dp_norms, bool step_last
     g2.accumulate = a->dw_valid ? 1 : 0;
     g2.dbg_krows = w.kp_cap;
     g2.nmb = nmb;
+    // units of a few K iterations (C3: ~128 positions per 256-feature block) are bound by
+    // their per-unit drains: share one accumulator (3.09 -> 2.63 ms at C3); long units
+    // (C2: ~1,000 positions per block) keep the double-buffered per-unit drains (0.90
+    // vs 0.93 ms)
+    g2.snap = c->pend_rows_per_block < 512;
     for (int u = 0; u < nmb; ++u) {
         const Workspace::SegSet S = seg_set(w, c->pend[u].set);
         g2.kseg_off_b[u] = S.kseg_off;
@@ -1319,6 +1324,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             // anything needs this agent's dW or reports (check_active, sync, poll)
             c->pend[c->npend++] = fm_ctx::PendingMB{kset, slot};
             c->pend_agent = a;
+            c->pend_rows_per_block = Qcap / nblk;
             queued = true;
             count_launch(3);
             if (!batch || c->npend == w.nsets || step_last) {

@@ -162,6 +162,7 @@ struct fm_ctx {
     fm_agent* pend_agent = nullptr;
     PendingMB pend[kGemmMaxBatch];
     int npend = 0;
+    int64_t pend_rows_per_block = 0;  // context positions per 256-feature block (segment length)
     std::map<std::string, void*> ipc_cache;  // peer buffers mapped over NVLink (slots, gang receive buffers)
     std::vector<std::pair<size_t, void*>> recv_pool;  // gang receive buffers + barrier tokens, recycled
     std::unordered_map<void*, size_t> pool_sizes;

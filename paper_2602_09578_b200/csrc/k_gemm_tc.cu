@@ -231,7 +231,10 @@ struct GradEpi {
     }
 };
 
-constexpr int P_STAGES = 5;
+#ifndef FM_G2_STAGES
+#define FM_G2_STAGES 5
+#endif
+constexpr int P_STAGES = FM_G2_STAGES;
 constexpr uint32_t P_A_STAGE = 128 * BK * 2;    // 16 KB: this CTA's 128 rows of A
 constexpr uint32_t P_B_STAGE = 128 * BK * 2;    // 16 KB: this CTA's half of B's 256 rows
 constexpr uint32_t P_STAGE_BYTES = P_A_STAGE + P_B_STAGE;
@@ -243,10 +246,18 @@ constexpr int kThreadsPair = 192;  // w0 TMA, w1 MMA, w2-5 epilogue
 // (8 KB each, the second at +8 KB = the descriptor's LBO).
 // kSeg: both operands MN-major; column tile nb runs the K rows of its segment
 // (args.kseg_off / kseg_iters); B' holds only 256 columns.
-template <bool kAmn, bool kBmn, bool kSeg>
+// kSnap (batched micro-batches): ONE accumulator per tile (TMEM columns 0-255)
+// collects all of the tile's units; after each unit the epilogue reads it and a
+// snapshot of the previous unit's total (columns 256-511), adds the squared
+// difference — exactly that unit's contribution — to the unit's sum of squares
+// and stores the new snapshot; only the last unit drains the tile into dW.  One
+// drain per tile instead of one per unit (the drain's smem staging bounded the
+// K-GEMM2 of short-K shapes: L1 / shared 86% busy at C3).
+template <bool kAmn, bool kBmn, bool kSeg, bool kSnap = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     gemm_grad_kernel(const __grid_constant__ GemmMaps maps, GemmArgs args) {
     static_assert(!kSeg || (kAmn && kBmn), "segment operands are MN-major");
+    static_assert(!kSnap || kSeg, "snapshots batch segmented units");
     constexpr uint32_t kId = idesc_bf16_f32<256, BN, kAmn, kBmn>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -360,6 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                 const int nb = tile_coord(t, tiles_m, tiles_n, args.group_m).nb;
                 for (int u = 0; u < nmb; ++u) {
                     const int ke = unit_iters(u, nb);
+                    if constexpr (kSnap) acc = 0;  // the one accumulator
                     mbar_wait(&tempty[acc], acc_phase ^ 1);
                     tc_fence_after();
                     const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -376,7 +388,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk)
                             umma_bf16_2sm(d_tmem, adesc + a_step * kk, bdesc + b_step * kk, kId,
-                                          (k != 0 || kk != 0));
+                                          (k != 0 || kk != 0 || (kSnap && u != 0)));
                         umma_commit_2sm(&empty[stage], 0x3);
                         if (++stage == P_STAGES) {
                             stage = 0;
@@ -384,8 +396,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                         }
                     }
                     umma_commit_2sm(&tfull[acc], 0x3);
-                    acc ^= 1;
-                    if (acc == 0) acc_phase ^= 1;
+                    if constexpr (kSnap) {
+                        acc_phase ^= 1;
+                    } else {
+                        acc ^= 1;
+                        if (acc == 0) acc_phase ^= 1;
+                    }
                 }
             }
         }
@@ -406,6 +422,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
             const TileCoord tc = tile_coord(t, tiles_m, tiles_n, args.group_m);
             const int row = tc.mb * 256 + row_in_tile;
             for (int u = 0; u < nmb; ++u) {
+                if constexpr (kSnap) {
+                    const bool last = u + 1 == nmb;
+                    mbar_wait(&tfull[0], acc_phase);
+                    tc_fence_after();
+                    if (u > 0) tmem_st_wait();  // the previous unit's snapshot has landed
+                    epi.accumulate = args.accumulate;
+                    const uint32_t lane_base = tmem_base + ((quad * 32u) << 16);
+                    float part = 0.f;
+#pragma unroll 1
+                    for (int c = 0; c < BN / 32; ++c) {
+                        uint32_t r[32], q[32];
+                        tmem_ld_32x32b_x32(lane_base + static_cast<uint32_t>(c * 32), r);
+                        if (u > 0) tmem_ld_32x32b_x32(lane_base + static_cast<uint32_t>(BN + c * 32), q);
+                        tmem_ld_wait();
+                        if (c == BN / 32 - 1) {
+                            // every accumulator column is read: the MMA may add the next unit
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader[0]);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const float d = __uint_as_float(r[j]) - (u > 0 ? __uint_as_float(q[j]) : 0.f);
+                            part = fmaf(d, d, part);
+                        }
+                        if (!last) tmem_st_32x32b_x32(lane_base + static_cast<uint32_t>(BN + c * 32), r);
+                        else epi.chunk(args, row, tc.nb * BN + c * 32, r);
+                    }
+#pragma unroll
+                    for (int j = 0; j < kGemmMaxBatch; ++j)
+                        if (j == u) sq[j] += static_cast<double>(part);
+                    acc_phase ^= 1;
+                    continue;
+                }
                 mbar_wait(&tfull[acc], acc_phase);
                 tc_fence_after();
                 epi.sumsq = 0.f;
@@ -423,6 +473,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                         __syncwarp();
                         if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader[acc]);
                     }
+#ifdef FM_G2_PROBE_NODRAIN  // timing probe only: units before the last skip their dW update
+                    if (u + 1 < nmb) {
+                        float part = 0.f;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) part += __uint_as_float(r[j]) * __uint_as_float(r[j]);
+                        epi.sumsq += part;
+                        continue;
+                    }
+#endif
                     epi.chunk(args, row, tc.nb * BN + c * 32, r);
                 }
 #pragma unroll
@@ -449,14 +508,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
     }
 }
 
-template <bool kAmn, bool kBmn, bool kSeg>
+template <bool kAmn, bool kBmn, bool kSeg, bool kSnap = false>
 cudaError_t launch_grad(const GemmMaps& maps, const GemmArgs& args, int num_sms, cudaStream_t stream) {
     const size_t smem = gemm_smem_bytes();
     const int tiles = ((args.M + 255) / 256) * ((args.N + BN - 1) / BN);
     if (tiles == 0) return cudaSuccess;
     const int pairs = num_sms / 2;
     const int grid = 2 * (tiles < pairs ? tiles : pairs);
-    auto k = gemm_grad_kernel<kAmn, kBmn, kSeg>;
+    auto k = gemm_grad_kernel<kAmn, kBmn, kSeg, kSnap>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     k<<<grid, kThreadsPair, smem, stream>>>(maps, args);
@@ -496,6 +555,7 @@ cudaError_t gemm_kseg_launch(const GemmMaps& maps, const GemmArgs& args_in, int 
         args.kseg_iters_b[0] = args.kseg_iters;
         args.sumsq_b[0] = args.sumsq;
     }
+    if (args.nmb > 1 && args.snap) return launch_grad<true, true, true, true>(maps, args, num_sms, stream);
     return launch_grad<true, true, true>(maps, args, num_sms, stream);
 }
 

@@ -623,3 +623,59 @@ def test_segment_buffer_reuse_across_widths(ctx):
             assert np.all(np.isfinite(g)), (V, D)
         finally:
             L.fm_agent_destroy(h)
+
+
+@pytest.mark.parametrize("V,D,resp", [(2048, 4096, 24), (1000, 256, 200)])
+def test_batched_reduction_equals_per_micro_batch(ctx, V, D, resp):
+    """The step's K-GEMM2 is queued and runs once for all of its micro-batches
+    (one TMEM accumulator with per-unit snapshots for short segments — the
+    first shape, ~9 positions per 256-feature block — or double-buffered
+    per-unit drains — the second).  Against the same step with every
+    micro-batch's reduction forced by fm_agent_sync: the gradient, every
+    micro-batch report (grad norm and loss) and the update agree to fp32
+    summation order."""
+    L = _lib.lib()
+    rng = np.random.default_rng(V + D)
+    W0 = np.ascontiguousarray(rng.normal(size=(V, D)) * 0.5)
+    batches = [[(rng.integers(0, V, size=6).astype(np.int32), rng.integers(0, V, size=resp).astype(np.int32))
+                for _ in range(4)] for _ in range(4)]
+    advs = [rng.normal(size=4) for _ in range(4)]
+
+    def run(sync_each):
+        h = C.c_void_p()
+        _lib.check(L.fm_agent_create(ctx.handle, b"q", V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
+        try:
+            _lib.check(L.fm_agent_set_weights(h, W0.ctypes.data))
+            tickets = []
+            for k in range(4):
+                arr = (_lib.fm_sample * 4)(*[_lib.fm_sample(ctx.put(orc.encode(p)), ctx.put(orc.encode(r)), float(a))
+                                             for (p, r), a in zip(batches[k], advs[k])])
+                t = C.c_int64()
+                _lib.check(L.fm_train_micro_batch(h, arr, 4, 16, C.byref(t)))
+                tickets.append(t.value)
+                if sync_each:
+                    _lib.check(L.fm_agent_sync(h))
+            g = np.empty(V * D)
+            _lib.check(L.fm_agent_read_grad(h, g.ctypes.data))
+            reps = []
+            for t in tickets:
+                rep = _lib.fm_report()
+                assert L.fm_agent_poll_report(h, t, C.byref(rep)) in (0, 1)
+                _lib.check(L.fm_agent_sync(h))
+                assert L.fm_agent_poll_report(h, t, C.byref(rep)) == 1
+                reps.append((rep.grad_norm, rep.loss))
+            gn = C.c_double()
+            _lib.check(L.fm_apply_update(h, 16, 1e-3, 0.9, 0.999, 1e-8, C.byref(gn), None))
+            W = np.empty(V * D)
+            _lib.check(L.fm_agent_read_weights(h, W.ctypes.data))
+            return g, np.array(reps), gn.value, W
+        finally:
+            L.fm_agent_destroy(h)
+
+    g1, r1, n1, W1 = run(True)
+    g4, r4, n4, W4 = run(False)
+    assert np.all(np.isfinite(g4)) and np.any(g4 != 0)
+    assert rel_fro(g4, g1) < 1e-5
+    np.testing.assert_allclose(r4, r1, rtol=1e-4)
+    assert abs(n4 - n1) <= 1e-5 * n1
+    assert rel_fro(W4 - W0.reshape(-1), W1 - W0.reshape(-1)) < 1e-3
