@@ -85,11 +85,6 @@ uint64_t arena_token_count(const fm_ctx* ctx, uint64_t offset, bool* found) {
 
 namespace fm {
 
-int env_int(const char* name, int dflt) {
-    const char* v = std::getenv(name);
-    return v && *v ? std::max(1, std::atoi(v)) : dflt;
-}
-
 int set_dev(const fm_ctx* c) {
     FM_CUDA(cudaSetDevice(c->device));
     return FM_OK;
@@ -1060,7 +1055,7 @@ static int gemm2_flush(fm_agent* a, bool exchange, bool dp_norms, bool step_last
     g2.K = 0;
     // raster: the 256-feature column tiles of a vocab row block run together, so the
     // row block's dW stripe and A' columns stay L2-local
-    g2.group_m = env_int("FM_G2_GROUP_M", 1);
+    g2.group_m = 1;
     g2.out = static_cast<float*>(a->dW) + static_cast<size_t>(c0) * a->D;
     g2.ld_out = static_cast<long long>(a->D);
     g2.accumulate = a->dw_valid ? 1 : 0;

@@ -319,7 +319,6 @@ struct fm_weights {
 
 // ---- runtime helpers (fm_runtime.cu) shared by the ABI translation units ----
 namespace fm {
-int env_int(const char* name, int dflt);
 int set_dev(const fm_ctx* c);
 int ipc_open_cached(fm_ctx* c, const cudaIpcMemHandle_t& h, void** out);
 int pool_take(fm_ctx* c, size_t bytes, void** out);

@@ -473,15 +473,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsPair, 1)
                         __syncwarp();
                         if (lane == 0) mbar_arrive_cluster_relaxed(tempty_leader[acc]);
                     }
-#ifdef FM_G2_PROBE_NODRAIN  // timing probe only: units before the last skip their dW update
-                    if (u + 1 < nmb) {
-                        float part = 0.f;
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) part += __uint_as_float(r[j]) * __uint_as_float(r[j]);
-                        epi.sumsq += part;
-                        continue;
-                    }
-#endif
                     epi.chunk(args, row, tc.nb * BN + c * 32, r);
                 }
 #pragma unroll
