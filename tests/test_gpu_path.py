@@ -679,3 +679,56 @@ def test_batched_reduction_equals_per_micro_batch(ctx, V, D, resp):
     np.testing.assert_allclose(r4, r1, rtol=1e-4)
     assert abs(n4 - n1) <= 1e-5 * n1
     assert rel_fro(W4 - W0.reshape(-1), W1 - W0.reshape(-1)) < 1e-3
+
+
+@pytest.mark.parametrize("tier", [_lib.TIER_HOST, _lib.TIER_DEVICE])
+def test_queued_reduction_survives_swap(ctx, tier):
+    """Two micro-batches queued (their K-GEMM2 not yet run), the agent
+    suspended and re-activated, two more trained, then the update: the
+    suspend runs the queued reduction first (check_active), the partial dW
+    travels with the parked state, and the result equals the uninterrupted
+    step's (same queue boundaries: 2 + 2 vs 4 units, fp32 summation order)."""
+    L = _lib.lib()
+    V, D = 1024, 512
+    rng = np.random.default_rng(23)
+    W0 = np.ascontiguousarray(rng.normal(size=(V, D)) * 0.5)
+    batches = [[(rng.integers(0, V, size=6).astype(np.int32), rng.integers(0, V, size=40).astype(np.int32))
+                for _ in range(4)] for _ in range(4)]
+    advs = [rng.normal(size=4) for _ in range(4)]
+
+    def run(swap):
+        h = C.c_void_p()
+        _lib.check(L.fm_agent_create(ctx.handle, b"s", V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
+        try:
+            _lib.check(L.fm_agent_set_weights(h, W0.ctypes.data))
+            tickets = []
+            for k in range(4):
+                if swap and k == 2:
+                    _lib.check(L.fm_agent_suspend(h, tier, -1))
+                    _lib.check(L.fm_agent_activate(h, ctx.handle))
+                arr = (_lib.fm_sample * 4)(*[_lib.fm_sample(ctx.put(orc.encode(p)), ctx.put(orc.encode(r)), float(a))
+                                             for (p, r), a in zip(batches[k], advs[k])])
+                t = C.c_int64()
+                _lib.check(L.fm_train_micro_batch(h, arr, 4, 16, C.byref(t)))
+                tickets.append(t.value)
+            gn = C.c_double()
+            _lib.check(L.fm_apply_update(h, 16, 1e-3, 0.9, 0.999, 1e-8, C.byref(gn), None))
+            norms = []
+            for t in tickets:
+                rep = _lib.fm_report()
+                assert L.fm_agent_poll_report(h, t, C.byref(rep)) in (0, 1)
+                _lib.check(L.fm_agent_sync(h))
+                assert L.fm_agent_poll_report(h, t, C.byref(rep)) == 1
+                norms.append(rep.grad_norm)
+            W = np.empty(V * D)
+            _lib.check(L.fm_agent_read_weights(h, W.ctypes.data))
+            return np.array(norms), gn.value, W
+        finally:
+            L.fm_agent_destroy(h)
+
+    n0, u0, W0r = run(False)
+    n1, u1, W1r = run(True)
+    assert np.all(np.isfinite(n1)) and np.all(n1 > 0)
+    np.testing.assert_allclose(n1, n0, rtol=1e-4)
+    assert abs(u1 - u0) <= 1e-5 * u0
+    assert rel_fro(W1r - W0.reshape(-1), W0r - W0.reshape(-1)) < 1e-3
