@@ -66,6 +66,16 @@ constexpr int kBandThreads = kBandConsumers + 32;    // + the producer warp
 template <bool kGrad>
 constexpr int kBandStagesT = kGrad ? FM_BAND_STAGES : FM_STATS_STAGES;
 constexpr int kBandRows = 128;                       // trained rows per CTA
+// vocabulary columns per consumer lane (4 fp32 pairs at 8): 8 by default; 4 halves
+// the per-thread state for a third CTA per SM
+#ifndef FM_BAND_CPL
+#define FM_BAND_CPL 8
+#endif
+constexpr int kCPL = FM_BAND_CPL;
+constexpr int kP = kCPL / 2;  // fp32 pairs per lane
+static_assert(kCPL == 8 || kCPL == 4, "8 or 4 columns per lane");
+constexpr int kBandMinBlocks = kCPL == 8 ? 2 : 3;
+using Frag = std::conditional_t<kCPL == 8, uint4, uint2>;  // a lane's kCPL bf16 columns
 // 8 columns per lane, two CTAs (18 warps) per SM: 16 columns per lane (measured:
 // K-stats 0.43-0.53 ms vs 0.33 ms at C2) needs more registers than two CTAs leave
 // and drops to one CTA per SM.
@@ -267,20 +277,29 @@ __global__ void __launch_bounds__(1024) pslot_place_kernel(const int32_t* __rest
 
 // ---- K-stats / K-band ------------------------------------------------------
 // 8 bf16 -> 4 fp32 pairs (exact)
-__device__ __forceinline__ void unpack8(uint4 u, float2 (&x)[4]) {
+__device__ __forceinline__ void unpack_frag(uint4 u, float2 (&x)[4]) {
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) x[i] = make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xffff0000u));
 }
-
-__device__ __forceinline__ uint4 pack8(const float2 (&x)[4]) {
-    uint32_t w[4];
+__device__ __forceinline__ void unpack_frag(uint2 u, float2 (&x)[2]) {
+    const uint32_t w[2] = {u.x, u.y};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 2; ++i) x[i] = make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xffff0000u));
+}
+
+__device__ __forceinline__ uint4 make_frag(const uint32_t (&w)[4]) { return make_uint4(w[0], w[1], w[2], w[3]); }
+__device__ __forceinline__ uint2 make_frag(const uint32_t (&w)[2]) { return make_uint2(w[0], w[1]); }
+
+// kP fp32 pairs -> kCPL bf16 (round to nearest)
+__device__ __forceinline__ Frag pack_frag(const float2 (&x)[kP]) {
+    uint32_t w[kP];
+#pragma unroll
+    for (int i = 0; i < kP; ++i) {
         const __nv_bfloat162 h = __floats2bfloat162_rn(x[i].x, x[i].y);
         w[i] = *reinterpret_cast<const uint32_t*>(&h);
     }
-    return make_uint4(w[0], w[1], w[2], w[3]);
+    return make_frag(w);
 }
 
 // 2^x, one MUFU op (inputs <= 0 here; results below 2^-126 flush to zero)
@@ -309,14 +328,14 @@ static_assert(kBandStagesT<false> % 4 == 0 && kBandStagesT<true> % 4 == 0,
 template <bool kGrad>
 constexpr size_t band_smem_bytes() {
     constexpr int kBandStages = kBandStagesT<kGrad>;
-    return kBandStages * kBandConsumers * 16 + 2 * kBandStages * sizeof(uint64_t) +
+    return kBandStages * kBandConsumers * 2 * kCPL + 2 * kBandStages * sizeof(uint64_t) +
            5 * kMetaRows * sizeof(int32_t) + (kGrad ? 0 : (kBandConsumers / 32) * 32 * kRedPitch * sizeof(float)) +
            kMaxQ * sizeof(int32_t);
 }
 
 template <bool kGrad, int kMinBlocks>
 __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const BandArgs A) {
-    constexpr int kCols = kBandConsumers * 8;  // vocabulary columns per item
+    constexpr int kCols = kBandConsumers * kCPL;  // vocabulary columns per item
     constexpr int kStage = kCols * 2;          // bytes of one position's W16^T slice
     constexpr int kBandStages = kBandStagesT<kGrad>;
     extern __shared__ __align__(128) uint8_t band_smem[];
@@ -452,15 +471,15 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
         }
         named_bar_sync(1, kBandConsumers);
 
-        const int64_t cb = v0 + static_cast<int64_t>(tid) * 8;
-        const int nv = A.V - cb >= 8 ? 8 : (A.V - cb > 0 ? static_cast<int>(A.V - cb) : 0);
-        const bool warp_full = __all_sync(0xffffffffu, nv == 8);
+        const int64_t cb = v0 + static_cast<int64_t>(tid) * kCPL;
+        const int nv = A.V - cb >= kCPL ? kCPL : (A.V - cb > 0 ? static_cast<int>(A.V - cb) : 0);
+        const bool warp_full = __all_sync(0xffffffffu, nv == kCPL);
         const int tile = static_cast<int>(v0 / kCols) * (kBandConsumers / 32) + warp;  // the warp's stats column
         // per position q: xp = X[q-1] (previous position's row), pr[q & 3] = X[q-1] + X[q];
         // the row ending at q sums pr[(q-2) & 3] + pr[q & 3] = X[q-3] + X[q-2] + X[q-1] + X[q]
-        float2 xp[4], pr[4][4], gr[4][4];
+        float2 xp[kP], pr[4][kP], gr[4][kP];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kP; ++j) {
             xp[j] = make_float2(0.f, 0.f);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -483,12 +502,12 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
 
         // pass A: the row's partial sum of exp2(z * log2e - bound * log2e) over the lane's
         // columns (the bound mrow >= every z of the row: no max reduction)
-        auto row_sum = [&](const float2 (&z4)[4], float c, float off, auto FullTag) -> float {
+        auto row_sum = [&](const float2 (&z4)[kP], float c, float off, auto FullTag) -> float {
             constexpr bool kFull = decltype(FullTag)::value;
             const float2 cc = make_float2(c, c), oo = make_float2(off, off);
-            float2 e[4];
+            float2 e[kP];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < kP; ++j) {
                 const float2 y = __ffma2_rn(z4[j], cc, oo);
                 e[j] = make_float2(ex2(y.x), ex2(y.y));
                 if constexpr (!kFull) {
@@ -496,21 +515,23 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
                     if (!valid(j, 1)) e[j].y = 0.f;
                 }
             }
-            const float2 s2 = __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3]));
+            float2 s2;
+            if constexpr (kP == 4) s2 = __fadd2_rn(__fadd2_rn(e[0], e[1]), __fadd2_rn(e[2], e[3]));
+            else s2 = __fadd2_rn(e[0], e[1]);
             return s2.x + s2.y;
         };
         // pass B: g = ce (delta(v, a) - exp(z - lse)) over the lane's columns (zero-advantage
         // rows and the sentinel give 0, training.hpp:394); dact = action column - the lane's first
-        auto row_grad = [&](const float2 (&z4)[4], float c, float off, float ce, int dact, float2 (&gg)[4]) {
+        auto row_grad = [&](const float2 (&z4)[kP], float c, float off, float ce, int dact, float2 (&gg)[kP]) {
             const float2 cc = make_float2(c, c), oo = make_float2(off, off), nce = make_float2(-ce, -ce);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < kP; ++j) {
                 const float2 y = __ffma2_rn(z4[j], cc, oo);
                 gg[j] = __fmul2_rn(make_float2(ex2(y.x), ex2(y.y)), nce);
             }
-            if (static_cast<unsigned>(dact) < 8u) {
+            if (static_cast<unsigned>(dact) < static_cast<unsigned>(kCPL)) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < kP; ++j) {
                     if (dact == 2 * j) gg[j].x += ce;
                     if (dact == 2 * j + 1) gg[j].y += ce;
                 }
@@ -526,23 +547,23 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
                 }
                 const int32_t sl = __shfl_sync(0xffffffffu, s_cur, p - sg);
                 if (sl >= 0 && nv > 0) {
-                    float2 h[4];
+                    float2 h[kP];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
+                    for (int j = 0; j < kP; ++j)
                         h[j] = __fadd2_rn(__fadd2_rn(gr[0][j], gr[1][j]), __fadd2_rn(gr[2][j], gr[3][j]));
-                    if (nv < 8) {
+                    if (nv < kCPL) {
                         // the row's columns past V (up to its 8-aligned pitch) hold arithmetic on
                         // stale ring bytes: store zeros, so every A' byte stays finite — A' is
                         // reused across agents of other widths, whose segment padding rows (B' = 0)
                         // may land there, and 0 x NaN would poison their dW
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
+                        for (int j = 0; j < kP; ++j) {
                             if (2 * j >= nv) h[j].x = 0.f;
                             if (2 * j + 1 >= nv) h[j].y = 0.f;
                         }
                     }
-                    FM_DCHECK(sl < A.dbg_kp && cb + 8 <= A.ld_a);
-                    *reinterpret_cast<uint4*>(A.aseg + static_cast<int64_t>(sl) * A.ld_a + cb) = pack8(h);
+                    FM_DCHECK(sl < A.dbg_kp && cb + kCPL <= A.ld_a);
+                    *reinterpret_cast<Frag*>(A.aseg + static_cast<int64_t>(sl) * A.ld_a + cb) = pack_frag(h);
                 }
             }
         };
@@ -577,25 +598,25 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
                 constexpr int S = decltype(Sc)::value;
                 if (q >= qa && q < qb) {
                     mbar_wait(&full[st], ph);
-                    const uint4 u = *reinterpret_cast<const uint4*>(ring + st * kStage + tid * 16);
+                    const Frag u = *reinterpret_cast<const Frag*>(ring + st * kStage + tid * sizeof(Frag));
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[st]);
                     if (++st == kBandStages) {
                         st = 0;
                         ph ^= 1u;
                     }
-                    float2 x[4];
-                    unpack8(u, x);
+                    float2 x[kP];
+                    unpack_frag(u, x);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
+                    for (int j = 0; j < kP; ++j) {
                         pr[S][j] = __fadd2_rn(xp[j], x[j]);
                         xp[j] = x[j];
                     }
                     if (q == next_end) {  // the row whose four positions end here
                         const int i = ri;
-                        float2 z4[4];
+                        float2 z4[kP];
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) z4[j] = __fadd2_rn(pr[(S + 2) & 3][j], pr[S][j]);
+                        for (int j = 0; j < kP; ++j) z4[j] = __fadd2_rn(pr[(S + 2) & 3][j], pr[S][j]);
                         if constexpr (!kGrad) {
                             const float s = warp_full ? row_sum(z4, m_c[i], m_off[i], std::true_type{})
                                                       : row_sum(z4, m_c[i], m_off[i], std::false_type{});
@@ -608,11 +629,11 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
                         next_end = m_q0[ri] + 3;
                     } else if constexpr (kGrad) {
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) gr[S][j] = make_float2(0.f, 0.f);  // no row ends here
+                        for (int j = 0; j < kP; ++j) gr[S][j] = make_float2(0.f, 0.f);  // no row ends here
                     }
                 } else if constexpr (kGrad) {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) gr[S][j] = make_float2(0.f, 0.f);  // past the last position
+                    for (int j = 0; j < kP; ++j) gr[S][j] = make_float2(0.f, 0.f);  // past the last position
                 }
                 if constexpr (kGrad) flush_h(q - 3);
             };
@@ -635,11 +656,11 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
         // pass A's per-column masks (only the last slice's boundary warp needs them)
         auto fast_loop = [&](auto FullTag) {
             for (int qq = qlo; qq < qhi; qq += 4) {
-                uint4 u[4];
+                Frag u[4];
 #pragma unroll
                 for (int S = 0; S < 4; ++S) {
                     mbar_wait(&full[st + S], ph);
-                    u[S] = *reinterpret_cast<const uint4*>(ring + (st + S) * kStage + tid * 16);
+                    u[S] = *reinterpret_cast<const Frag*>(ring + (st + S) * kStage + tid * sizeof(Frag));
                 }
                 __syncwarp();
                 if (lane == 0) {
@@ -654,17 +675,17 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
 #pragma unroll
                 for (int S = 0; S < 4; ++S) {
                     const int q = qq + S;
-                    float2 x[4];
-                    unpack8(u[S], x);
+                    float2 x[kP];
+                    unpack_frag(u[S], x);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
+                    for (int j = 0; j < kP; ++j) {
                         pr[S][j] = __fadd2_rn(xp[j], x[j]);
                         xp[j] = x[j];
                     }
                     const int i = m_end[q - qlo];
-                    float2 z4[4];
+                    float2 z4[kP];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) z4[j] = __fadd2_rn(pr[(S + 2) & 3][j], pr[S][j]);
+                    for (int j = 0; j < kP; ++j) z4[j] = __fadd2_rn(pr[(S + 2) & 3][j], pr[S][j]);
                     if constexpr (!kGrad) {
                         const float s = row_sum(z4, m_c[i], m_off[i], FullTag);
                         // partial sum parked in the warp's 32-row ring (slot i & 31)
@@ -730,7 +751,7 @@ cudaError_t launch_pslots(const int32_t* feat, int64_t Q, int nblk, int32_t* kco
 }
 
 int band_stats_ld(int64_t V) {
-    const int64_t cols = kBandConsumers * 8;
+    const int64_t cols = kBandConsumers * kCPL;
     return static_cast<int>((V + cols - 1) / cols) * (kBandConsumers / 32);
 }
 
@@ -746,14 +767,15 @@ cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int64_t grid = items >= 8 * static_cast<int64_t>(sms) ? items : (items < 2 * sms ? items : 2 * sms);
+        const int64_t slots = static_cast<int64_t>(kBandMinBlocks) * sms;
+        const int64_t grid = items >= 4 * slots ? items : (items < slots ? items : slots);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
         kern<<<static_cast<unsigned>(grid), kBandThreads, smem, s>>>(A);
         return cudaGetLastError();
     };
-    if (grad) return go(band_kernel<true, 2>, kBandConsumers * 8, band_smem_bytes<true>());
-    return go(band_kernel<false, 2>, kBandConsumers * 8, band_smem_bytes<false>());
+    if (grad) return go(band_kernel<true, kBandMinBlocks>, kBandConsumers * kCPL, band_smem_bytes<true>());
+    return go(band_kernel<false, kBandMinBlocks>, kBandConsumers * kCPL, band_smem_bytes<false>());
 }
 
 }  // namespace fm
