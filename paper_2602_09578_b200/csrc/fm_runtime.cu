@@ -1253,7 +1253,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
                 FM_CUDA(launch_positions(c->arena, w.sd, n, row_lo, M, a->D, w.pos_feat, Qcap, s));
                 FM_CUDA(launch_pslots(w.pos_feat, Qcap, nblk, w.kcount, S.kseg_off, S.kiters, w.pos_slot, S.bseg,
                                       w.kp_cap, w.kseg_rows, s));
-                count_launch(4);
+                count_launch(5);  // K-gather, K-pos, K-pslot count / scan / place
             }
             BandArgs ba{};
             ba.w16t = a->W16 + c0;
