@@ -1279,7 +1279,7 @@ static int train_impl(fm_agent* a, const SampleDesc* hsd, int n, int64_t M_total
             ba.dbg_D = static_cast<int64_t>(a->D);
             const bool cols = c1 > c0;  // (a vocabulary-gang rank may own no columns)
             {
-                // K-stats: per-(row, 256-column tile) softmax partials + the taken token's logit
+                // K-stats: per-(row, consumer warp) partial sums of exp(z - bound)
                 KScope k(c, K_STATS, s);
                 if (cols) FM_CUDA(launch_band(ba, false, s));
             }

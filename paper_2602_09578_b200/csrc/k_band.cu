@@ -28,8 +28,9 @@
 //   K-pos     positions of the micro-batch shard: feat[q] (prompt tail +
 //             response prefix of every sample), q0[row]       (codec.hpp:24-30)
 //   K-pslot   A'/B' slot of every position in its feature block's segment
-//   K-stats   pass A: per-(row, 256-column tile) softmax partials (max, sum)
-//             and the taken token's fp32 logit                (policy.hpp:62-70)
+//             (count, one scan, place)
+//   K-stats   pass A: per-(row, consumer warp) partial sums of exp(z - bound)
+//             against the row's fmax bound (no max pass)      (policy.hpp:62-70)
 //   K-band    pass B: p = exp(z - lse) (lse from K-lse), the per-row
 //             log-softmax gradient folded into the per-position H rows
 //                                                             (policy.hpp:83-90, training.hpp:394)
