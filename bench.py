@@ -399,7 +399,8 @@ def run_ours(args, dist: Dist) -> dict | None:
     #   K-GEMM2: A' (H rows incl. segment padding) read once + dW read-modify-write (the step's
     #            first micro-batch writes only)
     #   K-adam : 38 B/param (r: W8 m4 v4 g4; w: W8 m4 v4 W16^T 2)
-    bytes_stats = 2.0 * Q_local * ldw + 8.0 * M_local * ntile + 4.0 * M_local
+    stats_ld = int(np.ceil(V / 2048)) * 8  # K-stats partial sums per row (one per consumer warp and slice)
+    bytes_stats = 2.0 * Q_local * ldw + 4.0 * M_local * stats_ld + 4.0 * M_local
     bytes_band = 4.0 * Q_local * ldw + 8.0 * M_local * 2
     bytes_adam = 38.0 * P
     g_adam = len(place[mine[0]]) if mine and args.dp_mode == "gang" else 1
@@ -407,7 +408,8 @@ def run_ours(args, dist: Dist) -> dict | None:
         # sharded K-adam on P/g params: + the g-1 received fp32 partials read; the
         # bf16 rows it writes into the g-1 peers' shadows go over NVLink, not local HBM
         bytes_adam = (38.0 + 4.0 * (g_adam - 1)) * P / g_adam
-    bytes_lse = M_local * (ntile * 8 + 24)
+    # the row's partial sums + action, bound, taken logit, coefficient, loss weight; lse, logp, coef_eff
+    bytes_lse = M_local * (4.0 * stats_ld + 24 + 12)
     kernels = {}
     for i, name in enumerate(KINDS):
         if kcnt[i] == 0:
