@@ -392,7 +392,6 @@ def run_ours(args, dist: Dist) -> dict | None:
     # context positions of a micro-batch shard: its rows + 3 per sample
     Q_local = M_local + 3 * cfg.micro_batch
     ldw = int(np.ceil(V / 8) * 8)
-    ntile = int(np.ceil(V / 256))
     # algorithmic bytes per launch:
     #   K-stats: every position's W16^T row read once + per-(row, 256-col tile) partials written
     #   K-band : the position's W16^T row read once + its bf16 gradient row H written once
