@@ -393,10 +393,10 @@ def run_ours(args, dist: Dist) -> dict | None:
     Q_local = M_local + 3 * cfg.micro_batch
     ldw = int(np.ceil(V / 8) * 8)
     # algorithmic bytes per launch:
-    #   K-stats: every position's W16^T row read once + per-(row, 256-col tile) partials written
+    #   K-stats: every position's W16^T row read once + per-(row, warp slice) partials written
     #   K-band : the position's W16^T row read once + its bf16 gradient row H written once
-    #   K-GEMM2: A' (H rows incl. segment padding) read once + dW read-modify-write (the step's
-    #            first micro-batch writes only)
+    #   K-GEMM2: A' (H rows incl. segment padding) read once + dW written once per launch when
+    #            the step's micro-batches are batched (else read-modify-write after the first)
     #   K-adam : 38 B/param (r: W8 m4 v4 g4; w: W8 m4 v4 W16^T 2)
     stats_ld = int(np.ceil(V / 2048)) * 8  # K-stats partial sums per row (one per consumer warp and slice)
     bytes_stats = 2.0 * Q_local * ldw + 4.0 * M_local * stats_ld + 4.0 * M_local
