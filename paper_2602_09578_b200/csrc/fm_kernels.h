@@ -117,6 +117,7 @@ struct BandArgs {
     // vocabulary-parallel gang: w16t and aseg point at this rank's first column, V is its
     // range's width and actions are taken relative to col_base
     int64_t col_base = 0;
+    int rows_per_item = 0;  // (set by launch_band: 128, or 64 when that balances persistent CTAs better)
 };
 cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s);
 // K-stats partials per row (one per consumer warp of every vocabulary slice).

@@ -370,7 +370,8 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
     // items, so the producer prefetches the next item's rows while the consumers finish
     // (and load the metadata of) the current one — no partial last wave.
     const int nslices = static_cast<int>((A.V + kCols - 1) / kCols);
-    const int nitems = nslices * static_cast<int>((A.M + kBandRows - 1) / kBandRows);
+    const int rpi = A.rows_per_item;  // <= kBandRows
+    const int nitems = nslices * static_cast<int>((A.M + rpi - 1) / rpi);
     struct Item {
         int64_t v0;
         int ra, rb, rstart, nrows, qa, qb, qend, qlo, qhi;
@@ -379,8 +380,8 @@ __global__ void __launch_bounds__(kBandThreads, kMinBlocks) band_kernel(const Ba
     auto item_at = [&](int it) {
         Item g;
         g.v0 = static_cast<int64_t>(it % nslices) * kCols;
-        g.ra = (it / nslices) * kBandRows;
-        g.rb = g.ra + kBandRows < A.M ? g.ra + kBandRows : static_cast<int>(A.M);
+        g.ra = (it / nslices) * rpi;
+        g.rb = g.ra + rpi < A.M ? g.ra + rpi : static_cast<int>(A.M);
         g.rstart = kGrad ? (g.ra >= 3 ? g.ra - 3 : 0) : g.ra;
         g.nrows = g.rb - g.rstart;
         g.qa = __ldg(A.q0 + g.rstart);
@@ -763,16 +764,31 @@ cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s) {
         // one CTA per item while there are >= 4 waves of them (two CTAs per SM); fewer
         // items (a vocabulary-gang rank's slices) run on persistent CTAs that stream item
         // after item without a partial last wave (measured at C2: 6.9 waves 0.209 vs
-        // 0.219 ms K-stats one-per-item; 3.5 waves 0.150 vs 0.130 ms persistent)
-        const int64_t items = ((A.V + cols - 1) / cols) * ((A.M + kBandRows - 1) / kBandRows);
+        // 0.219 ms K-stats one-per-item; 3.5 waves 0.150 vs 0.130 ms persistent).  The
+        // persistent case takes 64-row items when that evens out the CTAs' loads (C2 gang
+        // of 2: 1,024 items of 131 positions = 4 per CTA at most, 3.5 on average, vs
+        // 2,048 of 67 = 7 / 6.9)
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int64_t slots = static_cast<int64_t>(kBandMinBlocks) * sms;
+        const int64_t nsl = (A.V + cols - 1) / cols;
+        auto items_of = [&](int64_t r) { return nsl * ((A.M + r - 1) / r); };
+        BandArgs B = A;
+        B.rows_per_item = kBandRows;
+        int64_t items = items_of(kBandRows);
+        if (items < 4 * slots) {
+            // the busiest CTA's positions for either item height (3 halo positions per item)
+            auto load = [&](int64_t r) { return (items_of(r) + slots - 1) / slots * (r + 3); };
+            if (load(kBandRows / 2) < load(kBandRows)) {
+                B.rows_per_item = kBandRows / 2;
+                items = items_of(kBandRows / 2);
+            }
+        }
         const int64_t grid = items >= 4 * slots ? items : (items < slots ? items : slots);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         if (e != cudaSuccess) return e;
-        kern<<<static_cast<unsigned>(grid), kBandThreads, smem, s>>>(A);
+        kern<<<static_cast<unsigned>(grid), kBandThreads, smem, s>>>(B);
         return cudaGetLastError();
     };
     if (grad) return go(band_kernel<true, kBandMinBlocks>, kBandConsumers * kCPL, band_smem_bytes<true>());
