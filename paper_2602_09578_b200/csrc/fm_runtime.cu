@@ -490,6 +490,7 @@ int fm_ctx_create(int device, fm_ctx** out) {
 int fm_ctx_destroy(fm_ctx* c) {
     if (!c) return FM_OK;
     cudaSetDevice(c->device);
+    ctx_flush(c);  // a queued K-GEMM2 still belongs to a live agent's dW and reports
     cudaDeviceSynchronize();
     ws_free(c->ws);
     cudaFree(c->arena);
