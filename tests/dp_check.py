@@ -89,6 +89,48 @@ def gang_vs_allreduce(ctx, comm, rank, world, gang_mode="gang") -> bool:
     return good
 
 
+def vocab_vs_single(ctx, comm, rank, world) -> bool:
+    """Bench-like widths (V = 8,192: 32 row tiles; D = 2,048; 2 x 16 samples of
+    64 + 256 tokens, so the band pass runs persistent 64-row items and K-GEMM2
+    reduces two queued micro-batches per launch): the vocabulary-parallel gang
+    and a plain one-GPU agent on the same batch must give the same gradient,
+    grad norm and update (different softmax-sum order only)."""
+    import workload_helpers as wh
+    L = _lib.lib()
+    V, D, G, mb = 8192, 2048, 32, 16
+    rng = np.random.default_rng(23)
+    W0 = rng.normal(size=(V, D)) * 0.02
+    batches = [[(rng.integers(0, V, 64).astype(np.int32), rng.integers(0, V, 256).astype(np.int32), float(a))
+                for a in rng.normal(size=mb)] for _ in range(G // mb)]
+    outs = {}
+    for mode in ("single", "vocab"):
+        h = C.c_void_p()
+        _lib.check(L.fm_agent_create(ctx.handle, mode.encode(), V, D, _lib.PRECISION_BF16_TC, C.byref(h)))
+        _lib.check(L.fm_agent_set_weights(h, np.ascontiguousarray(W0).ctypes.data))
+        if mode == "vocab":
+            _attach(L, h, comm, world, 1)
+        for bt in batches:
+            arr = (_lib.fm_sample * mb)(*[_lib.fm_sample(ctx.put(wh.enc(p)), ctx.put(wh.enc(r)), a) for p, r, a in bt])
+            t = C.c_int64()
+            _lib.check(L.fm_train_micro_batch(h, arr, mb, G, C.byref(t)))
+        g = np.empty(V * D)
+        _lib.check(L.fm_agent_read_grad(h, g.ctypes.data))
+        gn = C.c_double()
+        _lib.check(L.fm_apply_update(h, G, 1e-4, 0.9, 0.999, 1e-8, C.byref(gn), None))
+        W = np.empty(V * D)
+        _lib.check(L.fm_agent_read_weights(h, W.ctypes.data))
+        outs[mode] = (g.reshape(V, D), gn.value, W.reshape(V, D) - W0)
+        L.fm_agent_destroy(h)
+    eg = rel_fro(outs["vocab"][0], outs["single"][0])
+    en = abs(outs["vocab"][1] - outs["single"][1]) / outs["single"][1]
+    ew = rel_fro(outs["vocab"][2], outs["single"][2])
+    good = eg < 1e-4 and en < 1e-5 and ew < 1e-2
+    if rank == 0:
+        print(f"vocab vs single GPU (V=8192, D=2048): grad rel {eg:.3e}, grad-norm rel {en:.3e}, "
+              f"dW rel {ew:.3e} -> {'OK' if good else 'FAIL'}", flush=True)
+    return good
+
+
 def main():
     mode = sys.argv[1] if len(sys.argv) > 1 else "allreduce"
     # "norms": exact per-micro-batch grad norms under DP (fm_agent_set_dp_norms)
@@ -203,6 +245,8 @@ def main():
     L.fm_agent_destroy(h)
     if mode in ("gang", "vocab"):
         ok = ok and gang_vs_allreduce(ctx, comm, rank, world, mode)
+    if mode == "vocab":
+        ok = vocab_vs_single(ctx, comm, rank, world) and ok
     L.fm_comm_destroy(comm)
     ctx.close()
     okt = torch.tensor([1 if (ok and same and full_ok) else 0])
