@@ -56,10 +56,10 @@ namespace {
 
 constexpr int kBandConsumers = 256;                  // 8 consumer warps
 constexpr int kBandThreads = kBandConsumers + 32;    // + the producer warp
-// W16^T ring stages (4 KB each), both passes 16 (pass A also holds a 34 KB partial-sum buffer):
-// two CTAs per SM; 12 / 16 / 24 stages measured within 1% (tools/variant_libs.sh)
+// W16^T ring stages (4 KB each): pass B 16 at two CTAs per SM (12 / 16 / 24 measured within
+// 1%, tools/variant_libs.sh); pass A 8 (it also holds a 34 KB partial-sum buffer) at three
 #ifndef FM_STATS_STAGES
-#define FM_STATS_STAGES 16
+#define FM_STATS_STAGES 8
 #endif
 #ifndef FM_BAND_STAGES
 #define FM_BAND_STAGES 16
@@ -76,6 +76,13 @@ constexpr int kCPL = FM_BAND_CPL;
 constexpr int kP = kCPL / 2;  // fp32 pairs per lane
 static_assert(kCPL == 8 || kCPL == 4, "8 or 4 columns per lane");
 constexpr int kBandMinBlocks = kCPL == 8 ? 2 : 3;
+// pass A alone fits 72 registers at 8 columns per lane (no spills): three CTAs (27 warps) per
+// SM with an 8-stage ring, measured at C2 0.193 vs 0.211 ms (two CTAs, 16 stages) and 0.217
+// (two CTAs, 8 stages): K-stats is latency-bound, the extra warps hide it
+#ifndef FM_STATS_MIN_BLOCKS
+#define FM_STATS_MIN_BLOCKS (kCPL == 8 ? 3 : 4)
+#endif
+constexpr int kStatsMinBlocks = FM_STATS_MIN_BLOCKS;
 using Frag = std::conditional_t<kCPL == 8, uint4, uint2>;  // a lane's kCPL bf16 columns
 // 8 columns per lane, two CTAs (18 warps) per SM: 16 columns per lane (measured:
 // K-stats 0.43-0.53 ms vs 0.33 ms at C2) needs more registers than two CTAs leave
@@ -760,7 +767,7 @@ int band_stats_ld(int64_t V) {
 cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s) {
     if (A.M <= 0) return cudaSuccess;
     if (A.M + 3 * A.M >= INT32_MAX - 16) return cudaErrorInvalidValue;  // positions are int32
-    auto go = [&](auto kern, int cols, size_t smem) {
+    auto go = [&](auto kern, int min_blocks, int cols, size_t smem) {
         // one CTA per item while there are >= 4 waves of them (two CTAs per SM); fewer
         // items (a vocabulary-gang rank's slices) run on persistent CTAs that stream item
         // after item without a partial last wave (measured at C2: 6.9 waves 0.209 vs
@@ -771,7 +778,7 @@ cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s) {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int64_t slots = static_cast<int64_t>(kBandMinBlocks) * sms;
+        const int64_t slots = static_cast<int64_t>(min_blocks) * sms;
         const int64_t nsl = (A.V + cols - 1) / cols;
         auto items_of = [&](int64_t r) { return nsl * ((A.M + r - 1) / r); };
         BandArgs B = A;
@@ -791,8 +798,8 @@ cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s) {
         kern<<<static_cast<unsigned>(grid), kBandThreads, smem, s>>>(B);
         return cudaGetLastError();
     };
-    if (grad) return go(band_kernel<true, kBandMinBlocks>, kBandConsumers * kCPL, band_smem_bytes<true>());
-    return go(band_kernel<false, kBandMinBlocks>, kBandConsumers * kCPL, band_smem_bytes<false>());
+    if (grad) return go(band_kernel<true, kBandMinBlocks>, kBandMinBlocks, kBandConsumers * kCPL, band_smem_bytes<true>());
+    return go(band_kernel<false, kStatsMinBlocks>, kStatsMinBlocks, kBandConsumers * kCPL, band_smem_bytes<false>());
 }
 
 }  // namespace fm
