@@ -18,6 +18,7 @@ time-multiplexed with NVLink/HBM state swaps when N < #agents.
 from __future__ import annotations
 
 import argparse
+import atexit
 import ctypes as C
 import json
 import os
@@ -73,22 +74,55 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        """Start nvidia-smi (-lms 100) and wait for its first sample, so that the timed
+        region (0.2 s at C2) is covered from its first step; a reader thread stamps the
+        lines on arrival."""
+        self.lines, self.t0 = [], None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                                           "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
         except FileNotFoundError:
             self.proc = None
+            return
+
+        atexit.register(lambda p=self.proc: p.poll() is None and p.kill())  # error paths
+
+        def reader():
+            for line in self.proc.stdout:
+                self.lines.append((time.perf_counter(), line))
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+        deadline = time.perf_counter() + 10.0
+        while not self.lines and time.perf_counter() < deadline and self.proc.poll() is None:
+            time.sleep(0.01)
+        self.t0 = time.perf_counter()
+
+    def mark(self):
+        """The timed region starts now (start() runs before the warm-up steps, so that
+        nvidia-smi's start-up does not idle the GPU right before the timed steps)."""
+        self.t0 = time.perf_counter()
 
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.15)
+        t1 = time.perf_counter()
+        deadline = t1 + 1.0  # at least one sample stamped inside or right after the window
+        while time.perf_counter() < deadline and not any(t >= self.t0 for t, _ in self.lines):
+            time.sleep(0.01)
+        time.sleep(0.12)
         self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
+        try:
+            self.proc.wait(timeout=10)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=5)
+        # the window's samples plus the first one after it (a 100 ms period can straddle it)
+        inside = [ln for t, ln in self.lines if self.t0 - 0.05 <= t <= t1]
+        after = [ln for t, ln in self.lines if t > t1][:1]
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
+        for line in inside + after:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
@@ -342,6 +376,8 @@ def run_ours(args, dist: Dist) -> dict | None:
                 check(timed("update", L.fm_apply_update, h, G, cfg.lr, 0.9, 0.999, 1e-8, None, None))
         return ntok
 
+    clocks = ClockSampler(dist.local)
+    clocks.start()
     for s in range(args.warmup):
         one_step(s)
     ctx.synchronize()
@@ -351,8 +387,7 @@ def run_ours(args, dist: Dist) -> dict | None:
     kms = np.zeros(len(KINDS))
     kcnt = np.zeros(len(KINDS), dtype=np.int64)
     check(L.fm_ctx_kernel_times(ctx.handle, kms.ctypes.data, kcnt.ctypes.data, 1))  # reset
-    clocks = ClockSampler(dist.local)
-    clocks.start()
+    clocks.mark()
     launches0 = L.fm_launch_count()
     g2rows = C.c_int64()
     check(L.fm_ctx_gemm2_rows(ctx.handle, C.byref(g2rows), 1))  # reset the executed-K counter
