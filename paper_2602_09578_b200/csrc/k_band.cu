@@ -80,7 +80,7 @@ constexpr int kBandMinBlocks = kCPL == 8 ? 2 : 3;
 // SM with an 8-stage ring, measured at C2 0.193 vs 0.211 ms (two CTAs, 16 stages) and 0.217
 // (two CTAs, 8 stages): K-stats is latency-bound, the extra warps hide it
 #ifndef FM_STATS_MIN_BLOCKS
-#define FM_STATS_MIN_BLOCKS (kCPL == 8 ? 3 : 4)
+#define FM_STATS_MIN_BLOCKS 3
 #endif
 constexpr int kStatsMinBlocks = FM_STATS_MIN_BLOCKS;
 using Frag = std::conditional_t<kCPL == 8, uint4, uint2>;  // a lane's kCPL bf16 columns
