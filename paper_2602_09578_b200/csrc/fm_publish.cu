@@ -194,7 +194,8 @@ int fm_weights_broadcast(fm_weights* w, fm_comm* cm, int root) {
     FM_GUARD_BEGIN
     FM_CUDA(cudaSetDevice(w->device));
     if (w->device != cm->ctx->device) return fail(FM_ERR_CONFIG_ERROR, "weights and communicator on different GPUs");
-    const ncclDataType_t dt = w->dtype == 0 ? ncclFloat64 : w->dtype == 1 ? ncclFloat32 : ncclBfloat16;
+    // (dtype 3, f64 transposed, is rows x cols doubles like dtype 0)
+    const ncclDataType_t dt = w->dtype == 0 || w->dtype == 3 ? ncclFloat64 : w->dtype == 1 ? ncclFloat32 : ncclBfloat16;
     int64_t ver = w->version;
     int64_t* dver = nullptr;
     FM_CUDA(cudaMalloc(&dver, sizeof(int64_t)));

@@ -115,3 +115,14 @@ def test_peer_tier_swap_identity(back_on, tier):
             L.fm_agent_destroy(h)
         for c in ctxs:
             c.close()
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+def test_weight_broadcast():
+    """fm_weights_broadcast: every dtype arrives byte-identical with the root's
+    version on the other rank (tests/bcast_check.py)."""
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", "--master-port=29519", str(ROOT / "tests" / "bcast_check.py")],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "weight broadcast OK" in r.stdout, r.stdout[-3000:]
