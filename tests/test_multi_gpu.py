@@ -126,3 +126,15 @@ def test_weight_broadcast():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "weight broadcast OK" in r.stdout, r.stdout[-3000:]
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+def test_gang_dissolve():
+    """fm_gang_gather_state + fm_gang_detach (tests/gang_detach_check.py): the
+    lead rank ends up with the gang's whole state, a whole bf16 shadow, and the
+    gradients of a fresh one-GPU agent."""
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", "--master-port=29520", str(ROOT / "tests" / "gang_detach_check.py")],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "-> OK" in r.stdout, r.stdout[-3000:]
