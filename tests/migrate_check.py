@@ -9,6 +9,9 @@ update).  Checks:
   * version / Adam step / accumulated samples travel with it;
   * the migrated run's final W, m, v equal an unmigrated run of the same
     micro-batches on rank 0's GPU bit for bit (same kernels, same inputs).
+With argument "share" rank 0 exports with fm_agent_share_export instead (the
+agent stays active there, as when a DP gang forms around it — bench.py C4) and
+finishes the step itself as well: both copies must end bit-identical.
 """
 import ctypes as C
 import os
@@ -65,6 +68,7 @@ def checksum(h):
 def main():
     dist.init_process_group("gloo")
     rank = dist.get_rank()
+    share = len(sys.argv) > 1 and sys.argv[1] == "share"
     local = int(os.environ.get("LOCAL_RANK", rank))
     ctx = Context(local)
     bts = batches()  # step 1 = bts[0:4], step 2 = bts[4:8]
@@ -77,11 +81,16 @@ def main():
         train(ctx, h, bts[:6])  # one full step + half of the second: pending gradient
         before = (checksum(h), L.fm_agent_version(h), L.fm_agent_samples_accumulated(h))
         n = C.c_uint64()
-        _lib.check(L.fm_agent_migrate_export(h, None, 0, C.byref(n)))
+        export = L.fm_agent_share_export if share else L.fm_agent_migrate_export
+        _lib.check(export(h, None, 0, C.byref(n)))
         blob = (C.c_uint8 * n.value)()
-        _lib.check(L.fm_agent_migrate_export(h, blob, n.value, C.byref(n)))
+        _lib.check(export(h, blob, n.value, C.byref(n)))
         dist.broadcast_object_list([bytes(blob), before], src=0)
         dist.barrier()  # rank 1 imported: the parked copy may go
+        kept = None
+        if share:  # still active here: finish the step on this GPU too
+            train(ctx, h, bts[6:])
+            kept = state(h)
         _lib.check(L.fm_agent_destroy(h))
         # the unmigrated reference run on this GPU
         h2 = C.c_void_p()
@@ -99,6 +108,11 @@ def main():
         if step != ref[3]:
             print(f"FAIL adam step {step} vs {ref[3]}")
             ok = False
+        if kept is not None:
+            for name, a, b in (("W", kept[0], ref[0]), ("m", kept[1], ref[1]), ("v", kept[2], ref[2])):
+                if not np.array_equal(a, b):
+                    print(f"FAIL {name}: the sharing rank's own run differs")
+                    ok = False
         _lib.check(L.fm_agent_destroy(h2))
     else:
         msg = [None, None]

@@ -41,10 +41,13 @@ def test_dp_gang_parity_4(mode, port):
 
 
 @pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
-def test_cross_process_migration():
+@pytest.mark.parametrize("how,port", [("migrate", 29513), ("share", 29521)])
+def test_cross_process_migration(how, port):
+    """migrate: export parks the agent, the importer finishes the step; share:
+    fm_agent_share_export keeps it active on the exporter as well."""
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-                        "--master-addr=127.0.0.1", "--master-port=29513", str(ROOT / "tests" / "migrate_check.py")],
-                       capture_output=True, text=True, timeout=600)
+                        "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "tests" / "migrate_check.py"),
+                        how], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout, r.stdout[-3000:]
 
