@@ -768,7 +768,7 @@ cudaError_t launch_band(const BandArgs& A, bool grad, cudaStream_t s) {
     if (A.M <= 0) return cudaSuccess;
     if (A.M + 3 * A.M >= INT32_MAX - 16) return cudaErrorInvalidValue;  // positions are int32
     auto go = [&](auto kern, int min_blocks, int cols, size_t smem) {
-        // one CTA per item while there are >= 4 waves of them (two CTAs per SM); fewer
+        // one CTA per item while there are >= 4 waves of them (min_blocks CTAs per SM); fewer
         // items (a vocabulary-gang rank's slices) run on persistent CTAs that stream item
         // after item without a partial last wave (measured at C2: 6.9 waves 0.209 vs
         // 0.219 ms K-stats one-per-item; 3.5 waves 0.150 vs 0.130 ms persistent).  The
