@@ -63,3 +63,33 @@ def test_row_shards_partition(M, g):
     assert spans[0][0] == 0 and spans[-1][1] == M
     assert all(spans[i][1] == spans[i + 1][0] for i in range(g - 1))
     assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+
+
+def test_clock_sampler_window(tmp_path, monkeypatch):
+    """bench.ClockSampler: start() waits for nvidia-smi's first sample, mark()
+    opens the timed window, stop() keeps the window's samples (plus the first
+    one after it) and reports the median SM clock and any throttle reasons —
+    against a fake nvidia-smi printing a line every 50 ms."""
+    import time
+    import bench
+    fake = tmp_path / "nvidia-smi"
+    fake.write_text("#!/bin/sh\n"
+                    "i=0\n"
+                    "while true; do\n"
+                    "  if [ $i -lt 3 ]; then r='Not Active'; else r='Active'; fi\n"
+                    "  echo \"0, 1965, 1965, 700.0, 0x0, Not Active, Not Active, Not Active, $r\"\n"
+                    "  i=$((i+1)); sleep 0.05\n"
+                    "done\n")
+    fake.chmod(0o755)
+    monkeypatch.setenv("PATH", f"{tmp_path}:{os.environ['PATH']}")
+    c = bench.ClockSampler(0)
+    c.start()
+    assert c.lines, "start() returns once the first sample arrived"
+    time.sleep(0.3)  # warm-up steps
+    c.mark()
+    time.sleep(0.3)  # the timed region
+    out = c.stop()
+    assert out["sm_mhz"] == 1965.0 and out["sm_max_mhz"] == 1965.0
+    assert 3 <= out["samples"] <= 10
+    assert out["reasons"] == ["sw_power_cap"]
+    assert c.proc.poll() is not None  # nvidia-smi stopped
