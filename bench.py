@@ -811,7 +811,15 @@ def run_c4_dynamic(args, dist: Dist) -> dict:
             if me in dst_hosts and me != src:
                 h = new_agent(a)
                 b = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
-                check(L.fm_agent_migrate_import(h, ctx.handle, b, len(blob)))
+                if len(dst_hosts) > 1 and gang_mode_id(args) == 1:
+                    # joining a vocabulary gang: only this rank's rows of W / m / v (the gang
+                    # keeps no others current; fm_gang_attach_mode checks the range)
+                    g, k = len(dst_hosts), dst_hosts.index(me)
+                    tiles = (cfg.vocab + 255) // 256
+                    r0, r1 = (min(cfg.vocab, (tiles * o // g) * 256) for o in (k, k + 1))
+                    check(L.fm_agent_migrate_import_rows(h, ctx.handle, b, len(blob), r0, r1))
+                else:
+                    check(L.fm_agent_migrate_import(h, ctx.handle, b, len(blob)))
                 handles[a] = h
                 active[a] = True
                 version[a] = L.fm_agent_version(h)
@@ -821,7 +829,14 @@ def run_c4_dynamic(args, dist: Dist) -> dict:
                 active.pop(a, None)
             tlog(f"{a} migrate {src_hosts}->{dst_hosts}", tt)
             moved["agents"] += 1
-            moved["bytes"] += cfg.vocab * cfg.feat * 18 * len([r for r in dst_hosts if r != src])
+            for r in dst_hosts:  # W / m / v (16 B per parameter, own rows in a vocabulary gang) + shadow (2 B)
+                if r == src:
+                    continue
+                rows = cfg.vocab
+                if len(dst_hosts) > 1 and gang_mode_id(args) == 1:
+                    g, k, tiles = len(dst_hosts), dst_hosts.index(r), (cfg.vocab + 255) // 256
+                    rows = min(cfg.vocab, (tiles * (k + 1) // g) * 256) - min(cfg.vocab, (tiles * k // g) * 256)
+                moved["bytes"] += rows * cfg.feat * 16 + cfg.vocab * cfg.feat * 2
             if len(dst_hosts) > 1:
                 tt = time.perf_counter()
                 form_gang(a, dst_hosts)

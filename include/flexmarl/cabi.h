@@ -263,6 +263,12 @@ int fm_agent_state_checksum(fm_agent* a, uint64_t* out);
  * returned, the sender calls migrate_release (or destroy) to return the slot. */
 int fm_agent_migrate_export(fm_agent* a, uint8_t* blob_out, uint64_t cap, uint64_t* len);
 int fm_agent_migrate_import(fm_agent* a, fm_ctx* ctx, const uint8_t* blob, uint64_t len);
+/* Import only vocabulary rows [row_lo, row_hi) of W / m / v (and of a pending dW) plus the
+ * whole shadow: for a rank joining a vocabulary-parallel gang, which keeps only its own rows
+ * current (fm_gang_attach_mode 1 checks the range; until then, and unless a later
+ * fm_gang_gather_state completes it, every other use of the agent fails ConfigError). */
+int fm_agent_migrate_import_rows(fm_agent* a, fm_ctx* ctx, const uint8_t* blob, uint64_t len, uint64_t row_lo,
+                                 uint64_t row_hi);
 int fm_agent_migrate_release(fm_agent* a);
 /* Same blob, the agent stays active here: several processes may import it (a DP
  * gang forming around the agent); no work may be queued for it until every

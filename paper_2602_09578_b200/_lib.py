@@ -105,6 +105,7 @@ _PROTOS = {
     "fm_agent_state_checksum": (I, [P, PU64]),
     "fm_agent_migrate_export": (I, [P, P, U64, PU64]),
     "fm_agent_migrate_import": (I, [P, P, P, U64]),
+    "fm_agent_migrate_import_rows": (I, [P, P, P, U64, U64, U64]),
     "fm_agent_migrate_release": (I, [P]),
     "fm_agent_share_export": (I, [P, P, U64, PU64]),
     "fm_gang_gather_state": (I, [P]),

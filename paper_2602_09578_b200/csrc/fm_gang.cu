@@ -77,7 +77,11 @@ int fm_gang_attach_mode(fm_agent* a, fm_comm* cm, int mode, uint8_t* blob_out, u
     *len = sizeof(GangBlob);
     if (!blob_out) return FM_OK;
     if (cap < sizeof(GangBlob)) return fail(FM_ERR_INVALID_ARG, "blob buffer too small");
-    if (int st = check_active(a)) return st;
+    if (a->partial) {  // row-range import: nothing queued yet, its rows must be this rank's
+        if (!a->active || !a->ctx) return fail(FM_ERR_INACTIVE_GROUP, a->name);
+    } else if (int st = check_active(a)) {
+        return st;
+    }
     if (a->precision != FM_PRECISION_BF16_TC) return fail(FM_ERR_CONFIG_ERROR, "gang exchange needs the tensor-core path");
     if (cm->ctx != a->ctx) return fail(FM_ERR_CONFIG_ERROR, "communicator bound to another GPU");
     if (cm->nranks < 2 || cm->nranks > 8) return fail(FM_ERR_CONFIG_ERROR, "gang size must be 2..8");
@@ -93,6 +97,11 @@ int fm_gang_attach_mode(fm_agent* a, fm_comm* cm, int mode, uint8_t* blob_out, u
     for (int o = 0; o < gs->g; ++o) max_rows = std::max(max_rows, gs->lo[o + 1] - gs->lo[o]);
     const int64_t own = gs->lo[gs->rank + 1] - gs->lo[gs->rank];
     gs->vocab = mode == 1;
+    if (a->partial && (!gs->vocab || a->part_lo != gs->lo[gs->rank] || a->part_hi != gs->lo[gs->rank + 1])) {
+        const std::string want = std::to_string(gs->lo[gs->rank]) + ", " + std::to_string(gs->lo[gs->rank + 1]);
+        delete gs;
+        return fail(FM_ERR_CONFIG_ERROR, a->name + ": imported rows are not this rank's vocabulary range [" + want + ")");
+    }
     // the vocabulary-parallel gang exchanges no partial gradients: a token receive buffer only
     const size_t rbytes = gs->vocab ? 256 : static_cast<size_t>(gs->g - 1) * std::max<int64_t>(own, 1) * a->D * 4;
     fm_ctx* c = a->ctx;
@@ -209,6 +218,7 @@ int fm_gang_gather_state(fm_agent* a) {
         a->fmax_valid = false;
     }
     FM_CUDA(cudaStreamSynchronize(c->stream));
+    a->partial = false;  // every row is here now
     return FM_OK;
     FM_GUARD_END
 }

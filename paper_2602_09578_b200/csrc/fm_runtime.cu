@@ -673,6 +673,10 @@ void agent_free_device(fm_agent* a, cudaStream_t s) {
 // stream — only this agent's first use waits for its copy-in.
 int check_active(fm_agent* a, bool flush) {
     if (!a->active || !a->ctx) return fail(FM_ERR_INACTIVE_GROUP, a->name);
+    if (a->partial && !(a->gang && a->gang->vocab))
+        return fail(FM_ERR_CONFIG_ERROR, a->name + " holds vocabulary rows [" + std::to_string(a->part_lo) + ", " +
+                                             std::to_string(a->part_hi) +
+                                             ") only: attach it to its vocabulary gang (fm_gang_attach_mode 1)");
     if (flush && a->ctx->pend_agent == a)
         if (int st = agent_flush(a)) return st;
     if (a->pending_in) {

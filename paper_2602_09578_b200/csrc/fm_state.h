@@ -290,6 +290,10 @@ struct fm_agent {
     int ev_device = -1;            // the device the agent's events were created on
     fm_comm* norm_comm = nullptr;  // exact DP micro-batch grad norms over this communicator
     bool lent = false;             // exported by migration; slot reserved until migrate_release
+    // fm_agent_migrate_import_rows: only W / m / v rows [part_lo, part_hi) are this agent's —
+    // usable solely as that rank of a vocabulary-parallel gang (check_active refuses otherwise)
+    bool partial = false;
+    int64_t part_lo = 0, part_hi = 0;
     Slot* slot = nullptr;
     GangState* gang = nullptr;
 };

@@ -265,7 +265,10 @@ int fm_agent_migrate_release(fm_agent* a) {
     FM_GUARD_END
 }
 
-int fm_agent_migrate_import(fm_agent* a, fm_ctx* c, const uint8_t* blob, uint64_t len) {
+namespace {
+// rows [r0, r1) of W / m / v / dW (the whole shadow always: a vocabulary gang rank streams
+// its columns of every feature row)
+int migrate_import_range(fm_agent* a, fm_ctx* c, const uint8_t* blob, uint64_t len, uint64_t r0, uint64_t r1) {
     FM_GUARD_BEGIN
     if (len != sizeof(MigrateBlob)) return fail(FM_ERR_INVALID_ARG, "migration blob size mismatch");
     MigrateBlob b;
@@ -289,12 +292,18 @@ int fm_agent_migrate_import(fm_agent* a, fm_ctx* c, const uint8_t* blob, uint64_
     auto cp = [&](void* dst, uint64_t off, size_t n) {
         return cudaMemcpyPeerAsync(dst, c->device, p + off, b.src_device, n, c->copy_in);
     };
-    FM_CUDA(cp(a->W, b.off_w, P * 8));
-    FM_CUDA(cp(a->m, b.off_m, P * 4));
-    FM_CUDA(cp(a->v, b.off_v, P * 4));
-    if (b.dw_valid) FM_CUDA(cp(a->dW, b.off_dw, P * dw_elem(a)));
+    (void)P;
+    const uint64_t e0 = r0 * a->D, ne = (r1 - r0) * a->D;  // element range of the rows
+    FM_CUDA(cp(a->W + e0, b.off_w + e0 * 8, ne * 8));
+    FM_CUDA(cp(a->m + e0, b.off_m + e0 * 4, ne * 4));
+    FM_CUDA(cp(a->v + e0, b.off_v + e0 * 4, ne * 4));
+    if (b.dw_valid)
+        FM_CUDA(cp(static_cast<uint8_t*>(a->dW) + e0 * dw_elem(a), b.off_dw + e0 * dw_elem(a), ne * dw_elem(a)));
     if (a->W16) FM_CUDA(cp(a->W16, b.off_w16, w16_bytes(a)));
     FM_CUDA(cudaEventRecord(a->ev_in, c->copy_in));
+    a->partial = r0 != 0 || r1 != a->V;
+    a->part_lo = static_cast<int64_t>(r0);
+    a->part_hi = static_cast<int64_t>(r1);
     a->dw_valid = b.dw_valid;
     a->step = b.step;
     a->version = b.version;
@@ -306,6 +315,18 @@ int fm_agent_migrate_import(fm_agent* a, fm_ctx* c, const uint8_t* blob, uint64_
     cudaEventDestroy(ev);
     return FM_OK;
     FM_GUARD_END
+}
+}  // namespace
+
+int fm_agent_migrate_import(fm_agent* a, fm_ctx* c, const uint8_t* blob, uint64_t len) {
+    return migrate_import_range(a, c, blob, len, 0, a ? a->V : 0);
+}
+
+int fm_agent_migrate_import_rows(fm_agent* a, fm_ctx* c, const uint8_t* blob, uint64_t len, uint64_t row_lo,
+                                 uint64_t row_hi) {
+    if (!a || row_lo >= row_hi || row_hi > a->V)
+        return fail(FM_ERR_INVALID_ARG, "row range must satisfy row_lo < row_hi <= vocab");
+    return migrate_import_range(a, c, blob, len, row_lo, row_hi);
 }
 
 int fm_agent_state_checksum(fm_agent* a, uint64_t* out) {

@@ -141,3 +141,15 @@ def test_gang_dissolve():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "-> OK" in r.stdout, r.stdout[-3000:]
+
+
+@pytest.mark.skipif(_ngpu() < 2, reason="needs >= 2 GPUs")
+def test_gang_from_row_range_import():
+    """fm_agent_migrate_import_rows (tests/rows_import_check.py): a vocabulary
+    gang formed from a rank's own-rows import trains bit-identically to one
+    formed from a whole import; the partial agent is refused elsewhere."""
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr=127.0.0.1", "--master-port=29522", str(ROOT / "tests" / "rows_import_check.py")],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "-> OK" in r.stdout, r.stdout[-3000:]
